@@ -1,0 +1,26 @@
+// Library-level C-ABI: version, error strings, launch accounting.
+#include <atomic>
+
+#include "common.cuh"
+
+namespace ms {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace ms
+
+extern "C" int ms_version(void) { return 100; }
+
+extern "C" const char* ms_strerror(int status) {
+  switch (status) {
+    case MS_OK: return "ok";
+    case MS_ERR_VALUE: return "invalid argument";
+    case MS_ERR_LENGTH: return "length mismatch";
+    case MS_ERR_DIST_MISMATCH: return "distribution shape mismatch";
+    case MS_ERR_UNSUPPORTED: return "shape outside the kernel's supported range";
+    case MS_ERR_CUDA: return cudaGetErrorString(cudaPeekAtLastError());
+    default: return "unknown status";
+  }
+}
+
+extern "C" int64_t ms_launch_count(void) { return ms::g_launches.load(); }
+extern "C" void ms_reset_launch_count(void) { ms::g_launches.store(0); }
