@@ -100,6 +100,76 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
                             int32_t* emitted, int32_t* n_emit, int32_t* finished,
                             int32_t* kv_len, void* stream);
 
+/* ---- K1/K5/K8: linear layer on tcgen05 tensor cores ---------------------
+ * The projection GEMMs of the SSM decode step and the LLM verification
+ * forward, i.e. the compute behind ModelOracle.next_dist
+ * (aggspec/oracles.py:19-26) as called by draft_sequence (aggspec/oracles.py:148)
+ * and the target loop of _do_verify_batch (aggspec/engine.py:294-296).
+ *
+ *   out[m, n] = act(sum_k x[m, k] * w[n, k] + bias[n]) + residual[m, n]
+ *   x [M, ldx] bf16, w [N, K] bf16 (nn.Linear layout), bias [N] bf16 or NULL,
+ *   residual [M, ldr] bf16 or NULL, out [M, ldc] bf16 (out_f32 = 0) or fp32,
+ *   act 0 = identity, 1 = ReLU.
+ * splits: split-K factor (0 = ms_linear_splits(N, K), max 8): the CTAs of a
+ * tile form a thread-block cluster and reduce through distributed shared
+ * memory.  Results are deterministic, and a row's result does not depend on M
+ * (batch invariant) for a fixed `splits`.
+ * Limits: K % 8 == 0, ldx % 8 == 0, x and w 16-byte aligned.
+ */
+int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
+              const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
+              int M, int N, int K, int act, int splits, void* stream);
+/* Default split-K factor for an [N, K] weight (weight-streaming regime). */
+int ms_linear_splits(int N, int K);
+
+/* ---- decoder pieces around the GEMMs (OPT-style, pre-LN) ----------------
+ * Token + learned-position embedding of R = B*Q rows: row r = b*Q + i is at
+ * position start[b] + i; out[r] = tok_emb[tok[r]] + pos_emb[pos + pos_offset]
+ * (pos_emb may be NULL).  bf16 [R, d].
+ */
+int ms_embed(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,
+             const void* pos_emb, int pos_offset, int R, int d, void* out, void* stream);
+
+/* LayerNorm (fp32 statistics) into out [R, ldo]: output row r normalises input
+ * row rows[r] (rows == NULL: row r) of x [*, ldx] bf16. */
+int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,
+                 const void* beta, float eps, int R, int d, void* out, int64_t ldo, void* stream);
+
+/* KV-cache append: rows r = b*Q + i of qkv [B*Q, ldq] (layout [q | k | v],
+ * each H*D wide) are written at position start[b] + i of cache slot slot[b];
+ * caches are [slots, H, T, D] bf16.  Positions outside [0, T) are skipped. */
+int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
+                 const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                 void* v_cache, void* stream);
+
+/* Causal attention of Q query rows per request over the KV cache: query i of
+ * request b (row b*Q + i of qkv) is at position start[b] + i and attends to
+ * cache positions 0..start[b] + i.  out [B*Q, ldo] bf16, head h at columns
+ * h*D.. .  Q > 17 is processed in chunks of 16 queries per CTA.
+ * Limits: D in {64, 128}. */
+int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
+                 const int32_t* slot, const int32_t* start, int T, const void* k_cache,
+                 const void* v_cache, float scale, void* out, int64_t ldo, void* stream);
+
+/* ---- round glue ------------------------------------------------------------
+ * After an SSM decode step's argmax tok[B]: drafts[b, k, j] = tok[b] (the token
+ * list draft_sequence builds, aggspec/oracles.py:146-152) and next_tok[b] =
+ * tok[b] (NULL: not written).  With teacher != NULL (fidelity-injection bench
+ * mode), the token is replaced by teacher[b, ctx_len[b] + j] (a target greedy
+ * continuation, absolute positions, ld_teacher per row; -1 = none) when
+ * hash(seed, req_key[b], k, position) < fidelity — the device analogue of the
+ * PerturbedOracle fidelity knob (aggspec/oracles.py:108-132).
+ */
+int ms_draft_commit(const int32_t* tok, const int32_t* ctx_len, int B, int j, int k,
+                    int K, int S, const int32_t* teacher, int64_t ld_teacher,
+                    const int32_t* req_key, float fidelity, uint64_t seed,
+                    int32_t* drafts, int32_t* next_tok, void* stream);
+
+/* Verifier input rows vin[b] = [last[b], path[b, 0..S-1]] ([B, S+1] int32):
+ * the contexts ctx + tokens[:i] of aggspec/engine.py:294-296. */
+int ms_pack_verify(const int32_t* last, const int32_t* path, int B, int S,
+                   int32_t* vin, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

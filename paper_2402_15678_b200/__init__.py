@@ -31,13 +31,20 @@ from .selector import (  # noqa: F401
     observe,
     optimal_s_oracle,
 )
-from .verification import VerificationResult, acceptance_rate, verify  # noqa: F401
-from .voting import (  # noqa: F401
-    MajorityOutput,
-    SpeculationTree,
-    WeightTable,
-    merge,
-    record_acr,
-    select_majority,
-    update_weights,
-)
+
+# Device-facing names load libminions.so on first use (so that `build` can run
+# before the library exists); a missing library raises there — no fallback.
+_LAZY = {
+    "VerificationResult": "verification", "acceptance_rate": "verification", "verify": "verification",
+    "MajorityOutput": "voting", "SpeculationTree": "voting", "WeightTable": "voting",
+    "merge": "voting", "record_acr": "voting", "select_majority": "voting",
+    "update_weights": "voting",
+}
+
+
+def __getattr__(name):
+    mod = _LAZY.get(name)
+    if mod is None:
+        raise AttributeError(name)
+    import importlib
+    return getattr(importlib.import_module(f".{mod}", __name__), name)

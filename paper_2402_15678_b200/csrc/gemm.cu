@@ -1,0 +1,370 @@
+// K1/K5/K8 — the linear layers of the SSM decode and the LLM verify forward on
+// tcgen05 tensor cores.
+//
+//   out[M, N] = epi( X[M, K] · W[N, K]^T )      X: tokens (bf16), W: nn.Linear weight (bf16)
+//   epi(v)    = act(v + bias[n]) + residual[m, n]   -> bf16 or fp32
+//
+// Decode/verify GEMMs have few token rows (M = B·(s+1) = 16..~300) against
+// multi-GB weights: they are HBM-bound weight streams.  Layout "swap-AB": the
+// weight tile is the MMA's M side (128 output features per CTA) and the token
+// tile its N side (BN = 16..256), so a 16-row batch still issues full-height
+// MMAs and TMEM holds a 128 x BN fp32 accumulator.
+//
+// Per CTA: warp 0 = TMA producer (W tile 128x64 + X tile BNx64 per stage,
+// 128B swizzle, mbarrier complete_tx), warp 1 = TMEM allocator + single-thread
+// tcgen05.mma issuer, warps 2-5 = epilogue (tcgen05.ld -> bias/act/residual ->
+// global).  Split-K over the reduction dimension fills the 148 SMs: the
+// `splits` CTAs of an output tile form one thread-block cluster and reduce
+// their fp32 partial tiles through distributed shared memory (no global
+// scratch, no extra launch), adding ranks in order — results are
+// deterministic and, because the split count depends only on (N, K),
+// identical for a token row whatever M is (batch invariance: a request's
+// logits do not depend on what else is in the verify batch).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace ms {
+
+struct LinearParams {
+  int M, N, K;
+  const __nv_bfloat16* bias;      // [N] or null
+  const __nv_bfloat16* residual;  // [M, ldr] or null
+  int64_t ldr;
+  void* out;                      // [M, ldc] bf16 or fp32
+  int64_t ldc;
+  int out_f32;
+  int act;                        // 0 none, 1 relu
+  int splits;
+  int kb_total;                   // K / 64 (rounded up)
+  int n_tiles;
+};
+
+constexpr int kBM = 128;  // output features per CTA (MMA M)
+constexpr int kBK = 64;   // bf16 elements per 128-byte swizzled row
+constexpr int kThreads = 192;
+
+template <int BN>
+struct LinearCfg {
+  static constexpr int W_BYTES = kBM * kBK * 2;
+  static constexpr int X_BYTES = BN * kBK * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  // ~110 KB of pipeline per CTA => two CTAs per SM for the small-M shapes
+  static constexpr int STAGES_RAW = (112 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW < 2 ? 2 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int PART_BYTES = BN * kBM * 4;  // fp32 partial tile for the split-K reduction
+  static constexpr int DATA_BYTES = PIPE_BYTES > PART_BYTES ? PIPE_BYTES : PART_BYTES;
+  static constexpr int SMEM = 1024 /*align slack*/ + DATA_BYTES + (2 * STAGES + 1) * 8 + 16;
+};
+
+__device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v) {
+  if (p.bias) v += bf2f(p.bias[feat]);
+  if (p.act == 1) v = fmaxf(v, 0.0f);
+  if (p.residual) v += bf2f(p.residual[(int64_t)tok * p.ldr + feat]);
+  if (p.out_f32)
+    reinterpret_cast<float*>(p.out)[(int64_t)tok * p.ldc + feat] = v;
+  else
+    reinterpret_cast<__nv_bfloat16*>(p.out)[(int64_t)tok * p.ldc + feat] = f2bf(v);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// float4 load from the shared memory of CTA `rank` of this cluster
+__device__ __forceinline__ float4 ld_dsmem_f4(const float* local, int rank) {
+  uint32_t a = tc::smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+              const LinearParams p) {
+  using C = LinearCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + C::STAGES * C::W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tile_n = blockIdx.x / p.splits;
+  const int split = blockIdx.x - tile_n * p.splits;
+  const int n0 = tile_n * kBM;
+  const int m0 = blockIdx.y * BN;
+  const int kb0 = (int)((int64_t)split * p.kb_total / p.splits);
+  const int kb1 = (int)((int64_t)(split + 1) * p.kb_total / p.splits);
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmW);
+    tc::prefetch_tmap(&tmX);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
+      const uint64_t pol_x = tc::policy_evict_last();   // tokens are re-read by every tile
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, n0, pol_w);
+        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, m0, pol_x);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::fence_after_sync();
+        const uint64_t ad = tc::smem_desc_sw128(sW + stage * C::W_BYTES);
+        const uint64_t bd = tc::smem_desc_sw128(sX + stage * C::X_BYTES);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K per UMMA_K=16 step
+          tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+        tc::mma_commit(&empty[stage]);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      tc::mma_commit(tmem_full);
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5, TMEM lane quadrant = warp % 4 ----------
+    const int q = warp & 3;
+    const int feat = n0 + q * 32 + lane;
+    const bool feat_ok = feat < p.N;
+    const int m_hi = min(BN, p.M - m0);  // valid token columns in this tile
+    tc::mbar_wait(tmem_full, 0);
+    tc::fence_after_sync();
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+
+    if (p.splits == 1) {
+      for (int c0 = 0; c0 < m_hi; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(trow + c0, r);
+        tc::tmem_wait_ld();
+        if (feat_ok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < m_hi) epi_store(p, m0 + c0 + j, feat, __uint_as_float(r[j]));
+        }
+      }
+    } else {
+      // stage this split's fp32 partial tile in (now idle) pipeline smem,
+      // layout P[token][feature] so a warp's 32 lanes write 32 consecutive words
+      float* P = reinterpret_cast<float*>(smem);
+      for (int c0 = 0; c0 < m_hi; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(trow + c0, r);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) P[(c0 + j) * kBM + q * 32 + lane] = __uint_as_float(r[j]);
+      }
+    }
+  }
+  if (p.splits > 1) {
+    // split-K reduction across the thread-block cluster through DSMEM: CTA
+    // `split` reduces a 1/splits slice of the tile, adding the partials of
+    // ranks 0..splits-1 in rank order (deterministic), then runs the epilogue.
+    cluster_sync_all();
+    const int m_hi = min(BN, p.M - m0);
+    const int units = m_hi * (kBM / 4);  // float4 units of the [m_hi, 128] tile
+    const int u0 = (int)((int64_t)split * units / p.splits);
+    const int u1 = (int)((int64_t)(split + 1) * units / p.splits);
+    const float* P = reinterpret_cast<const float*>(smem);
+    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
+      const int j = u / (kBM / 4);
+      const int f4 = (u - j * (kBM / 4)) * 4;
+      float4 acc = ld_dsmem_f4(P + j * kBM + f4, 0);
+      for (int rk = 1; rk < p.splits; ++rk) {
+        const float4 v = ld_dsmem_f4(P + j * kBM + f4, rk);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      const int feat = n0 + f4;
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (feat + t < p.N) epi_store(p, m0 + j, feat + t, a4[t]);
+    }
+    cluster_sync_all();  // peers may still be reading this CTA's smem
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] with row stride ld (elements); box = [64 cols, box_rows].
+static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                      int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Split count for the weight-streaming regime: a function of (N, K) only.
+int linear_auto_splits(int N, int K) {
+  const int n_tiles = (N + kBM - 1) / kBM;
+  const int kb = (K + kBK - 1) / kBK;
+  const int slots = 148 * 2;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int sp = 1; sp <= 8; ++sp) {
+    if (sp > 1 && kb / sp < 4) break;
+    const int units = n_tiles * sp;
+    const int waves = (units + slots - 1) / slots;
+    const double per_unit = (double)((kb + sp - 1) / sp);
+    const double cost = waves * per_unit + (sp > 1 ? 2.0 : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+static int pick_bn(int M) {
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 48) return 48;
+  if (M <= 64) return 64;
+  if (M <= 80) return 80;
+  if (M <= 96) return 96;
+  if (M <= 128) return 128;
+  if (M <= 160) return 160;
+  if (M <= 192) return 192;
+  return 256;
+}
+
+template <int BN>
+static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p,
+                         int m_tiles, cudaStream_t st) {
+  using C = LinearCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM) != cudaSuccess)
+      return MS_ERR_CUDA;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_tiles * p.splits, m_tiles);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.splits;  // the split-K CTAs of a tile form one cluster
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, linear_kernel<BN>, tw, tx, p) != cudaSuccess) return MS_ERR_CUDA;
+  count_launch();
+  return launch_status();
+}
+
+}  // namespace ms
+
+extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }
+
+extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
+                         const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
+                         int M, int N, int K, int act, int splits, void* stream) {
+  using namespace ms;
+  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < N) return MS_ERR_VALUE;
+  if (M == 0) return MS_OK;
+  if (!x || !w || !out) return MS_ERR_VALUE;
+  if (K % 8 != 0 || ldx % 8 != 0) return MS_ERR_UNSUPPORTED;  // TMA: 16-byte row strides
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
+  if (residual && ldr < N) return MS_ERR_VALUE;
+  const int kb_total = (K + kBK - 1) / kBK;
+  if (splits <= 0) splits = linear_auto_splits(N, K);
+  if (splits > kb_total) splits = kb_total;
+  const int bn = pick_bn(M);
+  const int m_tiles = (M + bn - 1) / bn;
+  const int n_tiles = (N + kBM - 1) / kBM;
+  if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
+  if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
+  CUtensorMap tw, tx;
+  if (!make_tmap(&tw, w, N, K, K, kBM)) return MS_ERR_CUDA;
+  if (!make_tmap(&tx, x, M, K, ldx, bn)) return MS_ERR_CUDA;
+  LinearParams p;
+  p.M = M; p.N = N; p.K = K;
+  p.bias = (const __nv_bfloat16*)bias;
+  p.residual = (const __nv_bfloat16*)residual;
+  p.ldr = ldr;
+  p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
+  p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (bn) {
+    case 16: return launch_linear<16>(tw, tx, p, m_tiles, st);
+    case 32: return launch_linear<32>(tw, tx, p, m_tiles, st);
+    case 48: return launch_linear<48>(tw, tx, p, m_tiles, st);
+    case 64: return launch_linear<64>(tw, tx, p, m_tiles, st);
+    case 80: return launch_linear<80>(tw, tx, p, m_tiles, st);
+    case 96: return launch_linear<96>(tw, tx, p, m_tiles, st);
+    case 128: return launch_linear<128>(tw, tx, p, m_tiles, st);
+    case 160: return launch_linear<160>(tw, tx, p, m_tiles, st);
+    case 192: return launch_linear<192>(tw, tx, p, m_tiles, st);
+    default: return launch_linear<256>(tw, tx, p, m_tiles, st);
+  }
+}

@@ -1,0 +1,435 @@
+"""Speculate-vote-verify runtime on one B200: the device form of
+SpeculationEngine._do_draft_batch / _do_verify_batch (aggspec/engine.py:252-330).
+
+One round, entirely on the device (capturable as one CUDA graph per (s, Qc)):
+
+  for each SSM k (K drafters, own weights + KV cache):
+      step 0   catch-up forward of the Qc context tokens the SSM has not cached
+               (rollback: an SSM's cache is valid only up to its longest prefix
+               agreement with the emitted tokens), logits of the last row
+      step j   one-token decode of its previous draft           (K1/K2/K7)
+      argmax + draft_commit -> drafts[B, K, s]                   (K3)
+  vote (fp64 weights, reference tie rules) -> path[B, s], voted  (K4)
+  pack [last token | path] -> verify forward of s+1 rows          (K5/K6/K7)
+  LM head logits -> argmax -> greedy accept + commit              (K8/K9)
+
+then one device->host copy of the per-request results, after which the host
+replays the reference's bookkeeping verbatim: record_acr / update_weights
+(fp64), the Request lifecycle, the remaining-budget / stop-token commit and the
+adaptive speculation length (observe / maybe_adjust) fed with the MEASURED
+verify time (CUDA events), not a cost model.
+
+KV rollback is length arithmetic: the LLM's cache is valid for the first
+len(context) - 1 positions (the verify forward rewrites the rest), an SSM's for
+len(context_before_round) + lcp(its draft, emitted) positions.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev
+from . import _native
+from . import kernels as K
+import zlib
+
+from .core import AggSpecError, EngineConfig, Request, RequestState, validate_config
+from .opt import KVCache, OPTModel, OPTWeights
+from .selector import Decision, MonitorSample, SelectorState, maybe_adjust, observe
+from .verification import AcceptOut
+from .voting import WeightTable, record_acr, update_weights
+
+I32 = torch.int32
+
+
+class EngineFinished(AggSpecError):  # aggspec/engine.py:37
+    pass
+
+
+class DeadlockError(AggSpecError):  # aggspec/engine.py:41
+    pass
+
+
+class NoProgress(AggSpecError):  # aggspec/engine.py:44
+    pass
+
+
+@dataclass
+class RoundStats:
+    s: int
+    qc: int
+    t_verify_ms: float
+    t_round_ms: float
+    accepted: list
+    emitted: list
+    voted: list
+    vl: float
+    decision: str
+    s_next: int
+    weights: dict
+
+
+@dataclass
+class RunResult:
+    outputs: dict                     # request id -> generated tokens
+    rounds: list = field(default_factory=list)
+    tokens: int = 0
+    wall_s: float = 0.0
+
+    @property
+    def mean_accepted(self) -> float:
+        acc = [a for r in self.rounds for a in r.accepted]
+        return float(np.mean(acc)) if acc else 0.0
+
+    @property
+    def mean_emitted(self) -> float:
+        em = [e for r in self.rounds for e in r.emitted]
+        return float(np.mean(em)) if em else 0.0
+
+
+class SpecEngine:
+    """Greedy speculative decoding with K voting drafters on one GPU."""
+
+    def __init__(self, target: OPTWeights, drafters: list[OPTWeights], cfg: EngineConfig,
+                 slots: int, max_len: int, device="cuda", use_graphs: bool = True,
+                 fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True):
+        validate_config(cfg)
+        if len(cfg.initial_weights) != len(drafters):
+            raise ValueError("initial_weights must have one entry per drafter")
+        self.dev = torch.device(device)
+        _dev.require_cuda()
+        self.cfg = cfg
+        self.K = len(drafters)
+        self.B = slots
+        self.max_len = max_len
+        self.adaptive = adaptive
+        s_cap = cfg.s_max
+        self.max_rows_t = max(slots * (s_cap + 1), slots)
+        self.target = OPTModel(target, max_rows=max(self.max_rows_t, slots * max_len), device=device)
+        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device) for w in drafters]
+        self.t_cache = KVCache(target.cfg, slots, max_len, device)
+        self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
+        V = target.cfg.vocab
+        if any(w.cfg.vocab != V for w in drafters):
+            raise ValueError("drafters and target must share a vocabulary")
+        self.V = V
+        B = slots
+        z = lambda *sh: torch.zeros(sh, dtype=I32, device=self.dev)  # noqa: E731
+        # per-round inputs (uploaded once per round from one pinned buffer)
+        self.slot = torch.arange(B, dtype=I32, device=self.dev)
+        self.ctx_len = z(B)
+        self.c_start = z(B)
+        self.c_tok = z(B, s_cap + 1)
+        self.c_head = z(B)
+        self.v_start = z(B)
+        self.step_start = z(s_cap, B)
+        self.last = z(B)
+        self.remaining = z(B)
+        self.req_key = z(B)
+        self.w_dev = torch.zeros(self.K, dtype=torch.float64, device=self.dev)
+        # per-round device intermediates
+        self.drafts = z(B, self.K, s_cap)
+        self.step_tok = [z(B, 1) for _ in range(self.K)]
+        self.argmax = [z(B) for _ in range(self.K)]
+        self.argmax_ws = torch.zeros(max(B * (s_cap + 1), B), dtype=torch.int64, device=self.dev)
+        self.ssm_ws = [torch.zeros(B, dtype=torch.int64, device=self.dev) for _ in range(self.K)]
+        self.ssm_logits = [torch.empty(B, V, device=self.dev) for _ in range(self.K)]
+        self.path = z(B, s_cap)
+        self.voted = z(B)
+        self.vin = z(B, s_cap + 1)
+        self.v_logits = torch.empty(B * (s_cap + 1), V, device=self.dev)
+        self.acc = AcceptOut.alloc(B, s_cap, self.dev, with_argmax=True)
+        # fidelity injection (bench mode)
+        self.fidelity = list(fidelity) if fidelity is not None else None
+        self.inject_seed = inject_seed
+        self.teacher = z(B, max_len) - 1 if fidelity is not None else None
+        self.use_graphs = use_graphs
+        self.graphs: dict = {}
+        self.streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
+        self.ev_v0 = torch.cuda.Event(enable_timing=True)
+        self.ev_v1 = torch.cuda.Event(enable_timing=True)
+        self.pinned_out = None
+
+    # ------------------------------------------------------------------ setup
+    def prefill(self, requests: list[Request]) -> None:
+        """Assign slots and cache every prompt position but the last (the
+        first round feeds the last prompt token)."""
+        if len(requests) > self.B:
+            raise ValueError(f"{len(requests)} requests exceed {self.B} slots")
+        self.requests = list(requests)
+        self.n_active = len(requests)
+        self.ctx = [list(r.prompt) + list(r.generated) for r in requests]
+        lens = [len(c) for c in self.ctx]
+        if min(lens) < 1:
+            raise ValueError("context must be non-empty")
+        P = max(lens) - 1
+        if max(lens) + self.cfg.s_max + 2 > self.max_len or any(
+                len(c) + r.remaining + self.cfg.s_max + 2 > self.max_len for c, r in zip(self.ctx, requests)):
+            raise ValueError("max_len too small for prompt + max_new_tokens + s_max")
+        keys = np.zeros(self.B, np.int32)
+        for b, r in enumerate(requests):
+            keys[b] = zlib.crc32(str(r.id).encode()) & 0x7FFFFFFF
+        self.req_key.copy_(torch.from_numpy(keys))
+        self.ssm_cached = [[len(c) - 1 for c in self.ctx] + [0] * (self.B - len(requests))
+                           for _ in range(self.K)]
+        if P > 0:
+            toks = np.zeros((self.B, P), np.int32)
+            for b, c in enumerate(self.ctx):
+                toks[b, : len(c) - 1] = c[:-1]
+            t = torch.from_numpy(toks).to(self.dev)
+            zero = torch.zeros(self.B, dtype=I32, device=self.dev)
+            empty = torch.zeros(0, dtype=I32, device=self.dev)
+            dummy = torch.empty(0, self.V, device=self.dev)
+            self.target.forward(t, zero, self.slot, self.t_cache, dummy, head_rows=empty)
+            for m, c in zip(self.ssms, self.s_caches):
+                m.forward(t, zero, self.slot, c, dummy, head_rows=empty)
+        for r in requests:
+            if r.remaining <= 0 and r.state != RequestState.FINISHED:
+                r.state = RequestState.FINISHED
+        torch.cuda.synchronize(self.dev)
+
+    def set_teacher(self, teacher: dict) -> None:
+        """Target greedy continuations (request id -> tokens after the prompt)
+        for fidelity injection."""
+        if self.teacher is None:
+            raise ValueError("engine was built without fidelity injection")
+        t = np.full((self.B, self.max_len), -1, np.int32)
+        for b, r in enumerate(self.requests):
+            seq = teacher[r.id]
+            p0 = len(r.prompt)
+            t[b, p0: p0 + len(seq)] = seq
+        self.teacher.copy_(torch.from_numpy(t))
+
+    # --------------------------------------------------------- device round
+    def _device_draft(self, s: int, qc: int) -> None:
+        """K drafters (concurrent streams) + vote + verifier input rows."""
+        B = self.B
+        main = torch.cuda.current_stream(self.dev)
+        ev0 = torch.cuda.Event()
+        ev0.record(main)
+        done = []
+        for k, (m, cache) in enumerate(zip(self.ssms, self.s_caches)):
+            st = self.streams[k]
+            st.wait_event(ev0)
+            with torch.cuda.stream(st):
+                self._draft(k, m, cache, s, qc, st)
+                e = torch.cuda.Event()
+                e.record(st)
+                done.append(e)
+        for e in done:
+            main.wait_event(e)
+        sp = _dev.stream_ptr(main)
+        _native.call("ms_vote", self._drafts_s(s).data_ptr(), self.w_dev.data_ptr(), None, B, self.K, s,
+                     self.path.data_ptr(), self.voted.data_ptr(), sp)
+        _native.call("ms_pack_verify", self.last.data_ptr(), self.path.data_ptr(), B, s,
+                     self.vin.data_ptr(), sp)
+
+    def _device_verify(self, s: int) -> None:
+        """Verify forward of s+1 rows per request + greedy accept."""
+        B, V = self.B, self.V
+        sp = _dev.stream_ptr()
+        vin = self.vin.view(-1)[: B * (s + 1)].view(B, s + 1)
+        logits = self.v_logits[: B * (s + 1)]
+        self.target.forward(vin, self.v_start, self.slot, self.t_cache, logits)
+        a = self.acc
+        _native.call("ms_accept_greedy_logits", self.path.data_ptr(), logits.data_ptr(), 0, V,
+                     self.remaining.data_ptr(), -1 if self.cfg.stop_token is None else self.cfg.stop_token,
+                     B, s, a.tgt_argmax.data_ptr(), self.argmax_ws.data_ptr(), a.n_acc.data_ptr(),
+                     a.emitted.data_ptr(), a.n_emit.data_ptr(), a.finished.data_ptr(), None, sp)
+
+    def _drafts_s(self, s):
+        # drafts buffer viewed as [B, K, s] contiguous (the first B*K*s ints)
+        return self.drafts.view(-1)[: self.B * self.K * s].view(self.B, self.K, s)
+
+    def _draft(self, k, m: OPTModel, cache: KVCache, s: int, qc: int, st) -> None:
+        B = self.B
+        sp = _dev.stream_ptr(st)
+        dr = self._drafts_s(s)
+        tok_in = self.c_tok.view(-1)[: B * qc].view(B, qc)
+        teacher = self.teacher.data_ptr() if self.teacher is not None else None
+        f = float(self.fidelity[k]) if self.fidelity is not None else 0.0
+        for j in range(s):
+            if j == 0:
+                m.forward(tok_in, self.c_start, self.slot, cache, self.ssm_logits[k],
+                          head_rows=self.c_head, stream=st)
+            else:
+                m.forward(self.step_tok[k], self.step_start[j - 1], self.slot, cache,
+                          self.ssm_logits[k], stream=st)
+            _native.call("ms_argmax_rows", self.ssm_logits[k].data_ptr(), 0, B, self.V, self.V,
+                         self.argmax[k].data_ptr(), self.ssm_ws[k].data_ptr(), sp)
+            _native.call("ms_draft_commit", self.argmax[k].data_ptr(), self.ctx_len.data_ptr(), B, j, k,
+                         self.K, s, teacher, self.max_len, self.req_key.data_ptr(), f,
+                         self.inject_seed, dr.data_ptr(), self.step_tok[k].data_ptr(), sp)
+
+    def _replay(self, key, fn) -> None:
+        """Run fn eagerly the first time (sets kernel attributes, produces this
+        round's results), capture it as a CUDA graph for the next times."""
+        if not self.use_graphs:
+            fn()
+            return
+        g = self.graphs.get(key)
+        if g is None:
+            fn()
+            torch.cuda.synchronize(self.dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            self.graphs[key] = g
+            return
+        g.replay()
+
+    def _run_device_round(self, s: int, qc: int) -> None:
+        self._replay(("draft", s, qc), lambda: self._device_draft(s, qc))
+        self.ev_v0.record()
+        self._replay(("verify", s), lambda: self._device_verify(s))
+        self.ev_v1.record()
+
+    # ------------------------------------------------------------- host side
+    def _upload_round(self, s: int) -> int:
+        B = self.B
+        lens = np.array([len(c) for c in self.ctx] + [1] * (B - len(self.ctx)), np.int64)
+        active = np.array([r.state != RequestState.FINISHED for r in self.requests] +
+                          [False] * (B - len(self.requests)))
+        need = [lens[b] - self.ssm_cached[k][b] for k in range(self.K) for b in range(B) if active[b]]
+        qc = int(max(need)) if need else 1
+        qc = max(1, min(qc, s + 1))
+        start = np.maximum(lens - qc, 0)
+        c_tok = np.zeros((B, qc), np.int32)
+        for b, c in enumerate(self.ctx):
+            seg = c[start[b]: start[b] + qc]
+            c_tok[b, : len(seg)] = seg
+        c_head = np.arange(B) * qc + (lens - 1 - start)
+        rem = np.array([r.remaining if a else 0 for r, a in zip(self.requests, active)] +
+                       [0] * (B - len(self.requests)), np.int32)
+        last = np.array([c[-1] for c in self.ctx] + [0] * (B - len(self.ctx)), np.int32)
+        steps = np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]).astype(np.int32)
+        dev_vals = [
+            (self.ctx_len, lens.astype(np.int32)), (self.c_start, start.astype(np.int32)),
+            (self.c_head, c_head.astype(np.int32)), (self.v_start, (lens - 1).astype(np.int32)),
+            (self.last, last), (self.remaining, rem), (self.step_start, steps)]
+        for t, v in dev_vals:
+            t.copy_(torch.from_numpy(np.ascontiguousarray(v)), non_blocking=False)
+        self.c_tok.view(-1)[: B * qc].copy_(torch.from_numpy(c_tok.reshape(-1)))
+        w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)
+        self.w_dev.copy_(torch.from_numpy(w))
+        return qc
+
+    def run(self, requests: list[Request], max_rounds: int | None = None) -> RunResult:
+        """Generate until every request finishes (reference semantics)."""
+        self.prefill(requests)
+        return self.decode(max_rounds)
+
+    def decode(self, max_rounds: int | None = None) -> RunResult:
+        cfg = self.cfg
+        self.weights = WeightTable.from_config(list(range(self.K)), cfg)
+        self.selector = SelectorState.from_config(cfg)
+        res = RunResult(outputs={})
+        t0 = time.perf_counter()
+        rnd = 0
+        while any(r.state != RequestState.FINISHED for r in self.requests):
+            if max_rounds is not None and rnd >= max_rounds:
+                break
+            st = self._round(rnd)
+            res.rounds.append(st)
+            rnd += 1
+        torch.cuda.synchronize(self.dev)
+        res.wall_s = time.perf_counter() - t0
+        res.outputs = {r.id: list(r.generated) for r in self.requests}
+        res.tokens = sum(len(r.generated) for r in self.requests)
+        return res
+
+    def _round(self, rnd: int) -> RoundStats:
+        t_start = time.perf_counter()
+        s = self.selector.current_s
+        active = [b for b, r in enumerate(self.requests) if r.state != RequestState.FINISHED]
+        for b in active:
+            r = self.requests[b]
+            r.advance(RequestState.DRAFTING)
+        qc = self._upload_round(s)
+        self._run_device_round(s, qc)
+        # results (one sync)
+        a = self.acc
+        n_acc = a.n_acc.cpu().numpy()
+        n_emit = a.n_emit.cpu().numpy()
+        emitted = a.emitted.view(-1)[: self.B * (s + 1)].view(self.B, s + 1).cpu().numpy()
+        voted = self.voted.cpu().numpy()
+        drafts = self._drafts_s(s).cpu().numpy()
+        t_verify = self.ev_v0.elapsed_time(self.ev_v1)
+        accs, ems, vts = [], [], []
+        for b in active:
+            r = self.requests[b]
+            r.advance(RequestState.AWAITING_VERIFICATION)
+            acc = int(n_acc[b])
+            use = [int(t) for t in emitted[b, : n_emit[b]]]
+            record_acr(self.weights, int(voted[b]), acc / s)
+            if len(use) == 0:
+                raise NoProgress(f"request {r.id} made no progress")
+            len_before = len(self.ctx[b])
+            r.generated.extend(use)
+            self.ctx[b].extend(use)
+            stopped = self.cfg.stop_token is not None and self.cfg.stop_token in use
+            if stopped or r.remaining <= 0:
+                r.advance(RequestState.FINISHED)
+                r.finish_time = time.perf_counter()
+            else:
+                r.advance(RequestState.RUNNING)
+            # SSM rollback: valid up to the longest prefix agreement with `use`
+            for k in range(self.K):
+                mlen = 0
+                lim = min(s - 1, len(use) - 1)  # the last context token is always re-fed
+                while mlen < lim and drafts[b, k, mlen] == use[mlen]:
+                    mlen += 1
+                self.ssm_cached[k][b] = len_before + mlen
+            accs.append(acc)
+            ems.append(len(use))
+            vts.append(int(voted[b]))
+        update_weights(self.weights, self.cfg)
+        vl = float(np.mean(ems)) if ems else 1.0
+        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_verify, vl=vl, s_used=s))
+        decision = Decision.HOLD
+        if self.adaptive:
+            _, decision = maybe_adjust(self.selector)
+        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify,
+                          t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
+                          emitted=ems, voted=vts, vl=vl, decision=decision.value,
+                          s_next=self.selector.current_s, weights=dict(self.weights.weights))
+
+    # ----------------------------------------------------- greedy reference
+    def greedy_teacher(self, requests: list[Request], n_new: int) -> dict:
+        """Plain (non-speculative) greedy decoding with the target: one
+        forward of one row per request per token.  Used for fidelity injection
+        and as the lossless check (speculative output must equal it)."""
+        B = self.B
+        cache = self.t_cache
+        ctx = [list(r.prompt) for r in requests]
+        P = max(len(c) for c in ctx) - 1
+        toks = np.zeros((B, max(P, 1)), np.int32)
+        for b, c in enumerate(ctx):
+            toks[b, : len(c) - 1] = c[:-1]
+        zero = torch.zeros(B, dtype=I32, device=self.dev)
+        empty = torch.zeros(0, dtype=I32, device=self.dev)
+        dummy = torch.empty(0, self.V, device=self.dev)
+        if P > 0:
+            self.target.forward(torch.from_numpy(toks).to(self.dev), zero, self.slot, cache, dummy,
+                                head_rows=empty)
+        out = {r.id: [] for r in requests}
+        lens = np.array([len(c) for c in ctx] + [1] * (B - len(ctx)))
+        cur = np.array([c[-1] for c in ctx] + [0] * (B - len(ctx)), np.int32)
+        logits = torch.empty(B, self.V, device=self.dev)
+        am = torch.zeros(B, dtype=I32, device=self.dev)
+        ws = torch.zeros(B, dtype=torch.int64, device=self.dev)
+        for t in range(n_new):
+            self.target.forward(torch.from_numpy(cur[:, None].copy()).to(self.dev),
+                                torch.from_numpy((lens - 1).astype(np.int32)).to(self.dev),
+                                self.slot, cache, logits)
+            _native.call("ms_argmax_rows", logits.data_ptr(), 0, B, self.V, self.V, am.data_ptr(),
+                         ws.data_ptr(), _dev.stream_ptr())
+            nxt = am.cpu().numpy()
+            for b, r in enumerate(requests):
+                out[r.id].append(int(nxt[b]))
+            cur = nxt.astype(np.int32)
+            lens = lens + 1
+        return out

@@ -1,0 +1,90 @@
+"""Python wrappers of the model-forward kernels (csrc/gemm.cu, csrc/model.cu).
+
+Each wrapper checks shapes/dtypes, then calls the C-ABI with raw pointers on
+the current (or given) CUDA stream.  Nothing here allocates on the hot path
+when `out=` buffers are passed, so launches can be captured in CUDA graphs.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _dev
+from . import _native
+
+BF16 = torch.bfloat16
+
+
+def linear_splits(N: int, K: int) -> int:
+    return int(_native.lib.ms_linear_splits(N, K))
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
+           residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
+           out_f32: bool = False, splits: int = 0, stream=None) -> torch.Tensor:
+    """out = act(x @ w.T + bias) + residual on tcgen05 (ms_linear)."""
+    if x.dim() != 2 or w.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
+        raise ValueError("x [M, K] and w [N, K] must be 2-D bf16")
+    M, K = x.shape
+    N = w.shape[0]
+    if w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
+        raise ValueError("shape/stride mismatch")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    if out.stride(1) != 1 or out.shape != (M, N):
+        raise ValueError("out must be [M, N] with unit column stride")
+    if residual is not None and (residual.shape != (M, N) or residual.stride(1) != 1):
+        raise ValueError("residual must be [M, N]")
+    _native.call("ms_linear", x.data_ptr(), x.stride(0), w.data_ptr(),
+                 None if bias is None else _dev.ptr(bias, BF16, "bias"),
+                 None if residual is None else residual.data_ptr(),
+                 0 if residual is None else residual.stride(0),
+                 out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act,
+                 splits, _dev.stream_ptr(stream))
+    return out
+
+
+def embed(tok: torch.Tensor, start: torch.Tensor, Q: int, tok_emb: torch.Tensor,
+          pos_emb: torch.Tensor | None, pos_offset: int = 2, out: torch.Tensor | None = None,
+          stream=None) -> torch.Tensor:
+    """Rows r = b*Q + i (tok [B, Q] flattened) at positions start[b] + i."""
+    R = tok.numel()
+    d = tok_emb.shape[1]
+    out = out if out is not None else torch.empty((R, d), dtype=BF16, device=tok.device)
+    _native.call("ms_embed", _dev.ptr(tok, torch.int32, "tok"), _dev.ptr(start, torch.int32, "start"), Q,
+                 _dev.ptr(tok_emb, BF16), _dev.ptr(pos_emb, BF16), pos_offset, R, d,
+                 _dev.ptr(out, BF16), _dev.stream_ptr(stream))
+    return out
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5,
+              out: torch.Tensor | None = None, rows: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """LayerNorm of x's rows (or of x[rows] when a row-index tensor is given)."""
+    d = x.shape[1]
+    R = x.shape[0] if rows is None else rows.numel()
+    out = out if out is not None else torch.empty((R, d), dtype=BF16, device=x.device)
+    _native.call("ms_layernorm", x.data_ptr(), x.stride(0), _dev.ptr(rows, torch.int32, "rows"),
+                 _dev.ptr(gamma, BF16),
+                 _dev.ptr(beta, BF16), eps, R, d, out.data_ptr(), out.stride(0),
+                 _dev.stream_ptr(stream))
+    return out
+
+
+def kv_append(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
+              start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, stream=None) -> None:
+    T = k_cache.shape[2]
+    _native.call("ms_kv_append", qkv.data_ptr(), qkv.stride(0), B, Q, H, D,
+                 _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
+                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), _dev.stream_ptr(stream))
+
+
+def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
+              start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
+              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    T = k_cache.shape[2]
+    out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
+    _native.call("ms_attention", qkv.data_ptr(), qkv.stride(0), B, Q, H, D,
+                 _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
+                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), scale, out.data_ptr(),
+                 out.stride(0), _dev.stream_ptr(stream))
+    return out
