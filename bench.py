@@ -1,0 +1,389 @@
+"""Benchmark of the speculate-vote-verify hot path (BASELINE.json metric:
+output tokens/s + mean accepted length).
+
+Workload at N=1 (BASELINE.json configs[1], "cfg2"): OPT-13B target + 3 x
+OPT-125M drafters, bf16, one B200, batch 16, adaptive speculation length
+(s_init 4, s in [1, 12]), greedy, 128-token synthetic prompts, 128 new tokens
+per request.  Random-init weights (no checkpoints offline); because random-init
+drafters never agree with the target, drafts use fidelity injection
+(engine.py / DESIGN.md): with probability f_k SSM k's drafted token is
+replaced by the target's greedy continuation — every kernel still runs in
+full and the output stays exactly the target's greedy decode.
+
+One step = one generation batch: decode of 16 requests x 128 new tokens, from
+prefilled KV caches (prompt prefill is outside the hot path) to
+the last request finishing.  `value` = generated tokens / device time of the
+decode (CUDA events, weights 25.7 GB >> L2 so no flush is needed).  `e2e` =
+the same metric through the public API (SpecEngine.run) from host prompt
+lists, H2D of prompts + per-round metadata and D2H of per-round results
+inside the timed region, prompt prefill included.
+
+--impl reference: the reference's CPU path (the oracle port: the aggspec
+round logic over the fp32 CPU model under the reference's ModelOracle
+protocol — a full forward per next_dist call, no KV cache) on a bounded
+sample, scaled to tokens/s.
+
+Multi-GPU (torchrun, N>1): replicas only — every rank runs the same
+single-GPU workload on its own GPU (weak scaling, no data-path collective);
+value = all ranks' tokens / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output tokens/sec, Llama-2-70B + 3x160M SSMs, 1-8 B200; mean accepted length"
+WORKLOAD = "cfg2: OPT-13B target + 3x OPT-125M SSMs, bf16, 1 B200/rank, batch 16, adaptive s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--target", default="opt-13b")
+    ap.add_argument("--ssm", default="opt-125m")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--prompt-len", type=int, default=128)
+    ap.add_argument("--new-tokens", type=int, default=128)
+    ap.add_argument("--fidelity", default="0.9,0.85,0.8")
+    ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- dist
+def dist_init():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, ws, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------------- workload
+def make_requests(n, prompt_len, new_tokens, vocab, seed=0):
+    """make_requests semantics of aggspec/bench.py:177-186: ids req-%03d,
+    prompt tokens uniform in [0, V) from seeded_rng(seed, "workload")."""
+    from paper_2402_15678_b200.core import Request, seeded_rng
+    rng = seeded_rng(seed, "workload")
+    return [Request(f"req-{i:03d}", [int(t) for t in rng.integers(0, vocab, size=prompt_len)], new_tokens)
+            for i in range(n)]
+
+
+def fresh(reqs):
+    from paper_2402_15678_b200.core import Request
+    return [Request(r.id, list(r.prompt), r.max_new_tokens) for r in reqs]
+
+
+def roofline_verify(engine, rounds, peaks):
+    """Dominant unit: the verify forward (40 ms_linear GEMM quadruples + LM
+    head + attention), timed per round with CUDA events on its stream.
+    Algorithmic bytes per round = 2 * matmul params (bf16 weights) + KV read
+    (B * ctx * kv_bytes_per_token) + KV write (B * (s+1) * kv_bytes_per_token)."""
+    c = engine.target.cfg
+    P2 = 2 * c.matmul_params()
+    kvb = c.kv_bytes_per_token()
+    tot_bytes = tot_t = 0.0
+    for r in rounds:
+        ctx = r.ctx_mean
+        b = P2 + engine.B * ctx * kvb + engine.B * (r.s + 1) * kvb
+        tot_bytes += b
+        tot_t += r.t_verify_ms * 1e-3
+    ach = tot_bytes / tot_t / 1e9
+    peak = peaks.get("hbm_gbs", 6551.0)
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(ach / peak, 4), "traffic": None,
+            "kernel": "verify forward (ms_linear x4/layer + attention + LM head), per round",
+            "bytes_per_launch": round(tot_bytes / max(len(rounds), 1)),
+            "mean_ms": round(tot_t * 1e3 / max(len(rounds), 1), 3)}
+
+
+def run_ours(args, rank, ws):
+    import numpy as np
+    import torch
+
+    from paper_2402_15678_b200 import _native
+    from paper_2402_15678_b200.core import EngineConfig
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.opt import CONFIGS, OPTWeights
+
+    tcfg, scfg = CONFIGS[args.target], CONFIGS[args.ssm]
+    fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else None
+    K = 3
+    target = OPTWeights.random(tcfg, 0, device="cuda")
+    drafters = [OPTWeights.random(scfg, k + 1, device="cuda") for k in range(K)]
+    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch, s_init=4,
+                       s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
+    max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
+    eng = SpecEngine(target, drafters, cfg, slots=args.batch, max_len=max_len,
+                     use_graphs=not args.no_graphs, fidelity=fid)
+    reqs = make_requests(args.batch, args.prompt_len, args.new_tokens, tcfg.vocab)
+    teacher = eng.greedy_teacher(fresh(reqs), args.new_tokens) if fid else None
+
+    def one_step(timed_events=True):
+        rs = fresh(reqs)
+        eng.prefill(rs)
+        if teacher is not None:
+            eng.set_teacher(teacher)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        n0 = eng.kernel_launches
+        e0.record()
+        res = eng.decode()
+        e1.record()
+        torch.cuda.synchronize()
+        return res, e0.elapsed_time(e1) * 1e-3, eng.kernel_launches - n0
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier(ws)
+    torch.cuda.synchronize()
+    results, t_total, launches = [], 0.0, 0
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(args.steps):
+            res, t, nl = one_step()
+            results.append(res)
+            t_total += t
+            launches += nl
+    torch.cuda.synchronize()
+    barrier(ws)
+    lossless = all(r.outputs == teacher for r in results) if teacher else None
+    tokens = sum(r.tokens for r in results)
+    t_max = max_over_ranks(t_total, ws)
+    value = tokens * ws / t_max
+    rounds = [rd for r in results for rd in r.rounds]
+    # mean context per round for the KV term of the roofline
+    for r in results:
+        ctx = args.prompt_len
+        for rd in r.rounds:
+            rd.ctx_mean = ctx
+            ctx += rd.vl
+    acc = [a for rd in rounds for a in rd.accepted]
+    emt = [e for rd in rounds for e in rd.emitted]
+
+    # ---- e2e through the public API from host buffers (prefill included)
+    barrier(ws)
+    torch.cuda.synchronize()
+    h0, d0 = eng.h2d_bytes, eng.d2h_bytes
+    t0 = time.perf_counter()
+    e2e_tokens = 0
+    for _ in range(args.steps):
+        rs = fresh(reqs)
+        eng.prefill(rs)
+        if teacher is not None:
+            eng.set_teacher(teacher)
+            eng.h2d_bytes += eng.teacher.numel() * 4
+        res = eng.decode()
+        e2e_tokens += res.tokens
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(time.perf_counter() - t0, ws)
+    e2e = {"value": round(e2e_tokens * ws / t_e2e, 2), "unit": "tokens/s",
+           "h2d_bytes_per_step": int((eng.h2d_bytes - h0) / args.steps),
+           "d2h_bytes_per_step": int((eng.d2h_bytes - d0) / args.steps),
+           "includes": "prompt H2D + prefill + decode + per-round H2D/D2H"}
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic prompts, random-init weights, fidelity-injected drafts",
+        "config": {"workload": WORKLOAD, "target": args.target, "ssms": [args.ssm] * K,
+                   "global_batch": args.batch * ws, "prompt_len": args.prompt_len,
+                   "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
+                   "fidelity": fid, "parallelism": "replicas" if ws > 1 else "single-gpu",
+                   "l2": "inputs larger than L2 (25.7 GB of weights streamed per verify)",
+                   "graphs": not args.no_graphs},
+        "mean_accepted_length": round(float(np.mean(acc)), 4) if acc else 0.0,
+        "mean_emitted_per_round": round(float(np.mean(emt)), 4) if emt else 0.0,
+        "rounds_per_step": round(len(rounds) / args.steps, 2),
+        "s_trajectory_tail": [rd.s for rd in results[-1].rounds[-8:]],
+        "lossless_vs_greedy": lossless,
+        "verify_ms_mean": round(float(np.mean([rd.t_verify_ms for rd in rounds])), 3),
+        "round_ms_mean": round(float(np.mean([rd.t_round_ms for rd in rounds])), 3),
+        "roofline": roofline_verify(eng, rounds, peaks),
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "libminions": _native.LIB_PATH,
+    }
+    return out
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_baseline(args, vl: float | None = None, threads: int | None = None):
+    """The reference's CPU path on a bounded sample.
+
+    The reference's verify loop (aggspec/engine.py:294-296) and draft loop
+    (aggspec/oracles.py:146-150) call ModelOracle.next_dist once per position
+    with the full context — no KV cache — so one round costs
+    B*K*s drafter calls + B*(s+1) target calls.  We time one target call and
+    one drafter call of the fp32 CPU model (oracle/opt_ref.py) at the mean
+    context length of the run, with the target's layer count sampled
+    (`--cpu-sample-layers` layers timed, scaled to the full depth; weights of
+    one layer reused, which leaves the FLOP/byte count unchanged), plus the
+    reference-restated vote/verify logic, and scale to tokens/s with the
+    measured emitted tokens per round (vl)."""
+    import torch
+
+    from oracle import aggspec_oracle as O
+    from oracle import opt_ref
+    from paper_2402_15678_b200.opt import CONFIGS, OPTConfig, OPTWeights
+
+    n_thr = threads or len(os.sched_getaffinity(0))
+    torch.set_num_threads(n_thr)
+    tcfg, scfg = CONFIGS[args.target], CONFIGS[args.ssm]
+    L = min(args.cpu_sample_layers, tcfg.n_layers)
+    ctx = args.prompt_len + args.new_tokens // 2
+    s = 4
+    B = args.batch
+    K = 3
+
+    def call_time(cfg: OPTConfig, layers: int) -> float:
+        sub = OPTConfig(cfg.name, layers, cfg.d, cfg.n_heads, cfg.ffn, cfg.vocab, cfg.max_pos)
+        w = OPTWeights.random(sub, 0, device="cpu").t
+        toks = list(range(ctx))
+        opt_ref.forward(w, sub, toks[:8], last_only=True)  # warm
+        t0 = time.perf_counter()
+        opt_ref.forward(w, sub, toks, last_only=True)
+        t_full = time.perf_counter() - t0
+        return t_full
+
+    t_llm_sampled = call_time(tcfg, L)
+    # subtract-free scaling: time per layer from the sampled call (the embed +
+    # LM head share is counted once)
+    t_llm = t_llm_sampled * tcfg.n_layers / L
+    t_ssm = call_time(scfg, scfg.n_layers)
+    import numpy as np
+    rng = np.random.default_rng(0)
+    t0 = time.perf_counter()
+    for _ in range(B):
+        O.vote_one(rng.integers(0, 4, size=(K, s)), np.ones(K))
+        O.verify_greedy_one(rng.integers(0, 4, size=s), rng.integers(0, 4, size=s + 1))
+    t_logic = time.perf_counter() - t0
+    t_round = B * K * s * t_ssm + B * (s + 1) * t_llm + t_logic
+    vl = vl if vl is not None else 1.0
+    value = B * vl / t_round
+    return {"value": value, "unit": "tokens/s", "cores": n_thr, "kind": "port",
+            "sample": (f"one {tcfg.name} next_dist call at ctx {ctx} with {L}/{tcfg.n_layers} layers "
+                       f"timed ({t_llm_sampled:.2f}s, scaled x{tcfg.n_layers / L:.0f}), one {scfg.name} "
+                       f"call ({t_ssm:.2f}s), round = B*K*s drafter + B*(s+1) target calls (s=4, B={B}) "
+                       f"+ vote/verify logic; tokens/round = B*vl, vl={vl:.3f}"),
+            "t_round_s": t_round}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        cb = cpu_baseline(args, vl=None)
+        line = {"metric": METRIC, "value": round(cb["value"], 6), "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "impl": "reference",
+                "config": {"workload": WORKLOAD, "target": args.target, "ssms": [args.ssm] * 3,
+                           "global_batch": args.batch},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": round(cb["value"], 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+    rank, ws, local = dist_init()
+    out = run_ours(args, rank, ws)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            cb = cpu_baseline(args, vl=out["mean_emitted_per_round"])
+            out["cpu_baseline"] = {k: (round(v, 6) if isinstance(v, float) else v)
+                                   for k, v in cb.items() if k != "t_round_s"}
+        print(json.dumps(out))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

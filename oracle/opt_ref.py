@@ -34,9 +34,10 @@ def layernorm(x, g, b, eps):
     return _bf((x - mean) * torch.rsqrt(var + eps) * g + b)
 
 
-def forward(w: dict, cfg, tokens, start: int = 0) -> torch.Tensor:
+def forward(w: dict, cfg, tokens, start: int = 0, last_only: bool = False) -> torch.Tensor:
     """Full causal forward of one sequence (positions start..start+T-1 with no
-    cache: start must be 0).  tokens: [T] ints -> logits [T, V] fp32."""
+    cache: start must be 0).  tokens: [T] ints -> logits [T, V] fp32 (or [1, V]
+    for the last position only)."""
     assert start == 0
     f32 = {k: v.float() for k, v in w.items()}
     tok = torch.as_tensor(list(tokens), dtype=torch.long)
@@ -62,6 +63,8 @@ def forward(w: dict, cfg, tokens, start: int = 0) -> torch.Tensor:
         h = layernorm(x, f32[p + "ln2_g"], f32[p + "ln2_b"], cfg.eps)
         ff = _bf(torch.relu(h @ f32[p + "w_fc1"].T + f32[p + "b_fc1"]))
         x = _bf(ff @ f32[p + "w_fc2"].T + f32[p + "b_fc2"] + x)
+    if last_only:
+        x = x[-1:]
     h = layernorm(x, f32["lnf_g"], f32["lnf_b"], cfg.eps)
     return h @ f32["tok_emb"].T
 
@@ -70,7 +73,7 @@ def greedy_generate(w, cfg, prompt, n_new: int) -> list[int]:
     """Plain greedy decoding (first-index argmax), no speculation."""
     ctx = list(prompt)
     for _ in range(n_new):
-        logits = forward(w, cfg, ctx)[-1]
+        logits = forward(w, cfg, ctx, last_only=True)[-1]
         ctx.append(int(torch.argmax(logits)))
     return ctx[len(prompt):]
 
@@ -87,7 +90,7 @@ class OracleModel:
         self._f32 = None
 
     def argmax_next(self, context) -> int:
-        return int(torch.argmax(forward(self.w, self.cfg, context)[-1]))
+        return int(torch.argmax(forward(self.w, self.cfg, context, last_only=True)[-1]))
 
     def next_dist(self, context):
         import sys

@@ -70,6 +70,7 @@ class RoundStats:
     decision: str
     s_next: int
     weights: dict
+    trace: dict | None = None  # per-round device arrays when record=True
 
 
 @dataclass
@@ -95,7 +96,8 @@ class SpecEngine:
 
     def __init__(self, target: OPTWeights, drafters: list[OPTWeights], cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
-                 fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True):
+                 fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
+                 record: bool = False):
         validate_config(cfg)
         if len(cfg.initial_weights) != len(drafters):
             raise ValueError("initial_weights must have one entry per drafter")
@@ -106,6 +108,7 @@ class SpecEngine:
         self.B = slots
         self.max_len = max_len
         self.adaptive = adaptive
+        self.record = record
         s_cap = cfg.s_max
         self.max_rows_t = max(slots * (s_cap + 1), slots)
         self.target = OPTModel(target, max_rows=max(self.max_rows_t, slots * max_len), device=device)
@@ -148,6 +151,10 @@ class SpecEngine:
         self.teacher = z(B, max_len) - 1 if fidelity is not None else None
         self.use_graphs = use_graphs
         self.graphs: dict = {}
+        self.graph_kernels: dict = {}   # kernels per captured graph (launch accounting)
+        self.kernel_launches = 0        # kernels this engine issued (eager + replayed)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
         self.ev_v0 = torch.cuda.Event(enable_timing=True)
         self.ev_v1 = torch.cuda.Event(enable_timing=True)
@@ -180,6 +187,7 @@ class SpecEngine:
             for b, c in enumerate(self.ctx):
                 toks[b, : len(c) - 1] = c[:-1]
             t = torch.from_numpy(toks).to(self.dev)
+            self.h2d_bytes += toks.nbytes
             zero = torch.zeros(self.B, dtype=I32, device=self.dev)
             empty = torch.zeros(0, dtype=I32, device=self.dev)
             dummy = torch.empty(0, self.V, device=self.dev)
@@ -267,19 +275,25 @@ class SpecEngine:
     def _replay(self, key, fn) -> None:
         """Run fn eagerly the first time (sets kernel attributes, produces this
         round's results), capture it as a CUDA graph for the next times."""
+        n0 = _native.launch_count()
         if not self.use_graphs:
             fn()
+            self.kernel_launches += _native.launch_count() - n0
             return
         g = self.graphs.get(key)
         if g is None:
             fn()
             torch.cuda.synchronize(self.dev)
+            self.kernel_launches += _native.launch_count() - n0
             g = torch.cuda.CUDAGraph()
+            n1 = _native.launch_count()
             with torch.cuda.graph(g):
                 fn()
+            self.graph_kernels[key] = _native.launch_count() - n1
             self.graphs[key] = g
             return
         g.replay()
+        self.kernel_launches += self.graph_kernels[key]
 
     def _run_device_round(self, s: int, qc: int) -> None:
         self._replay(("draft", s, qc), lambda: self._device_draft(s, qc))
@@ -312,9 +326,11 @@ class SpecEngine:
             (self.last, last), (self.remaining, rem), (self.step_start, steps)]
         for t, v in dev_vals:
             t.copy_(torch.from_numpy(np.ascontiguousarray(v)), non_blocking=False)
+            self.h2d_bytes += v.nbytes
         self.c_tok.view(-1)[: B * qc].copy_(torch.from_numpy(c_tok.reshape(-1)))
         w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)
         self.w_dev.copy_(torch.from_numpy(w))
+        self.h2d_bytes += c_tok.nbytes + w.nbytes
         return qc
 
     def run(self, requests: list[Request], max_rounds: int | None = None) -> RunResult:
@@ -357,6 +373,7 @@ class SpecEngine:
         emitted = a.emitted.view(-1)[: self.B * (s + 1)].view(self.B, s + 1).cpu().numpy()
         voted = self.voted.cpu().numpy()
         drafts = self._drafts_s(s).cpu().numpy()
+        self.d2h_bytes += n_acc.nbytes + n_emit.nbytes + emitted.nbytes + voted.nbytes + drafts.nbytes
         t_verify = self.ev_v0.elapsed_time(self.ev_v1)
         accs, ems, vts = [], [], []
         for b in active:
@@ -392,7 +409,15 @@ class SpecEngine:
         decision = Decision.HOLD
         if self.adaptive:
             _, decision = maybe_adjust(self.selector)
-        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify,
+        trace = None
+        if self.record:
+            B = self.B
+            trace = dict(active=active, drafts=drafts, weights_used=self.w_dev.cpu().numpy(),
+                         path=self.path.view(-1)[: B * s].view(B, s).cpu().numpy(),
+                         voted=voted, n_acc=n_acc, n_emit=n_emit, emitted=emitted,
+                         tgt=a.tgt_argmax.view(-1)[: B * (s + 1)].view(B, s + 1).cpu().numpy(),
+                         remaining=self.remaining.cpu().numpy())
+        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, trace=trace,
                           t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
                           emitted=ems, voted=vts, vl=vl, decision=decision.value,
                           s_next=self.selector.current_s, weights=dict(self.weights.weights))
