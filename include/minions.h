@@ -144,12 +144,13 @@ int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
 
 /* Causal attention of Q query rows per request over the KV cache: query i of
  * request b (row b*Q + i of qkv) is at position start[b] + i and attends to
- * cache positions 0..start[b] + i.  out [B*Q, ldo] bf16, head h at columns
- * h*D.. .  Q > 17 is processed in chunks of 16 queries per CTA.
- * Limits: D in {64, 128}. */
+ * cache positions 0..start[b] + i.  With append != 0 the K/V columns of the Q
+ * rows are first written into the cache (fused into the kernel when Q <= 16,
+ * else an ms_kv_append launch precedes it).  out [B*Q, ldo] bf16, head h at
+ * columns h*D.. .  Limits: D in {64, 128}. */
 int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
-                 const int32_t* slot, const int32_t* start, int T, const void* k_cache,
-                 const void* v_cache, float scale, void* out, int64_t ldo, void* stream);
+                 const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                 void* v_cache, float scale, int append, void* out, int64_t ldo, void* stream);
 
 /* ---- round glue ------------------------------------------------------------
  * After an SSM decode step's argmax tok[B]: drafts[b, k, j] = tok[b] (the token

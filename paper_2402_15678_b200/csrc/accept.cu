@@ -35,6 +35,8 @@ template <bool kBf16>
 __global__ void __launch_bounds__(kArgmaxThreads)
 argmax_rows_kernel(const void* __restrict__ logits, int V, int64_t ld, int chunk,
                    unsigned long long* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.y;
   const int lo = blockIdx.x * chunk;
   const int hi = min(V, lo + chunk);
@@ -100,11 +102,15 @@ argmax_rows_kernel(const void* __restrict__ logits, int V, int64_t ld, int chunk
 }
 
 __global__ void argmax_init_kernel(unsigned long long* ws, int R) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < R) ws[i] = 0ull;
 }
 
 __global__ void argmax_finalize_kernel(const unsigned long long* ws, int R, int32_t* out) {
+  pdl_wait();
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < R) out[i] = ws[i] ? key_index(ws[i]) : 0;  // all-NaN row -> 0 like np.argmax
 }
@@ -120,6 +126,8 @@ accept_greedy_kernel(const int32_t* __restrict__ draft, const int32_t* __restric
                      int32_t* __restrict__ n_acc_out, int32_t* __restrict__ emitted,
                      int32_t* __restrict__ n_emit_out, int32_t* __restrict__ finished_out,
                      int32_t* __restrict__ kv_len) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = lane_id();
   const int b = blockIdx.x * kAcceptWarps + (threadIdx.x >> 5);
   if (b >= B) return;
@@ -173,15 +181,14 @@ static int launch_argmax(const void* logits, int is_bf16, int R, int V, int64_t 
   chunk = (chunk + 7) & ~7;  // keep slices 16B aligned for bf16 / fp32 vectors
   chunks = (V + chunk - 1) / chunk;
   const int tb = 256;
-  argmax_init_kernel<<<(R + tb - 1) / tb, tb, 0, st>>>(ws, R);
+  int s = launch(argmax_init_kernel, dim3((R + tb - 1) / tb), dim3(tb), 0, st, 1, ws, R);
+  if (s) return s;
   dim3 grid(chunks, R);
-  if (is_bf16)
-    argmax_rows_kernel<true><<<grid, kArgmaxThreads, 0, st>>>(logits, V, ld, chunk, ws);
-  else
-    argmax_rows_kernel<false><<<grid, kArgmaxThreads, 0, st>>>(logits, V, ld, chunk, ws);
-  argmax_finalize_kernel<<<(R + tb - 1) / tb, tb, 0, st>>>(ws, R, out);
-  count_launch(3);
-  return launch_status();
+  s = is_bf16 ? launch(argmax_rows_kernel<true>, grid, dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, chunk, ws)
+              : launch(argmax_rows_kernel<false>, grid, dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, chunk, ws);
+  if (s) return s;
+  return launch(argmax_finalize_kernel, dim3((R + tb - 1) / tb), dim3(tb), 0, st, 1,
+                (const unsigned long long*)ws, R, out);
 }
 
 }  // namespace ms
@@ -207,11 +214,9 @@ extern "C" int ms_accept_greedy(const int32_t* draft, const int32_t* tgt_argmax,
   if (!draft || !tgt_argmax || !remaining || !n_acc || !emitted || !n_emit || !finished)
     return MS_ERR_VALUE;
   const int blocks = (B + ms::kAcceptWarps - 1) / ms::kAcceptWarps;
-  ms::accept_greedy_kernel<<<blocks, ms::kAcceptWarps * 32, 0, (cudaStream_t)stream>>>(
-      draft, tgt_argmax, remaining, stop_token, B, S, n_acc, emitted, n_emit, finished,
-      kv_len);
-  ms::count_launch();
-  return ms::launch_status();
+  return ms::launch(ms::accept_greedy_kernel, dim3(blocks), dim3(ms::kAcceptWarps * 32), 0,
+                    (cudaStream_t)stream, 1, draft, tgt_argmax, remaining, stop_token, B, S, n_acc,
+                    emitted, n_emit, finished, kv_len);
 }
 
 extern "C" int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf16,

@@ -1,11 +1,20 @@
 // Library-level C-ABI: version, error strings, launch accounting.
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace ms {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 }  // namespace ms
 
 extern "C" int ms_version(void) { return 100; }

@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/minions.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -15,6 +17,45 @@ namespace ms {
 // Count of kernel launches issued through the C-ABI (read by bench.py as
 // `gpu_launches`).  Defined in capi.cu.
 void count_launch(int n = 1);
+
+// Programmatic dependent launch (PDL): every kernel of this library is
+// launched with programmatic stream serialization, waits on its predecessor
+// with griddepcontrol.wait before touching data the predecessor may have
+// written, and releases its dependents early with launch_dependents — so
+// the next kernel's prologue (TMEM alloc, barrier init, descriptor fetch,
+// weight-tile prefetch) overlaps this kernel's tail, in streams and in CUDA
+// graphs alike.  MS_PDL=0 in the environment disables the attribute.
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline int launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                  int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  ++n;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  if (cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) != cudaSuccess) return -5;
+  count_launch();
+  return 0;
+}
 
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();

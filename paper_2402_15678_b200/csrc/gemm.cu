@@ -128,20 +128,31 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     if (lane == 0) {
       const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
       const uint64_t pol_x = tc::policy_evict_last();   // tokens are re-read by every tile
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-        tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, n0, pol_w);
-        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, m0, pol_x);
-        if (++stage == C::STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+      // The first STAGES weight tiles do not depend on the previous kernel:
+      // issue them before the programmatic-dependency wait (PDL prefetch).
+      const int nkb = kb1 - kb0;
+      const int pre = nkb < C::STAGES ? nkb : C::STAGES;
+      for (int i = 0; i < pre; ++i) {
+        tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (kb0 + i) * kBK, n0, pol_w);
       }
+      pdl_wait();
+      pdl_trigger();
+      for (int i = 0; i < nkb; ++i) {
+        const int stage = i % C::STAGES;
+        const int kb = kb0 + i;
+        if (i >= pre) {
+          tc::mbar_wait(&empty[stage], ((i / C::STAGES) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, n0, pol_w);
+        }
+        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, m0, pol_x);
+      }
+    } else {
+      pdl_trigger();
     }
   } else if (warp == 1) {
+    pdl_trigger();
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
       int stage = 0;
@@ -168,6 +179,8 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     const int feat = n0 + q * 32 + lane;
     const bool feat_ok = feat < p.N;
     const int m_hi = min(BN, p.M - m0);  // valid token columns in this tile
+    pdl_wait();  // residual / outputs are ordered after the previous kernel
+    pdl_trigger();
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -197,6 +210,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
   }
   if (p.splits > 1) {
+    pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
     // `split` reduces a 1/splits slice of the tile, adding the partials of
     // ranks 0..splits-1 in rank order (deterministic), then runs the epilogue.
@@ -305,21 +319,8 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const Lin
       return MS_ERR_CUDA;
     attr_set = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_tiles * p.splits, m_tiles);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.splits;  // the split-K CTAs of a tile form one cluster
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, linear_kernel<BN>, tw, tx, p) != cudaSuccess) return MS_ERR_CUDA;
-  count_launch();
-  return launch_status();
+  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::SMEM, st,
+                p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
 }  // namespace ms

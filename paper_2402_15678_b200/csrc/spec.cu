@@ -28,6 +28,8 @@ __global__ void draft_commit_kernel(const int32_t* __restrict__ tok, const int32
                                     const int32_t* __restrict__ teacher, int64_t ld_teacher,
                                     const int32_t* __restrict__ req_key, float f, uint64_t seed,
                                     int32_t* __restrict__ drafts, int32_t* __restrict__ next_tok) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   int t = tok[b];
@@ -47,6 +49,8 @@ __global__ void draft_commit_kernel(const int32_t* __restrict__ tok, const int32
 
 __global__ void pack_verify_kernel(const int32_t* __restrict__ last, const int32_t* __restrict__ path,
                                    int B, int S, int32_t* __restrict__ vin) {
+  pdl_wait();
+  pdl_trigger();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B * (S + 1)) return;
   const int b = e / (S + 1), i = e - b * (S + 1);
@@ -62,10 +66,9 @@ extern "C" int ms_draft_commit(const int32_t* tok, const int32_t* ctx_len, int B
   if (B < 0 || j < 0 || j >= S || k < 0 || k >= K) return MS_ERR_VALUE;
   if (B == 0) return MS_OK;
   if (!tok || !drafts || (teacher && (!ctx_len || !req_key))) return MS_ERR_VALUE;
-  ms::draft_commit_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-      tok, ctx_len, B, j, k, K, S, teacher, ld_teacher, req_key, fidelity, seed, drafts, next_tok);
-  ms::count_launch();
-  return ms::launch_status();
+  return ms::launch(ms::draft_commit_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1,
+                    tok, ctx_len, B, j, k, K, S, teacher, ld_teacher, req_key, fidelity, seed, drafts,
+                    next_tok);
 }
 
 extern "C" int ms_pack_verify(const int32_t* last, const int32_t* path, int B, int S,
@@ -74,7 +77,6 @@ extern "C" int ms_pack_verify(const int32_t* last, const int32_t* path, int B, i
   if (B == 0) return MS_OK;
   if (!last || !path || !vin) return MS_ERR_VALUE;
   const int n = B * (S + 1);
-  ms::pack_verify_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(last, path, B, S, vin);
-  ms::count_launch();
-  return ms::launch_status();
+  return ms::launch(ms::pack_verify_kernel, dim3((n + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1,
+                    last, path, B, S, vin);
 }

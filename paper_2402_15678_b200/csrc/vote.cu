@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(kVoteWarps * 32)
 vote_kernel(const int32_t* __restrict__ tokens, const double* __restrict__ weights,
             const int32_t* __restrict__ rank, int B, int K, int S,
             int32_t* __restrict__ path, int32_t* __restrict__ voted) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = lane_id();
   const int b = blockIdx.x * kVoteWarps + (threadIdx.x >> 5);
   if (b >= B) return;  // warp-uniform
@@ -87,8 +89,6 @@ extern "C" int ms_vote(const int32_t* tokens, const double* weights, const int32
   if (B == 0) return MS_OK;
   if (!tokens || !weights || !path || !voted) return MS_ERR_VALUE;
   const int blocks = (B + ms::kVoteWarps - 1) / ms::kVoteWarps;
-  ms::vote_kernel<<<blocks, ms::kVoteWarps * 32, 0, (cudaStream_t)stream>>>(
-      tokens, weights, rank, B, K, S, path, voted);
-  ms::count_launch();
-  return ms::launch_status();
+  return ms::launch(ms::vote_kernel, dim3(blocks), dim3(ms::kVoteWarps * 32), 0, (cudaStream_t)stream, 1,
+                    tokens, weights, rank, B, K, S, path, voted);
 }

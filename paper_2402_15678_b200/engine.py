@@ -121,30 +121,52 @@ class SpecEngine:
         self.V = V
         B = slots
         z = lambda *sh: torch.zeros(sh, dtype=I32, device=self.dev)  # noqa: E731
-        # per-round inputs (uploaded once per round from one pinned buffer)
+        # per-round inputs: views into ONE int32 buffer uploaded with one H2D
+        # copy from a pinned mirror (the fp64 vote weights ride at its head)
+        Kw = 2 * self.K
+        sizes = [("w", Kw), ("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
+                 ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
+        n_meta = sum(n for _, n in sizes)
+        self.meta = torch.zeros(n_meta, dtype=I32, device=self.dev)
+        self.meta_h = torch.zeros(n_meta, dtype=I32, pin_memory=True)
+        self._meta_off = {}
+        o = 0
+        for name, n in sizes:
+            self._meta_off[name] = (o, n)
+            o += n
+        mv = lambda name: self.meta[self._meta_off[name][0]: sum(self._meta_off[name])]  # noqa: E731
+        self.w_dev = mv("w").view(torch.float64)
+        self.ctx_len, self.c_start, self.c_head = mv("ctx_len"), mv("c_start"), mv("c_head")
+        self.v_start, self.last, self.remaining = mv("v_start"), mv("last"), mv("remaining")
+        self.step_start = mv("step_start").view(s_cap, B)
+        self.c_tok = mv("c_tok")
         self.slot = torch.arange(B, dtype=I32, device=self.dev)
-        self.ctx_len = z(B)
-        self.c_start = z(B)
-        self.c_tok = z(B, s_cap + 1)
-        self.c_head = z(B)
-        self.v_start = z(B)
-        self.step_start = z(s_cap, B)
-        self.last = z(B)
-        self.remaining = z(B)
         self.req_key = z(B)
-        self.w_dev = torch.zeros(self.K, dtype=torch.float64, device=self.dev)
+        # per-round results: views into ONE int32 buffer downloaded with one D2H copy
+        rsz = [("n_acc", B), ("n_emit", B), ("finished", B), ("voted", B),
+               ("emitted", B * (s_cap + 1)), ("tgt", B * (s_cap + 1)), ("drafts", B * self.K * s_cap),
+               ("path", B * s_cap)]
+        n_res = sum(n for _, n in rsz)
+        self.res = torch.zeros(n_res, dtype=I32, device=self.dev)
+        self.res_h = torch.zeros(n_res, dtype=I32, pin_memory=True)
+        self._res_off = {}
+        o = 0
+        for name, n in rsz:
+            self._res_off[name] = (o, n)
+            o += n
+        rv = lambda name: self.res[self._res_off[name][0]: sum(self._res_off[name])]  # noqa: E731
+        self.drafts = rv("drafts")
+        self.path = rv("path")
+        self.voted = rv("voted")
+        self.acc = AcceptOut(rv("n_acc"), rv("emitted"), rv("n_emit"), rv("finished"), rv("tgt"))
         # per-round device intermediates
-        self.drafts = z(B, self.K, s_cap)
         self.step_tok = [z(B, 1) for _ in range(self.K)]
         self.argmax = [z(B) for _ in range(self.K)]
         self.argmax_ws = torch.zeros(max(B * (s_cap + 1), B), dtype=torch.int64, device=self.dev)
         self.ssm_ws = [torch.zeros(B, dtype=torch.int64, device=self.dev) for _ in range(self.K)]
         self.ssm_logits = [torch.empty(B, V, device=self.dev) for _ in range(self.K)]
-        self.path = z(B, s_cap)
-        self.voted = z(B)
         self.vin = z(B, s_cap + 1)
         self.v_logits = torch.empty(B * (s_cap + 1), V, device=self.dev)
-        self.acc = AcceptOut.alloc(B, s_cap, self.dev, with_argmax=True)
         # fidelity injection (bench mode)
         self.fidelity = list(fidelity) if fidelity is not None else None
         self.inject_seed = inject_seed
@@ -250,13 +272,13 @@ class SpecEngine:
 
     def _drafts_s(self, s):
         # drafts buffer viewed as [B, K, s] contiguous (the first B*K*s ints)
-        return self.drafts.view(-1)[: self.B * self.K * s].view(self.B, self.K, s)
+        return self.drafts[: self.B * self.K * s].view(self.B, self.K, s)
 
     def _draft(self, k, m: OPTModel, cache: KVCache, s: int, qc: int, st) -> None:
         B = self.B
         sp = _dev.stream_ptr(st)
         dr = self._drafts_s(s)
-        tok_in = self.c_tok.view(-1)[: B * qc].view(B, qc)
+        tok_in = self.c_tok[: B * qc].view(B, qc)
         teacher = self.teacher.data_ptr() if self.teacher is not None else None
         f = float(self.fidelity[k]) if self.fidelity is not None else 0.0
         for j in range(s):
@@ -320,17 +342,25 @@ class SpecEngine:
                        [0] * (B - len(self.requests)), np.int32)
         last = np.array([c[-1] for c in self.ctx] + [0] * (B - len(self.ctx)), np.int32)
         steps = np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]).astype(np.int32)
-        dev_vals = [
-            (self.ctx_len, lens.astype(np.int32)), (self.c_start, start.astype(np.int32)),
-            (self.c_head, c_head.astype(np.int32)), (self.v_start, (lens - 1).astype(np.int32)),
-            (self.last, last), (self.remaining, rem), (self.step_start, steps)]
-        for t, v in dev_vals:
-            t.copy_(torch.from_numpy(np.ascontiguousarray(v)), non_blocking=False)
-            self.h2d_bytes += v.nbytes
-        self.c_tok.view(-1)[: B * qc].copy_(torch.from_numpy(c_tok.reshape(-1)))
+        mh = self.meta_h.numpy()
+
+        def put(name, v):
+            o, n = self._meta_off[name]
+            v = np.ascontiguousarray(v, dtype=np.int32).reshape(-1)
+            mh[o: o + v.size] = v
+
         w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)
-        self.w_dev.copy_(torch.from_numpy(w))
-        self.h2d_bytes += c_tok.nbytes + w.nbytes
+        put("w", w.view(np.int32))
+        put("ctx_len", lens)
+        put("c_start", start)
+        put("c_head", c_head)
+        put("v_start", lens - 1)
+        put("last", last)
+        put("remaining", rem)
+        put("step_start", steps)
+        put("c_tok", c_tok)
+        self.meta.copy_(self.meta_h, non_blocking=True)  # one H2D for the whole round
+        self.h2d_bytes += self.meta_h.numel() * 4
         return qc
 
     def run(self, requests: list[Request], max_rounds: int | None = None) -> RunResult:
@@ -367,13 +397,21 @@ class SpecEngine:
         qc = self._upload_round(s)
         self._run_device_round(s, qc)
         # results (one sync)
-        a = self.acc
-        n_acc = a.n_acc.cpu().numpy()
-        n_emit = a.n_emit.cpu().numpy()
-        emitted = a.emitted.view(-1)[: self.B * (s + 1)].view(self.B, s + 1).cpu().numpy()
-        voted = self.voted.cpu().numpy()
-        drafts = self._drafts_s(s).cpu().numpy()
-        self.d2h_bytes += n_acc.nbytes + n_emit.nbytes + emitted.nbytes + voted.nbytes + drafts.nbytes
+        self.res_h.copy_(self.res, non_blocking=True)  # one D2H for the whole round
+        torch.cuda.current_stream(self.dev).synchronize()
+        self.d2h_bytes += self.res_h.numel() * 4
+        rh = self.res_h.numpy()
+
+        def get(name, n=None):
+            o, m = self._res_off[name]
+            return rh[o: o + (m if n is None else n)]
+
+        B = self.B
+        n_acc = get("n_acc")
+        n_emit = get("n_emit")
+        emitted = get("emitted", B * (s + 1)).reshape(B, s + 1)
+        voted = get("voted")
+        drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = self.ev_v0.elapsed_time(self.ev_v1)
         accs, ems, vts = [], [], []
         for b in active:
@@ -412,10 +450,10 @@ class SpecEngine:
         trace = None
         if self.record:
             B = self.B
-            trace = dict(active=active, drafts=drafts, weights_used=self.w_dev.cpu().numpy(),
-                         path=self.path.view(-1)[: B * s].view(B, s).cpu().numpy(),
-                         voted=voted, n_acc=n_acc, n_emit=n_emit, emitted=emitted,
-                         tgt=a.tgt_argmax.view(-1)[: B * (s + 1)].view(B, s + 1).cpu().numpy(),
+            trace = dict(active=active, drafts=drafts.copy(), weights_used=self.w_dev.cpu().numpy(),
+                         path=get("path", B * s).reshape(B, s).copy(), voted=voted.copy(),
+                         n_acc=n_acc.copy(), n_emit=n_emit.copy(), emitted=emitted.copy(),
+                         tgt=get("tgt", B * (s + 1)).reshape(B, s + 1).copy(),
                          remaining=self.remaining.cpu().numpy())
         return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, trace=trace,
                           t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,

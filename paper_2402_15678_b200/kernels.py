@@ -80,11 +80,12 @@ def kv_append(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
 
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
-              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+              out: torch.Tensor | None = None, append: bool = True, stream=None) -> torch.Tensor:
+    """Causal KV-cache attention of Q rows per request (K/V append fused when append)."""
     T = k_cache.shape[2]
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
     _native.call("ms_attention", qkv.data_ptr(), qkv.stride(0), B, Q, H, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
-                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), scale, out.data_ptr(),
-                 out.stride(0), _dev.stream_ptr(stream))
+                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), scale, int(append),
+                 out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
     return out

@@ -163,7 +163,6 @@ class OPTModel:
             p = f"l{i}."
             K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
             K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, splits=sp["qkv"], stream=stream)
-            K.kv_append(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
                         self.scale, out=at, stream=stream)
             K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, splits=sp["o"], stream=stream)
