@@ -274,25 +274,18 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
-// Split count for the weight-streaming regime: a function of (N, K) only.
+// Split count for the weight-streaming regime, a function of (N, K) only:
+// the smallest split that puts ~one CTA on each of the 148 SMs (measured best
+// on the OPT-13B / OPT-125M shapes: more splits add cluster-reduction and
+// prologue overhead, fewer leave SMs idle), capped at the portable cluster
+// size 8 and at >= 2 k-blocks (128 K-elements) per split.
 int linear_auto_splits(int N, int K) {
   const int n_tiles = (N + kBM - 1) / kBM;
   const int kb = (K + kBK - 1) / kBK;
-  const int slots = 148 * 2;
-  int best = 1;
-  double best_cost = 1e30;
-  for (int sp = 1; sp <= 8; ++sp) {
-    if (sp > 1 && kb / sp < 4) break;
-    const int units = n_tiles * sp;
-    const int waves = (units + slots - 1) / slots;
-    const double per_unit = (double)((kb + sp - 1) / sp);
-    const double cost = waves * per_unit + (sp > 1 ? 2.0 : 0.0);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = sp;
-    }
-  }
-  return best;
+  int sp = (148 + n_tiles - 1) / n_tiles;
+  sp = sp > 8 ? 8 : sp;
+  while (sp > 1 && kb / sp < 2) --sp;
+  return sp < 1 ? 1 : sp;
 }
 
 static int pick_bn(int M) {
