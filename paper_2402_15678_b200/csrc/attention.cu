@@ -5,21 +5,26 @@
 // (aggspec/oracles.py:19-26) for the draft (aggspec/oracles.py:148) and
 // verify (aggspec/engine.py:294-296) positions.
 //
-// One CTA (4 warps) per (request, head[, query chunk]).  The request's K and
-// V streams [T, D] are staged through shared memory in tiles of 64 keys with
-// cp.async double buffering (16-byte copies, every thread issuing several in
-// flight), so each K/V byte is read from HBM once for all the queries of the
-// request — the kernel is HBM-bound on the KV cache.  Scores, online softmax
-// and P·V run from shared memory in fp32.
+// One CTA (4 warps) per (request, head[, 16-query chunk]).  The request's K
+// and V streams [T, D] are staged through shared memory in tiles of 64 keys
+// with cp.async double buffering (16-byte copies, all threads issuing), so
+// each K/V byte is read from HBM once for all the queries of the request: the
+// kernel is bound by the KV-cache stream.  The (<= 16 queries) x (64 keys)
+// score tile and the P·V product run on warp-level tensor-core MMAs
+// (mma.m16n8k16 bf16 -> fp32; decode has far too few query rows for a
+// 128-row tcgen05 tile): warp w owns keys 16w..16w+15 of every tile, keeps
+// its own online-softmax state and output accumulator in registers, and the
+// 4 warps are merged in warp order at the end.
 //
-// Batch invariance: a query's score/softmax/P·V arithmetic is fixed by its own
-// position (same tile order, same per-tile reductions); other queries only add
-// fully-masked tiles whose contribution is exactly zero.
+// Batch invariance: a query row's arithmetic (its MMA rows, per-row quad
+// reductions, tile order, warp-order merge) does not depend on the other
+// rows; rows of other queries only add fully-masked keys that contribute
+// exactly zero.
 #include "common.cuh"
 
 namespace ms {
 
-constexpr int kKT = 64;        // keys per tile
+constexpr int kKT = 64;  // keys per tile (16 per warp)
 constexpr int kAThreads = 128;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -31,37 +36,56 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int D, int QM>
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// D(16x8) += A(16x16, row) * B(16x8, col), bf16 in, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+
+template <int D>
 struct AttnSmem {
-  static constexpr int LD = D + 8;  // padded row: 16-byte row chunks land in distinct bank groups
-  static constexpr int KV_BYTES = 2 * 2 * kKT * LD * 2;  // [K|V][buf][KT][LD] bf16
-  static constexpr int Q_BYTES = QM * D * 4;
-  static constexpr int P_BYTES = QM * kKT * 4;
-  static constexpr int BYTES = KV_BYTES + Q_BYTES + P_BYTES + 3 * QM * 4;
+  static constexpr int LD = D + 8;  // padded rows: fragment loads are bank-conflict free
+  static constexpr int TILE = kKT * LD;                  // elements per K (or V) tile
+  static constexpr int KV_BYTES = 2 * 2 * TILE * 2;      // [K|V][buf] bf16
+  static constexpr int MERGE_BYTES = 4 * 16 * (D + 2) * 4;  // per-warp (m, l, O) for the merge
+  static constexpr int BYTES = KV_BYTES > MERGE_BYTES ? KV_BYTES : MERGE_BYTES;
 };
 
-template <int D, int QM>
+template <int D>
 __global__ void __launch_bounds__(kAThreads)
 attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int H,
                  const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
-                 __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale,
+                 __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                  int fuse_append, __nv_bfloat16* __restrict__ out, int64_t ldo) {
-  using S = AttnSmem<D, QM>;
+  using S = AttnSmem<D>;
   constexpr int LD = S::LD;
+  constexpr int KC = D / 16;  // 16-dim chunks (MMA k-steps for Q.K^T)
+  constexpr int NT = D / 8;   // 8-dim output tiles for P.V
   extern __shared__ __align__(16) uint8_t smem[];
   pdl_wait();
   pdl_trigger();
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem);  // [2][KT][LD]
-  __nv_bfloat16* sV = sK + 2 * kKT * LD;                          // [2][KT][LD]
-  float* sQ = reinterpret_cast<float*>(smem + S::KV_BYTES);        // [QM][D]
-  float* sP = sQ + QM * D;                                         // [QM][KT]
-  float* sCorr = sP + QM * kKT;                                    // [QM]
-  float* sL = sCorr + QM;                                          // [QM]
+  __nv_bfloat16* sV = sK + 2 * S::TILE;                           // [2][KT][LD]
 
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q0 = blockIdx.z * QM;
-  const int Q = min(QM, Qtot - q0);
+  const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  const int q0 = blockIdx.z * 16;
+  const int Q = min(16, Qtot - q0);
   const int pstart = start[b];
   const int p0 = pstart + q0;
   const int64_t cbase = ((int64_t)slot[b] * H + h) * T * D;
@@ -83,12 +107,33 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
     }
     __threadfence();
+    __syncthreads();
   }
-  for (int e = tid; e < Q * D; e += kAThreads) {
-    const int i = e / D, dd = e - i * D;
-    sQ[e] = bf2f(qkv[(int64_t)(b * Qtot + q0 + i) * ldq + h * D + dd]) * scale;
+
+  // Q fragments (rows g, g+8 of the 16-query tile); the softmax scale
+  // log2(e)/sqrt(D) is applied to the fp32 scores
+  uint32_t qa[KC][4];
+  {
+    const int r0 = g, r1 = g + 8;
+    const __nv_bfloat16* q0p = qkv + (int64_t)(b * Qtot + q0 + r0) * ldq + h * D;
+    const __nv_bfloat16* q1p = qkv + (int64_t)(b * Qtot + q0 + r1) * ldq + h * D;
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      float f[8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int dd = c * 16 + 2 * t4 + 8 * u;
+        f[4 * u + 0] = r0 < Q ? bf2f(q0p[dd]) : 0.f;
+        f[4 * u + 1] = r0 < Q ? bf2f(q0p[dd + 1]) : 0.f;
+        f[4 * u + 2] = r1 < Q ? bf2f(q1p[dd]) : 0.f;
+        f[4 * u + 3] = r1 < Q ? bf2f(q1p[dd + 1]) : 0.f;
+      }
+      qa[c][0] = pack_bf16(f[0], f[1]);  // (row g,   k 2t..2t+1)
+      qa[c][1] = pack_bf16(f[2], f[3]);  // (row g+8, k 2t..2t+1)
+      qa[c][2] = pack_bf16(f[4], f[5]);  // (row g,   k 2t+8..)
+      qa[c][3] = pack_bf16(f[6], f[7]);  // (row g+8, k 2t+8..)
+    }
   }
-  __syncthreads();
 
   const int n_keys = min(p0 + Q, T);  // keys 0 .. p0+Q-1
   const int n_tiles = (n_keys + kKT - 1) / kKT;
@@ -101,31 +146,22 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       const int kv = e >= kKT * V8;
       const int e2 = e - kv * kKT * V8;
       const int j = e2 / V8, c = e2 - j * V8;
-      if (j < rows) {
-        const __nv_bfloat16* src = (kv ? V : K) + (int64_t)(t0 + j) * D + c * 8;
-        __nv_bfloat16* dst = (kv ? sV : sK) + (buf * kKT + j) * LD + c * 8;
-        cp_async16(dst, src);
-      }
+      __nv_bfloat16* dst = (kv ? sV : sK) + buf * S::TILE + j * LD + c * 8;
+      if (j < rows)
+        cp_async16(dst, (kv ? V : K) + (int64_t)(t0 + j) * D + c * 8);
+      else
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);  // masked keys must be finite
     }
     cp_async_commit();
   };
 
-  // per-query softmax state lives in the warp that owns query i (i % 4 == warp)
-  constexpr int QW = (QM + 3) / 4;
-  float m_r[QW], l_r[QW];
+  float m_r[2] = {-INFINITY, -INFINITY};  // rows g, g+8 (log2 domain)
+  float l_r[2] = {0.f, 0.f};
+  float o[NT][4];
 #pragma unroll
-  for (int u = 0; u < QW; ++u) {
-    m_r[u] = -INFINITY;
-    l_r[u] = 0.f;
-  }
-  // P·V ownership: thread -> output dim d, queries i = g, g + NG, ...
-  constexpr int NG = kAThreads / D;  // 1 (D=128) or 2 (D=64)
-  constexpr int QT = (QM + NG - 1) / NG;
-  const int d = tid % D;
-  const int g = tid / D;
-  float acc[QT];
-#pragma unroll
-  for (int u = 0; u < QT; ++u) acc[u] = 0.f;
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  const int row_lim0 = g < Q ? p0 + g : -1;      // last key position row g may see
+  const int row_lim1 = g + 8 < Q ? p0 + g + 8 : -1;
 
   if (n_tiles > 0) load_tile(0, 0);
   for (int tile = 0; tile < n_tiles; ++tile) {
@@ -137,117 +173,141 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       cp_async_wait<0>();
     }
     __syncthreads();
-    const int t0 = tile * kKT;
-    // scores S[i][j] = q_i . k_j (fp32, sequential over d)
-    const __nv_bfloat16* kt = sK + buf * kKT * LD;
-    for (int e = tid; e < Q * kKT; e += kAThreads) {
-      const int i = e / kKT, j = e - i * kKT;
-      const int t = t0 + j;
-      float sc = -INFINITY;
-      if (t < n_keys && t <= p0 + i) {
-        const float* qr = sQ + i * D;
-        const __nv_bfloat16* kr = kt + j * LD;
-        float a = 0.f;
-#pragma unroll 4
-        for (int c = 0; c < D / 8; ++c) {
-          float kf[8];
-          unpack8(*reinterpret_cast<const bf16x8*>(kr + c * 8), kf);
-          const float4 qa = *reinterpret_cast<const float4*>(qr + c * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(qr + c * 8 + 4);
-          a = fmaf(qa.x, kf[0], a);
-          a = fmaf(qa.y, kf[1], a);
-          a = fmaf(qa.z, kf[2], a);
-          a = fmaf(qa.w, kf[3], a);
-          a = fmaf(qb.x, kf[4], a);
-          a = fmaf(qb.y, kf[5], a);
-          a = fmaf(qb.z, kf[6], a);
-          a = fmaf(qb.w, kf[7], a);
-        }
-        sc = a;
-      }
-      sP[i * kKT + j] = sc;
-    }
-    __syncthreads();
-    // online softmax per query (warp `i % 4`), 64 keys = 2 per lane
+    const int kbase = tile * kKT + warp * 16;  // this warp's 16 keys
+    const __nv_bfloat16* kt = sK + buf * S::TILE + (warp * 16) * LD;
+    const __nv_bfloat16* vt = sV + buf * S::TILE + (warp * 16) * LD;
+    // S = Q K^T for two 8-key n-tiles
+    float s[2][4];
 #pragma unroll
-    for (int u = 0; u < QW; ++u) {
-      const int i = warp + 4 * u;
-      if (i < Q) {
-        const float v0 = sP[i * kKT + lane], v1 = sP[i * kKT + lane + 32];
-        const float mx = warp_max(fmaxf(v0, v1));
-        const float mn = fmaxf(m_r[u], mx);
-        float e0 = 0.f, e1 = 0.f, corr = 1.f;
-        if (mn != -INFINITY) {
-          e0 = __expf(v0 - mn);
-          e1 = __expf(v1 - mn);
-          corr = __expf(m_r[u] - mn);
-        }
-        l_r[u] = l_r[u] * corr + warp_sum(e0 + e1);
-        m_r[u] = mn;
-        sP[i * kKT + lane] = e0;
-        sP[i * kKT + lane + 32] = e1;
-        if (lane == 0) sCorr[i] = corr;
+    for (int n = 0; n < 2; ++n) {
+      s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+      const __nv_bfloat16* kr = kt + (n * 8 + g) * LD + 2 * t4;
+#pragma unroll
+      for (int c = 0; c < KC; ++c) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + c * 16);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + c * 16 + 8);
+        mma16816(s[n], qa[c], b0, b1);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[n][e] *= scale_log2;
+    }
+    // causal / length mask, online softmax (rows g and g+8; the 4 lanes of a
+    // quad hold a row's 16 keys)
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kbase + n * 8 + 2 * t4 + (e & 1);
+        const int lim = (e < 2) ? row_lim0 : row_lim1;
+        if (key > lim || key >= n_keys) s[n][e] = -INFINITY;
+        mx[e >> 1] = fmaxf(mx[e >> 1], s[n][e]);
       }
     }
-    __syncthreads();
-    // P·V from shared memory
-    const __nv_bfloat16* vt = sV + buf * kKT * LD;
-    const int kmax = min(kKT, n_keys - t0);
+    float corr[2], psum[2];
 #pragma unroll
-    for (int u = 0; u < QT; ++u) {
-      const int i = g + NG * u;
-      if (i < Q) acc[u] *= sCorr[i];
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      const float mn = fmaxf(m_r[r], mx[r]);
+      corr[r] = (mn == -INFINITY) ? 1.f : exp2f(m_r[r] - mn);
+      m_r[r] = mn;
+      psum[r] = 0.f;
     }
-    for (int j = 0; j < kmax; ++j) {
-      const float v = bf2f(vt[j * LD + d]);
 #pragma unroll
-      for (int u = 0; u < QT; ++u) {
-        const int i = g + NG * u;
-        if (i < Q) acc[u] = fmaf(sP[i * kKT + j], v, acc[u]);
+    for (int n = 0; n < 2; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = e >> 1;
+        const float p = (m_r[r] == -INFINITY || s[n][e] == -INFINITY) ? 0.f : exp2f(s[n][e] - m_r[r]);
+        s[n][e] = p;
+        psum[r] += p;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 1);
+      psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 2);
+      l_r[r] = l_r[r] * corr[r] + psum[r];
+    }
+    // P (bf16) as the A operand straight from the score accumulators
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[0][0], s[0][1]);
+    pa[1] = pack_bf16(s[0][2], s[0][3]);
+    pa[2] = pack_bf16(s[1][0], s[1][1]);
+    pa[3] = pack_bf16(s[1][2], s[1][3]);
+    // O = O * corr + P V   (V fragments via ldmatrix.trans, two 8-dim tiles per load)
+    const int lrow = lane & 15;              // key row within the warp's 16
+    const int lcol = (lane >> 4) * 8;        // dim offset 0 / 8 within a 16-dim pair
+#pragma unroll
+    for (int n2 = 0; n2 < NT / 2; ++n2) {
+      uint32_t vb[4];
+      ldmatrix_x4_trans(vb, vt + lrow * LD + n2 * 16 + lcol);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        float* on = o[2 * n2 + u];
+        on[0] *= corr[0];
+        on[1] *= corr[0];
+        on[2] *= corr[1];
+        on[3] *= corr[1];
+        mma16816(o[2 * n2 + u], pa, vb[2 * u], vb[2 * u + 1]);
       }
     }
     __syncthreads();
   }
+  // merge the 4 warps' (m, l, O) in warp order
+  float* sm = reinterpret_cast<float*>(smem);  // [4][16] m, [4][16] l, [4][16][D] O
+  float* sl = sm + 4 * 16;
+  float* so = sl + 4 * 16;
+  if (t4 == 0) {
+    sm[warp * 16 + g] = m_r[0];
+    sm[warp * 16 + g + 8] = m_r[1];
+    sl[warp * 16 + g] = l_r[0];
+    sl[warp * 16 + g + 8] = l_r[1];
+  }
 #pragma unroll
-  for (int u = 0; u < QW; ++u) {
-    const int i = warp + 4 * u;
-    if (i < Q && lane == 0) sL[i] = l_r[u];
+  for (int n = 0; n < NT; ++n) {
+    const int c = n * 8 + 2 * t4;
+    so[(warp * 16 + g) * D + c] = o[n][0];
+    so[(warp * 16 + g) * D + c + 1] = o[n][1];
+    so[(warp * 16 + g + 8) * D + c] = o[n][2];
+    so[(warp * 16 + g + 8) * D + c + 1] = o[n][3];
   }
   __syncthreads();
+  for (int e = tid; e < Q * D; e += kAThreads) {
+    const int i = e / D, dd = e - i * D;
+    float mxx = sm[i];
 #pragma unroll
-  for (int u = 0; u < QT; ++u) {
-    const int i = g + NG * u;
-    if (i < Q) out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + d] = f2bf(acc[u] / sL[i]);
+    for (int w = 1; w < 4; ++w) mxx = fmaxf(mxx, sm[w * 16 + i]);
+    float L = 0.f, A = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sm[w * 16 + i];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - mxx);
+      L += sl[w * 16 + i] * f;
+      A += so[(w * 16 + i) * D + dd] * f;
+    }
+    out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + dd] = f2bf(A / L);
   }
 }
 
-template <int D, int QM>
+template <int D>
 static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, const int32_t* slot,
                        const int32_t* start, int T, void* kc, void* vc, float scale, int fuse,
                        void* out, int64_t ldo, cudaStream_t st) {
-  using S = AttnSmem<D, QM>;
+  using S = AttnSmem<D>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attention_kernel<D, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(attention_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              S::BYTES) != cudaSuccess)
       return MS_ERR_CUDA;
     attr = true;
   }
-  dim3 grid(B, H, (Q + QM - 1) / QM);
-  return launch(attention_kernel<D, QM>, grid, dim3(kAThreads), S::BYTES, st, 1,
+  const float scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(B, H, (Q + 15) / 16);
+  return launch(attention_kernel<D>, grid, dim3(kAThreads), S::BYTES, st, 1,
                 (const __nv_bfloat16*)qkv, ldq, Q, H, slot, start, T, (__nv_bfloat16*)kc,
-                (__nv_bfloat16*)vc, scale, fuse, (__nv_bfloat16*)out, ldo);
-}
-
-template <int D>
-static int attention_d(const void* qkv, int64_t ldq, int B, int Q, int H, const int32_t* slot,
-                       const int32_t* start, int T, void* kc, void* vc, float scale, int fuse,
-                       void* out, int64_t ldo, cudaStream_t st) {
-  if (Q <= 1) return launch_attn<D, 1>(qkv, ldq, B, Q, H, slot, start, T, kc, vc, scale, fuse, out, ldo, st);
-  if (Q <= 2) return launch_attn<D, 2>(qkv, ldq, B, Q, H, slot, start, T, kc, vc, scale, fuse, out, ldo, st);
-  if (Q <= 4) return launch_attn<D, 4>(qkv, ldq, B, Q, H, slot, start, T, kc, vc, scale, fuse, out, ldo, st);
-  if (Q <= 8) return launch_attn<D, 8>(qkv, ldq, B, Q, H, slot, start, T, kc, vc, scale, fuse, out, ldo, st);
-  return launch_attn<D, 16>(qkv, ldq, B, Q, H, slot, start, T, kc, vc, scale, fuse, out, ldo, st);
+                (__nv_bfloat16*)vc, scale_log2, fuse, (__nv_bfloat16*)out, ldo);
 }
 
 }  // namespace ms
@@ -275,8 +335,8 @@ extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, i
     }
   }
   if (D == 64)
-    return ms::attention_d<64>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
+    return ms::launch_attn<64>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
   if (D == 128)
-    return ms::attention_d<128>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
+    return ms::launch_attn<128>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
   return MS_ERR_UNSUPPORTED;
 }
