@@ -110,17 +110,26 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
  *   x [M, ldx] bf16, w [N, K] bf16 (nn.Linear layout), bias [N] bf16 or NULL,
  *   residual [M, ldr] bf16 or NULL, out [M, ldc] bf16 (out_f32 = 0) or fp32,
  *   act 0 = identity, 1 = ReLU.
- * splits: split-K factor (0 = ms_linear_splits(N, K), max 8): the CTAs of a
- * tile form a thread-block cluster and reduce through distributed shared
- * memory.  Results are deterministic, and a row's result does not depend on M
- * (batch invariant) for a fixed `splits`.
+ * Two schedules, both deterministic and batch invariant (a row's result does
+ * not depend on M, because the work partition depends only on N and K):
+ *  - M <= 256, splits == 0 and scratch given: persistent stream-K kernel (one
+ *    CTA per SM, deep TMA pipeline, (tile, k-block) iterations split evenly
+ *    over the SMs, partial tiles combined in k order by the last CTA of a
+ *    tile).  Scratch: ws >= ms_linear_workspace() bytes, counters >=
+ *    n_counters ints, zero on first use (every launch leaves them zero).
+ *  - otherwise: one CTA per (128-feature tile, split); the `splits` CTAs of a
+ *    tile (0 = ms_linear_splits(N, K), max 8) form a thread-block cluster and
+ *    reduce through distributed shared memory.
  * Limits: K % 8 == 0, ldx % 8 == 0, x and w 16-byte aligned.
  */
 int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-              int M, int N, int K, int act, int splits, void* stream);
-/* Default split-K factor for an [N, K] weight (weight-streaming regime). */
+              int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
+              int* counters, int n_counters, void* stream);
+/* Default split-K factor for an [N, K] weight (cluster path). */
 int ms_linear_splits(int N, int K);
+/* Scratch the stream-K path needs for this shape. */
+int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* n_counters);
 
 /* ---- decoder pieces around the GEMMs (OPT-style, pre-LN) ----------------
  * Token + learned-position embedding of R = B*Q rows: row r = b*Q + i is at

@@ -230,12 +230,17 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 2);
       l_r[r] = l_r[r] * corr[r] + psum[r];
     }
-    // P (bf16) as the A operand straight from the score accumulators
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
+    // P as the A operand straight from the score accumulators, split into
+    // bf16 hi + lo parts (P = hi + lo to ~2^-16) so P.V keeps fp32-like accuracy
+    uint32_t pa[4], pl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float x0 = s[u >> 1][2 * (u & 1)], x1 = s[u >> 1][2 * (u & 1) + 1];
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(x0, x1);
+      const float2 hf = __bfloat1622float2(hi);
+      pa[u] = *reinterpret_cast<const uint32_t*>(&hi);
+      pl[u] = pack_bf16(x0 - hf.x, x1 - hf.y);
+    }
     // O = O * corr + P V   (V fragments via ldmatrix.trans, two 8-dim tiles per load)
     const int lrow = lane & 15;              // key row within the warp's 16
     const int lcol = (lane >> 4) * 8;        // dim offset 0 / 8 within a 16-dim pair
@@ -251,6 +256,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
         on[2] *= corr[1];
         on[3] *= corr[1];
         mma16816(o[2 * n2 + u], pa, vb[2 * u], vb[2 * u + 1]);
+        mma16816(o[2 * n2 + u], pl, vb[2 * u], vb[2 * u + 1]);
       }
     }
     __syncthreads();

@@ -245,6 +245,224 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
 }
 
 // ---------------------------------------------------------------------------
+// Persistent stream-K variant for the decode / verify regime (one token tile,
+// M <= 256).  G persistent CTAs (one per SM, deep TMA pipeline: 8-11 stages of
+// weight tiles in flight) split the n_tiles x kb_total (tile, k-block)
+// iterations into G equal contiguous ranges, so every SM streams the same
+// number of weight bytes whatever N and K are.  A CTA walks its range tile
+// segment by tile segment, accumulating in one of two TMEM buffers while the
+// epilogue warps drain the other.  A segment that covers a whole tile is
+// stored directly; partial segments go to a per-CTA fp32 slot and the LAST
+// CTA to finish a tile (atomic counter) adds the slots in segment (= k) order
+// and runs the epilogue — deterministic, and M-independent (the partition is
+// a function of N, K and G only), so batch-invariant like the split-K path.
+// ---------------------------------------------------------------------------
+struct SKParams {
+  int iters;       // n_tiles * kb_total
+  int grid;        // G
+  float* ws;       // [G][2][BN][128] fp32 partial slots
+  int* counters;   // [n_tiles], zero on entry, left zero
+};
+
+template <int BN>
+struct SKCfg {
+  static constexpr int W_BYTES = kBM * kBK * 2;
+  static constexpr int X_BYTES = BN * kBK * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  static constexpr int STAGES_RAW = (216 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered accumulator
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
+};
+
+__device__ __forceinline__ int sk_begin(int c, int iters, int G) {
+  return (int)((int64_t)c * iters / G);
+}
+// CTA whose range contains iteration i
+__device__ __forceinline__ int sk_owner(int i, int iters, int G) {
+  int c = (int)((int64_t)i * G / iters);
+  while (c + 1 < G && sk_begin(c + 1, iters, G) <= i) ++c;
+  while (c > 0 && sk_begin(c, iters, G) > i) --c;
+  return c;
+}
+
+__device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                 const LinearParams p, const SKParams sk) {
+  using C = SKCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + C::STAGES * C::W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int kbt = p.kb_total;
+  const int it0 = sk_begin(c, sk.iters, sk.grid);
+  const int it1 = sk_begin(c + 1, sk.iters, sk.grid);
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmW);
+    tc::prefetch_tmap(&tmX);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = tc::policy_evict_first();
+      const uint64_t pol_x = tc::policy_evict_last();
+      const int n = it1 - it0;
+      const int pre = n < C::STAGES ? n : C::STAGES;
+      for (int i = 0; i < pre; ++i) {  // weight tiles: independent of the previous kernel
+        const int it = it0 + i;
+        tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (it % kbt) * kBK, (it / kbt) * kBM, pol_w);
+      }
+      pdl_wait();
+      pdl_trigger();
+      for (int i = 0; i < n; ++i) {
+        const int it = it0 + i;
+        const int stage = i % C::STAGES;
+        if (i >= pre) {
+          tc::mbar_wait(&empty[stage], ((i / C::STAGES) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], (it % kbt) * kBK, (it / kbt) * kBM, pol_w);
+        }
+        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], (it % kbt) * kBK, 0, pol_x);
+      }
+    } else {
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    pdl_trigger();
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
+      int i = 0, seg = 0;
+      for (int it = it0; it < it1; ++seg) {
+        const int tile = it / kbt;
+        const int seg_end = min(it1, (tile + 1) * kbt);
+        const int buf = seg & 1;
+        tc::mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t dt = tmem + buf * C::ACC_COLS;
+        for (int j = it; j < seg_end; ++j, ++i) {
+          const int stage = i % C::STAGES;
+          tc::mbar_wait(&full[stage], (i / C::STAGES) & 1);
+          tc::fence_after_sync();
+          const uint64_t ad = tc::smem_desc_sw128(sW + stage * C::W_BYTES);
+          const uint64_t bd = tc::smem_desc_sw128(sX + stage * C::X_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            tc::mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (j > it || k > 0) ? 1u : 0u);
+          tc::mma_commit(&empty[stage]);
+        }
+        tc::mma_commit(&tfull[buf]);
+        it = seg_end;
+      }
+    }
+  } else {
+    // ------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4 -------------
+    pdl_wait();
+    pdl_trigger();
+    const int q = warp & 3;
+    const int f = q * 32 + lane;  // feature within the tile
+    const int m_hi = min(BN, p.M);
+    int seg = 0;
+    for (int it = it0; it < it1; ++seg) {
+      const int tile = it / kbt;
+      const int seg_end = min(it1, (tile + 1) * kbt);
+      const bool whole = (it == tile * kbt) && (seg_end == (tile + 1) * kbt);
+      const int buf = seg & 1;
+      const int feat = tile * kBM + f;
+      const bool feat_ok = feat < p.N;
+      tc::mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t trow = tmem + buf * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      const int slot = (it == it0) ? 0 : 1;
+      float* my_ws = sk.ws + ((int64_t)(c * 2 + slot) * BN) * kBM;
+      for (int c0 = 0; c0 < m_hi; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(trow + c0, r);
+        tc::tmem_wait_ld();
+        if (whole) {
+          if (feat_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < m_hi) epi_store(p, c0 + j, feat, __uint_as_float(r[j]));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < m_hi) __stcg(my_ws + (c0 + j) * kBM + f, __uint_as_float(r[j]));
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[buf]);  // TMEM buffer may be refilled
+      if (!whole) {
+        __threadfence();
+        epi_bar128();
+        if (warp == 2 && lane == 0) {
+          const int c_first = sk_owner(tile * kbt, sk.iters, sk.grid);
+          const int c_last = sk_owner((tile + 1) * kbt - 1, sk.iters, sk.grid);
+          const int nseg = c_last - c_first + 1;
+          const int old = atomicAdd(sk.counters + tile, 1);
+          s_last = (old == nseg - 1) ? (c_first | (c_last << 16)) : -1;
+          if (old == nseg - 1) sk.counters[tile] = 0;
+        }
+        epi_bar128();
+        const int lastv = s_last;
+        if (lastv >= 0) {
+          __threadfence();
+          const int c_first = lastv & 0xffff, c_last = lastv >> 16;
+          for (int j = 0; j < m_hi; ++j) {
+            float acc = 0.f;
+            for (int cc = c_first; cc <= c_last; ++cc) {
+              // cc's segment of this tile is its first (slot 0) iff the tile starts cc's range
+              const int sl = (sk_begin(cc, sk.iters, sk.grid) / kbt == tile) ? 0 : 1;
+              const float v = __ldcg(sk.ws + ((int64_t)(cc * 2 + sl) * BN + j) * kBM + f);
+              acc = (cc == c_first) ? v : acc + v;
+            }
+            if (feat_ok) epi_store(p, j, feat, acc);
+          }
+        }
+        epi_bar128();  // s_last is reused by the next segment
+      }
+      it = seg_end;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -316,13 +534,45 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const Lin
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
+// Persistent grid for the stream-K path: a function of (N, K) only.
+int linear_sk_grid(int N, int K) {
+  const int iters = ((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK);
+  int g = iters / 4;  // >= 4 k-blocks per CTA
+  g = g > 148 ? 148 : g;
+  return g < 1 ? 1 : g;
+}
+
+template <int BN>
+static int launch_linear_sk(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p,
+                            const SKParams& sk, cudaStream_t st) {
+  using C = SKCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(linear_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM) != cudaSuccess)
+      return MS_ERR_CUDA;
+    attr_set = true;
+  }
+  return launch(linear_sk_kernel<BN>, dim3(sk.grid), dim3(kThreads), C::SMEM, st, 1, tw, tx, p, sk);
+}
+
 }  // namespace ms
 
 extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }
 
+extern "C" int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* n_counters) {
+  if (M < 0 || N < 1 || K < 1) return MS_ERR_VALUE;
+  const int bn = ms::pick_bn(M);
+  const int g = ms::linear_sk_grid(N, K);
+  if (ws_bytes) *ws_bytes = (int64_t)g * 2 * bn * ms::kBM * 4;
+  if (n_counters) *n_counters = (N + ms::kBM - 1) / ms::kBM;
+  return MS_OK;
+}
+
 extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
                          const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-                         int M, int N, int K, int act, int splits, void* stream) {
+                         int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
+                         int* counters, int n_counters, void* stream) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < N) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
@@ -331,12 +581,9 @@ extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* 
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
   const int kb_total = (K + kBK - 1) / kBK;
-  if (splits <= 0) splits = linear_auto_splits(N, K);
-  if (splits > kb_total) splits = kb_total;
   const int bn = pick_bn(M);
   const int m_tiles = (M + bn - 1) / bn;
   const int n_tiles = (N + kBM - 1) / kBM;
-  if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
   if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
   CUtensorMap tw, tx;
   if (!make_tmap(&tw, w, N, K, K, kBM)) return MS_ERR_CUDA;
@@ -349,6 +596,33 @@ extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* 
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
   cudaStream_t st = (cudaStream_t)stream;
+  // decode / verify regime: persistent stream-K kernel when scratch is given
+  const int g = linear_sk_grid(N, K);
+  if (splits == 0 && m_tiles == 1 && ws && counters &&
+      ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
+    SKParams sk;
+    sk.iters = n_tiles * kb_total;
+    sk.grid = g;
+    sk.ws = (float*)ws;
+    sk.counters = counters;
+    p.splits = 1;
+    switch (bn) {
+      case 16: return launch_linear_sk<16>(tw, tx, p, sk, st);
+      case 32: return launch_linear_sk<32>(tw, tx, p, sk, st);
+      case 48: return launch_linear_sk<48>(tw, tx, p, sk, st);
+      case 64: return launch_linear_sk<64>(tw, tx, p, sk, st);
+      case 80: return launch_linear_sk<80>(tw, tx, p, sk, st);
+      case 96: return launch_linear_sk<96>(tw, tx, p, sk, st);
+      case 128: return launch_linear_sk<128>(tw, tx, p, sk, st);
+      case 160: return launch_linear_sk<160>(tw, tx, p, sk, st);
+      case 192: return launch_linear_sk<192>(tw, tx, p, sk, st);
+      default: return launch_linear_sk<256>(tw, tx, p, sk, st);
+    }
+  }
+  if (splits <= 0) splits = linear_auto_splits(N, K);
+  if (splits > kb_total) splits = kb_total;
+  if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
+  p.splits = splits;
   switch (bn) {
     case 16: return launch_linear<16>(tw, tx, p, m_tiles, st);
     case 32: return launch_linear<32>(tw, tx, p, m_tiles, st);

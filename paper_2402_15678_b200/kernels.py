@@ -6,6 +6,8 @@ when `out=` buffers are passed, so launches can be captured in CUDA graphs.
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _dev
@@ -14,14 +16,39 @@ from . import _native
 BF16 = torch.bfloat16
 
 
+class Workspace:
+    """Scratch of the stream-K linear path (partial tiles + per-tile counters).
+    One per stream of concurrently running GEMMs; allocated once (so launches
+    are CUDA-graph capturable) and grown on demand outside capture."""
+
+    def __init__(self, device, ws_bytes: int = 40 << 20, n_counters: int = 1024):
+        self.device = device
+        self.ws = torch.empty(ws_bytes // 4, dtype=torch.float32, device=device)
+        self.counters = torch.zeros(n_counters, dtype=torch.int32, device=device)
+
+    def fit(self, M: int, N: int, K: int) -> bool:
+        b = ctypes.c_int64()
+        c = ctypes.c_int()
+        _native.check(_native.lib.ms_linear_workspace(M, N, K, ctypes.byref(b), ctypes.byref(c)),
+                      "ms_linear_workspace")
+        if b.value > self.ws.numel() * 4:
+            self.ws = torch.empty((b.value + 3) // 4, dtype=torch.float32, device=self.device)
+        if c.value > self.counters.numel():
+            self.counters = torch.zeros(c.value, dtype=torch.int32, device=self.device)
+        return True
+
+
 def linear_splits(N: int, K: int) -> int:
     return int(_native.lib.ms_linear_splits(N, K))
 
 
 def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
            residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
-           out_f32: bool = False, splits: int = 0, stream=None) -> torch.Tensor:
-    """out = act(x @ w.T + bias) + residual on tcgen05 (ms_linear)."""
+           out_f32: bool = False, splits: int = 0, ws: Workspace | None = None,
+           stream=None) -> torch.Tensor:
+    """out = act(x @ w.T + bias) + residual on tcgen05 (ms_linear).  With a
+    Workspace and splits=0 the persistent stream-K schedule is used for
+    M <= 256; otherwise the cluster split-K schedule."""
     if x.dim() != 2 or w.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
         raise ValueError("x [M, K] and w [N, K] must be 2-D bf16")
     M, K = x.shape
@@ -39,7 +66,9 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
                  None if residual is None else residual.data_ptr(),
                  0 if residual is None else residual.stride(0),
                  out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act,
-                 splits, _dev.stream_ptr(stream))
+                 splits, None if ws is None else ws.ws.data_ptr(), 0 if ws is None else ws.ws.numel() * 4,
+                 None if ws is None else ws.counters.data_ptr(), 0 if ws is None else ws.counters.numel(),
+                 _dev.stream_ptr(stream))
     return out
 
 

@@ -136,11 +136,10 @@ class OPTModel:
         self.attn = torch.empty((max_rows, c.d), dtype=BF16, device=device)
         self.ff = torch.empty((max_rows, c.ffn), dtype=BF16, device=device)
         self.scale = 1.0 / math.sqrt(c.head_dim)
-        # fixed split-K factor per weight shape (batch invariance: never depends on M)
-        self.splits = {
-            "qkv": K.linear_splits(3 * c.d, c.d), "o": K.linear_splits(c.d, c.d),
-            "fc1": K.linear_splits(c.ffn, c.d), "fc2": K.linear_splits(c.d, c.ffn),
-            "head": K.linear_splits(c.vocab, c.d)}
+        # stream-K scratch for this model's GEMMs (one model = one stream)
+        self.ws = K.Workspace(self.device)
+        for n, k in ((3 * c.d, c.d), (c.d, c.d), (c.ffn, c.d), (c.d, c.ffn), (c.vocab, c.d)):
+            self.ws.fit(min(max_rows, 256), n, k)
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
                 logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -157,21 +156,21 @@ class OPTModel:
         if R > self.max_rows:
             raise ValueError(f"{R} rows exceed max_rows={self.max_rows}")
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
-        sp = self.splits
+        ws = self.ws
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
         for i in range(c.n_layers):
             p = f"l{i}."
             K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
-            K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, splits=sp["qkv"], stream=stream)
+            K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, ws=ws, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
                         self.scale, out=at, stream=stream)
-            K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, splits=sp["o"], stream=stream)
+            K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, ws=ws, stream=stream)
             K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
-            K.linear(h, w[p + "w_fc1"], w[p + "b_fc1"], act=1, out=ff, splits=sp["fc1"], stream=stream)
-            K.linear(ff, w[p + "w_fc2"], w[p + "b_fc2"], residual=x, out=x, splits=sp["fc2"],
+            K.linear(h, w[p + "w_fc1"], w[p + "b_fc1"], act=1, out=ff, ws=ws, stream=stream)
+            K.linear(ff, w[p + "w_fc2"], w[p + "b_fc2"], residual=x, out=x, ws=ws,
                      stream=stream)
         Rh = R if head_rows is None else head_rows.numel()
         hf = self.h[:Rh]
         K.layernorm(x, w["lnf_g"], w["lnf_b"], c.eps, out=hf, rows=head_rows, stream=stream)
-        K.linear(hf, w["tok_emb"], out=logits, out_f32=True, splits=sp["head"], stream=stream)
+        K.linear(hf, w["tok_emb"], out=logits, out_f32=True, ws=ws, stream=stream)
         return logits

@@ -22,10 +22,16 @@ def _ref_linear(x, w, bias=None, residual=None, act=0, out_f32=False):
 
 
 @pytest.mark.parametrize("M,N,K", [(16, 768, 768), (80, 15360, 5120), (1, 50272, 256),
-                                   (300, 1000, 200), (208, 3072, 768), (5, 128, 64)])
-@pytest.mark.parametrize("splits", [0, 1, 3])
+                                   (300, 1000, 200), (208, 3072, 768), (5, 128, 64),
+                                   (256, 5120, 20480), (33, 2304, 768)])
+@pytest.mark.parametrize("splits", ["sk", 0, 1, 3])
 def test_linear_vs_torch(M, N, K, splits):
     from paper_2402_15678_b200 import kernels as Kn
+    ws = None
+    if splits == "sk":  # persistent stream-K schedule (M <= 256)
+        ws = Kn.Workspace("cuda")
+        ws.fit(M, N, K)
+        splits = 0
     g = torch.Generator().manual_seed(M * 7 + N + K)
     x = torch.randn(M, K, generator=g).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16)
@@ -33,7 +39,7 @@ def test_linear_vs_torch(M, N, K, splits):
     r = torch.randn(M, N, generator=g).to(torch.bfloat16)
     for act, res, f32 in ((0, None, True), (1, r, False), (0, r, False)):
         got = Kn.linear(x.cuda(), w.cuda(), b.cuda(), None if res is None else res.cuda(), act=act,
-                        out_f32=f32, splits=splits).cpu()
+                        out_f32=f32, splits=splits, ws=ws).cpu()
         want = _ref_linear(x, w, b, res, act, f32)
         if f32:
             torch.testing.assert_close(got, want, rtol=1e-4, atol=1e-4)
@@ -41,20 +47,26 @@ def test_linear_vs_torch(M, N, K, splits):
             torch.testing.assert_close(got.float(), want.float(), rtol=1.6e-2, atol=1e-2)
 
 
-def test_linear_rows_independent_of_batch():
-    """A row's result is bitwise the same whatever M (fixed split count)."""
+@pytest.mark.parametrize("N,K", [(5120, 5120), (50272, 768), (2304, 768)])
+def test_linear_rows_independent_of_batch(N, K):
+    """A row's result is bitwise the same whatever M, on both schedules
+    (fixed split count; stream-K partition fixed by N, K)."""
     from paper_2402_15678_b200 import kernels as Kn
     g = torch.Generator().manual_seed(1)
-    N, K = 5120, 5120
     w = (torch.randn(N, K, generator=g) * 0.02).to(torch.bfloat16).cuda()
     x = torch.randn(300, K, generator=g).to(torch.bfloat16).cuda()
     sp = Kn.linear_splits(N, K)
     full = Kn.linear(x, w, out_f32=True, splits=sp)
+    ws = Kn.Workspace("cuda")
+    ws.fit(256, N, K)
+    sk = Kn.linear(x[:256].contiguous(), w, out_f32=True, ws=ws)
     for M in (1, 16, 17, 80, 129, 208):
         part = Kn.linear(x[:M].contiguous(), w, out_f32=True, splits=sp)
         assert torch.equal(part, full[:M]), M
-    again = Kn.linear(x, w, out_f32=True, splits=sp)
-    assert torch.equal(again, full)  # deterministic
+        part_sk = Kn.linear(x[:M].contiguous(), w, out_f32=True, ws=ws)
+        assert torch.equal(part_sk, sk[:M]), M
+    assert torch.equal(Kn.linear(x, w, out_f32=True, splits=sp), full)  # deterministic
+    assert torch.equal(Kn.linear(x[:256].contiguous(), w, out_f32=True, ws=ws), sk)
 
 
 def _tiny(seed=0, cfg_name="tiny-target"):

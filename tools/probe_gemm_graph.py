@@ -7,7 +7,7 @@ import torch
 from paper_2402_15678_b200 import kernels as K
 
 M_list = [int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["16", "80"])]
-split_opts = [int(a) for a in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"])]
+split_opts = [a for a in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["sk"])]
 shapes = [("13b qkv", 15360, 5120), ("13b o", 5120, 5120), ("13b fc1", 20480, 5120),
           ("13b fc2", 5120, 20480), ("13b head", 50272, 5120), ("125m qkv", 2304, 768),
           ("125m o", 768, 768), ("125m fc1", 3072, 768), ("125m fc2", 768, 3072), ("125m head", 50272, 768)]
@@ -19,10 +19,16 @@ for M in M_list:
         f32 = "head" in name
         out = torch.empty(M, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
         for sp in split_opts:
-            spv = sp or K.linear_splits(N, Kd)
+            wsp = None
+            if sp == "sk":
+                wsp = K.Workspace("cuda")
+                wsp.fit(M, N, Kd)
+                spv = 0
+            else:
+                spv = int(sp) or K.linear_splits(N, Kd)
             def run():
                 for w in ws:
-                    K.linear(x, w, out=out, out_f32=f32, splits=spv)
+                    K.linear(x, w, out=out, out_f32=f32, splits=spv, ws=wsp)
             run(); torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -35,6 +41,6 @@ for M in M_list:
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) * 1e-3 / (3 * L)
             byts = N * Kd * 2 + M * Kd * 2 + M * N * (4 if f32 else 2)
-            print(f"M={M:4d} {name:10s} N={N:6d} K={Kd:6d} splits={spv} L={L:3d} {t*1e6:8.2f} us/launch {byts/t/1e9:7.0f} GB/s", flush=True)
+            print(f"M={M:4d} {name:10s} N={N:6d} K={Kd:6d} splits={sp if sp == "sk" else spv} L={L:3d} {t*1e6:8.2f} us/launch {byts/t/1e9:7.0f} GB/s", flush=True)
         del ws
         torch.cuda.empty_cache()
