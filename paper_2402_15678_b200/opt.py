@@ -19,6 +19,7 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -136,10 +137,14 @@ class OPTModel:
         self.attn = torch.empty((max_rows, c.d), dtype=BF16, device=device)
         self.ff = torch.empty((max_rows, c.ffn), dtype=BF16, device=device)
         self.scale = 1.0 / math.sqrt(c.head_dim)
-        # stream-K scratch for this model's GEMMs (one model = one stream)
-        self.ws = K.Workspace(self.device)
-        for n, k in ((3 * c.d, c.d), (c.d, c.d), (c.ffn, c.d), (c.d, c.ffn), (c.vocab, c.d)):
-            self.ws.fit(min(max_rows, 256), n, k)
+        # GEMM schedule: cluster split-K (measured faster than the persistent
+        # stream-K path, whose tile fix-up is a serial tail — tools/probe_gemm_graph.py);
+        # MS_STREAM_K=1 selects stream-K (scratch is per model = per stream)
+        self.ws = None
+        if os.environ.get("MS_STREAM_K", "0") == "1":
+            self.ws = K.Workspace(self.device)
+            for n, k in ((3 * c.d, c.d), (c.d, c.d), (c.ffn, c.d), (c.d, c.ffn), (c.vocab, c.d)):
+                self.ws.fit(min(max_rows, 256), n, k)
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
                 logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:

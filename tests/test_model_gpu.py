@@ -41,8 +41,8 @@ def test_linear_vs_torch(M, N, K, splits):
         got = Kn.linear(x.cuda(), w.cuda(), b.cuda(), None if res is None else res.cuda(), act=act,
                         out_f32=f32, splits=splits, ws=ws).cpu()
         want = _ref_linear(x, w, b, res, act, f32)
-        if f32:
-            torch.testing.assert_close(got, want, rtol=1e-4, atol=1e-4)
+        if f32:  # fp32 sums of K products in a different order
+            torch.testing.assert_close(got, want, rtol=1e-4, atol=2e-5 * (K ** 0.5))
         else:  # one bf16 rounding of a value whose fp32 sum order differs
             torch.testing.assert_close(got.float(), want.float(), rtol=1.6e-2, atol=1e-2)
 
