@@ -40,6 +40,7 @@ struct LinearParams {
   int splits;
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
+  int stages;                     // TMA pipeline depth of this launch (cluster path)
 };
 
 constexpr int kBM = 128;  // output features per CTA (MMA M)
@@ -51,14 +52,22 @@ struct LinearCfg {
   static constexpr int W_BYTES = kBM * kBK * 2;
   static constexpr int X_BYTES = BN * kBK * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  // ~110 KB of pipeline per CTA => two CTAs per SM for the small-M shapes
-  static constexpr int STAGES_RAW = (112 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW < 2 ? 2 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+  static constexpr int MAX_STAGES = 12;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;
   static constexpr int PART_BYTES = BN * kBM * 4;  // fp32 partial tile for the split-K reduction
-  static constexpr int DATA_BYTES = PIPE_BYTES > PART_BYTES ? PIPE_BYTES : PART_BYTES;
-  static constexpr int SMEM = 1024 /*align slack*/ + DATA_BYTES + (2 * STAGES + 1) * 8 + 16;
+  // Pipeline depth is chosen per launch: bytes in flight per SM bound a weight
+  // stream (Little's law: ~6.5 TB/s x ~2 us), so one CTA per SM gets a deep
+  // pipeline (~210 KB), two CTAs per SM ~105 KB each.
+  __host__ __device__ static int stages_for(int ctas_per_sm) {
+    const int budget = ctas_per_sm <= 1 ? 210 * 1024 : 104 * 1024;
+    int st = budget / STAGE_BYTES;
+    return st < 2 ? 2 : (st > MAX_STAGES ? MAX_STAGES : st);
+  }
+  __host__ __device__ static int data_bytes(int stages) {
+    const int pipe = stages * STAGE_BYTES;
+    return pipe > PART_BYTES ? pipe : PART_BYTES;
+  }
+  __host__ __device__ static int smem(int stages) { return 1024 + data_bytes(stages) + (2 * MAX_STAGES + 1) * 8 + 16; }
 };
 
 __device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v) {
@@ -93,10 +102,11 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  uint8_t* sX = smem + C::STAGES * C::W_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;
+  const int STAGES = p.stages;
+  uint8_t* sX = smem + STAGES * C::W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::data_bytes(STAGES));
+  uint64_t* empty = full + C::MAX_STAGES;
+  uint64_t* tmem_full = empty + C::MAX_STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -111,7 +121,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmW);
     tc::prefetch_tmap(&tmX);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
@@ -131,7 +141,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       // The first STAGES weight tiles do not depend on the previous kernel:
       // issue them before the programmatic-dependency wait (PDL prefetch).
       const int nkb = kb1 - kb0;
-      const int pre = nkb < C::STAGES ? nkb : C::STAGES;
+      const int pre = nkb < STAGES ? nkb : STAGES;
       for (int i = 0; i < pre; ++i) {
         tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
         tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (kb0 + i) * kBK, n0, pol_w);
@@ -139,10 +149,10 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       pdl_wait();
       pdl_trigger();
       for (int i = 0; i < nkb; ++i) {
-        const int stage = i % C::STAGES;
+        const int stage = i % STAGES;
         const int kb = kb0 + i;
         if (i >= pre) {
-          tc::mbar_wait(&empty[stage], ((i / C::STAGES) & 1) ^ 1);
+          tc::mbar_wait(&empty[stage], ((i / STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, n0, pol_w);
         }
@@ -166,7 +176,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K per UMMA_K=16 step
           tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
         tc::mma_commit(&empty[stage]);
-        if (++stage == C::STAGES) {
+        if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -493,14 +503,14 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t co
 }
 
 // Split count for the weight-streaming regime, a function of (N, K) only:
-// the smallest split that puts ~one CTA on each of the 148 SMs (measured best
-// on the OPT-13B / OPT-125M shapes: more splits add cluster-reduction and
-// prologue overhead, fewer leave SMs idle), capped at the portable cluster
-// size 8 and at >= 2 k-blocks (128 K-elements) per split.
+// the largest split that keeps one CTA per SM (<= 148 CTAs, each then gets a
+// deep ~210 KB TMA pipeline), capped at the portable cluster size 8 and at
+// >= 2 k-blocks per split; weights with more than 148 tiles run unsplit at
+// two CTAs per SM.
 int linear_auto_splits(int N, int K) {
   const int n_tiles = (N + kBM - 1) / kBM;
   const int kb = (K + kBK - 1) / kBK;
-  int sp = (148 + n_tiles - 1) / n_tiles;
+  int sp = 148 / n_tiles;
   sp = sp > 8 ? 8 : sp;
   while (sp > 1 && kb / sp < 2) --sp;
   return sp < 1 ? 1 : sp;
@@ -520,17 +530,19 @@ static int pick_bn(int M) {
 }
 
 template <int BN>
-static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p,
+static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p,
                          int m_tiles, cudaStream_t st) {
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM) != cudaSuccess)
+                             C::smem(C::stages_for(1))) != cudaSuccess)
       return MS_ERR_CUDA;
     attr_set = true;
   }
-  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::SMEM, st,
+  const int grid = p.n_tiles * p.splits * m_tiles;
+  p.stages = C::stages_for(grid <= 148 ? 1 : 2);
+  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::smem(p.stages), st,
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
