@@ -502,15 +502,15 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
-// Split count for the weight-streaming regime, a function of (N, K) only:
-// the largest split that keeps one CTA per SM (<= 148 CTAs, each then gets a
-// deep ~210 KB TMA pipeline), capped at the portable cluster size 8 and at
-// >= 2 k-blocks per split; weights with more than 148 tiles run unsplit at
-// two CTAs per SM.
+// Split count for the weight-streaming regime, a function of (N, K) only.
+// From the measured sweep (tools/probe_gemm_graph.py, OPT-13B / OPT-125M
+// shapes at M = 16 and 80): about 260 CTAs (~1.75 per SM) is best — fewer
+// leave SMs idle, more add cluster-reduction and prologue cost — capped at
+// the portable cluster size 8 and at >= 2 k-blocks per split.
 int linear_auto_splits(int N, int K) {
   const int n_tiles = (N + kBM - 1) / kBM;
   const int kb = (K + kBK - 1) / kBK;
-  int sp = 148 / n_tiles;
+  int sp = 260 / n_tiles;
   sp = sp > 8 ? 8 : sp;
   while (sp > 1 && kb / sp < 2) --sp;
   return sp < 1 ? 1 : sp;

@@ -63,6 +63,7 @@ class RoundStats:
     qc: int
     t_verify_ms: float
     t_round_ms: float
+    t_draft_ms: float
     accepted: list
     emitted: list
     voted: list
@@ -180,6 +181,7 @@ class SpecEngine:
         self.streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
         self.ev_v0 = torch.cuda.Event(enable_timing=True)
         self.ev_v1 = torch.cuda.Event(enable_timing=True)
+        self.ev_d0 = torch.cuda.Event(enable_timing=True)
         self.pinned_out = None
 
     # ------------------------------------------------------------------ setup
@@ -318,6 +320,7 @@ class SpecEngine:
         self.kernel_launches += self.graph_kernels[key]
 
     def _run_device_round(self, s: int, qc: int) -> None:
+        self.ev_d0.record()
         self._replay(("draft", s, qc), lambda: self._device_draft(s, qc))
         self.ev_v0.record()
         self._replay(("verify", s), lambda: self._device_verify(s))
@@ -413,6 +416,7 @@ class SpecEngine:
         voted = get("voted")
         drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = self.ev_v0.elapsed_time(self.ev_v1)
+        t_draft = self.ev_d0.elapsed_time(self.ev_v0)
         accs, ems, vts = [], [], []
         for b in active:
             r = self.requests[b]
@@ -455,7 +459,7 @@ class SpecEngine:
                          n_acc=n_acc.copy(), n_emit=n_emit.copy(), emitted=emitted.copy(),
                          tgt=get("tgt", B * (s + 1)).reshape(B, s + 1).copy(),
                          remaining=self.remaining.cpu().numpy())
-        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, trace=trace,
+        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, t_draft_ms=t_draft, trace=trace,
                           t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
                           emitted=ems, voted=vts, vl=vl, decision=decision.value,
                           s_next=self.selector.current_s, weights=dict(self.weights.weights))

@@ -20,4 +20,5 @@ reqs = [Request(f"req-{i:03d}", torch.randint(0, tcfg.vocab, (128,), generator=g
 eng.prefill(reqs)
 res = eng.decode(max_rounds=rounds)
 torch.cuda.synchronize()
-print("rounds", len(res.rounds), [round(r.t_verify_ms, 3) for r in res.rounds], [round(r.t_round_ms, 3) for r in res.rounds])
+print("rounds", len(res.rounds), "verify", [round(r.t_verify_ms, 3) for r in res.rounds])
+print("draft", [round(r.t_draft_ms, 3) for r in res.rounds], "round", [round(r.t_round_ms, 3) for r in res.rounds])
