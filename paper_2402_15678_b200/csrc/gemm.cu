@@ -541,7 +541,11 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
     attr_set = true;
   }
   const int grid = p.n_tiles * p.splits * m_tiles;
+  // never deeper than the k-blocks a CTA streams: small (SSM) GEMMs then use
+  // little shared memory and several kernels / streams can share an SM
+  const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
   p.stages = C::stages_for(grid <= 148 ? 1 : 2);
+  if (p.stages > kb_per_cta) p.stages = kb_per_cta < 2 ? 2 : kb_per_cta;
   return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::smem(p.stages), st,
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
