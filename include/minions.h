@@ -180,6 +180,25 @@ int ms_draft_commit(const int32_t* tok, const int32_t* ctx_len, int B, int j, in
 int ms_pack_verify(const int32_t* last, const int32_t* path, int B, int S,
                    int32_t* vin, void* stream);
 
+/* ---- K10: stochastic accept (speculative sampling) ------------------------
+ * verify() of aggspec/verification.py:29-77 on general distributions, bit-exact
+ * given the same fp64 probabilities and uniforms:
+ *   draft [B, S] int32, q [B, S, V] fp64 (voted drafter's dists),
+ *   o [B, S+1, V] fp64 (target dists), uniforms [B, S+1] fp64 — the next S+1
+ *   doubles of each request's verify stream (the kernel uses n_draws of them),
+ *   scratch [B, V] fp64.  Outputs as ms_accept_greedy plus n_draws [B] (the
+ *   number of uniforms the reference consumed: i+2 on a rejection at i, S+1 on
+ *   full acceptance), so the host advances its generator identically.
+ * The residual normaliser is NumPy's pairwise sum (exact emulation) and the
+ * inverse-CDF scan is sequential fp64 (np.cumsum + searchsorted 'right').
+ * Limits: V <= 65536.
+ */
+int ms_accept_stochastic(const int32_t* draft, const double* q, const double* o,
+                         const double* uniforms, const int32_t* remaining, int stop_token,
+                         int B, int S, int V, double* scratch, int32_t* n_acc,
+                         int32_t* emitted, int32_t* n_emit, int32_t* finished,
+                         int32_t* n_draws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

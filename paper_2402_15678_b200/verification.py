@@ -3,9 +3,11 @@
 `verify(draft_tokens, draft_dists, target_dists, rng)` keeps the reference's
 signature, result type, errors and RNG consumption.  Greedy verification —
 every draft and target distribution a point mass, which is what a greedy
-drafter/target produces — runs `ms_accept_greedy` (csrc/accept.cu); the
-result equals the reference's on those inputs, including the number of
-uniforms drawn from `rng` (one per considered position plus one for the
+drafter/target produces — runs `ms_accept_greedy` (csrc/accept.cu); general
+distributions run `ms_accept_stochastic` (csrc/accept_stochastic.cu) on the
+uniforms peeked from `rng`.  Either way the result equals the reference's on
+the same inputs, and `rng` ends up advanced by exactly the number of uniforms
+the reference draws (one per considered position plus one for the
 correction/bonus, aggspec/verification.py:55-76).
 
 The batched engine path calls `accept_batch` / `accept_batch_logits` on device
@@ -26,7 +28,8 @@ from . import _native
 from .core import DistMismatch, ProbDist
 
 __all__ = ["DistMismatch", "VerificationResult", "verify", "acceptance_rate", "accept_batch",
-           "accept_batch_logits", "argmax_rows", "AcceptOut"]
+           "accept_batch_logits", "accept_batch_stochastic", "argmax_rows", "AcceptOut",
+           "peek_uniforms"]
 
 
 @dataclass(frozen=True)
@@ -112,6 +115,42 @@ def accept_batch_logits(draft: torch.Tensor, logits: torch.Tensor, remaining: to
     return out
 
 
+def accept_batch_stochastic(draft: torch.Tensor, q: torch.Tensor, o: torch.Tensor,
+                            uniforms: torch.Tensor, remaining: torch.Tensor,
+                            stop_token: int | None = None, out: AcceptOut | None = None,
+                            scratch: torch.Tensor | None = None, stream=None):
+    """K10 on device tensors: draft [B, S] int32, q [B, S, V] fp64, o [B, S+1, V]
+    fp64, uniforms [B, S+1] fp64 (peeked from each request's verify stream).
+    Returns (AcceptOut, n_draws [B] int32)."""
+    dev = _dev.require_cuda()
+    B, S = draft.shape
+    V = q.shape[-1]
+    if q.shape != (B, S, V) or o.shape != (B, S + 1, V):
+        raise DistMismatch(f"expected q [{B}, {S}, V] and o [{B}, {S + 1}, V]")
+    if uniforms.shape != (B, S + 1):
+        raise ValueError(f"expected uniforms [{B}, {S + 1}]")
+    out = out or AcceptOut.alloc(B, S, dev)
+    n_draws = torch.empty(B, dtype=torch.int32, device=dev)
+    scratch = scratch if scratch is not None else torch.empty((B, V), dtype=torch.float64, device=dev)
+    _native.call("ms_accept_stochastic", _dev.ptr(draft, torch.int32, "draft"),
+                 _dev.ptr(q, torch.float64, "q"), _dev.ptr(o, torch.float64, "o"),
+                 _dev.ptr(uniforms, torch.float64, "uniforms"),
+                 _dev.ptr(remaining, torch.int32, "remaining"),
+                 -1 if stop_token is None else int(stop_token), B, S, V,
+                 _dev.ptr(scratch, torch.float64), _dev.ptr(out.n_acc), _dev.ptr(out.emitted),
+                 _dev.ptr(out.n_emit), _dev.ptr(out.finished), _dev.ptr(n_draws),
+                 _dev.stream_ptr(stream))
+    return out, n_draws
+
+
+def peek_uniforms(rng: np.random.Generator, n: int) -> np.ndarray:
+    """The next n doubles of rng without consuming them (PCG64 state peek)."""
+    state = rng.bit_generator.state
+    u = rng.random(n)
+    rng.bit_generator.state = state
+    return u
+
+
 def verify(draft_tokens: Sequence[int], draft_dists: Sequence[ProbDist],
            target_dists: Sequence[ProbDist], rng: np.random.Generator) -> VerificationResult:
     """aggspec/verification.py:29-77 with the same checks and RNG consumption."""
@@ -127,18 +166,26 @@ def verify(draft_tokens: Sequence[int], draft_dists: Sequence[ProbDist],
         raise DistMismatch("draft and target distributions must share a vocabulary")
     q_tok = [d.point_mass_token() for d in draft_dists]
     o_tok = [d.point_mass_token() for d in target_dists]
-    if any(t is None for t in (*q_tok, *o_tok)) or any(
-            q != int(t) for q, t in zip(q_tok, draft_tokens)):
-        raise NotImplementedError(
-            "stochastic (non point-mass) verification is not implemented on the device path yet")
     dev = _dev.require_cuda()
     draft = torch.tensor([list(map(int, draft_tokens))], dtype=torch.int32, device=dev)
-    tgt = torch.tensor([o_tok], dtype=torch.int32, device=dev)
     rem = torch.tensor([s + 1], dtype=torch.int32, device=dev)
-    o = accept_batch(draft, tgt, rem)
+    if all(t is not None for t in (*q_tok, *o_tok)) and all(
+            qt == int(t) for qt, t in zip(q_tok, draft_tokens)):
+        # greedy fast path (K9): point masses on both sides
+        tgt = torch.tensor([o_tok], dtype=torch.int32, device=dev)
+        o = accept_batch(draft, tgt, rem)
+        acc = int(o.n_acc[0])
+        emitted = o.emitted[0, : acc + 1].tolist()
+        rng.random(acc + 2 if acc < s else s + 1)  # uniforms the reference consumes
+        return VerificationResult(acc, emitted, acc / s)
+    # general speculative sampling (K10), bit-exact on the same fp64 dists / uniforms
+    qd = torch.from_numpy(np.stack([d.probs for d in draft_dists])[None]).to(dev)
+    od = torch.from_numpy(np.stack([d.probs for d in target_dists])[None]).to(dev)
+    u = torch.from_numpy(peek_uniforms(rng, s + 1)[None]).to(dev)
+    o, n_draws = accept_batch_stochastic(draft, qd, od, u, rem)
     acc = int(o.n_acc[0])
     emitted = o.emitted[0, : acc + 1].tolist()
-    rng.random(acc + 2 if acc < s else s + 1)  # uniforms the reference consumes
+    rng.random(int(n_draws[0]))  # advance the stream exactly as the reference did
     return VerificationResult(acc, emitted, acc / s)
 
 

@@ -105,3 +105,82 @@ def test_accept_from_logits_matches_two_step():
     assert np.array_equal(o.tgt_argmax.cpu().numpy(), tgt.numpy())
     assert np.array_equal(o.n_acc.cpu().numpy(), n_acc)
     assert np.array_equal(o.emitted.cpu().numpy(), em)
+
+
+# ---------------------------------------------------------------- K10 (stochastic)
+def _stoch_group(g, V):
+    S = g[f"V{V}_S"]
+    return {k: g[f"V{V}_{k}"] for k in ("q", "o", "draft", "uniforms", "S", "accepted", "emitted")}
+
+
+@pytest.mark.parametrize("V", [5, 37, 300])
+def test_stochastic_accept_matches_reference_golden(V):
+    from paper_2402_15678_b200.verification import accept_batch_stochastic
+    g = _stoch_group(_load("verify_stoch.npz"), V)
+    for s in np.unique(g["S"]):
+        idx = np.flatnonzero(g["S"] == s)
+        draft = torch.tensor(g["draft"][idx, :s], dtype=torch.int32, device="cuda")
+        q = torch.tensor(g["q"][idx, :s], dtype=torch.float64, device="cuda")
+        o = torch.tensor(g["o"][idx, : s + 1], dtype=torch.float64, device="cuda")
+        us = g["uniforms"][idx, : s + 1].copy()
+        us[us < 0] = 0.5  # draws the reference did not make are never read
+        u = torch.tensor(us, dtype=torch.float64, device="cuda")
+        rem = torch.full((idx.size,), 10_000, dtype=torch.int32, device="cuda")
+        out, nd = accept_batch_stochastic(draft, q, o, u, rem)
+        acc = out.n_acc.cpu().numpy()
+        assert np.array_equal(acc, g["accepted"][idx])
+        em = out.emitted.cpu().numpy()
+        nd = nd.cpu().numpy()
+        for j, i in enumerate(idx):
+            a = int(acc[j])
+            assert em[j, : a + 1].tolist() == g["emitted"][i, : a + 1].tolist()
+            assert nd[j] == int((g["uniforms"][i] >= 0).sum())
+
+
+def test_stochastic_big_vocab_through_verify_api():
+    """V = 50272 (OPT) cases regenerated from seeds, run through verify() with the
+    reference's RNG stream; accepted/emitted/stream position must match."""
+    import hashlib
+    import json
+    from paper_2402_15678_b200 import ProbDist, seeded_rng, verify
+    with open(os.path.join(GOLDEN, "verify_stoch_bigv.json")) as fh:
+        cases = json.load(fh)
+    for c in cases:
+        gen = np.random.default_rng(c["seed"])
+        V, s = c["V"], c["s"]
+        q = [ProbDist(gen.dirichlet(np.full(V, c["conc"]))) for _ in range(s)]
+        o = [ProbDist(gen.dirichlet(np.full(V, c["conc"]))) for _ in range(s + 1)]
+        h = hashlib.sha256()
+        for d in (*q, *o):
+            h.update(d.probs.tobytes())
+        assert h.hexdigest() == c["sha256"]
+        rng = seeded_rng(c["seed"] - 1000, "verify/bigv")
+        res = verify(c["draft"], q, o, rng)
+        assert res.accepted_count == c["accepted"] and res.emitted == c["emitted"]
+        ref = seeded_rng(c["seed"] - 1000, "verify/bigv")
+        ref.random(len(c["uniforms"]))
+        assert rng.random() == ref.random()
+
+
+def test_stochastic_pairwise_sum_is_numpy():
+    """Residual normaliser = numpy pairwise sum: a rejection with a residual whose
+    pairwise and sequential sums differ must still pick numpy's sample."""
+    from paper_2402_15678_b200.verification import accept_batch_stochastic
+    rng = np.random.default_rng(3)
+    V = 50272
+    hits = 0
+    for t in range(20):
+        q = rng.dirichlet(np.full(V, 0.3))
+        o = rng.dirichlet(np.full(V, 0.3))
+        tok = int(np.argmax(q - o))  # q > o there: likely rejection
+        u0 = 0.999999
+        u1 = float(rng.random())
+        acc, em, nd = O.verify_stochastic_one([tok], [q], [o, o], [u0, u1])
+        out, ndd = accept_batch_stochastic(
+            torch.tensor([[tok]], dtype=torch.int32, device="cuda"),
+            torch.tensor(q[None, None], device="cuda"), torch.tensor(np.stack([o, o])[None], device="cuda"),
+            torch.tensor([[u0, u1]], device="cuda"), torch.tensor([5], dtype=torch.int32, device="cuda"))
+        assert int(out.n_acc[0]) == acc
+        assert out.emitted[0, : acc + 1].tolist() == em
+        hits += int(acc == 0)
+    assert hits > 10
