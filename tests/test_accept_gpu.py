@@ -179,7 +179,8 @@ def test_stochastic_pairwise_sum_is_numpy():
         out, ndd = accept_batch_stochastic(
             torch.tensor([[tok]], dtype=torch.int32, device="cuda"),
             torch.tensor(q[None, None], device="cuda"), torch.tensor(np.stack([o, o])[None], device="cuda"),
-            torch.tensor([[u0, u1]], device="cuda"), torch.tensor([5], dtype=torch.int32, device="cuda"))
+            torch.tensor([[u0, u1]], dtype=torch.float64, device="cuda"),
+            torch.tensor([5], dtype=torch.int32, device="cuda"))
         assert int(out.n_acc[0]) == acc
         assert out.emitted[0, : acc + 1].tolist() == em
         hits += int(acc == 0)

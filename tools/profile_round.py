@@ -10,10 +10,11 @@ from paper_2402_15678_b200.opt import CONFIGS, OPTWeights
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 tgt = sys.argv[2] if len(sys.argv) > 2 else "opt-13b"
 ssm = sys.argv[3] if len(sys.argv) > 3 else "opt-125m"
+nssm = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 tcfg, scfg = CONFIGS[tgt], CONFIGS[ssm]
 t = OPTWeights.random(tcfg, 0)
-ds = [OPTWeights.random(scfg, k + 1) for k in range(3)]
-cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=16, b_ssm=16, initial_weights=(1.0,) * 3, s_init=4)
+ds = [OPTWeights.random(scfg, k + 1) for k in range(nssm)]
+cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=16, b_ssm=16, initial_weights=(1.0,) * nssm, s_init=4)
 eng = SpecEngine(t, ds, cfg, slots=16, max_len=300, adaptive=False)
 g = torch.Generator().manual_seed(0)
 reqs = [Request(f"req-{i:03d}", torch.randint(0, tcfg.vocab, (128,), generator=g).tolist(), 64) for i in range(16)]
