@@ -173,7 +173,7 @@ def test_stochastic_pairwise_sum_is_numpy():
         q = rng.dirichlet(np.full(V, 0.3))
         o = rng.dirichlet(np.full(V, 0.3))
         tok = int(np.argmax(q - o))  # q > o there: likely rejection
-        u0 = 0.999999
+        u0 = 0.0  # q > o: rejected for any u < 1 - o/q
         u1 = float(rng.random())
         acc, em, nd = O.verify_stochastic_one([tok], [q], [o, o], [u0, u1])
         out, ndd = accept_batch_stochastic(
