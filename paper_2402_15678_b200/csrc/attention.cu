@@ -106,8 +106,6 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
           qkv + (int64_t)(b * Qtot + i) * ldq + (1 + kv) * HD + h * D + c * 8);
       *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
     }
-    __threadfence();
-    __syncthreads();
   }
 
   // Q fragments (rows g, g+8 of the 16-query tile); the softmax scale
@@ -147,9 +145,16 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       const int e2 = e - kv * kKT * V8;
       const int j = e2 / V8, c = e2 - j * V8;
       __nv_bfloat16* dst = (kv ? sV : sK) + buf * S::TILE + j * LD + c * 8;
-      if (j < rows)
-        cp_async16(dst, (kv ? V : K) + (int64_t)(t0 + j) * D + c * 8);
-      else
+      const int t = t0 + j;
+      if (j < rows) {
+        // this call's own rows come straight from qkv (no dependence on the
+        // cache writes above), older keys from the cache
+        const __nv_bfloat16* src =
+            (fuse_append && t >= pstart)
+                ? qkv + (int64_t)(b * Qtot + (t - pstart)) * ldq + (1 + kv) * HD + h * D + c * 8
+                : (kv ? V : K) + (int64_t)t * D + c * 8;
+        cp_async16(dst, src);
+      } else
         *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);  // masked keys must be finite
     }
     cp_async_commit();
