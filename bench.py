@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    ap.add_argument("--schedule", default="sequential", choices=["sequential", "pipelined"],
+                    help="pipelined: two request groups of --batch each (2x requests), verify of one "
+                         "overlapping drafting of the other (aggspec/engine.py:494-576)")
     return ap.parse_args()
 
 
@@ -163,7 +166,8 @@ def roofline_verify(engine, rounds, peaks):
     tot_bytes = tot_t = 0.0
     for r in rounds:
         ctx = r.ctx_mean
-        b = P2 + engine.B * ctx * kvb + engine.B * (r.s + 1) * kvb
+        nb = len(r.accepted) if r.accepted else engine.B
+        b = P2 + nb * ctx * kvb + nb * (r.s + 1) * kvb
         tot_bytes += b
         tot_t += r.t_verify_ms * 1e-3
     ach = tot_bytes / tot_t / 1e9
@@ -192,9 +196,11 @@ def run_ours(args, rank, ws):
     cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch, s_init=4,
                        s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
     max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
-    eng = SpecEngine(target, drafters, cfg, slots=args.batch, max_len=max_len,
-                     use_graphs=not args.no_graphs, fidelity=fid)
-    reqs = make_requests(args.batch, args.prompt_len, args.new_tokens, tcfg.vocab)
+    pipelined = args.schedule == "pipelined"
+    n_req = args.batch * (2 if pipelined else 1)
+    eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
+                     use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined)
+    reqs = make_requests(n_req, args.prompt_len, args.new_tokens, tcfg.vocab)
     teacher = eng.greedy_teacher(fresh(reqs), args.new_tokens) if fid else None
 
     def one_step(timed_events=True):
@@ -271,7 +277,7 @@ def run_ours(args, rank, ws):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts, random-init weights, fidelity-injected drafts",
         "config": {"workload": WORKLOAD, "target": args.target, "ssms": [args.ssm] * K,
-                   "global_batch": args.batch * ws, "prompt_len": args.prompt_len,
+                   "global_batch": n_req * ws, "schedule": args.schedule, "prompt_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
                    "fidelity": fid, "parallelism": "replicas" if ws > 1 else "single-gpu",
                    "l2": "inputs larger than L2 (25.7 GB of weights streamed per verify)",

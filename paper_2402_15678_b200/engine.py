@@ -1,9 +1,12 @@
 """Speculate-vote-verify runtime on one B200: the device form of
-SpeculationEngine._do_draft_batch / _do_verify_batch (aggspec/engine.py:252-330).
+SpeculationEngine._do_draft_batch / _do_verify_batch (aggspec/engine.py:252-330)
+and of its two schedules, sequential and pipelined (aggspec/engine.py:337-342,
+494-576).
 
-One round, entirely on the device (capturable as one CUDA graph per (s, Qc)):
+One round of a request group, entirely on the device (two CUDA graphs per
+(s, Qc): draft and verify):
 
-  for each SSM k (K drafters, own weights + KV cache):
+  for each SSM k (K drafters, own weights + KV cache, own stream):
       step 0   catch-up forward of the Qc context tokens the SSM has not cached
                (rollback: an SSM's cache is valid only up to its longest prefix
                agreement with the emitted tokens), logits of the last row
@@ -13,11 +16,20 @@ One round, entirely on the device (capturable as one CUDA graph per (s, Qc)):
   pack [last token | path] -> verify forward of s+1 rows          (K5/K6/K7)
   LM head logits -> argmax -> greedy accept + commit              (K8/K9)
 
-then one device->host copy of the per-request results, after which the host
+then one device->host copy of the group's results, after which the host
 replays the reference's bookkeeping verbatim: record_acr / update_weights
 (fp64), the Request lifecycle, the remaining-budget / stop-token commit and the
 adaptive speculation length (observe / maybe_adjust) fed with the MEASURED
 verify time (CUDA events), not a cost model.
+
+Schedules:
+  sequential  one group holding every slot: draft, then verify, per round.
+  pipelined   two groups (the reference's pool of depth b_llm, throttle
+              len(pool) < b_llm): while the LLM verifies group A on the verify
+              stream, the drafters draft group B on the draft stream; each
+              phase ends with the verified group's results on the host.
+              Weights are snapshotted at draft start, so a vote may use weights
+              one verify stale — the reference's pipelined semantics.
 
 KV rollback is length arithmetic: the LLM's cache is valid for the first
 len(context) - 1 positions (the verify forward rewrites the rest), an SSM's for
@@ -26,6 +38,7 @@ len(context_before_round) + lcp(its draft, emitted) positions.
 from __future__ import annotations
 
 import time
+import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -33,9 +46,6 @@ import torch
 
 from . import _dev
 from . import _native
-from . import kernels as K
-import zlib
-
 from .core import AggSpecError, EngineConfig, Request, RequestState, validate_config
 from .opt import KVCache, OPTModel, OPTWeights
 from .selector import Decision, MonitorSample, SelectorState, maybe_adjust, observe
@@ -71,6 +81,7 @@ class RoundStats:
     decision: str
     s_next: int
     weights: dict
+    group: int = 0
     trace: dict | None = None  # per-round device arrays when record=True
 
 
@@ -92,16 +103,81 @@ class RunResult:
         return float(np.mean(em)) if em else 0.0
 
 
+class _Group:
+    """Per-group device buffers (one pinned upload / one download per round),
+    host request state and the drafts awaiting verification.  Slots
+    [slot0, slot0 + B)."""
+
+    def __init__(self, eng: "SpecEngine", gid: int, slot0: int, B: int):
+        self.gid, self.slot0, self.B = gid, slot0, B
+        dev, K, s_cap, V = eng.dev, eng.K, eng.cfg.s_max, eng.V
+        z = lambda *sh: torch.zeros(sh, dtype=I32, device=dev)  # noqa: E731
+        sizes = [("w", 2 * K), ("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
+                 ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
+        self.meta, self.meta_h, self.meta_off = self._packed(sizes, dev)
+        mv = lambda n: self.meta[self.meta_off[n][0]: sum(self.meta_off[n])]  # noqa: E731
+        self.w_dev = mv("w").view(torch.float64)
+        self.ctx_len, self.c_start, self.c_head = mv("ctx_len"), mv("c_start"), mv("c_head")
+        self.v_start, self.last, self.remaining = mv("v_start"), mv("last"), mv("remaining")
+        self.step_start = mv("step_start").view(s_cap, B)
+        self.c_tok = mv("c_tok")
+        rsz = [("n_acc", B), ("n_emit", B), ("finished", B), ("voted", B),
+               ("emitted", B * (s_cap + 1)), ("tgt", B * (s_cap + 1)), ("drafts", B * K * s_cap),
+               ("path", B * s_cap)]
+        self.res, self.res_h, self.res_off = self._packed(rsz, dev)
+        rv = lambda n: self.res[self.res_off[n][0]: sum(self.res_off[n])]  # noqa: E731
+        self.drafts, self.path, self.voted = rv("drafts"), rv("path"), rv("voted")
+        self.acc = AcceptOut(rv("n_acc"), rv("emitted"), rv("n_emit"), rv("finished"), rv("tgt"))
+        self.slot = torch.arange(slot0, slot0 + B, dtype=I32, device=dev)
+        self.req_key = z(B)
+        self.step_tok = [z(B, 1) for _ in range(K)]
+        self.argmax = [z(B) for _ in range(K)]
+        self.ssm_ws = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(K)]
+        self.ssm_logits = [torch.empty(B, V, device=dev) for _ in range(K)]
+        self.argmax_ws = torch.zeros(B * (s_cap + 1), dtype=torch.int64, device=dev)
+        self.vin = z(B, s_cap + 1)
+        self.v_logits = torch.empty(B * (s_cap + 1), V, device=dev)
+        self.ev_d0 = torch.cuda.Event(enable_timing=True)
+        self.ev_d1 = torch.cuda.Event(enable_timing=True)
+        self.ev_v0 = torch.cuda.Event(enable_timing=True)
+        self.ev_v1 = torch.cuda.Event(enable_timing=True)
+        self.ev_res = torch.cuda.Event()
+        self.K = K
+        # host state
+        self.requests: list[Request] = []
+        self.ctx: list[list[int]] = []
+        self.ssm_cached: list[list[int]] = []
+        self.pending = None  # (s, qc, active, t_start) of drafts awaiting verification
+
+    @staticmethod
+    def _packed(sizes, dev):
+        n = sum(m for _, m in sizes)
+        off, o = {}, 0
+        for name, m in sizes:
+            off[name] = (o, m)
+            o += m
+        return (torch.zeros(n, dtype=I32, device=dev), torch.zeros(n, dtype=I32, pin_memory=True), off)
+
+    def drafts_s(self, s):
+        # drafts buffer viewed as [B, K, s] contiguous (the first B*K*s ints)
+        return self.drafts[: self.B * self.K * s].view(self.B, self.K, s)
+
+    def active(self):
+        return [b for b, r in enumerate(self.requests) if r.state != RequestState.FINISHED]
+
+
 class SpecEngine:
     """Greedy speculative decoding with K voting drafters on one GPU."""
 
     def __init__(self, target: OPTWeights, drafters: list[OPTWeights], cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
-                 record: bool = False):
+                 record: bool = False, pipelined: bool = False):
         validate_config(cfg)
         if len(cfg.initial_weights) != len(drafters):
             raise ValueError("initial_weights must have one entry per drafter")
+        if pipelined and slots % 2:
+            raise ValueError("pipelined mode needs an even number of slots (two groups)")
         self.dev = torch.device(device)
         _dev.require_cuda()
         self.cfg = cfg
@@ -110,105 +186,62 @@ class SpecEngine:
         self.max_len = max_len
         self.adaptive = adaptive
         self.record = record
-        s_cap = cfg.s_max
-        self.max_rows_t = max(slots * (s_cap + 1), slots)
-        self.target = OPTModel(target, max_rows=max(self.max_rows_t, slots * max_len), device=device)
-        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device) for w in drafters]
-        self.t_cache = KVCache(target.cfg, slots, max_len, device)
-        self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
+        self.pipelined = pipelined
         V = target.cfg.vocab
         if any(w.cfg.vocab != V for w in drafters):
             raise ValueError("drafters and target must share a vocabulary")
         self.V = V
-        B = slots
-        z = lambda *sh: torch.zeros(sh, dtype=I32, device=self.dev)  # noqa: E731
-        # per-round inputs: views into ONE int32 buffer uploaded with one H2D
-        # copy from a pinned mirror (the fp64 vote weights ride at its head)
-        Kw = 2 * self.K
-        sizes = [("w", Kw), ("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
-                 ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
-        n_meta = sum(n for _, n in sizes)
-        self.meta = torch.zeros(n_meta, dtype=I32, device=self.dev)
-        self.meta_h = torch.zeros(n_meta, dtype=I32, pin_memory=True)
-        self._meta_off = {}
-        o = 0
-        for name, n in sizes:
-            self._meta_off[name] = (o, n)
-            o += n
-        mv = lambda name: self.meta[self._meta_off[name][0]: sum(self._meta_off[name])]  # noqa: E731
-        self.w_dev = mv("w").view(torch.float64)
-        self.ctx_len, self.c_start, self.c_head = mv("ctx_len"), mv("c_start"), mv("c_head")
-        self.v_start, self.last, self.remaining = mv("v_start"), mv("last"), mv("remaining")
-        self.step_start = mv("step_start").view(s_cap, B)
-        self.c_tok = mv("c_tok")
-        self.slot = torch.arange(B, dtype=I32, device=self.dev)
-        self.req_key = z(B)
-        # per-round results: views into ONE int32 buffer downloaded with one D2H copy
-        rsz = [("n_acc", B), ("n_emit", B), ("finished", B), ("voted", B),
-               ("emitted", B * (s_cap + 1)), ("tgt", B * (s_cap + 1)), ("drafts", B * self.K * s_cap),
-               ("path", B * s_cap)]
-        n_res = sum(n for _, n in rsz)
-        self.res = torch.zeros(n_res, dtype=I32, device=self.dev)
-        self.res_h = torch.zeros(n_res, dtype=I32, pin_memory=True)
-        self._res_off = {}
-        o = 0
-        for name, n in rsz:
-            self._res_off[name] = (o, n)
-            o += n
-        rv = lambda name: self.res[self._res_off[name][0]: sum(self._res_off[name])]  # noqa: E731
-        self.drafts = rv("drafts")
-        self.path = rv("path")
-        self.voted = rv("voted")
-        self.acc = AcceptOut(rv("n_acc"), rv("emitted"), rv("n_emit"), rv("finished"), rv("tgt"))
-        # per-round device intermediates
-        self.step_tok = [z(B, 1) for _ in range(self.K)]
-        self.argmax = [z(B) for _ in range(self.K)]
-        self.argmax_ws = torch.zeros(max(B * (s_cap + 1), B), dtype=torch.int64, device=self.dev)
-        self.ssm_ws = [torch.zeros(B, dtype=torch.int64, device=self.dev) for _ in range(self.K)]
-        self.ssm_logits = [torch.empty(B, V, device=self.dev) for _ in range(self.K)]
-        self.vin = z(B, s_cap + 1)
-        self.v_logits = torch.empty(B * (s_cap + 1), V, device=self.dev)
-        # fidelity injection (bench mode)
+        s_cap = cfg.s_max
+        self.target = OPTModel(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
+        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device) for w in drafters]
+        self.t_cache = KVCache(target.cfg, slots, max_len, device)
+        self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
+        ng = 2 if pipelined else 1
+        gb = slots // ng
+        self.groups = [_Group(self, g, g * gb, gb) for g in range(ng)]
+        self.slot = torch.arange(slots, dtype=I32, device=self.dev)
         self.fidelity = list(fidelity) if fidelity is not None else None
         self.inject_seed = inject_seed
-        self.teacher = z(B, max_len) - 1 if fidelity is not None else None
+        self.teacher = (torch.full((slots, max_len), -1, dtype=I32, device=self.dev)
+                        if fidelity is not None else None)
         self.use_graphs = use_graphs
         self.graphs: dict = {}
         self.graph_kernels: dict = {}   # kernels per captured graph (launch accounting)
         self.kernel_launches = 0        # kernels this engine issued (eager + replayed)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
-        self.streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
-        self.ev_v0 = torch.cuda.Event(enable_timing=True)
-        self.ev_v1 = torch.cuda.Event(enable_timing=True)
-        self.ev_d0 = torch.cuda.Event(enable_timing=True)
-        self.pinned_out = None
+        self.ssm_streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
+        self.draft_stream = torch.cuda.Stream(self.dev)
+        self.verify_stream = torch.cuda.Stream(self.dev)
+        self.requests: list[Request] = []
 
     # ------------------------------------------------------------------ setup
     def prefill(self, requests: list[Request]) -> None:
-        """Assign slots and cache every prompt position but the last (the
-        first round feeds the last prompt token)."""
+        """Assign slots (request i -> slot i; a group is a slot range) and cache
+        every prompt position but the last (the first round feeds the last
+        prompt token)."""
         if len(requests) > self.B:
             raise ValueError(f"{len(requests)} requests exceed {self.B} slots")
         self.requests = list(requests)
-        self.n_active = len(requests)
-        self.ctx = [list(r.prompt) + list(r.generated) for r in requests]
-        lens = [len(c) for c in self.ctx]
-        if min(lens) < 1:
+        ctx = [list(r.prompt) + list(r.generated) for r in requests]
+        if min(len(c) for c in ctx) < 1:
             raise ValueError("context must be non-empty")
-        P = max(lens) - 1
-        if max(lens) + self.cfg.s_max + 2 > self.max_len or any(
-                len(c) + r.remaining + self.cfg.s_max + 2 > self.max_len for c, r in zip(self.ctx, requests)):
+        if any(len(c) + r.remaining + self.cfg.s_max + 2 > self.max_len for c, r in zip(ctx, requests)):
             raise ValueError("max_len too small for prompt + max_new_tokens + s_max")
-        keys = np.zeros(self.B, np.int32)
-        for b, r in enumerate(requests):
-            keys[b] = zlib.crc32(str(r.id).encode()) & 0x7FFFFFFF
-        self.req_key.copy_(torch.from_numpy(keys))
-        self.ssm_cached = [[len(c) - 1 for c in self.ctx] + [0] * (self.B - len(requests))
-                           for _ in range(self.K)]
+        for g in self.groups:
+            idx = range(g.slot0, min(g.slot0 + g.B, len(requests)))
+            g.requests = [requests[i] for i in idx]
+            g.ctx = [ctx[i] for i in idx]
+            g.ssm_cached = [[len(c) - 1 for c in g.ctx] + [0] * (g.B - len(g.ctx)) for _ in range(self.K)]
+            keys = np.zeros(g.B, np.int32)
+            for b, r in enumerate(g.requests):
+                keys[b] = zlib.crc32(str(r.id).encode()) & 0x7FFFFFFF
+            g.req_key.copy_(torch.from_numpy(keys))
+            g.pending = None
+        P = max(len(c) for c in ctx) - 1
         if P > 0:
             toks = np.zeros((self.B, P), np.int32)
-            for b, c in enumerate(self.ctx):
+            for b, c in enumerate(ctx):
                 toks[b, : len(c) - 1] = c[:-1]
             t = torch.from_numpy(toks).to(self.dev)
             self.h2d_bytes += toks.nbytes
@@ -235,66 +268,60 @@ class SpecEngine:
             t[b, p0: p0 + len(seq)] = seq
         self.teacher.copy_(torch.from_numpy(t))
 
-    # --------------------------------------------------------- device round
-    def _device_draft(self, s: int, qc: int) -> None:
+    # --------------------------------------------------------- device work
+    def _device_draft(self, g: _Group, s: int, qc: int) -> None:
         """K drafters (concurrent streams) + vote + verifier input rows."""
-        B = self.B
         main = torch.cuda.current_stream(self.dev)
         ev0 = torch.cuda.Event()
         ev0.record(main)
         done = []
-        for k, (m, cache) in enumerate(zip(self.ssms, self.s_caches)):
-            st = self.streams[k]
+        for k in range(self.K):
+            st = self.ssm_streams[k]
             st.wait_event(ev0)
             with torch.cuda.stream(st):
-                self._draft(k, m, cache, s, qc, st)
+                self._draft(g, k, s, qc, st)
                 e = torch.cuda.Event()
                 e.record(st)
                 done.append(e)
         for e in done:
             main.wait_event(e)
         sp = _dev.stream_ptr(main)
-        _native.call("ms_vote", self._drafts_s(s).data_ptr(), self.w_dev.data_ptr(), None, B, self.K, s,
-                     self.path.data_ptr(), self.voted.data_ptr(), sp)
-        _native.call("ms_pack_verify", self.last.data_ptr(), self.path.data_ptr(), B, s,
-                     self.vin.data_ptr(), sp)
+        _native.call("ms_vote", g.drafts_s(s).data_ptr(), g.w_dev.data_ptr(), None, g.B, self.K, s,
+                     g.path.data_ptr(), g.voted.data_ptr(), sp)
+        _native.call("ms_pack_verify", g.last.data_ptr(), g.path.data_ptr(), g.B, s, g.vin.data_ptr(), sp)
 
-    def _device_verify(self, s: int) -> None:
-        """Verify forward of s+1 rows per request + greedy accept."""
-        B, V = self.B, self.V
-        sp = _dev.stream_ptr()
-        vin = self.vin.view(-1)[: B * (s + 1)].view(B, s + 1)
-        logits = self.v_logits[: B * (s + 1)]
-        self.target.forward(vin, self.v_start, self.slot, self.t_cache, logits)
-        a = self.acc
-        _native.call("ms_accept_greedy_logits", self.path.data_ptr(), logits.data_ptr(), 0, V,
-                     self.remaining.data_ptr(), -1 if self.cfg.stop_token is None else self.cfg.stop_token,
-                     B, s, a.tgt_argmax.data_ptr(), self.argmax_ws.data_ptr(), a.n_acc.data_ptr(),
-                     a.emitted.data_ptr(), a.n_emit.data_ptr(), a.finished.data_ptr(), None, sp)
-
-    def _drafts_s(self, s):
-        # drafts buffer viewed as [B, K, s] contiguous (the first B*K*s ints)
-        return self.drafts[: self.B * self.K * s].view(self.B, self.K, s)
-
-    def _draft(self, k, m: OPTModel, cache: KVCache, s: int, qc: int, st) -> None:
-        B = self.B
+    def _draft(self, g: _Group, k: int, s: int, qc: int, st) -> None:
+        B, m, cache = g.B, self.ssms[k], self.s_caches[k]
         sp = _dev.stream_ptr(st)
-        dr = self._drafts_s(s)
-        tok_in = self.c_tok[: B * qc].view(B, qc)
-        teacher = self.teacher.data_ptr() if self.teacher is not None else None
+        dr = g.drafts_s(s)
+        tok_in = g.c_tok[: B * qc].view(B, qc)
+        teacher = None
+        if self.teacher is not None:
+            teacher = self.teacher.data_ptr() + g.slot0 * self.max_len * 4  # the group's rows
         f = float(self.fidelity[k]) if self.fidelity is not None else 0.0
         for j in range(s):
             if j == 0:
-                m.forward(tok_in, self.c_start, self.slot, cache, self.ssm_logits[k],
-                          head_rows=self.c_head, stream=st)
+                m.forward(tok_in, g.c_start, g.slot, cache, g.ssm_logits[k], head_rows=g.c_head, stream=st)
             else:
-                m.forward(self.step_tok[k], self.step_start[j - 1], self.slot, cache,
-                          self.ssm_logits[k], stream=st)
-            _native.call("ms_argmax_rows", self.ssm_logits[k].data_ptr(), 0, B, self.V, self.V,
-                         self.argmax[k].data_ptr(), self.ssm_ws[k].data_ptr(), sp)
-            _native.call("ms_draft_commit", self.argmax[k].data_ptr(), self.ctx_len.data_ptr(), B, j, k,
-                         self.K, s, teacher, self.max_len, self.req_key.data_ptr(), f,
-                         self.inject_seed, dr.data_ptr(), self.step_tok[k].data_ptr(), sp)
+                m.forward(g.step_tok[k], g.step_start[j - 1], g.slot, cache, g.ssm_logits[k], stream=st)
+            _native.call("ms_argmax_rows", g.ssm_logits[k].data_ptr(), 0, B, self.V, self.V,
+                         g.argmax[k].data_ptr(), g.ssm_ws[k].data_ptr(), sp)
+            _native.call("ms_draft_commit", g.argmax[k].data_ptr(), g.ctx_len.data_ptr(), B, j, k,
+                         self.K, s, teacher, self.max_len, g.req_key.data_ptr(), f,
+                         self.inject_seed, dr.data_ptr(), g.step_tok[k].data_ptr(), sp)
+
+    def _device_verify(self, g: _Group, s: int) -> None:
+        """Verify forward of s+1 rows per request + greedy accept."""
+        B, V = g.B, self.V
+        sp = _dev.stream_ptr()
+        vin = g.vin.view(-1)[: B * (s + 1)].view(B, s + 1)
+        logits = g.v_logits[: B * (s + 1)]
+        self.target.forward(vin, g.v_start, g.slot, self.t_cache, logits)
+        a = g.acc
+        _native.call("ms_accept_greedy_logits", g.path.data_ptr(), logits.data_ptr(), 0, V,
+                     g.remaining.data_ptr(), -1 if self.cfg.stop_token is None else self.cfg.stop_token,
+                     B, s, a.tgt_argmax.data_ptr(), g.argmax_ws.data_ptr(), a.n_acc.data_ptr(),
+                     a.emitted.data_ptr(), a.n_emit.data_ptr(), a.finished.data_ptr(), None, sp)
 
     def _replay(self, key, fn) -> None:
         """Run fn eagerly the first time (sets kernel attributes, produces this
@@ -304,55 +331,64 @@ class SpecEngine:
             fn()
             self.kernel_launches += _native.launch_count() - n0
             return
-        g = self.graphs.get(key)
-        if g is None:
+        gr = self.graphs.get(key)
+        if gr is None:
             fn()
-            torch.cuda.synchronize(self.dev)
+            torch.cuda.current_stream(self.dev).synchronize()
             self.kernel_launches += _native.launch_count() - n0
-            g = torch.cuda.CUDAGraph()
+            gr = torch.cuda.CUDAGraph()
             n1 = _native.launch_count()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(gr, stream=torch.cuda.current_stream(self.dev)):
                 fn()
             self.graph_kernels[key] = _native.launch_count() - n1
-            self.graphs[key] = g
+            self.graphs[key] = gr
             return
-        g.replay()
+        gr.replay()
         self.kernel_launches += self.graph_kernels[key]
 
-    def _run_device_round(self, s: int, qc: int) -> None:
-        self.ev_d0.record()
-        self._replay(("draft", s, qc), lambda: self._device_draft(s, qc))
-        self.ev_v0.record()
-        self._replay(("verify", s), lambda: self._device_verify(s))
-        self.ev_v1.record()
+    def _launch_draft(self, g: _Group, s: int, qc: int) -> None:
+        with torch.cuda.stream(self.draft_stream):
+            g.ev_d0.record()
+            self._replay(("draft", g.gid, s, qc), lambda: self._device_draft(g, s, qc))
+            g.ev_d1.record()
+
+    def _launch_verify(self, g: _Group, s: int) -> None:
+        with torch.cuda.stream(self.verify_stream):
+            self.verify_stream.wait_event(g.ev_d1)  # this group's drafts
+            g.ev_v0.record()
+            self._replay(("verify", g.gid, s), lambda: self._device_verify(g, s))
+            g.ev_v1.record()
+            g.res_h.copy_(g.res, non_blocking=True)  # one D2H for the whole round
+            g.ev_res.record()
 
     # ------------------------------------------------------------- host side
-    def _upload_round(self, s: int) -> int:
-        B = self.B
-        lens = np.array([len(c) for c in self.ctx] + [1] * (B - len(self.ctx)), np.int64)
-        active = np.array([r.state != RequestState.FINISHED for r in self.requests] +
-                          [False] * (B - len(self.requests)))
-        need = [lens[b] - self.ssm_cached[k][b] for k in range(self.K) for b in range(B) if active[b]]
-        qc = int(max(need)) if need else 1
-        qc = max(1, min(qc, s + 1))
+    def _upload(self, g: _Group, s: int) -> int:
+        """Pack the group's round inputs into its pinned buffer; one H2D copy
+        on the draft stream.  Returns Qc (catch-up rows)."""
+        B = g.B
+        lens = np.array([len(c) for c in g.ctx] + [1] * (B - len(g.ctx)), np.int64)
+        act = g.active()
+        need = [lens[b] - g.ssm_cached[k][b] for k in range(self.K) for b in act]
+        qc = max(1, min(int(max(need)) if need else 1, s + 1))
         start = np.maximum(lens - qc, 0)
         c_tok = np.zeros((B, qc), np.int32)
-        for b, c in enumerate(self.ctx):
+        for b, c in enumerate(g.ctx):
             seg = c[start[b]: start[b] + qc]
             c_tok[b, : len(seg)] = seg
         c_head = np.arange(B) * qc + (lens - 1 - start)
-        rem = np.array([r.remaining if a else 0 for r, a in zip(self.requests, active)] +
-                       [0] * (B - len(self.requests)), np.int32)
-        last = np.array([c[-1] for c in self.ctx] + [0] * (B - len(self.ctx)), np.int32)
-        steps = np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]).astype(np.int32)
-        mh = self.meta_h.numpy()
+        rem = np.zeros(B, np.int32)
+        for b in act:
+            rem[b] = g.requests[b].remaining
+        last = np.array([c[-1] for c in g.ctx] + [0] * (B - len(g.ctx)), np.int32)
+        steps = np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)])
+        mh = g.meta_h.numpy()
 
         def put(name, v):
-            o, n = self._meta_off[name]
+            o, _ = g.meta_off[name]
             v = np.ascontiguousarray(v, dtype=np.int32).reshape(-1)
             mh[o: o + v.size] = v
 
-        w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)
+        w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)  # snapshot
         put("w", w.view(np.int32))
         put("ctx_len", lens)
         put("c_start", start)
@@ -362,9 +398,90 @@ class SpecEngine:
         put("remaining", rem)
         put("step_start", steps)
         put("c_tok", c_tok)
-        self.meta.copy_(self.meta_h, non_blocking=True)  # one H2D for the whole round
-        self.h2d_bytes += self.meta_h.numel() * 4
+        with torch.cuda.stream(self.draft_stream):
+            g.meta.copy_(g.meta_h, non_blocking=True)
+        self.h2d_bytes += g.meta_h.numel() * 4
         return qc
+
+    def _start_draft(self, g: _Group) -> bool:
+        """Take the group's unfinished requests as a draft batch (s = the
+        selector's current s, weights snapshot) and launch its drafting."""
+        act = g.active()
+        if not act:
+            return False
+        s = self.selector.current_s
+        for b in act:
+            g.requests[b].advance(RequestState.DRAFTING)
+        qc = self._upload(g, s)
+        self._launch_draft(g, s, qc)
+        g.pending = (s, qc, act, time.perf_counter())
+        return True
+
+    def _finish_verify(self, g: _Group, rnd: int) -> RoundStats:
+        """Host bookkeeping of a verified group (reference semantics)."""
+        s, qc, active, t_start = g.pending
+        g.pending = None
+        g.ev_res.synchronize()
+        self.d2h_bytes += g.res_h.numel() * 4
+        rh = g.res_h.numpy()
+
+        def get(name, n=None):
+            o, m = g.res_off[name]
+            return rh[o: o + (m if n is None else n)]
+
+        B = g.B
+        n_acc = get("n_acc")
+        n_emit = get("n_emit")
+        emitted = get("emitted", B * (s + 1)).reshape(B, s + 1)
+        voted = get("voted")
+        drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
+        t_verify = g.ev_v0.elapsed_time(g.ev_v1)
+        t_draft = g.ev_d0.elapsed_time(g.ev_d1)
+        accs, ems, vts = [], [], []
+        for b in active:
+            r = g.requests[b]
+            r.advance(RequestState.AWAITING_VERIFICATION)
+            acc = int(n_acc[b])
+            use = [int(t) for t in emitted[b, : n_emit[b]]]
+            record_acr(self.weights, int(voted[b]), acc / s)
+            if len(use) == 0:
+                raise NoProgress(f"request {r.id} made no progress")
+            len_before = len(g.ctx[b])
+            r.generated.extend(use)
+            g.ctx[b].extend(use)
+            stopped = self.cfg.stop_token is not None and self.cfg.stop_token in use
+            if stopped or r.remaining <= 0:
+                r.advance(RequestState.FINISHED)
+                r.finish_time = time.perf_counter()
+            else:
+                r.advance(RequestState.RUNNING)
+            # SSM rollback: valid up to the longest prefix agreement with `use`
+            for k in range(self.K):
+                mlen = 0
+                lim = min(s - 1, len(use) - 1)  # the last context token is always re-fed
+                while mlen < lim and drafts[b, k, mlen] == use[mlen]:
+                    mlen += 1
+                g.ssm_cached[k][b] = len_before + mlen
+            accs.append(acc)
+            ems.append(len(use))
+            vts.append(int(voted[b]))
+        update_weights(self.weights, self.cfg)
+        vl = float(np.mean(ems)) if ems else 1.0
+        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_verify, vl=vl, s_used=s))
+        decision = Decision.HOLD
+        if self.adaptive:
+            _, decision = maybe_adjust(self.selector)
+        trace = None
+        if self.record:
+            trace = dict(active=active, drafts=drafts.copy(), weights_used=g.w_dev.cpu().numpy(),
+                         path=get("path", B * s).reshape(B, s).copy(), voted=voted.copy(),
+                         n_acc=n_acc.copy(), n_emit=n_emit.copy(), emitted=emitted.copy(),
+                         tgt=get("tgt", B * (s + 1)).reshape(B, s + 1).copy(),
+                         remaining=g.remaining.cpu().numpy())
+        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, t_draft_ms=t_draft, trace=trace,
+                          t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
+                          emitted=ems, voted=vts, vl=vl, decision=decision.value, group=g.gid,
+                          s_next=self.selector.current_s, weights=dict(self.weights.weights))
 
     def run(self, requests: list[Request], max_rounds: int | None = None) -> RunResult:
         """Generate until every request finishes (reference semantics)."""
@@ -378,91 +495,36 @@ class SpecEngine:
         res = RunResult(outputs={})
         t0 = time.perf_counter()
         rnd = 0
-        while any(r.state != RequestState.FINISHED for r in self.requests):
-            if max_rounds is not None and rnd >= max_rounds:
-                break
-            st = self._round(rnd)
-            res.rounds.append(st)
-            rnd += 1
+        if not self.pipelined:
+            g = self.groups[0]
+            while (max_rounds is None or rnd < max_rounds) and self._start_draft(g):
+                self._launch_verify(g, g.pending[0])
+                res.rounds.append(self._finish_verify(g, rnd))
+                rnd += 1
+        else:
+            # phase: verify `cur` on the verify stream while drafting `nxt` on the
+            # draft stream (the drafter runs only while the pool holds < 1 batch)
+            cur, nxt = self.groups
+            self._start_draft(cur)
+            while max_rounds is None or rnd < max_rounds:
+                if cur.pending is None:  # nothing to verify here: try the other group
+                    if nxt.pending is None and not self._start_draft(nxt):
+                        if not self._start_draft(cur):
+                            break
+                        continue
+                    cur, nxt = nxt, cur
+                    continue
+                self._launch_verify(cur, cur.pending[0])
+                if nxt.pending is None:
+                    self._start_draft(nxt)
+                res.rounds.append(self._finish_verify(cur, rnd))
+                rnd += 1
+                cur, nxt = nxt, cur
         torch.cuda.synchronize(self.dev)
         res.wall_s = time.perf_counter() - t0
         res.outputs = {r.id: list(r.generated) for r in self.requests}
         res.tokens = sum(len(r.generated) for r in self.requests)
         return res
-
-    def _round(self, rnd: int) -> RoundStats:
-        t_start = time.perf_counter()
-        s = self.selector.current_s
-        active = [b for b, r in enumerate(self.requests) if r.state != RequestState.FINISHED]
-        for b in active:
-            r = self.requests[b]
-            r.advance(RequestState.DRAFTING)
-        qc = self._upload_round(s)
-        self._run_device_round(s, qc)
-        # results (one sync)
-        self.res_h.copy_(self.res, non_blocking=True)  # one D2H for the whole round
-        torch.cuda.current_stream(self.dev).synchronize()
-        self.d2h_bytes += self.res_h.numel() * 4
-        rh = self.res_h.numpy()
-
-        def get(name, n=None):
-            o, m = self._res_off[name]
-            return rh[o: o + (m if n is None else n)]
-
-        B = self.B
-        n_acc = get("n_acc")
-        n_emit = get("n_emit")
-        emitted = get("emitted", B * (s + 1)).reshape(B, s + 1)
-        voted = get("voted")
-        drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
-        t_verify = self.ev_v0.elapsed_time(self.ev_v1)
-        t_draft = self.ev_d0.elapsed_time(self.ev_v0)
-        accs, ems, vts = [], [], []
-        for b in active:
-            r = self.requests[b]
-            r.advance(RequestState.AWAITING_VERIFICATION)
-            acc = int(n_acc[b])
-            use = [int(t) for t in emitted[b, : n_emit[b]]]
-            record_acr(self.weights, int(voted[b]), acc / s)
-            if len(use) == 0:
-                raise NoProgress(f"request {r.id} made no progress")
-            len_before = len(self.ctx[b])
-            r.generated.extend(use)
-            self.ctx[b].extend(use)
-            stopped = self.cfg.stop_token is not None and self.cfg.stop_token in use
-            if stopped or r.remaining <= 0:
-                r.advance(RequestState.FINISHED)
-                r.finish_time = time.perf_counter()
-            else:
-                r.advance(RequestState.RUNNING)
-            # SSM rollback: valid up to the longest prefix agreement with `use`
-            for k in range(self.K):
-                mlen = 0
-                lim = min(s - 1, len(use) - 1)  # the last context token is always re-fed
-                while mlen < lim and drafts[b, k, mlen] == use[mlen]:
-                    mlen += 1
-                self.ssm_cached[k][b] = len_before + mlen
-            accs.append(acc)
-            ems.append(len(use))
-            vts.append(int(voted[b]))
-        update_weights(self.weights, self.cfg)
-        vl = float(np.mean(ems)) if ems else 1.0
-        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_verify, vl=vl, s_used=s))
-        decision = Decision.HOLD
-        if self.adaptive:
-            _, decision = maybe_adjust(self.selector)
-        trace = None
-        if self.record:
-            B = self.B
-            trace = dict(active=active, drafts=drafts.copy(), weights_used=self.w_dev.cpu().numpy(),
-                         path=get("path", B * s).reshape(B, s).copy(), voted=voted.copy(),
-                         n_acc=n_acc.copy(), n_emit=n_emit.copy(), emitted=emitted.copy(),
-                         tgt=get("tgt", B * (s + 1)).reshape(B, s + 1).copy(),
-                         remaining=self.remaining.cpu().numpy())
-        return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, t_draft_ms=t_draft, trace=trace,
-                          t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
-                          emitted=ems, voted=vts, vl=vl, decision=decision.value,
-                          s_next=self.selector.current_s, weights=dict(self.weights.weights))
 
     # ----------------------------------------------------- greedy reference
     def greedy_teacher(self, requests: list[Request], n_new: int) -> dict:

@@ -113,3 +113,34 @@ def test_stop_token_and_budget():
         t = teacher[r.id]
         want = t[: t.index(stop) + 1] if stop in t else t
         assert res.outputs[r.id] == want
+
+
+@pytest.mark.parametrize("fidelity", [None, [0.9, 0.8, 0.6]])
+def test_pipelined_schedule_is_lossless_and_alternates(fidelity):
+    """Pipelined mode (two request groups: the verifier works on one while the
+    drafters draft the other, aggspec/engine.py:494-576) produces the same
+    token streams as plain greedy decoding — the reference's sequential ==
+    pipelined token-stream equivalence (tests/test_engine.py:106-133)."""
+    from paper_2402_15678_b200.core import EngineConfig, Request
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.opt import CONFIGS, OPTWeights
+    tcfg, scfg = CONFIGS["tiny-target"], CONFIGS["tiny-ssm"]
+    target = OPTWeights.random(tcfg, 0, device="cuda", std=0.05, bias_std=0.02)
+    drafters = [OPTWeights.random(scfg, k + 1, device="cuda", std=0.05, bias_std=0.02) for k in range(3)]
+    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=4, b_ssm=4, initial_weights=(1.0, 1.0, 1.0),
+                       decision_threshold=3)
+    eng = SpecEngine(target, drafters, cfg, slots=8, max_len=120, pipelined=True, fidelity=fidelity)
+    rng = np.random.default_rng(5)
+    reqs = [Request(f"req-{i:03d}", [int(t) for t in rng.integers(0, tcfg.vocab, size=int(rng.integers(4, 9)))],
+                    int(rng.integers(20, 48))) for i in range(7)]
+    teacher = eng.greedy_teacher([Request(r.id, list(r.prompt), r.max_new_tokens) for r in reqs], 48)
+    eng.prefill(reqs)
+    if fidelity:
+        eng.set_teacher(teacher)
+    res = eng.decode()
+    for r in reqs:
+        assert res.outputs[r.id] == teacher[r.id][: r.max_new_tokens]
+    groups = [rd.group for rd in res.rounds]
+    assert groups[:6] == [0, 1, 0, 1, 0, 1]
+    if fidelity:
+        assert res.mean_accepted > 1.0
