@@ -126,6 +126,17 @@ int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
               int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
               int* counters, int n_counters, void* stream);
+/* ms_linear with the LayerNorm that precedes the projection fused in:
+ *   out = act(LN(x) . w^T + bias) + residual,  LN(x) = (x - mean) * rstd * gamma + beta
+ * (fp32 two-pass row statistics, eps).  Every CTA recomputes the statistics of
+ * its token rows from x and normalises the TMA-loaded x tiles in shared memory
+ * before the MMA reads them: one launch instead of LayerNorm + GEMM, meant for
+ * the small decode shapes (M*K up to ~10^5) where launches, not bytes, cost.
+ * Cluster split-K schedule; splits as in ms_linear. */
+int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const void* beta, float eps,
+                 const void* w, const void* bias, const void* residual, int64_t ldr,
+                 void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                 int splits, void* stream);
 /* Default split-K factor for an [N, K] weight (cluster path). */
 int ms_linear_splits(int N, int K);
 /* Scratch the stream-K path needs for this shape. */

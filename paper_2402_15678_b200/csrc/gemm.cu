@@ -41,6 +41,14 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int stages;                     // TMA pipeline depth of this launch (cluster path)
+  // fused LayerNorm of the X operand (ln_g != null): X = LN(x) * g + b, the raw
+  // rows x [M, ldx] read for the row statistics, the TMA tile normalised in
+  // shared memory before the MMA consumes it
+  const __nv_bfloat16* ln_g;
+  const __nv_bfloat16* ln_b;
+  const __nv_bfloat16* ln_x;
+  int64_t ldx;
+  float ln_eps;
 };
 
 constexpr int kBM = 128;  // output features per CTA (MMA M)
@@ -67,7 +75,9 @@ struct LinearCfg {
     const int pipe = stages * STAGE_BYTES;
     return pipe > PART_BYTES ? pipe : PART_BYTES;
   }
-  __host__ __device__ static int smem(int stages) { return 1024 + data_bytes(stages) + (2 * MAX_STAGES + 1) * 8 + 16; }
+  __host__ __device__ static int smem(int stages) {
+    return 1024 + data_bytes(stages) + (3 * MAX_STAGES + 1) * 8 + 16 + 2 * BN * 4;
+  }
 };
 
 __device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v) {
@@ -107,7 +117,11 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::data_bytes(STAGES));
   uint64_t* empty = full + C::MAX_STAGES;
   uint64_t* tmem_full = empty + C::MAX_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* normed = tmem_full + 1;  // [MAX_STAGES] X tile normalised (fused LayerNorm)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(normed + C::MAX_STAGES);
+  float* s_mean = reinterpret_cast<float*>(tmem_slot + 4);  // [BN]
+  float* s_rstd = s_mean + BN;                              // [BN]
+  const bool fuse_ln = p.ln_g != nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -124,6 +138,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&normed[s], 128);
     }
     tc::mbar_init(tmem_full, 1);
     tc::fence_barrier_init();
@@ -133,6 +148,8 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  // X operand ready for the MMA: the TMA barrier, or the normalisation barrier
+  uint64_t* x_ready = fuse_ln ? normed : full;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -168,7 +185,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
+        tc::mbar_wait(&x_ready[stage], phase);
         tc::fence_after_sync();
         const uint64_t ad = tc::smem_desc_sw128(sW + stage * C::W_BYTES);
         const uint64_t bd = tc::smem_desc_sw128(sX + stage * C::X_BYTES);
@@ -191,6 +208,64 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     const int m_hi = min(BN, p.M - m0);  // valid token columns in this tile
     pdl_wait();  // residual / outputs are ordered after the previous kernel
     pdl_trigger();
+    if (fuse_ln) {
+      // (1) row statistics of the raw rows, fp32, two-pass, one warp per row
+      const int et = threadIdx.x - 64;  // 0..127
+      const int ew = et >> 5;
+      for (int r = ew; r < BN; r += 4) {
+        float mean = 0.f, rstd = 0.f;
+        if (r < m_hi) {
+          const __nv_bfloat16* xr = p.ln_x + (int64_t)(m0 + r) * p.ldx;
+          float sum = 0.f;
+          for (int c = lane * 8; c < p.K; c += 256) {
+            float f[8];
+            unpack8(*reinterpret_cast<const bf16x8*>(xr + c), f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum += f[j];
+          }
+          mean = warp_sum(sum) / (float)p.K;
+          float sq = 0.f;
+          for (int c = lane * 8; c < p.K; c += 256) {
+            float f[8];
+            unpack8(*reinterpret_cast<const bf16x8*>(xr + c), f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sq += (f[j] - mean) * (f[j] - mean);
+          }
+          rstd = rsqrtf(warp_sum(sq) / (float)p.K + p.ln_eps);
+        }
+        if (lane == 0) {
+          s_mean[r] = mean;
+          s_rstd[r] = rstd;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // (2) per stage: normalise the swizzled X tile in place, hand it to the MMA
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        uint8_t* xs = sX + stage * C::X_BYTES;
+        for (int ch = et; ch < BN * 8; ch += 128) {  // 16-byte chunks: row r, logical chunk j
+          const int r = ch >> 3, j = ch & 7;
+          bf16x8* ptr = reinterpret_cast<bf16x8*>(xs + r * 128 + ((j ^ (r & 7)) << 4));
+          const int col = kb * kBK + j * 8;
+          float f[8], gg[8], bb[8];
+          unpack8(*ptr, f);
+          unpack8(*reinterpret_cast<const bf16x8*>(p.ln_g + col), gg);
+          unpack8(*reinterpret_cast<const bf16x8*>(p.ln_b + col), bb);
+          const float mu = s_mean[r], rs = s_rstd[r];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gg[e] + bb[e];
+          *ptr = pack8(f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+        tc::mbar_arrive(&normed[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -585,10 +660,11 @@ extern "C" int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* 
   return MS_OK;
 }
 
-extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
-                         const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-                         int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
-                         int* counters, int n_counters, void* stream) {
+static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias,
+                       const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
+                       int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
+                       int* counters, int n_counters, const void* g_ln_g, const void* g_ln_b,
+                       float g_ln_eps, void* stream) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < N) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
@@ -611,6 +687,13 @@ extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* 
   p.ldr = ldr;
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
+  p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
+  if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
+    p.ln_g = (const __nv_bfloat16*)g_ln_g;
+    p.ln_b = (const __nv_bfloat16*)g_ln_b;
+    p.ln_x = (const __nv_bfloat16*)x;
+    p.ln_eps = g_ln_eps;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
@@ -652,3 +735,22 @@ extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* 
     default: return launch_linear<256>(tw, tx, p, m_tiles, st);
   }
 }
+
+extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
+                         const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
+                         int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
+                         int* counters, int n_counters, void* stream) {
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, ws,
+                     ws_bytes, counters, n_counters, nullptr, nullptr, 0.f, stream);
+}
+
+extern "C" int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const void* beta, float eps,
+                            const void* w, const void* bias, const void* residual, int64_t ldr,
+                            void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                            int splits, void* stream) {
+  if (!gamma || !beta) return MS_ERR_VALUE;
+  if (residual && residual == x) return MS_ERR_VALUE;  // the raw rows are re-read for statistics
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr,
+                     0, nullptr, 0, gamma, beta, eps, stream);
+}
+

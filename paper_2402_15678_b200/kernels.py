@@ -72,6 +72,28 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     return out
 
 
+def linear_ln(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, w: torch.Tensor,
+              bias: torch.Tensor | None = None, eps: float = 1e-5, residual: torch.Tensor | None = None,
+              act: int = 0, out: torch.Tensor | None = None, out_f32: bool = False, splits: int = 0,
+              stream=None) -> torch.Tensor:
+    """out = act(LayerNorm(x) @ w.T + bias) + residual in one launch (ms_linear_ln)."""
+    if x.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
+        raise ValueError("x [M, K] and w [N, K] must be bf16")
+    M, K = x.shape
+    N = w.shape[0]
+    if w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
+        raise ValueError("shape/stride mismatch")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    _native.call("ms_linear_ln", x.data_ptr(), x.stride(0), _dev.ptr(gamma, BF16, "gamma"),
+                 _dev.ptr(beta, BF16, "beta"), eps, w.data_ptr(),
+                 None if bias is None else _dev.ptr(bias, BF16, "bias"),
+                 None if residual is None else residual.data_ptr(),
+                 0 if residual is None else residual.stride(0), out.data_ptr(), out.stride(0),
+                 int(out.dtype == torch.float32), M, N, K, act, splits, _dev.stream_ptr(stream))
+    return out
+
+
 def embed(tok: torch.Tensor, start: torch.Tensor, Q: int, tok_emb: torch.Tensor,
           pos_emb: torch.Tensor | None, pos_offset: int = 2, out: torch.Tensor | None = None,
           stream=None) -> torch.Tensor:

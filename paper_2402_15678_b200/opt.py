@@ -126,6 +126,10 @@ class OPTModel:
     """Batched forward over the kernels with static activation buffers (so a
     forward of a given (B, Q) can be captured in a CUDA graph)."""
 
+    # fuse LayerNorm into the QKV / FC1 GEMMs when rows x d is at most this
+    # (every GEMM CTA re-reads the rows for their statistics)
+    FUSE_LN_ELEMS = 131072
+
     def __init__(self, w: OPTWeights, max_rows: int, device="cuda"):
         self.w, self.cfg = w, w.cfg
         c = self.cfg
@@ -163,15 +167,25 @@ class OPTModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         ws = self.ws
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
+        # small (decode-sized) activations: LayerNorm fused into the next GEMM
+        fuse_ln = R * c.d <= self.FUSE_LN_ELEMS
         for i in range(c.n_layers):
             p = f"l{i}."
-            K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
-            K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, ws=ws, stream=stream)
+            if fuse_ln:
+                K.linear_ln(x, w[p + "ln1_g"], w[p + "ln1_b"], w[p + "w_qkv"], w[p + "b_qkv"], c.eps,
+                            out=qkv, stream=stream)
+            else:
+                K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
+                K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, ws=ws, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
                         self.scale, out=at, stream=stream)
             K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, ws=ws, stream=stream)
-            K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
-            K.linear(h, w[p + "w_fc1"], w[p + "b_fc1"], act=1, out=ff, ws=ws, stream=stream)
+            if fuse_ln:
+                K.linear_ln(x, w[p + "ln2_g"], w[p + "ln2_b"], w[p + "w_fc1"], w[p + "b_fc1"], c.eps,
+                            act=1, out=ff, stream=stream)
+            else:
+                K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
+                K.linear(h, w[p + "w_fc1"], w[p + "b_fc1"], act=1, out=ff, ws=ws, stream=stream)
             K.linear(ff, w[p + "w_fc2"], w[p + "b_fc2"], residual=x, out=x, ws=ws,
                      stream=stream)
         Rh = R if head_rows is None else head_rows.numel()

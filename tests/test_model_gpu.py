@@ -165,3 +165,19 @@ def test_head_rows_gather():
     part = torch.empty(4, cfg.vocab, device="cuda")
     model.forward(toks, start, slot, KVCache(cfg, B, 16), part, head_rows=rows)
     assert torch.equal(part, full[rows.long()])
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 2304, 768), (80, 3072, 768), (5, 768, 256), (33, 1024, 256)])
+def test_linear_ln_matches_layernorm_then_linear(M, N, K):
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(M + N)
+    x = (torch.randn(M, K, generator=g) * 2 + 0.5).to(torch.bfloat16).cuda()
+    gam = (1 + 0.1 * torch.randn(K, generator=g)).to(torch.bfloat16).cuda()
+    bet = (0.1 * torch.randn(K, generator=g)).to(torch.bfloat16).cuda()
+    w = (torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    b = torch.randn(N, generator=g).to(torch.bfloat16).cuda()
+    for act in (0, 1):
+        ref = Kn.linear(Kn.layernorm(x, gam, bet, 1e-5), w, b, act=act, out_f32=True)
+        got = Kn.linear_ln(x, gam, bet, w, b, 1e-5, act=act, out_f32=True)
+        torch.testing.assert_close(got, ref, rtol=2e-2, atol=2e-2)
+        assert torch.equal(got, Kn.linear_ln(x, gam, bet, w, b, 1e-5, act=act, out_f32=True))
