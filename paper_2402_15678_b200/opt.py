@@ -127,8 +127,11 @@ class OPTModel:
     forward of a given (B, Q) can be captured in a CUDA graph)."""
 
     # fuse LayerNorm into the QKV / FC1 GEMMs when rows x d is at most this
-    # (every GEMM CTA re-reads the rows for their statistics)
-    FUSE_LN_ELEMS = 131072
+    # (every GEMM CTA re-reads the rows for their statistics).  Off by default:
+    # measured slower on the OPT-125M decode chain (2.51 vs 2.17 ms per draft
+    # round) — the statistics pass sits on the GEMM's critical path, so the
+    # saved launch is paid back; MS_FUSE_LN=1 enables it.
+    FUSE_LN_ELEMS = 131072 if os.environ.get("MS_FUSE_LN", "0") == "1" else 0
 
     def __init__(self, w: OPTWeights, max_rows: int, device="cuda"):
         self.w, self.cfg = w, w.cfg
