@@ -167,10 +167,16 @@ int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
  * cache positions 0..start[b] + i.  With append != 0 the K/V columns of the Q
  * rows are first written into the cache (fused into the kernel when Q <= 16,
  * else an ms_kv_append launch precedes it).  out [B*Q, ldo] bf16, head h at
- * columns h*D.. .  Limits: D in {64, 128}. */
+ * columns h*D.. .  Deterministic and batch invariant (fixed key partition,
+ * fixed merge order).  Limits: D in {64, 128}. */
 int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
                  const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                 void* v_cache, float scale, int append, void* out, int64_t ldo, void* stream);
+                 void* v_cache, float scale, int append, void* out, int64_t ldo,
+                 void* ws, int64_t ws_bytes, int* counters, int n_counters, void* stream);
+/* With ws != NULL the KV range is split into fixed 128-key chunks, one CTA each
+ * (more CTAs in flight on the KV stream); the last chunk of a (request, head)
+ * merges the chunk partials in chunk order.  ws / counters sizes: */
+int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes, int* n_counters);
 
 /* ---- round glue ------------------------------------------------------------
  * After an SSM decode step's argmax tok[B]: drafts[b, k, j] = tok[b] (the token

@@ -42,7 +42,8 @@ _SIGS = {
     "ms_kv_append": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
     "ms_draft_commit": [_P, _P, _I, _I, _I, _I, _I, _P, _I64, _P, _F, ctypes.c_uint64, _P, _P, _P],
     "ms_pack_verify": [_P, _P, _I, _I, _P, _P],
-    "ms_attention": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _F, _I, _P, _I64, _P],
+    "ms_attention": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _F, _I, _P, _I64, _P, _I64, _P, _I, _P],
+    "ms_attention_workspace": [_I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
 }
 _RESTYPE = {"ms_strerror": ctypes.c_char_p, "ms_launch_count": ctypes.c_int64,
             "ms_reset_launch_count": None}

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kAThreads)
 attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int H,
                  const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                  __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
-                 int fuse_append, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+                 int fuse_append, __nv_bfloat16* __restrict__ out, int64_t ldo,
+                 int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters) {
   using S = AttnSmem<D>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;  // 16-dim chunks (MMA k-steps for Q.K^T)
@@ -84,7 +85,10 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
-  const int q0 = blockIdx.z * 16;
+  // blockIdx.z = (query chunk of 16 rows, KV chunk of kct tiles)
+  const int qc = blockIdx.z / n_kv, kvc = blockIdx.z - qc * n_kv;
+  const int nqc = gridDim.z / n_kv;
+  const int q0 = qc * 16;
   const int Q = min(16, Qtot - q0);
   const int pstart = start[b];
   const int p0 = pstart + q0;
@@ -93,8 +97,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   __nv_bfloat16* V = vc + cbase;
   const int HD = H * D;
 
-  if (fuse_append) {
-    // this request's new K/V rows for head h -> cache (single query chunk only)
+  if (fuse_append && kvc == 0) {
+    // this request's new K/V rows for head h -> cache (single query chunk only;
+    // this kernel reads them back from qkv, so no fence is needed)
     constexpr int V8 = D / 8;
     for (int e = tid; e < 2 * Qtot * V8; e += kAThreads) {
       const int kv = e >= Qtot * V8;
@@ -134,7 +139,13 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   }
 
   const int n_keys = min(p0 + Q, T);  // keys 0 .. p0+Q-1
-  const int n_tiles = (n_keys + kKT - 1) / kKT;
+  const int n_tiles_all = (n_keys + kKT - 1) / kKT;
+  // split-KV: this CTA owns tiles [tile0, tile1) — fixed 64*kct-key chunks
+  // from position 0, so a query's partition never depends on the other rows
+  const int n_chunks = (n_tiles_all + kct - 1) / kct;
+  if (kvc >= n_chunks) return;  // nothing for this request here (uniform per CTA)
+  const int tile0 = kvc * kct;
+  const int n_tiles = min(n_tiles_all, tile0 + kct);
 
   auto load_tile = [&](int tile, int buf) {
     constexpr int V8 = D / 8;
@@ -168,9 +179,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int row_lim0 = g < Q ? p0 + g : -1;      // last key position row g may see
   const int row_lim1 = g + 8 < Q ? p0 + g + 8 : -1;
 
-  if (n_tiles > 0) load_tile(0, 0);
-  for (int tile = 0; tile < n_tiles; ++tile) {
-    const int buf = tile & 1;
+  if (n_tiles > tile0) load_tile(tile0, 0);
+  for (int tile = tile0; tile < n_tiles; ++tile) {
+    const int buf = (tile - tile0) & 1;
     if (tile + 1 < n_tiles) {
       load_tile(tile + 1, buf ^ 1);
       cp_async_wait<1>();
@@ -285,7 +296,29 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
     so[(warp * 16 + g + 8) * D + c + 1] = o[n][3];
   }
   __syncthreads();
-  for (int e = tid; e < Q * D; e += kAThreads) {
+  // this CTA's partial: (m, L, O = A / L) per query row
+  if (n_chunks == 1) {
+    for (int e = tid; e < Q * D; e += kAThreads) {
+      const int i = e / D, dd = e - i * D;
+      float mxx = sm[i];
+#pragma unroll
+      for (int w = 1; w < 4; ++w) mxx = fmaxf(mxx, sm[w * 16 + i]);
+      float L = 0.f, A = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float mw = sm[w * 16 + i];
+        const float f = mw == -INFINITY ? 0.f : exp2f(mw - mxx);
+        L += sl[w * 16 + i] * f;
+        A += so[(w * 16 + i) * D + dd] * f;
+      }
+      out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + dd] = f2bf(A / L);
+    }
+    return;
+  }
+  constexpr int PS = 16 * (D + 2);  // partial record: m[16], L[16], O[16][D]
+  const int64_t unit = ((int64_t)b * H + h) * nqc + qc;
+  float* rec = ws + (unit * n_kv + kvc) * PS;
+  for (int e = tid; e < 16 * D; e += kAThreads) {
     const int i = e / D, dd = e - i * D;
     float mxx = sm[i];
 #pragma unroll
@@ -298,14 +331,49 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       L += sl[w * 16 + i] * f;
       A += so[(w * 16 + i) * D + dd] * f;
     }
-    out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + dd] = f2bf(A / L);
+    __stcg(rec + 32 + e, L > 0.f ? A / L : 0.f);
+    if (dd == 0) {
+      __stcg(rec + i, mxx);
+      __stcg(rec + 16 + i, L);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  if (tid == 0) {
+    const int old = atomicAdd(counters + unit, 1);
+    s_last = old == n_chunks - 1;
+    if (s_last) counters[unit] = 0;  // leave zero for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last chunk to finish merges all chunks in chunk order (deterministic)
+  const float* recs = ws + unit * n_kv * PS;
+  for (int e = tid; e < Q * D; e += kAThreads) {
+    const int i = e / D;
+    float mxx = -INFINITY;
+    for (int cc = 0; cc < n_chunks; ++cc) mxx = fmaxf(mxx, __ldcg(recs + cc * PS + i));
+    float L = 0.f, A = 0.f;
+    for (int cc = 0; cc < n_chunks; ++cc) {
+      const float mc = __ldcg(recs + cc * PS + i);
+      const float wgt = mc == -INFINITY ? 0.f : __ldcg(recs + cc * PS + 16 + i) * exp2f(mc - mxx);
+      L += wgt;
+      A += wgt * __ldcg(recs + cc * PS + 32 + e);
+    }
+    out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + (e - i * D)] = f2bf(A / L);
   }
 }
+
+// KV chunk (in 64-key tiles) per CTA for the split-KV schedule: a fixed
+// constant, so the partition never depends on the batch.
+constexpr int kKvChunkTiles = 2;
 
 template <int D>
 static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, const int32_t* slot,
                        const int32_t* start, int T, void* kc, void* vc, float scale, int fuse,
-                       void* out, int64_t ldo, cudaStream_t st) {
+                       void* out, int64_t ldo, float* ws, int64_t ws_bytes, int* counters,
+                       int n_counters, cudaStream_t st) {
   using S = AttnSmem<D>;
   static bool attr = false;
   if (!attr) {
@@ -315,10 +383,18 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, const 
     attr = true;
   }
   const float scale_log2 = scale * 1.4426950408889634f;
-  dim3 grid(B, H, (Q + 15) / 16);
+  const int nqc = (Q + 15) / 16;
+  int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
+  if (ws) {
+    kct = kKvChunkTiles;
+    n_kv = ((T + kKT - 1) / kKT + kct - 1) / kct;
+    const int64_t need = (int64_t)B * H * nqc * n_kv * 16 * (D + 2) * 4;
+    if (ws_bytes < need || n_counters < B * H * nqc) return MS_ERR_VALUE;
+  }
+  dim3 grid(B, H, nqc * n_kv);
   return launch(attention_kernel<D>, grid, dim3(kAThreads), S::BYTES, st, 1,
                 (const __nv_bfloat16*)qkv, ldq, Q, H, slot, start, T, (__nv_bfloat16*)kc,
-                (__nv_bfloat16*)vc, scale_log2, fuse, (__nv_bfloat16*)out, ldo);
+                (__nv_bfloat16*)vc, scale_log2, fuse, (__nv_bfloat16*)out, ldo, n_kv, kct, ws, counters);
 }
 
 }  // namespace ms
@@ -327,9 +403,19 @@ extern "C" int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, i
                             const int32_t* slot, const int32_t* start, int T, void* k_cache,
                             void* v_cache, void* stream);
 
+extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes,
+                                      int* n_counters) {
+  const int nqc = (Q + 15) / 16;
+  const int n_kv = ((T + ms::kKT - 1) / ms::kKT + ms::kKvChunkTiles - 1) / ms::kKvChunkTiles;
+  if (ws_bytes) *ws_bytes = (int64_t)B * H * nqc * n_kv * 16 * (D + 2) * 4;
+  if (n_counters) *n_counters = B * H * nqc;
+  return MS_OK;
+}
+
 extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
                             const int32_t* slot, const int32_t* start, int T, void* k_cache,
                             void* v_cache, float scale, int append, void* out, int64_t ldo,
+                            void* ws, int64_t ws_bytes, int* counters, int n_counters,
                             void* stream) {
   if (B < 0 || Q < 1 || H < 1 || T < 1) return MS_ERR_VALUE;
   if (B == 0) return MS_OK;
@@ -346,8 +432,10 @@ extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, i
     }
   }
   if (D == 64)
-    return ms::launch_attn<64>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
+    return ms::launch_attn<64>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo,
+                               (float*)ws, ws_bytes, counters, n_counters, st);
   if (D == 128)
-    return ms::launch_attn<128>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo, st);
+    return ms::launch_attn<128>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo,
+                                (float*)ws, ws_bytes, counters, n_counters, st);
   return MS_ERR_UNSUPPORTED;
 }

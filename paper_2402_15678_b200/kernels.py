@@ -129,14 +129,32 @@ def kv_append(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
                  _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), _dev.stream_ptr(stream))
 
 
+class AttnWorkspace:
+    """Split-KV scratch of ms_attention (chunk partials + per-(request, head)
+    counters), sized for a model's (B, Q, H, D, T) envelope."""
+
+    def __init__(self, B: int, Q: int, H: int, D: int, T: int, device):
+        b = ctypes.c_int64()
+        c = ctypes.c_int()
+        _native.check(_native.lib.ms_attention_workspace(B, Q, H, D, T, ctypes.byref(b), ctypes.byref(c)),
+                      "ms_attention_workspace")
+        self.ws = torch.empty((b.value + 3) // 4, dtype=torch.float32, device=device)
+        self.counters = torch.zeros(c.value, dtype=torch.int32, device=device)
+
+
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
-              out: torch.Tensor | None = None, append: bool = True, stream=None) -> torch.Tensor:
-    """Causal KV-cache attention of Q rows per request (K/V append fused when append)."""
+              out: torch.Tensor | None = None, append: bool = True, ws: AttnWorkspace | None = None,
+              stream=None) -> torch.Tensor:
+    """Causal KV-cache attention of Q rows per request (K/V append fused when
+    append; split-KV over fixed 128-key chunks when a workspace is given)."""
     T = k_cache.shape[2]
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
     _native.call("ms_attention", qkv.data_ptr(), qkv.stride(0), B, Q, H, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
                  _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), scale, int(append),
-                 out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
+                 out.data_ptr(), out.stride(0),
+                 None if ws is None else ws.ws.data_ptr(), 0 if ws is None else ws.ws.numel() * 4,
+                 None if ws is None else ws.counters.data_ptr(), 0 if ws is None else ws.counters.numel(),
+                 _dev.stream_ptr(stream))
     return out

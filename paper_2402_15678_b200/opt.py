@@ -144,6 +144,7 @@ class OPTModel:
         self.attn = torch.empty((max_rows, c.d), dtype=BF16, device=device)
         self.ff = torch.empty((max_rows, c.ffn), dtype=BF16, device=device)
         self.scale = 1.0 / math.sqrt(c.head_dim)
+        self._aws: dict = {}
         # GEMM schedule: cluster split-K (measured faster than the persistent
         # stream-K path, whose tile fix-up is a serial tail — tools/probe_gemm_graph.py);
         # MS_STREAM_K=1 selects stream-K (scratch is per model = per stream)
@@ -152,6 +153,15 @@ class OPTModel:
             self.ws = K.Workspace(self.device)
             for n, k in ((3 * c.d, c.d), (c.d, c.d), (c.ffn, c.d), (c.d, c.ffn), (c.vocab, c.d)):
                 self.ws.fit(min(max_rows, 256), n, k)
+
+    def _attn_ws(self, B: int, Q: int, T: int):
+        """Split-KV attention scratch, one per (B, Q, T) shape (allocated on the
+        first, eager call — never inside a graph capture)."""
+        key = (B, Q, T)
+        if key not in self._aws:
+            c = self.cfg
+            self._aws[key] = K.AttnWorkspace(B, Q, c.n_heads, c.head_dim, T, self.device)
+        return self._aws[key]
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
                 logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -170,6 +180,7 @@ class OPTModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         ws = self.ws
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
+        aws = self._attn_ws(B, Q, cache.max_len)
         # small (decode-sized) activations: LayerNorm fused into the next GEMM
         fuse_ln = R * c.d <= self.FUSE_LN_ELEMS
         for i in range(c.n_layers):
@@ -181,7 +192,7 @@ class OPTModel:
                 K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
                 K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, ws=ws, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
-                        self.scale, out=at, stream=stream)
+                        self.scale, out=at, ws=aws, stream=stream)
             K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, ws=ws, stream=stream)
             if fuse_ln:
                 K.linear_ln(x, w[p + "ln2_g"], w[p + "ln2_b"], w[p + "w_fc1"], w[p + "b_fc1"], c.eps,
