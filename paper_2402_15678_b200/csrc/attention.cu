@@ -296,8 +296,10 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
     so[(warp * 16 + g + 8) * D + c + 1] = o[n][3];
   }
   __syncthreads();
-  // this CTA's partial: (m, L, O = A / L) per query row
-  if (n_chunks == 1) {
+  // this CTA's partial: (m, L, O = A / L) per query row.  With a workspace the
+  // chunk merge below runs even for a single chunk, so a query's output goes
+  // through the same arithmetic whatever the other rows' key counts are.
+  if (ws == nullptr) {
     for (int e = tid; e < Q * D; e += kAThreads) {
       const int i = e / D, dd = e - i * D;
       float mxx = sm[i];
