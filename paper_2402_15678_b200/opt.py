@@ -132,6 +132,7 @@ class OPTModel:
     # round) — the statistics pass sits on the GEMM's critical path, so the
     # saved launch is paid back; MS_FUSE_LN=1 enables it.
     FUSE_LN_ELEMS = 131072 if os.environ.get("MS_FUSE_LN", "0") == "1" else 0
+    SPLIT_KV = os.environ.get("MS_SPLITKV", "0") == "1"
 
     def __init__(self, w: OPTWeights, max_rows: int, device="cuda"):
         self.w, self.cfg = w, w.cfg
@@ -180,7 +181,8 @@ class OPTModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         ws = self.ws
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
-        aws = self._attn_ws(B, Q, cache.max_len)
+        # split-KV attention is opt-in: measured slower at these context lengths
+        aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
         # small (decode-sized) activations: LayerNorm fused into the next GEMM
         fuse_ln = R * c.d <= self.FUSE_LN_ELEMS
         for i in range(c.n_layers):

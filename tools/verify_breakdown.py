@@ -34,7 +34,7 @@ def gemms():
 def attn():
     for i in range(c.n_layers):
         K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], m.scale, out=at,
-                    ws=m._attn_ws(B, Q, cache.max_len) if os.environ.get("MS_SPLITKV", "1") == "1" else None)
+                    ws=m._attn_ws(B, Q, cache.max_len) if os.environ.get("MS_SPLITKV", "0") == "1" else None)
 
 def lns():
     for i in range(c.n_layers):
