@@ -87,13 +87,8 @@ def barrier(ws):
 
 
 def max_over_ranks(x: float, ws: int) -> float:
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2402_15678_b200.dist import max_over_ranks as mx
+    return mx(x, device="cuda") if ws > 1 else x
 
 
 # ------------------------------------------------------------------------ clocks
@@ -200,7 +195,10 @@ def run_ours(args, rank, ws):
     n_req = args.batch * (2 if pipelined else 1)
     eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
                      use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined)
-    reqs = make_requests(n_req, args.prompt_len, args.new_tokens, tcfg.vocab)
+    # weak scaling: the global request list is n_req per rank; each rank serves
+    # its own contiguous slice (requests are independent — no data-path collective)
+    from paper_2402_15678_b200.dist import shard_requests
+    reqs = shard_requests(make_requests(n_req * ws, args.prompt_len, args.new_tokens, tcfg.vocab), rank, ws)
     teacher = eng.greedy_teacher(fresh(reqs), args.new_tokens) if fid else None
 
     def one_step(timed_events=True):
