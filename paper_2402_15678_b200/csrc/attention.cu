@@ -118,23 +118,15 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   uint32_t qa[KC][4];
   {
     const int r0 = g, r1 = g + 8;
-    const __nv_bfloat16* q0p = qkv + (int64_t)(b * Qtot + q0 + r0) * ldq + h * D;
-    const __nv_bfloat16* q1p = qkv + (int64_t)(b * Qtot + q0 + r1) * ldq + h * D;
+    const uint32_t* q0p = reinterpret_cast<const uint32_t*>(qkv + (int64_t)(b * Qtot + q0 + r0) * ldq + h * D);
+    const uint32_t* q1p = reinterpret_cast<const uint32_t*>(qkv + (int64_t)(b * Qtot + q0 + r1) * ldq + h * D);
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
-      float f[8];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int dd = c * 16 + 2 * t4 + 8 * u;
-        f[4 * u + 0] = r0 < Q ? bf2f(q0p[dd]) : 0.f;
-        f[4 * u + 1] = r0 < Q ? bf2f(q0p[dd + 1]) : 0.f;
-        f[4 * u + 2] = r1 < Q ? bf2f(q1p[dd]) : 0.f;
-        f[4 * u + 3] = r1 < Q ? bf2f(q1p[dd + 1]) : 0.f;
-      }
-      qa[c][0] = pack_bf16(f[0], f[1]);  // (row g,   k 2t..2t+1)
-      qa[c][1] = pack_bf16(f[2], f[3]);  // (row g+8, k 2t..2t+1)
-      qa[c][2] = pack_bf16(f[4], f[5]);  // (row g,   k 2t+8..)
-      qa[c][3] = pack_bf16(f[6], f[7]);  // (row g+8, k 2t+8..)
+      const int w = c * 8 + t4;  // 32-bit word: dims 2*t4 .. 2*t4+1 of chunk c
+      qa[c][0] = r0 < Q ? q0p[w] : 0u;      // (row g,   k 2t..2t+1)
+      qa[c][1] = r1 < Q ? q1p[w] : 0u;      // (row g+8, k 2t..2t+1)
+      qa[c][2] = r0 < Q ? q0p[w + 4] : 0u;  // (row g,   k 2t+8..)
+      qa[c][3] = r1 < Q ? q1p[w + 4] : 0u;  // (row g+8, k 2t+8..)
     }
   }
 
@@ -147,26 +139,32 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int tile0 = kvc * kct;
   const int n_tiles = min(n_tiles_all, tile0 + kct);
 
+  // tile loader: thread -> fixed 16-byte column chunk `lc` and rows lr0 + p*LRS
+  // (no per-element index arithmetic); the call's own rows (t >= pstart) come
+  // straight from qkv, older keys from the cache
+  constexpr int V8 = D / 8;
+  constexpr int LRS = kAThreads / V8;  // rows per pass
+  constexpr int LNP = kKT / LRS;       // passes per tile
+  const int lc = tid % V8, lr0 = tid / V8;
+  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + HD + h * D + lc * 8;
+  const __nv_bfloat16* qkv_v = qkv_k + HD;
   auto load_tile = [&](int tile, int buf) {
-    constexpr int V8 = D / 8;
     const int t0 = tile * kKT;
-    const int rows = min(kKT, n_keys - t0);
-    for (int e = tid; e < 2 * kKT * V8; e += kAThreads) {
-      const int kv = e >= kKT * V8;
-      const int e2 = e - kv * kKT * V8;
-      const int j = e2 / V8, c = e2 - j * V8;
-      __nv_bfloat16* dst = (kv ? sV : sK) + buf * S::TILE + j * LD + c * 8;
+    __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
+    __nv_bfloat16* dv = sV + buf * S::TILE + lc * 8;
+#pragma unroll
+    for (int pp = 0; pp < LNP; ++pp) {
+      const int j = lr0 + pp * LRS;
       const int t = t0 + j;
-      if (j < rows) {
-        // this call's own rows come straight from qkv (no dependence on the
-        // cache writes above), older keys from the cache
-        const __nv_bfloat16* src =
-            (fuse_append && t >= pstart)
-                ? qkv + (int64_t)(b * Qtot + (t - pstart)) * ldq + (1 + kv) * HD + h * D + c * 8
-                : (kv ? V : K) + (int64_t)t * D + c * 8;
-        cp_async16(dst, src);
-      } else
-        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);  // masked keys must be finite
+      if (t < n_keys) {
+        const bool fresh = fuse_append && t >= pstart;
+        const int64_t qrow = (int64_t)(t - pstart) * ldq;
+        cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : V + (int64_t)t * D + lc * 8);
+      } else {  // masked keys must be finite
+        *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
+      }
     }
     cp_async_commit();
   };
