@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    ap.add_argument("--fixed-s", type=int, default=0, help="disable the adaptive selector, use this s")
     ap.add_argument("--schedule", default="sequential", choices=["sequential", "pipelined"],
                     help="pipelined: two request groups of --batch each (2x requests), verify of one "
                          "overlapping drafting of the other (aggspec/engine.py:494-576)")
@@ -188,13 +189,14 @@ def run_ours(args, rank, ws):
     K = 3
     target = OPTWeights.random(tcfg, 0, device="cuda")
     drafters = [OPTWeights.random(scfg, k + 1, device="cuda") for k in range(K)]
-    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch, s_init=4,
-                       s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
+    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch,
+                       s_init=args.fixed_s or 4, s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
     max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
     pipelined = args.schedule == "pipelined"
     n_req = args.batch * (2 if pipelined else 1)
     eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
-                     use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined)
+                     use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined,
+                     adaptive=not args.fixed_s)
     # weak scaling: the global request list is n_req per rank; each rank serves
     # its own contiguous slice (requests are independent — no data-path collective)
     from paper_2402_15678_b200.dist import shard_requests
@@ -284,6 +286,8 @@ def run_ours(args, rank, ws):
         "mean_emitted_per_round": round(float(np.mean(emt)), 4) if emt else 0.0,
         "rounds_per_step": round(len(rounds) / args.steps, 2),
         "s_trajectory_tail": [rd.s for rd in results[-1].rounds[-8:]],
+        "s_hist": {int(k): int(v) for k, v in zip(*np.unique([rd.s for rd in rounds], return_counts=True))},
+        "draft_ms_mean": round(float(np.mean([rd.t_draft_ms for rd in rounds])), 3),
         "lossless_vs_greedy": lossless,
         "verify_ms_mean": round(float(np.mean([rd.t_verify_ms for rd in rounds])), 3),
         "round_ms_mean": round(float(np.mean([rd.t_round_ms for rd in rounds])), 3),
