@@ -201,6 +201,7 @@ def run_ours(args, rank, ws):
     # its own contiguous slice (requests are independent — no data-path collective)
     from paper_2402_15678_b200.dist import shard_requests
     reqs = shard_requests(make_requests(n_req * ws, args.prompt_len, args.new_tokens, tcfg.vocab), rank, ws)
+    eng.capture_graphs()  # every s, before timing (and before prefill)
     teacher = eng.greedy_teacher(fresh(reqs), args.new_tokens) if fid else None
 
     def one_step(timed_events=True):
