@@ -349,7 +349,7 @@ class SpecEngine:
     def _launch_draft(self, g: _Group, s: int, qc: int) -> None:
         with torch.cuda.stream(self.draft_stream):
             g.ev_d0.record()
-            self._replay(("draft", g.gid, s), lambda: self._device_draft(g, s, qc))
+            self._replay(("draft", g.gid, s, qc), lambda: self._device_draft(g, s, qc))
             g.ev_d1.record()
 
     def _launch_verify(self, g: _Group, s: int) -> None:
@@ -400,12 +400,12 @@ class SpecEngine:
         lens = np.array([len(c) for c in g.ctx] + [1] * (B - len(g.ctx)), np.int64)
         act = g.active()
         need = [lens[b] - g.ssm_cached[k][b] for k in range(self.K) for b in act]
-        assert not need or max(need) <= s + 1
-        # fixed catch-up width s+1 (the most any drafter can lag): one draft graph
-        # per s.  Rows an SSM has already cached are recomputed and rewritten
-        # with identical K/V (the forward is batch invariant), so this only
-        # costs a slightly wider first step.
-        qc = s + 1
+        # catch-up width s+1 (the most a drafter can lag when s did not shrink):
+        # one draft graph per s.  Rows an SSM has already cached are recomputed
+        # and rewritten with identical K/V (the forward is batch invariant), so
+        # this only costs a slightly wider first step.  After the selector
+        # lowered s a drafter can lag by up to s_prev+1: a wider graph then.
+        qc = max(s + 1, int(max(need)) if need else 1)
         start = np.maximum(lens - qc, 0)
         c_tok = np.zeros((B, qc), np.int32)
         for b, c in enumerate(g.ctx):
