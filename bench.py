@@ -282,6 +282,7 @@ def run_ours(args, rank, ws):
                    "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
                    "fidelity": fid, "parallelism": "replicas" if ws > 1 else "single-gpu",
                    "l2": "inputs larger than L2 (25.7 GB of weights streamed per verify)",
+                   "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
                    "graphs": not args.no_graphs},
         "mean_accepted_length": round(float(np.mean(acc)), 4) if acc else 0.0,
         "mean_emitted_per_round": round(float(np.mean(emt)), 4) if emt else 0.0,

@@ -524,10 +524,16 @@ class SpecEngine:
         self.prefill(requests)
         return self.decode(max_rounds)
 
-    def decode(self, max_rounds: int | None = None) -> RunResult:
+    def decode(self, max_rounds: int | None = None, reset_controllers: bool = False) -> RunResult:
+        """Run rounds until the prefilled requests finish.  The drafter weights
+        and the speculation-length selector persist across calls (a serving
+        engine keeps adapting over its request stream); the first call or
+        reset_controllers=True starts them from the config (s_init, initial
+        weights), as the reference engine does per run."""
         cfg = self.cfg
-        self.weights = WeightTable.from_config(list(range(self.K)), cfg)
-        self.selector = SelectorState.from_config(cfg)
+        if reset_controllers or getattr(self, "selector", None) is None:
+            self.weights = WeightTable.from_config(list(range(self.K)), cfg)
+            self.selector = SelectorState.from_config(cfg)
         res = RunResult(outputs={})
         t0 = time.perf_counter()
         rnd = 0
