@@ -137,6 +137,14 @@ int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const void* beta
                  const void* w, const void* bias, const void* residual, int64_t ldr,
                  void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                  int splits, void* stream);
+/* Low-latency projection for M <= 64 token rows (the drafters' decode steps):
+ * same contract as ms_linear (bias / ReLU / residual, bf16 or fp32 out), one
+ * CTA per 16 output features, K split over 4 warps reduced in shared memory,
+ * warp-level MMAs fed by 16-byte global loads; no TMEM, clusters or scratch.
+ * Deterministic; a row's result does not depend on M.  K % 32 == 0. */
+int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+            int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+            void* stream);
 /* Default split-K factor for an [N, K] weight (cluster path). */
 int ms_linear_splits(int N, int K);
 /* Scratch the stream-K path needs for this shape. */

@@ -193,7 +193,7 @@ class SpecEngine:
         self.V = V
         s_cap = cfg.s_max
         self.target = OPTModel(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
-        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device) for w in drafters]
+        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device, small_gemm=True) for w in drafters]
         self.t_cache = KVCache(target.cfg, slots, max_len, device)
         self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
         ng = 2 if pipelined else 1

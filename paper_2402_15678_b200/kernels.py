@@ -72,6 +72,24 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     return out
 
 
+def gemv(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
+         residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
+         out_f32: bool = False, stream=None) -> torch.Tensor:
+    """out = act(x @ w.T + bias) + residual for M <= 64 rows (ms_gemv, low latency)."""
+    M, K = x.shape
+    N = w.shape[0]
+    if x.dtype != BF16 or w.dtype != BF16 or w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
+        raise ValueError("x [M, K] and w [N, K] must be bf16 with unit column stride")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    _native.call("ms_gemv", x.data_ptr(), x.stride(0), w.data_ptr(),
+                 None if bias is None else _dev.ptr(bias, BF16, "bias"),
+                 None if residual is None else residual.data_ptr(),
+                 0 if residual is None else residual.stride(0), out.data_ptr(), out.stride(0),
+                 int(out.dtype == torch.float32), M, N, K, act, _dev.stream_ptr(stream))
+    return out
+
+
 def linear_ln(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, w: torch.Tensor,
               bias: torch.Tensor | None = None, eps: float = 1e-5, residual: torch.Tensor | None = None,
               act: int = 0, out: torch.Tensor | None = None, out_f32: bool = False, splits: int = 0,

@@ -134,8 +134,12 @@ class OPTModel:
     FUSE_LN_ELEMS = 131072 if os.environ.get("MS_FUSE_LN", "0") == "1" else 0
     SPLIT_KV = os.environ.get("MS_SPLITKV", "0") == "1"
 
-    def __init__(self, w: OPTWeights, max_rows: int, device="cuda"):
+    def __init__(self, w: OPTWeights, max_rows: int, device="cuda", small_gemm: bool = False):
+        """small_gemm: layer GEMMs of <= 64 token rows use the low-latency
+        ms_gemv (drafters' decode steps); the verifier keeps the tcgen05 path
+        everywhere, so its numerics never depend on the row count."""
         self.w, self.cfg = w, w.cfg
+        self.small_gemm = small_gemm
         c = self.cfg
         self.device = torch.device(device)
         self.max_rows = max_rows
@@ -185,25 +189,31 @@ class OPTModel:
         aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
         # small (decode-sized) activations: LayerNorm fused into the next GEMM
         fuse_ln = R * c.d <= self.FUSE_LN_ELEMS
+        small = self.small_gemm and R <= 64
+
+        def lin(xx, wname, bname, **kw):
+            if small:
+                return K.gemv(xx, w[wname], w[bname], stream=stream, **kw)
+            return K.linear(xx, w[wname], w[bname], ws=ws, stream=stream, **kw)
+
         for i in range(c.n_layers):
             p = f"l{i}."
-            if fuse_ln:
+            if fuse_ln and not small:
                 K.linear_ln(x, w[p + "ln1_g"], w[p + "ln1_b"], w[p + "w_qkv"], w[p + "b_qkv"], c.eps,
                             out=qkv, stream=stream)
             else:
                 K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
-                K.linear(h, w[p + "w_qkv"], w[p + "b_qkv"], out=qkv, ws=ws, stream=stream)
+                lin(h, p + "w_qkv", p + "b_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
                         self.scale, out=at, ws=aws, stream=stream)
-            K.linear(at, w[p + "w_o"], w[p + "b_o"], residual=x, out=x, ws=ws, stream=stream)
-            if fuse_ln:
+            lin(at, p + "w_o", p + "b_o", residual=x, out=x)
+            if fuse_ln and not small:
                 K.linear_ln(x, w[p + "ln2_g"], w[p + "ln2_b"], w[p + "w_fc1"], w[p + "b_fc1"], c.eps,
                             act=1, out=ff, stream=stream)
             else:
                 K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
-                K.linear(h, w[p + "w_fc1"], w[p + "b_fc1"], act=1, out=ff, ws=ws, stream=stream)
-            K.linear(ff, w[p + "w_fc2"], w[p + "b_fc2"], residual=x, out=x, ws=ws,
-                     stream=stream)
+                lin(h, p + "w_fc1", p + "b_fc1", act=1, out=ff)
+            lin(ff, p + "w_fc2", p + "b_fc2", residual=x, out=x)
         Rh = R if head_rows is None else head_rows.numel()
         hf = self.h[:Rh]
         K.layernorm(x, w["lnf_g"], w["lnf_b"], c.eps, out=hf, rows=head_rows, stream=stream)

@@ -205,3 +205,51 @@ def test_attention_split_kv_matches_and_is_batch_invariant(D, H, Q):
     ws1 = Kn.AttnWorkspace(B, 1, H, D, T, "cuda")
     a1 = Kn.attention(q1, B, 1, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws1)
     assert torch.equal(a1, a.view(B, Q, -1)[:, 0])
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 2304, 768), (1, 768, 3072), (33, 3072, 768), (64, 100, 256), (5, 1000, 96)])
+def test_gemv_vs_torch_and_row_invariance(M, N, K):
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(M * 3 + N)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, generator=g).to(torch.bfloat16)
+    r = torch.randn(M, N, generator=g).to(torch.bfloat16)
+    for act, res, f32 in ((0, None, True), (1, r, False)):
+        got = Kn.gemv(x.cuda(), w.cuda(), b.cuda(), None if res is None else res.cuda(), act=act,
+                      out_f32=f32).cpu()
+        want = _ref_linear(x, w, b, res, act, f32)
+        if f32:
+            torch.testing.assert_close(got, want, rtol=1e-4, atol=2e-5 * (K ** 0.5))
+        else:
+            torch.testing.assert_close(got.float(), want.float(), rtol=1.6e-2, atol=1e-2)
+    full = Kn.gemv(x.cuda(), w.cuda(), out_f32=True)
+    one = Kn.gemv(x[:1].cuda().contiguous(), w.cuda(), out_f32=True)
+    assert torch.equal(one, full[:1])
+
+
+def test_drafter_forward_small_gemm_vs_reference():
+    """The drafter path (ms_gemv for <= 64 rows) against the fp32 reference."""
+    from paper_2402_15678_b200.opt import CONFIGS, KVCache, OPTModel, OPTWeights
+    cfg = CONFIGS["tiny-ssm"]
+    w_cpu = OPTWeights.random(cfg, 3, device="cpu", std=0.05, bias_std=0.02)
+    m = OPTModel(w_cpu.to("cuda"), max_rows=256, small_gemm=True)
+    B, T0 = 4, 12
+    rng = np.random.default_rng(3)
+    toks = rng.integers(0, cfg.vocab, size=(B, T0 + 3)).astype(np.int32)
+    cache = KVCache(cfg, B, 64)
+    slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    lg = torch.empty(B * T0, cfg.vocab, device="cuda")
+    m.forward(torch.tensor(toks[:, :T0], device="cuda"), torch.zeros(B, dtype=torch.int32, device="cuda"),
+              slot, cache, lg)
+    outs = [lg.view(B, T0, -1).cpu()]
+    for j in range(3):
+        l1 = torch.empty(B, cfg.vocab, device="cuda")
+        m.forward(torch.tensor(toks[:, T0 + j:T0 + j + 1], device="cuda"),
+                  torch.full((B,), T0 + j, dtype=torch.int32, device="cuda"), slot, cache, l1)
+        outs.append(l1.view(B, 1, -1).cpu())
+    got = torch.cat(outs, 1)
+    for b in range(B):
+        ref = opt_ref.forward(w_cpu.t, cfg, toks[b])
+        err = (got[b] - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 2e-2, err
