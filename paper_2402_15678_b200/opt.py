@@ -192,7 +192,9 @@ class OPTModel:
         small = self.small_gemm and R <= 64
 
         def lin(xx, wname, bname, **kw):
-            if small:
+            # ms_gemv only where it measured faster (tools/probe_gemm_graph.py):
+            # short K; long-K projections (FC2) keep the cluster split-K path
+            if small and xx.shape[1] <= 1024:
                 return K.gemv(xx, w[wname], w[bname], stream=stream, **kw)
             return K.linear(xx, w[wname], w[bname], ws=ws, stream=stream, **kw)
 
