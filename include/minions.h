@@ -109,7 +109,10 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
  *   out[m, n] = act(sum_k x[m, k] * w[n, k] + bias[n]) + residual[m, n]
  *   x [M, ldx] bf16, w [N, K] bf16 (nn.Linear layout), bias [N] bf16 or NULL,
  *   residual [M, ldr] bf16 or NULL, out [M, ldc] bf16 (out_f32 = 0) or fp32,
- *   act 0 = identity, 1 = ReLU.
+ *   act 0 = identity, 1 = ReLU, 2 = gated SiLU (Llama SwiGLU MLP): w holds the
+ *   gate and up projections interleaved in 64-row blocks (rows 128t..128t+63 =
+ *   gate rows 64t.., rows 128t+64..128t+127 = up rows 64t..) and
+ *   out [M, N/2] = silu(gate) * up, bf16, no bias / residual, N % 128 == 0.
  * Two schedules, both deterministic and batch invariant (a row's result does
  * not depend on M, because the work partition depends only on N and K):
  *  - M <= 256, splits == 0 and scratch given: persistent stream-K kernel (one
@@ -162,6 +165,10 @@ int ms_embed(const int32_t* tok, const int32_t* start, int Q, const void* tok_em
  * row rows[r] (rows == NULL: row r) of x [*, ldx] bf16. */
 int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,
                  const void* beta, float eps, int R, int d, void* out, int64_t ldo, void* stream);
+/* RMSNorm (Llama): out = x * rsqrt(mean(x^2) + eps) * gamma, fp32 statistics,
+ * one bf16 rounding; rows as in ms_layernorm. */
+int ms_rmsnorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, float eps,
+               int R, int d, void* out, int64_t ldo, void* stream);
 
 /* KV-cache append: rows r = b*Q + i of qkv [B*Q, ldq] (layout [q | k | v],
  * each H*D wide) are written at position start[b] + i of cache slot slot[b];
@@ -169,6 +176,13 @@ int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* ga
 int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
                  const int32_t* slot, const int32_t* start, int T, void* k_cache,
                  void* v_cache, void* stream);
+/* Grouped-query form: qkv row layout [q (H*D) | k (Hkv*D) | v (Hkv*D)], caches
+ * [slots, Hkv, T, D]; with rope != NULL (float2 [>= T, D/2] of (cos, sin) of
+ * position p times frequency i, Llama rotate-half pairing i <-> i + D/2) the K
+ * rows are rotated at their absolute position before they are stored. */
+int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                     const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                     void* v_cache, const void* rope, void* stream);
 
 /* Causal attention of Q query rows per request over the KV cache: query i of
  * request b (row b*Q + i of qkv) is at position start[b] + i and attends to
@@ -185,6 +199,17 @@ int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
  * (more CTAs in flight on the KV stream); the last chunk of a (request, head)
  * merges the chunk partials in chunk order.  ws / counters sizes: */
 int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes, int* n_counters);
+/* Grouped-query attention with optional RoPE (Llama-2: H = 64 query heads over
+ * Hkv = 8 KV heads): layouts as in ms_kv_append_gqa; query head h reads KV head
+ * h / (H / Hkv).  One CTA per (request, KV head, 16 flattened (position, head)
+ * rows), so a KV head's keys are staged once for all its query heads; Q is
+ * rotated in registers, the call's own K rows while staged / appended.  The
+ * workspace of ms_attention_workspace(B, Q, H, D, T) suffices. */
+int ms_attention_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                     const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                     void* v_cache, const void* rope, float scale, int append, void* out,
+                     int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                     void* stream);
 
 /* ---- round glue ------------------------------------------------------------
  * After an SSM decode step's argmax tok[B]: drafts[b, k, j] = tok[b] (the token

@@ -16,6 +16,15 @@
 // its own online-softmax state and output accumulator in registers, and the
 // 4 warps are merged in warp order at the end.
 //
+// Grouped-query attention (Llama-2-70B: 64 query heads over 8 KV heads): the
+// CTA is per (request, KV head[, chunk]) and its MMA rows are the flattened
+// (position i, query head j of the group) pairs, row = i * G + j, so every K/V
+// byte of a KV head is staged once for all G·Q query rows that read it.  With
+// a RoPE table (Llama) the Q fragments are rotated in registers (the
+// rotate-half partner of dim d, d + D/2, sits in the same thread's fragment
+// of chunk c + D/32) and the call's fresh K rows are rotated while staged and
+// appended; cached K rows are stored rotated.
+//
 // Batch invariance: a query row's arithmetic (its MMA rows, per-row quad
 // reductions, tile order, warp-order merge) does not depend on the other
 // rows; rows of other queries only add fully-masked keys that contribute
@@ -65,13 +74,25 @@ struct AttnSmem {
   static constexpr int BYTES = KV_BYTES > MERGE_BYTES ? KV_BYTES : MERGE_BYTES;
 };
 
+__device__ __forceinline__ uint32_t rope_pair_lo(uint32_t x, uint32_t y, float2 c0, float2 c1) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x));
+  const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&y));
+  return pack_bf16(a.x * c0.x - p.x * c0.y, a.y * c1.x - p.y * c1.y);
+}
+__device__ __forceinline__ uint32_t rope_pair_hi(uint32_t x, uint32_t y, float2 c0, float2 c1) {
+  // x: dims d + D/2 (own), y: dims d (partner)
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x));
+  const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&y));
+  return pack_bf16(a.x * c0.x + p.x * c0.y, a.y * c1.x + p.y * c1.y);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kAThreads)
-attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int H,
+attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                  const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                  __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
-                 int fuse_append, __nv_bfloat16* __restrict__ out, int64_t ldo,
-                 int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters) {
+                 int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
+                 int64_t ldo, int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters) {
   using S = AttnSmem<D>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;  // 16-dim chunks (MMA k-steps for Q.K^T)
@@ -82,55 +103,88 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem);  // [2][KT][LD]
   __nv_bfloat16* sV = sK + 2 * S::TILE;                           // [2][KT][LD]
 
-  const int b = blockIdx.x, h = blockIdx.y;
+  const int b = blockIdx.x, h = blockIdx.y;  // h: KV head
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
-  // blockIdx.z = (query chunk of 16 rows, KV chunk of kct tiles)
+  const int G = Hq / Hkv;                  // query heads per KV head
+  const int rows_tot = Qtot * G;           // flattened (position, group head) rows
+  // blockIdx.z = (query-row chunk of 16, KV chunk of kct tiles)
   const int qc = blockIdx.z / n_kv, kvc = blockIdx.z - qc * n_kv;
   const int nqc = gridDim.z / n_kv;
-  const int q0 = qc * 16;
-  const int Q = min(16, Qtot - q0);
+  const int q0 = qc * 16;                  // first flattened row of this chunk
+  const int Q = min(16, rows_tot - q0);    // rows in this chunk
   const int pstart = start[b];
-  const int p0 = pstart + q0;
-  const int64_t cbase = ((int64_t)slot[b] * H + h) * T * D;
+  const int64_t cbase = ((int64_t)slot[b] * Hkv + h) * T * D;
   __nv_bfloat16* K = kc + cbase;
   __nv_bfloat16* V = vc + cbase;
-  const int HD = H * D;
+  const int QD = Hq * D, KVD = Hkv * D;
+  constexpr int V8 = D / 8;
 
-  if (fuse_append && kvc == 0) {
-    // this request's new K/V rows for head h -> cache (single query chunk only;
-    // this kernel reads them back from qkv, so no fence is needed)
-    constexpr int V8 = D / 8;
+  if (fuse_append && kvc == 0 && qc == 0) {
+    // this request's new K/V rows for KV head h -> cache (K rotated when
+    // RoPE); this kernel reads them back from qkv, so no fence is needed
     for (int e = tid; e < 2 * Qtot * V8; e += kAThreads) {
       const int kv = e >= Qtot * V8;
       const int e2 = e - kv * Qtot * V8;
       const int i = e2 / V8, c = e2 - i * V8;
       const int p = pstart + i;
       if (p < 0 || p >= T) continue;
-      const bf16x8 val = *reinterpret_cast<const bf16x8*>(
-          qkv + (int64_t)(b * Qtot + i) * ldq + (1 + kv) * HD + h * D + c * 8);
+      const __nv_bfloat16* row = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * D;
+      bf16x8 val = *reinterpret_cast<const bf16x8*>(row + c * 8);
+      if (!kv && rope) {
+        const int pc = c < V8 / 2 ? c + V8 / 2 : c - V8 / 2;
+        float fv[8], pf[8];
+        unpack8(val, fv);
+        unpack8(*reinterpret_cast<const bf16x8*>(row + pc * 8), pf);
+        rope8(fv, pf, rope + (int64_t)p * (D / 2), c * 8, D / 2);
+        val = pack8(fv);
+      }
       *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
     }
   }
 
-  // Q fragments (rows g, g+8 of the 16-query tile); the softmax scale
-  // log2(e)/sqrt(D) is applied to the fp32 scores
+  // Q fragments (rows g, g+8 of the 16-row tile; flattened row -> position
+  // fr / G, query head h*G + fr % G); the softmax scale log2(e)/sqrt(D) is
+  // applied to the fp32 scores
+  const int fr0 = q0 + g, fr1 = q0 + g + 8;
+  const int pos0 = pstart + fr0 / G, pos1 = pstart + fr1 / G;
   uint32_t qa[KC][4];
   {
-    const int r0 = g, r1 = g + 8;
-    const uint32_t* q0p = reinterpret_cast<const uint32_t*>(qkv + (int64_t)(b * Qtot + q0 + r0) * ldq + h * D);
-    const uint32_t* q1p = reinterpret_cast<const uint32_t*>(qkv + (int64_t)(b * Qtot + q0 + r1) * ldq + h * D);
+    const bool v0 = g < Q, v1 = g + 8 < Q;
+    const uint32_t* q0p = reinterpret_cast<const uint32_t*>(
+        qkv + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldq + (h * G + fr0 % G) * D);
+    const uint32_t* q1p = reinterpret_cast<const uint32_t*>(
+        qkv + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldq + (h * G + fr1 % G) * D);
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
       const int w = c * 8 + t4;  // 32-bit word: dims 2*t4 .. 2*t4+1 of chunk c
-      qa[c][0] = r0 < Q ? q0p[w] : 0u;      // (row g,   k 2t..2t+1)
-      qa[c][1] = r1 < Q ? q1p[w] : 0u;      // (row g+8, k 2t..2t+1)
-      qa[c][2] = r0 < Q ? q0p[w + 4] : 0u;  // (row g,   k 2t+8..)
-      qa[c][3] = r1 < Q ? q1p[w + 4] : 0u;  // (row g+8, k 2t+8..)
+      qa[c][0] = v0 ? q0p[w] : 0u;      // (row g,   k 2t..2t+1)
+      qa[c][1] = v1 ? q1p[w] : 0u;      // (row g+8, k 2t..2t+1)
+      qa[c][2] = v0 ? q0p[w + 4] : 0u;  // (row g,   k 2t+8..)
+      qa[c][3] = v1 ? q1p[w + 4] : 0u;  // (row g+8, k 2t+8..)
+    }
+    if (rope) {
+      // fragment word u of chunk c holds dims c*16 + (u >= 2 ? 8 : 0) + 2*t4 (+1)
+      // of row g (u even) / g+8 (u odd); its partner is chunk c + KC/2
+      const float2* cs0 = rope + (int64_t)(v0 ? pos0 : 0) * (D / 2);
+      const float2* cs1 = rope + (int64_t)(v1 ? pos1 : 0) * (D / 2);
+#pragma unroll
+      for (int c = 0; c < KC / 2; ++c) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2* cs = (u & 1) ? cs1 : cs0;
+          const int d = c * 16 + (u >= 2 ? 8 : 0) + 2 * t4;
+          const float2 c0 = cs[d], c1 = cs[d + 1];
+          const uint32_t lo = qa[c][u], hi = qa[c + KC / 2][u];
+          qa[c][u] = rope_pair_lo(lo, hi, c0, c1);
+          qa[c + KC / 2][u] = rope_pair_hi(hi, lo, c0, c1);
+        }
+      }
     }
   }
 
-  const int n_keys = min(p0 + Q, T);  // keys 0 .. p0+Q-1
+  const int last_pos = pstart + (q0 + Q - 1) / G;
+  const int n_keys = min(last_pos + 1, T);  // keys 0 .. last position of the chunk
   const int n_tiles_all = (n_keys + kKT - 1) / kKT;
   // split-KV: this CTA owns tiles [tile0, tile1) — fixed 64*kct-key chunks
   // from position 0, so a query's partition never depends on the other rows
@@ -141,13 +195,13 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
 
   // tile loader: thread -> fixed 16-byte column chunk `lc` and rows lr0 + p*LRS
   // (no per-element index arithmetic); the call's own rows (t >= pstart) come
-  // straight from qkv, older keys from the cache
-  constexpr int V8 = D / 8;
+  // straight from qkv (K rotated on the way when RoPE), older keys from the cache
   constexpr int LRS = kAThreads / V8;  // rows per pass
   constexpr int LNP = kKT / LRS;       // passes per tile
   const int lc = tid % V8, lr0 = tid / V8;
-  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + HD + h * D + lc * 8;
-  const __nv_bfloat16* qkv_v = qkv_k + HD;
+  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
+  const __nv_bfloat16* qkv_v = qkv_k + KVD;
+  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;  // RoPE partner chunk
   auto load_tile = [&](int tile, int buf) {
     const int t0 = tile * kKT;
     __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
@@ -159,7 +213,15 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       if (t < n_keys) {
         const bool fresh = fuse_append && t >= pstart;
         const int64_t qrow = (int64_t)(t - pstart) * ldq;
-        cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+        if (fresh && rope) {
+          float fv[8], pf[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
+          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
+          *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
+        } else {
+          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+        }
         cp_async16(dv + j * LD, fresh ? qkv_v + qrow : V + (int64_t)t * D + lc * 8);
       } else {  // masked keys must be finite
         *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
@@ -174,8 +236,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   float o[NT][4];
 #pragma unroll
   for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  const int row_lim0 = g < Q ? p0 + g : -1;      // last key position row g may see
-  const int row_lim1 = g + 8 < Q ? p0 + g + 8 : -1;
+  const int row_lim0 = g < Q ? pos0 : -1;      // last key position row g may see
+  const int row_lim1 = g + 8 < Q ? pos1 : -1;
 
   if (n_tiles > tile0) load_tile(tile0, 0);
   for (int tile = tile0; tile < n_tiles; ++tile) {
@@ -311,12 +373,13 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
         L += sl[w * 16 + i] * f;
         A += so[(w * 16 + i) * D + dd] * f;
       }
-      out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + dd] = f2bf(A / L);
+      const int fr = q0 + i;
+      out[(int64_t)(b * Qtot + fr / G) * ldo + (h * G + fr % G) * D + dd] = f2bf(A / L);
     }
     return;
   }
   constexpr int PS = 16 * (D + 2);  // partial record: m[16], L[16], O[16][D]
-  const int64_t unit = ((int64_t)b * H + h) * nqc + qc;
+  const int64_t unit = ((int64_t)b * Hkv + h) * nqc + qc;
   float* rec = ws + (unit * n_kv + kvc) * PS;
   for (int e = tid; e < 16 * D; e += kAThreads) {
     const int i = e / D, dd = e - i * D;
@@ -361,7 +424,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       L += wgt;
       A += wgt * __ldcg(recs + cc * PS + 32 + e);
     }
-    out[(int64_t)(b * Qtot + q0 + i) * ldo + h * D + (e - i * D)] = f2bf(A / L);
+    const int fr = q0 + i;
+    out[(int64_t)(b * Qtot + fr / G) * ldo + (h * G + fr % G) * D + (e - i * D)] = f2bf(A / L);
   }
 }
 
@@ -370,9 +434,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
 constexpr int kKvChunkTiles = 2;
 
 template <int D>
-static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, const int32_t* slot,
-                       const int32_t* start, int T, void* kc, void* vc, float scale, int fuse,
-                       void* out, int64_t ldo, float* ws, int64_t ws_bytes, int* counters,
+static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, const int32_t* slot,
+                       const int32_t* start, int T, void* kc, void* vc, const float2* rope, float scale,
+                       int fuse, void* out, int64_t ldo, float* ws, int64_t ws_bytes, int* counters,
                        int n_counters, cudaStream_t st) {
   using S = AttnSmem<D>;
   static bool attr = false;
@@ -383,25 +447,26 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, const 
     attr = true;
   }
   const float scale_log2 = scale * 1.4426950408889634f;
-  const int nqc = (Q + 15) / 16;
+  const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
   if (ws) {
     kct = kKvChunkTiles;
     n_kv = ((T + kKT - 1) / kKT + kct - 1) / kct;
-    const int64_t need = (int64_t)B * H * nqc * n_kv * 16 * (D + 2) * 4;
-    if (ws_bytes < need || n_counters < B * H * nqc) return MS_ERR_VALUE;
+    const int64_t need = (int64_t)B * Hkv * nqc * n_kv * 16 * (D + 2) * 4;
+    if (ws_bytes < need || n_counters < B * Hkv * nqc) return MS_ERR_VALUE;
   }
-  dim3 grid(B, H, nqc * n_kv);
+  dim3 grid(B, Hkv, nqc * n_kv);
   return launch(attention_kernel<D>, grid, dim3(kAThreads), S::BYTES, st, 1,
-                (const __nv_bfloat16*)qkv, ldq, Q, H, slot, start, T, (__nv_bfloat16*)kc,
-                (__nv_bfloat16*)vc, scale_log2, fuse, (__nv_bfloat16*)out, ldo, n_kv, kct, ws, counters);
+                (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
+                (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, n_kv, kct, ws,
+                counters);
 }
 
 }  // namespace ms
 
-extern "C" int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
-                            const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                            void* v_cache, void* stream);
+extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                void* v_cache, const void* rope, void* stream);
 
 extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes,
                                       int* n_counters) {
@@ -412,12 +477,13 @@ extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t
   return MS_OK;
 }
 
-extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
-                            const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                            void* v_cache, float scale, int append, void* out, int64_t ldo,
-                            void* ws, int64_t ws_bytes, int* counters, int n_counters,
-                            void* stream) {
-  if (B < 0 || Q < 1 || H < 1 || T < 1) return MS_ERR_VALUE;
+extern "C" int ms_attention_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                void* v_cache, const void* rope, float scale, int append, void* out,
+                                int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                                void* stream) {
+  if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || T < 1) return MS_ERR_VALUE;
+  if (H % Hkv) return MS_ERR_VALUE;
   if (B == 0) return MS_OK;
   if (!qkv || !slot || !start || !k_cache || !v_cache || !out) return MS_ERR_VALUE;
   if (ldq % 8) return MS_ERR_UNSUPPORTED;
@@ -425,17 +491,27 @@ extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, i
   int fuse = 0;
   if (append) {
     if (Q <= 16) {
-      fuse = 1;  // one query chunk per (request, head): append inside the kernel
+      fuse = 1;  // appended inside the kernel by the first query chunk's CTA
     } else {
-      const int s = ms_kv_append(qkv, ldq, B, Q, H, D, slot, start, T, k_cache, v_cache, stream);
+      const int s = ms_kv_append_gqa(qkv, ldq, B, Q, H, Hkv, D, slot, start, T, k_cache, v_cache, rope,
+                                     stream);
       if (s != MS_OK) return s;
     }
   }
   if (D == 64)
-    return ms::launch_attn<64>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo,
-                               (float*)ws, ws_bytes, counters, n_counters, st);
+    return ms::launch_attn<64>(qkv, ldq, B, Q, H, Hkv, slot, start, T, k_cache, v_cache, (const float2*)rope,
+                               scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st);
   if (D == 128)
-    return ms::launch_attn<128>(qkv, ldq, B, Q, H, slot, start, T, k_cache, v_cache, scale, fuse, out, ldo,
-                                (float*)ws, ws_bytes, counters, n_counters, st);
+    return ms::launch_attn<128>(qkv, ldq, B, Q, H, Hkv, slot, start, T, k_cache, v_cache, (const float2*)rope,
+                                scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st);
   return MS_ERR_UNSUPPORTED;
+}
+
+extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
+                            const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                            void* v_cache, float scale, int append, void* out, int64_t ldo,
+                            void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                            void* stream) {
+  return ms_attention_gqa(qkv, ldq, B, Q, H, H, D, slot, start, T, k_cache, v_cache, nullptr, scale, append,
+                          out, ldo, ws, ws_bytes, counters, n_counters, stream);
 }

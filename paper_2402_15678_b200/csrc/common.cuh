@@ -88,6 +88,24 @@ __device__ __forceinline__ bf16x8 pack8(const float* f) {
   return v;
 }
 
+// Rotary position embedding, rotate-half pairing (dim i <-> i + D/2, the
+// Llama convention): for i < D/2, with (c, s) = rope[pos][i],
+//   y[i] = x[i] c - x[i + D/2] s,   y[i + D/2] = x[i + D/2] c + x[i] s.
+// Rotates the 8 dims [dim0, dim0 + 8) of one head in place; `pf` holds the
+// partner dims (dim0 +- D/2), `cs` the table row of the position (fp32).
+__device__ __forceinline__ void rope8(float* f, const float* pf, const float2* __restrict__ cs, int dim0,
+                                      int half) {
+  const bool lo = dim0 < half;
+  const int i0 = lo ? dim0 : dim0 - half;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 t = cs[i0 + j];
+    f[j] = lo ? f[j] * t.x - pf[j] * t.y : f[j] * t.x + pf[j] * t.y;
+  }
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -3,6 +3,10 @@
 //
 //   out[M, N] = epi( X[M, K] · W[N, K]^T )      X: tokens (bf16), W: nn.Linear weight (bf16)
 //   epi(v)    = act(v + bias[n]) + residual[m, n]   -> bf16 or fp32
+//   act 2 (gated SiLU, Llama's SwiGLU MLP): W = the gate and up projections
+//   interleaved in 64-row blocks (rows 128t..128t+63 = gate rows 64t.., rows
+//   128t+64.. = up rows 64t..), out[m, 64t + j] = silu(g) * u in fp32, one
+//   bf16 rounding — the [M, 2F] gate/up activations never reach HBM.
 //
 // Decode/verify GEMMs have few token rows (M = B·(s+1) = 16..~300) against
 // multi-GB weights: they are HBM-bound weight streams.  Layout "swap-AB": the
@@ -36,7 +40,7 @@ struct LinearParams {
   void* out;                      // [M, ldc] bf16 or fp32
   int64_t ldc;
   int out_f32;
-  int act;                        // 0 none, 1 relu
+  int act;                        // 0 none, 1 relu, 2 gated SiLU (interleaved gate/up)
   int splits;
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
@@ -270,7 +274,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 
-    if (p.splits == 1) {
+    if (p.splits == 1 && p.act != 2) {
       for (int c0 = 0; c0 < m_hi; c0 += 16) {
         uint32_t r[16];
         tc::tmem_ld16(trow + c0, r);
@@ -294,32 +298,53 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       }
     }
   }
-  if (p.splits > 1) {
+  if (p.splits > 1 || p.act == 2) {
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
     // `split` reduces a 1/splits slice of the tile, adding the partials of
     // ranks 0..splits-1 in rank order (deterministic), then runs the epilogue.
-    cluster_sync_all();
+    // Gated SiLU: a unit covers gate features f4..f4+3 and their up partners
+    // f4+64.. of the same (staged) tile.
+    const bool cl = p.splits > 1;
+    if (cl) cluster_sync_all(); else __syncthreads();
     const int m_hi = min(BN, p.M - m0);
-    const int units = m_hi * (kBM / 4);  // float4 units of the [m_hi, 128] tile
+    const bool gated = p.act == 2;
+    const int upr = (gated ? kBM / 2 : kBM) / 4;  // float4 units per token row
+    const int units = m_hi * upr;
     const int u0 = (int)((int64_t)split * units / p.splits);
     const int u1 = (int)((int64_t)(split + 1) * units / p.splits);
     const float* P = reinterpret_cast<const float*>(smem);
+    auto ld4 = [&](const float* a, int rk) {
+      return cl ? ld_dsmem_f4(a, rk) : *reinterpret_cast<const float4*>(a);
+    };
     for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
-      const int j = u / (kBM / 4);
-      const int f4 = (u - j * (kBM / 4)) * 4;
-      float4 acc = ld_dsmem_f4(P + j * kBM + f4, 0);
+      const int j = u / upr;
+      const int f4 = (u - j * upr) * 4;
+      float4 acc = ld4(P + j * kBM + f4, 0);
       for (int rk = 1; rk < p.splits; ++rk) {
-        const float4 v = ld_dsmem_f4(P + j * kBM + f4, rk);
+        const float4 v = ld4(P + j * kBM + f4, rk);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-      const int feat = n0 + f4;
       const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      if (gated) {
+        float4 up = ld4(P + j * kBM + f4 + kBM / 2, 0);
+        for (int rk = 1; rk < p.splits; ++rk) {
+          const float4 v = ld4(P + j * kBM + f4 + kBM / 2, rk);
+          up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
+        }
+        const float u4[4] = {up.x, up.y, up.z, up.w};
+        const int of = tile_n * (kBM / 2) + f4;  // output feature
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(m0 + j) * p.ldc + of;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
+        continue;
+      }
+      const int feat = n0 + f4;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (feat + t < p.N) epi_store(p, m0 + j, feat + t, a4[t]);
     }
-    cluster_sync_all();  // peers may still be reading this CTA's smem
+    if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -666,9 +691,11 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
                        int* counters, int n_counters, const void* g_ln_g, const void* g_ln_b,
                        float g_ln_eps, void* stream) {
   using namespace ms;
-  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < N) return MS_ERR_VALUE;
+  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
   if (!x || !w || !out) return MS_ERR_VALUE;
+  if (act < 0 || act > 2) return MS_ERR_VALUE;
+  if (act == 2 && (N % kBM || bias || residual || out_f32)) return MS_ERR_UNSUPPORTED;
   if (K % 8 != 0 || ldx % 8 != 0) return MS_ERR_UNSUPPORTED;  // TMA: 16-byte row strides
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
@@ -697,7 +724,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   cudaStream_t st = (cudaStream_t)stream;
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
-  if (splits == 0 && m_tiles == 1 && ws && counters &&
+  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 &&
       ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
     SKParams sk;
     sk.iters = n_tiles * kb_total;

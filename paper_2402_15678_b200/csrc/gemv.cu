@@ -16,6 +16,10 @@
 // steps.  The reduction order is fixed, so results are deterministic and a
 // row's result does not depend on M.  Weight loads for the first chunks are
 // issued before griddepcontrol.wait (PDL), like the tcgen05 path.
+//
+// act 2 (gated SiLU over the 64-row interleaved gate/up weight of ms_linear):
+// a CTA computes 8 gate rows and their 8 up partners (+64) and writes the 8
+// outputs silu(g) * u.
 #include "common.cuh"
 
 namespace ms {
@@ -40,12 +44,15 @@ gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat1
   __shared__ float red[kGvWarps][MT * 16][kGvN + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int n0 = blockIdx.x * kGvN;
+  const bool gated = act == 2;
+  // gated: outputs o0..o0+7, gate rows (o0 / 64) * 128 + o0 % 64 + [0, 8), up rows +64
+  const int o0 = blockIdx.x * (kGvN / 2);
+  const int n0 = gated ? (o0 / 64) * 128 + o0 % 64 : blockIdx.x * kGvN;
   // this warp's K range, in 32-element chunks
   const int nch = K / 32;
   const int c0 = warp * nch / kGvWarps, c1 = (warp + 1) * nch / kGvWarps;
   // weight rows of the two n8 tiles (clamped: rows >= N are computed, not stored)
-  const int wr0 = min(n0 + g, N - 1), wr1 = min(n0 + 8 + g, N - 1);
+  const int wr0 = min(n0 + g, N - 1), wr1 = min(n0 + (gated ? 64 : 8) + g, N - 1);
   const uint4* w0 = reinterpret_cast<const uint4*>(w + (int64_t)wr0 * K) + t;
   const uint4* w1 = reinterpret_cast<const uint4*>(w + (int64_t)wr1 * K) + t;
 
@@ -113,6 +120,19 @@ gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat1
       red[warp][m * 16 + g + 8][n * 8 + 2 * t + 1] = acc[m][n][3];
     }
   __syncthreads();
+  if (gated) {
+    for (int e = threadIdx.x; e < M * 8; e += kGvWarps * 32) {
+      const int r = e >> 3, f = e & 7;
+      float gv = red[0][r][f], uv = red[0][r][8 + f];
+#pragma unroll
+      for (int wi = 1; wi < kGvWarps; ++wi) {
+        gv += red[wi][r][f];
+        uv += red[wi][r][8 + f];
+      }
+      reinterpret_cast<__nv_bfloat16*>(out)[(int64_t)r * ldc + o0 + f] = f2bf(silu_mul(gv, uv));
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < M * kGvN; e += kGvWarps * 32) {
     const int r = e / kGvN, f = e - r * kGvN;
     const int feat = n0 + f;
@@ -135,9 +155,11 @@ gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat1
 extern "C" int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                        int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                        void* stream) {
-  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < N) return MS_ERR_VALUE;
+  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
   if (!x || !w || !out) return MS_ERR_VALUE;
+  if (act < 0 || act > 2) return MS_ERR_VALUE;
+  if (act == 2 && (N % 128 || bias || residual || out_f32)) return MS_ERR_UNSUPPORTED;
   if (M > 64 || K % 32 || ldx % 8) return MS_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;

@@ -43,10 +43,12 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __r
 }
 
 // ---------------------------------------------------------------------------
-// LayerNorm over d (fp32 statistics, two-pass on registers), bf16 out.
-// One CTA of 128 threads per row; each thread holds d/1024 16-byte vectors.
+// LayerNorm over d (fp32 statistics, two-pass on registers), bf16 out; with
+// RMS = true the Llama RMSNorm y = x * rsqrt(mean(x^2) + eps) * g (no mean,
+// no bias).  One CTA of 128 threads per row; each thread holds d/1024 16-byte
+// vectors.
 // ---------------------------------------------------------------------------
-template <int VPT>  // bf16x8 vectors per thread
+template <int VPT, bool RMS = false>  // bf16x8 vectors per thread
 __global__ void __launch_bounds__(128)
 layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, float eps,
@@ -69,6 +71,7 @@ layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t
   }
   __shared__ float red[4];
   __shared__ float stat;
+  if (RMS) s = 0.f;  // no centring
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -82,7 +85,7 @@ layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t
     if (i < nv) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float c = v[k][j] - mean;
+        const float c = RMS ? v[k][j] : v[k][j] - mean;
         q += c * c;
       }
     }
@@ -103,35 +106,53 @@ layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t
     if (i < nv) {
       float fg[8], fb[8], y[8];
       unpack8(gv[i], fg);
-      unpack8(bv[i], fb);
+      if (RMS) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) y[j] = (v[k][j] - mean) * rstd * fg[j] + fb[j];
+        for (int j = 0; j < 8; ++j) y[j] = v[k][j] * rstd * fg[j];
+      } else {
+        unpack8(bv[i], fb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y[j] = (v[k][j] - mean) * rstd * fg[j] + fb[j];
+      }
       o[i] = pack8(y);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// KV append: rows r = b*Q + i of qkv [R, 3*H*D] -> cache[slot[b], h, start[b]+i, :]
-// cache layout [slots, H, T, D] bf16 (K and V separate).
+// KV append: rows r = b*Q + i of qkv [R, (H + 2*Hkv)*D] (Q | K | V column
+// blocks) -> cache[slot[b], hk, start[b]+i, :], cache layout [slots, Hkv, T, D]
+// bf16 (K and V separate).  With a RoPE table the K rows are rotated at their
+// absolute position first (fp32, one bf16 rounding).
 // ---------------------------------------------------------------------------
-__global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Q, int H, int D,
-                                 const int32_t* __restrict__ slot, const int32_t* __restrict__ start,
-                                 int T, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc) {
+__global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Q, int H, int Hkv,
+                                 int D, const int32_t* __restrict__ slot, const int32_t* __restrict__ start,
+                                 int T, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                                 const float2* __restrict__ rope) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   const int b = r / Q, i = r - b * Q;
   const int p = start[b] + i;
   if (p < 0 || p >= T) return;
-  const int hd8 = H * D / 8;
-  const bf16x8* src = reinterpret_cast<const bf16x8*>(qkv + (int64_t)r * ldq);
-  const int64_t sb = (int64_t)slot[b] * H;
+  const int hd8 = Hkv * D / 8;
+  const bf16x8* src = reinterpret_cast<const bf16x8*>(qkv + (int64_t)r * ldq + (int64_t)H * D);  // skip Q
+  const int64_t sb = (int64_t)slot[b] * Hkv;
+  const int v8 = D / 8;
   for (int e = threadIdx.x; e < 2 * hd8; e += blockDim.x) {
     const int kv = e >= hd8;
     const int f = (e - kv * hd8) * 8;  // feature within K (or V)
     const int h = f / D, dd = f - h * D;
-    bf16x8 val = src[hd8 + e];  // skip Q
+    bf16x8 val = src[e];
+    if (!kv && rope) {
+      const int c = dd / 8;
+      const int pc = c < v8 / 2 ? c + v8 / 2 : c - v8 / 2;
+      float fv[8], pf[8];
+      unpack8(val, fv);
+      unpack8(src[h * v8 + pc], pf);
+      rope8(fv, pf, rope + (int64_t)p * (D / 2), dd, D / 2);
+      val = pack8(fv);
+    }
     __nv_bfloat16* dst = (kv ? vc : kc) + ((sb + h) * T + p) * D + dd;
     *reinterpret_cast<bf16x8*>(dst) = val;
   }
@@ -150,13 +171,13 @@ extern "C" int ms_embed(const int32_t* tok, const int32_t* start, int Q, const v
                     (__nv_bfloat16*)out);
 }
 
-extern "C" int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,
-                            const void* beta, float eps, int R, int d, void* out, int64_t ldo,
-                            void* stream) {
+template <bool RMS>
+static int norm_launch(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, const void* beta,
+                       float eps, int R, int d, void* out, int64_t ldo, void* stream) {
   if (R < 0 || d < 8) return MS_ERR_VALUE;
   if (d % 8 || d > 8 * 128 * 8 || ldx % 8 || ldo % 8) return MS_ERR_UNSUPPORTED;
   if (R == 0) return MS_OK;
-  if (!x || !gamma || !beta || !out) return MS_ERR_VALUE;
+  if (!x || !gamma || (!RMS && !beta) || !out) return MS_ERR_VALUE;
   const int vpt = (d / 8 + 127) / 128;
   cudaStream_t st = (cudaStream_t)stream;
   auto* xi = (const __nv_bfloat16*)x;
@@ -164,25 +185,43 @@ extern "C" int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, con
   auto* b = (const __nv_bfloat16*)beta;
   auto* o = (__nv_bfloat16*)out;
   switch (vpt) {
-    case 1: return ms::launch(ms::layernorm_kernel<1>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 2: return ms::launch(ms::layernorm_kernel<2>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 3: return ms::launch(ms::layernorm_kernel<3>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 4: return ms::launch(ms::layernorm_kernel<4>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 5: return ms::launch(ms::layernorm_kernel<5>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 6: return ms::launch(ms::layernorm_kernel<6>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 7: return ms::launch(ms::layernorm_kernel<7>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    default: return ms::launch(ms::layernorm_kernel<8>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 1: return ms::launch(ms::layernorm_kernel<1, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 2: return ms::launch(ms::layernorm_kernel<2, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 3: return ms::launch(ms::layernorm_kernel<3, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 4: return ms::launch(ms::layernorm_kernel<4, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 5: return ms::launch(ms::layernorm_kernel<5, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 6: return ms::launch(ms::layernorm_kernel<6, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 7: return ms::launch(ms::layernorm_kernel<7, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    default: return ms::launch(ms::layernorm_kernel<8, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
   }
+}
+
+extern "C" int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,
+                            const void* beta, float eps, int R, int d, void* out, int64_t ldo,
+                            void* stream) {
+  return norm_launch<false>(x, ldx, rows, gamma, beta, eps, R, d, out, ldo, stream);
+}
+
+extern "C" int ms_rmsnorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, float eps,
+                          int R, int d, void* out, int64_t ldo, void* stream) {
+  return norm_launch<true>(x, ldx, rows, gamma, nullptr, eps, R, d, out, ldo, stream);
+}
+
+extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                void* v_cache, const void* rope, void* stream) {
+  if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || D < 8 || T < 1) return MS_ERR_VALUE;
+  if (H % Hkv) return MS_ERR_VALUE;
+  if (D % 8 || ldq % 8 || (rope && D % 16)) return MS_ERR_UNSUPPORTED;
+  if (B == 0) return MS_OK;
+  if (!qkv || !slot || !start || !k_cache || !v_cache) return MS_ERR_VALUE;
+  return ms::launch(ms::kv_append_kernel, dim3(B * Q), dim3(128), 0, (cudaStream_t)stream, 1,
+                    (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, D, slot, start, T, (__nv_bfloat16*)k_cache,
+                    (__nv_bfloat16*)v_cache, (const float2*)rope);
 }
 
 extern "C" int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
                             const int32_t* slot, const int32_t* start, int T, void* k_cache,
                             void* v_cache, void* stream) {
-  if (B < 0 || Q < 1 || H < 1 || D < 8 || T < 1) return MS_ERR_VALUE;
-  if (D % 8 || ldq % 8) return MS_ERR_UNSUPPORTED;
-  if (B == 0) return MS_OK;
-  if (!qkv || !slot || !start || !k_cache || !v_cache) return MS_ERR_VALUE;
-  return ms::launch(ms::kv_append_kernel, dim3(B * Q), dim3(128), 0, (cudaStream_t)stream, 1,
-                    (const __nv_bfloat16*)qkv, ldq, Q, H, D, slot, start, T, (__nv_bfloat16*)k_cache,
-                    (__nv_bfloat16*)v_cache);
+  return ms_kv_append_gqa(qkv, ldq, B, Q, H, H, D, slot, start, T, k_cache, v_cache, nullptr, stream);
 }

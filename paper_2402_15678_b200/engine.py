@@ -47,7 +47,8 @@ import torch
 from . import _dev
 from . import _native
 from .core import AggSpecError, EngineConfig, Request, RequestState, validate_config
-from .opt import KVCache, OPTModel, OPTWeights
+from .models import make_model
+from .opt import KVCache
 from .selector import Decision, MonitorSample, SelectorState, maybe_adjust, observe
 from .verification import AcceptOut
 from .voting import WeightTable, record_acr, update_weights
@@ -169,7 +170,7 @@ class _Group:
 class SpecEngine:
     """Greedy speculative decoding with K voting drafters on one GPU."""
 
-    def __init__(self, target: OPTWeights, drafters: list[OPTWeights], cfg: EngineConfig,
+    def __init__(self, target, drafters: list, cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
                  record: bool = False, pipelined: bool = False):
@@ -192,8 +193,8 @@ class SpecEngine:
             raise ValueError("drafters and target must share a vocabulary")
         self.V = V
         s_cap = cfg.s_max
-        self.target = OPTModel(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
-        self.ssms = [OPTModel(w, max_rows=slots * max_len, device=device, small_gemm=True) for w in drafters]
+        self.target = make_model(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
+        self.ssms = [make_model(w, max_rows=slots * max_len, device=device, small_gemm=True) for w in drafters]
         self.t_cache = KVCache(target.cfg, slots, max_len, device)
         self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
         ng = 2 if pipelined else 1

@@ -48,17 +48,19 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
            stream=None) -> torch.Tensor:
     """out = act(x @ w.T + bias) + residual on tcgen05 (ms_linear).  With a
     Workspace and splits=0 the persistent stream-K schedule is used for
-    M <= 256; otherwise the cluster split-K schedule."""
+    M <= 256; otherwise the cluster split-K schedule.  act=2: gated SiLU over
+    a 64-row interleaved gate/up weight, out [M, N/2]."""
     if x.dim() != 2 or w.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
         raise ValueError("x [M, K] and w [N, K] must be 2-D bf16")
     M, K = x.shape
     N = w.shape[0]
     if w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
         raise ValueError("shape/stride mismatch")
+    No = N // 2 if act == 2 else N
     if out is None:
-        out = torch.empty((M, N), dtype=torch.float32 if out_f32 else BF16, device=x.device)
-    if out.stride(1) != 1 or out.shape != (M, N):
-        raise ValueError("out must be [M, N] with unit column stride")
+        out = torch.empty((M, No), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    if out.stride(1) != 1 or out.shape != (M, No):
+        raise ValueError(f"out must be [M, {No}] with unit column stride")
     if residual is not None and (residual.shape != (M, N) or residual.stride(1) != 1):
         raise ValueError("residual must be [M, N]")
     _native.call("ms_linear", x.data_ptr(), x.stride(0), w.data_ptr(),
@@ -81,7 +83,8 @@ def gemv(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     if x.dtype != BF16 or w.dtype != BF16 or w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
         raise ValueError("x [M, K] and w [N, K] must be bf16 with unit column stride")
     if out is None:
-        out = torch.empty((M, N), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+        out = torch.empty((M, N // 2 if act == 2 else N), dtype=torch.float32 if out_f32 else BF16,
+                          device=x.device)
     _native.call("ms_gemv", x.data_ptr(), x.stride(0), w.data_ptr(),
                  None if bias is None else _dev.ptr(bias, BF16, "bias"),
                  None if residual is None else residual.data_ptr(),
@@ -139,6 +142,27 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
     return out
 
 
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float = 1e-5, out: torch.Tensor | None = None,
+            rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """RMSNorm of x's rows (or of x[rows]) — Llama's pre-norm."""
+    d = x.shape[1]
+    R = x.shape[0] if rows is None else rows.numel()
+    out = out if out is not None else torch.empty((R, d), dtype=BF16, device=x.device)
+    _native.call("ms_rmsnorm", x.data_ptr(), x.stride(0), _dev.ptr(rows, torch.int32, "rows"),
+                 _dev.ptr(gamma, BF16), eps, R, d, out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
+    return out
+
+
+def rope_table(max_pos: int, head_dim: int, theta: float = 10000.0, device="cuda") -> torch.Tensor:
+    """(cos, sin) of p * theta^(-2i/D), i < D/2, as fp32 [max_pos, D/2, 2]
+    (computed in fp64 on the host, rounded once)."""
+    import numpy as np
+    inv = theta ** (-np.arange(0, head_dim, 2, dtype=np.float64) / head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    t = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+    return torch.from_numpy(t).to(device)
+
+
 def kv_append(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, stream=None) -> None:
     T = k_cache.shape[2]
@@ -163,14 +187,22 @@ class AttnWorkspace:
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
               out: torch.Tensor | None = None, append: bool = True, ws: AttnWorkspace | None = None,
-              stream=None) -> torch.Tensor:
+              stream=None, n_kv_heads: int | None = None, rope: torch.Tensor | None = None) -> torch.Tensor:
     """Causal KV-cache attention of Q rows per request (K/V append fused when
-    append; split-KV over fixed 128-key chunks when a workspace is given)."""
+    append; split-KV over fixed 128-key chunks when a workspace is given).
+    n_kv_heads < H: grouped-query attention (qkv = [q H*D | k Hkv*D | v Hkv*D],
+    caches [slots, Hkv, T, D]); rope: the fp32 (cos, sin) table of rope_table."""
     T = k_cache.shape[2]
+    Hkv = H if n_kv_heads is None else n_kv_heads
+    if k_cache.shape[1] != Hkv:
+        raise ValueError("cache heads != n_kv_heads")
+    if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < T or rope.shape[1] * 2 != D):
+        raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
-    _native.call("ms_attention", qkv.data_ptr(), qkv.stride(0), B, Q, H, D,
+    _native.call("ms_attention_gqa", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
-                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), scale, int(append),
+                 _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16),
+                 None if rope is None else rope.data_ptr(), scale, int(append),
                  out.data_ptr(), out.stride(0),
                  None if ws is None else ws.ws.data_ptr(), 0 if ws is None else ws.ws.numel() * 4,
                  None if ws is None else ws.counters.data_ptr(), 0 if ws is None else ws.counters.numel(),

@@ -1,0 +1,188 @@
+"""Llama-2-style decoder (pre-RMSNorm, rotary positions, grouped-query
+attention, SwiGLU MLP, untied LM head) on the libminions kernels — the model
+family BASELINE.json's headline metric names: Llama-2-70B as the verifier and
+Llama-160M drafters (cfg3), Llama-2-13B (cfg5).
+
+As for opt.py, the reference has no model: this is the compute behind
+ModelOracle.next_dist (aggspec/oracles.py:19-26), called per draft position by
+draft_sequence (aggspec/oracles.py:135-153) and for the s+1 verify positions by
+_do_verify_batch (aggspec/engine.py:294-296), batched over requests and
+positions against a KV cache.
+
+Memory layout (HBM):
+  weights    bf16 [out, in]; w_qkv [(H + 2 Hkv) D, d] (q | k | v rows);
+             w_gu [2F, d] = gate and up rows interleaved in 64-row blocks
+             (rows 128t..128t+63 = gate 64t.., rows 128t+64.. = up 64t..), so
+             the SwiGLU product is the epilogue of one GEMM (ms_linear act=2)
+  rope       fp32 (cos, sin) table [max_pos, D/2, 2]
+  KV cache   per layer K and V [slots, Hkv, T, D] bf16, K stored rotated
+  activations x [B*Q, d] bf16 residual stream, updated in place by the
+             O-proj / down-proj epilogues (residual add fused)
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import kernels as K
+from .opt import KVCache  # noqa: F401  (shared cache layout)
+
+BF16 = torch.bfloat16
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    name: str
+    n_layers: int
+    d: int
+    n_heads: int
+    n_kv_heads: int
+    ffn: int
+    vocab: int = 32000
+    max_pos: int = 4096
+    eps: float = 1e-5
+    rope_theta: float = 10000.0
+
+    family = "llama"
+
+    @property
+    def head_dim(self) -> int:
+        return self.d // self.n_heads
+
+    @property
+    def qkv_out(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    def matmul_params(self) -> int:
+        """Parameters streamed per forward (layers + LM head)."""
+        per_layer = self.d * self.qkv_out + self.d * self.d + 3 * self.d * self.ffn
+        return self.n_layers * per_layer + self.vocab * self.d
+
+    def kv_bytes_per_token(self) -> int:
+        return self.n_layers * 2 * self.n_kv_heads * self.head_dim * 2
+
+
+CONFIGS = {
+    "llama-2-70b": LlamaConfig("llama-2-70b", 80, 8192, 64, 8, 28672),
+    "llama-2-13b": LlamaConfig("llama-2-13b", 40, 5120, 40, 40, 13824),
+    "llama-160m": LlamaConfig("llama-160m", 12, 768, 12, 12, 3072, max_pos=2048, eps=1e-6),
+    # test-sized Llama shapes (GQA 2:1, D = 64)
+    "tiny-llama": LlamaConfig("tiny-llama", 4, 256, 4, 2, 512, max_pos=1024),
+    "tiny-llama-ssm": LlamaConfig("tiny-llama-ssm", 1, 256, 4, 4, 512, max_pos=1024),
+}
+
+
+def gate_up_rows(ffn: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Row indices of the gate and up projections inside the interleaved w_gu."""
+    j = torch.arange(ffn)
+    gate = (j // 64) * 128 + j % 64
+    return gate, gate + 64
+
+
+class LlamaWeights:
+    """Random-init weights (normal(0, 0.02) for Linear/Embedding — the HF
+    initializer_range —, unit RMSNorm gains), seeded torch.Generator on `device`."""
+
+    def __init__(self, cfg: LlamaConfig, tensors: dict[str, torch.Tensor]):
+        self.cfg = cfg
+        self.t = tensors
+
+    @classmethod
+    def random(cls, cfg: LlamaConfig, seed: int, device="cuda", std: float = 0.02,
+               norm_std: float = 0.0) -> "LlamaWeights":
+        if cfg.ffn % 64:
+            raise ValueError("ffn must be a multiple of 64 (interleaved gate/up blocks)")
+        g = torch.Generator(device=device).manual_seed(seed)
+        dev = torch.device(device)
+
+        def normal(*shape, s=std):
+            out = torch.empty(*shape, dtype=BF16, device=dev)
+            rows = max(1, (1 << 27) // max(1, shape[-1]))  # <= 512 MB fp32 temporaries
+            flat = out.view(-1, shape[-1])
+            for r0 in range(0, flat.shape[0], rows):
+                n = min(rows, flat.shape[0] - r0)
+                flat[r0: r0 + n] = (torch.randn(n, shape[-1], generator=g, device=dev) * s).to(BF16)
+            return out
+
+        def gain(n):
+            if norm_std > 0:
+                return (1.0 + torch.randn(n, generator=g, device=dev) * norm_std).to(BF16)
+            return torch.ones(n, dtype=BF16, device=dev)
+
+        d, f = cfg.d, cfg.ffn
+        t = {"tok_emb": normal(cfg.vocab, d), "norm_f": gain(d), "lm_head": normal(cfg.vocab, d)}
+        for i in range(cfg.n_layers):
+            p = f"l{i}."
+            t[p + "attn_norm"] = gain(d)
+            t[p + "w_qkv"] = normal(cfg.qkv_out, d)
+            t[p + "w_o"] = normal(d, cfg.n_heads * cfg.head_dim)
+            t[p + "mlp_norm"] = gain(d)
+            t[p + "w_gu"] = normal(2 * f, d)
+            t[p + "w_down"] = normal(d, f)
+        return cls(cfg, t)
+
+    def to(self, device) -> "LlamaWeights":
+        return LlamaWeights(self.cfg, {k: v.to(device) for k, v in self.t.items()})
+
+    def __getitem__(self, k: str) -> torch.Tensor:
+        return self.t[k]
+
+
+class LlamaModel:
+    """Batched forward over the kernels with static activation buffers (CUDA
+    graph capturable), same interface as opt.OPTModel."""
+
+    def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False):
+        """small_gemm: projections of <= 64 token rows with K <= 1024 use the
+        low-latency ms_gemv (drafters' decode steps); the verifier keeps the
+        tcgen05 path everywhere, so its numerics never depend on the row count."""
+        self.w, self.cfg = w, w.cfg
+        self.small_gemm = small_gemm
+        c = self.cfg
+        self.device = torch.device(device)
+        self.max_rows = max_rows
+        self.x = torch.empty((max_rows, c.d), dtype=BF16, device=device)
+        self.h = torch.empty((max_rows, c.d), dtype=BF16, device=device)
+        self.qkv = torch.empty((max_rows, c.qkv_out), dtype=BF16, device=device)
+        self.attn = torch.empty((max_rows, c.n_heads * c.head_dim), dtype=BF16, device=device)
+        self.ff = torch.empty((max_rows, c.ffn), dtype=BF16, device=device)
+        self.scale = 1.0 / math.sqrt(c.head_dim)
+        self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
+        self.ws = None
+
+    def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
+                logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Run Q positions for B requests (contract of OPTModel.forward)."""
+        c, w = self.cfg, self.w
+        B, Q = tokens.shape
+        R = B * Q
+        if R > self.max_rows:
+            raise ValueError(f"{R} rows exceed max_rows={self.max_rows}")
+        if cache.max_len > c.max_pos:
+            raise ValueError("KV cache longer than the RoPE table")
+        x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
+        K.embed(tokens, start, Q, w["tok_emb"], None, 0, out=x, stream=stream)
+        small = self.small_gemm and R <= 64
+
+        def lin(xx, wname, **kw):
+            if small and xx.shape[1] <= 1024:
+                return K.gemv(xx, w[wname], stream=stream, **kw)
+            return K.linear(xx, w[wname], stream=stream, **kw)
+
+        for i in range(c.n_layers):
+            p = f"l{i}."
+            K.rmsnorm(x, w[p + "attn_norm"], c.eps, out=h, stream=stream)
+            lin(h, p + "w_qkv", out=qkv)
+            K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+            lin(at, p + "w_o", residual=x, out=x)
+            K.rmsnorm(x, w[p + "mlp_norm"], c.eps, out=h, stream=stream)
+            lin(h, p + "w_gu", act=2, out=ff)
+            lin(ff, p + "w_down", residual=x, out=x)
+        Rh = R if head_rows is None else head_rows.numel()
+        hf = self.h[:Rh]
+        K.rmsnorm(x, w["norm_f"], c.eps, out=hf, rows=head_rows, stream=stream)
+        K.linear(hf, w["lm_head"], out=logits, out_f32=True, stream=stream)
+        return logits

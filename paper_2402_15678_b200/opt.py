@@ -41,9 +41,15 @@ class OPTConfig:
     eps: float = 1e-5
     pos_offset: int = 2  # OPT's learned-position offset
 
+    family = "opt"
+
     @property
     def head_dim(self) -> int:
         return self.d // self.n_heads
+
+    @property
+    def n_kv_heads(self) -> int:
+        return self.n_heads
 
     def matmul_params(self) -> int:
         """Parameters streamed per forward (layers + tied LM head)."""
@@ -110,10 +116,11 @@ class OPTWeights:
 
 
 class KVCache:
-    """Per-layer K/V caches [slots, H, T, D] bf16."""
+    """Per-layer K/V caches [slots, Hkv, T, D] bf16 (Hkv = KV heads: the query
+    heads for OPT, the grouped KV heads for Llama-2-70B)."""
 
-    def __init__(self, cfg: OPTConfig, slots: int, max_len: int, device="cuda"):
-        shape = (slots, cfg.n_heads, max_len, cfg.head_dim)
+    def __init__(self, cfg, slots: int, max_len: int, device="cuda"):
+        shape = (slots, cfg.n_kv_heads, max_len, cfg.head_dim)
         self.k = [torch.zeros(shape, dtype=BF16, device=device) for _ in range(cfg.n_layers)]
         self.v = [torch.zeros(shape, dtype=BF16, device=device) for _ in range(cfg.n_layers)]
         self.slots, self.max_len = slots, max_len

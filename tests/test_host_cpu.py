@@ -80,3 +80,40 @@ def test_probdist_guards():
     d = core.ProbDist([0.0, 1.0])
     assert d.point_mass_token() == 1
     assert core.ProbDist([0.5, 0.5]).point_mass_token() is None
+
+
+def test_llama_rope_table_and_gate_up_layout_match_reference():
+    """Host-side Llama plumbing (no kernels): the RoPE table and the interleaved
+    gate/up row map the device path uses equal the fp32 reference's."""
+    import torch
+    from oracle import llama_ref
+    from paper_2402_15678_b200 import kernels as Kn
+    from paper_2402_15678_b200.llama import CONFIGS, gate_up_rows
+    assert torch.equal(Kn.rope_table(64, 128, 10000.0, device="cpu"), llama_ref.rope_table(64, 128, 10000.0))
+    g, u = gate_up_rows(192)
+    w = torch.arange(384).float()[:, None]
+    wg, wu = llama_ref.split_gate_up(w, 192)
+    assert torch.equal(wg[:, 0].long(), g) and torch.equal(wu[:, 0].long(), u)
+    assert sorted(torch.cat([g, u]).tolist()) == list(range(384))
+    c = CONFIGS["llama-2-70b"]
+    assert c.matmul_params() == 68_713_185_280  # 68.71 G (SURVEY §8d) incl. LM head
+    assert c.kv_bytes_per_token() == 327_680
+    assert CONFIGS["llama-2-13b"].kv_bytes_per_token() == 819_200
+
+
+def test_llama_reference_gqa_equals_mha_with_repeated_kv():
+    """oracle/llama_ref: a GQA model equals the MHA model whose K/V projection
+    rows are repeated per group (checks the reference's head mapping)."""
+    import torch
+    from oracle import llama_ref
+    from paper_2402_15678_b200.llama import LlamaConfig, LlamaWeights
+    gq = LlamaConfig("g", 1, 64, 4, 2, 128, vocab=50, max_pos=64)
+    mh = LlamaConfig("m", 1, 64, 4, 4, 128, vocab=50, max_pos=64)
+    w = LlamaWeights.random(gq, 0, device="cpu", std=0.1).t
+    D = 16
+    wq, wk, wv = w["l0.w_qkv"][:64], w["l0.w_qkv"][64:96], w["l0.w_qkv"][96:]
+    rep = lambda m: m.view(2, D, 64).repeat_interleave(2, dim=0).reshape(64, 64)  # noqa: E731
+    w2 = dict(w)
+    w2["l0.w_qkv"] = torch.cat([wq, rep(wk), rep(wv)])
+    toks = [3, 7, 1, 40, 2, 9]
+    torch.testing.assert_close(llama_ref.forward(w, gq, toks), llama_ref.forward(w2, mh, toks))
