@@ -1,11 +1,13 @@
 """Benchmark of the speculate-vote-verify hot path (BASELINE.json metric:
 output tokens/s + mean accepted length).
 
-Workload at N=1 (BASELINE.json configs[1], "cfg2"): OPT-13B target + 3 x
-OPT-125M drafters, bf16, one B200, batch 16, adaptive speculation length
+Workload at N=1: the configuration BASELINE.json's metric is quoted on —
+Llama-2-70B target + 3 x Llama-160M drafters — which fits one B200 (137.4 GB
+of bf16 weights in 180 GB): bf16, batch 16, adaptive speculation length
 (s_init 4, s in [1, 12]), greedy, 128-token synthetic prompts, 128 new tokens
-per request.  Random-init weights (no checkpoints offline); because random-init
-drafters never agree with the target, drafts use fidelity injection
+per request.  `--target opt-13b --ssm opt-125m` runs configs[1] (cfg2).
+Random-init weights (no checkpoints offline); because random-init drafters
+never agree with the target, drafts use fidelity injection
 (engine.py / DESIGN.md): with probability f_k SSM k's drafted token is
 replaced by the target's greedy continuation — every kernel still runs in
 full and the output stays exactly the target's greedy decode.
@@ -13,7 +15,7 @@ full and the output stays exactly the target's greedy decode.
 One step = one generation batch: decode of 16 requests x 128 new tokens, from
 prefilled KV caches (prompt prefill is outside the hot path) to
 the last request finishing.  `value` = generated tokens / device time of the
-decode (CUDA events, weights 25.7 GB >> L2 so no flush is needed).  `e2e` =
+decode (CUDA events, weights 137 GB >> L2 so no flush is needed).  `e2e` =
 the same metric through the public API (SpecEngine.run) from host prompt
 lists, H2D of prompts + per-round metadata and D2H of per-round results
 inside the timed region, prompt prefill included.
@@ -41,7 +43,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "output tokens/sec, Llama-2-70B + 3x160M SSMs, 1-8 B200; mean accepted length"
-WORKLOAD = "cfg2: OPT-13B target + 3x OPT-125M SSMs, bf16, 1 B200/rank, batch 16, adaptive s"
+
+
+def workload(args) -> str:
+    if args.target == "llama-2-70b":
+        return (f"cfg3 model set at TP=1: Llama-2-70B target + 3x {args.ssm} SSMs, bf16, 1 B200/rank, "
+                f"batch {args.batch}, adaptive s")
+    return f"{args.target} target + 3x {args.ssm} SSMs, bf16, 1 B200/rank, batch {args.batch}, adaptive s"
 
 
 def parse():
@@ -50,8 +58,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--target", default="opt-13b")
-    ap.add_argument("--ssm", default="opt-125m")
+    ap.add_argument("--target", default="llama-2-70b")
+    ap.add_argument("--ssm", default="llama-160m")
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--new-tokens", type=int, default=128)
@@ -152,7 +160,7 @@ def fresh(reqs):
 
 
 def roofline_verify(engine, rounds, peaks):
-    """Dominant unit: the verify forward (40 ms_linear GEMM quadruples + LM
+    """Dominant unit: the verify forward (4 ms_linear GEMMs per layer + LM
     head + attention), timed per round with CUDA events on its stream.
     Algorithmic bytes per round = 2 * matmul params (bf16 weights) + KV read
     (B * ctx * kv_bytes_per_token) + KV write (B * (s+1) * kv_bytes_per_token)."""
@@ -182,13 +190,13 @@ def run_ours(args, rank, ws):
     from paper_2402_15678_b200 import _native
     from paper_2402_15678_b200.core import EngineConfig
     from paper_2402_15678_b200.engine import SpecEngine
-    from paper_2402_15678_b200.opt import CONFIGS, OPTWeights
+    from paper_2402_15678_b200.models import config, random_weights
 
-    tcfg, scfg = CONFIGS[args.target], CONFIGS[args.ssm]
+    tcfg, scfg = config(args.target), config(args.ssm)
     fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else None
     K = 3
-    target = OPTWeights.random(tcfg, 0, device="cuda")
-    drafters = [OPTWeights.random(scfg, k + 1, device="cuda") for k in range(K)]
+    target = random_weights(tcfg, 0, device="cuda")
+    drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
     cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch,
                        s_init=args.fixed_s or 4, s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
     max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
@@ -277,11 +285,12 @@ def run_ours(args, rank, ws):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts, random-init weights, fidelity-injected drafts",
-        "config": {"workload": WORKLOAD, "target": args.target, "ssms": [args.ssm] * K,
+        "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * K,
                    "global_batch": n_req * ws, "schedule": args.schedule, "prompt_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
                    "fidelity": fid, "parallelism": "replicas" if ws > 1 else "single-gpu",
-                   "l2": "inputs larger than L2 (25.7 GB of weights streamed per verify)",
+                   "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
+                          "streamed per verify)"),
                    "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
                    "graphs": not args.no_graphs},
         "mean_accepted_length": round(float(np.mean(acc)), 4) if acc else 0.0,
@@ -311,8 +320,9 @@ def simulated_vl(args, s: int, rounds: int = 64) -> float:
 
     from oracle import aggspec_oracle as O
     fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else [0.0] * 3
+    from paper_2402_15678_b200.models import config
     rng = np.random.default_rng(0)
-    V = 50272
+    V = config(args.target).vocab
     em = []
     for _ in range(rounds * args.batch):
         tgt = rng.integers(0, V, size=s + 1)
@@ -338,26 +348,29 @@ def cpu_baseline(args, vl: float | None = None, threads: int | None = None):
     measured emitted tokens per round (vl)."""
     import torch
 
+    import dataclasses
+
     from oracle import aggspec_oracle as O
-    from oracle import opt_ref
-    from paper_2402_15678_b200.opt import CONFIGS, OPTConfig, OPTWeights
+    from oracle import llama_ref, opt_ref
+    from paper_2402_15678_b200.models import config, random_weights
 
     n_thr = threads or len(os.sched_getaffinity(0))
     torch.set_num_threads(n_thr)
-    tcfg, scfg = CONFIGS[args.target], CONFIGS[args.ssm]
+    tcfg, scfg = config(args.target), config(args.ssm)
     L = min(args.cpu_sample_layers, tcfg.n_layers)
     ctx = args.prompt_len + args.new_tokens // 2
     s = 4
     B = args.batch
     K = 3
 
-    def call_time(cfg: OPTConfig, layers: int) -> float:
-        sub = OPTConfig(cfg.name, layers, cfg.d, cfg.n_heads, cfg.ffn, cfg.vocab, cfg.max_pos)
-        w = OPTWeights.random(sub, 0, device="cpu").t
+    def call_time(cfg, layers: int) -> float:
+        sub = dataclasses.replace(cfg, n_layers=layers)
+        w = random_weights(sub, 0, device="cpu").t
+        ref = llama_ref if cfg.family == "llama" else opt_ref
         toks = list(range(ctx))
-        opt_ref.forward(w, sub, toks[:8], last_only=True)  # warm
+        ref.forward(w, sub, toks[:8], last_only=True)  # warm
         t0 = time.perf_counter()
-        opt_ref.forward(w, sub, toks, last_only=True)
+        ref.forward(w, sub, toks, last_only=True)
         t_full = time.perf_counter() - t0
         return t_full
 
@@ -398,7 +411,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "impl": "reference",
-                "config": {"workload": WORKLOAD, "target": args.target, "ssms": [args.ssm] * 3,
+                "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * 3,
                            "global_batch": args.batch},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": round(cb["value"], 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,

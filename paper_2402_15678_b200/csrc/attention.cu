@@ -70,7 +70,7 @@ struct AttnSmem {
   static constexpr int LD = D + 8;  // padded rows: fragment loads are bank-conflict free
   static constexpr int TILE = kKT * LD;                  // elements per K (or V) tile
   static constexpr int KV_BYTES = 2 * 2 * TILE * 2;      // [K|V][buf] bf16
-  static constexpr int MERGE_BYTES = 4 * 16 * (D + 2) * 4;  // per-warp (m, l, O) for the merge
+  static constexpr int MERGE_BYTES = 4 * 16 * (D + 3) * 4 + 2 * 16 * 4;  // per-warp (m, l, O, f) + row (m, L)
   static constexpr int BYTES = KV_BYTES > MERGE_BYTES ? KV_BYTES : MERGE_BYTES;
 };
 
@@ -338,9 +338,12 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
     __syncthreads();
   }
   // merge the 4 warps' (m, l, O) in warp order
-  float* sm = reinterpret_cast<float*>(smem);  // [4][16] m, [4][16] l, [4][16][D] O
+  float* sm = reinterpret_cast<float*>(smem);  // [4][16] m, [4][16] l, [4][16][D] O, [4][16] f, [16] m, [16] L
   float* sl = sm + 4 * 16;
   float* so = sl + 4 * 16;
+  float* sf = so + 4 * 16 * D;  // per-(warp, row) merge factor
+  float* rm = sf + 4 * 16;      // per-row max
+  float* rL = rm + 16;          // per-row sum
   if (t4 == 0) {
     sm[warp * 16 + g] = m_r[0];
     sm[warp * 16 + g + 8] = m_r[1];
@@ -356,25 +359,38 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
     so[(warp * 16 + g + 8) * D + c + 1] = o[n][3];
   }
   __syncthreads();
+  // per-row merge factors, once per row: f_w = exp2(m_w - m) / L (the 4 warps'
+  // softmax states combined in warp order)
+  if (tid < 16) {
+    const int i = tid;
+    float mxx = sm[i];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) mxx = fmaxf(mxx, sm[w * 16 + i]);
+    float fw[4], L = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sm[w * 16 + i];
+      fw[w] = mw == -INFINITY ? 0.f : exp2f(mw - mxx);
+      L += sl[w * 16 + i] * fw[w];
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) sf[w * 16 + i] = fw[w] * inv;
+    rm[i] = mxx;
+    rL[i] = L;
+  }
+  __syncthreads();
   // this CTA's partial: (m, L, O = A / L) per query row.  With a workspace the
   // chunk merge below runs even for a single chunk, so a query's output goes
   // through the same arithmetic whatever the other rows' key counts are.
   if (ws == nullptr) {
     for (int e = tid; e < Q * D; e += kAThreads) {
       const int i = e / D, dd = e - i * D;
-      float mxx = sm[i];
+      float A = 0.f;
 #pragma unroll
-      for (int w = 1; w < 4; ++w) mxx = fmaxf(mxx, sm[w * 16 + i]);
-      float L = 0.f, A = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float mw = sm[w * 16 + i];
-        const float f = mw == -INFINITY ? 0.f : exp2f(mw - mxx);
-        L += sl[w * 16 + i] * f;
-        A += so[(w * 16 + i) * D + dd] * f;
-      }
+      for (int w = 0; w < 4; ++w) A += so[(w * 16 + i) * D + dd] * sf[w * 16 + i];
       const int fr = q0 + i;
-      out[(int64_t)(b * Qtot + fr / G) * ldo + (h * G + fr % G) * D + dd] = f2bf(A / L);
+      out[(int64_t)(b * Qtot + fr / G) * ldo + (h * G + fr % G) * D + dd] = f2bf(A);
     }
     return;
   }
@@ -383,21 +399,13 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   float* rec = ws + (unit * n_kv + kvc) * PS;
   for (int e = tid; e < 16 * D; e += kAThreads) {
     const int i = e / D, dd = e - i * D;
-    float mxx = sm[i];
+    float A = 0.f;
 #pragma unroll
-    for (int w = 1; w < 4; ++w) mxx = fmaxf(mxx, sm[w * 16 + i]);
-    float L = 0.f, A = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = sm[w * 16 + i];
-      const float f = mw == -INFINITY ? 0.f : exp2f(mw - mxx);
-      L += sl[w * 16 + i] * f;
-      A += so[(w * 16 + i) * D + dd] * f;
-    }
-    __stcg(rec + 32 + e, L > 0.f ? A / L : 0.f);
+    for (int w = 0; w < 4; ++w) A += so[(w * 16 + i) * D + dd] * sf[w * 16 + i];
+    __stcg(rec + 32 + e, A);
     if (dd == 0) {
-      __stcg(rec + i, mxx);
-      __stcg(rec + 16 + i, L);
+      __stcg(rec + i, rm[i]);
+      __stcg(rec + 16 + i, rL[i]);
     }
   }
   __threadfence();

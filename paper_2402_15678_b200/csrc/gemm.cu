@@ -616,17 +616,11 @@ int linear_auto_splits(int N, int K) {
   return sp < 1 ? 1 : sp;
 }
 
+// Token tile = M rounded up to 16 (the MMA's N granularity), so a verify of
+// B*(s+1) rows streams no padded X rows; 256 max, larger M tiles over M.
 static int pick_bn(int M) {
-  if (M <= 16) return 16;
-  if (M <= 32) return 32;
-  if (M <= 48) return 48;
-  if (M <= 64) return 64;
-  if (M <= 80) return 80;
-  if (M <= 96) return 96;
-  if (M <= 128) return 128;
-  if (M <= 160) return 160;
-  if (M <= 192) return 192;
-  return 256;
+  if (M >= 256) return 256;
+  return M <= 16 ? 16 : (M + 15) / 16 * 16;
 }
 
 template <int BN>
@@ -645,6 +639,9 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
   // little shared memory and several kernels / streams can share an SM
   const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
   p.stages = C::stages_for(grid <= 148 ? 1 : 2);
+  // the fp32 staging tile (split-K / gated epilogue) may already rule out two
+  // CTAs per SM: then take the deep single-CTA pipeline
+  if ((p.splits > 1 || p.act == 2) && C::smem(p.stages) > 113 * 1024) p.stages = C::stages_for(1);
   if (p.stages > kb_per_cta) p.stages = kb_per_cta < 2 ? 2 : kb_per_cta;
   return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::smem(p.stages), st,
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
@@ -739,9 +736,15 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
       case 64: return launch_linear_sk<64>(tw, tx, p, sk, st);
       case 80: return launch_linear_sk<80>(tw, tx, p, sk, st);
       case 96: return launch_linear_sk<96>(tw, tx, p, sk, st);
+      case 112: return launch_linear_sk<112>(tw, tx, p, sk, st);
       case 128: return launch_linear_sk<128>(tw, tx, p, sk, st);
+      case 144: return launch_linear_sk<144>(tw, tx, p, sk, st);
       case 160: return launch_linear_sk<160>(tw, tx, p, sk, st);
+      case 176: return launch_linear_sk<176>(tw, tx, p, sk, st);
       case 192: return launch_linear_sk<192>(tw, tx, p, sk, st);
+      case 208: return launch_linear_sk<208>(tw, tx, p, sk, st);
+      case 224: return launch_linear_sk<224>(tw, tx, p, sk, st);
+      case 240: return launch_linear_sk<240>(tw, tx, p, sk, st);
       default: return launch_linear_sk<256>(tw, tx, p, sk, st);
     }
   }
@@ -756,9 +759,15 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
     case 64: return launch_linear<64>(tw, tx, p, m_tiles, st);
     case 80: return launch_linear<80>(tw, tx, p, m_tiles, st);
     case 96: return launch_linear<96>(tw, tx, p, m_tiles, st);
+    case 112: return launch_linear<112>(tw, tx, p, m_tiles, st);
     case 128: return launch_linear<128>(tw, tx, p, m_tiles, st);
+    case 144: return launch_linear<144>(tw, tx, p, m_tiles, st);
     case 160: return launch_linear<160>(tw, tx, p, m_tiles, st);
+    case 176: return launch_linear<176>(tw, tx, p, m_tiles, st);
     case 192: return launch_linear<192>(tw, tx, p, m_tiles, st);
+    case 208: return launch_linear<208>(tw, tx, p, m_tiles, st);
+    case 224: return launch_linear<224>(tw, tx, p, m_tiles, st);
+    case 240: return launch_linear<240>(tw, tx, p, m_tiles, st);
     default: return launch_linear<256>(tw, tx, p, m_tiles, st);
   }
 }
