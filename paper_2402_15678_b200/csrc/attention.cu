@@ -437,6 +437,266 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-split schedule for grouped-query attention (G = H / Hkv > 1, e.g.
+// Llama-2-70B's 8 query heads per KV head): one CTA per (request, KV head, 64
+// flattened (position, group head) rows); warp w owns rows 16w..16w+15 and
+// walks EVERY key of each 64-key tile (8 n-tiles of 8 keys), so each K/V byte
+// is staged once for all of the KV head's query rows and no cross-warp merge
+// is needed.  The schedule is chosen by G alone (never by Q), so a row's
+// arithmetic is the same in a Q=1 decode and a Q=s+1 verify (batch
+// invariance: extra fully-masked keys contribute exactly zero).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kAThreads)
+attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
+                      const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
+                      __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
+                      int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
+                      int64_t ldo) {
+  using S = AttnSmem<D>;
+  constexpr int LD = S::LD;
+  constexpr int KC = D / 16;
+  constexpr int NT = D / 8;
+  constexpr int V8 = D / 8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  pdl_wait();
+  pdl_trigger();
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem);  // [2][KT][LD]
+  __nv_bfloat16* sV = sK + 2 * S::TILE;                           // [2][KT][LD]
+
+  const int b = blockIdx.x, h = blockIdx.y;  // h: KV head
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = Hq / Hkv;
+  const int rows_tot = Qtot * G;
+  const int c0 = blockIdx.z * 64;             // first flattened row of the CTA
+  const int crows = min(64, rows_tot - c0);
+  const int q0 = c0 + warp * 16;              // first row of this warp
+  const int Q = max(0, min(16, rows_tot - q0));  // rows of this warp (0: idle)
+  const int pstart = start[b];
+  const int64_t cbase = ((int64_t)slot[b] * Hkv + h) * T * D;
+  __nv_bfloat16* K = kc + cbase;
+  __nv_bfloat16* V = vc + cbase;
+  const int QD = Hq * D, KVD = Hkv * D;
+
+  if (fuse_append && blockIdx.z == 0) {
+    for (int e = tid; e < 2 * Qtot * V8; e += kAThreads) {
+      const int kv = e >= Qtot * V8;
+      const int e2 = e - kv * Qtot * V8;
+      const int i = e2 / V8, c = e2 - i * V8;
+      const int p = pstart + i;
+      if (p < 0 || p >= T) continue;
+      const __nv_bfloat16* row = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * D;
+      bf16x8 val = *reinterpret_cast<const bf16x8*>(row + c * 8);
+      if (!kv && rope) {
+        const int pc = c < V8 / 2 ? c + V8 / 2 : c - V8 / 2;
+        float fv[8], pf[8];
+        unpack8(val, fv);
+        unpack8(*reinterpret_cast<const bf16x8*>(row + pc * 8), pf);
+        rope8(fv, pf, rope + (int64_t)p * (D / 2), c * 8, D / 2);
+        val = pack8(fv);
+      }
+      *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
+    }
+  }
+
+  const int fr0 = q0 + g, fr1 = q0 + g + 8;
+  const bool v0 = g < Q, v1 = g + 8 < Q;
+  const int pos0 = pstart + fr0 / G, pos1 = pstart + fr1 / G;
+  uint32_t qa[KC][4];
+  {
+    const uint32_t* q0p = reinterpret_cast<const uint32_t*>(
+        qkv + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldq + (h * G + (v0 ? fr0 % G : 0)) * D);
+    const uint32_t* q1p = reinterpret_cast<const uint32_t*>(
+        qkv + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldq + (h * G + (v1 ? fr1 % G : 0)) * D);
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      const int w = c * 8 + t4;
+      qa[c][0] = v0 ? q0p[w] : 0u;
+      qa[c][1] = v1 ? q1p[w] : 0u;
+      qa[c][2] = v0 ? q0p[w + 4] : 0u;
+      qa[c][3] = v1 ? q1p[w + 4] : 0u;
+    }
+    if (rope) {
+      const float2* cs0 = rope + (int64_t)(v0 ? pos0 : 0) * (D / 2);
+      const float2* cs1 = rope + (int64_t)(v1 ? pos1 : 0) * (D / 2);
+#pragma unroll
+      for (int c = 0; c < KC / 2; ++c) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2* cs = (u & 1) ? cs1 : cs0;
+          const int d = c * 16 + (u >= 2 ? 8 : 0) + 2 * t4;
+          const float2 cc0 = cs[d], cc1 = cs[d + 1];
+          const uint32_t lo = qa[c][u], hi = qa[c + KC / 2][u];
+          qa[c][u] = rope_pair_lo(lo, hi, cc0, cc1);
+          qa[c + KC / 2][u] = rope_pair_hi(hi, lo, cc0, cc1);
+        }
+      }
+    }
+  }
+
+  const int last_pos = pstart + (c0 + crows - 1) / G;
+  const int n_keys = min(last_pos + 1, T);
+  const int n_tiles = (n_keys + kKT - 1) / kKT;
+
+  constexpr int LRS = kAThreads / V8;
+  constexpr int LNP = kKT / LRS;
+  const int lc = tid % V8, lr0 = tid / V8;
+  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
+  const __nv_bfloat16* qkv_v = qkv_k + KVD;
+  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;
+  auto load_tile = [&](int tile, int buf) {
+    const int t0 = tile * kKT;
+    __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
+    __nv_bfloat16* dv = sV + buf * S::TILE + lc * 8;
+#pragma unroll
+    for (int pp = 0; pp < LNP; ++pp) {
+      const int j = lr0 + pp * LRS;
+      const int t = t0 + j;
+      if (t < n_keys) {
+        const bool fresh = fuse_append && t >= pstart;
+        const int64_t qrow = (int64_t)(t - pstart) * ldq;
+        if (fresh && rope) {
+          float fv[8], pf[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
+          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
+          *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
+        } else {
+          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+        }
+        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : V + (int64_t)t * D + lc * 8);
+      } else {
+        *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    cp_async_commit();
+  };
+
+  float m_r[2] = {-INFINITY, -INFINITY};
+  float l_r[2] = {0.f, 0.f};
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  const int row_lim0 = v0 ? pos0 : -1;
+  const int row_lim1 = v1 ? pos1 : -1;
+  const int lrow = lane & 15;
+  const int lcol = (lane >> 4) * 8;
+
+  if (n_tiles > 0) load_tile(0, 0);
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    const int buf = tile & 1;
+    if (tile + 1 < n_tiles) {
+      load_tile(tile + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (Q > 0) {  // warp-uniform
+      const __nv_bfloat16* kt = sK + buf * S::TILE;
+      const __nv_bfloat16* vt = sV + buf * S::TILE;
+      const int kbase = tile * kKT;
+      float sc[8][4];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+        const __nv_bfloat16* kr = kt + (n * 8 + g) * LD + 2 * t4;
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + c * 16);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + c * 16 + 8);
+          mma16816(sc[n], qa[c], b0, b1);
+        }
+      }
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kbase + n * 8 + 2 * t4 + (e & 1);
+          const int lim = (e < 2) ? row_lim0 : row_lim1;
+          float v = sc[n][e] * scale_log2;
+          if (key > lim || key >= n_keys) v = -INFINITY;
+          sc[n][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      }
+      float corr[2], psum[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float mn = fmaxf(m_r[r], mx[r]);
+        corr[r] = (mn == -INFINITY) ? 1.f : exp2f(m_r[r] - mn);
+        m_r[r] = mn;
+        psum[r] = 0.f;
+      }
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = e >> 1;
+          const float pv = (m_r[r] == -INFINITY || sc[n][e] == -INFINITY) ? 0.f : exp2f(sc[n][e] - m_r[r]);
+          sc[n][e] = pv;
+          psum[r] += pv;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 1);
+        psum[r] += __shfl_xor_sync(0xffffffffu, psum[r], 2);
+        l_r[r] = l_r[r] * corr[r] + psum[r];
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        o[n][0] *= corr[0];
+        o[n][1] *= corr[0];
+        o[n][2] *= corr[1];
+        o[n][3] *= corr[1];
+      }
+      // O += P V over the tile's four 16-key blocks (P split bf16 hi + lo)
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        uint32_t pa[4], pl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float x0 = sc[2 * kb + (u >> 1)][2 * (u & 1)], x1 = sc[2 * kb + (u >> 1)][2 * (u & 1) + 1];
+          const __nv_bfloat162 hi = __floats2bfloat162_rn(x0, x1);
+          const float2 hf = __bfloat1622float2(hi);
+          pa[u] = *reinterpret_cast<const uint32_t*>(&hi);
+          pl[u] = pack_bf16(x0 - hf.x, x1 - hf.y);
+        }
+#pragma unroll
+        for (int n2 = 0; n2 < NT / 2; ++n2) {
+          uint32_t vb[4];
+          ldmatrix_x4_trans(vb, vt + (kb * 16 + lrow) * LD + n2 * 16 + lcol);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            mma16816(o[2 * n2 + u], pa, vb[2 * u], vb[2 * u + 1]);
+            mma16816(o[2 * n2 + u], pl, vb[2 * u], vb[2 * u + 1]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (Q == 0) return;
+  const float inv0 = l_r[0] > 0.f ? 1.f / l_r[0] : 0.f;
+  const float inv1 = l_r[1] > 0.f ? 1.f / l_r[1] : 0.f;
+  __nv_bfloat16* o0p = out + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldo + (h * G + (v0 ? fr0 % G : 0)) * D;
+  __nv_bfloat16* o1p = out + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldo + (h * G + (v1 ? fr1 % G : 0)) * D;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int col = n * 8 + 2 * t4;
+    if (v0) *reinterpret_cast<uint32_t*>(o0p + col) = pack_bf16(o[n][0] * inv0, o[n][1] * inv0);
+    if (v1) *reinterpret_cast<uint32_t*>(o1p + col) = pack_bf16(o[n][2] * inv1, o[n][3] * inv1);
+  }
+}
+
 // KV chunk (in 64-key tiles) per CTA for the split-KV schedule: a fixed
 // constant, so the partition never depends on the batch.
 constexpr int kKvChunkTiles = 2;
@@ -455,6 +715,19 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
     attr = true;
   }
   const float scale_log2 = scale * 1.4426950408889634f;
+  if (Hkv < H) {  // grouped-query: row-split schedule (chosen by G, never by Q)
+    static bool attr_r = false;
+    if (!attr_r) {
+      if (cudaFuncSetAttribute(attention_rows_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               S::BYTES) != cudaSuccess)
+        return MS_ERR_CUDA;
+      attr_r = true;
+    }
+    dim3 grid(B, Hkv, (Q * (H / Hkv) + 63) / 64);
+    return launch(attention_rows_kernel<D>, grid, dim3(kAThreads), S::BYTES, st, 1,
+                  (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
+                  (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo);
+  }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
   if (ws) {

@@ -548,15 +548,44 @@ linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
         if (lastv >= 0) {
           __threadfence();
           const int c_first = lastv & 0xffff, c_last = lastv >> 16;
-          for (int j = 0; j < m_hi; ++j) {
-            float acc = 0.f;
+          // fix-up: thread -> 4 consecutive features x rows rg, rg+4, ...; UNR
+          // independent 16-byte loads in flight per segment, segments added in
+          // k order (deterministic)
+          constexpr int UNR = 8;
+          const int et = threadIdx.x - 64;
+          const int fq = (et & 31) * 4, rg = et >> 5;
+          const int feat4 = tile * kBM + fq;
+          for (int j0 = rg; j0 < m_hi; j0 += 4 * UNR) {
+            float4 acc[UNR];
             for (int cc = c_first; cc <= c_last; ++cc) {
-              // cc's segment of this tile is its first (slot 0) iff the tile starts cc's range
               const int sl = (sk_begin(cc, sk.iters, sk.grid) / kbt == tile) ? 0 : 1;
-              const float v = __ldcg(sk.ws + ((int64_t)(cc * 2 + sl) * BN + j) * kBM + f);
-              acc = (cc == c_first) ? v : acc + v;
+              const float* base = sk.ws + ((int64_t)(cc * 2 + sl) * BN) * kBM + fq;
+              float4 v[UNR];
+#pragma unroll
+              for (int u = 0; u < UNR; ++u) {
+                const int j = j0 + 4 * u;
+                v[u] = j < m_hi ? __ldcg(reinterpret_cast<const float4*>(base + (int64_t)j * kBM))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int u = 0; u < UNR; ++u) {
+                if (cc == c_first) {
+                  acc[u] = v[u];
+                } else {
+                  acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+                }
+              }
             }
-            if (feat_ok) epi_store(p, j, feat, acc);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+              const int j = j0 + 4 * u;
+              if (j < m_hi) {
+                const float a4[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  if (feat4 + t < p.N) epi_store(p, j, feat4 + t, a4[t]);
+              }
+            }
           }
         }
         epi_bar128();  // s_last is reused by the next segment
