@@ -42,6 +42,10 @@ int ms_version(void);
 const char* ms_strerror(int status);
 /* Number of kernels launched through this library since load / last reset. */
 int64_t ms_launch_count(void);
+/* Load every kernel of the library now (instead of lazily at first launch:
+ * the tensor-parallel peer protocol runs spin-waiting kernels concurrently
+ * with other streams' kernels, and a lazy load can block behind them). */
+int ms_preload(void);
 void ms_reset_launch_count(void);
 
 /* ---- K4: weighted-majority vote ---------------------------------------
@@ -248,6 +252,44 @@ int ms_accept_stochastic(const int32_t* draft, const double* q, const double* o,
                          int B, int S, int V, double* scratch, int32_t* n_acc,
                          int32_t* emitted, int32_t* n_emit, int32_t* finished,
                          int32_t* n_draws, void* stream);
+
+/* ---- tensor-parallel verify over peer memory -----------------
+ * Symmetric buffers: ms_ipc_alloc cudaMallocs `bytes` (zeroed) and exports a
+ * CUDA IPC handle (ms_ipc_handle_size() bytes) that peers open with
+ * ms_ipc_open.  Flag sets hold one int per rank; `epoch` is a device counter
+ * per flag set (ms_tp_signal bumps it and publishes it to slot `rank` of every
+ * rank's flags with a system-scope release; waits acquire until every slot
+ * reaches the local epoch, bounded: on timeout *err = 1 and the kernel
+ * proceeds — no hang).  early != 0 releases the dependent kernel (PDL) before
+ * the wait — only when every rank has its own GPU.  Pointer arrays (peer_*) are device arrays of the t
+ * ranks' buffer addresses, rank order.  Replaces the NCCL allreduce of the
+ * Megatron row-parallel projections with a fixed-order, batch-invariant sum. */
+int ms_ipc_alloc(int64_t bytes, void** ptr, void* handle);
+int ms_ipc_handle_size(void);
+int ms_ipc_open(const void* handle, void** ptr);
+int ms_ipc_close(void* ptr);
+int ms_free(void* ptr);
+int ms_tp_signal(int* const* peer_flags, int rank, int t, int* epoch, void* stream);
+/* Two-shot sum after a row-parallel GEMM: waits for flag set `flags`, then
+ * rank `rank` adds column slice [rank*d/t, (rank+1)*d/t) of the t fp32
+ * partials parts[j] [R, ldp] in rank order (one bf16 rounding) and stores it
+ * into every rank's residual stream xs[j] [R, ldx] bf16.  d % (4t) == 0. */
+int ms_tp_reduce_gather(const float* const* parts, int64_t ldp, void* const* xs, int64_t ldx,
+                        const int* flags, const int* epoch, int rank, int t, int R, int d,
+                        int* err, int early, void* stream);
+/* RMSNorm of x [R, ldx] (as ms_rmsnorm) after waiting for flag set `flags`
+ * (every rank's slice of x has landed). */
+int ms_rmsnorm_wait(const void* x, int64_t ldx, const void* gamma, float eps, int R, int d,
+                    void* out, int64_t ldo, const int* flags, const int* epoch, int t, int* err,
+                    int early, void* stream);
+/* Vocab-parallel argmax: per row of this rank's logits slice [R, Vr] (global
+ * ids v0..v0+Vr-1) a u64 key (order-preserving value | ~index, so the max key
+ * is the first-index argmax; NaN never wins); combine waits for the flags and
+ * takes the max key over the t ranks' keys -> out [R] int32 (every rank). */
+int ms_tp_argmax_local(const float* logits, int64_t ld, int R, int Vr, int v0, uint64_t* out,
+                       void* stream);
+int ms_tp_argmax_combine(const uint64_t* const* peer, int t, int R, const int* flags,
+                         const int* epoch, int32_t* out, int* err, int early, void* stream);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,7 @@ _SIGS = {
     "ms_strerror": [_I],
     "ms_launch_count": [],
     "ms_reset_launch_count": [],
+    "ms_preload": [],
     "ms_vote": [_P, _P, _P, _I, _I, _I, _P, _P, _P],
     "ms_accept_greedy": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "ms_argmax_rows": [_P, _I, _I, _I, _I64, _P, _P, _P],
@@ -48,6 +49,16 @@ _SIGS = {
     "ms_draft_commit": [_P, _P, _I, _I, _I, _I, _I, _P, _I64, _P, _F, ctypes.c_uint64, _P, _P, _P],
     "ms_pack_verify": [_P, _P, _I, _I, _P, _P],
     "ms_attention": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _F, _I, _P, _I64, _P, _I64, _P, _I, _P],
+    "ms_ipc_alloc": [_I64, ctypes.POINTER(ctypes.c_void_p), _P],
+    "ms_ipc_handle_size": [],
+    "ms_ipc_open": [_P, ctypes.POINTER(ctypes.c_void_p)],
+    "ms_ipc_close": [_P],
+    "ms_free": [_P],
+    "ms_tp_signal": [_P, _I, _I, _P, _P],
+    "ms_tp_reduce_gather": [_P, _I64, _P, _I64, _P, _P, _I, _I, _I, _I, _P, _I, _P],
+    "ms_rmsnorm_wait": [_P, _I64, _P, _F, _I, _I, _P, _I64, _P, _P, _I, _P, _I, _P],
+    "ms_tp_argmax_local": [_P, _I64, _I, _I, _I, _P, _P],
+    "ms_tp_argmax_combine": [_P, _I, _I, _P, _P, _P, _P, _I, _P],
     "ms_attention_workspace": [_I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
 }
 _RESTYPE = {"ms_strerror": ctypes.c_char_p, "ms_launch_count": ctypes.c_int64,

@@ -191,6 +191,11 @@ static int launch_argmax(const void* logits, int is_bf16, int R, int V, int64_t 
                 (const unsigned long long*)ws, R, out);
 }
 
+int preload_accept() {
+  return preload_fn(argmax_rows_kernel<true>) + preload_fn(argmax_rows_kernel<false>) +
+         preload_fn(argmax_init_kernel) + preload_fn(argmax_finalize_kernel) + preload_fn(accept_greedy_kernel);
+}
+
 }  // namespace ms
 
 extern "C" int ms_argmax_rows(const void* logits, int is_bf16, int R, int V, int64_t ld,

@@ -224,6 +224,8 @@ accept_stochastic_kernel(const int32_t* __restrict__ draft, const double* __rest
   }
 }
 
+int preload_accept_stochastic() { return preload_fn(accept_stochastic_kernel); }
+
 }  // namespace ms
 
 extern "C" int ms_accept_stochastic(const int32_t* draft, const double* q, const double* o,

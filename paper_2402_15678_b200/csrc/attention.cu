@@ -743,6 +743,11 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
                 counters);
 }
 
+int preload_attention() {
+  return preload_fn(attention_kernel<64>) + preload_fn(attention_kernel<128>) +
+         preload_fn(attention_rows_kernel<64>) + preload_fn(attention_rows_kernel<128>);
+}
+
 }  // namespace ms
 
 extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,

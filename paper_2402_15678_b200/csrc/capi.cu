@@ -17,7 +17,26 @@ bool pdl_enabled() {
 }
 }  // namespace ms
 
+namespace ms {
+int preload_accept();
+int preload_accept_stochastic();
+int preload_vote();
+int preload_spec();
+int preload_model();
+int preload_attention();
+int preload_gemv();
+int preload_gemm();
+int preload_tp();
+}  // namespace ms
+
 extern "C" int ms_version(void) { return 100; }
+
+extern "C" int ms_preload(void) {
+  const int bad = ms::preload_accept() + ms::preload_accept_stochastic() + ms::preload_vote() +
+                  ms::preload_spec() + ms::preload_model() + ms::preload_attention() + ms::preload_gemv() +
+                  ms::preload_gemm() + ms::preload_tp();
+  return bad ? MS_ERR_CUDA : MS_OK;
+}
 
 extern "C" const char* ms_strerror(int status) {
   switch (status) {

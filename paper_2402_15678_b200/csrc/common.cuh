@@ -57,6 +57,15 @@ inline int launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   return 0;
 }
 
+// Force-load a kernel (lazy module loading would otherwise load it at first
+// launch, which can block behind a spin-waiting kernel of another stream —
+// the tensor-parallel peer protocol relies on concurrent kernels).
+template <typename F>
+inline int preload_fn(F f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MS_OK : MS_ERR_CUDA;

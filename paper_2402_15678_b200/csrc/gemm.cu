@@ -698,6 +698,27 @@ static int launch_linear_sk(const CUtensorMap& tw, const CUtensorMap& tx, const 
   return launch(linear_sk_kernel<BN>, dim3(sk.grid), dim3(kThreads), C::SMEM, st, 1, tw, tx, p, sk);
 }
 
+int preload_gemm() {
+  int n = 0;
+  n += preload_fn(linear_kernel<16>) + preload_fn(linear_sk_kernel<16>);
+  n += preload_fn(linear_kernel<32>) + preload_fn(linear_sk_kernel<32>);
+  n += preload_fn(linear_kernel<48>) + preload_fn(linear_sk_kernel<48>);
+  n += preload_fn(linear_kernel<64>) + preload_fn(linear_sk_kernel<64>);
+  n += preload_fn(linear_kernel<80>) + preload_fn(linear_sk_kernel<80>);
+  n += preload_fn(linear_kernel<96>) + preload_fn(linear_sk_kernel<96>);
+  n += preload_fn(linear_kernel<112>) + preload_fn(linear_sk_kernel<112>);
+  n += preload_fn(linear_kernel<128>) + preload_fn(linear_sk_kernel<128>);
+  n += preload_fn(linear_kernel<144>) + preload_fn(linear_sk_kernel<144>);
+  n += preload_fn(linear_kernel<160>) + preload_fn(linear_sk_kernel<160>);
+  n += preload_fn(linear_kernel<176>) + preload_fn(linear_sk_kernel<176>);
+  n += preload_fn(linear_kernel<192>) + preload_fn(linear_sk_kernel<192>);
+  n += preload_fn(linear_kernel<208>) + preload_fn(linear_sk_kernel<208>);
+  n += preload_fn(linear_kernel<224>) + preload_fn(linear_sk_kernel<224>);
+  n += preload_fn(linear_kernel<240>) + preload_fn(linear_sk_kernel<240>);
+  n += preload_fn(linear_kernel<256>) + preload_fn(linear_sk_kernel<256>);
+  return n;
+}
+
 }  // namespace ms
 
 extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }

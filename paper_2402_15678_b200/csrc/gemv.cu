@@ -150,6 +150,11 @@ gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat1
   }
 }
 
+int preload_gemv() {
+  return preload_fn(gemv_kernel<1>) + preload_fn(gemv_kernel<2>) + preload_fn(gemv_kernel<3>) +
+         preload_fn(gemv_kernel<4>);
+}
+
 }  // namespace ms
 
 extern "C" int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,

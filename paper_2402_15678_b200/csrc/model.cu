@@ -158,6 +158,19 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
   }
 }
 
+int preload_model() {
+  int n = preload_fn(embed_kernel) + preload_fn(kv_append_kernel);
+  n += preload_fn(layernorm_kernel<1, false>) + preload_fn(layernorm_kernel<2, false>) +
+       preload_fn(layernorm_kernel<3, false>) + preload_fn(layernorm_kernel<4, false>) +
+       preload_fn(layernorm_kernel<5, false>) + preload_fn(layernorm_kernel<6, false>) +
+       preload_fn(layernorm_kernel<7, false>) + preload_fn(layernorm_kernel<8, false>);
+  n += preload_fn(layernorm_kernel<1, true>) + preload_fn(layernorm_kernel<2, true>) +
+       preload_fn(layernorm_kernel<3, true>) + preload_fn(layernorm_kernel<4, true>) +
+       preload_fn(layernorm_kernel<5, true>) + preload_fn(layernorm_kernel<6, true>) +
+       preload_fn(layernorm_kernel<7, true>) + preload_fn(layernorm_kernel<8, true>);
+  return n;
+}
+
 }  // namespace ms
 
 extern "C" int ms_embed(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,

@@ -57,6 +57,8 @@ __global__ void pack_verify_kernel(const int32_t* __restrict__ last, const int32
   vin[e] = i == 0 ? last[b] : path[(int64_t)b * S + i - 1];
 }
 
+int preload_spec() { return preload_fn(draft_commit_kernel) + preload_fn(pack_verify_kernel); }
+
 }  // namespace ms
 
 extern "C" int ms_draft_commit(const int32_t* tok, const int32_t* ctx_len, int B, int j, int k,

@@ -78,6 +78,8 @@ vote_kernel(const int32_t* __restrict__ tokens, const double* __restrict__ weigh
   if (lane == 0) voted[b] = k;
 }
 
+int preload_vote() { return preload_fn(vote_kernel); }
+
 }  // namespace ms
 
 extern "C" int ms_vote(const int32_t* tokens, const double* weights, const int32_t* rank,

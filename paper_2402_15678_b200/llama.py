@@ -44,12 +44,13 @@ class LlamaConfig:
     max_pos: int = 4096
     eps: float = 1e-5
     rope_theta: float = 10000.0
+    hd: int = 0  # head dim when it is not d / n_heads (a tensor-parallel shard)
 
     family = "llama"
 
     @property
     def head_dim(self) -> int:
-        return self.d // self.n_heads
+        return self.hd or self.d // self.n_heads
 
     @property
     def qkv_out(self) -> int:
@@ -57,7 +58,7 @@ class LlamaConfig:
 
     def matmul_params(self) -> int:
         """Parameters streamed per forward (layers + LM head)."""
-        per_layer = self.d * self.qkv_out + self.d * self.d + 3 * self.d * self.ffn
+        per_layer = self.d * self.qkv_out + self.d * self.n_heads * self.head_dim + 3 * self.d * self.ffn
         return self.n_layers * per_layer + self.vocab * self.d
 
     def kv_bytes_per_token(self) -> int:
@@ -71,6 +72,8 @@ CONFIGS = {
     # test-sized Llama shapes (GQA 2:1, D = 64)
     "tiny-llama": LlamaConfig("tiny-llama", 4, 256, 4, 2, 512, max_pos=1024),
     "tiny-llama-ssm": LlamaConfig("tiny-llama-ssm", 1, 256, 4, 4, 512, max_pos=1024),
+    # tensor-parallel test shape: splits over 2, 4 and 8 ranks (GQA 2:1, D = 64)
+    "tiny-llama-tp": LlamaConfig("tiny-llama-tp", 2, 1024, 16, 8, 4096, max_pos=1024),
 }
 
 

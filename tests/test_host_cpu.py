@@ -117,3 +117,52 @@ def test_llama_reference_gqa_equals_mha_with_repeated_kv():
     w2["l0.w_qkv"] = torch.cat([wq, rep(wk), rep(wv)])
     toks = [3, 7, 1, 40, 2, 9]
     torch.testing.assert_close(llama_ref.forward(w, gq, toks), llama_ref.forward(w2, mh, toks))
+
+
+def test_tp_shard_math_reproduces_full_layer():
+    """The Megatron split of tp.shard_llama (column-parallel QKV / gate-up,
+    row-parallel O / down, vocab-parallel head): summing the ranks' fp32
+    partials reproduces the unsharded computation (CPU, fp32, no kernels)."""
+    import math
+    import torch
+    from oracle import llama_ref
+    from paper_2402_15678_b200.llama import LlamaConfig, LlamaWeights
+    from paper_2402_15678_b200.tp import shard_llama
+    c = LlamaConfig("t", 1, 64, 8, 4, 256, vocab=64, max_pos=32)
+    w = LlamaWeights.random(c, 0, device="cpu", std=0.1)
+    f = {k: v.float() for k, v in w.t.items()}
+    T = 5
+    x = torch.randn(T, c.d)
+    table = llama_ref.rope_table(T, c.head_dim, c.rope_theta)
+    pos = torch.arange(T)
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
+
+    def attn(wqkv, H, Hkv):
+        D = c.head_dim
+        qkv = x @ wqkv.T
+        q = llama_ref.rope(qkv[:, :H * D].view(T, H, D), pos, table)
+        k = llama_ref.rope(qkv[:, H * D:(H + Hkv) * D].view(T, Hkv, D), pos, table).repeat_interleave(H // Hkv, 1)
+        v = qkv[:, (H + Hkv) * D:].view(T, Hkv, D).repeat_interleave(H // Hkv, 1)
+        s = (q.transpose(0, 1) @ k.transpose(0, 1).transpose(1, 2)) / math.sqrt(D)
+        return (torch.softmax(s.masked_fill(mask, float("-inf")), -1) @ v.transpose(0, 1)).transpose(0, 1).reshape(T, -1)
+
+    def mlp(wgu, wd, F):
+        g, u = llama_ref.split_gate_up(wgu, F)
+        a, b = x @ g.T, x @ u.T
+        return (a / (1 + torch.exp(-a)) * b) @ wd.T
+
+    want_o = attn(f["l0.w_qkv"], c.n_heads, c.n_kv_heads) @ f["l0.w_o"].T
+    want_m = mlp(f["l0.w_gu"], f["l0.w_down"], c.ffn)
+    for t in (2, 4):
+        got_o = torch.zeros_like(want_o)
+        got_m = torch.zeros_like(want_m)
+        heads = []
+        for r in range(t):
+            s = {k: v.float() for k, v in shard_llama(w, r, t).t.items()}
+            sc = shard_llama(w, r, t).cfg
+            got_o += attn(s["l0.w_qkv"], sc.n_heads, sc.n_kv_heads) @ s["l0.w_o"].T
+            got_m += mlp(s["l0.w_gu"], s["l0.w_down"], sc.ffn)
+            heads.append(x @ s["lm_head"].T)
+        torch.testing.assert_close(got_o, want_o, rtol=1e-4, atol=1e-5)
+        torch.testing.assert_close(got_m, want_m, rtol=1e-4, atol=1e-5)
+        torch.testing.assert_close(torch.cat(heads, 1), x @ f["lm_head"].T)
