@@ -137,7 +137,7 @@ class _Group:
         self.ssm_logits = [torch.empty(B, V, device=dev) for _ in range(K)]
         self.argmax_ws = torch.zeros(B * (s_cap + 1), dtype=torch.int64, device=dev)
         self.vin = z(B, s_cap + 1)
-        self.v_logits = torch.empty(B * (s_cap + 1), V, device=dev)
+        self.v_logits = torch.empty(B * (s_cap + 1), eng.Vt, device=dev)  # target's vocab slice
         self.ev_d0 = torch.cuda.Event(enable_timing=True)
         self.ev_d1 = torch.cuda.Event(enable_timing=True)
         self.ev_v0 = torch.cuda.Event(enable_timing=True)
@@ -173,7 +173,12 @@ class SpecEngine:
     def __init__(self, target, drafters: list, cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
-                 record: bool = False, pipelined: bool = False):
+                 record: bool = False, pipelined: bool = False, sync_time=None):
+        """target: weights (a model is built here) or a prebuilt model — e.g. a
+        tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
+        argmax() combines across ranks.  sync_time(ms) -> ms: makes the
+        selector's verify time identical on every rank (tensor parallel: every
+        rank must take the same decisions); None = local time."""
         validate_config(cfg)
         if len(cfg.initial_weights) != len(drafters):
             raise ValueError("initial_weights must have one entry per drafter")
@@ -188,14 +193,20 @@ class SpecEngine:
         self.adaptive = adaptive
         self.record = record
         self.pipelined = pipelined
-        V = target.cfg.vocab
+        s_cap = cfg.s_max
+        if hasattr(target, "forward"):
+            self.target = target
+        else:
+            self.target = make_model(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
+        self.tp = hasattr(self.target, "comm")
+        self.Vt = self.target.cfg.vocab                       # width of the target's logits
+        V = self.Vt * (self.target.tp if self.tp else 1)      # full vocabulary
         if any(w.cfg.vocab != V for w in drafters):
             raise ValueError("drafters and target must share a vocabulary")
         self.V = V
-        s_cap = cfg.s_max
-        self.target = make_model(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
+        self.sync_time = sync_time
         self.ssms = [make_model(w, max_rows=slots * max_len, device=device, small_gemm=True) for w in drafters]
-        self.t_cache = KVCache(target.cfg, slots, max_len, device)
+        self.t_cache = KVCache(self.target.cfg, slots, max_len, device)
         self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
         ng = 2 if pipelined else 1
         gb = slots // ng
@@ -248,8 +259,9 @@ class SpecEngine:
             self.h2d_bytes += toks.nbytes
             zero = torch.zeros(self.B, dtype=I32, device=self.dev)
             empty = torch.zeros(0, dtype=I32, device=self.dev)
+            self.target.forward(t, zero, self.slot, self.t_cache, torch.empty(0, self.Vt, device=self.dev),
+                                head_rows=empty)
             dummy = torch.empty(0, self.V, device=self.dev)
-            self.target.forward(t, zero, self.slot, self.t_cache, dummy, head_rows=empty)
             for m, c in zip(self.ssms, self.s_caches):
                 m.forward(t, zero, self.slot, c, dummy, head_rows=empty)
         for r in requests:
@@ -319,6 +331,13 @@ class SpecEngine:
         logits = g.v_logits[: B * (s + 1)]
         self.target.forward(vin, g.v_start, g.slot, self.t_cache, logits)
         a = g.acc
+        if self.tp:  # vocab-parallel logits: cross-rank argmax, then accept
+            R = B * (s + 1)
+            self.target.argmax(logits, a.tgt_argmax[:R])
+            _native.call("ms_accept_greedy", g.path.data_ptr(), a.tgt_argmax.data_ptr(), g.remaining.data_ptr(),
+                         -1 if self.cfg.stop_token is None else self.cfg.stop_token, B, s, a.n_acc.data_ptr(),
+                         a.emitted.data_ptr(), a.n_emit.data_ptr(), a.finished.data_ptr(), None, sp)
+            return
         _native.call("ms_accept_greedy_logits", g.path.data_ptr(), logits.data_ptr(), 0, V,
                      g.remaining.data_ptr(), -1 if self.cfg.stop_token is None else self.cfg.stop_token,
                      B, s, a.tgt_argmax.data_ptr(), g.argmax_ws.data_ptr(), a.n_acc.data_ptr(),
@@ -339,7 +358,7 @@ class SpecEngine:
             self.kernel_launches += _native.launch_count() - n0
             gr = torch.cuda.CUDAGraph()
             n1 = _native.launch_count()
-            with torch.cuda.graph(gr, stream=torch.cuda.current_stream(self.dev)):
+            with torch.cuda.graph(gr, stream=torch.cuda.current_stream(self.dev), capture_error_mode="thread_local"):
                 fn()
             self.graph_kernels[key] = _native.launch_count() - n1
             self.graphs[key] = gr
@@ -473,6 +492,8 @@ class SpecEngine:
         voted = get("voted")
         drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = g.ev_v0.elapsed_time(g.ev_v1)
+        if self.sync_time is not None:
+            t_verify = float(self.sync_time(t_verify))
         t_draft = g.ev_d0.elapsed_time(g.ev_d1)
         accs, ems, vts = [], [], []
         for b in active:
@@ -583,22 +604,25 @@ class SpecEngine:
             toks[b, : len(c) - 1] = c[:-1]
         zero = torch.zeros(B, dtype=I32, device=self.dev)
         empty = torch.zeros(0, dtype=I32, device=self.dev)
-        dummy = torch.empty(0, self.V, device=self.dev)
+        dummy = torch.empty(0, self.Vt, device=self.dev)
         if P > 0:
             self.target.forward(torch.from_numpy(toks).to(self.dev), zero, self.slot, cache, dummy,
                                 head_rows=empty)
         out = {r.id: [] for r in requests}
         lens = np.array([len(c) for c in ctx] + [1] * (B - len(ctx)))
         cur = np.array([c[-1] for c in ctx] + [0] * (B - len(ctx)), np.int32)
-        logits = torch.empty(B, self.V, device=self.dev)
+        logits = torch.empty(B, self.Vt, device=self.dev)
         am = torch.zeros(B, dtype=I32, device=self.dev)
         ws = torch.zeros(B, dtype=torch.int64, device=self.dev)
         for t in range(n_new):
             self.target.forward(torch.from_numpy(cur[:, None].copy()).to(self.dev),
                                 torch.from_numpy((lens - 1).astype(np.int32)).to(self.dev),
                                 self.slot, cache, logits)
-            _native.call("ms_argmax_rows", logits.data_ptr(), 0, B, self.V, self.V, am.data_ptr(),
-                         ws.data_ptr(), _dev.stream_ptr())
+            if self.tp:
+                self.target.argmax(logits, am)
+            else:
+                _native.call("ms_argmax_rows", logits.data_ptr(), 0, B, self.V, self.V, am.data_ptr(),
+                             ws.data_ptr(), _dev.stream_ptr())
             nxt = am.cpu().numpy()
             for b, r in enumerate(requests):
                 out[r.id].append(int(nxt[b]))

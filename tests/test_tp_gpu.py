@@ -125,3 +125,127 @@ def test_tp_forward_batch_invariant_and_deterministic():
     for r in range(t):
         assert torch.equal(a_lg[r][:, T0:], b_lg[r][:, T0:])
         assert torch.equal(b_lg[r], c_lg[r])
+
+
+def test_tp_engine_lossless_ranks_agree():
+    """Two TP ranks (threads on one GPU) each run the full speculation engine
+    (replicated drafters, TP verifier): identical decisions on both ranks,
+    speculative output == the TP target's greedy decode."""
+    from paper_2402_15678_b200.core import EngineConfig, Request
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    from paper_2402_15678_b200.tp import LlamaTPModel, TPComm, shard_llama
+    t, B, n_new = 2, 4, 32
+    tcfg, scfg = CONFIGS["tiny-llama"], CONFIGS["tiny-llama-ssm"]
+    w = LlamaWeights.random(tcfg, 0, device="cpu", std=0.05, norm_std=0.1)
+    dw = [LlamaWeights.random(scfg, k + 1, device="cpu", std=0.05, norm_std=0.1) for k in range(3)]
+    max_len = 96
+    comms = TPComm.local_group(t, B * max_len, tcfg.d)
+    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=B, b_ssm=B, s_init=4, initial_weights=(1.0,) * 3,
+                       decision_threshold=3)
+    bar = threading.Barrier(t)
+    times = [0.0] * t
+
+    def sync_max(r):
+        def f(ms):
+            times[r] = ms
+            bar.wait()
+            m = max(times)
+            bar.wait()
+            return m
+        return f
+
+    engines = [SpecEngine(LlamaTPModel(shard_llama(w, r, t).to("cuda"), comms[r], max_rows=B * max_len),
+                          [d.to("cuda") for d in dw], cfg, slots=B, max_len=max_len, fidelity=[0.9, 0.7, 0.5],
+                          use_graphs=False, sync_time=sync_max(r)) for r in range(t)]
+    rng = np.random.default_rng(0)
+    prompts = [[int(x) for x in rng.integers(0, tcfg.vocab, size=6)] for _ in range(B)]
+    out = [None] * t
+
+    def run(r):
+        def f():
+            eng = engines[r]
+            reqs = [Request(f"req-{i:03d}", list(p), n_new) for i, p in enumerate(prompts)]
+            teacher = eng.greedy_teacher([Request(q.id, list(q.prompt), n_new) for q in reqs], n_new)
+            eng.prefill(reqs)
+            eng.set_teacher(teacher)
+            res = eng.decode()
+            out[r] = (teacher, res.outputs, [rd.s for rd in res.rounds], res.mean_accepted)
+        return f
+
+    _run_ranks([run(r) for r in range(t)])
+    for c in comms:
+        c.check()
+    teacher, outputs, s_seq, acc = out[0]
+    assert outputs == teacher
+    assert acc > 1.0
+    for r in range(1, t):
+        assert out[r][0] == teacher and out[r][1] == outputs and out[r][2] == s_seq
+
+
+def _ipc_rank(rank, world, port, result_path):
+    import os
+    import pickle
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    from paper_2402_15678_b200.opt import KVCache
+    from paper_2402_15678_b200.tp import LlamaTPModel, TPComm, shard_llama
+    cfg = CONFIGS["tiny-llama"]
+    B, T0 = 2, 12
+    w = LlamaWeights.random(cfg, 5, device="cpu", std=0.05, norm_std=0.1)
+    comm = TPComm.from_process_group(B * 32, cfg.d)
+    m = LlamaTPModel(shard_llama(w, rank, world).to("cuda"), comm, max_rows=B * 32)
+    cache = KVCache(m.cfg, B, 32)
+    rng = np.random.default_rng(2)
+    toks = torch.tensor(rng.integers(0, cfg.vocab, size=(B, T0)).astype(np.int32), device="cuda")
+    slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    lg = torch.empty(B * T0, m.cfg.vocab, device="cuda")
+    am = torch.zeros(B * T0, dtype=torch.int32, device="cuda")
+    m.argmax(m.forward(toks, torch.zeros(B, dtype=torch.int32, device="cuda"), slot, cache, lg), am)
+    torch.cuda.synchronize()
+    comm.check()
+    with open(f"{result_path}.{rank}", "wb") as fh:
+        pickle.dump({"am": am.cpu(), "lg": lg.cpu()}, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+    os._exit(0)
+
+
+def test_tp_two_processes_over_cuda_ipc(tmp_path):
+    """The process-group path: two processes (sharing this one GPU) map each
+    other's symmetric buffers through CUDA IPC handles exchanged over
+    torch.distributed (gloo) and run the TP forward; both ranks agree and the
+    gathered logits match the single-process model."""
+    import pickle
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    res = str(tmp_path / "r")
+    ctx = mp.get_context("spawn")
+    ps = [ctx.Process(target=_ipc_rank, args=(r, 2, port, res)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=240)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    r0, r1 = (pickle.load(open(f"{res}.{r}", "rb")) for r in range(2))
+    assert torch.equal(r0["am"], r1["am"])
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaModel, LlamaWeights
+    from paper_2402_15678_b200.opt import KVCache
+    cfg = CONFIGS["tiny-llama"]
+    B, T0 = 2, 12
+    w = LlamaWeights.random(cfg, 5, device="cpu", std=0.05, norm_std=0.1)
+    full = LlamaModel(w.to("cuda"), max_rows=64)
+    rng = np.random.default_rng(2)
+    toks = torch.tensor(rng.integers(0, cfg.vocab, size=(B, T0)).astype(np.int32), device="cuda")
+    ref = torch.empty(B * T0, cfg.vocab, device="cuda")
+    full.forward(toks, torch.zeros(B, dtype=torch.int32, device="cuda"), torch.arange(B, dtype=torch.int32,
+                 device="cuda"), KVCache(cfg, B, 32), ref)
+    got = torch.cat([r0["lg"], r1["lg"]], 1)
+    ref = ref.cpu()
+    assert (got - ref).abs().max().item() / ref.abs().max().item() < 3e-2
+    assert torch.equal(r0["am"].long(), got.argmax(-1))
