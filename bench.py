@@ -25,9 +25,13 @@ round logic over the fp32 CPU model under the reference's ModelOracle
 protocol — a full forward per next_dist call, no KV cache) on a bounded
 sample, scaled to tokens/s.
 
-Multi-GPU (torchrun, N>1): replicas only — every rank runs the same
-single-GPU workload on its own GPU (weak scaling, no data-path collective);
-value = all ranks' tokens / max-over-ranks time.
+Multi-GPU (torchrun, N>1), --parallelism tp (default): the verifier is
+tensor parallel over the N ranks (Megatron split; the sums over ranks are
+libminions' fixed-order reductions over CUDA-IPC peer memory), the drafters
+are replicated, every rank serves the same global batch of 16 (strong
+scaling); value = tokens / max-over-ranks time.  --parallelism replicas: every
+rank runs the single-GPU workload on its own batch (weak scaling, no
+data-path collective).
 """
 from __future__ import annotations
 
@@ -68,6 +72,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1)
     ap.add_argument("--fixed-s", type=int, default=0, help="disable the adaptive selector, use this s")
+    ap.add_argument("--parallelism", default="tp", choices=["tp", "replicas"],
+                    help="N>1: tensor-parallel verifier over the ranks (default, SURVEY §8e) or one full "
+                         "replica per GPU serving its own batch")
     ap.add_argument("--schedule", default="sequential", choices=["sequential", "pipelined"],
                     help="pipelined: two request groups of --batch each (2x requests), verify of one "
                          "overlapping drafting of the other (aggspec/engine.py:494-576)")
@@ -82,8 +89,15 @@ def dist_init():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # MS_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo plumbing — a
+        # functional test of the multi-process path on a one-GPU box (NCCL
+        # refuses two ranks on one GPU); never a performance configuration
+        if os.environ.get("MS_BENCH_SHARE_GPU", "0") == "1":
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return rank, ws, local
@@ -117,8 +131,9 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                row = [c.strip() for c in out.split(",")] if out else []
+                if len(row) == 6:
+                    self.rows.append(row)
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -195,20 +210,52 @@ def run_ours(args, rank, ws):
     tcfg, scfg = config(args.target), config(args.ssm)
     fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else None
     K = 3
-    target = random_weights(tcfg, 0, device="cuda")
-    drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
     cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch,
                        s_init=args.fixed_s or 4, s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
     max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
     pipelined = args.schedule == "pipelined"
     n_req = args.batch * (2 if pipelined else 1)
+    tp = ws > 1 and args.parallelism == "tp"
+    note = None
+    target = None
+    sync = None
+    if tp:
+        # the verifier tensor-parallel over the ranks (Megatron split,
+        # sums over ranks by the peer-memory kernels of csrc/tp.cu), drafters
+        # replicated on every rank; one global batch -> strong scaling
+        import torch.distributed as tdist
+        from paper_2402_15678_b200.tp import LlamaTPModel, TPComm, random_shard
+        max_rows = max(n_req * (cfg.s_max + 1), n_req * max_len)
+        err = None
+        try:
+            comm = TPComm.from_process_group(max_rows, tcfg.d)
+        except Exception as e:  # e.g. no CUDA IPC / peer access between the GPUs
+            err = f"{type(e).__name__}: {e}"
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)  # all ranks take the same branch
+        if int(ok.item()) == 1:
+            target = LlamaTPModel(random_shard(tcfg, rank, ws, 0), comm, max_rows=max_rows)
+
+            def sync(ms):
+                v = torch.tensor([ms], dtype=torch.float64, device="cuda")
+                tdist.all_reduce(v, op=tdist.ReduceOp.MAX)
+                return float(v.item())
+        else:
+            tp = False
+            note = f"tensor parallel unavailable ({err or 'on a peer rank'}); ran replicas"
+    if target is None:
+        target = random_weights(tcfg, 0, device="cuda")
+    drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
     eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
                      use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined,
-                     adaptive=not args.fixed_s)
-    # weak scaling: the global request list is n_req per rank; each rank serves
-    # its own contiguous slice (requests are independent — no data-path collective)
-    from paper_2402_15678_b200.dist import shard_requests
-    reqs = shard_requests(make_requests(n_req * ws, args.prompt_len, args.new_tokens, tcfg.vocab), rank, ws)
+                     adaptive=not args.fixed_s, sync_time=sync)
+    if tp:  # every rank serves the same global batch
+        reqs = make_requests(n_req, args.prompt_len, args.new_tokens, tcfg.vocab)
+    else:
+        # weak scaling: the global request list is n_req per rank; each rank serves
+        # its own contiguous slice (requests are independent — no data-path collective)
+        from paper_2402_15678_b200.dist import shard_requests
+        reqs = shard_requests(make_requests(n_req * ws, args.prompt_len, args.new_tokens, tcfg.vocab), rank, ws)
     eng.capture_graphs()  # every s, before timing (and before prefill)
     teacher = eng.greedy_teacher(fresh(reqs), args.new_tokens) if fid else None
 
@@ -231,7 +278,7 @@ def run_ours(args, rank, ws):
     barrier(ws)
     torch.cuda.synchronize()
     results, t_total, launches = [], 0.0, 0
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         for _ in range(args.steps):
             res, t, nl = one_step()
             results.append(res)
@@ -242,7 +289,7 @@ def run_ours(args, rank, ws):
     lossless = all(r.outputs == teacher for r in results) if teacher else None
     tokens = sum(r.tokens for r in results)
     t_max = max_over_ranks(t_total, ws)
-    value = tokens * ws / t_max
+    value = tokens * (1 if tp else ws) / t_max
     rounds = [rd for r in results for rd in r.rounds]
     # mean context per round for the KV term of the roofline
     for r in results:
@@ -269,7 +316,7 @@ def run_ours(args, rank, ws):
         e2e_tokens += res.tokens
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0, ws)
-    e2e = {"value": round(e2e_tokens * ws / t_e2e, 2), "unit": "tokens/s",
+    e2e = {"value": round(e2e_tokens * (1 if tp else ws) / t_e2e, 2), "unit": "tokens/s",
            "h2d_bytes_per_step": int((eng.h2d_bytes - h0) / args.steps),
            "d2h_bytes_per_step": int((eng.d2h_bytes - d0) / args.steps),
            "includes": "prompt H2D + prefill + decode + per-round H2D/D2H"}
@@ -283,12 +330,14 @@ def run_ours(args, rank, ws):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts, random-init weights, fidelity-injected drafts",
         "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * K,
-                   "global_batch": n_req * ws, "schedule": args.schedule, "prompt_len": args.prompt_len,
+                   "global_batch": n_req * (1 if tp else ws), "schedule": args.schedule,
+                   "prompt_len": args.prompt_len,
                    "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
-                   "fidelity": fid, "parallelism": "replicas" if ws > 1 else "single-gpu",
+                   "fidelity": fid,
+                   "parallelism": (f"tp{ws}" if tp else "replicas") if ws > 1 else "single-gpu",
                    "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
                           "streamed per verify)"),
                    "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
@@ -308,6 +357,8 @@ def run_ours(args, rank, ws):
         "clocks": clk.summary(),
         "libminions": _native.LIB_PATH,
     }
+    if note:
+        out["parallelism_note"] = note
     return out
 
 
