@@ -492,9 +492,14 @@ class SpecEngine:
         voted = get("voted")
         drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = g.ev_v0.elapsed_time(g.ev_v1)
-        if self.sync_time is not None:
-            t_verify = float(self.sync_time(t_verify))
         t_draft = g.ev_d0.elapsed_time(g.ev_d1)
+        # selector input (MonitorSample.t_llm): the verify's device time.  In the
+        # sequential single-GPU schedule the drafters do not overlap the
+        # verifier, so the round period the reference's pipelined assumption
+        # equates with t_llm is verify + draft; the selector gets that.
+        t_sel = t_verify if self.pipelined else t_verify + t_draft
+        if self.sync_time is not None:
+            t_sel = float(self.sync_time(t_sel))
         accs, ems, vts = [], [], []
         for b in active:
             r = g.requests[b]
@@ -525,7 +530,7 @@ class SpecEngine:
             vts.append(int(voted[b]))
         update_weights(self.weights, self.cfg)
         vl = float(np.mean(ems)) if ems else 1.0
-        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_verify, vl=vl, s_used=s))
+        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_sel, vl=vl, s_used=s))
         decision = Decision.HOLD
         if self.adaptive:
             _, decision = maybe_adjust(self.selector)

@@ -135,7 +135,18 @@ class LlamaWeights:
 
 class LlamaModel:
     """Batched forward over the kernels with static activation buffers (CUDA
-    graph capturable), same interface as opt.OPTModel."""
+    graph capturable), same interface as opt.OPTModel.
+
+    Prompt prefill (R >= PREFILL_ROWS token rows, SURVEY §8f — outside the
+    speculate-vote-verify path) is compute-bound: its layer GEMMs go to cuBLAS
+    as plain library GEMMs (measured 1.4-1.55 PFLOP/s vs 0.6-1.0 for the
+    weight-streaming ms_linear at M = 2032, tools/prefill_gemm_probe.py);
+    every decode / verify / drafter GEMM (R <= 16 * 13 rows) is ms_linear or
+    ms_gemv.  The row threshold is a constant, so a given call shape always
+    takes the same path (deterministic; prefill caches are identical for the
+    greedy teacher and the speculative run)."""
+
+    PREFILL_ROWS = 512
 
     def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False):
         """small_gemm: projections of <= 64 token rows with K <= 1024 use the
@@ -168,8 +179,11 @@ class LlamaModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         K.embed(tokens, start, Q, w["tok_emb"], None, 0, out=x, stream=stream)
         small = self.small_gemm and R <= 64
+        prefill = R >= self.PREFILL_ROWS
 
         def lin(xx, wname, **kw):
+            if prefill:
+                return _prefill_linear(xx, w[wname], stream=stream, **kw)
             if small and xx.shape[1] <= 1024:
                 return K.gemv(xx, w[wname], stream=stream, **kw)
             return K.linear(xx, w[wname], stream=stream, **kw)
@@ -189,3 +203,26 @@ class LlamaModel:
         K.rmsnorm(x, w["norm_f"], c.eps, out=hf, rows=head_rows, stream=stream)
         K.linear(hf, w["lm_head"], out=logits, out_f32=True, stream=stream)
         return logits
+
+
+def _prefill_linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residual=None, act: int = 0,
+                    stream=None) -> torch.Tensor:
+    """Prefill GEMM on cuBLAS (plain library GEMM, see LlamaModel): out =
+    x @ w^T (+ residual, in place when out is residual) or, act=2, the gated
+    SiLU of the 64-row interleaved gate/up weight from fp32 GEMM outputs
+    (fp32 silu * up, one bf16 rounding, as ms_linear's epilogue)."""
+    with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+        if act == 2:
+            gu = torch.mm(x, w.t(), out_dtype=torch.float32)
+            M, N = gu.shape
+            g4 = gu.view(M, N // 128, 2, 64)
+            out.copy_((torch.nn.functional.silu(g4[:, :, 0, :]) * g4[:, :, 1, :]).reshape(M, N // 2))
+            return out
+        if residual is not None:
+            if out.data_ptr() == residual.data_ptr():
+                out.addmm_(x, w.t())
+            else:
+                torch.addmm(residual, x, w.t(), out=out)
+            return out
+        torch.mm(x, w.t(), out=out)
+        return out

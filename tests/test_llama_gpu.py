@@ -217,3 +217,30 @@ def test_llama_engine_lossless_and_rounds_match_oracle():
             assert np.array_equal(t["path"][b], p) and int(t["voted"][b]) == int(v)
             acc, em, _ = O.verify_greedy_one(t["path"][b], t["tgt"][b, : rd.s + 1])
             assert int(t["n_acc"][b]) == acc
+
+
+def test_llama_prefill_path_large_m_vs_reference():
+    """R >= PREFILL_ROWS token rows take the prefill (cuBLAS) GEMMs; the cache
+    they build is continued by the decode kernels: both against the fp32 CPU
+    reference."""
+    from paper_2402_15678_b200.llama import LlamaModel
+    cfg, w_cpu = _tiny_llama(4)
+    model = LlamaModel(w_cpu.to("cuda"), max_rows=1024)
+    B, T0 = 4, 144
+    assert B * T0 >= model.PREFILL_ROWS
+    rng = np.random.default_rng(4)
+    toks = rng.integers(0, cfg.vocab, size=(B, T0 + 3)).astype(np.int32)
+    cache = _kv(cfg, B, 160)
+    slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    lg = torch.empty(B * T0, cfg.vocab, device="cuda")
+    model.forward(torch.tensor(toks[:, :T0], device="cuda"), torch.zeros(B, dtype=torch.int32, device="cuda"),
+                  slot, cache, lg)
+    l3 = torch.empty(B * 3, cfg.vocab, device="cuda")
+    model.forward(torch.tensor(toks[:, T0:], device="cuda"), torch.full((B,), T0, dtype=torch.int32, device="cuda"),
+                  slot, cache, l3)
+    got = torch.cat([lg.view(B, T0, -1).cpu(), l3.view(B, 3, -1).cpu()], 1)
+    for b in range(2):
+        ref = llama_ref.forward(w_cpu.t, cfg, toks[b])
+        err = (got[b] - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 3e-2, err
+        assert (got[b].argmax(-1) == ref.argmax(-1)).float().mean().item() >= 0.95
