@@ -391,25 +391,30 @@ class SpecEngine:
         s_values = s_values or range(self.cfg.s_min, self.cfg.s_max + 1)
         for g in self.groups:
             for s in s_values:
-                if ("verify", g.gid, s) in self.graphs:
-                    continue
-                B, qc = g.B, s + 1
-                lens = np.full(B, 2 * qc + 1, np.int64)
-                mh = g.meta_h.numpy()
-                mh[:] = 0
-                o, _ = g.meta_off["w"]
-                mh[o: o + 2 * self.K] = np.ones(self.K, np.float64).view(np.int32)
-                for name, v in (("ctx_len", lens), ("c_start", lens - qc), ("v_start", lens - 1),
-                                ("c_head", np.arange(B) * qc + qc - 1),
-                                ("step_start", np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]))):
-                    o, _ = g.meta_off[name]
-                    v = np.ascontiguousarray(v, dtype=np.int32).reshape(-1)
-                    mh[o: o + v.size] = v
-                with torch.cuda.stream(self.draft_stream):
-                    g.meta.copy_(g.meta_h, non_blocking=True)
-                self._launch_draft(g, s, qc)  # eager run, then capture (_replay)
-                self._launch_verify(g, s)
-                g.ev_res.synchronize()
+                # every catch-up width a round at this s can need: s+1, or up to
+                # s_prev+1 <= s_max+1 after the selector lowered s
+                for qc in range(s + 1, self.cfg.s_max + 2):
+                    if ("draft", g.gid, s, qc) in self.graphs:
+                        continue
+                    B = g.B
+                    lens = np.full(B, 2 * qc + 1, np.int64)
+                    mh = g.meta_h.numpy()
+                    mh[:] = 0
+                    o, _ = g.meta_off["w"]
+                    mh[o: o + 2 * self.K] = np.ones(self.K, np.float64).view(np.int32)
+                    for name, v in (("ctx_len", lens), ("c_start", lens - qc), ("v_start", lens - 1),
+                                    ("c_head", np.arange(B) * qc + qc - 1),
+                                    ("step_start", np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]))):
+                        o, _ = g.meta_off[name]
+                        v = np.ascontiguousarray(v, dtype=np.int32).reshape(-1)
+                        mh[o: o + v.size] = v
+                    with torch.cuda.stream(self.draft_stream):
+                        g.meta.copy_(g.meta_h, non_blocking=True)
+                    self._launch_draft(g, s, qc)  # eager run, then capture (_replay)
+                    if ("verify", g.gid, s) not in self.graphs:
+                        self._launch_verify(g, s)
+                    g.ev_res.synchronize()
+                    torch.cuda.synchronize(self.dev)
         torch.cuda.synchronize(self.dev)
 
     # ------------------------------------------------------------- host side
