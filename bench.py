@@ -190,9 +190,24 @@ def roofline_verify(engine, rounds, peaks):
         tot_bytes += b
         tot_t += r.t_verify_ms * 1e-3
     ach = tot_bytes / tot_t / 1e9
-    peak = peaks.get("hbm_gbs", 6551.0)
+    # measured copy bandwidth (MEASURED_PEAKS.json, driver-written) or the
+    # fallback of B200_PROFILING.md (6.65 TB/s) when the file is absent
+    peak = peaks.get("hbm_gbs")
+    src = "measured"
+    if not peak:
+        peak, src = 6650.0, "fallback"
+    traffic, tnote = None, None
+    try:  # ncu --metrics dram__bytes_{read,write}.sum of one verify forward (profiles/)
+        with open(os.path.join(ROOT, "profiles", "r1h_verify_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr["model"] == c.name.split("/")[0] and engine.B == tr["B"] and not getattr(engine, "tp", False):
+            traffic = tr["dram_bytes"]
+            tnote = (f"ncu DRAM bytes of one verify forward at Q={tr['Q']}, ctx={tr['ctx']} "
+                     f"(algorithmic {tr['algorithmic_bytes']} B: {tr['dram_bytes'] / tr['algorithmic_bytes']:.3f}x)")
+    except (OSError, KeyError, ValueError):
+        pass
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(ach / peak, 4), "traffic": None,
+            "frac": round(ach / peak, 4), "peak_source": src, "traffic": traffic, "traffic_note": tnote,
             "kernel": "verify forward (ms_linear x4/layer + attention + LM head), per round",
             "bytes_per_launch": round(tot_bytes / max(len(rounds), 1)),
             "mean_ms": round(tot_t * 1e3 / max(len(rounds), 1), 3)}
