@@ -4,8 +4,8 @@
   `context_cap`, `next_dist(context) -> ProbDist` (aggspec/oracles.py:19-26).
 * `draft_sequence(oracle, context, s, rng)` — s autoregressive steps, same
   signature / errors / RNG use as aggspec/oracles.py:135-153.
-* `OPTOracle` — a GPU model (opt.OPTModel on libminions kernels) behind that
-  protocol, greedy: next_dist is the point mass on the first-index argmax.  It
+* `GPUOracle` (alias `OPTOracle`) — a GPU model of either family (OPT or
+  Llama-2, models.make_model on libminions kernels) behind that protocol, greedy: next_dist is the point mass on the first-index argmax.  It
   keeps a one-slot KV cache and feeds only the context suffix it has not seen,
   so the reference's per-position call pattern (draft_sequence, the verify
   loop of aggspec/engine.py:294-296) costs one decode step per call instead of
@@ -22,9 +22,10 @@ import torch
 from . import _dev
 from . import _native
 from .core import ContextTooLong, ProbDist
-from .opt import KVCache, OPTModel, OPTWeights
+from .models import make_model
+from .opt import KVCache
 
-__all__ = ["ContextTooLong", "ModelOracle", "draft_sequence", "OPTOracle"]
+__all__ = ["ContextTooLong", "ModelOracle", "draft_sequence", "GPUOracle", "OPTOracle"]
 
 DEFAULT_CONTEXT_CAP = 4096
 
@@ -61,15 +62,15 @@ def draft_sequence(oracle: ModelOracle, context: Sequence[int], s: int,
     return toks, dists
 
 
-class OPTOracle:
-    """Greedy GPU model behind the ModelOracle protocol."""
+class GPUOracle:
+    """Greedy GPU model (OPT or Llama-2 weights) behind the ModelOracle protocol."""
 
-    def __init__(self, weights: OPTWeights, context_cap: int = 1024, device="cuda"):
+    def __init__(self, weights, context_cap: int = 1024, device="cuda"):
         _dev.require_cuda()
         self.cfg = weights.cfg
         self.vocab_size = weights.cfg.vocab
         self.context_cap = context_cap
-        self.model = OPTModel(weights, max_rows=context_cap, device=device)
+        self.model = make_model(weights, max_rows=context_cap, device=device)
         self.cache = KVCache(weights.cfg, 1, context_cap + 1, device)
         self.dev = torch.device(device)
         self._seen: list[int] = []  # tokens whose KV is cached
@@ -100,3 +101,6 @@ class OPTOracle:
         p = np.zeros(self.vocab_size)
         p[self.argmax_next(context)] = 1.0
         return ProbDist(p)
+
+
+OPTOracle = GPUOracle  # the name the OPT-only first version exported

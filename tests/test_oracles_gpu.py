@@ -54,3 +54,21 @@ def test_context_errors():
         o.next_dist([])
     with pytest.raises(ContextTooLong):
         o.next_dist(list(range(300)))
+
+
+def test_llama_oracle_greedy_matches_reference():
+    """GPUOracle over Llama-2-family weights (the headline model family) drives
+    the reference's per-position protocol; greedy drafts agree with the fp32
+    CPU Llama reference."""
+    from oracle import llama_ref
+    from paper_2402_15678_b200.core import seeded_rng
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    from paper_2402_15678_b200.oracles import GPUOracle, ModelOracle, draft_sequence
+    cfg = CONFIGS["tiny-llama"]
+    w = LlamaWeights.random(cfg, 2, device="cpu", std=0.05, norm_std=0.1)
+    o = GPUOracle(w.to("cuda"), context_cap=256)
+    assert isinstance(o, ModelOracle)
+    ctx = list(range(7, 20))
+    toks, _ = draft_sequence(o, ctx, 6, seeded_rng(0, "draft/req-000/0"))
+    want = llama_ref.greedy_generate(w.t, cfg, ctx, 6)
+    assert sum(int(a == b) for a, b in zip(toks, want)) >= 5
