@@ -253,6 +253,34 @@ int ms_accept_stochastic(const int32_t* draft, const double* q, const double* o,
                          int32_t* emitted, int32_t* n_emit, int32_t* finished,
                          int32_t* n_draws, void* stream);
 
+/* ---- grouped drafters -------------------------------------------------------
+ * The K drafters of a round (same architecture, own weights) run as ONE
+ * launch per op: G row groups, group k = drafter k, each with its own weights
+ * (stacked [G, ...]) and its own KV-cache slots.  Rows of group g are rows
+ * g*M .. g*M + M-1 of x / out (M rows per group).  Replaces the per-drafter
+ * loop of draft_sequence calls in _do_draft_batch (aggspec/engine.py:262-276).
+ *   ms_linear_grouped: W = [G*N, K] (group g's weight = rows g*N..), bias [G*N],
+ *     cluster split-K schedule, otherwise as ms_linear.
+ *   ms_gemv_grouped:   group g's weight at w + g*w_gstride elements.
+ *   ms_embed_grouped / ms_rmsnorm_grouped: output row r uses table / gain
+ *     number r / rpg (stride tstride / gstride elements).
+ *   ms_draft_commit_grouped: tok [G*B] -> drafts[b, k, j] = tok[k*B + b] (with
+ *     drafter k's fidelity[k], host array of G <= 8 floats), next_tok [G*B]. */
+int ms_linear_grouped(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                      int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                      int splits, int G, void* stream);
+int ms_gemv_grouped(const void* x, int64_t ldx, const void* w, int64_t w_gstride, const void* bias,
+                    const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N,
+                    int K, int act, int G, void* stream);
+int ms_embed_grouped(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb, int64_t tstride,
+                     int rpg, const void* pos_emb, int pos_offset, int R, int d, void* out, void* stream);
+int ms_rmsnorm_grouped(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, int64_t gstride,
+                       int rpg, float eps, int R, int d, void* out, int64_t ldo, void* stream);
+int ms_draft_commit_grouped(const int32_t* tok, const int32_t* ctx_len, int B, int j, int G, int S,
+                            const int32_t* teacher, int64_t ld_teacher, const int32_t* req_key,
+                            const float* fidelity, uint64_t seed, int32_t* drafts, int32_t* next_tok,
+                            void* stream);
+
 /* ---- tensor-parallel verify over peer memory -----------------
  * Symmetric buffers: ms_ipc_alloc cudaMallocs `bytes` (zeroed) and exports a
  * CUDA IPC handle (ms_ipc_handle_size() bytes) that peers open with

@@ -75,17 +75,22 @@ struct LinearCfg {
     int st = budget / STAGE_BYTES;
     return st < 2 ? 2 : (st > MAX_STAGES ? MAX_STAGES : st);
   }
-  __host__ __device__ static int data_bytes(int stages) {
+  // the fp32 partial tile is staged in the (idle) pipeline smem only for the
+  // split-K cluster reduction; the single-split gated epilogue exchanges
+  // gate/up through a 4 KB buffer instead
+  __host__ __device__ static int data_bytes(int stages, bool part) {
     const int pipe = stages * STAGE_BYTES;
-    return pipe > PART_BYTES ? pipe : PART_BYTES;
+    const int need = part ? PART_BYTES : 4096;
+    return pipe > need ? pipe : need;
   }
-  __host__ __device__ static int smem(int stages) {
-    return 1024 + data_bytes(stages) + (3 * MAX_STAGES + 1) * 8 + 16 + 2 * BN * 4;
+  __host__ __device__ static int smem(int stages, bool part) {
+    return 1024 + data_bytes(stages, part) + (3 * MAX_STAGES + 1) * 8 + 16 + 2 * BN * 4;
   }
 };
 
-__device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v) {
-  if (p.bias) v += bf2f(p.bias[feat]);
+// tok: global output row; feat: feature within the row group grp
+__device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v, int grp = 0) {
+  if (p.bias) v += bf2f(p.bias[(int64_t)grp * p.N + feat]);
   if (p.act == 1) v = fmaxf(v, 0.0f);
   if (p.residual) v += bf2f(p.residual[(int64_t)tok * p.ldr + feat]);
   if (p.out_f32)
@@ -93,6 +98,8 @@ __device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int fe
   else
     reinterpret_cast<__nv_bfloat16*>(p.out)[(int64_t)tok * p.ldc + feat] = f2bf(v);
 }
+
+__device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -118,7 +125,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   uint8_t* sW = smem;
   const int STAGES = p.stages;
   uint8_t* sX = smem + STAGES * C::W_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::data_bytes(STAGES));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::data_bytes(STAGES, p.splits > 1));
   uint64_t* empty = full + C::MAX_STAGES;
   uint64_t* tmem_full = empty + C::MAX_STAGES;
   uint64_t* normed = tmem_full + 1;  // [MAX_STAGES] X tile normalised (fused LayerNorm)
@@ -133,6 +140,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   const int split = blockIdx.x - tile_n * p.splits;
   const int n0 = tile_n * kBM;
   const int m0 = blockIdx.y * BN;
+  // row group (grouped drafters): M rows of X / out and N rows of W per group
+  const int grp = blockIdx.z;
+  const int wrow = grp * p.N + n0, xrow = grp * p.M + m0, orow = grp * p.M + m0;
   const int kb0 = (int)((int64_t)split * p.kb_total / p.splits);
   const int kb1 = (int)((int64_t)(split + 1) * p.kb_total / p.splits);
 
@@ -165,7 +175,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       const int pre = nkb < STAGES ? nkb : STAGES;
       for (int i = 0; i < pre; ++i) {
         tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (kb0 + i) * kBK, n0, pol_w);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (kb0 + i) * kBK, wrow, pol_w);
       }
       pdl_wait();
       pdl_trigger();
@@ -175,9 +185,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         if (i >= pre) {
           tc::mbar_wait(&empty[stage], ((i / STAGES) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, n0, pol_w);
+          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, wrow, pol_w);
         }
-        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, m0, pol_x);
+        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, xrow, pol_x);
       }
     } else {
       pdl_trigger();
@@ -274,7 +284,32 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 
-    if (p.splits == 1 && p.act != 2) {
+    if (p.splits == 1 && p.act == 2) {
+      // gated SiLU, one split: the up warps (TMEM lanes 64..127) hand their
+      // 16-column chunk to the gate warps (lanes 0..63) through 4 KB of smem
+      // (the pipeline smem is idle once tmem_full fired)
+      float* xb = reinterpret_cast<float*>(smem);  // [64][17]
+      const bool up = q >= 2;
+      const int of = tile_n * (kBM / 2) + (q & 1) * 32 + lane;  // output feature (gate warps)
+      for (int c0 = 0; c0 < m_hi; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(trow + c0, r);
+        tc::tmem_wait_ld();
+        if (up) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xb[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+        }
+        epi_bar128();
+        if (!up) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + of;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < m_hi)
+              o[(int64_t)(orow + c0 + j) * p.ldc] = f2bf(silu_mul(__uint_as_float(r[j]), xb[(q * 32 + lane) * 17 + j]));
+        }
+        epi_bar128();
+      }
+    } else if (p.splits == 1) {
       for (int c0 = 0; c0 < m_hi; c0 += 16) {
         uint32_t r[16];
         tc::tmem_ld16(trow + c0, r);
@@ -282,7 +317,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         if (feat_ok) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi) epi_store(p, m0 + c0 + j, feat, __uint_as_float(r[j]));
+            if (c0 + j < m_hi) epi_store(p, orow + c0 + j, feat, __uint_as_float(r[j]), grp);
         }
       }
     } else {
@@ -298,7 +333,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       }
     }
   }
-  if (p.splits > 1 || p.act == 2) {
+  if (p.splits > 1) {
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
     // `split` reduces a 1/splits slice of the tile, adding the partials of
@@ -334,7 +369,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
         const float u4[4] = {up.x, up.y, up.z, up.w};
         const int of = tile_n * (kBM / 2) + f4;  // output feature
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(m0 + j) * p.ldc + of;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
 #pragma unroll
         for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
         continue;
@@ -342,7 +377,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       const int feat = n0 + f4;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (feat + t < p.N) epi_store(p, m0 + j, feat + t, a4[t]);
+        if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
     }
     if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
   }
@@ -397,7 +432,6 @@ __device__ __forceinline__ int sk_owner(int i, int iters, int G) {
   return c;
 }
 
-__device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -654,25 +688,26 @@ static int pick_bn(int M) {
 
 template <int BN>
 static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p,
-                         int m_tiles, cudaStream_t st) {
+                         int m_tiles, cudaStream_t st, int G) {
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::smem(C::stages_for(1))) != cudaSuccess)
+                             C::smem(C::stages_for(1), true)) != cudaSuccess)
       return MS_ERR_CUDA;
     attr_set = true;
   }
-  const int grid = p.n_tiles * p.splits * m_tiles;
+  const int grid = p.n_tiles * p.splits * m_tiles * G;
   // never deeper than the k-blocks a CTA streams: small (SSM) GEMMs then use
   // little shared memory and several kernels / streams can share an SM
   const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
+  const bool part = p.splits > 1;
   p.stages = C::stages_for(grid <= 148 ? 1 : 2);
-  // the fp32 staging tile (split-K / gated epilogue) may already rule out two
-  // CTAs per SM: then take the deep single-CTA pipeline
-  if ((p.splits > 1 || p.act == 2) && C::smem(p.stages) > 113 * 1024) p.stages = C::stages_for(1);
+  // the fp32 split-K staging tile may already rule out two CTAs per SM: then
+  // take the deep single-CTA pipeline
+  if (part && C::smem(p.stages, part) > 113 * 1024) p.stages = C::stages_for(1);
   if (p.stages > kb_per_cta) p.stages = kb_per_cta < 2 ? 2 : kb_per_cta;
-  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles), dim3(kThreads), C::smem(p.stages), st,
+  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(p.stages, part), st,
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
@@ -736,7 +771,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
                        const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
                        int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
                        int* counters, int n_counters, const void* g_ln_g, const void* g_ln_b,
-                       float g_ln_eps, void* stream) {
+                       float g_ln_eps, void* stream, int G = 1) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
@@ -752,8 +787,9 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   const int n_tiles = (N + kBM - 1) / kBM;
   if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
   CUtensorMap tw, tx;
-  if (!make_tmap(&tw, w, N, K, K, kBM)) return MS_ERR_CUDA;
-  if (!make_tmap(&tx, x, M, K, ldx, bn)) return MS_ERR_CUDA;
+  if (G < 1 || G > 65535 || (G > 1 && g_ln_g)) return MS_ERR_VALUE;
+  if (!make_tmap(&tw, w, (int64_t)G * N, K, K, kBM)) return MS_ERR_CUDA;
+  if (!make_tmap(&tx, x, (int64_t)G * M, K, ldx, bn)) return MS_ERR_CUDA;
   LinearParams p;
   p.M = M; p.N = N; p.K = K;
   p.bias = (const __nv_bfloat16*)bias;
@@ -771,7 +807,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   cudaStream_t st = (cudaStream_t)stream;
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
-  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 &&
+  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 &&
       ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
     SKParams sk;
     sk.iters = n_tiles * kb_total;
@@ -803,22 +839,22 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
   p.splits = splits;
   switch (bn) {
-    case 16: return launch_linear<16>(tw, tx, p, m_tiles, st);
-    case 32: return launch_linear<32>(tw, tx, p, m_tiles, st);
-    case 48: return launch_linear<48>(tw, tx, p, m_tiles, st);
-    case 64: return launch_linear<64>(tw, tx, p, m_tiles, st);
-    case 80: return launch_linear<80>(tw, tx, p, m_tiles, st);
-    case 96: return launch_linear<96>(tw, tx, p, m_tiles, st);
-    case 112: return launch_linear<112>(tw, tx, p, m_tiles, st);
-    case 128: return launch_linear<128>(tw, tx, p, m_tiles, st);
-    case 144: return launch_linear<144>(tw, tx, p, m_tiles, st);
-    case 160: return launch_linear<160>(tw, tx, p, m_tiles, st);
-    case 176: return launch_linear<176>(tw, tx, p, m_tiles, st);
-    case 192: return launch_linear<192>(tw, tx, p, m_tiles, st);
-    case 208: return launch_linear<208>(tw, tx, p, m_tiles, st);
-    case 224: return launch_linear<224>(tw, tx, p, m_tiles, st);
-    case 240: return launch_linear<240>(tw, tx, p, m_tiles, st);
-    default: return launch_linear<256>(tw, tx, p, m_tiles, st);
+    case 16: return launch_linear<16>(tw, tx, p, m_tiles, st, G);
+    case 32: return launch_linear<32>(tw, tx, p, m_tiles, st, G);
+    case 48: return launch_linear<48>(tw, tx, p, m_tiles, st, G);
+    case 64: return launch_linear<64>(tw, tx, p, m_tiles, st, G);
+    case 80: return launch_linear<80>(tw, tx, p, m_tiles, st, G);
+    case 96: return launch_linear<96>(tw, tx, p, m_tiles, st, G);
+    case 112: return launch_linear<112>(tw, tx, p, m_tiles, st, G);
+    case 128: return launch_linear<128>(tw, tx, p, m_tiles, st, G);
+    case 144: return launch_linear<144>(tw, tx, p, m_tiles, st, G);
+    case 160: return launch_linear<160>(tw, tx, p, m_tiles, st, G);
+    case 176: return launch_linear<176>(tw, tx, p, m_tiles, st, G);
+    case 192: return launch_linear<192>(tw, tx, p, m_tiles, st, G);
+    case 208: return launch_linear<208>(tw, tx, p, m_tiles, st, G);
+    case 224: return launch_linear<224>(tw, tx, p, m_tiles, st, G);
+    case 240: return launch_linear<240>(tw, tx, p, m_tiles, st, G);
+    default: return launch_linear<256>(tw, tx, p, m_tiles, st, G);
   }
 }
 
@@ -840,3 +876,10 @@ extern "C" int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const
                      0, nullptr, 0, gamma, beta, eps, stream);
 }
 
+
+extern "C" int ms_linear_grouped(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                                 int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                                 int splits, int G, void* stream) {
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
+                     nullptr, nullptr, 0.f, stream, G);
+}

@@ -40,8 +40,18 @@ template <int MT>  // 16-row token tiles
 __global__ void __launch_bounds__(kGvWarps * 32)
 gemv_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const __nv_bfloat16* __restrict__ w,
             const __nv_bfloat16* __restrict__ bias, const __nv_bfloat16* __restrict__ residual,
-            int64_t ldr, void* __restrict__ out, int64_t ldc, int out_f32, int M, int N, int K, int act) {
+            int64_t ldr, void* __restrict__ out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+            int64_t w_gstride) {
   __shared__ float red[kGvWarps][MT * 16][kGvN + 1];
+  // row group blockIdx.y (grouped drafters): its M rows, its own weight
+  {
+    const int grp = blockIdx.y;
+    x += (int64_t)grp * M * ldx;
+    w += grp * w_gstride;
+    if (bias) bias += (int64_t)grp * N;
+    if (residual) residual += (int64_t)grp * M * ldr;
+    out = reinterpret_cast<char*>(out) + (int64_t)grp * M * ldc * (out_f32 ? 4 : 2);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const bool gated = act == 2;
@@ -157,18 +167,18 @@ int preload_gemv() {
 
 }  // namespace ms
 
-extern "C" int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
-                       int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
-                       void* stream) {
-  if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
+extern "C" int ms_gemv_grouped(const void* x, int64_t ldx, const void* w, int64_t w_gstride, const void* bias,
+                               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N,
+                               int K, int act, int G, void* stream) {
+  if (M < 0 || N < 1 || K < 1 || G < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
   if (!x || !w || !out) return MS_ERR_VALUE;
   if (act < 0 || act > 2) return MS_ERR_VALUE;
   if (act == 2 && (N % 128 || bias || residual || out_f32)) return MS_ERR_UNSUPPORTED;
-  if (M > 64 || K % 32 || ldx % 8) return MS_ERR_UNSUPPORTED;
+  if (M > 64 || K % 32 || ldx % 8 || w_gstride % 8) return MS_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
-  const dim3 grid((N + ms::kGvN - 1) / ms::kGvN);
+  const dim3 grid((N + ms::kGvN - 1) / ms::kGvN, G);
   const dim3 block(ms::kGvWarps * 32);
   cudaStream_t st = (cudaStream_t)stream;
   const auto* xb = (const __nv_bfloat16*)x;
@@ -176,9 +186,15 @@ extern "C" int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bi
   const auto* bb = (const __nv_bfloat16*)bias;
   const auto* rb = (const __nv_bfloat16*)residual;
   switch ((M + 15) / 16) {
-    case 1: return ms::launch(ms::gemv_kernel<1>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act);
-    case 2: return ms::launch(ms::gemv_kernel<2>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act);
-    case 3: return ms::launch(ms::gemv_kernel<3>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act);
-    default: return ms::launch(ms::gemv_kernel<4>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act);
+    case 1: return ms::launch(ms::gemv_kernel<1>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act, w_gstride);
+    case 2: return ms::launch(ms::gemv_kernel<2>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act, w_gstride);
+    case 3: return ms::launch(ms::gemv_kernel<3>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act, w_gstride);
+    default: return ms::launch(ms::gemv_kernel<4>, grid, block, 0, st, 1, xb, ldx, wb, bb, rb, ldr, out, ldc, out_f32, M, N, K, act, w_gstride);
   }
+}
+
+extern "C" int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                       int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                       void* stream) {
+  return ms_gemv_grouped(x, ldx, w, 0, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, 1, stream);
 }

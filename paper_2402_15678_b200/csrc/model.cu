@@ -22,11 +22,12 @@ namespace ms {
 // ---------------------------------------------------------------------------
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ start, int Q,
                              const __nv_bfloat16* __restrict__ te, const __nv_bfloat16* __restrict__ pe,
-                             int pos_offset, int d, __nv_bfloat16* __restrict__ out) {
+                             int pos_offset, int d, __nv_bfloat16* __restrict__ out, int rpg, int64_t tstride) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   const int pos = start[r / Q] + r % Q;
+  if (rpg > 0) te += (int64_t)(r / rpg) * tstride;  // row group = its own table (grouped drafters)
   const bf16x8* a = reinterpret_cast<const bf16x8*>(te + (int64_t)tok[r] * d);
   const bf16x8* b = pe ? reinterpret_cast<const bf16x8*>(pe + (int64_t)(pos + pos_offset) * d) : nullptr;
   bf16x8* o = reinterpret_cast<bf16x8*>(out + (int64_t)r * d);
@@ -52,10 +53,11 @@ template <int VPT, bool RMS = false>  // bf16x8 vectors per thread
 __global__ void __launch_bounds__(128)
 layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t* __restrict__ rows,
                  const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, float eps,
-                 int d, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+                 int d, __nv_bfloat16* __restrict__ out, int64_t ldo, int rpg, int64_t gstride) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
+  if (rpg > 0) g += (int64_t)(r / rpg) * gstride;  // output-row group = its own gain (grouped drafters)
   const int nv = d / 8;
   const bf16x8* xr = reinterpret_cast<const bf16x8*>(x + (int64_t)(rows ? rows[r] : r) * ldx);
   float v[VPT][8];
@@ -173,20 +175,27 @@ int preload_model() {
 
 }  // namespace ms
 
-extern "C" int ms_embed(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,
-                        const void* pos_emb, int pos_offset, int R, int d, void* out, void* stream) {
-  if (R < 0 || d < 8 || Q < 1) return MS_ERR_VALUE;
+extern "C" int ms_embed_grouped(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,
+                                int64_t tstride, int rpg, const void* pos_emb, int pos_offset, int R, int d,
+                                void* out, void* stream) {
+  if (R < 0 || d < 8 || Q < 1 || rpg < 0) return MS_ERR_VALUE;
   if (d % 8) return MS_ERR_UNSUPPORTED;
   if (R == 0) return MS_OK;
   if (!tok || !start || !tok_emb || !out) return MS_ERR_VALUE;
   return ms::launch(ms::embed_kernel, dim3(R), dim3(128), 0, (cudaStream_t)stream, 1, tok, start, Q,
                     (const __nv_bfloat16*)tok_emb, (const __nv_bfloat16*)pos_emb, pos_offset, d,
-                    (__nv_bfloat16*)out);
+                    (__nv_bfloat16*)out, rpg, tstride);
+}
+
+extern "C" int ms_embed(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,
+                        const void* pos_emb, int pos_offset, int R, int d, void* out, void* stream) {
+  return ms_embed_grouped(tok, start, Q, tok_emb, 0, 0, pos_emb, pos_offset, R, d, out, stream);
 }
 
 template <bool RMS>
 static int norm_launch(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, const void* beta,
-                       float eps, int R, int d, void* out, int64_t ldo, void* stream) {
+                       float eps, int R, int d, void* out, int64_t ldo, void* stream, int rpg = 0,
+                       int64_t gstride = 0) {
   if (R < 0 || d < 8) return MS_ERR_VALUE;
   if (d % 8 || d > 8 * 128 * 8 || ldx % 8 || ldo % 8) return MS_ERR_UNSUPPORTED;
   if (R == 0) return MS_OK;
@@ -198,14 +207,14 @@ static int norm_launch(const void* x, int64_t ldx, const int32_t* rows, const vo
   auto* b = (const __nv_bfloat16*)beta;
   auto* o = (__nv_bfloat16*)out;
   switch (vpt) {
-    case 1: return ms::launch(ms::layernorm_kernel<1, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 2: return ms::launch(ms::layernorm_kernel<2, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 3: return ms::launch(ms::layernorm_kernel<3, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 4: return ms::launch(ms::layernorm_kernel<4, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 5: return ms::launch(ms::layernorm_kernel<5, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 6: return ms::launch(ms::layernorm_kernel<6, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    case 7: return ms::launch(ms::layernorm_kernel<7, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
-    default: return ms::launch(ms::layernorm_kernel<8, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo);
+    case 1: return ms::launch(ms::layernorm_kernel<1, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 2: return ms::launch(ms::layernorm_kernel<2, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 3: return ms::launch(ms::layernorm_kernel<3, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 4: return ms::launch(ms::layernorm_kernel<4, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 5: return ms::launch(ms::layernorm_kernel<5, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 6: return ms::launch(ms::layernorm_kernel<6, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    case 7: return ms::launch(ms::layernorm_kernel<7, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
+    default: return ms::launch(ms::layernorm_kernel<8, RMS>, dim3(R), dim3(128), 0, st, 1, xi, ldx, rows, g, b, eps, d, o, ldo, rpg, gstride);
   }
 }
 
@@ -218,6 +227,13 @@ extern "C" int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, con
 extern "C" int ms_rmsnorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, float eps,
                           int R, int d, void* out, int64_t ldo, void* stream) {
   return norm_launch<true>(x, ldx, rows, gamma, nullptr, eps, R, d, out, ldo, stream);
+}
+
+extern "C" int ms_rmsnorm_grouped(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,
+                                  int64_t gstride, int rpg, float eps, int R, int d, void* out, int64_t ldo,
+                                  void* stream) {
+  if (rpg < 1) return MS_ERR_VALUE;
+  return norm_launch<true>(x, ldx, rows, gamma, nullptr, eps, R, d, out, ldo, stream, rpg, gstride);
 }
 
 extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,

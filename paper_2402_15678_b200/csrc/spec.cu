@@ -47,6 +47,37 @@ __global__ void draft_commit_kernel(const int32_t* __restrict__ tok, const int32
   if (next_tok) next_tok[b] = t;
 }
 
+// Grouped form (the K drafters batched as row groups, tok [G*B], group k =
+// drafter k): drafts[b, k, j] = tok[k*B + b] (with drafter k's fidelity).
+struct Fidelity8 {
+  float f[8];
+};
+
+__global__ void draft_commit_grouped_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ ctx_len,
+                                            int B, int j, int G, int S, const int32_t* __restrict__ teacher,
+                                            int64_t ld_teacher, const int32_t* __restrict__ req_key,
+                                            Fidelity8 fid, uint64_t seed, int32_t* __restrict__ drafts,
+                                            int32_t* __restrict__ next_tok) {
+  pdl_wait();
+  pdl_trigger();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G * B) return;
+  const int k = e / B, b = e - k * B;
+  int t = tok[e];
+  if (teacher) {
+    const int64_t p = (int64_t)ctx_len[b] + j;
+    const uint64_t key = (uint64_t)(uint32_t)req_key[b];
+    const uint64_t h = splitmix64(seed ^ splitmix64((key << 40) ^ ((uint64_t)k << 32) ^ (uint64_t)p));
+    const float u = (float)(h >> 40) * (1.0f / 16777216.0f);
+    if (u < fid.f[k] && p < ld_teacher) {
+      const int32_t tt = teacher[(int64_t)b * ld_teacher + p];
+      if (tt >= 0) t = tt;
+    }
+  }
+  drafts[((int64_t)b * G + k) * S + j] = t;
+  if (next_tok) next_tok[e] = t;
+}
+
 __global__ void pack_verify_kernel(const int32_t* __restrict__ last, const int32_t* __restrict__ path,
                                    int B, int S, int32_t* __restrict__ vin) {
   pdl_wait();
@@ -57,7 +88,9 @@ __global__ void pack_verify_kernel(const int32_t* __restrict__ last, const int32
   vin[e] = i == 0 ? last[b] : path[(int64_t)b * S + i - 1];
 }
 
-int preload_spec() { return preload_fn(draft_commit_kernel) + preload_fn(pack_verify_kernel); }
+int preload_spec() {
+  return preload_fn(draft_commit_kernel) + preload_fn(draft_commit_grouped_kernel) + preload_fn(pack_verify_kernel);
+}
 
 }  // namespace ms
 
@@ -81,4 +114,18 @@ extern "C" int ms_pack_verify(const int32_t* last, const int32_t* path, int B, i
   const int n = B * (S + 1);
   return ms::launch(ms::pack_verify_kernel, dim3((n + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1,
                     last, path, B, S, vin);
+}
+
+extern "C" int ms_draft_commit_grouped(const int32_t* tok, const int32_t* ctx_len, int B, int j, int G, int S,
+                                       const int32_t* teacher, int64_t ld_teacher, const int32_t* req_key,
+                                       const float* fidelity, uint64_t seed, int32_t* drafts, int32_t* next_tok,
+                                       void* stream) {
+  if (B < 0 || G < 1 || G > 8 || S < 1 || j < 0 || j >= S) return MS_ERR_VALUE;
+  if (B == 0) return MS_OK;
+  if (!tok || !ctx_len || !drafts || (teacher && (!req_key || !fidelity))) return MS_ERR_VALUE;
+  ms::Fidelity8 f;
+  for (int k = 0; k < 8; ++k) f.f[k] = (fidelity && k < G) ? fidelity[k] : 0.f;
+  const int n = G * B;
+  return ms::launch(ms::draft_commit_grouped_kernel, dim3((n + 127) / 128), dim3(128), 0, (cudaStream_t)stream, 1,
+                    tok, ctx_len, B, j, G, S, teacher, ld_teacher, req_key, f, seed, drafts, next_tok);
 }

@@ -37,6 +37,7 @@ len(context_before_round) + lcp(its draft, emitted) positions.
 """
 from __future__ import annotations
 
+import ctypes
 import time
 import zlib
 from dataclasses import dataclass, field
@@ -47,6 +48,9 @@ import torch
 from . import _dev
 from . import _native
 from .core import AggSpecError, EngineConfig, Request, RequestState, validate_config
+import os
+
+from .llama import GroupedLlamaModel
 from .models import make_model
 from .opt import KVCache
 from .selector import Decision, MonitorSample, SelectorState, maybe_adjust, observe
@@ -115,8 +119,21 @@ class _Group:
         z = lambda *sh: torch.zeros(sh, dtype=I32, device=dev)  # noqa: E731
         sizes = [("w", 2 * K), ("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
                  ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
+        if eng.grouped:  # the drafters' inputs replicated per row group (drafter)
+            sizes += [("g_c_start", K * B), ("g_c_head", K * B), ("g_step_start", s_cap * K * B),
+                      ("g_c_tok", K * B * (s_cap + 1))]
         self.meta, self.meta_h, self.meta_off = self._packed(sizes, dev)
         mv = lambda n: self.meta[self.meta_off[n][0]: sum(self.meta_off[n])]  # noqa: E731
+        if eng.grouped:
+            self.g_c_start, self.g_c_head = mv("g_c_start"), mv("g_c_head")
+            self.g_step_start = mv("g_step_start").view(s_cap, K * B)
+            self.g_c_tok = mv("g_c_tok")
+            self.g_slot = torch.tensor([k * eng.B + slot0 + b for k in range(K) for b in range(B)], dtype=I32,
+                                       device=dev)
+            self.g_step_tok = z(K * B, 1)
+            self.g_argmax = z(K * B)
+            self.g_ws = torch.zeros(K * B, dtype=torch.int64, device=dev)
+            self.g_logits = torch.empty(K * B, V, device=dev)
         self.w_dev = mv("w").view(torch.float64)
         self.ctx_len, self.c_start, self.c_head = mv("ctx_len"), mv("c_start"), mv("c_head")
         self.v_start, self.last, self.remaining = mv("v_start"), mv("last"), mv("remaining")
@@ -205,9 +222,19 @@ class SpecEngine:
             raise ValueError("drafters and target must share a vocabulary")
         self.V = V
         self.sync_time = sync_time
-        self.ssms = [make_model(w, max_rows=slots * max_len, device=device, small_gemm=True) for w in drafters]
+        # K Llama drafters of one architecture run as row groups of one model
+        # (one launch per op for all drafters); MS_GROUPED_DRAFT=0 disables
+        self.grouped = (len(drafters) > 1 and all(getattr(w.cfg, "family", "") == "llama" for w in drafters)
+                        and all(w.cfg == drafters[0].cfg for w in drafters)
+                        and os.environ.get("MS_GROUPED_DRAFT", "1") != "0")
+        self.ssms = [] if self.grouped else [make_model(w, max_rows=slots * max_len, device=device, small_gemm=True)
+                                             for w in drafters]
+        if self.grouped:
+            self.ssm_g = GroupedLlamaModel(drafters, max_rows=slots * max_len, device=device)
+            self.s_cache_g = KVCache(drafters[0].cfg, self.K * slots, max_len, device)
+            self.fid_arr = None
         self.t_cache = KVCache(self.target.cfg, slots, max_len, device)
-        self.s_caches = [KVCache(w.cfg, slots, max_len, device) for w in drafters]
+        self.s_caches = [] if self.grouped else [KVCache(w.cfg, slots, max_len, device) for w in drafters]
         ng = 2 if pipelined else 1
         gb = slots // ng
         self.groups = [_Group(self, g, g * gb, gb) for g in range(ng)]
@@ -264,6 +291,11 @@ class SpecEngine:
             dummy = torch.empty(0, self.V, device=self.dev)
             for m, c in zip(self.ssms, self.s_caches):
                 m.forward(t, zero, self.slot, c, dummy, head_rows=empty)
+            if self.grouped:
+                G = self.K
+                self.ssm_g.forward(t.repeat(G, 1), torch.zeros(G * self.B, dtype=I32, device=self.dev),
+                                   torch.arange(G * self.B, dtype=I32, device=self.dev), self.s_cache_g, dummy,
+                                   head_rows=empty)
         for r in requests:
             if r.remaining <= 0 and r.state != RequestState.FINISHED:
                 r.state = RequestState.FINISHED
@@ -285,6 +317,13 @@ class SpecEngine:
     def _device_draft(self, g: _Group, s: int, qc: int) -> None:
         """K drafters (concurrent streams) + vote + verifier input rows."""
         main = torch.cuda.current_stream(self.dev)
+        if self.grouped:
+            self._draft_grouped(g, s, qc)
+            sp = _dev.stream_ptr(main)
+            _native.call("ms_vote", g.drafts_s(s).data_ptr(), g.w_dev.data_ptr(), None, g.B, self.K, s,
+                         g.path.data_ptr(), g.voted.data_ptr(), sp)
+            _native.call("ms_pack_verify", g.last.data_ptr(), g.path.data_ptr(), g.B, s, g.vin.data_ptr(), sp)
+            return
         ev0 = torch.cuda.Event()
         ev0.record(main)
         done = []
@@ -302,6 +341,38 @@ class SpecEngine:
         _native.call("ms_vote", g.drafts_s(s).data_ptr(), g.w_dev.data_ptr(), None, g.B, self.K, s,
                      g.path.data_ptr(), g.voted.data_ptr(), sp)
         _native.call("ms_pack_verify", g.last.data_ptr(), g.path.data_ptr(), g.B, s, g.vin.data_ptr(), sp)
+
+    def _draft_grouped(self, g: _Group, s: int, qc: int) -> None:
+        """All K drafters' s steps as row groups of one model (one launch per op)."""
+        B, G, m = g.B, self.K, self.ssm_g
+        sp = _dev.stream_ptr()
+        dr = g.drafts_s(s)
+        tok_in = g.g_c_tok[: G * B * qc].view(G * B, qc)
+        teacher = None
+        if self.teacher is not None:
+            teacher = self.teacher.data_ptr() + g.slot0 * self.max_len * 4
+        fid = (ctypes.c_float * 8)(*([float(f) for f in self.fidelity] if self.fidelity else [0.0] * G))
+        for j in range(s):
+            if j == 0:
+                m.forward(tok_in, g.g_c_start, g.g_slot, self.s_cache_g, g.g_logits, head_rows=g.g_c_head)
+            else:
+                m.forward(g.g_step_tok, g.g_step_start[j - 1], g.g_slot, self.s_cache_g, g.g_logits)
+            _native.call("ms_argmax_rows", g.g_logits.data_ptr(), 0, G * B, self.V, self.V,
+                         g.g_argmax.data_ptr(), g.g_ws.data_ptr(), sp)
+            _native.call("ms_draft_commit_grouped", g.g_argmax.data_ptr(), g.ctx_len.data_ptr(), B, j, G, s,
+                         teacher, self.max_len, g.req_key.data_ptr(), fid if self.fidelity else None,
+                         self.inject_seed, dr.data_ptr(), g.g_step_tok.data_ptr(), sp)
+
+    def _put_grouped_meta(self, g: _Group, put, start, c_head, steps, c_tok, qc) -> None:
+        """Replicate the drafters' round inputs per row group (drafter)."""
+        if not self.grouped:
+            return
+        G, B = self.K, g.B
+        put("g_c_start", np.tile(np.asarray(start).reshape(-1), G))
+        put("g_c_head", np.concatenate([k * B * qc + np.asarray(c_head).reshape(-1) for k in range(G)]))
+        put("g_step_start", np.tile(np.asarray(steps).reshape(steps.shape[0], -1), (1, G)))
+        if c_tok is not None:
+            put("g_c_tok", np.tile(np.asarray(c_tok).reshape(B, -1), (G, 1)))
 
     def _draft(self, g: _Group, k: int, s: int, qc: int, st) -> None:
         B, m, cache = g.B, self.ssms[k], self.s_caches[k]
@@ -402,12 +473,16 @@ class SpecEngine:
                     mh[:] = 0
                     o, _ = g.meta_off["w"]
                     mh[o: o + 2 * self.K] = np.ones(self.K, np.float64).view(np.int32)
-                    for name, v in (("ctx_len", lens), ("c_start", lens - qc), ("v_start", lens - 1),
-                                    ("c_head", np.arange(B) * qc + qc - 1),
-                                    ("step_start", np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)]))):
+                    def put(name, v):
                         o, _ = g.meta_off[name]
                         v = np.ascontiguousarray(v, dtype=np.int32).reshape(-1)
                         mh[o: o + v.size] = v
+
+                    steps = np.stack([lens + j - 1 for j in range(1, self.cfg.s_max + 1)])
+                    for name, v in (("ctx_len", lens), ("c_start", lens - qc), ("v_start", lens - 1),
+                                    ("c_head", np.arange(B) * qc + qc - 1), ("step_start", steps)):
+                        put(name, v)
+                    self._put_grouped_meta(g, put, lens - qc, np.arange(B) * qc + qc - 1, steps, None, qc)
                     with torch.cuda.stream(self.draft_stream):
                         g.meta.copy_(g.meta_h, non_blocking=True)
                     self._launch_draft(g, s, qc)  # eager run, then capture (_replay)
@@ -459,6 +534,7 @@ class SpecEngine:
         put("remaining", rem)
         put("step_start", steps)
         put("c_tok", c_tok)
+        self._put_grouped_meta(g, put, start, c_head, steps, c_tok, qc)
         with torch.cuda.stream(self.draft_stream):
             g.meta.copy_(g.meta_h, non_blocking=True)
         self.h2d_bytes += g.meta_h.numel() * 4

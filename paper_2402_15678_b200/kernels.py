@@ -208,3 +208,58 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
                  None if ws is None else ws.counters.data_ptr(), 0 if ws is None else ws.counters.numel(),
                  _dev.stream_ptr(stream))
     return out
+
+
+# ------------------------------------------------------------ grouped drafters
+def linear_grouped(x: torch.Tensor, w: torch.Tensor, G: int, residual: torch.Tensor | None = None, act: int = 0,
+                   out: torch.Tensor | None = None, out_f32: bool = False, stream=None) -> torch.Tensor:
+    """G row groups in one launch: x [G*M, K], w [G*N, K] (stacked), out [G*M, N']."""
+    GM, K = x.shape
+    N = w.shape[0] // G
+    M = GM // G
+    if GM % G or w.shape[0] % G or w.shape[1] != K or x.dtype != BF16 or w.dtype != BF16 or not w.is_contiguous():
+        raise ValueError("x [G*M, K], w [G*N, K] bf16")
+    No = N // 2 if act == 2 else N
+    if out is None:
+        out = torch.empty((GM, No), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    _native.call("ms_linear_grouped", x.data_ptr(), x.stride(0), w.data_ptr(), None,
+                 None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
+                 out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, 0, G,
+                 _dev.stream_ptr(stream))
+    return out
+
+
+def gemv_grouped(x: torch.Tensor, w: torch.Tensor, G: int, residual: torch.Tensor | None = None, act: int = 0,
+                 out: torch.Tensor | None = None, out_f32: bool = False, stream=None) -> torch.Tensor:
+    """ms_gemv over G row groups: x [G*M, K] (M <= 64), w [G, N, K] stacked."""
+    GM, K = x.shape
+    M = GM // G
+    N = w.shape[-2]
+    if out is None:
+        out = torch.empty((GM, N // 2 if act == 2 else N), dtype=torch.float32 if out_f32 else BF16,
+                          device=x.device)
+    _native.call("ms_gemv_grouped", x.data_ptr(), x.stride(0), w.data_ptr(), N * K, None,
+                 None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
+                 out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, G,
+                 _dev.stream_ptr(stream))
+    return out
+
+
+def embed_grouped(tok: torch.Tensor, start: torch.Tensor, Q: int, tok_emb: torch.Tensor, rpg: int,
+                  out: torch.Tensor, stream=None) -> torch.Tensor:
+    """tok_emb [G, V, d] stacked; row r uses table r // rpg."""
+    R = tok.numel()
+    G, V, d = tok_emb.shape
+    _native.call("ms_embed_grouped", _dev.ptr(tok, torch.int32, "tok"), _dev.ptr(start, torch.int32, "start"), Q,
+                 _dev.ptr(tok_emb, BF16), V * d, rpg, None, 0, R, d, _dev.ptr(out, BF16), _dev.stream_ptr(stream))
+    return out
+
+
+def rmsnorm_grouped(x: torch.Tensor, gamma: torch.Tensor, rpg: int, eps: float, out: torch.Tensor,
+                    rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """gamma [G, d] stacked; output row r uses gain r // rpg."""
+    d = x.shape[1]
+    R = x.shape[0] if rows is None else rows.numel()
+    _native.call("ms_rmsnorm_grouped", x.data_ptr(), x.stride(0), _dev.ptr(rows, torch.int32, "rows"),
+                 _dev.ptr(gamma, BF16), d, rpg, eps, R, d, out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
+    return out

@@ -226,3 +226,70 @@ def _prefill_linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residua
             return out
         torch.mm(x, w.t(), out=out)
         return out
+
+
+class GroupedLlamaModel:
+    """The K drafters of a round (one Llama architecture, K weight sets) as ONE
+    forward: drafter k is row group k — its weights stacked at index k, its KV
+    cache slots k*S + s of one cache with K*S slots — so every op of a decode
+    step is a single launch for all drafters (ms_*_grouped) instead of K
+    launches on K streams.  Replaces the per-drafter draft_sequence loop of
+    _do_draft_batch (aggspec/engine.py:262-276).
+
+    forward(tokens [K*B, Q], start [K*B], slot [K*B], cache, logits [K*Bh, V],
+    head_rows [K*Bh] | None): rows of group k are k*B*Q .. (k+1)*B*Q - 1; the
+    head rows must be group-major (Bh per group)."""
+
+    def __init__(self, ws: list[LlamaWeights], max_rows: int, device="cuda"):
+        c = ws[0].cfg
+        if any(w.cfg != c for w in ws):
+            raise ValueError("grouped drafters must share one architecture")
+        self.cfg, self.G = c, len(ws)
+        self.device = torch.device(device)
+        self.t = {k: torch.stack([w[k] for w in ws]).contiguous() for k in ws[0].t}
+        G = self.G
+        self.max_rows = max_rows  # per group
+        R = G * max_rows
+        self.x = torch.empty((R, c.d), dtype=BF16, device=device)
+        self.h = torch.empty((R, c.d), dtype=BF16, device=device)
+        self.qkv = torch.empty((R, c.qkv_out), dtype=BF16, device=device)
+        self.attn = torch.empty((R, c.n_heads * c.head_dim), dtype=BF16, device=device)
+        self.ff = torch.empty((R, c.ffn), dtype=BF16, device=device)
+        self.scale = 1.0 / math.sqrt(c.head_dim)
+        self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
+
+    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
+        c, t, G = self.cfg, self.t, self.G
+        GB, Q = tokens.shape
+        B = GB // G
+        M = B * Q  # rows per group
+        R = G * M
+        if M > self.max_rows:
+            raise ValueError(f"{M} rows per group exceed max_rows={self.max_rows}")
+        x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
+        K.embed_grouped(tokens, start, Q, t["tok_emb"], M, out=x, stream=stream)
+
+        def lin(xx, name, **kw):
+            wt = t[name]  # [G, N, K]
+            if M <= 64 and wt.shape[2] <= 1024:
+                return K.gemv_grouped(xx, wt, G, stream=stream, **kw)
+            return K.linear_grouped(xx, wt.view(-1, wt.shape[2]), G, stream=stream, **kw)
+
+        for i in range(c.n_layers):
+            p = f"l{i}."
+            K.rmsnorm_grouped(x, t[p + "attn_norm"], M, c.eps, out=h, stream=stream)
+            lin(h, p + "w_qkv", out=qkv)
+            K.attention(qkv, GB, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+            lin(at, p + "w_o", residual=x, out=x)
+            K.rmsnorm_grouped(x, t[p + "mlp_norm"], M, c.eps, out=h, stream=stream)
+            lin(h, p + "w_gu", act=2, out=ff)
+            lin(ff, p + "w_down", residual=x, out=x)
+        Rh = R if head_rows is None else head_rows.numel()
+        if Rh == 0:
+            return logits
+        hf = self.h[:Rh]
+        K.rmsnorm_grouped(x, t["norm_f"], Rh // G, c.eps, out=hf, rows=head_rows, stream=stream)
+        head = t["lm_head"]
+        K.linear_grouped(hf, head.view(-1, head.shape[2]), G, out=logits, out_f32=True, stream=stream)
+        return logits

@@ -244,3 +244,65 @@ def test_llama_prefill_path_large_m_vs_reference():
         err = (got[b] - ref).abs().max().item() / ref.abs().max().item()
         assert err < 3e-2, err
         assert (got[b].argmax(-1) == ref.argmax(-1)).float().mean().item() >= 0.95
+
+
+@pytest.mark.parametrize("Q,B", [(1, 16), (6, 16), (13, 4)])
+def test_grouped_drafters_equal_separate_models(Q, B):
+    """K drafters as row groups of one GroupedLlamaModel (one launch per op)
+    give bitwise the logits of K separate LlamaModel forwards (gemv and
+    tcgen05 grouped paths; per-group weights, caches and gains)."""
+    from paper_2402_15678_b200.llama import CONFIGS, GroupedLlamaModel, LlamaModel, LlamaWeights
+    cfg = CONFIGS["tiny-llama-ssm"]
+    ws = [LlamaWeights.random(cfg, k + 7, device="cuda", std=0.05, norm_std=0.1) for k in range(3)]
+    G = len(ws)
+    gm = GroupedLlamaModel(ws, max_rows=B * 32)
+    singles = [LlamaModel(w, max_rows=B * 32, small_gemm=True) for w in ws]
+    T0 = 9
+    rng = np.random.default_rng(Q)
+    toks = torch.tensor(rng.integers(0, cfg.vocab, size=(B, T0 + Q)).astype(np.int32), device="cuda")
+    gcache = _kv(cfg, G * B, 32)
+    caches = [_kv(cfg, B, 32) for _ in range(G)]
+    slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    gslot = torch.arange(G * B, dtype=torch.int32, device="cuda")
+    z = torch.zeros(B, dtype=torch.int32, device="cuda")
+    dummy = torch.empty(0, cfg.vocab, device="cuda")
+    empty = torch.zeros(0, dtype=torch.int32, device="cuda")
+    for m, c in zip(singles, caches):
+        m.forward(toks[:, :T0].contiguous(), z, slot, c, dummy, head_rows=empty)
+    gm.forward(toks[:, :T0].repeat(G, 1).contiguous(), z.repeat(G), gslot, gcache, dummy, head_rows=empty)
+    st = torch.full((B,), T0, dtype=torch.int32, device="cuda")
+    ref = []
+    for m, c in zip(singles, caches):
+        lg = torch.empty(B * Q, cfg.vocab, device="cuda")
+        m.forward(toks[:, T0:].contiguous(), st, slot, c, lg)
+        ref.append(lg)
+    glg = torch.empty(G * B * Q, cfg.vocab, device="cuda")
+    gm.forward(toks[:, T0:].repeat(G, 1).contiguous(), st.repeat(G), gslot, gcache, glg)
+    assert torch.equal(glg, torch.cat(ref))
+
+
+def test_llama_engine_grouped_equals_per_drafter(monkeypatch):
+    """The engine's grouped drafting and the per-drafter streams produce the
+    same rounds (drafts, votes, accepted counts)."""
+    from paper_2402_15678_b200.core import EngineConfig, Request
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    tcfg, scfg = CONFIGS["tiny-llama"], CONFIGS["tiny-llama-ssm"]
+    target = LlamaWeights.random(tcfg, 0, device="cuda", std=0.05)
+    drafters = [LlamaWeights.random(scfg, k + 1, device="cuda", std=0.05) for k in range(3)]
+    outs = []
+    for grouped in ("1", "0"):
+        monkeypatch.setenv("MS_GROUPED_DRAFT", grouped)
+        cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=4, b_ssm=4, s_init=4, initial_weights=(1.0,) * 3)
+        eng = SpecEngine(target, drafters, cfg, slots=4, max_len=128, fidelity=[0.9, 0.7, 0.5], record=True,
+                         adaptive=False)
+        assert eng.grouped == (grouped == "1")
+        rng = np.random.default_rng(0)
+        reqs = [Request(f"req-{i:03d}", [int(t) for t in rng.integers(0, tcfg.vocab, size=6)], 40) for i in range(4)]
+        teacher = eng.greedy_teacher([Request(r.id, list(r.prompt), 40) for r in reqs], 40)
+        eng.prefill(reqs)
+        eng.set_teacher(teacher)
+        res = eng.decode()
+        assert res.outputs == teacher
+        outs.append([(rd.trace["drafts"].tolist(), rd.trace["voted"].tolist(), rd.accepted) for rd in res.rounds])
+    assert outs[0] == outs[1]
