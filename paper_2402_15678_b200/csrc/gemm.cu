@@ -44,7 +44,7 @@ struct LinearParams {
   int splits;
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
-  int stages;                     // TMA pipeline depth of this launch (cluster path)
+  int sw, sx;                     // W / X ring depths of this launch (cluster path)
   // fused LayerNorm of the X operand (ln_g != null): X = LN(x) * g + b, the raw
   // rows x [M, ldx] read for the row statistics, the TMA tile normalised in
   // shared memory before the MMA consumes it
@@ -57,34 +57,43 @@ struct LinearParams {
 
 constexpr int kBM = 128;  // output features per CTA (MMA M)
 constexpr int kBK = 64;   // bf16 elements per 128-byte swizzled row
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;    // cluster path: W producer, MMA, 4 epilogue warps, X producer
+constexpr int kSKThreads = 192;  // stream-K path
 
 template <int BN>
 struct LinearCfg {
   static constexpr int W_BYTES = kBM * kBK * 2;
   static constexpr int X_BYTES = BN * kBK * 2;
-  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int MAX_STAGES = 12;
+  static constexpr int MAX_SW = 14;
+  static constexpr int MAX_SX = 6;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int PART_BYTES = BN * kBM * 4;  // fp32 partial tile for the split-K reduction
-  // Pipeline depth is chosen per launch: bytes in flight per SM bound a weight
-  // stream (Little's law: ~6.5 TB/s x ~2 us), so one CTA per SM gets a deep
-  // pipeline (~210 KB), two CTAs per SM ~105 KB each.
-  __host__ __device__ static int stages_for(int ctas_per_sm) {
-    const int budget = ctas_per_sm <= 1 ? 210 * 1024 : 104 * 1024;
-    int st = budget / STAGE_BYTES;
-    return st < 2 ? 2 : (st > MAX_STAGES ? MAX_STAGES : st);
+  // Two decoupled TMA rings: the weight ring (HBM stream — its depth is the
+  // bytes in flight that bound a weight stream by Little's law, ~6.5 TB/s x
+  // ~2 us per GPU) and a shallow token ring (the X tile is re-read by every
+  // CTA, an L2 hit).  With one shared ring, a large token tile (M ~ 200)
+  // crowded the weight stages out of the smem budget.  Budget: ~210 KB at one
+  // CTA per SM, ~104 KB at two.
+  __host__ __device__ static void rings_for(int budget, int* sw, int* sx) {
+    int x = budget >= 150 * 1024 ? 4 : (X_BYTES <= 8192 ? 3 : 2);
+    int w = (budget - x * X_BYTES) / W_BYTES;
+    if (w < 3 && x > 2) {
+      x = 2;
+      w = (budget - x * X_BYTES) / W_BYTES;
+    }
+    *sw = w < 2 ? 2 : (w > MAX_SW ? MAX_SW : w);
+    *sx = x > MAX_SX ? MAX_SX : x;
   }
-  // the fp32 partial tile is staged in the (idle) pipeline smem only for the
+  // the fp32 partial tile is staged in the (idle) ring smem only for the
   // split-K cluster reduction; the single-split gated epilogue exchanges
   // gate/up through a 4 KB buffer instead
-  __host__ __device__ static int data_bytes(int stages, bool part) {
-    const int pipe = stages * STAGE_BYTES;
+  __host__ __device__ static int data_bytes(int sw, int sx, bool part) {
+    const int pipe = sw * W_BYTES + sx * X_BYTES;
     const int need = part ? PART_BYTES : 4096;
     return pipe > need ? pipe : need;
   }
-  __host__ __device__ static int smem(int stages, bool part) {
-    return 1024 + data_bytes(stages, part) + (3 * MAX_STAGES + 1) * 8 + 16 + 2 * BN * 4;
+  __host__ __device__ static int smem(int sw, int sx, bool part) {
+    return 1024 + data_bytes(sw, sx, part) + (2 * MAX_SW + 3 * MAX_SX + 1) * 8 + 16 + 2 * BN * 4;
   }
 };
 
@@ -123,13 +132,15 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  const int STAGES = p.stages;
-  uint8_t* sX = smem + STAGES * C::W_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::data_bytes(STAGES, p.splits > 1));
-  uint64_t* empty = full + C::MAX_STAGES;
-  uint64_t* tmem_full = empty + C::MAX_STAGES;
-  uint64_t* normed = tmem_full + 1;  // [MAX_STAGES] X tile normalised (fused LayerNorm)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(normed + C::MAX_STAGES);
+  const int SW = p.sw, SX = p.sx;
+  uint8_t* sX = smem + SW * C::W_BYTES;
+  uint64_t* fullW = reinterpret_cast<uint64_t*>(smem + C::data_bytes(SW, SX, p.splits > 1));
+  uint64_t* emptyW = fullW + C::MAX_SW;
+  uint64_t* fullX = emptyW + C::MAX_SW;
+  uint64_t* emptyX = fullX + C::MAX_SX;
+  uint64_t* normed = emptyX + C::MAX_SX;  // [MAX_SX] X tile normalised (fused LayerNorm)
+  uint64_t* tmem_full = normed + C::MAX_SX;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   float* s_mean = reinterpret_cast<float*>(tmem_slot + 4);  // [BN]
   float* s_rstd = s_mean + BN;                              // [BN]
   const bool fuse_ln = p.ln_g != nullptr;
@@ -149,9 +160,13 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmW);
     tc::prefetch_tmap(&tmX);
-    for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
+    for (int s = 0; s < SW; ++s) {
+      tc::mbar_init(&fullW[s], 1);
+      tc::mbar_init(&emptyW[s], 1);
+    }
+    for (int s = 0; s < SX; ++s) {
+      tc::mbar_init(&fullX[s], 1);
+      tc::mbar_init(&emptyX[s], 1);
       tc::mbar_init(&normed[s], 128);
     }
     tc::mbar_init(tmem_full, 1);
@@ -163,31 +178,41 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   // X operand ready for the MMA: the TMA barrier, or the normalisation barrier
-  uint64_t* x_ready = fuse_ln ? normed : full;
+  uint64_t* x_ready = fuse_ln ? normed : fullX;
 
+  const int nkb = kb1 - kb0;
   if (warp == 0) {
     if (lane == 0) {
+      // weight producer: the first SW weight tiles do not depend on the previous
+      // kernel — issued before the programmatic-dependency wait (PDL prefetch)
       const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
-      const uint64_t pol_x = tc::policy_evict_last();   // tokens are re-read by every tile
-      // The first STAGES weight tiles do not depend on the previous kernel:
-      // issue them before the programmatic-dependency wait (PDL prefetch).
-      const int nkb = kb1 - kb0;
-      const int pre = nkb < STAGES ? nkb : STAGES;
+      const int pre = nkb < SW ? nkb : SW;
       for (int i = 0; i < pre; ++i) {
-        tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (kb0 + i) * kBK, wrow, pol_w);
+        tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
       }
       pdl_wait();
       pdl_trigger();
+      for (int i = pre; i < nkb; ++i) {
+        const int st = i % SW;
+        tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
+        tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
+      }
+    } else {
+      pdl_trigger();
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {
+      // token producer (the X tile depends on the previous kernel)
+      const uint64_t pol_x = tc::policy_evict_last();  // tokens are re-read by every tile
+      pdl_wait();
+      pdl_trigger();
       for (int i = 0; i < nkb; ++i) {
-        const int stage = i % STAGES;
-        const int kb = kb0 + i;
-        if (i >= pre) {
-          tc::mbar_wait(&empty[stage], ((i / STAGES) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], kb * kBK, wrow, pol_w);
-        }
-        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], kb * kBK, xrow, pol_x);
+        const int st = i % SX;
+        if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+        tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, pol_x);
       }
     } else {
       pdl_trigger();
@@ -196,21 +221,18 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     pdl_trigger();
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&x_ready[stage], phase);
+      for (int i = 0; i < nkb; ++i) {
+        const int ws = i % SW, xs = i % SX;
+        tc::mbar_wait(&fullW[ws], (i / SW) & 1);
+        tc::mbar_wait(&x_ready[xs], (i / SX) & 1);
         tc::fence_after_sync();
-        const uint64_t ad = tc::smem_desc_sw128(sW + stage * C::W_BYTES);
-        const uint64_t bd = tc::smem_desc_sw128(sX + stage * C::X_BYTES);
+        const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
+        const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K per UMMA_K=16 step
-          tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-        tc::mma_commit(&empty[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+          tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        tc::mma_commit(&emptyW[ws]);
+        tc::mma_commit(&emptyX[xs]);
       }
       tc::mma_commit(tmem_full);
     }
@@ -254,10 +276,10 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       // (2) per stage: normalise the swizzled X tile in place, hand it to the MMA
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
+      for (int i = 0; i < nkb; ++i) {
+        const int stage = i % SX;
+        const int kb = kb0 + i;
+        tc::mbar_wait(&fullX[stage], (i / SX) & 1);
         uint8_t* xs = sX + stage * C::X_BYTES;
         for (int ch = et; ch < BN * 8; ch += 128) {  // 16-byte chunks: row r, logical chunk j
           const int r = ch >> 3, j = ch & 7;
@@ -274,10 +296,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
         tc::mbar_arrive(&normed[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
     }
     tc::mbar_wait(tmem_full, 0);
@@ -434,7 +452,7 @@ __device__ __forceinline__ int sk_owner(int i, int iters, int G) {
 
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kSKThreads, 1)
 linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                  const LinearParams p, const SKParams sk) {
   using C = SKCfg<BN>;
@@ -692,8 +710,10 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
+    int sw, sx;
+    C::rings_for(210 * 1024, &sw, &sx);
     if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::smem(C::stages_for(1), true)) != cudaSuccess)
+                             C::smem(sw, sx, true)) != cudaSuccess)
       return MS_ERR_CUDA;
     attr_set = true;
   }
@@ -702,12 +722,16 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
   // little shared memory and several kernels / streams can share an SM
   const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
   const bool part = p.splits > 1;
-  p.stages = C::stages_for(grid <= 148 ? 1 : 2);
+  int sw, sx;
+  C::rings_for(grid <= 148 ? 210 * 1024 : 104 * 1024, &sw, &sx);
   // the fp32 split-K staging tile may already rule out two CTAs per SM: then
-  // take the deep single-CTA pipeline
-  if (part && C::smem(p.stages, part) > 113 * 1024) p.stages = C::stages_for(1);
-  if (p.stages > kb_per_cta) p.stages = kb_per_cta < 2 ? 2 : kb_per_cta;
-  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(p.stages, part), st,
+  // take the deep single-CTA rings
+  if (part && C::smem(sw, sx, part) > 113 * 1024) C::rings_for(210 * 1024, &sw, &sx);
+  if (sw > kb_per_cta) sw = kb_per_cta < 2 ? 2 : kb_per_cta;
+  if (sx > kb_per_cta) sx = kb_per_cta < 2 ? 2 : kb_per_cta;
+  p.sw = sw;
+  p.sx = sx;
+  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part), st,
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
@@ -730,7 +754,7 @@ static int launch_linear_sk(const CUtensorMap& tw, const CUtensorMap& tx, const 
       return MS_ERR_CUDA;
     attr_set = true;
   }
-  return launch(linear_sk_kernel<BN>, dim3(sk.grid), dim3(kThreads), C::SMEM, st, 1, tw, tx, p, sk);
+  return launch(linear_sk_kernel<BN>, dim3(sk.grid), dim3(kSKThreads), C::SMEM, st, 1, tw, tx, p, sk);
 }
 
 int preload_gemm() {
