@@ -271,6 +271,13 @@ class GroupedLlamaModel:
 
         def lin(xx, name, **kw):
             wt = t[name]  # [G, N, K]
+            if M >= LlamaModel.PREFILL_ROWS:  # prompt prefill: per-group cuBLAS (see LlamaModel)
+                out, res = kw["out"], kw.get("residual")
+                for g in range(G):
+                    sl = slice(g * M, (g + 1) * M)
+                    _prefill_linear(xx[sl], wt[g], out=out[sl], residual=None if res is None else res[sl],
+                                    act=kw.get("act", 0), stream=stream)
+                return out
             if M <= 64 and wt.shape[2] <= 1024:
                 return K.gemv_grouped(xx, wt, G, stream=stream, **kw)
             return K.linear_grouped(xx, wt.view(-1, wt.shape[2]), G, stream=stream, **kw)
