@@ -24,6 +24,8 @@
 // deterministic and, because the split count depends only on (N, K),
 // identical for a token row whatever M is (batch invariance: a request's
 // logits do not depend on what else is in the verify batch).
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -653,6 +655,207 @@ linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent weight-streaming schedule for GEMMs with >= one tile per SM
+// (the 70B gate/up projection: 448 tiles, the LM head: 250): one CTA per SM
+// walks tiles c, c + P, c + 2P, ... with
+//   * decoupled TMA rings sized for ONE CTA per SM (~144 KB of weight tiles in
+//     flight — what a 6.5 TB/s stream needs per SM by Little's law — next to a
+//     shallow token ring), flowing across tile boundaries without a drain;
+//   * a double-buffered TMEM accumulator (2 x BN columns): the epilogue of tile
+//     t overlaps the mainloop of tile t + 1.
+// Whole tiles, full-K accumulation: bitwise the arithmetic of the one-split
+// cluster path, so the schedule choice never changes a result.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct PKCfg {
+  static constexpr int W_BYTES = kBM * kBK * 2;
+  static constexpr int X_BYTES = BN * kBK * 2;
+  static constexpr int MAX_SW = 16;
+  static constexpr int MAX_SX = 6;
+  static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int XB_BYTES = 64 * 17 * 4;  // gated-epilogue exchange buffer
+  __host__ __device__ static void rings(int* sw, int* sx) {
+    const int budget = 206 * 1024 - XB_BYTES;
+    int x = X_BYTES <= 16384 ? 4 : 3;
+    int w = (budget - x * X_BYTES) / W_BYTES;
+    *sw = w > MAX_SW ? MAX_SW : w;
+    *sx = x;
+  }
+  __host__ __device__ static int smem(int sw, int sx) {
+    return 1024 + sw * W_BYTES + sx * X_BYTES + XB_BYTES + (2 * MAX_SW + 2 * MAX_SX + 4) * 8 + 16;
+  }
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                 const LinearParams p) {
+  using C = PKCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int SW = p.sw, SX = p.sx;
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + SW * C::W_BYTES;
+  float* xb = reinterpret_cast<float*>(sX + SX * C::X_BYTES);  // [64][17]
+  uint64_t* fullW = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xb) + C::XB_BYTES);
+  uint64_t* emptyW = fullW + C::MAX_SW;
+  uint64_t* fullX = emptyW + C::MAX_SW;
+  uint64_t* emptyX = fullX + C::MAX_SX;
+  uint64_t* tfull = emptyX + C::MAX_SX;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int P = gridDim.x, c = blockIdx.x;
+  const int kbt = p.kb_total;
+  const int n_my = c < p.n_tiles ? (p.n_tiles - c + P - 1) / P : 0;  // tiles c, c+P, ...
+  const int total = n_my * kbt;                                       // flat k-block iterations
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmW);
+    tc::prefetch_tmap(&tmX);
+    for (int s = 0; s < SW; ++s) {
+      tc::mbar_init(&fullW[s], 1);
+      tc::mbar_init(&emptyW[s], 1);
+    }
+    for (int s = 0; s < SX; ++s) {
+      tc::mbar_init(&fullX[s], 1);
+      tc::mbar_init(&emptyX[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = tc::policy_evict_first();
+      const int pre = total < SW ? total : SW;
+      for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel (PDL prefetch)
+        tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (i % kbt) * kBK, (c + (i / kbt) * P) * kBM, pol_w);
+      }
+      pdl_wait();
+      pdl_trigger();
+      for (int i = pre; i < total; ++i) {
+        const int st = i % SW;
+        tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
+        tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (i % kbt) * kBK, (c + (i / kbt) * P) * kBM, pol_w);
+      }
+    } else {
+      pdl_trigger();
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {
+      const uint64_t pol_x = tc::policy_evict_last();
+      pdl_wait();
+      pdl_trigger();
+      for (int i = 0; i < total; ++i) {
+        const int st = i % SX;
+        if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+        tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (i % kbt) * kBK, 0, pol_x);
+      }
+    } else {
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    pdl_trigger();
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
+      int i = 0;
+      for (int t = 0; t < n_my; ++t) {
+        const int buf = t & 1;
+        tc::mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        tc::fence_after_sync();
+        const uint32_t acc = tmem + buf * C::ACC_COLS;
+        for (int kb = 0; kb < kbt; ++kb, ++i) {
+          const int ws = i % SW, xs = i % SX;
+          tc::mbar_wait(&fullW[ws], (i / SW) & 1);
+          tc::mbar_wait(&fullX[xs], (i / SX) & 1);
+          tc::fence_after_sync();
+          const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
+          const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            tc::mma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          tc::mma_commit(&emptyW[ws]);
+          tc::mma_commit(&emptyX[xs]);
+        }
+        tc::mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4 ----------------
+    pdl_wait();
+    pdl_trigger();
+    const int q = warp & 3;
+    const int m_hi = min(BN, p.M);
+    for (int t = 0; t < n_my; ++t) {
+      const int buf = t & 1;
+      const int tile = c + t * P;
+      tc::mbar_wait(&tfull[buf], (t >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t trow = tmem + buf * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      if (p.act == 2) {
+        const bool up = q >= 2;
+        const int of = tile * (kBM / 2) + (q & 1) * 32 + lane;
+        for (int c0 = 0; c0 < m_hi; c0 += 16) {
+          uint32_t r[16];
+          tc::tmem_ld16(trow + c0, r);
+          tc::tmem_wait_ld();
+          if (up) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xb[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+          }
+          epi_bar128();
+          if (!up) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + of;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < m_hi)
+                o[(int64_t)(c0 + j) * p.ldc] = f2bf(silu_mul(__uint_as_float(r[j]), xb[(q * 32 + lane) * 17 + j]));
+          }
+          epi_bar128();
+        }
+      } else {
+        const int feat = tile * kBM + q * 32 + lane;
+        const bool feat_ok = feat < p.N;
+        for (int c0 = 0; c0 < m_hi; c0 += 16) {
+          uint32_t r[16];
+          tc::tmem_ld16(trow + c0, r);
+          tc::tmem_wait_ld();
+          if (feat_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < m_hi) epi_store(p, c0 + j, feat, __uint_as_float(r[j]));
+          }
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -735,6 +938,45 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
                 p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN>
+static int launch_linear_pk(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, cudaStream_t st) {
+  using C = PKCfg<BN>;
+  int sw, sx;
+  C::rings(&sw, &sx);
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(linear_pk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(sw, sx)) !=
+        cudaSuccess)
+      return MS_ERR_CUDA;
+    attr_set = true;
+  }
+  p.sw = sw;
+  p.sx = sx;
+  p.splits = 1;
+  const int grid = p.n_tiles < sm_count() ? p.n_tiles : sm_count();
+  return launch(linear_pk_kernel<BN>, dim3(grid), dim3(kThreads), C::smem(sw, sx), st, 1, tw, tx, p);
+}
+static bool pk_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_PK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+
 // Persistent grid for the stream-K path: a function of (N, K) only.
 int linear_sk_grid(int N, int K) {
   const int iters = ((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK);
@@ -759,22 +1001,22 @@ static int launch_linear_sk(const CUtensorMap& tw, const CUtensorMap& tx, const 
 
 int preload_gemm() {
   int n = 0;
-  n += preload_fn(linear_kernel<16>) + preload_fn(linear_sk_kernel<16>);
-  n += preload_fn(linear_kernel<32>) + preload_fn(linear_sk_kernel<32>);
-  n += preload_fn(linear_kernel<48>) + preload_fn(linear_sk_kernel<48>);
-  n += preload_fn(linear_kernel<64>) + preload_fn(linear_sk_kernel<64>);
-  n += preload_fn(linear_kernel<80>) + preload_fn(linear_sk_kernel<80>);
-  n += preload_fn(linear_kernel<96>) + preload_fn(linear_sk_kernel<96>);
-  n += preload_fn(linear_kernel<112>) + preload_fn(linear_sk_kernel<112>);
-  n += preload_fn(linear_kernel<128>) + preload_fn(linear_sk_kernel<128>);
-  n += preload_fn(linear_kernel<144>) + preload_fn(linear_sk_kernel<144>);
-  n += preload_fn(linear_kernel<160>) + preload_fn(linear_sk_kernel<160>);
-  n += preload_fn(linear_kernel<176>) + preload_fn(linear_sk_kernel<176>);
-  n += preload_fn(linear_kernel<192>) + preload_fn(linear_sk_kernel<192>);
-  n += preload_fn(linear_kernel<208>) + preload_fn(linear_sk_kernel<208>);
-  n += preload_fn(linear_kernel<224>) + preload_fn(linear_sk_kernel<224>);
-  n += preload_fn(linear_kernel<240>) + preload_fn(linear_sk_kernel<240>);
-  n += preload_fn(linear_kernel<256>) + preload_fn(linear_sk_kernel<256>);
+  n += preload_fn(linear_kernel<16>) + preload_fn(linear_sk_kernel<16>) + preload_fn(linear_pk_kernel<16>);
+  n += preload_fn(linear_kernel<32>) + preload_fn(linear_sk_kernel<32>) + preload_fn(linear_pk_kernel<32>);
+  n += preload_fn(linear_kernel<48>) + preload_fn(linear_sk_kernel<48>) + preload_fn(linear_pk_kernel<48>);
+  n += preload_fn(linear_kernel<64>) + preload_fn(linear_sk_kernel<64>) + preload_fn(linear_pk_kernel<64>);
+  n += preload_fn(linear_kernel<80>) + preload_fn(linear_sk_kernel<80>) + preload_fn(linear_pk_kernel<80>);
+  n += preload_fn(linear_kernel<96>) + preload_fn(linear_sk_kernel<96>) + preload_fn(linear_pk_kernel<96>);
+  n += preload_fn(linear_kernel<112>) + preload_fn(linear_sk_kernel<112>) + preload_fn(linear_pk_kernel<112>);
+  n += preload_fn(linear_kernel<128>) + preload_fn(linear_sk_kernel<128>) + preload_fn(linear_pk_kernel<128>);
+  n += preload_fn(linear_kernel<144>) + preload_fn(linear_sk_kernel<144>) + preload_fn(linear_pk_kernel<144>);
+  n += preload_fn(linear_kernel<160>) + preload_fn(linear_sk_kernel<160>) + preload_fn(linear_pk_kernel<160>);
+  n += preload_fn(linear_kernel<176>) + preload_fn(linear_sk_kernel<176>) + preload_fn(linear_pk_kernel<176>);
+  n += preload_fn(linear_kernel<192>) + preload_fn(linear_sk_kernel<192>) + preload_fn(linear_pk_kernel<192>);
+  n += preload_fn(linear_kernel<208>) + preload_fn(linear_sk_kernel<208>) + preload_fn(linear_pk_kernel<208>);
+  n += preload_fn(linear_kernel<224>) + preload_fn(linear_sk_kernel<224>) + preload_fn(linear_pk_kernel<224>);
+  n += preload_fn(linear_kernel<240>) + preload_fn(linear_sk_kernel<240>) + preload_fn(linear_pk_kernel<240>);
+  n += preload_fn(linear_kernel<256>) + preload_fn(linear_sk_kernel<256>) + preload_fn(linear_pk_kernel<256>);
   return n;
 }
 
@@ -856,6 +1098,28 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
       case 224: return launch_linear_sk<224>(tw, tx, p, sk, st);
       case 240: return launch_linear_sk<240>(tw, tx, p, sk, st);
       default: return launch_linear_sk<256>(tw, tx, p, sk, st);
+    }
+  }
+  // weight-streaming GEMMs with at least one 128-feature tile per SM: the
+  // persistent schedule (whole tiles; MS_PK=0 disables, for A/B runs)
+  if (splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && n_tiles >= sm_count() && pk_enabled()) {
+    switch (bn) {
+      case 16: return launch_linear_pk<16>(tw, tx, p, st);
+      case 32: return launch_linear_pk<32>(tw, tx, p, st);
+      case 48: return launch_linear_pk<48>(tw, tx, p, st);
+      case 64: return launch_linear_pk<64>(tw, tx, p, st);
+      case 80: return launch_linear_pk<80>(tw, tx, p, st);
+      case 96: return launch_linear_pk<96>(tw, tx, p, st);
+      case 112: return launch_linear_pk<112>(tw, tx, p, st);
+      case 128: return launch_linear_pk<128>(tw, tx, p, st);
+      case 144: return launch_linear_pk<144>(tw, tx, p, st);
+      case 160: return launch_linear_pk<160>(tw, tx, p, st);
+      case 176: return launch_linear_pk<176>(tw, tx, p, st);
+      case 192: return launch_linear_pk<192>(tw, tx, p, st);
+      case 208: return launch_linear_pk<208>(tw, tx, p, st);
+      case 224: return launch_linear_pk<224>(tw, tx, p, st);
+      case 240: return launch_linear_pk<240>(tw, tx, p, st);
+      default: return launch_linear_pk<256>(tw, tx, p, st);
     }
   }
   if (splits <= 0) splits = linear_auto_splits(N, K);

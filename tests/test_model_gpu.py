@@ -253,3 +253,21 @@ def test_drafter_forward_small_gemm_vs_reference():
         ref = opt_ref.forward(w_cpu.t, cfg, toks[b])
         err = (got[b] - ref).abs().max().item() / ref.abs().max().item()
         assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("M,N,K,act", [(112, 57344, 1024, 2), (176, 19200, 512, 0), (16, 32000, 768, 0),
+                                       (200, 38400, 256, 2), (1, 50272, 256, 0)])
+def test_persistent_schedule_equals_one_split_cluster(M, N, K, act, monkeypatch):
+    """GEMMs with >= one tile per SM take the persistent schedule (whole tiles,
+    full-K accumulation): bitwise the one-split cluster path's arithmetic."""
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(M + N + K)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    w = (torch.randn(N, K, generator=g) * 0.03).to(torch.bfloat16).cuda()
+    r = None if act == 2 else torch.randn(M, N, generator=g).to(torch.bfloat16).cuda()
+    pk = Kn.linear(x, w, residual=r, act=act)            # splits=0 -> persistent (N/128 >= 148 tiles)
+    cl = Kn.linear(x, w, residual=r, act=act, splits=1)  # cluster path, one split
+    assert torch.equal(pk, cl)
+    ref = _ref_linear(x.cpu(), w.cpu(), None, None if r is None else r.cpu(), 0, True) if act == 0 else None
+    if ref is not None:
+        torch.testing.assert_close(pk.cpu().float(), ref.float(), rtol=1.6e-2, atol=2e-2)
