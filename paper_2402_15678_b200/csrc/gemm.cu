@@ -47,6 +47,7 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int sw, sx;                     // W / X ring depths of this launch (cluster path)
+  int nc;                         // N tiles sharing one multicast X tile (cluster = splits * nc CTAs)
   // fused LayerNorm of the X operand (ln_g != null): X = LN(x) * g + b, the raw
   // rows x [M, ldx] read for the row statistics, the TMA tile normalised in
   // shared memory before the MMA consumes it
@@ -70,6 +71,7 @@ struct LinearCfg {
   static constexpr int MAX_SX = 6;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int PART_BYTES = BN * kBM * 4;  // fp32 partial tile for the split-K reduction
+  static constexpr int NBAR = 2 * MAX_SW + 4 * MAX_SX + 1;  // mbarriers
   // Two decoupled TMA rings: the weight ring (HBM stream — its depth is the
   // bytes in flight that bound a weight stream by Little's law, ~6.5 TB/s x
   // ~2 us per GPU) and a shallow token ring (the X tile is re-read by every
@@ -95,7 +97,7 @@ struct LinearCfg {
     return pipe > need ? pipe : need;
   }
   __host__ __device__ static int smem(int sw, int sx, bool part) {
-    return 1024 + data_bytes(sw, sx, part) + (2 * MAX_SW + 3 * MAX_SX + 1) * 8 + 16 + 2 * BN * 4;
+    return 1024 + data_bytes(sw, sx, part) + NBAR * 8 + 16 + 2 * BN * 4;
   }
 };
 
@@ -141,7 +143,8 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   uint64_t* fullX = emptyW + C::MAX_SW;
   uint64_t* emptyX = fullX + C::MAX_SX;
   uint64_t* normed = emptyX + C::MAX_SX;  // [MAX_SX] X tile normalised (fused LayerNorm)
-  uint64_t* tmem_full = normed + C::MAX_SX;
+  uint64_t* emptyXl = normed + C::MAX_SX;  // [MAX_SX] this CTA's MMA done with an X stage (multicast peers)
+  uint64_t* tmem_full = emptyXl + C::MAX_SX;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   float* s_mean = reinterpret_cast<float*>(tmem_slot + 4);  // [BN]
   float* s_rstd = s_mean + BN;                              // [BN]
@@ -149,8 +152,18 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int tile_n = blockIdx.x / p.splits;
-  const int split = blockIdx.x - tile_n * p.splits;
+  // cluster = nc N-tiles x splits K-slices; rank = j * splits + split.  The
+  // nc CTAs of one split read the same X k-blocks: the j == 0 CTA loads each
+  // X tile once from L2 and multicasts it to the others (the L2 -> SM stream
+  // of re-read token tiles, not HBM, bounds large-M weight streaming).
+  const int csize = p.splits * p.nc;
+  const int crank = (int)(blockIdx.x % csize);
+  const int jn = crank / p.splits;
+  const int split = crank - jn * p.splits;
+  const int tile_n = (int)(blockIdx.x / csize) * p.nc + jn;
+  const bool x_leader = jn == 0;
+  uint16_t x_mask = 0;
+  for (int jj = 0; jj < p.nc; ++jj) x_mask |= (uint16_t)(1u << (jj * p.splits + split));
   const int n0 = tile_n * kBM;
   const int m0 = blockIdx.y * BN;
   // row group (grouped drafters): M rows of X / out and N rows of W per group
@@ -168,8 +181,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
     for (int s = 0; s < SX; ++s) {
       tc::mbar_init(&fullX[s], 1);
-      tc::mbar_init(&emptyX[s], 1);
+      tc::mbar_init(&emptyX[s], p.nc);  // leader: every multicast peer's MMA
       tc::mbar_init(&normed[s], 128);
+      tc::mbar_init(&emptyXl[s], 1);
     }
     tc::mbar_init(tmem_full, 1);
     tc::fence_barrier_init();
@@ -177,6 +191,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
+  if (p.nc > 1) cluster_sync_all();  // peers' barriers exist before any multicast / remote arrive
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   // X operand ready for the MMA: the TMA barrier, or the normalisation barrier
@@ -212,9 +227,22 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       pdl_trigger();
       for (int i = 0; i < nkb; ++i) {
         const int st = i % SX;
-        if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-        tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, pol_x);
+        if (p.nc == 1) {
+          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+          tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, pol_x);
+        } else if (x_leader) {
+          // stage free in every peer (each peer's MMA arrived on this barrier)
+          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+          tc::tma_load_2d_mc(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, x_mask, pol_x);
+        } else {
+          // arm this CTA's barrier for the leader's multicast once our MMA
+          // released the stage (the bytes may land first: tx-count goes
+          // transiently negative, the phase still needs this arrival)
+          if (i >= SX) tc::mbar_wait(&emptyXl[st], ((i / SX) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+        }
       }
     } else {
       pdl_trigger();
@@ -234,7 +262,12 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K per UMMA_K=16 step
           tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
         tc::mma_commit(&emptyW[ws]);
-        tc::mma_commit(&emptyX[xs]);
+        if (p.nc == 1) {
+          tc::mma_commit(&emptyX[xs]);
+        } else {
+          tc::mma_commit_mc(&emptyX[xs], (uint16_t)(1u << split));  // the leader of this split
+          tc::mma_commit(&emptyXl[xs]);
+        }
       }
       tc::mma_commit(tmem_full);
     }
@@ -324,7 +357,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + of;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi)
+            if (c0 + j < m_hi && n0 < p.N)  // n0 >= N: the padding tile of an odd multicast pair
               o[(int64_t)(orow + c0 + j) * p.ldc] = f2bf(silu_mul(__uint_as_float(r[j]), xb[(q * 32 + lane) * 17 + j]));
         }
         epi_bar128();
@@ -369,8 +402,8 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     const int u0 = (int)((int64_t)split * units / p.splits);
     const int u1 = (int)((int64_t)(split + 1) * units / p.splits);
     const float* P = reinterpret_cast<const float*>(smem);
-    auto ld4 = [&](const float* a, int rk) {
-      return cl ? ld_dsmem_f4(a, rk) : *reinterpret_cast<const float4*>(a);
+    auto ld4 = [&](const float* a, int rk) {  // rank rk of this N-tile's split group
+      return cl ? ld_dsmem_f4(a, jn * p.splits + rk) : *reinterpret_cast<const float4*>(a);
     };
     for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
       const int j = u / upr;
@@ -389,6 +422,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
         const float u4[4] = {up.x, up.y, up.z, up.w};
         const int of = tile_n * (kBM / 2) + f4;  // output feature
+        if (n0 >= p.N) continue;                 // padding tile of an odd multicast pair
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
 #pragma unroll
         for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
@@ -401,6 +435,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
     if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
   }
+  if (p.nc > 1 && p.splits == 1) cluster_sync_all();  // multicast peers done with each other's smem
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) {
@@ -677,9 +712,13 @@ struct PKCfg {
   static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int XB_BYTES = 64 * 17 * 4;  // gated-epilogue exchange buffer
+  // both rings sized by latency: weight tiles (HBM, ~2 us loaded) and token
+  // tiles (L2, ~1.2 us) are consumed one of each per k-block, so the stage
+  // counts go ~5:3 within the budget
   __host__ __device__ static void rings(int* sw, int* sx) {
     const int budget = 206 * 1024 - XB_BYTES;
-    int x = X_BYTES <= 16384 ? 4 : 3;
+    int x = budget * 3 / (5 * W_BYTES + 3 * X_BYTES);
+    x = x < 2 ? 2 : (x > MAX_SX ? MAX_SX : x);
     int w = (budget - x * X_BYTES) / W_BYTES;
     *sw = w > MAX_SW ? MAX_SW : w;
     *sx = x;
@@ -907,6 +946,18 @@ static int pick_bn(int M) {
   return M <= 16 ? 16 : (M + 15) / 16 * 16;
 }
 
+// Opt-in (MS_MC=1): multicasting the token tile to N-tile pairs measured
+// neutral to slightly slower (QKV at M = 176: 40.9 vs 39.9 us) — L2 -> SM
+// bandwidth (30% of peak per ncu) is not what bounds these GEMMs.
+static bool mc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MS_MC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int BN>
 static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p,
                          int m_tiles, cudaStream_t st, int G) {
@@ -920,7 +971,11 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
       return MS_ERR_CUDA;
     attr_set = true;
   }
-  const int grid = p.n_tiles * p.splits * m_tiles * G;
+  // multicast pairs along N once the token tile is big enough for its L2
+  // re-reads to matter (M > 48), within the portable cluster size 8
+  p.nc = (BN > 48 && p.n_tiles > 1 && p.splits * 2 <= 8 && mc_enabled()) ? 2 : 1;
+  const int n_tiles_pad = (p.n_tiles + p.nc - 1) / p.nc * p.nc;
+  const int grid = n_tiles_pad * p.splits * m_tiles * G;
   // never deeper than the k-blocks a CTA streams: small (SSM) GEMMs then use
   // little shared memory and several kernels / streams can share an SM
   const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
@@ -934,8 +989,8 @@ static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearPar
   if (sx > kb_per_cta) sx = kb_per_cta < 2 ? 2 : kb_per_cta;
   p.sw = sw;
   p.sx = sx;
-  return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part), st,
-                p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
+  return launch(linear_kernel<BN>, dim3(n_tiles_pad * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part),
+                st, p.splits * p.nc /* split-K CTAs x multicast N-tiles form one cluster */, tw, tx, p);
 }
 
 
@@ -967,11 +1022,15 @@ static int launch_linear_pk(const CUtensorMap& tw, const CUtensorMap& tx, Linear
   const int grid = p.n_tiles < sm_count() ? p.n_tiles : sm_count();
   return launch(linear_pk_kernel<BN>, dim3(grid), dim3(kThreads), C::smem(sw, sx), st, 1, tw, tx, p);
 }
+// Opt-in (MS_PK=1): measured no faster than the cluster path on the 70B
+// shapes (gate/up at M = 112 / 176: 201 / 219 us vs 183 / 213 us) — with deep
+// rings either way the large-M tiles stay ~35% tensor-active and ~50% DRAM:
+// neither ring depth nor wave quantization is the limiter there.
 static bool pk_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MS_PK");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }

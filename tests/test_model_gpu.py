@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import ROOT
 from oracle import opt_ref
 
 pytestmark = pytest.mark.gpu
@@ -257,9 +258,29 @@ def test_drafter_forward_small_gemm_vs_reference():
 
 @pytest.mark.parametrize("M,N,K,act", [(112, 57344, 1024, 2), (176, 19200, 512, 0), (16, 32000, 768, 0),
                                        (200, 38400, 256, 2), (1, 50272, 256, 0)])
-def test_persistent_schedule_equals_one_split_cluster(M, N, K, act, monkeypatch):
-    """GEMMs with >= one tile per SM take the persistent schedule (whole tiles,
-    full-K accumulation): bitwise the one-split cluster path's arithmetic."""
+def test_persistent_schedule_equals_one_split_cluster(M, N, K, act):
+    """The persistent schedule (MS_PK=1: whole tiles, full-K accumulation) is
+    bitwise the one-split cluster path's arithmetic.  The env switch is read
+    once per process, so the persistent run happens in a subprocess."""
+    import subprocess
+    import sys
+    code = f"""
+import torch, sys
+sys.path.insert(0, {ROOT!r})
+from paper_2402_15678_b200 import kernels as Kn
+g = torch.Generator().manual_seed({M + N + K})
+x = torch.randn({M}, {K}, generator=g).to(torch.bfloat16).cuda()
+w = (torch.randn({N}, {K}, generator=g) * 0.03).to(torch.bfloat16).cuda()
+r = None if {act} == 2 else torch.randn({M}, {N}, generator=g).to(torch.bfloat16).cuda()
+pk = Kn.linear(x, w, residual=r, act={act})
+cl = Kn.linear(x, w, residual=r, act={act}, splits=1)
+assert torch.equal(pk, cl)
+print("ok")
+"""
+    for env in ({"MS_PK": "1"}, {"MS_MC": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], env={**__import__("os").environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
     from paper_2402_15678_b200 import kernels as Kn
     g = torch.Generator().manual_seed(M + N + K)
     x = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
