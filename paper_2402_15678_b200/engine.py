@@ -88,6 +88,14 @@ class RoundStats:
     weights: dict
     group: int = 0
     trace: dict | None = None  # per-round device arrays when record=True
+    # device timestamps (ms since the decode's first kernel) for the trace
+    round_index: int = 0
+    request_ids: tuple = ()
+    pool_depth: int = 0
+    draft_start: float | None = None
+    draft_end: float | None = None
+    verify_start: float | None = None
+    verify_end: float | None = None
 
 
 @dataclass
@@ -106,6 +114,17 @@ class RunResult:
     def mean_emitted(self) -> float:
         em = [e for r in self.rounds for e in r.emitted]
         return float(np.mean(em)) if em else 0.0
+
+    def trace(self):
+        """Device-timed TraceEvents in the reference's format (trace.py)."""
+        from .trace import trace_from_rounds
+        return trace_from_rounds(self.rounds)
+
+    def metrics(self, requests):
+        """RunMetrics (aggspec/engine.py:100-168) from the device-timed trace;
+        request finish times are the device end of their last verify."""
+        from .trace import collect_metrics
+        return collect_metrics(self.trace(), requests)
 
 
 class _Group:
@@ -253,6 +272,7 @@ class SpecEngine:
         self.draft_stream = torch.cuda.Stream(self.dev)
         self.verify_stream = torch.cuda.Stream(self.dev)
         self.requests: list[Request] = []
+        self._run_t0 = None
 
     # ------------------------------------------------------------------ setup
     def prefill(self, requests: list[Request]) -> None:
@@ -582,6 +602,9 @@ class SpecEngine:
         if self.sync_time is not None:
             t_sel = float(self.sync_time(t_sel))
         accs, ems, vts = [], [], []
+        t0 = self._run_t0
+        ts = (t0.elapsed_time(g.ev_d0), t0.elapsed_time(g.ev_d1), t0.elapsed_time(g.ev_v0),
+              t0.elapsed_time(g.ev_v1)) if t0 is not None else (None,) * 4
         for b in active:
             r = g.requests[b]
             r.advance(RequestState.AWAITING_VERIFICATION)
@@ -596,7 +619,7 @@ class SpecEngine:
             stopped = self.cfg.stop_token is not None and self.cfg.stop_token in use
             if stopped or r.remaining <= 0:
                 r.advance(RequestState.FINISHED)
-                r.finish_time = time.perf_counter()
+                r.finish_time = ts[3] if ts[3] is not None else time.perf_counter()  # device ms
             else:
                 r.advance(RequestState.RUNNING)
             # SSM rollback: valid up to the longest prefix agreement with `use`
@@ -625,7 +648,10 @@ class SpecEngine:
         return RoundStats(s=s, qc=qc, t_verify_ms=t_verify, t_draft_ms=t_draft, trace=trace,
                           t_round_ms=(time.perf_counter() - t_start) * 1e3, accepted=accs,
                           emitted=ems, voted=vts, vl=vl, decision=decision.value, group=g.gid,
-                          s_next=self.selector.current_s, weights=dict(self.weights.weights))
+                          s_next=self.selector.current_s, weights=dict(self.weights.weights),
+                          round_index=rnd, request_ids=tuple(g.requests[b].id for b in active),
+                          pool_depth=sum(1 for x in self.groups if x.pending is not None),
+                          draft_start=ts[0], draft_end=ts[1], verify_start=ts[2], verify_end=ts[3])
 
     def run(self, requests: list[Request], max_rounds: int | None = None) -> RunResult:
         """Generate until every request finishes (reference semantics)."""
@@ -645,6 +671,11 @@ class SpecEngine:
         res = RunResult(outputs={})
         t0 = time.perf_counter()
         rnd = 0
+        # device clock origin of this decode (trace timestamps, request finish times)
+        self._run_t0 = torch.cuda.Event(enable_timing=True)
+        self._run_t0.record(self.draft_stream)
+        for r in self.requests:
+            r.arrival_time = 0.0
         if not self.pipelined:
             g = self.groups[0]
             while (max_rounds is None or rnd < max_rounds) and self._start_draft(g):

@@ -166,3 +166,33 @@ def test_tp_shard_math_reproduces_full_layer():
         torch.testing.assert_close(got_o, want_o, rtol=1e-4, atol=1e-5)
         torch.testing.assert_close(got_m, want_m, rtol=1e-4, atol=1e-5)
         torch.testing.assert_close(torch.cat(heads, 1), x @ f["lm_head"].T)
+
+
+def test_trace_and_metrics_match_reference_golden(golden_dir):
+    """trace.TraceEvent.to_json and collect_metrics reproduce the reference's
+    (aggspec/engine.py:49-168) on a golden trace generated by running it."""
+    import json
+    import os
+    from paper_2402_15678_b200.core import Request
+    from paper_2402_15678_b200.trace import TraceEvent, collect_metrics
+    g = json.load(open(os.path.join(golden_dir, "metrics_golden.json")))
+    evs = []
+    for e in g["events"]:
+        ev = TraceEvent(e["seq"], e["kind"], e["start"], e["end"], e["s"], e["request_ids"], e["pool_depth"])
+        if e["kind"] == "verify":
+            ev.round_index, ev.accepted, ev.emitted, ev.voted = e["round"], e["accepted"], e["emitted"], e["voted"]
+            ev.vl, ev.decision, ev.s_next = e["vl"], e["decision"], e["s_next"]
+            ev.weights = {int(k): v for k, v in e["weights"].items()}
+        assert json.loads(ev.to_json()) == e
+        evs.append(ev)
+    reqs = []
+    for r in g["requests"]:
+        q = Request(r["id"], [1], 20)
+        q.generated = r["generated"]
+        q.finish_time = r["finish_time"]
+        reqs.append(q)
+    m = collect_metrics(evs, reqs)
+    for k, v in g["metrics"].items():
+        assert getattr(m, k) == v, k
+    assert {str(k): v for k, v in m.per_ssm_acceptance.items()} == g["per_ssm_acceptance"]
+    assert [list(x) for x in m.s_trajectory] == g["s_trajectory"]

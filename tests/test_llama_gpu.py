@@ -210,6 +210,14 @@ def test_llama_engine_lossless_and_rounds_match_oracle():
     res = eng.decode()
     assert res.outputs == teacher
     assert res.mean_accepted > 1.0
+    # device-timed trace / metrics in the reference's format (trace.py)
+    tr = res.trace()
+    assert len(tr) == 2 * len(res.rounds)
+    for d, v in zip(tr[0::2], tr[1::2]):
+        assert d.kind == "draft" and v.kind == "verify" and d.start <= d.end <= v.start + 1e-3 and v.start <= v.end
+    m = res.metrics(reqs)
+    assert m.tokens_emitted == res.tokens and m.throughput > 0 and 0 < m.llm_utilization <= 1.0
+    assert all(r.finish_time is not None and r.finish_time <= m.total_time + 1e-3 for r in reqs)
     for rd in res.rounds:
         t = rd.trace
         for b in t["active"]:
