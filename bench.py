@@ -3,9 +3,11 @@ output tokens/s + mean accepted length).
 
 Workload at N=1: the configuration BASELINE.json's metric is quoted on —
 Llama-2-70B target + 3 x Llama-160M drafters — which fits one B200 (137.4 GB
-of bf16 weights in 180 GB): bf16, batch 16, adaptive speculation length
-(s_init 4, s in [1, 12]), greedy, 128-token synthetic prompts, 128 new tokens
-per request.  `--target opt-13b --ssm opt-125m` runs configs[1] (cfg2).
+of bf16 weights in 180 GB): bf16, verify batch 16, pipelined SSM decode / LLM
+verify as cfg3 specifies (two request groups of 16: the drafters draft one
+while the verifier verifies the other), adaptive speculation length (s_init
+4, s in [1, 12]), greedy, 128-token synthetic prompts, 128 new tokens per
+request.  --schedule sequential runs one group of 16.  `--target opt-13b --ssm opt-125m` runs configs[1] (cfg2).
 Random-init weights (no checkpoints offline); because random-init drafters
 never agree with the target, drafts use fidelity injection
 (engine.py / DESIGN.md): with probability f_k SSM k's drafted token is
@@ -75,9 +77,10 @@ def parse():
     ap.add_argument("--parallelism", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor-parallel verifier over the ranks (default, SURVEY §8e) or one full "
                          "replica per GPU serving its own batch")
-    ap.add_argument("--schedule", default="sequential", choices=["sequential", "pipelined"],
-                    help="pipelined: two request groups of --batch each (2x requests), verify of one "
-                         "overlapping drafting of the other (aggspec/engine.py:494-576)")
+    ap.add_argument("--schedule", default="pipelined", choices=["sequential", "pipelined"],
+                    help="pipelined (cfg3, default): two request groups of --batch each (verify batch "
+                         "--batch, 2x requests in flight), verify of one overlapping drafting of the "
+                         "other (aggspec/engine.py:494-576); sequential: one group, draft then verify")
     return ap.parse_args()
 
 
