@@ -13,7 +13,7 @@ import os
 from .core import DistMismatch, LengthMismatch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libminions.so")
+LIB_PATH = os.environ.get("MS_LIB") or os.path.join(_HERE, "lib", "libminions.so")  # MS_LIB: diagnostic builds
 
 MS_OK, MS_ERR_VALUE, MS_ERR_LENGTH, MS_ERR_DIST, MS_ERR_UNSUPPORTED, MS_ERR_CUDA = 0, -1, -2, -3, -4, -5
 

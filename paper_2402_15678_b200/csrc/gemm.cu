@@ -91,9 +91,11 @@ struct LinearCfg {
   // the fp32 partial tile is staged in the (idle) ring smem only for the
   // split-K cluster reduction; the single-split gated epilogue exchanges
   // gate/up through a 4 KB buffer instead
+  static constexpr int GATED_EPI_BYTES = BN * 65 * 4 + BN * 64 * 2;  // up half + bf16 output tile
   __host__ __device__ static int data_bytes(int sw, int sx, bool part) {
     const int pipe = sw * W_BYTES + sx * X_BYTES;
-    const int need = part ? PART_BYTES : 4096;
+    int need = part ? PART_BYTES : GATED_EPI_BYTES;
+    if (need < GATED_EPI_BYTES) need = GATED_EPI_BYTES;
     return pipe > need ? pipe : need;
   }
   __host__ __device__ static int smem(int sw, int sx, bool part) {
@@ -229,6 +231,12 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         const int st = i % SX;
         if (p.nc == 1) {
           if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+#ifdef MS_EXP_NOX  // diagnostic build only: reuse the first SX token tiles (wrong results)
+          if (i >= SX) {
+            tc::mbar_arrive(&fullX[st]);
+            continue;
+          }
+#endif
           tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
           tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, pol_x);
         } else if (x_leader) {
@@ -250,7 +258,11 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   } else if (warp == 1) {
     pdl_trigger();
     if (lane == 0) {
+#ifdef MS_EXP_N16  // diagnostic build only: 16-column MMAs (wrong results)
+      constexpr uint32_t idesc = tc::idesc_bf16(kBM, 16);
+#else
       constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
+#endif
       for (int i = 0; i < nkb; ++i) {
         const int ws = i % SW, xs = i % SX;
         tc::mbar_wait(&fullW[ws], (i / SW) & 1);
@@ -336,31 +348,56 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+#ifdef MS_EXP_NOEPI  // diagnostic build only: no epilogue (no outputs)
+    if (p.splits == 1) goto epi_done;
+#endif
 
     if (p.splits == 1 && p.act == 2) {
-      // gated SiLU, one split: the up warps (TMEM lanes 64..127) hand their
-      // 16-column chunk to the gate warps (lanes 0..63) through 4 KB of smem
-      // (the pipeline smem is idle once tmem_full fired)
-      float* xb = reinterpret_cast<float*>(smem);  // [64][17]
+      // gated SiLU, one split (the pipeline smem is idle once tmem_full fired):
+      // (1) the up warps (TMEM lanes 64..127) park the whole up half in smem,
+      // (2) one barrier, the gate warps form silu(g) * u into a bf16 output
+      // tile in smem, (3) one barrier, all four warps store the tile with
+      // coalesced 16-byte writes.  (The previous per-16-column exchange with
+      // two barriers per chunk and 2-byte stores cost ~13% of the 70B gate/up
+      // GEMM at M = 176.)
+      float* U = reinterpret_cast<float*>(smem);                            // [BN][65] fp32
+      __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(U + BN * 65);    // [BN][64] bf16
       const bool up = q >= 2;
-      const int of = tile_n * (kBM / 2) + (q & 1) * 32 + lane;  // output feature (gate warps)
-      for (int c0 = 0; c0 < m_hi; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(trow + c0, r);
+      const int f = (q & 1) * 32 + lane;  // gate / up feature within the 64-wide half
+      for (int c0 = 0; c0 < m_hi; c0 += 32) {
+        uint32_t r[32];
+        tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
+        tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
         tc::tmem_wait_ld();
         if (up) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) xb[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < m_hi) U[(c0 + j) * 65 + f] = __uint_as_float(r[j]);
         }
-        epi_bar128();
-        if (!up) {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + of;
+      }
+      epi_bar128();
+      // the gate warps read their TMEM half after the barrier (re-loading is
+      // cheaper than holding up to 256 columns in registers)
+      if (!up) {
+        for (int c0 = 0; c0 < m_hi; c0 += 32) {
+          uint32_t r[32];
+          tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+          tc::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi && n0 < p.N)  // n0 >= N: the padding tile of an odd multicast pair
-              o[(int64_t)(orow + c0 + j) * p.ldc] = f2bf(silu_mul(__uint_as_float(r[j]), xb[(q * 32 + lane) * 17 + j]));
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < m_hi) O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]), U[(c0 + j) * 65 + f]));
         }
-        epi_bar128();
+      }
+      epi_bar128();
+      if (n0 < p.N) {  // n0 >= N: the padding tile of an odd multicast pair
+        const int et = threadIdx.x - 64;  // 0..127
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
+        for (int e = et; e < m_hi * 8; e += 128) {
+          const int row = e >> 3, ch = e & 7;
+          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
+              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
+        }
       }
     } else if (p.splits == 1) {
       for (int c0 = 0; c0 < m_hi; c0 += 16) {
@@ -386,6 +423,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       }
     }
   }
+#ifdef MS_EXP_NOEPI
+epi_done:
+#endif
   if (p.splits > 1) {
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
@@ -1102,7 +1142,9 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (M == 0) return MS_OK;
   if (!x || !w || !out) return MS_ERR_VALUE;
   if (act < 0 || act > 2) return MS_ERR_VALUE;
-  if (act == 2 && (N % kBM || bias || residual || out_f32)) return MS_ERR_UNSUPPORTED;
+  if (act == 2 && (N % kBM || bias || residual || out_f32 || ldc % 8 ||
+                   (reinterpret_cast<uintptr_t>(out) & 15)))
+    return MS_ERR_UNSUPPORTED;  // gated epilogue stores 16-byte vectors
   if (K % 8 != 0 || ldx % 8 != 0) return MS_ERR_UNSUPPORTED;  // TMA: 16-byte row strides
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
