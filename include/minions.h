@@ -133,6 +133,19 @@ int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
               int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
               int* counters, int n_counters, void* stream);
+/* ms_linear with the RMSNorm folded across GEMMs (the norm's gain is
+ * pre-multiplied into the consumer's weight, so no normalised activation is
+ * written): rms_out != NULL — a residual-writing split-K GEMM (bf16 out,
+ * splits >= 2) also writes, per 128-feature tile t and row m, the sum of
+ * squares of the bf16 values it stored: rms_out[m * rms_ld + t] (a row's
+ * partials contiguous); rms_in != NULL — the GEMM runs on the raw residual
+ * stream x and scales its fp32 accumulator by rstd[m] = rsqrt(sum_{t <
+ * rms_nparts} rms_in[m * rms_ld + t] / K + eps) before the epilogue (bias / activation / gated SiLU / residual).
+ * Fixed summation orders: deterministic and batch invariant. */
+int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                  int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                  int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
+                  int64_t rms_ld, void* stream);
 /* ms_linear with the LayerNorm that precedes the projection fused in:
  *   out = act(LN(x) . w^T + bias) + residual,  LN(x) = (x - mean) * rstd * gamma + beta
  * (fp32 two-pass row statistics, eps).  Every CTA recomputes the statistics of

@@ -52,9 +52,33 @@ def split_gate_up(w_gu: torch.Tensor, ffn: int):
     return w_gu[gate], w_gu[gate + 64]
 
 
-def forward(w: dict, cfg, tokens, last_only: bool = False) -> torch.Tensor:
+def fold(w: dict, cfg) -> dict:
+    """LlamaWeights.fold_norms restated: gains folded into the consuming
+    projection with one bf16 rounding, gains := 1."""
+    out = dict(w)
+    pairs = [(f"l{i}.attn_norm", f"l{i}.w_qkv") for i in range(cfg.n_layers)]
+    pairs += [(f"l{i}.mlp_norm", f"l{i}.w_gu") for i in range(cfg.n_layers)] + [("norm_f", "lm_head")]
+    for g, name in pairs:
+        out[name] = (w[name].float() * w[g].float()[None, :]).to(BF16)
+        out[g] = torch.ones_like(w[g])
+    return out
+
+
+def rstd(x, eps):
+    return torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
+
+
+def forward(w: dict, cfg, tokens, last_only: bool = False, fused_norm: bool = False) -> torch.Tensor:
     """Full causal forward of one sequence from position 0 (no cache).
-    tokens [T] -> logits [T, V] fp32 (or [1, V])."""
+    tokens [T] -> logits [T, V] fp32 (or [1, V]).
+
+    fused_norm: the verifier's contract (LlamaModel fuse_norm): gains folded
+    into the next projection; for every layer but the first the projection
+    runs on the raw residual stream and its fp32 result is scaled by
+    rstd(x) = rsqrt(mean(x^2) + eps), rounded once — no bf16 normalised
+    activation in between."""
+    if fused_norm:
+        w = fold(w, cfg)
     f32 = {k: v.float() for k, v in w.items()}
     tok = torch.as_tensor(list(tokens), dtype=torch.long)
     T = tok.numel()
@@ -67,8 +91,11 @@ def forward(w: dict, cfg, tokens, last_only: bool = False) -> torch.Tensor:
     mask = torch.triu(torch.ones(T, T, dtype=torch.bool), 1)
     for i in range(cfg.n_layers):
         p = f"l{i}."
-        h = rmsnorm(x, f32[p + "attn_norm"], cfg.eps)
-        qkv = _bf(h @ f32[p + "w_qkv"].T)
+        if fused_norm and i > 0:
+            qkv = _bf((x @ f32[p + "w_qkv"].T) * rstd(x, cfg.eps))
+        else:
+            h = rmsnorm(x, f32[p + "attn_norm"], cfg.eps)
+            qkv = _bf(h @ f32[p + "w_qkv"].T)
         q = rope(qkv[:, : H * D].view(T, H, D), pos, table)
         k = rope(qkv[:, H * D: (H + Hkv) * D].view(T, Hkv, D), pos, table)
         v = qkv[:, (H + Hkv) * D:].view(T, Hkv, D)
@@ -78,18 +105,24 @@ def forward(w: dict, cfg, tokens, last_only: bool = False) -> torch.Tensor:
         sc = sc.masked_fill(mask, float("-inf"))
         a = _bf((torch.softmax(sc, dim=-1) @ v.transpose(0, 1)).transpose(0, 1).reshape(T, H * D))
         x = _bf(a @ f32[p + "w_o"].T + x)
-        h = rmsnorm(x, f32[p + "mlp_norm"], cfg.eps)
         wg, wu = split_gate_up(f32[p + "w_gu"], cfg.ffn)
-        gt, up = h @ wg.T, h @ wu.T
+        if fused_norm:
+            r = rstd(x, cfg.eps)
+            gt, up = (x @ wg.T) * r, (x @ wu.T) * r
+        else:
+            h = rmsnorm(x, f32[p + "mlp_norm"], cfg.eps)
+            gt, up = h @ wg.T, h @ wu.T
         ff = _bf(gt / (1.0 + torch.exp(-gt)) * up)
         x = _bf(ff @ f32[p + "w_down"].T + x)
     if last_only:
         x = x[-1:]
+    if fused_norm:
+        return (x @ f32["lm_head"].T) * rstd(x, cfg.eps)
     return rmsnorm(x, f32["norm_f"], cfg.eps) @ f32["lm_head"].T
 
 
-def greedy_generate(w, cfg, prompt, n_new: int) -> list[int]:
+def greedy_generate(w, cfg, prompt, n_new: int, fused_norm: bool = False) -> list[int]:
     ctx = list(prompt)
     for _ in range(n_new):
-        ctx.append(int(torch.argmax(forward(w, cfg, ctx, last_only=True)[-1])))
+        ctx.append(int(torch.argmax(forward(w, cfg, ctx, last_only=True, fused_norm=fused_norm)[-1])))
     return ctx[len(prompt):]

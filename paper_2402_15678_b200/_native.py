@@ -35,6 +35,7 @@ _SIGS = {
     "ms_accept_greedy_logits": [_P, _P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "ms_accept_stochastic": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I64, _P, _I, _P],
+    "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _P],
     "ms_gemv": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
     "ms_linear_ln": [_P, _I64, _P, _P, _F, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P],
     "ms_linear_workspace": [_I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],

@@ -48,6 +48,17 @@ struct LinearParams {
   int n_tiles;
   int sw, sx;                     // W / X ring depths of this launch (cluster path)
   int nc;                         // N tiles sharing one multicast X tile (cluster = splits * nc CTAs)
+  // RMSNorm folded across GEMMs (gains pre-multiplied into the consumer's
+  // weight): a residual-writing split-K GEMM emits per-(row, tile) sums of
+  // squares of the bf16 values it stores (rms_out[row * rms_ld + tile], a row's
+  // partials contiguous); the next GEMM runs on the raw residual stream and
+  // scales its fp32 accumulator by rstd[row] = rsqrt(sum_t rms_in[row * rms_ld
+  // + t] / K + eps).
+  float* rms_out;
+  const float* rms_in;
+  int rms_nparts;
+  int64_t rms_ld;
+  float rms_eps;
   // fused LayerNorm of the X operand (ln_g != null): X = LN(x) * g + b, the raw
   // rows x [M, ldx] read for the row statistics, the TMA tile normalised in
   // shared memory before the MMA consumes it
@@ -103,15 +114,19 @@ struct LinearCfg {
   }
 };
 
-// tok: global output row; feat: feature within the row group grp
-__device__ __forceinline__ void epi_store(const LinearParams& p, int tok, int feat, float v, int grp = 0) {
+// tok: global output row; feat: feature within the row group grp.  Returns
+// the value as stored (bf16-rounded for bf16 outputs).
+__device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int feat, float v, int grp = 0) {
   if (p.bias) v += bf2f(p.bias[(int64_t)grp * p.N + feat]);
   if (p.act == 1) v = fmaxf(v, 0.0f);
   if (p.residual) v += bf2f(p.residual[(int64_t)tok * p.ldr + feat]);
-  if (p.out_f32)
+  if (p.out_f32) {
     reinterpret_cast<float*>(p.out)[(int64_t)tok * p.ldc + feat] = v;
-  else
-    reinterpret_cast<__nv_bfloat16*>(p.out)[(int64_t)tok * p.ldc + feat] = f2bf(v);
+    return v;
+  }
+  const __nv_bfloat16 b = f2bf(v);
+  reinterpret_cast<__nv_bfloat16*>(p.out)[(int64_t)tok * p.ldc + feat] = b;
+  return bf2f(b);
 }
 
 __device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -345,6 +360,20 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         tc::mbar_arrive(&normed[stage]);
       }
     }
+    if (p.rms_in) {
+      // folded RMSNorm: this tile's rows' rstd from the producer's partials
+      // (fixed summation order), while the mainloop runs
+      // one warp per row: lanes take partials l, l+32, ... (coalesced), then a
+      // fixed shuffle tree
+      for (int r = q; r < m_hi; r += 4) {
+        const float* pr = p.rms_in + (int64_t)(orow + r) * p.rms_ld;
+        float sq = 0.f;
+        for (int t = lane; t < p.rms_nparts; t += 32) sq += pr[t];
+        sq = warp_sum(sq);
+        if (lane == 0) s_rstd[r] = rsqrtf(sq / (float)p.K + p.rms_eps);
+      }
+      epi_bar128();
+    }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
@@ -372,7 +401,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         if (up) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (c0 + j < m_hi) U[(c0 + j) * 65 + f] = __uint_as_float(r[j]);
+            if (c0 + j < m_hi) U[(c0 + j) * 65 + f] = __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f);
         }
       }
       epi_bar128();
@@ -386,7 +415,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
           tc::tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (c0 + j < m_hi) O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]), U[(c0 + j) * 65 + f]));
+            if (c0 + j < m_hi)
+              O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f),
+                                                   U[(c0 + j) * 65 + f]));
         }
       }
       epi_bar128();
@@ -407,7 +438,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         if (feat_ok) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi) epi_store(p, orow + c0 + j, feat, __uint_as_float(r[j]), grp);
+            if (c0 + j < m_hi) epi_store(p, orow + c0 + j, feat, __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f), grp);
         }
       }
     } else {
@@ -445,22 +476,50 @@ epi_done:
     auto ld4 = [&](const float* a, int rk) {  // rank rk of this N-tile's split group
       return cl ? ld_dsmem_f4(a, jn * p.splits + rk) : *reinterpret_cast<const float4*>(a);
     };
+    if (p.rms_out && !gated) {
+      // residual producer of a folded RMSNorm: token-granular slices, one warp
+      // per token row, lane l = features 4l..4l+3; the row's sum of squares of
+      // the stored bf16 values over this tile's 128 features is a fixed-order
+      // warp reduction written to its own (tile, row) slot — deterministic
+      const int t0 = split * m_hi / p.splits, t1 = (split + 1) * m_hi / p.splits;
+      for (int j = t0 + warp; j < t1; j += kThreads / 32) {
+        const int f4 = lane * 4;
+        float4 acc = ld4(P + j * kBM + f4, 0);
+        for (int rk = 1; rk < p.splits; ++rk) {
+          const float4 v = ld4(P + j * kBM + f4, rk);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        const float rs = p.rms_in ? s_rstd[j] : 1.f;
+        const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
+        const int feat = n0 + f4;
+        float sq = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (feat + t < p.N) {
+            const float st = epi_store(p, orow + j, feat + t, a4[t], grp);
+            sq += st * st;
+          }
+        sq = warp_sum(sq);
+        if (lane == 0 && n0 < p.N) p.rms_out[(int64_t)(orow + j) * p.rms_ld + tile_n] = sq;
+      }
+    } else {
     for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
       const int j = u / upr;
       const int f4 = (u - j * upr) * 4;
+      const float rs = p.rms_in ? s_rstd[j] : 1.f;
       float4 acc = ld4(P + j * kBM + f4, 0);
       for (int rk = 1; rk < p.splits; ++rk) {
         const float4 v = ld4(P + j * kBM + f4, rk);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
       if (gated) {
         float4 up = ld4(P + j * kBM + f4 + kBM / 2, 0);
         for (int rk = 1; rk < p.splits; ++rk) {
           const float4 v = ld4(P + j * kBM + f4 + kBM / 2, rk);
           up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
         }
-        const float u4[4] = {up.x, up.y, up.z, up.w};
+        const float u4[4] = {up.x * rs, up.y * rs, up.z * rs, up.w * rs};
         const int of = tile_n * (kBM / 2) + f4;  // output feature
         if (n0 >= p.N) continue;                 // padding tile of an odd multicast pair
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
@@ -472,6 +531,7 @@ epi_done:
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
+    }
     }
     if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
   }
@@ -1132,11 +1192,19 @@ extern "C" int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* 
   return MS_OK;
 }
 
+struct RmsArgs {
+  float* out = nullptr;
+  const float* in = nullptr;
+  int nparts = 0;
+  int64_t ld = 0;
+  float eps = 0.f;
+};
+
 static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias,
                        const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
                        int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
                        int* counters, int n_counters, const void* g_ln_g, const void* g_ln_b,
-                       float g_ln_eps, void* stream, int G = 1) {
+                       float g_ln_eps, void* stream, int G = 1, RmsArgs rms = RmsArgs()) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
@@ -1164,6 +1232,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.ldr = ldr;
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
+  p.rms_out = nullptr; p.rms_in = nullptr; p.rms_nparts = 0; p.rms_ld = 0; p.rms_eps = 0.f; p.nc = 1;
   p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
   if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
     p.ln_g = (const __nv_bfloat16*)g_ln_g;
@@ -1172,9 +1241,11 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
     p.ln_eps = g_ln_eps;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
+  const bool folded = rms.out || rms.in;
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
-  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 &&
+  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded &&
       ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
     SKParams sk;
     sk.iters = n_tiles * kb_total;
@@ -1203,7 +1274,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   }
   // weight-streaming GEMMs with at least one 128-feature tile per SM: the
   // persistent schedule (whole tiles; MS_PK=0 disables, for A/B runs)
-  if (splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && n_tiles >= sm_count() && pk_enabled()) {
+  if (splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count() && pk_enabled()) {
     switch (bn) {
       case 16: return launch_linear_pk<16>(tw, tx, p, st);
       case 32: return launch_linear_pk<32>(tw, tx, p, st);
@@ -1226,6 +1297,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (splits <= 0) splits = linear_auto_splits(N, K);
   if (splits > kb_total) splits = kb_total;
   if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
+  if (rms.out && (splits < 2 || act == 2 || out_f32)) return MS_ERR_UNSUPPORTED;  // producer: split-K bf16 path
   p.splits = splits;
   switch (bn) {
     case 16: return launch_linear<16>(tw, tx, p, m_tiles, st, G);
@@ -1271,4 +1343,21 @@ extern "C" int ms_linear_grouped(const void* x, int64_t ldx, const void* w, cons
                                  int splits, int G, void* stream) {
   return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
                      nullptr, nullptr, 0.f, stream, G);
+}
+
+extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                             int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                             int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
+                             int64_t rms_ld, void* stream) {
+  if ((rms_in && rms_nparts < 1) || (!rms_in && !rms_out) || (rms_in && rms_ld < rms_nparts) ||
+      (rms_out && rms_ld < (N + 127) / 128))
+    return MS_ERR_VALUE;
+  RmsArgs r;
+  r.out = rms_out;
+  r.in = rms_in;
+  r.nparts = rms_nparts;
+  r.ld = rms_ld;
+  r.eps = rms_eps;
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
+                     nullptr, nullptr, 0.f, stream, 1, r);
 }

@@ -74,6 +74,27 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     return out
 
 
+def linear_rms(x: torch.Tensor, w: torch.Tensor, *, residual: torch.Tensor | None = None, act: int = 0,
+               out: torch.Tensor, out_f32: bool = False, rms_in: torch.Tensor | None = None, eps: float = 1e-5,
+               rms_out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """ms_linear with the RMSNorm folded across GEMMs: rms_in [rows, n_parts]
+    fp32 partial sums of squares (from the producer) -> scale by rstd; rms_out
+    [rows, N / 128] fp32 -> this (residual-writing, split-K) GEMM emits them."""
+    M, K = x.shape
+    N = w.shape[0]
+    if x.dtype != BF16 or w.dtype != BF16 or w.shape[1] != K or not w.is_contiguous():
+        raise ValueError("x [M, K] and w [N, K] must be bf16")
+    ref = rms_in if rms_in is not None else rms_out
+    if ref is None or ref.dtype != torch.float32 or not ref.is_contiguous():
+        raise ValueError("rms partial buffers must be contiguous fp32 [parts, ld]")
+    _native.call("ms_linear_rms", x.data_ptr(), x.stride(0), w.data_ptr(), None,
+                 None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
+                 out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, 0,
+                 None if rms_in is None else rms_in.data_ptr(), 0 if rms_in is None else rms_in.shape[1], eps,
+                 None if rms_out is None else rms_out.data_ptr(), ref.stride(0), _dev.stream_ptr(stream))
+    return out
+
+
 def gemv(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
          residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
          out_f32: bool = False, stream=None) -> torch.Tensor:

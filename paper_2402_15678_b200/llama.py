@@ -129,6 +129,23 @@ class LlamaWeights:
     def to(self, device) -> "LlamaWeights":
         return LlamaWeights(self.cfg, {k: v.to(device) for k, v in self.t.items()})
 
+    def fold_norms(self) -> "LlamaWeights":
+        """Fold every RMSNorm gain into the projection that consumes it, in
+        place: w_qkv[:, k] *= attn_norm[k], w_gu[:, k] *= mlp_norm[k],
+        lm_head[:, k] *= norm_f[k] (one bf16 rounding), gains := 1.  Exact
+        no-op on values for unit gains (random init)."""
+        if getattr(self, "folded", False):
+            return self
+        c, t = self.cfg, self.t
+        pairs = [(f"l{i}.attn_norm", f"l{i}.w_qkv") for i in range(c.n_layers)]
+        pairs += [(f"l{i}.mlp_norm", f"l{i}.w_gu") for i in range(c.n_layers)] + [("norm_f", "lm_head")]
+        for g, w in pairs:
+            if not bool(torch.all(t[g] == 1)):
+                t[w].mul_(t[g].to(t[w].dtype)[None, :])
+            t[g] = torch.ones_like(t[g])  # a new tensor: shared gains elsewhere are untouched
+        self.folded = True
+        return self
+
     def __getitem__(self, k: str) -> torch.Tensor:
         return self.t[k]
 
@@ -148,13 +165,32 @@ class LlamaModel:
 
     PREFILL_ROWS = 512
 
-    def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False):
+    def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False,
+                 fuse_norm: bool | None = None):
         """small_gemm: projections of <= 64 token rows with K <= 1024 use the
         low-latency ms_gemv (drafters' decode steps); the verifier keeps the
-        tcgen05 path everywhere, so its numerics never depend on the row count."""
+        tcgen05 path everywhere, so its numerics never depend on the row count.
+
+        fuse_norm (default: the verifier, i.e. not small_gemm): RMSNorm folded
+        across GEMMs — the gains are folded into w_qkv / w_gu / lm_head
+        (LlamaWeights.fold_norms, in place), the O / down GEMMs emit per-row
+        sums of squares and the QKV / gate-up / LM-head GEMMs scale by rstd:
+        no RMSNorm kernel and no normalised activation between layers (one
+        explicit norm before layer 0).  Numerics: out = rstd * (x . (g * W)^T)
+        in fp32, one rounding (oracle/llama_ref.forward(fused_norm=True))."""
         self.w, self.cfg = w, w.cfg
         self.small_gemm = small_gemm
         c = self.cfg
+        if fuse_norm is None:
+            fuse_norm = not small_gemm
+        o_split = K.linear_splits(c.d, c.n_heads * c.head_dim)
+        d_split = K.linear_splits(c.d, c.ffn)
+        self.fuse_norm = bool(fuse_norm) and o_split > 1 and d_split > 1  # producers need split-K
+        if self.fuse_norm:
+            w.fold_norms()
+        self.n_parts = (c.d + 127) // 128
+        self.rms_a = torch.zeros((max_rows, self.n_parts), dtype=torch.float32, device=device) if self.fuse_norm else None
+        self.rms_b = torch.zeros((max_rows, self.n_parts), dtype=torch.float32, device=device) if self.fuse_norm else None
         self.device = torch.device(device)
         self.max_rows = max_rows
         self.x = torch.empty((max_rows, c.d), dtype=BF16, device=device)
@@ -180,6 +216,8 @@ class LlamaModel:
         K.embed(tokens, start, Q, w["tok_emb"], None, 0, out=x, stream=stream)
         small = self.small_gemm and R <= 64
         prefill = R >= self.PREFILL_ROWS
+        if self.fuse_norm and not prefill:
+            return self._forward_fused(tokens, start, slot, cache, logits, head_rows, stream)
 
         def lin(xx, wname, **kw):
             if prefill:
@@ -202,6 +240,34 @@ class LlamaModel:
         hf = self.h[:Rh]
         K.rmsnorm(x, w["norm_f"], c.eps, out=hf, rows=head_rows, stream=stream)
         K.linear(hf, w["lm_head"], out=logits, out_f32=True, stream=stream)
+        return logits
+
+    def _forward_fused(self, tokens, start, slot, cache, logits, head_rows, stream):
+        """Layers with the RMSNorms folded across GEMMs (see __init__); x is
+        already embedded."""
+        c, w = self.cfg, self.w
+        B, Q = tokens.shape
+        R = B * Q
+        x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
+        ra, rb = self.rms_a, self.rms_b
+        for i in range(c.n_layers):
+            p = f"l{i}."
+            if i == 0:  # the embedding has no producer GEMM: one explicit norm (gain folded: ones)
+                K.rmsnorm(x, w[p + "attn_norm"], c.eps, out=h, stream=stream)
+                K.linear(h, w[p + "w_qkv"], out=qkv, stream=stream)
+            else:
+                K.linear_rms(x, w[p + "w_qkv"], out=qkv, rms_in=rb, eps=c.eps, stream=stream)
+            K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+            K.linear_rms(at, w[p + "w_o"], residual=x, out=x, rms_out=ra, stream=stream)
+            K.linear_rms(x, w[p + "w_gu"], act=2, out=ff, rms_in=ra, eps=c.eps, stream=stream)
+            K.linear_rms(ff, w[p + "w_down"], residual=x, out=x, rms_out=rb, stream=stream)
+        if head_rows is None:
+            K.linear_rms(x, w["lm_head"], out=logits, out_f32=True, rms_in=rb, eps=c.eps, stream=stream)
+        elif head_rows.numel() > 0:
+            hf = self.h[: head_rows.numel()]
+            K.rmsnorm(x, w["norm_f"], c.eps, out=hf, rows=head_rows, stream=stream)
+            K.linear(hf, w["lm_head"], out=logits, out_f32=True, stream=stream)
         return logits
 
 

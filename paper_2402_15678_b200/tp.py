@@ -227,7 +227,7 @@ class LlamaTPModel(LlamaModel):
     def __init__(self, shard: LlamaWeights, comm: TPComm, max_rows: int, device="cuda"):
         if max_rows > comm.max_rows:
             raise ValueError("max_rows exceeds the symmetric buffers")
-        super().__init__(shard, max_rows=max_rows, device=device)
+        super().__init__(shard, max_rows=max_rows, device=device, fuse_norm=False)
         self.comm = comm
         self.tp = comm.t
         self.x = comm.x  # residual stream = symmetric buffer

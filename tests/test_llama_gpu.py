@@ -148,8 +148,9 @@ def test_llama_forward_prefill_and_decode_vs_reference(small_gemm, name):
     got = torch.cat(outs, 1)
     agree = total = 0
     worst = 0.0
+    assert model.fuse_norm == (not small_gemm)
     for b in range(B):
-        ref = llama_ref.forward(w_cpu.t, cfg, toks[b])
+        ref = llama_ref.forward(w_cpu.t, cfg, toks[b], fused_norm=model.fuse_norm)
         worst = max(worst, (got[b] - ref).abs().max().item() / ref.abs().max().item())
         agree += int((got[b].argmax(-1) == ref.argmax(-1)).sum())
         total += ref.shape[0]
@@ -202,7 +203,7 @@ def test_llama_engine_lossless_and_rounds_match_oracle():
     fresh = [Request(r.id, list(r.prompt), 48) for r in reqs]
     teacher = eng.greedy_teacher(fresh, 48)
     # greedy decode on the device == the fp32 CPU reference's greedy decode (first tokens)
-    ref = llama_ref.greedy_generate(target.t, tcfg, reqs[0].prompt, 12)
+    ref = llama_ref.greedy_generate(target.t, tcfg, reqs[0].prompt, 12, fused_norm=True)
     n = next((i for i in range(12) if ref[i] != teacher[reqs[0].id][i]), 12)
     assert n >= 6, (ref, teacher[reqs[0].id][:12])
     eng.prefill(reqs)
@@ -314,3 +315,35 @@ def test_llama_engine_grouped_equals_per_drafter(monkeypatch):
         assert res.outputs == teacher
         outs.append([(rd.trace["drafts"].tolist(), rd.trace["voted"].tolist(), rd.accepted) for rd in res.rounds])
     assert outs[0] == outs[1]
+
+
+def test_folded_rmsnorm_matches_explicit_norm_and_reference():
+    """RMSNorm folded across GEMMs (fuse_norm) vs the explicit-norm forward of
+    the same weights: logits agree to bf16 tolerance; both agree with their
+    fp32 reference restatements; the fold leaves unit-gain models unchanged."""
+    from paper_2402_15678_b200.llama import LlamaModel, LlamaWeights
+    cfg, w_cpu = _tiny_llama(6)
+    fused = LlamaModel(w_cpu.to("cuda"), max_rows=256)
+    plain = LlamaModel(w_cpu.to("cuda"), max_rows=256, fuse_norm=False)
+    assert fused.fuse_norm and not plain.fuse_norm
+    B, T0 = 3, 20
+    rng = np.random.default_rng(6)
+    toks = rng.integers(0, cfg.vocab, size=(B, T0)).astype(np.int32)
+    slot = torch.arange(B, dtype=torch.int32, device="cuda")
+    z = torch.zeros(B, dtype=torch.int32, device="cuda")
+    outs = []
+    for m in (fused, plain):
+        lg = torch.empty(B * T0, cfg.vocab, device="cuda")
+        m.forward(torch.tensor(toks, device="cuda"), z, slot, _kv(cfg, B, 32), lg)
+        outs.append(lg.view(B, T0, -1).cpu())
+    rel = (outs[0] - outs[1]).abs().max().item() / outs[1].abs().max().item()
+    assert rel < 2e-2, rel
+    for b in range(B):
+        for got, fz in ((outs[0][b], True), (outs[1][b], False)):
+            ref = llama_ref.forward(w_cpu.t, cfg, toks[b], fused_norm=fz)
+            assert (got - ref).abs().max().item() / ref.abs().max().item() < 2e-2
+    # unit gains: folding is an exact no-op on the weights
+    wu = LlamaWeights.random(cfg, 7, device="cpu", std=0.05)
+    before = {k: v.clone() for k, v in wu.t.items()}
+    wu.fold_norms()
+    assert all(torch.equal(before[k], wu.t[k]) for k in before)

@@ -45,7 +45,7 @@ def _setup(t, B=4, T=64, seed=0, name="tiny-llama"):
     from paper_2402_15678_b200.tp import LlamaTPModel, TPComm, shard_llama
     cfg = CONFIGS[name]
     w = LlamaWeights.random(cfg, seed, device="cpu", std=0.05, norm_std=0.1)
-    full = LlamaModel(w.to("cuda"), max_rows=B * T)
+    full = LlamaModel(w.to("cuda"), max_rows=B * T, fuse_norm=False)  # TP keeps the explicit-norm contract
     comms = TPComm.local_group(t, B * T, cfg.d)
     shards = [shard_llama(w, r, t).to("cuda") for r in range(t)]
     models = [LlamaTPModel(shards[r], comms[r], max_rows=B * T) for r in range(t)]
