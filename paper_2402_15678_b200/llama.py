@@ -22,6 +22,7 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -171,7 +172,7 @@ class LlamaModel:
         low-latency ms_gemv (drafters' decode steps); the verifier keeps the
         tcgen05 path everywhere, so its numerics never depend on the row count.
 
-        fuse_norm (default: the verifier, i.e. not small_gemm): RMSNorm folded
+        fuse_norm (opt-in, MS_FUSE_NORM=1 or True): RMSNorm folded
         across GEMMs — the gains are folded into w_qkv / w_gu / lm_head
         (LlamaWeights.fold_norms, in place), the O / down GEMMs emit per-row
         sums of squares and the QKV / gate-up / LM-head GEMMs scale by rstd:
@@ -182,7 +183,11 @@ class LlamaModel:
         self.small_gemm = small_gemm
         c = self.cfg
         if fuse_norm is None:
-            fuse_norm = not small_gemm
+            # opt-in (MS_FUSE_NORM=1): the bench A/B measured no gain — 1,929 vs
+            # 2,052 tokens/s pipelined (graph A/B of the forward alone: -0.9 ms
+            # at Q = 7, +0.35 ms at Q = 11; the token-granular producer epilogue
+            # offsets the saved norm kernels)
+            fuse_norm = os.environ.get("MS_FUSE_NORM", "0") == "1" and not small_gemm
         o_split = K.linear_splits(c.d, c.n_heads * c.head_dim)
         d_split = K.linear_splits(c.d, c.ffn)
         self.fuse_norm = bool(fuse_norm) and o_split > 1 and d_split > 1  # producers need split-K

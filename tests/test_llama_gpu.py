@@ -126,7 +126,7 @@ def _kv(cfg, B, T):
 def test_llama_forward_prefill_and_decode_vs_reference(small_gemm, name):
     from paper_2402_15678_b200.llama import LlamaModel
     cfg, w_cpu = _tiny_llama(0, name)
-    model = LlamaModel(w_cpu.to("cuda"), max_rows=256, small_gemm=small_gemm)
+    model = LlamaModel(w_cpu.to("cuda"), max_rows=256, small_gemm=small_gemm, fuse_norm=not small_gemm)
     B, T0 = 4, 24
     rng = np.random.default_rng(0)
     toks = rng.integers(0, cfg.vocab, size=(B, T0 + 6)).astype(np.int32)
@@ -203,7 +203,7 @@ def test_llama_engine_lossless_and_rounds_match_oracle():
     fresh = [Request(r.id, list(r.prompt), 48) for r in reqs]
     teacher = eng.greedy_teacher(fresh, 48)
     # greedy decode on the device == the fp32 CPU reference's greedy decode (first tokens)
-    ref = llama_ref.greedy_generate(target.t, tcfg, reqs[0].prompt, 12, fused_norm=True)
+    ref = llama_ref.greedy_generate(target.t, tcfg, reqs[0].prompt, 12, fused_norm=eng.target.fuse_norm)
     n = next((i for i in range(12) if ref[i] != teacher[reqs[0].id][i]), 12)
     assert n >= 6, (ref, teacher[reqs[0].id][:12])
     eng.prefill(reqs)
@@ -323,7 +323,7 @@ def test_folded_rmsnorm_matches_explicit_norm_and_reference():
     fp32 reference restatements; the fold leaves unit-gain models unchanged."""
     from paper_2402_15678_b200.llama import LlamaModel, LlamaWeights
     cfg, w_cpu = _tiny_llama(6)
-    fused = LlamaModel(w_cpu.to("cuda"), max_rows=256)
+    fused = LlamaModel(w_cpu.to("cuda"), max_rows=256, fuse_norm=True)
     plain = LlamaModel(w_cpu.to("cuda"), max_rows=256, fuse_norm=False)
     assert fused.fuse_norm and not plain.fuse_norm
     B, T0 = 3, 20
