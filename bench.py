@@ -52,10 +52,12 @@ METRIC = "output tokens/sec, Llama-2-70B + 3x160M SSMs, 1-8 B200; mean accepted 
 
 
 def workload(args) -> str:
+    sched = ("pipelined SSM decode / LLM verify (2 groups)" if args.schedule == "pipelined"
+             else "sequential draft / verify")
     if args.target == "llama-2-70b":
-        return (f"cfg3 model set at TP=1: Llama-2-70B target + 3x {args.ssm} SSMs, bf16, 1 B200/rank, "
-                f"batch {args.batch}, adaptive s")
-    return f"{args.target} target + 3x {args.ssm} SSMs, bf16, 1 B200/rank, batch {args.batch}, adaptive s"
+        return (f"cfg3: Llama-2-70B target + 3x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, "
+                f"adaptive s")
+    return (f"{args.target} target + 3x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, adaptive s")
 
 
 def parse():
@@ -481,7 +483,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "impl": "reference",
                 "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * 3,
-                           "global_batch": args.batch},
+                           "global_batch": args.batch * (2 if args.schedule == "pipelined" else 1),
+                           "schedule": args.schedule},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": round(cb["value"], 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
