@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1)
     ap.add_argument("--fixed-s", type=int, default=0, help="disable the adaptive selector, use this s")
+    ap.add_argument("--kv-block-size", type=int, default=0,
+                    help="> 0: the verifier's KV cache is paged with this block size (paged.PagedKVCache)")
     ap.add_argument("--parallelism", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor-parallel verifier over the ranks (default, SURVEY §8e) or one full "
                          "replica per GPU serving its own batch")
@@ -268,7 +270,7 @@ def run_ours(args, rank, ws):
     drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
     eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
                      use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined,
-                     adaptive=not args.fixed_s, sync_time=sync)
+                     adaptive=not args.fixed_s, sync_time=sync, kv_block_size=args.kv_block_size)
     if tp:  # every rank serves the same global batch
         reqs = make_requests(n_req, args.prompt_len, args.new_tokens, tcfg.vocab)
     else:
@@ -361,6 +363,7 @@ def run_ours(args, rank, ws):
                    "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
                           "streamed per verify)"),
                    "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
+                   "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous",
                    "graphs": not args.no_graphs},
         "mean_accepted_length": round(float(np.mean(acc)), 4) if acc else 0.0,
         "mean_emitted_per_round": round(float(np.mean(emt)), 4) if emt else 0.0,

@@ -266,6 +266,25 @@ int ms_accept_stochastic(const int32_t* draft, const double* q, const double* o,
                          int32_t* emitted, int32_t* n_emit, int32_t* finished,
                          int32_t* n_draws, void* stream);
 
+/* ---- paged KV cache ------------------------------------------
+ * K/V live in block pools [n_blocks, Hkv, block_size, D] bf16; block_table
+ * [slots, max_blocks] int32 maps position t of a slot to pool block
+ * table[slot][t / block_size], row t % block_size (T <= max_blocks *
+ * block_size).  Same arithmetic as the contiguous entry points (bitwise):
+ * only K/V row addresses change.  A host block manager
+ * (paper_2402_15678_b200/paged.py) grows a sequence's blocks before a round
+ * and frees the blocks past the accepted length after it — the KV of
+ * rejected speculative tokens. */
+int ms_attention_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                       const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                       void* v_cache, const void* rope, float scale, int append, void* out,
+                       int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                       const int32_t* block_table, int max_blocks, int block_size, void* stream);
+int ms_kv_append_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                       const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                       void* v_cache, const void* rope, const int32_t* block_table, int max_blocks,
+                       int block_size, void* stream);
+
 /* ---- grouped drafters -------------------------------------------------------
  * The K drafters of a round (same architecture, own weights) run as ONE
  * launch per op: G row groups, group k = drafter k, each with its own weights

@@ -93,7 +93,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
                  const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                  __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                  int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
-                 int64_t ldo, int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters) {
+                 int64_t ldo, int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters, KVPage pg) {
   using S = AttnSmem<D, NBUF>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;  // 16-dim chunks (MMA k-steps for Q.K^T)
@@ -115,9 +115,8 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int q0 = qc * 16;                  // first flattened row of this chunk
   const int Q = min(16, rows_tot - q0);    // rows in this chunk
   const int pstart = start[b];
-  const int64_t cbase = ((int64_t)slot[b] * Hkv + h) * T * D;
-  __nv_bfloat16* K = kc + cbase;
-  __nv_bfloat16* V = vc + cbase;
+  const int kv_slot = slot[b];
+  auto krow = [&](int t) -> int64_t { return kv_row(pg, kv_slot, Hkv, h, T, t) * D; };  // element offset
   const int QD = Hq * D, KVD = Hkv * D;
   constexpr int V8 = D / 8;
 
@@ -140,7 +139,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
         rope8(fv, pf, rope + (int64_t)p * (D / 2), c * 8, D / 2);
         val = pack8(fv);
       }
-      *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
+      *reinterpret_cast<bf16x8*>((kv ? vc : kc) + krow(p) + c * 8) = val;
     }
   }
 
@@ -221,9 +220,9 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
           rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
           *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
         } else {
-          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
         }
-        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : V + (int64_t)t * D + lc * 8);
+        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
       } else {  // masked keys must be finite
         *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
@@ -458,7 +457,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
                       const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                       int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
-                      int64_t ldo) {
+                      int64_t ldo, KVPage pg) {
   using S = AttnSmem<D, NBUF>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;
@@ -480,9 +479,8 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int q0 = c0 + warp * 16;              // first row of this warp
   const int Q = max(0, min(16, rows_tot - q0));  // rows of this warp (0: idle)
   const int pstart = start[b];
-  const int64_t cbase = ((int64_t)slot[b] * Hkv + h) * T * D;
-  __nv_bfloat16* K = kc + cbase;
-  __nv_bfloat16* V = vc + cbase;
+  const int kv_slot = slot[b];
+  auto krow = [&](int t) -> int64_t { return kv_row(pg, kv_slot, Hkv, h, T, t) * D; };  // element offset
   const int QD = Hq * D, KVD = Hkv * D;
 
   if (fuse_append && blockIdx.z == 0) {
@@ -502,7 +500,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
         rope8(fv, pf, rope + (int64_t)p * (D / 2), c * 8, D / 2);
         val = pack8(fv);
       }
-      *reinterpret_cast<bf16x8*>((kv ? V : K) + (int64_t)p * D + c * 8) = val;
+      *reinterpret_cast<bf16x8*>((kv ? vc : kc) + krow(p) + c * 8) = val;
     }
   }
 
@@ -569,9 +567,9 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
           rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
           *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
         } else {
-          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : K + (int64_t)t * D + lc * 8);
+          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
         }
-        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : V + (int64_t)t * D + lc * 8);
+        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
       } else {
         *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
@@ -710,7 +708,7 @@ template <int D>
 static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, const int32_t* slot,
                        const int32_t* start, int T, void* kc, void* vc, const float2* rope, float scale,
                        int fuse, void* out, int64_t ldo, float* ws, int64_t ws_bytes, int* counters,
-                       int n_counters, cudaStream_t st) {
+                       int n_counters, cudaStream_t st, KVPage pg) {
   // ring depth 2: deeper rings (3-4) measured slower — the extra shared
   // memory costs more resident CTAs than the hidden tile latency gains
   // (Llama-160M B=48 decode attention 13.8 -> 16 us, 70B verify 2.0 -> 3.0 ms)
@@ -732,7 +730,7 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
     dim3 grid(B, Hkv, (Q * (H / Hkv) + 63) / 64);
     return launch(attention_rows_kernel<D, NBR>, grid, dim3(kAThreads), SR::BYTES, st, 1,
                   (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
-                  (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo);
+                  (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, pg);
   }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
@@ -746,7 +744,7 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   return launch(attention_kernel<D, NB>, grid, dim3(kAThreads), S::BYTES, st, 1,
                 (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
                 (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, n_kv, kct, ws,
-                counters);
+                counters, pg);
 }
 
 int preload_attention() {
@@ -756,9 +754,10 @@ int preload_attention() {
 
 }  // namespace ms
 
-extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
-                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                                void* v_cache, const void* rope, void* stream);
+extern "C" int ms_kv_append_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                  const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                  void* v_cache, const void* rope, const int32_t* block_table, int max_blocks,
+                                  int block_size, void* stream);
 
 extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes,
                                       int* n_counters) {
@@ -769,34 +768,45 @@ extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t
   return MS_OK;
 }
 
-extern "C" int ms_attention_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
-                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                                void* v_cache, const void* rope, float scale, int append, void* out,
-                                int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
-                                void* stream) {
+extern "C" int ms_attention_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                  const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                  void* v_cache, const void* rope, float scale, int append, void* out,
+                                  int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                                  const int32_t* block_table, int max_blocks, int block_size, void* stream) {
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || T < 1) return MS_ERR_VALUE;
   if (H % Hkv) return MS_ERR_VALUE;
+  if (block_table && (block_size < 1 || max_blocks < 1 || T > max_blocks * block_size)) return MS_ERR_VALUE;
   if (B == 0) return MS_OK;
   if (!qkv || !slot || !start || !k_cache || !v_cache || !out) return MS_ERR_VALUE;
   if (ldq % 8) return MS_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
+  const ms::KVPage pg{block_table, max_blocks, block_size};
   int fuse = 0;
   if (append) {
     if (Q <= 16) {
       fuse = 1;  // appended inside the kernel by the first query chunk's CTA
     } else {
-      const int s = ms_kv_append_gqa(qkv, ldq, B, Q, H, Hkv, D, slot, start, T, k_cache, v_cache, rope,
-                                     stream);
+      const int s = ms_kv_append_paged(qkv, ldq, B, Q, H, Hkv, D, slot, start, T, k_cache, v_cache, rope,
+                                       block_table, max_blocks, block_size, stream);
       if (s != MS_OK) return s;
     }
   }
   if (D == 64)
     return ms::launch_attn<64>(qkv, ldq, B, Q, H, Hkv, slot, start, T, k_cache, v_cache, (const float2*)rope,
-                               scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st);
+                               scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st, pg);
   if (D == 128)
     return ms::launch_attn<128>(qkv, ldq, B, Q, H, Hkv, slot, start, T, k_cache, v_cache, (const float2*)rope,
-                                scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st);
+                                scale, fuse, out, ldo, (float*)ws, ws_bytes, counters, n_counters, st, pg);
   return MS_ERR_UNSUPPORTED;
+}
+
+extern "C" int ms_attention_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                void* v_cache, const void* rope, float scale, int append, void* out,
+                                int64_t ldo, void* ws, int64_t ws_bytes, int* counters, int n_counters,
+                                void* stream) {
+  return ms_attention_paged(qkv, ldq, B, Q, H, Hkv, D, slot, start, T, k_cache, v_cache, rope, scale, append, out,
+                            ldo, ws, ws_bytes, counters, n_counters, nullptr, 0, 0, stream);
 }
 
 extern "C" int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,

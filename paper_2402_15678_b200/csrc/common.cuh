@@ -115,6 +115,22 @@ __device__ __forceinline__ void rope8(float* f, const float* pf, const float2* _
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
 
+// KV-cache addressing.  Contiguous: caches [slots, Hkv, T, D].  Paged (table
+// != null): a block pool [n_blocks, Hkv, bs, D] and a block table [slots,
+// max_blocks] of pool indices, position t of a slot living in block
+// table[slot][t / bs], row t % bs.  Returns the ROW index (times D = element).
+struct KVPage {
+  const int32_t* table;
+  int max_blocks;
+  int bs;
+};
+
+__device__ __forceinline__ int64_t kv_row(const KVPage& pg, int slot, int Hkv, int h, int T, int t) {
+  if (!pg.table) return ((int64_t)slot * Hkv + h) * T + t;
+  const int blk = pg.table[(int64_t)slot * pg.max_blocks + t / pg.bs];
+  return ((int64_t)blk * Hkv + h) * pg.bs + (t % pg.bs);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

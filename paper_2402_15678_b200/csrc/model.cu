@@ -130,7 +130,7 @@ layernorm_kernel(const __nv_bfloat16* __restrict__ x, int64_t ldx, const int32_t
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Q, int H, int Hkv,
                                  int D, const int32_t* __restrict__ slot, const int32_t* __restrict__ start,
                                  int T, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
-                                 const float2* __restrict__ rope) {
+                                 const float2* __restrict__ rope, KVPage pg) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
@@ -139,7 +139,7 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
   if (p < 0 || p >= T) return;
   const int hd8 = Hkv * D / 8;
   const bf16x8* src = reinterpret_cast<const bf16x8*>(qkv + (int64_t)r * ldq + (int64_t)H * D);  // skip Q
-  const int64_t sb = (int64_t)slot[b] * Hkv;
+  const int sl = slot[b];
   const int v8 = D / 8;
   for (int e = threadIdx.x; e < 2 * hd8; e += blockDim.x) {
     const int kv = e >= hd8;
@@ -155,7 +155,7 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
       rope8(fv, pf, rope + (int64_t)p * (D / 2), dd, D / 2);
       val = pack8(fv);
     }
-    __nv_bfloat16* dst = (kv ? vc : kc) + ((sb + h) * T + p) * D + dd;
+    __nv_bfloat16* dst = (kv ? vc : kc) + kv_row(pg, sl, Hkv, h, T, p) * D + dd;
     *reinterpret_cast<bf16x8*>(dst) = val;
   }
 }
@@ -236,17 +236,27 @@ extern "C" int ms_rmsnorm_grouped(const void* x, int64_t ldx, const int32_t* row
   return norm_launch<true>(x, ldx, rows, gamma, nullptr, eps, R, d, out, ldo, stream, rpg, gstride);
 }
 
-extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
-                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
-                                void* v_cache, const void* rope, void* stream) {
+extern "C" int ms_kv_append_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                  const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                  void* v_cache, const void* rope, const int32_t* block_table, int max_blocks,
+                                  int block_size, void* stream) {
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || D < 8 || T < 1) return MS_ERR_VALUE;
   if (H % Hkv) return MS_ERR_VALUE;
+  if (block_table && (block_size < 1 || max_blocks < 1 || T > max_blocks * block_size)) return MS_ERR_VALUE;
   if (D % 8 || ldq % 8 || (rope && D % 16)) return MS_ERR_UNSUPPORTED;
   if (B == 0) return MS_OK;
   if (!qkv || !slot || !start || !k_cache || !v_cache) return MS_ERR_VALUE;
+  const ms::KVPage pg{block_table, max_blocks, block_size};
   return ms::launch(ms::kv_append_kernel, dim3(B * Q), dim3(128), 0, (cudaStream_t)stream, 1,
                     (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, D, slot, start, T, (__nv_bfloat16*)k_cache,
-                    (__nv_bfloat16*)v_cache, (const float2*)rope);
+                    (__nv_bfloat16*)v_cache, (const float2*)rope, pg);
+}
+
+extern "C" int ms_kv_append_gqa(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                                const int32_t* slot, const int32_t* start, int T, void* k_cache,
+                                void* v_cache, const void* rope, void* stream) {
+  return ms_kv_append_paged(qkv, ldq, B, Q, H, Hkv, D, slot, start, T, k_cache, v_cache, rope, nullptr, 0, 0,
+                            stream);
 }
 
 extern "C" int ms_kv_append(const void* qkv, int64_t ldq, int B, int Q, int H, int D,

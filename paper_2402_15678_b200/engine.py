@@ -209,12 +209,17 @@ class SpecEngine:
     def __init__(self, target, drafters: list, cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
-                 record: bool = False, pipelined: bool = False, sync_time=None):
+                 record: bool = False, pipelined: bool = False, sync_time=None,
+                 kv_block_size: int = 0, kv_blocks: int | None = None):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
         selector's verify time identical on every rank (tensor parallel: every
-        rank must take the same decisions); None = local time."""
+        rank must take the same decisions); None = local time.
+        kv_block_size > 0: the verifier's KV cache is paged (paged.PagedKVCache,
+        kv_blocks pool blocks; default = slots x max_len worth): blocks are
+        grown before each round and the blocks past the accepted length —
+        the KV of rejected speculative tokens — are freed after it."""
         validate_config(cfg)
         if len(cfg.initial_weights) != len(drafters):
             raise ValueError("initial_weights must have one entry per drafter")
@@ -252,7 +257,12 @@ class SpecEngine:
             self.ssm_g = GroupedLlamaModel(drafters, max_rows=slots * max_len, device=device)
             self.s_cache_g = KVCache(drafters[0].cfg, self.K * slots, max_len, device)
             self.fid_arr = None
-        self.t_cache = KVCache(self.target.cfg, slots, max_len, device)
+        if kv_block_size > 0:
+            from .paged import PagedKVCache
+            self.t_cache = PagedKVCache(self.target.cfg, slots, max_len, kv_block_size, kv_blocks, device)
+        else:
+            self.t_cache = KVCache(self.target.cfg, slots, max_len, device)
+        self.paged = kv_block_size > 0
         self.s_caches = [] if self.grouped else [KVCache(w.cfg, slots, max_len, device) for w in drafters]
         ng = 2 if pipelined else 1
         gb = slots // ng
@@ -298,6 +308,13 @@ class SpecEngine:
             g.req_key.copy_(torch.from_numpy(keys))
             g.pending = None
         P = max(len(c) for c in ctx) - 1
+        if self.paged:  # a fresh batch: every slot's blocks back to the pool, prompts' blocks in
+            mgr = self.t_cache.mgr
+            for b in range(self.B):
+                mgr.release(b)
+            for b in range(self.B):  # padding slots too: the prefill forward writes P rows for every slot
+                mgr.ensure(b, max(P, 1))
+            self.h2d_bytes += self.t_cache.upload()
         if P > 0:
             toks = np.zeros((self.B, P), np.int32)
             for b, c in enumerate(ctx):
@@ -480,6 +497,10 @@ class SpecEngine:
         if not self.use_graphs:
             return
         s_values = s_values or range(self.cfg.s_min, self.cfg.s_max + 1)
+        if self.paged:  # the dummy rounds write up to position ~3 (s_max + 1) of every slot
+            for b in range(self.B):
+                self.t_cache.mgr.ensure(b, min(self.t_cache.max_len, 3 * (self.cfg.s_max + 2)))
+            self.t_cache.upload()
         for g in self.groups:
             for s in s_values:
                 # every catch-up width a round at this s can need: s+1, or up to
@@ -558,6 +579,10 @@ class SpecEngine:
         with torch.cuda.stream(self.draft_stream):
             g.meta.copy_(g.meta_h, non_blocking=True)
         self.h2d_bytes += g.meta_h.numel() * 4
+        if self.paged:  # the verify writes positions len(ctx)-1 .. len(ctx)-1+s
+            for b in act:
+                self.t_cache.mgr.ensure(g.slot0 + b, len(g.ctx[b]) + s)
+            self.h2d_bytes += self.t_cache.upload(slice(g.slot0, g.slot0 + B), stream=self.draft_stream)
         return qc
 
     def _start_draft(self, g: _Group) -> bool:
@@ -622,6 +647,11 @@ class SpecEngine:
                 r.finish_time = ts[3] if ts[3] is not None else time.perf_counter()  # device ms
             else:
                 r.advance(RequestState.RUNNING)
+            if self.paged:  # free blocks holding only rejected tokens' KV (or all, when finished)
+                if r.state == RequestState.FINISHED:
+                    self.t_cache.mgr.release(g.slot0 + b)
+                else:
+                    self.t_cache.mgr.truncate(g.slot0 + b, len(g.ctx[b]))
             # SSM rollback: valid up to the longest prefix agreement with `use`
             for k in range(self.K):
                 mlen = 0
@@ -722,6 +752,12 @@ class SpecEngine:
         zero = torch.zeros(B, dtype=I32, device=self.dev)
         empty = torch.zeros(0, dtype=I32, device=self.dev)
         dummy = torch.empty(0, self.Vt, device=self.dev)
+        if self.paged:
+            for b in range(B):
+                cache.mgr.release(b)
+            for b in range(B):
+                cache.mgr.ensure(b, (len(ctx[b]) if b < len(ctx) else 1) + n_new + 1)
+            cache.upload()
         if P > 0:
             self.target.forward(torch.from_numpy(toks).to(self.dev), zero, self.slot, cache, dummy,
                                 head_rows=empty)

@@ -208,25 +208,30 @@ class AttnWorkspace:
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
               out: torch.Tensor | None = None, append: bool = True, ws: AttnWorkspace | None = None,
-              stream=None, n_kv_heads: int | None = None, rope: torch.Tensor | None = None) -> torch.Tensor:
+              stream=None, n_kv_heads: int | None = None, rope: torch.Tensor | None = None,
+              page=None) -> torch.Tensor:
     """Causal KV-cache attention of Q rows per request (K/V append fused when
     append; split-KV over fixed 128-key chunks when a workspace is given).
     n_kv_heads < H: grouped-query attention (qkv = [q H*D | k Hkv*D | v Hkv*D],
     caches [slots, Hkv, T, D]); rope: the fp32 (cos, sin) table of rope_table."""
-    T = k_cache.shape[2]
+    # page: (block_table [slots, max_blocks] int32, block_size) of a paged cache
+    # (k_cache / v_cache are then block pools [n_blocks, Hkv, bs, D])
+    T = k_cache.shape[2] if page is None else page[0].shape[1] * page[1]
     Hkv = H if n_kv_heads is None else n_kv_heads
     if k_cache.shape[1] != Hkv:
         raise ValueError("cache heads != n_kv_heads")
     if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < T or rope.shape[1] * 2 != D):
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
-    _native.call("ms_attention_gqa", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
+    _native.call("ms_attention_paged", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
                  _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16),
                  None if rope is None else rope.data_ptr(), scale, int(append),
                  out.data_ptr(), out.stride(0),
                  None if ws is None else ws.ws.data_ptr(), 0 if ws is None else ws.ws.numel() * 4,
                  None if ws is None else ws.counters.data_ptr(), 0 if ws is None else ws.counters.numel(),
+                 None if page is None else _dev.ptr(page[0], torch.int32, "block_table"),
+                 0 if page is None else page[0].shape[1], 0 if page is None else page[1],
                  _dev.stream_ptr(stream))
     return out
 

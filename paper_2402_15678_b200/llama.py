@@ -236,7 +236,8 @@ class LlamaModel:
             K.rmsnorm(x, w[p + "attn_norm"], c.eps, out=h, stream=stream)
             lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
-                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
+                        page=getattr(cache, "page", None))
             lin(at, p + "w_o", residual=x, out=x)
             K.rmsnorm(x, w[p + "mlp_norm"], c.eps, out=h, stream=stream)
             lin(h, p + "w_gu", act=2, out=ff)
@@ -263,7 +264,8 @@ class LlamaModel:
             else:
                 K.linear_rms(x, w[p + "w_qkv"], out=qkv, rms_in=rb, eps=c.eps, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
-                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
+                        page=getattr(cache, "page", None))
             K.linear_rms(at, w[p + "w_o"], residual=x, out=x, rms_out=ra, stream=stream)
             K.linear_rms(x, w[p + "w_gu"], act=2, out=ff, rms_in=ra, eps=c.eps, stream=stream)
             K.linear_rms(ff, w[p + "w_down"], residual=x, out=x, rms_out=rb, stream=stream)
@@ -358,7 +360,8 @@ class GroupedLlamaModel:
             K.rmsnorm_grouped(x, t[p + "attn_norm"], M, c.eps, out=h, stream=stream)
             lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, GB, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
-                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
+                        page=getattr(cache, "page", None))
             lin(at, p + "w_o", residual=x, out=x)
             K.rmsnorm_grouped(x, t[p + "mlp_norm"], M, c.eps, out=h, stream=stream)
             lin(h, p + "w_gu", act=2, out=ff)

@@ -249,7 +249,8 @@ class LlamaTPModel(LlamaModel):
             p = f"l{i}."
             K.linear(h, w[p + "w_qkv"], out=qkv, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
-                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope)
+                        out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
+                        page=getattr(cache, "page", None))
             K.linear(at, w[p + "w_o"], residual=x if r0 else None, out=P, out_f32=True, stream=stream)
             cm.allreduce_norm(R, w[p + "mlp_norm"], c.eps, h, stream)
             K.linear(h, w[p + "w_gu"], act=2, out=ff, stream=stream)

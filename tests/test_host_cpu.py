@@ -196,3 +196,18 @@ def test_trace_and_metrics_match_reference_golden(golden_dir):
         assert getattr(m, k) == v, k
     assert {str(k): v for k, v in m.per_ssm_acceptance.items()} == g["per_ssm_acceptance"]
     assert [list(x) for x in m.s_trajectory] == g["s_trajectory"]
+
+
+def test_block_manager_rollback_and_exhaustion():
+    import pytest
+    from paper_2402_15678_b200.paged import BlockManager, KVPoolExhausted
+    m = BlockManager(n_blocks=6, slots=2, max_blocks=4, block_size=8)
+    m.ensure(0, 17)                    # 3 blocks
+    m.ensure(1, 8)                     # 1 block
+    assert m.used() == 4 and int(m.table[0, 2]) != m.scratch
+    assert m.truncate(0, 9) == 1       # positions >= 16 rejected: block 2 freed
+    assert int(m.table[0, 2]) == m.scratch and m.used() == 3
+    m.ensure(1, 32)                    # 3 more -> 6 used
+    with pytest.raises(KVPoolExhausted):
+        m.ensure(0, 25)
+    assert m.release(1) == 4 and m.used() == 2
