@@ -216,6 +216,9 @@ int ms_attention(const void* qkv, int64_t ldq, int B, int Q, int H, int D,
  * (more CTAs in flight on the KV stream); the last chunk of a (request, head)
  * merges the chunk partials in chunk order.  ws / counters sizes: */
 int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes, int* n_counters);
+/* Split-KV scratch for grouped-query attention (Hkv < H: the row-split kernel's records). */
+int ms_attention_workspace_gqa(int B, int Q, int H, int Hkv, int D, int T, int64_t* ws_bytes,
+                               int* n_counters);
 /* Grouped-query attention with optional RoPE (Llama-2: H = 64 query heads over
  * Hkv = 8 KV heads): layouts as in ms_kv_append_gqa; query head h reads KV head
  * h / (H / Hkv).  One CTA per (request, KV head, 16 flattened (position, head)

@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t rope_pair_hi(uint32_t x, uint32_t y, float2 
   return pack_bf16(a.x * c0.x + p.x * c0.y, a.y * c1.x + p.y * c1.y);
 }
 
-template <int D, int NBUF>
+template <int D, int NBUF, bool PAGED>
 __global__ void __launch_bounds__(kAThreads)
 attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                  const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
@@ -116,7 +116,17 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int Q = min(16, rows_tot - q0);    // rows in this chunk
   const int pstart = start[b];
   const int kv_slot = slot[b];
-  auto krow = [&](int t) -> int64_t { return kv_row(pg, kv_slot, Hkv, h, T, t) * D; };  // element offset
+  // K/V row t's element offset: contiguous [slots, Hkv, T, D], or through the
+  // block table (PAGED, a separate instantiation so the contiguous path keeps
+  // its single multiply-add)
+  const int64_t cbase = ((int64_t)kv_slot * Hkv + h) * T * D;
+  auto krow = [&](int t) -> int64_t {
+    if constexpr (PAGED) {
+      return kv_row(pg, kv_slot, Hkv, h, T, t) * D;
+    } else {
+      return cbase + (int64_t)t * D;
+    }
+  };
   const int QD = Hq * D, KVD = Hkv * D;
   constexpr int V8 = D / 8;
 
@@ -451,7 +461,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
 // arithmetic is the same in a Q=1 decode and a Q=s+1 verify (batch
 // invariance: extra fully-masked keys contribute exactly zero).
 // ---------------------------------------------------------------------------
-template <int D, int NBUF>
+template <int D, int NBUF, bool PAGED>
 __global__ void __launch_bounds__(kAThreads)
 attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                       const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
@@ -480,7 +490,17 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int Q = max(0, min(16, rows_tot - q0));  // rows of this warp (0: idle)
   const int pstart = start[b];
   const int kv_slot = slot[b];
-  auto krow = [&](int t) -> int64_t { return kv_row(pg, kv_slot, Hkv, h, T, t) * D; };  // element offset
+  // K/V row t's element offset: contiguous [slots, Hkv, T, D], or through the
+  // block table (PAGED, a separate instantiation so the contiguous path keeps
+  // its single multiply-add)
+  const int64_t cbase = ((int64_t)kv_slot * Hkv + h) * T * D;
+  auto krow = [&](int t) -> int64_t {
+    if constexpr (PAGED) {
+      return kv_row(pg, kv_slot, Hkv, h, T, t) * D;
+    } else {
+      return cbase + (int64_t)t * D;
+    }
+  };
   const int QD = Hq * D, KVD = Hkv * D;
 
   if (fuse_append && blockIdx.z == 0) {
@@ -718,19 +738,24 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   using SR = AttnSmem<D, NBR>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attention_kernel<D, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(attention_kernel<D, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              S::BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(attention_rows_kernel<D, NBR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(attention_kernel<D, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             S::BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(attention_rows_kernel<D, NBR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SR::BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(attention_rows_kernel<D, NBR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SR::BYTES) != cudaSuccess)
       return MS_ERR_CUDA;
     attr = true;
   }
+  const bool paged = pg.table != nullptr;
   const float scale_log2 = scale * 1.4426950408889634f;
   if (Hkv < H) {  // grouped-query: row-split schedule (chosen by G, never by Q)
     dim3 grid(B, Hkv, (Q * (H / Hkv) + 63) / 64);
-    return launch(attention_rows_kernel<D, NBR>, grid, dim3(kAThreads), SR::BYTES, st, 1,
-                  (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
-                  (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, pg);
+    return launch(paged ? attention_rows_kernel<D, NBR, true> : attention_rows_kernel<D, NBR, false>, grid,
+                  dim3(kAThreads), SR::BYTES, st, 1, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
+                  (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, pg);
   }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
@@ -741,15 +766,19 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
     if (ws_bytes < need || n_counters < B * Hkv * nqc) return MS_ERR_VALUE;
   }
   dim3 grid(B, Hkv, nqc * n_kv);
-  return launch(attention_kernel<D, NB>, grid, dim3(kAThreads), S::BYTES, st, 1,
-                (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
+  return launch(paged ? attention_kernel<D, NB, true> : attention_kernel<D, NB, false>, grid, dim3(kAThreads),
+                S::BYTES, st, 1, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T, (__nv_bfloat16*)kc,
                 (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, n_kv, kct, ws,
                 counters, pg);
 }
 
 int preload_attention() {
-  return preload_fn(attention_kernel<64, 2>) + preload_fn(attention_kernel<128, 2>) +
-         preload_fn(attention_rows_kernel<64, 2>) + preload_fn(attention_rows_kernel<128, 2>);
+  int n = 0;
+  n += preload_fn(attention_kernel<64, 2, false>) + preload_fn(attention_kernel<128, 2, false>);
+  n += preload_fn(attention_kernel<64, 2, true>) + preload_fn(attention_kernel<128, 2, true>);
+  n += preload_fn(attention_rows_kernel<64, 2, false>) + preload_fn(attention_rows_kernel<128, 2, false>);
+  n += preload_fn(attention_rows_kernel<64, 2, true>) + preload_fn(attention_rows_kernel<128, 2, true>);
+  return n;
 }
 
 }  // namespace ms
@@ -759,13 +788,22 @@ extern "C" int ms_kv_append_paged(const void* qkv, int64_t ldq, int B, int Q, in
                                   void* v_cache, const void* rope, const int32_t* block_table, int max_blocks,
                                   int block_size, void* stream);
 
+extern "C" int ms_attention_workspace_gqa(int B, int Q, int H, int Hkv, int D, int T, int64_t* ws_bytes,
+                                          int* n_counters) {
+  // split-KV scratch of the MHA kernel (the GQA row-split kernel has no
+  // split-KV path: measured 4x slower at decode contexts — the per-chunk
+  // records of 64 rows x D and the serial last-CTA merge outweigh the extra CTAs)
+  if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || H % Hkv || T < 1) return MS_ERR_VALUE;
+  const int nqc = (Q * (H / Hkv) + 15) / 16;
+  const int n_kv = ((T + ms::kKT - 1) / ms::kKT + ms::kKvChunkTiles - 1) / ms::kKvChunkTiles;
+  if (ws_bytes) *ws_bytes = (int64_t)B * Hkv * nqc * n_kv * 16 * (D + 2) * 4;
+  if (n_counters) *n_counters = B * Hkv * nqc;
+  return MS_OK;
+}
+
 extern "C" int ms_attention_workspace(int B, int Q, int H, int D, int T, int64_t* ws_bytes,
                                       int* n_counters) {
-  const int nqc = (Q + 15) / 16;
-  const int n_kv = ((T + ms::kKT - 1) / ms::kKT + ms::kKvChunkTiles - 1) / ms::kKvChunkTiles;
-  if (ws_bytes) *ws_bytes = (int64_t)B * H * nqc * n_kv * 16 * (D + 2) * 4;
-  if (n_counters) *n_counters = B * H * nqc;
-  return MS_OK;
+  return ms_attention_workspace_gqa(B, Q, H, H, D, T, ws_bytes, n_counters);
 }
 
 extern "C" int ms_attention_paged(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,

@@ -196,11 +196,12 @@ class AttnWorkspace:
     """Split-KV scratch of ms_attention (chunk partials + per-(request, head)
     counters), sized for a model's (B, Q, H, D, T) envelope."""
 
-    def __init__(self, B: int, Q: int, H: int, D: int, T: int, device):
+    def __init__(self, B: int, Q: int, H: int, D: int, T: int, device, n_kv_heads: int | None = None):
         b = ctypes.c_int64()
         c = ctypes.c_int()
-        _native.check(_native.lib.ms_attention_workspace(B, Q, H, D, T, ctypes.byref(b), ctypes.byref(c)),
-                      "ms_attention_workspace")
+        Hkv = H if n_kv_heads is None else n_kv_heads
+        _native.check(_native.lib.ms_attention_workspace_gqa(B, Q, H, Hkv, D, T, ctypes.byref(b), ctypes.byref(c)),
+                      "ms_attention_workspace_gqa")
         self.ws = torch.empty((b.value + 3) // 4, dtype=torch.float32, device=device)
         self.counters = torch.zeros(c.value, dtype=torch.int32, device=device)
 

@@ -206,6 +206,23 @@ class LlamaModel:
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
         self.ws = None
+        # split-KV attention scratch: only the MHA kernel has a split-KV path
+        # (opt-in MS_SPLITKV=1, as for OPT); the GQA row-split kernel walks its
+        # keys in one CTA (a split-KV variant measured 4x slower at decode
+        # contexts)
+        self.split_kv = c.n_kv_heads == c.n_heads and os.environ.get("MS_SPLITKV", "0") == "1"
+        self._aws: dict = {}
+
+    def _attn_ws(self, B: int, Q: int, T: int):
+        """Split-KV scratch per (B, Q, T) call shape (allocated on the first,
+        eager call of a shape — never inside a CUDA-graph capture)."""
+        if not self.split_kv:
+            return None
+        key = (B, Q, T)
+        if key not in self._aws:
+            c = self.cfg
+            self._aws[key] = K.AttnWorkspace(B, Q, c.n_heads, c.head_dim, T, self.device, n_kv_heads=c.n_kv_heads)
+        return self._aws[key]
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
                 logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -237,7 +254,7 @@ class LlamaModel:
             lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
-                        page=getattr(cache, "page", None))
+                        page=getattr(cache, "page", None), ws=self._attn_ws(B, Q, cache.max_len))
             lin(at, p + "w_o", residual=x, out=x)
             K.rmsnorm(x, w[p + "mlp_norm"], c.eps, out=h, stream=stream)
             lin(h, p + "w_gu", act=2, out=ff)
@@ -265,7 +282,7 @@ class LlamaModel:
                 K.linear_rms(x, w[p + "w_qkv"], out=qkv, rms_in=rb, eps=c.eps, stream=stream)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
-                        page=getattr(cache, "page", None))
+                        page=getattr(cache, "page", None), ws=self._attn_ws(B, Q, cache.max_len))
             K.linear_rms(at, w[p + "w_o"], residual=x, out=x, rms_out=ra, stream=stream)
             K.linear_rms(x, w[p + "w_gu"], act=2, out=ff, rms_in=ra, eps=c.eps, stream=stream)
             K.linear_rms(ff, w[p + "w_down"], residual=x, out=x, rms_out=rb, stream=stream)

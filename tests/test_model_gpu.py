@@ -184,27 +184,30 @@ def test_linear_ln_matches_layernorm_then_linear(M, N, K):
         assert torch.equal(got, Kn.linear_ln(x, gam, bet, w, b, 1e-5, act=act, out_f32=True))
 
 
-@pytest.mark.parametrize("D,H,Q", [(128, 8, 5), (64, 12, 1), (64, 4, 13)])
-def test_attention_split_kv_matches_and_is_batch_invariant(D, H, Q):
-    """Split-KV (fixed 128-key chunks, chunk-order merge) agrees with the
-    single-CTA walk and, per query, does not depend on the other queries."""
+@pytest.mark.parametrize("D,H,Hkv,Q", [(128, 8, 8, 5), (64, 12, 12, 1), (64, 4, 4, 13)])
+def test_attention_split_kv_matches_and_is_batch_invariant(D, H, Hkv, Q):
+    """Split-KV (fixed 128-key chunks, chunk-order merge; the MHA kernel)
+    agrees with the single-CTA walk and, per query, does not depend on the
+    other queries."""
     from paper_2402_15678_b200 import kernels as Kn
     B, T = 6, 512
-    g = torch.Generator().manual_seed(D + Q)
-    kc = (torch.randn(B, H, T, D, generator=g)).to(torch.bfloat16).cuda()
-    vc = (torch.randn(B, H, T, D, generator=g)).to(torch.bfloat16).cuda()
+    g = torch.Generator().manual_seed(D + Q + H)
+    kc = (torch.randn(B, Hkv, T, D, generator=g)).to(torch.bfloat16).cuda()
+    vc = (torch.randn(B, Hkv, T, D, generator=g)).to(torch.bfloat16).cuda()
     start = torch.tensor([0, 63, 64, 127, 200, 480], dtype=torch.int32, device="cuda")
     slot = torch.arange(B, dtype=torch.int32, device="cuda")
-    qkv = torch.randn(B * Q, 3 * H * D, generator=g).to(torch.bfloat16).cuda()
-    ws = Kn.AttnWorkspace(B, Q, H, D, T, "cuda")
-    a = Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws)
-    b = Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=None)
+    qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g).to(torch.bfloat16).cuda()
+    kw = dict(n_kv_heads=Hkv)
+    ws = Kn.AttnWorkspace(B, Q, H, D, T, "cuda", n_kv_heads=Hkv)
+    a = Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws, **kw)
+    b = Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=None, **kw)
     torch.testing.assert_close(a.float(), b.float(), rtol=2e-2, atol=2e-2)
-    assert torch.equal(a, Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws))
+    assert torch.equal(a, Kn.attention(qkv, B, Q, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws,
+                                       **kw))
     # the first query row of every request alone (Q=1) == row 0 of the Q-row call
     q1 = qkv.view(B, Q, -1)[:, :1].contiguous().view(B, -1)
-    ws1 = Kn.AttnWorkspace(B, 1, H, D, T, "cuda")
-    a1 = Kn.attention(q1, B, 1, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws1)
+    ws1 = Kn.AttnWorkspace(B, 1, H, D, T, "cuda", n_kv_heads=Hkv)
+    a1 = Kn.attention(q1, B, 1, H, D, slot, start, kc.clone(), vc.clone(), D ** -0.5, ws=ws1, **kw)
     assert torch.equal(a1, a.view(B, Q, -1)[:, 0])
 
 

@@ -25,7 +25,7 @@ for name, B, Q, H, Hkv, D, ctx, rope, skv in cases:
     start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
     out = torch.empty(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
     tab = K.rope_table(T, D, device="cuda") if rope else None
-    ws = K.AttnWorkspace(B, Q, H, D, T, "cuda") if skv else None
+    ws = K.AttnWorkspace(B, Q, H, D, T, "cuda", n_kv_heads=Hkv) if skv else None
     def run():
         K.attention(qkv, B, Q, H, D, slot, start, kc, vc, D ** -0.5, out=out, n_kv_heads=Hkv, rope=tab, ws=ws)
     run(); torch.cuda.synchronize()
