@@ -340,6 +340,18 @@ int ms_tp_signal(int* const* peer_flags, int rank, int t, int* epoch, void* stre
 int ms_tp_reduce_gather(const float* const* parts, int64_t ldp, void* const* xs, int64_t ldx,
                         const int* flags, const int* epoch, int rank, int t, int R, int d,
                         int* err, int early, void* stream);
+/* Fused GEMM -> reduce-scatter: out = x . w^T (+ residual, rank 0), fp32,
+ * written straight into the receive slots of the rank owning each column
+ * slice: recv[f / (N/t)][(rank * rows + m) * (N/t) + f % (N/t)] (recv: device
+ * array of the t ranks' receive buffers) — peer stores issued as each output
+ * tile completes, overlapped with the other tiles' math.  Cluster split-K. */
+int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, const void* residual, int64_t ldr,
+                         int M, int N, int K, float* const* recv, int rank, int t, int rows, void* stream);
+/* After the flags: sum the t local receive slots [t][rows_cap][slice] in rank
+ * order, store the bf16 slice into every rank's residual stream xs[j]. */
+int ms_tp_reduce_recv_gather(const float* recv, int rows_cap, int slice, void* const* xs, int64_t ldx,
+                             const int* flags, const int* epoch, int rank, int t, int R, int* err,
+                             int early, void* stream);
 /* RMSNorm of x [R, ldx] (as ms_rmsnorm) after waiting for flag set `flags`
  * (every rank's slice of x has landed). */
 int ms_rmsnorm_wait(const void* x, int64_t ldx, const void* gamma, float eps, int R, int d,

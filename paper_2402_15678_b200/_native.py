@@ -57,6 +57,8 @@ _SIGS = {
     "ms_free": [_P],
     "ms_tp_signal": [_P, _I, _I, _P, _P],
     "ms_tp_reduce_gather": [_P, _I64, _P, _I64, _P, _P, _I, _I, _I, _I, _P, _I, _P],
+    "ms_linear_tp_scatter": [_P, _I64, _P, _P, _I64, _I, _I, _I, _P, _I, _I, _I, _P],
+    "ms_tp_reduce_recv_gather": [_P, _I, _I, _P, _I64, _P, _P, _I, _I, _I, _P, _I, _P],
     "ms_rmsnorm_wait": [_P, _I64, _P, _F, _I, _I, _P, _I64, _P, _P, _I, _P, _I, _P],
     "ms_tp_argmax_local": [_P, _I64, _I, _I, _I, _P, _P],
     "ms_tp_argmax_combine": [_P, _I, _I, _P, _P, _P, _P, _I, _P],

@@ -54,6 +54,13 @@ struct LinearParams {
   // partials contiguous); the next GEMM runs on the raw residual stream and
   // scales its fp32 accumulator by rstd[row] = rsqrt(sum_t rms_in[row * rms_ld
   // + t] / K + eps).
+  // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
+  // output (row m, feature f) is stored straight into the receive slot of the
+  // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
+  // m) * tp_slice + f % tp_slice] (peer memory over NVLink), tile by tile as
+  // each CTA finishes, overlapping the transfer with other CTAs' mainloops
+  float* const* tp_recv;
+  int tp_rank, tp_slice, tp_rows;
   float* rms_out;
   const float* rms_in;
   int rms_nparts;
@@ -120,6 +127,11 @@ __device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int f
   if (p.bias) v += bf2f(p.bias[(int64_t)grp * p.N + feat]);
   if (p.act == 1) v = fmaxf(v, 0.0f);
   if (p.residual) v += bf2f(p.residual[(int64_t)tok * p.ldr + feat]);
+  if (p.tp_recv) {  // reduce-scatter: fp32 partial into the owning rank's receive slot
+    const int dst = feat / p.tp_slice;
+    p.tp_recv[dst][((int64_t)p.tp_rank * p.tp_rows + tok) * p.tp_slice + (feat - dst * p.tp_slice)] = v;
+    return v;
+  }
   if (p.out_f32) {
     reinterpret_cast<float*>(p.out)[(int64_t)tok * p.ldc + feat] = v;
     return v;
@@ -1198,6 +1210,9 @@ struct RmsArgs {
   int nparts = 0;
   int64_t ld = 0;
   float eps = 0.f;
+  // tensor-parallel reduce-scatter epilogue (see LinearParams)
+  float* const* tp_recv = nullptr;
+  int tp_rank = 0, tp_slice = 1, tp_rows = 0;
 };
 
 static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias,
@@ -1233,6 +1248,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
   p.rms_out = nullptr; p.rms_in = nullptr; p.rms_nparts = 0; p.rms_ld = 0; p.rms_eps = 0.f; p.nc = 1;
+  p.tp_recv = nullptr; p.tp_rank = 0; p.tp_slice = 1; p.tp_rows = 0;
   p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
   if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
     p.ln_g = (const __nv_bfloat16*)g_ln_g;
@@ -1242,7 +1258,8 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   }
   cudaStream_t st = (cudaStream_t)stream;
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
-  const bool folded = rms.out || rms.in;
+  p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
+  const bool folded = rms.out || rms.in || rms.tp_recv;
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
   if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded &&
@@ -1360,4 +1377,20 @@ extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const vo
   r.eps = rms_eps;
   return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
                      nullptr, nullptr, 0.f, stream, 1, r);
+}
+
+extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, const void* residual, int64_t ldr,
+                                    int M, int N, int K, float* const* recv, int rank, int t, int rows,
+                                    void* stream) {
+  // out = x . w^T (+ residual), fp32, scattered to the t ranks' receive slots
+  // by column slice (N / t columns each); cluster split-K path
+  if (!recv || t < 1 || rank < 0 || rank >= t || N % t || (N / t) % 4 || rows < M) return MS_ERR_VALUE;
+  RmsArgs r;
+  r.tp_recv = recv;
+  r.tp_rank = rank;
+  r.tp_slice = N / t;
+  r.tp_rows = rows;
+  // `out` is unused on this path but must be a valid pointer for the checks
+  return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, nullptr, 0,
+                     nullptr, 0, nullptr, nullptr, 0.f, stream, 1, r);
 }

@@ -118,6 +118,40 @@ tp_reduce_gather_kernel(const float* const* __restrict__ parts, int64_t ldp,
   }
 }
 
+// Fused variant: the row-parallel GEMM's epilogue already pushed every
+// rank's fp32 partial of THIS rank's column slice into local receive slots
+// recv[j][row][0..slice) (ms_linear_tp_scatter, peer stores overlapped with
+// the GEMM's other tiles); after the flags, the sum is local reads only, and
+// the bf16 slice is stored into every rank's residual stream (all-gather).
+__global__ void __launch_bounds__(256)
+tp_reduce_recv_kernel(const float* __restrict__ recv, int rows_cap, int slice,
+                      __nv_bfloat16* const* __restrict__ xs, int64_t ldx, const int* flags, const int* epoch,
+                      int rank, int t, int R, int* err, int early) {
+  pdl_wait();
+  if (early) pdl_trigger();
+  wait_flags(flags, epoch, t, err);
+  if (!early) pdl_trigger();
+  const int n4 = slice / 4;
+  const int rows_per = (R + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per, r1 = min(R, r0 + rows_per);
+  const int64_t src_stride = (int64_t)rows_cap * slice;
+  for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < (r1 - r0) * n4; e += blockDim.x * gridDim.y) {
+    const int r = r0 + e / n4;
+    const int c = (e % n4) * 4;
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(recv + (int64_t)r * slice + c));
+    for (int j = 1; j < t; ++j) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(recv + j * src_stride + (int64_t)r * slice + c));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    const int col = rank * slice + c;
+    for (int j = 0; j < t; ++j) *reinterpret_cast<uint2*>(xs[j] + (int64_t)r * ldx + col) = pk;
+  }
+}
+
 // RMSNorm with a leading wait on the second flag set (rows of x complete on
 // every rank), one CTA of 128 threads per row, fp32 statistics.
 __global__ void __launch_bounds__(128)
@@ -207,7 +241,8 @@ __global__ void tp_argmax_combine_kernel(const unsigned long long* const* __rest
 }
 
 int preload_tp() {
-  return preload_fn(tp_signal_kernel) + preload_fn(tp_reduce_gather_kernel) + preload_fn(rmsnorm_wait_kernel) +
+  return preload_fn(tp_signal_kernel) + preload_fn(tp_reduce_gather_kernel) + preload_fn(tp_reduce_recv_kernel) +
+         preload_fn(rmsnorm_wait_kernel) +
          preload_fn(tp_argmax_local_kernel) + preload_fn(tp_argmax_combine_kernel);
 }
 
@@ -289,4 +324,18 @@ extern "C" int ms_tp_argmax_combine(const uint64_t* const* peer, int t, int R, c
   if (R == 0) return MS_OK;
   return ms::launch(ms::tp_argmax_combine_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, 1,
                     (const unsigned long long* const*)peer, t, R, flags, epoch, out, err, early);
+}
+
+extern "C" int ms_tp_reduce_recv_gather(const float* recv, int rows_cap, int slice, void* const* xs_v, int64_t ldx,
+                                        const int* flags, const int* epoch, int rank, int t, int R, int* err,
+                                        int early, void* stream) {
+  auto* const* xs = reinterpret_cast<__nv_bfloat16* const*>(xs_v);
+  if (!recv || !xs || !flags || !epoch || !err || t < 1 || rank < 0 || rank >= t || R < 0 || rows_cap < R)
+    return MS_ERR_VALUE;
+  if (slice % 4 || ldx % 4) return MS_ERR_UNSUPPORTED;
+  if (R == 0) return MS_OK;
+  const int gy = (slice / 4 + 255) / 256;
+  const int gx = R < 32 ? R : 32;
+  return ms::launch(ms::tp_reduce_recv_kernel, dim3(gx, gy), dim3(256), 0, (cudaStream_t)stream, 1, recv, rows_cap,
+                    slice, xs, ldx, flags, epoch, rank, t, R, err, early);
 }

@@ -132,6 +132,28 @@ class TPComm:
                      out.data_ptr(), out.stride(0), self.flags[64:128].data_ptr(), self.epoch[1:2].data_ptr(),
                      self.t, self.err.data_ptr(), self.early, _dev.stream_ptr(stream))
 
+    def linear_scatter(self, x: torch.Tensor, w: torch.Tensor, residual: torch.Tensor | None, stream=None) -> None:
+        """Row-parallel GEMM with the reduce-scatter fused into its epilogue:
+        fp32 partials pushed into the owning ranks' receive slots (the P
+        regions, viewed [t][max_rows][d/t])."""
+        M, Kd = x.shape
+        _native.call("ms_linear_tp_scatter", x.data_ptr(), x.stride(0), w.data_ptr(),
+                     None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
+                     M, self.d, Kd, self.peer_p.data_ptr(), self.rank, self.t, self.max_rows,
+                     _dev.stream_ptr(stream))
+
+    def reduce_recv(self, R: int, stream=None) -> None:
+        _native.call("ms_tp_reduce_recv_gather", self.p.data_ptr(), self.max_rows, self.d // self.t,
+                     self.peer_x.data_ptr(), self.d, self.flags[0:64].data_ptr(), self.epoch[0:1].data_ptr(),
+                     self.rank, self.t, R, self.err.data_ptr(), self.early, _dev.stream_ptr(stream))
+
+    def scatter_allreduce_norm(self, R: int, gamma: torch.Tensor, eps: float, out: torch.Tensor, stream=None) -> None:
+        """After linear_scatter: x[:R] = sum of the received slots, then out = RMSNorm(x) * gamma."""
+        self.signal(0, stream)
+        self.reduce_recv(R, stream)
+        self.signal(1, stream)
+        self.rmsnorm_wait(R, gamma, eps, out, stream)
+
     def allreduce_norm(self, R: int, gamma: torch.Tensor, eps: float, out: torch.Tensor, stream=None) -> None:
         """x[:R] = sum over ranks of P[:R] (rank order), then out = RMSNorm(x) * gamma."""
         self.signal(0, stream)
@@ -232,6 +254,10 @@ class LlamaTPModel(LlamaModel):
         self.tp = comm.t
         self.x = comm.x  # residual stream = symmetric buffer
         self.v0 = comm.rank * shard.cfg.vocab
+        # fused GEMM -> reduce-scatter (peer stores from the O / down epilogues);
+        # MS_TP_FUSED=0: GEMM to a local partial + two-shot pull reduction
+        import os
+        self.fused = os.environ.get("MS_TP_FUSED", "1") != "0"
 
     def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
         """Rank-local vocab slice of the logits ([R', V/t] fp32)."""
@@ -251,11 +277,18 @@ class LlamaTPModel(LlamaModel):
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
                         page=getattr(cache, "page", None))
+            nxt = w[f"l{i + 1}.attn_norm"] if i + 1 < c.n_layers else w["norm_f"]
+            if self.fused:
+                cm.linear_scatter(at, w[p + "w_o"], x if r0 else None, stream)
+                cm.scatter_allreduce_norm(R, w[p + "mlp_norm"], c.eps, h, stream)
+                K.linear(h, w[p + "w_gu"], act=2, out=ff, stream=stream)
+                cm.linear_scatter(ff, w[p + "w_down"], x if r0 else None, stream)
+                cm.scatter_allreduce_norm(R, nxt, c.eps, h, stream)
+                continue
             K.linear(at, w[p + "w_o"], residual=x if r0 else None, out=P, out_f32=True, stream=stream)
             cm.allreduce_norm(R, w[p + "mlp_norm"], c.eps, h, stream)
             K.linear(h, w[p + "w_gu"], act=2, out=ff, stream=stream)
             K.linear(ff, w[p + "w_down"], residual=x if r0 else None, out=P, out_f32=True, stream=stream)
-            nxt = w[f"l{i + 1}.attn_norm"] if i + 1 < c.n_layers else w["norm_f"]
             cm.allreduce_norm(R, nxt, c.eps, h, stream)
         if head_rows is None:
             hf = h

@@ -39,7 +39,7 @@ def _run_ranks(fns):
         raise errs[0]
 
 
-def _setup(t, B=4, T=64, seed=0, name="tiny-llama"):
+def _setup(t, B=4, T=64, seed=0, name="tiny-llama", fused=True):
     from paper_2402_15678_b200.llama import CONFIGS, LlamaModel, LlamaWeights
     from paper_2402_15678_b200.opt import KVCache
     from paper_2402_15678_b200.tp import LlamaTPModel, TPComm, shard_llama
@@ -49,6 +49,8 @@ def _setup(t, B=4, T=64, seed=0, name="tiny-llama"):
     comms = TPComm.local_group(t, B * T, cfg.d)
     shards = [shard_llama(w, r, t).to("cuda") for r in range(t)]
     models = [LlamaTPModel(shards[r], comms[r], max_rows=B * T) for r in range(t)]
+    for m in models:
+        m.fused = fused  # GEMM -> reduce-scatter fused into the epilogue, or the two-shot pull
     caches = [KVCache(shards[r].cfg, B, T) for r in range(t)]
     return cfg, full, KVCache(cfg, B, T), models, caches, comms
 
@@ -70,9 +72,10 @@ def _tp_step(models, caches, toks, start, slot):
 
 # t <= 4: eight ranks' spin-waiting kernels sharing ONE GPU can starve each
 # other of SM resources; with one rank per GPU (the product) that cannot happen.
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("t,name", [(2, "tiny-llama"), (4, "tiny-llama-tp")])
-def test_tp_forward_matches_single_gpu(t, name):
-    cfg, full, fcache, models, caches, _ = _setup(t, name=name)
+def test_tp_forward_matches_single_gpu(t, name, fused):
+    cfg, full, fcache, models, caches, _ = _setup(t, name=name, fused=fused)
     B, T0 = 4, 20
     rng = np.random.default_rng(0)
     toks = torch.tensor(rng.integers(0, cfg.vocab, size=(B, T0 + 5)).astype(np.int32), device="cuda")
