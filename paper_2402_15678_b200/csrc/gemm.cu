@@ -121,6 +121,11 @@ struct LinearCfg {
   }
 };
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 // tok: global output row; feat: feature within the row group grp.  Returns
 // the value as stored (bf16-rounded for bf16 outputs).
 __device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int feat, float v, int grp = 0) {
@@ -157,11 +162,24 @@ __device__ __forceinline__ float4 ld_dsmem_f4(const float* local, int rank) {
   return v;
 }
 
+#ifdef MS_EXP_TIMING  // diagnostic build only: per-CTA globaltimer stamps
+__device__ unsigned long long g_exp_stamps[4096 * 4];
+__device__ __forceinline__ unsigned long long exp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const LinearParams p) {
   using C = LinearCfg<BN>;
+#ifdef MS_EXP_TIMING
+  const int exp_id = blockIdx.x + blockIdx.y * gridDim.x;
+  if (threadIdx.x == 0 && exp_id < 4096) g_exp_stamps[exp_id * 4] = exp_now();
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
@@ -388,6 +406,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
+#ifdef MS_EXP_TIMING
+    if (threadIdx.x == 64 && exp_id < 4096) g_exp_stamps[exp_id * 4 + 1] = exp_now();
+#endif
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 #ifdef MS_EXP_NOEPI  // diagnostic build only: no epilogue (no outputs)
     if (p.splits == 1) goto epi_done;
@@ -514,6 +535,74 @@ epi_done:
         sq = warp_sum(sq);
         if (lane == 0 && n0 < p.N) p.rms_out[(int64_t)(orow + j) * p.rms_ld + tile_n] = sq;
       }
+    } else if (!gated) {
+      // batched for memory-level parallelism: each thread holds up to UB of
+      // its units, issues every partial (DSMEM) and residual load first, then
+      // computes and stores 4-wide — one latency per batch instead of one per
+      // unit (the unbatched loop cost ~12 us on a 176-row O projection, half
+      // of its mainloop)
+      constexpr int UB = 8;
+      const bool vec = (p.N % 4 == 0) && (p.ldc % 4 == 0) && (!p.residual || p.ldr % 4 == 0) && !p.tp_recv &&
+                       ((reinterpret_cast<uintptr_t>(p.out) & (p.out_f32 ? 15 : 7)) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(p.residual) & 7) == 0) && !p.bias;
+      for (int ub = u0 + (int)threadIdx.x; ub < u1; ub += kThreads * UB) {
+        float4 acc[UB];
+        uint2 res[UB];
+#pragma unroll
+        for (int i = 0; i < UB; ++i) {
+          const int u = ub + i * kThreads;
+          if (u < u1) {
+            const int j = u / upr, f4 = (u - j * upr) * 4;
+            acc[i] = ld4(P + j * kBM + f4, 0);
+            if (vec && p.residual && n0 + f4 < p.N)
+              res[i] = *reinterpret_cast<const uint2*>(p.residual + (int64_t)(orow + j) * p.ldr + n0 + f4);
+          }
+        }
+        for (int rk = 1; rk < p.splits; ++rk) {
+#pragma unroll
+          for (int i = 0; i < UB; ++i) {
+            const int u = ub + i * kThreads;
+            if (u < u1) {
+              const int j = u / upr, f4 = (u - j * upr) * 4;
+              const float4 v = ld4(P + j * kBM + f4, rk);
+              acc[i].x += v.x; acc[i].y += v.y; acc[i].z += v.z; acc[i].w += v.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < UB; ++i) {
+          const int u = ub + i * kThreads;
+          if (u >= u1) continue;
+          const int j = u / upr, f4 = (u - j * upr) * 4;
+          const float rs = p.rms_in ? s_rstd[j] : 1.f;
+          float a4[4] = {acc[i].x * rs, acc[i].y * rs, acc[i].z * rs, acc[i].w * rs};
+          const int feat = n0 + f4;
+          if (vec && feat < p.N) {
+            if (p.act == 1) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t) a4[t] = fmaxf(a4[t], 0.f);
+            }
+            if (p.residual) {
+              const __nv_bfloat162* rr = reinterpret_cast<const __nv_bfloat162*>(&res[i]);
+              const float2 r01 = __bfloat1622float2(rr[0]), r23 = __bfloat1622float2(rr[1]);
+              a4[0] += r01.x; a4[1] += r01.y; a4[2] += r23.x; a4[3] += r23.y;
+            }
+            if (p.out_f32) {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) =
+                  make_float4(a4[0], a4[1], a4[2], a4[3]);
+            } else {
+              uint2 pk;
+              pk.x = pack_bf16x2(a4[0], a4[1]);
+              pk.y = pack_bf16x2(a4[2], a4[3]);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) = pk;
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
+          }
+        }
+      }
     } else {
     for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
       const int j = u / upr;
@@ -525,24 +614,17 @@ epi_done:
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
-      if (gated) {
-        float4 up = ld4(P + j * kBM + f4 + kBM / 2, 0);
-        for (int rk = 1; rk < p.splits; ++rk) {
-          const float4 v = ld4(P + j * kBM + f4 + kBM / 2, rk);
-          up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
-        }
-        const float u4[4] = {up.x * rs, up.y * rs, up.z * rs, up.w * rs};
-        const int of = tile_n * (kBM / 2) + f4;  // output feature
-        if (n0 >= p.N) continue;                 // padding tile of an odd multicast pair
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
-        continue;
+      float4 up = ld4(P + j * kBM + f4 + kBM / 2, 0);
+      for (int rk = 1; rk < p.splits; ++rk) {
+        const float4 v = ld4(P + j * kBM + f4 + kBM / 2, rk);
+        up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
       }
-      const int feat = n0 + f4;
+      const float u4[4] = {up.x * rs, up.y * rs, up.z * rs, up.w * rs};
+      const int of = tile_n * (kBM / 2) + f4;  // output feature
+      if (n0 >= p.N) continue;                 // padding tile of an odd multicast pair
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
+      for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
     }
     }
     if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
@@ -550,6 +632,14 @@ epi_done:
   if (p.nc > 1 && p.splits == 1) cluster_sync_all();  // multicast peers done with each other's smem
   tc::fence_before_sync();
   __syncthreads();
+#ifdef MS_EXP_TIMING
+  if (threadIdx.x == 0 && exp_id < 4096) {
+    g_exp_stamps[exp_id * 4 + 2] = exp_now();
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_exp_stamps[exp_id * 4 + 3] = smid;
+  }
+#endif
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc<C::TMEM_COLS>(tmem);
@@ -1394,3 +1484,9 @@ extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, c
   return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, nullptr, 0,
                      nullptr, 0, nullptr, nullptr, 0.f, stream, 1, r);
 }
+
+#ifdef MS_EXP_TIMING
+extern "C" int ms_exp_stamps(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, ms::g_exp_stamps, (size_t)n * 4 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -5;
+}
+#endif
