@@ -54,10 +54,14 @@ METRIC = "output tokens/sec, Llama-2-70B + 3x160M SSMs, 1-8 B200; mean accepted 
 def workload(args) -> str:
     sched = ("pipelined SSM decode / LLM verify (2 groups)" if args.schedule == "pipelined"
              else "sequential draft / verify")
+    k = len(args.fidelity.split(",")) if args.fidelity else 3
     if args.target == "llama-2-70b":
-        return (f"cfg3: Llama-2-70B target + 3x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, "
+        return (f"cfg3: Llama-2-70B target + {k}x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, "
                 f"adaptive s")
-    return (f"{args.target} target + 3x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, adaptive s")
+    if args.preset == "cfg5":
+        return (f"cfg5 on one GPU: Llama-2-13B target + {k}x {args.ssm} SSMs, {args.prompt_len}-token prompts, "
+                f"bf16, verify batch {args.batch}, {sched}, adaptive s (KV-cache-bound verify)")
+    return (f"{args.target} target + {k}x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, adaptive s")
 
 
 def parse():
@@ -71,7 +75,11 @@ def parse():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--prompt-len", type=int, default=128)
     ap.add_argument("--new-tokens", type=int, default=128)
-    ap.add_argument("--fidelity", default="0.9,0.85,0.8")
+    ap.add_argument("--fidelity", default="0.9,0.85,0.8",
+                    help="one per drafter (the drafter count is the number of values)")
+    ap.add_argument("--preset", default="", choices=["", "cfg2", "cfg5"],
+                    help="cfg2: OPT-13B + 3x OPT-125M, sequential; cfg5: Llama-2-13B + 5 drafters, 4K prompts "
+                         "(verify batch 16 x 2 pipelined groups on one GPU: B=64 needs ~218 GB of KV)")
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=1)
@@ -85,7 +93,13 @@ def parse():
                     help="pipelined (cfg3, default): two request groups of --batch each (verify batch "
                          "--batch, 2x requests in flight), verify of one overlapping drafting of the "
                          "other (aggspec/engine.py:494-576); sequential: one group, draft then verify")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.preset == "cfg2":
+        a.target, a.ssm, a.schedule = "opt-13b", "opt-125m", "sequential"
+    elif a.preset == "cfg5":
+        a.target, a.ssm, a.prompt_len = "llama-2-13b", "llama-160m", 4096
+        a.fidelity = "0.9,0.85,0.8,0.75,0.7"
+    return a
 
 
 # --------------------------------------------------------------------------- dist
@@ -231,7 +245,7 @@ def run_ours(args, rank, ws):
 
     tcfg, scfg = config(args.target), config(args.ssm)
     fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else None
-    K = 3
+    K = len(fid) if fid else 3
     cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=args.batch, b_ssm=args.batch,
                        s_init=args.fixed_s or 4, s_min=1, s_max=12, initial_weights=(1.0,) * K, seed=0)
     max_len = args.prompt_len + args.new_tokens + cfg.s_max + 4
@@ -485,7 +499,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "impl": "reference",
-                "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * 3,
+                "config": {"workload": workload(args), "target": args.target,
+                           "ssms": [args.ssm] * (len(args.fidelity.split(",")) if args.fidelity else 3),
                            "global_batch": args.batch * (2 if args.schedule == "pipelined" else 1),
                            "schedule": args.schedule},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},

@@ -720,9 +720,14 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   }
 }
 
-// KV chunk (in 64-key tiles) per CTA for the split-KV schedule: a fixed
-// constant, so the partition never depends on the batch.
-constexpr int kKvChunkTiles = 2;
+// KV chunk (in 64-key tiles) per CTA for the split-KV schedule: a function of
+// the cache length T only (at most 8 chunks, at least 2 tiles each), so the
+// partition never depends on the batch or on Q.
+__host__ __device__ inline int kv_chunk_tiles(int T) {
+  const int tiles = (T + kKT - 1) / kKT;
+  const int c = (tiles + 7) / 8;
+  return c < 2 ? 2 : c;
+}
 
 template <int D>
 static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, const int32_t* slot,
@@ -760,7 +765,7 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
   if (ws) {
-    kct = kKvChunkTiles;
+    kct = kv_chunk_tiles(T);
     n_kv = ((T + kKT - 1) / kKT + kct - 1) / kct;
     const int64_t need = (int64_t)B * Hkv * nqc * n_kv * 16 * (D + 2) * 4;
     if (ws_bytes < need || n_counters < B * Hkv * nqc) return MS_ERR_VALUE;
@@ -795,7 +800,8 @@ extern "C" int ms_attention_workspace_gqa(int B, int Q, int H, int Hkv, int D, i
   // records of 64 rows x D and the serial last-CTA merge outweigh the extra CTAs)
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || H % Hkv || T < 1) return MS_ERR_VALUE;
   const int nqc = (Q * (H / Hkv) + 15) / 16;
-  const int n_kv = ((T + ms::kKT - 1) / ms::kKT + ms::kKvChunkTiles - 1) / ms::kKvChunkTiles;
+  const int kct = ms::kv_chunk_tiles(T);
+  const int n_kv = ((T + ms::kKT - 1) / ms::kKT + kct - 1) / kct;
   if (ws_bytes) *ws_bytes = (int64_t)B * Hkv * nqc * n_kv * 16 * (D + 2) * 4;
   if (n_counters) *n_counters = B * Hkv * nqc;
   return MS_OK;

@@ -206,6 +206,8 @@ class _Group:
 class SpecEngine:
     """Greedy speculative decoding with K voting drafters on one GPU."""
 
+    PREFILL_CHUNK = 1024  # prompt positions per prefill forward
+
     def __init__(self, target, drafters: list, cfg: EngineConfig,
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
@@ -238,7 +240,8 @@ class SpecEngine:
         if hasattr(target, "forward"):
             self.target = target
         else:
-            self.target = make_model(target, max_rows=max(slots * (s_cap + 1), slots * max_len), device=device)
+            rows_t = max(slots * (s_cap + 1), slots * min(max_len, self.PREFILL_CHUNK))
+            self.target = make_model(target, max_rows=rows_t, device=device)
         self.tp = hasattr(self.target, "comm")
         self.Vt = self.target.cfg.vocab                       # width of the target's logits
         V = self.Vt * (self.target.tp if self.tp else 1)      # full vocabulary
@@ -251,10 +254,11 @@ class SpecEngine:
         self.grouped = (len(drafters) > 1 and all(getattr(w.cfg, "family", "") == "llama" for w in drafters)
                         and all(w.cfg == drafters[0].cfg for w in drafters)
                         and os.environ.get("MS_GROUPED_DRAFT", "1") != "0")
-        self.ssms = [] if self.grouped else [make_model(w, max_rows=slots * max_len, device=device, small_gemm=True)
+        rows = slots * min(max_len, max(self.PREFILL_CHUNK, cfg.s_max + 2))
+        self.ssms = [] if self.grouped else [make_model(w, max_rows=rows, device=device, small_gemm=True)
                                              for w in drafters]
         if self.grouped:
-            self.ssm_g = GroupedLlamaModel(drafters, max_rows=slots * max_len, device=device)
+            self.ssm_g = GroupedLlamaModel(drafters, max_rows=rows, device=device)
             self.s_cache_g = KVCache(drafters[0].cfg, self.K * slots, max_len, device)
             self.fid_arr = None
         if kv_block_size > 0:
@@ -321,22 +325,31 @@ class SpecEngine:
                 toks[b, : len(c) - 1] = c[:-1]
             t = torch.from_numpy(toks).to(self.dev)
             self.h2d_bytes += toks.nbytes
-            zero = torch.zeros(self.B, dtype=I32, device=self.dev)
-            empty = torch.zeros(0, dtype=I32, device=self.dev)
-            self.target.forward(t, zero, self.slot, self.t_cache, torch.empty(0, self.Vt, device=self.dev),
-                                head_rows=empty)
-            dummy = torch.empty(0, self.V, device=self.dev)
-            for m, c in zip(self.ssms, self.s_caches):
-                m.forward(t, zero, self.slot, c, dummy, head_rows=empty)
-            if self.grouped:
-                G = self.K
-                self.ssm_g.forward(t.repeat(G, 1), torch.zeros(G * self.B, dtype=I32, device=self.dev),
-                                   torch.arange(G * self.B, dtype=I32, device=self.dev), self.s_cache_g, dummy,
-                                   head_rows=empty)
+            self._prefill_chunks(t)
         for r in requests:
             if r.remaining <= 0 and r.state != RequestState.FINISHED:
                 r.state = RequestState.FINISHED
         torch.cuda.synchronize(self.dev)
+
+    def _prefill_chunks(self, t: torch.Tensor) -> None:
+        """Cache prompt positions 0..P-1 (t [B, P]) in every model, PREFILL_CHUNK
+        positions at a time (chunked prefill — activation buffers
+        and GEMM temporaries are sized for a chunk, not a 4K-token prompt);
+        each chunk's queries attend to the cached earlier chunks."""
+        B, P = t.shape
+        empty = torch.zeros(0, dtype=I32, device=self.dev)
+        tgt_dummy = torch.empty(0, self.Vt, device=self.dev)
+        dummy = torch.empty(0, self.V, device=self.dev)
+        G = self.K
+        gslot = torch.arange(G * B, dtype=I32, device=self.dev)
+        for c0 in range(0, P, self.PREFILL_CHUNK):
+            tc = t[:, c0: c0 + self.PREFILL_CHUNK].contiguous()
+            st = torch.full((B,), c0, dtype=I32, device=self.dev)
+            self.target.forward(tc, st, self.slot, self.t_cache, tgt_dummy, head_rows=empty)
+            for m, c in zip(self.ssms, self.s_caches):
+                m.forward(tc, st, self.slot, c, dummy, head_rows=empty)
+            if self.grouped:
+                self.ssm_g.forward(tc.repeat(G, 1), st.repeat(G), gslot, self.s_cache_g, dummy, head_rows=empty)
 
     def set_teacher(self, teacher: dict) -> None:
         """Target greedy continuations (request id -> tokens after the prompt)
@@ -758,8 +771,10 @@ class SpecEngine:
             for b in range(B):
                 cache.mgr.ensure(b, (len(ctx[b]) if b < len(ctx) else 1) + n_new + 1)
             cache.upload()
-        if P > 0:
-            self.target.forward(torch.from_numpy(toks).to(self.dev), zero, self.slot, cache, dummy,
+        tt = torch.from_numpy(toks).to(self.dev)
+        for c0 in range(0, P, self.PREFILL_CHUNK):
+            self.target.forward(tt[:, c0: c0 + self.PREFILL_CHUNK].contiguous(),
+                                torch.full((B,), c0, dtype=I32, device=self.dev), self.slot, cache, dummy,
                                 head_rows=empty)
         out = {r.id: [] for r in requests}
         lens = np.array([len(c) for c in ctx] + [1] * (B - len(ctx)))

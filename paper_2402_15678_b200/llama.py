@@ -42,7 +42,7 @@ class LlamaConfig:
     n_kv_heads: int
     ffn: int
     vocab: int = 32000
-    max_pos: int = 4096
+    max_pos: int = 8192  # RoPE table length (cfg5: 4K prompts + generation exceed Llama-2's 4096)
     eps: float = 1e-5
     rope_theta: float = 10000.0
     hd: int = 0  # head dim when it is not d / n_heads (a tensor-parallel shard)
@@ -69,7 +69,9 @@ class LlamaConfig:
 CONFIGS = {
     "llama-2-70b": LlamaConfig("llama-2-70b", 80, 8192, 64, 8, 28672),
     "llama-2-13b": LlamaConfig("llama-2-13b", 40, 5120, 40, 40, 13824),
-    "llama-160m": LlamaConfig("llama-160m", 12, 768, 12, 12, 3072, max_pos=2048, eps=1e-6),
+    # max_pos = RoPE table length: 8192 so the drafters cover cfg5's 4K prompts
+    # (the released Llama-160M was trained at 2048; rotary positions extend)
+    "llama-160m": LlamaConfig("llama-160m", 12, 768, 12, 12, 3072, max_pos=8192, eps=1e-6),
     # test-sized Llama shapes (GQA 2:1, D = 64)
     "tiny-llama": LlamaConfig("tiny-llama", 4, 256, 4, 2, 512, max_pos=1024),
     "tiny-llama-ssm": LlamaConfig("tiny-llama-ssm", 1, 256, 4, 4, 512, max_pos=1024),
@@ -206,17 +208,18 @@ class LlamaModel:
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
         self.ws = None
-        # split-KV attention scratch: only the MHA kernel has a split-KV path
-        # (opt-in MS_SPLITKV=1, as for OPT); the GQA row-split kernel walks its
-        # keys in one CTA (a split-KV variant measured 4x slower at decode
-        # contexts)
+        # split-KV attention: opt-in (MS_SPLITKV=1), MHA kernel only.  Measured
+        # slower wherever tried — Llama-2-13B B=64 4K context: 1.24 ms vs 0.89 ms
+        # unsplit (chunk size from the cache length, <= 8 chunks) — and its
+        # per-shape scratch is large at prefill shapes
         self.split_kv = c.n_kv_heads == c.n_heads and os.environ.get("MS_SPLITKV", "0") == "1"
+        self.split_kv_min_len = 0
         self._aws: dict = {}
 
     def _attn_ws(self, B: int, Q: int, T: int):
         """Split-KV scratch per (B, Q, T) call shape (allocated on the first,
         eager call of a shape — never inside a CUDA-graph capture)."""
-        if not self.split_kv:
+        if not self.split_kv or T < self.split_kv_min_len:
             return None
         key = (B, Q, T)
         if key not in self._aws:

@@ -67,3 +67,30 @@ def test_engine_paged_kv_same_tokens_and_frees_rejected(pipelined):
         if bs:
             assert eng.t_cache.mgr.used() == 0  # every request finished: all blocks back in the pool
     assert outs[0] == outs[1]
+
+
+def test_chunked_prefill_same_generation():
+    """Prompt prefill in 8-position chunks (SURVEY §8f chunked prefill) gives
+    exactly the generations of a one-chunk prefill (every forward here stays
+    below the cuBLAS prefill threshold, and the kernels are batch-invariant)."""
+    from paper_2402_15678_b200.core import EngineConfig, Request
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    tcfg, scfg = CONFIGS["tiny-llama"], CONFIGS["tiny-llama-ssm"]
+    target = LlamaWeights.random(tcfg, 3, device="cuda", std=0.05)
+    drafters = [LlamaWeights.random(scfg, k + 5, device="cuda", std=0.05) for k in range(3)]
+    outs = []
+    for chunk in (1024, 8):
+        cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=4, b_ssm=4, s_init=3, initial_weights=(1.0,) * 3)
+        eng = SpecEngine(target, drafters, cfg, slots=4, max_len=128, fidelity=[0.9, 0.6, 0.3], adaptive=False)
+        eng.PREFILL_CHUNK = chunk
+        rng = np.random.default_rng(2)
+        reqs = [Request(f"req-{i:03d}", [int(t) for t in rng.integers(0, tcfg.vocab, size=int(rng.integers(20, 40)))],
+                        24) for i in range(4)]
+        teacher = eng.greedy_teacher([Request(r.id, list(r.prompt), 24) for r in reqs], 24)
+        eng.prefill(reqs)
+        eng.set_teacher(teacher)
+        res = eng.decode()
+        assert res.outputs == teacher
+        outs.append((teacher, res.outputs))
+    assert outs[0] == outs[1]
