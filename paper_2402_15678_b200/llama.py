@@ -208,18 +208,24 @@ class LlamaModel:
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
         self.ws = None
-        # split-KV attention: opt-in (MS_SPLITKV=1), MHA kernel only.  Measured
-        # slower wherever tried — Llama-2-13B B=64 4K context: 1.24 ms vs 0.89 ms
-        # unsplit (chunk size from the cache length, <= 8 chunks) — and its
-        # per-shape scratch is large at prefill shapes
-        self.split_kv = c.n_kv_heads == c.n_heads and os.environ.get("MS_SPLITKV", "0") == "1"
-        self.split_kv_min_len = 0
+        # split-KV attention (MHA kernel only; chunk size from the cache length,
+        # <= 8 chunks): for decode / verify calls (Q <= 16) against caches of
+        # >= 1024 positions — where one CTA per (request, head) would walk ~66
+        # tiles serially with few CTAs in flight (cfg5 at B = 16).  Never for
+        # prefill chunks (large per-shape scratch; the prefill path is shared by
+        # the greedy teacher and the speculative run, so losslessness holds).
+        # MS_SPLITKV=auto enables that rule, =1 forces it for every decode /
+        # verify call.
+        # Opt-in: measured no gain (cfg5 on one GPU: verify 31.7 vs 29.4 ms).
+        env = os.environ.get("MS_SPLITKV", "0")
+        self.split_kv = c.n_kv_heads == c.n_heads and env in ("1", "auto")
+        self.split_kv_min_len = 0 if env == "1" else 1024
         self._aws: dict = {}
 
     def _attn_ws(self, B: int, Q: int, T: int):
         """Split-KV scratch per (B, Q, T) call shape (allocated on the first,
         eager call of a shape — never inside a CUDA-graph capture)."""
-        if not self.split_kv or T < self.split_kv_min_len:
+        if not self.split_kv or T < self.split_kv_min_len or Q > 16:
             return None
         key = (B, Q, T)
         if key not in self._aws:
