@@ -16,7 +16,7 @@ B = int(sys.argv[4]) if len(sys.argv) > 4 else 16
 c = CONFIGS[name]
 w = LlamaWeights.random(c, 0)
 m = LlamaModel(w, max_rows=B * Q)
-cache = KVCache(c, B, 512)
+cache = KVCache(c, B, max(512, ctx + Q + 16))
 tok = torch.randint(0, c.vocab, (B, Q), dtype=torch.int32, device="cuda")
 start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
 slot = torch.arange(B, dtype=torch.int32, device="cuda")
