@@ -203,10 +203,11 @@ def roofline_verify(engine, rounds, peaks):
     c = engine.target.cfg
     P2 = 2 * c.matmul_params()
     kvb = c.kv_bytes_per_token()
+    vb = engine.groups[0].B  # rows of one verify (one group's slots)
     tot_bytes = tot_t = 0.0
     for r in rounds:
         ctx = r.ctx_mean
-        nb = len(r.accepted) if r.accepted else engine.B
+        nb = len(r.accepted) if r.accepted else vb
         b = P2 + nb * ctx * kvb + nb * (r.s + 1) * kvb
         tot_bytes += b
         tot_t += r.t_verify_ms * 1e-3
@@ -221,7 +222,7 @@ def roofline_verify(engine, rounds, peaks):
     try:  # ncu --metrics dram__bytes_{read,write}.sum of one verify forward (profiles/)
         with open(os.path.join(ROOT, "profiles", "r1h_verify_traffic.json")) as fh:
             tr = json.load(fh)
-        if tr["model"] == c.name.split("/")[0] and engine.B == tr["B"] and not getattr(engine, "tp", False):
+        if tr["model"] == c.name.split("/")[0] and vb == tr["B"] and not getattr(engine, "tp", False):
             traffic = tr["dram_bytes"]
             tnote = (f"ncu DRAM bytes of one verify forward at Q={tr['Q']}, ctx={tr['ctx']} "
                      f"(algorithmic {tr['algorithmic_bytes']} B: {tr['dram_bytes'] / tr['algorithmic_bytes']:.3f}x)")

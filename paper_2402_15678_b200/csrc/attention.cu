@@ -453,22 +453,51 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
 
 // ---------------------------------------------------------------------------
 // Row-split schedule for grouped-query attention (G = H / Hkv > 1, e.g.
-// Llama-2-70B's 8 query heads per KV head): one CTA per (request, KV head, 64
-// flattened (position, group head) rows); warp w owns rows 16w..16w+15 and
-// walks EVERY key of each 64-key tile (8 n-tiles of 8 keys), so each K/V byte
-// is staged once for all of the KV head's query rows and no cross-warp merge
-// is needed.  The schedule is chosen by G alone (never by Q), so a row's
-// arithmetic is the same in a Q=1 decode and a Q=s+1 verify (batch
-// invariance: extra fully-masked keys contribute exactly zero).
+// Llama-2-70B's 8 query heads per KV head): one CTA per (request, KV head, 96
+// flattened (position, group head) rows), 12 warps = 6 row warps x 2 key
+// groups.  Row warp r owns rows 16r..16r+15; key group j takes the 32-key
+// tiles t with t % 2 == j, so each round stages 64 keys once for all of the
+// KV head's query rows and the two groups' online softmax states are merged
+// once at the end (group 0 then group 1).  The query tile (RoPE applied) sits
+// in shared memory, so a thread holds little more than its O accumulator.
+// One CTA per SM covers a verify of up to 12 positions.  (The previous one-group schedule —
+// 4 warps, 180 registers, 64-key tiles walked serially — was issue-latency
+// bound: one warp per scheduler, 0.6-1 TB/s at every context.)
+// The schedule is fixed by G alone (never by Q or the cache length), so a
+// row's arithmetic is the same in a Q=1 decode and a Q=s+1 verify (batch
+// invariance: tiles beyond a row's keys are exact no-ops, and the key-group
+// merge always runs).
 // ---------------------------------------------------------------------------
-template <int D, int NBUF, bool PAGED>
-__global__ void __launch_bounds__(kAThreads)
+constexpr int kRW = 6;                 // row warps: 96 flattened rows per CTA (Q <= 12 at G = 8)
+constexpr int kRRows = 16 * kRW;
+constexpr int kRThreads = 2 * 32 * kRW;  // row warps x 2 key groups
+constexpr int kRKT = 32;               // keys per tile; a round = one tile per key group
+
+template <int D>
+struct RowsSmem {
+  static constexpr int LD = D + 8;             // padded rows: conflict-free ldmatrix
+  static constexpr int TILE = kRKT * LD;       // elements per K (or V) tile
+  static constexpr int Q_ELEMS = kRRows * LD;  // the CTA's query rows
+  static constexpr int KV_ELEMS = 2 * 2 * 2 * TILE;  // [round buf][key group][K|V]
+  static constexpr int MERGE_BYTES = kRW * 16 * (D + 2) * 4;  // key group 1's (O, m, l) per row
+  static constexpr int KV_BYTES = KV_ELEMS * 2 > MERGE_BYTES ? KV_ELEMS * 2 : MERGE_BYTES;
+  static constexpr int BYTES = Q_ELEMS * 2 + KV_BYTES;
+};
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+
+template <int D, bool PAGED>
+__global__ void __launch_bounds__(kRThreads, 1)
 attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                       const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                       int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
                       int64_t ldo, KVPage pg) {
-  using S = AttnSmem<D, NBUF>;
+  using S = RowsSmem<D>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;
   constexpr int NT = D / 8;
@@ -476,17 +505,18 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   extern __shared__ __align__(16) uint8_t smem[];
   pdl_wait();
   pdl_trigger();
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem);  // [2][KT][LD]
-  __nv_bfloat16* sV = sK + NBUF * S::TILE;                        // [NBUF][KT][LD]
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem);  // [kRRows][LD]
+  __nv_bfloat16* sKV = sQ + S::Q_ELEMS;                          // [2][2][K|V][kRKT][LD]
 
   const int b = blockIdx.x, h = blockIdx.y;  // h: KV head
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rw = warp % kRW, kg = warp / kRW;  // row warp, key group
   const int g = lane >> 2, t4 = lane & 3;
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
-  const int c0 = blockIdx.z * 64;             // first flattened row of the CTA
-  const int crows = min(64, rows_tot - c0);
-  const int q0 = c0 + warp * 16;              // first row of this warp
+  const int c0 = blockIdx.z * kRRows;         // first flattened row of the CTA
+  const int crows = min(kRRows, rows_tot - c0);
+  const int q0 = c0 + rw * 16;                // first row of this warp
   const int Q = max(0, min(16, rows_tot - q0));  // rows of this warp (0: idle)
   const int pstart = start[b];
   const int kv_slot = slot[b];
@@ -504,7 +534,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int QD = Hq * D, KVD = Hkv * D;
 
   if (fuse_append && blockIdx.z == 0) {
-    for (int e = tid; e < 2 * Qtot * V8; e += kAThreads) {
+    for (int e = tid; e < 2 * Qtot * V8; e += kRThreads) {
       const int kv = e >= Qtot * V8;
       const int e2 = e - kv * Qtot * V8;
       const int i = e2 / V8, c = e2 - i * V8;
@@ -524,60 +554,56 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
     }
   }
 
+  // the CTA's query rows -> shared memory (row r = flattened row c0 + r:
+  // position r / G, query head h*G + r % G), RoPE on 32-bit words (dims 2w,
+  // 2w+1 paired with 2w+D/2, 2w+D/2+1); rows past the call are zero
+  for (int e = tid; e < kRRows * (D / 4); e += kRThreads) {
+    const int r = e / (D / 4), w = e - r * (D / 4);
+    const int fr = c0 + r;
+    uint32_t lo = 0u, hi = 0u;
+    if (fr < rows_tot) {
+      const uint32_t* qp =
+          reinterpret_cast<const uint32_t*>(qkv + (int64_t)(b * Qtot + fr / G) * ldq + (h * G + fr % G) * D);
+      lo = qp[w];
+      hi = qp[w + D / 4];
+      if (rope) {
+        const float2* cs = rope + (int64_t)(pstart + fr / G) * (D / 2);
+        const float2 cc0 = cs[2 * w], cc1 = cs[2 * w + 1];
+        const uint32_t l2 = rope_pair_lo(lo, hi, cc0, cc1);
+        hi = rope_pair_hi(hi, lo, cc0, cc1);
+        lo = l2;
+      }
+    }
+    uint32_t* qs = reinterpret_cast<uint32_t*>(sQ + r * LD);
+    qs[w] = lo;
+    qs[w + D / 4] = hi;
+  }
+
   const int fr0 = q0 + g, fr1 = q0 + g + 8;
   const bool v0 = g < Q, v1 = g + 8 < Q;
   const int pos0 = pstart + fr0 / G, pos1 = pstart + fr1 / G;
-  uint32_t qa[KC][4];
-  {
-    const uint32_t* q0p = reinterpret_cast<const uint32_t*>(
-        qkv + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldq + (h * G + (v0 ? fr0 % G : 0)) * D);
-    const uint32_t* q1p = reinterpret_cast<const uint32_t*>(
-        qkv + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldq + (h * G + (v1 ? fr1 % G : 0)) * D);
-#pragma unroll
-    for (int c = 0; c < KC; ++c) {
-      const int w = c * 8 + t4;
-      qa[c][0] = v0 ? q0p[w] : 0u;
-      qa[c][1] = v1 ? q1p[w] : 0u;
-      qa[c][2] = v0 ? q0p[w + 4] : 0u;
-      qa[c][3] = v1 ? q1p[w + 4] : 0u;
-    }
-    if (rope) {
-      const float2* cs0 = rope + (int64_t)(v0 ? pos0 : 0) * (D / 2);
-      const float2* cs1 = rope + (int64_t)(v1 ? pos1 : 0) * (D / 2);
-#pragma unroll
-      for (int c = 0; c < KC / 2; ++c) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2* cs = (u & 1) ? cs1 : cs0;
-          const int d = c * 16 + (u >= 2 ? 8 : 0) + 2 * t4;
-          const float2 cc0 = cs[d], cc1 = cs[d + 1];
-          const uint32_t lo = qa[c][u], hi = qa[c + KC / 2][u];
-          qa[c][u] = rope_pair_lo(lo, hi, cc0, cc1);
-          qa[c + KC / 2][u] = rope_pair_hi(hi, lo, cc0, cc1);
-        }
-      }
-    }
-  }
-
   const int last_pos = pstart + (c0 + crows - 1) / G;
   const int n_keys = min(last_pos + 1, T);
-  const int n_tiles = (n_keys + kKT - 1) / kKT;
+  const int n_rounds = (n_keys + 2 * kRKT - 1) / (2 * kRKT);
+  // keys every valid row of this warp sees (the warp's first row has the
+  // smallest position): tiles below it need no causal mask
+  const int warp_lim = pstart + q0 / G;
 
-  constexpr int LRS = kAThreads / V8;
-  constexpr int LNP = kKT / LRS;
+  constexpr int LRS = kRThreads / V8;   // key rows per pass
   const int lc = tid % V8, lr0 = tid / V8;
   const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
   const __nv_bfloat16* qkv_v = qkv_k + KVD;
   const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;
-  auto load_tile = [&](int tile, int buf) {
-    const int t0 = tile * kKT;
-    __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
-    __nv_bfloat16* dv = sV + buf * S::TILE + lc * 8;
-#pragma unroll
-    for (int pp = 0; pp < LNP; ++pp) {
-      const int j = lr0 + pp * LRS;
+  // round rd = keys 64rd .. 64rd+63: tile 2rd (key group 0), tile 2rd+1 (group 1)
+  auto load_round = [&](int rd, int rb) {
+    const int t0 = rd * 2 * kRKT;
+    for (int j = lr0; j < 2 * kRKT; j += LRS) {
       const int t = t0 + j;
+      __nv_bfloat16* dk = sKV + ((rb * 2 + j / kRKT) * 2) * S::TILE + (j % kRKT) * LD + lc * 8;
+      __nv_bfloat16* dv = dk + S::TILE;
       if (t < n_keys) {
+        // the call's own rows (t >= pstart) come straight from qkv (K rotated
+        // on the way when RoPE), older keys from the cache
         const bool fresh = fuse_append && t >= pstart;
         const int64_t qrow = (int64_t)(t - pstart) * ldq;
         if (fresh && rope) {
@@ -585,14 +611,14 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
           unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
           unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
           rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
-          *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
+          *reinterpret_cast<bf16x8*>(dk) = pack8(fv);
         } else {
-          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
+          cp_async16(dk, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
         }
-        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
+        cp_async16(dv, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
       } else {
-        *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dk) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dv) = make_uint4(0, 0, 0, 0);
       }
     }
     cp_async_commit();
@@ -607,46 +633,59 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int row_lim1 = v1 ? pos1 : -1;
   const int lrow = lane & 15;
   const int lcol = (lane >> 4) * 8;
+  const __nv_bfloat16* qw = sQ + (rw * 16 + lrow) * LD + lcol;  // this lane's ldmatrix row
 
-#pragma unroll
-  for (int pp = 0; pp < NBUF - 1; ++pp) {
-    if (pp < n_tiles) load_tile(pp, pp);
+  if (n_rounds > 0) load_round(0, 0);
+  else cp_async_commit();
+  for (int rd = 0; rd < n_rounds; ++rd) {
+    const int rb = rd & 1;
+    if (rd + 1 < n_rounds) load_round(rd + 1, rb ^ 1);
     else cp_async_commit();
-  }
-  for (int tile = 0; tile < n_tiles; ++tile) {
-    const int buf = tile % NBUF;
-    if (tile + NBUF - 1 < n_tiles) load_tile(tile + NBUF - 1, (tile + NBUF - 1) % NBUF);
-    else cp_async_commit();
-    cp_async_wait<NBUF - 1>();
-    __syncthreads();
-    if (Q > 0) {  // warp-uniform
-      const __nv_bfloat16* kt = sK + buf * S::TILE;
-      const __nv_bfloat16* vt = sV + buf * S::TILE;
-      const int kbase = tile * kKT;
-      float sc[8][4];
+    cp_async_wait<1>();
+    __syncthreads();  // (first round: also the query tile)
+    const int kbase = (rd * 2 + kg) * kRKT;
+    if (Q > 0 && kbase < n_keys) {  // warp-uniform
+      const __nv_bfloat16* kt = sKV + ((rb * 2 + kg) * 2) * S::TILE;
+      const __nv_bfloat16* vt = kt + S::TILE;
+      float sc[4][4];
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
-        const __nv_bfloat16* kr = kt + (n * 8 + g) * LD + 2 * t4;
+      for (int n = 0; n < 4; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
 #pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + c * 16);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + c * 16 + 8);
-          mma16816(sc[n], qa[c], b0, b1);
+      for (int c = 0; c < KC; c += 2) {
+        uint32_t qa0[4], qa1[4];
+        ldmatrix_x4(qa0, qw + c * 16);
+        ldmatrix_x4(qa1, qw + (c + 1) * 16);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          uint32_t kb[4];  // keys n*8..n*8+7, dims c*16 .. c*16+31
+          ldmatrix_x4(kb, kt + (n * 8 + (lane & 7)) * LD + c * 16 + (lane >> 3) * 8);
+          mma16816(sc[n], qa0, kb[0], kb[1]);
+          mma16816(sc[n], qa1, kb[2], kb[3]);
         }
       }
       float mx[2] = {-INFINITY, -INFINITY};
+      if (kbase + kRKT - 1 <= warp_lim && kbase + kRKT <= n_keys) {
+        // every key of the tile is visible to every valid row of the warp
+        // (invalid rows carry zero queries and are never stored)
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
+        for (int n = 0; n < 4; ++n)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = kbase + n * 8 + 2 * t4 + (e & 1);
-          const int lim = (e < 2) ? row_lim0 : row_lim1;
-          float v = sc[n][e] * scale_log2;
-          if (key > lim || key >= n_keys) v = -INFINITY;
-          sc[n][e] = v;
-          mx[e >> 1] = fmaxf(mx[e >> 1], v);
-        }
+          for (int e = 0; e < 4; ++e) {
+            sc[n][e] *= scale_log2;
+            mx[e >> 1] = fmaxf(mx[e >> 1], sc[n][e]);
+          }
+      } else {
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = kbase + n * 8 + 2 * t4 + (e & 1);
+            const int lim = (e < 2) ? row_lim0 : row_lim1;
+            float v = sc[n][e] * scale_log2;
+            if (key > lim || key >= n_keys) v = -INFINITY;
+            sc[n][e] = v;
+            mx[e >> 1] = fmaxf(mx[e >> 1], v);
+          }
       }
       float corr[2], psum[2];
 #pragma unroll
@@ -659,7 +698,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
         psum[r] = 0.f;
       }
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
+      for (int n = 0; n < 4; ++n) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = e >> 1;
@@ -681,9 +720,9 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
         o[n][2] *= corr[1];
         o[n][3] *= corr[1];
       }
-      // O += P V over the tile's four 16-key blocks (P split bf16 hi + lo)
+      // O += P V over the tile's two 16-key blocks (P split bf16 hi + lo)
 #pragma unroll
-      for (int kb = 0; kb < 4; ++kb) {
+      for (int kb = 0; kb < 2; ++kb) {
         uint32_t pa[4], pl[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -705,18 +744,53 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // the round buffer is refilled by the next iteration's prefetch
   }
-  if (Q == 0) return;
-  const float inv0 = l_r[0] > 0.f ? 1.f / l_r[0] : 0.f;
-  const float inv1 = l_r[1] > 0.f ? 1.f / l_r[1] : 0.f;
+  cp_async_wait<0>();
+  __syncthreads();
+  // key group 1 hands its (O, m, l) to group 0 through the idle KV buffers;
+  // group 0 merges (group 0 first, always — also when group 1 saw no key)
+  float* mg = reinterpret_cast<float*>(sKV) + rw * 16 * (D + 2);
+  if (kg == 1 && Q > 0) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int col = n * 8 + 2 * t4;
+      *reinterpret_cast<float2*>(mg + g * (D + 2) + col) = make_float2(o[n][0], o[n][1]);
+      *reinterpret_cast<float2*>(mg + (g + 8) * (D + 2) + col) = make_float2(o[n][2], o[n][3]);
+    }
+    if (t4 == 0) {
+      mg[g * (D + 2) + D] = m_r[0];
+      mg[g * (D + 2) + D + 1] = l_r[0];
+      mg[(g + 8) * (D + 2) + D] = m_r[1];
+      mg[(g + 8) * (D + 2) + D + 1] = l_r[1];
+    }
+  }
+  __syncthreads();
+  if (kg == 1 || Q == 0) return;
+  float f0[2], f1[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const float* mr = mg + (g + 8 * r) * (D + 2);
+    const float m1 = mr[D], l1 = mr[D + 1];
+    const float m = fmaxf(m_r[r], m1);
+    const float a0 = m_r[r] == -INFINITY ? 0.f : exp2f(m_r[r] - m);
+    const float a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - m);
+    const float L = l_r[r] * a0 + l1 * a1;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    f0[r] = a0 * inv;
+    f1[r] = a1 * inv;
+  }
   __nv_bfloat16* o0p = out + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldo + (h * G + (v0 ? fr0 % G : 0)) * D;
   __nv_bfloat16* o1p = out + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldo + (h * G + (v1 ? fr1 % G : 0)) * D;
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
     const int col = n * 8 + 2 * t4;
-    if (v0) *reinterpret_cast<uint32_t*>(o0p + col) = pack_bf16(o[n][0] * inv0, o[n][1] * inv0);
-    if (v1) *reinterpret_cast<uint32_t*>(o1p + col) = pack_bf16(o[n][2] * inv1, o[n][3] * inv1);
+    const float2 p0 = *reinterpret_cast<const float2*>(mg + g * (D + 2) + col);
+    const float2 p1 = *reinterpret_cast<const float2*>(mg + (g + 8) * (D + 2) + col);
+    if (v0) *reinterpret_cast<uint32_t*>(o0p + col) =
+        pack_bf16(o[n][0] * f0[0] + p0.x * f1[0], o[n][1] * f0[0] + p0.y * f1[0]);
+    if (v1) *reinterpret_cast<uint32_t*>(o1p + col) =
+        pack_bf16(o[n][2] * f0[1] + p1.x * f1[1], o[n][3] * f0[1] + p1.y * f1[1]);
   }
 }
 
@@ -738,18 +812,17 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   // memory costs more resident CTAs than the hidden tile latency gains
   // (Llama-160M B=48 decode attention 13.8 -> 16 us, 70B verify 2.0 -> 3.0 ms)
   constexpr int NB = 2;
-  constexpr int NBR = 2;
   using S = AttnSmem<D, NB>;
-  using SR = AttnSmem<D, NBR>;
+  using SR = RowsSmem<D>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attention_kernel<D, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              S::BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(attention_kernel<D, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              S::BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(attention_rows_kernel<D, NBR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(attention_rows_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SR::BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(attention_rows_kernel<D, NBR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(attention_rows_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SR::BYTES) != cudaSuccess)
       return MS_ERR_CUDA;
     attr = true;
@@ -757,9 +830,9 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   const bool paged = pg.table != nullptr;
   const float scale_log2 = scale * 1.4426950408889634f;
   if (Hkv < H) {  // grouped-query: row-split schedule (chosen by G, never by Q)
-    dim3 grid(B, Hkv, (Q * (H / Hkv) + 63) / 64);
-    return launch(paged ? attention_rows_kernel<D, NBR, true> : attention_rows_kernel<D, NBR, false>, grid,
-                  dim3(kAThreads), SR::BYTES, st, 1, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
+    dim3 grid(B, Hkv, (Q * (H / Hkv) + kRRows - 1) / kRRows);
+    return launch(paged ? attention_rows_kernel<D, true> : attention_rows_kernel<D, false>, grid,
+                  dim3(kRThreads), SR::BYTES, st, 1, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                   (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, pg);
   }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
@@ -781,8 +854,8 @@ int preload_attention() {
   int n = 0;
   n += preload_fn(attention_kernel<64, 2, false>) + preload_fn(attention_kernel<128, 2, false>);
   n += preload_fn(attention_kernel<64, 2, true>) + preload_fn(attention_kernel<128, 2, true>);
-  n += preload_fn(attention_rows_kernel<64, 2, false>) + preload_fn(attention_rows_kernel<128, 2, false>);
-  n += preload_fn(attention_rows_kernel<64, 2, true>) + preload_fn(attention_rows_kernel<128, 2, true>);
+  n += preload_fn(attention_rows_kernel<64, false>) + preload_fn(attention_rows_kernel<128, false>);
+  n += preload_fn(attention_rows_kernel<64, true>) + preload_fn(attention_rows_kernel<128, true>);
   return n;
 }
 

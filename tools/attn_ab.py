@@ -1,37 +1,57 @@
-"""A/B of ms_attention_gqa between two builds of libminions (raw ctypes, so
-an older ABI works): python tools/attn_ab.py lib_a.so lib_b.so"""
+"""A/B of the GQA verify attention (ms_attention_gqa, Llama-2-70B heads,
+RoPE) between builds of libminions (raw ctypes, so an older build works):
+device time per call (20 back-to-back launches) and the max |difference| of
+each build's output vs the first build's.
+usage: python tools/attn_ab.py lib_a.so lib_b.so ..."""
 import ctypes, sys
 import torch
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 P, I, I64, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
 libs = [ctypes.CDLL(p) for p in sys.argv[1:]]
 for lib in libs:
     lib.ms_attention_gqa.argtypes = [P, I64, I, I, I, I, I, P, P, I, P, P, P, F, I, P, I64, P, I64, P, I, P]
-for name, B, Q, H, Hkv, D, ctx in (("70b ctx190", 16, 11, 64, 8, 128, 190), ("70b ctx1k", 16, 11, 64, 8, 128, 1024),
-                                  ("160m ctx200", 48, 1, 12, 12, 64, 200)):
-    T = ctx + Q + 8
-    kc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
-    vc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
-    qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, device="cuda").to(torch.bfloat16)
-    slot = torch.arange(B, dtype=torch.int32, device="cuda")
-    start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
-    out = torch.empty(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
-    res = []
-    for li, lib in enumerate(libs):
-        def run():
-            st = torch.cuda.current_stream().cuda_stream
-            assert lib.ms_attention_gqa(qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D, slot.data_ptr(),
-                                        start.data_ptr(), T, kc.data_ptr(), vc.data_ptr(), None, D ** -0.5, 1,
-                                        out.data_ptr(), out.stride(0), None, 0, None, 0, st) == 0
-        for _ in range(3):
-            run()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(5):
-            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            e0.record()
-            for _ in range(20):
+
+
+def rope_table(T, D, theta=10000.0):
+    inv = 1.0 / (theta ** (torch.arange(0, D, 2, dtype=torch.float64) / D))
+    ang = torch.arange(T, dtype=torch.float64)[:, None] * inv[None, :]
+    return torch.stack([ang.cos(), ang.sin()], -1).float().cuda().contiguous()
+
+
+print("case", [p.split("/")[-1] for p in sys.argv[1:]], "us; max|diff| vs first", flush=True)
+for ctx in (190, 1024, 4096):
+    for Q in (1, 5, 8, 11):
+        B, H, Hkv, D = 16, 64, 8, 128
+        T = ctx + Q + 8
+        torch.manual_seed(0)
+        kc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
+        vc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
+        qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, device="cuda").to(torch.bfloat16)
+        slot = torch.arange(B, dtype=torch.int32, device="cuda")
+        start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
+        tab = rope_table(T, D)
+        res, outs = [], []
+        for lib in libs:
+            out = torch.zeros(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
+
+            def run():
+                st = torch.cuda.current_stream().cuda_stream
+                assert lib.ms_attention_gqa(qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D, slot.data_ptr(),
+                                            start.data_ptr(), T, kc.data_ptr(), vc.data_ptr(), tab.data_ptr(),
+                                            D ** -0.5, 1, out.data_ptr(), out.stride(0), None, 0, None, 0, st) == 0
+            for _ in range(3):
                 run()
-            e1.record(); torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / 20 * 1e3)
-        res.append(round(sorted(ts)[2], 1))
-    print(name, res, flush=True)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+                e0.record()
+                for _ in range(20):
+                    run()
+                e1.record(); torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / 20 * 1e3)
+            res.append(round(sorted(ts)[2], 1))
+            outs.append(out.float())
+        diffs = [round((o - outs[0]).abs().max().item(), 5) for o in outs[1:]]
+        byts = B * Hkv * (ctx + Q) * D * 4
+        print(f"ctx={ctx:5d} Q={Q:2d}", res, diffs, [f"{byts / t / 1e3:.0f} GB/s" for t in res], flush=True)
