@@ -61,6 +61,11 @@ struct LinearParams {
   // each CTA finishes, overlapping the transfer with other CTAs' mainloops
   float* const* tp_recv;
   int tp_rank, tp_slice, tp_rows;
+  // stream-K persistent schedule (linear_pk_kernel): two fp32 partial slots
+  // [BN][128] per CTA-range boundary, one arrival counter per boundary (zero
+  // on entry, left zero); null: whole-tile persistent schedule
+  float* sk_ws;
+  int* sk_cnt;
   float* rms_out;
   const float* rms_in;
   int rms_nparts;
@@ -896,14 +901,33 @@ linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
 // ---------------------------------------------------------------------------
 // Persistent weight-streaming schedule for GEMMs with >= one tile per SM
 // (the 70B gate/up projection: 448 tiles, the LM head: 250): one CTA per SM
-// walks tiles c, c + P, c + 2P, ... with
+// with
 //   * decoupled TMA rings sized for ONE CTA per SM (~144 KB of weight tiles in
 //     flight — what a 6.5 TB/s stream needs per SM by Little's law — next to a
 //     shallow token ring), flowing across tile boundaries without a drain;
 //   * a double-buffered TMEM accumulator (2 x BN columns): the epilogue of tile
 //     t overlaps the mainloop of tile t + 1.
-// Whole tiles, full-K accumulation: bitwise the arithmetic of the one-split
-// cluster path, so the schedule choice never changes a result.
+// Two work partitions:
+//   * whole tiles (MS_PK=1, no workspace): tiles c, c + P, ... — bitwise the
+//     arithmetic of the one-split cluster path, but 448 tiles over 148 CTAs is
+//     4 vs 3 tiles per CTA (a 33% tail);
+//   * stream-K (a workspace is passed): CTA c owns the flat k-block range
+//     [c T / P, (c+1) T / P) of the tile-major iteration space (T = tiles x
+//     k-blocks), so every CTA streams the same number of weight bytes.  As a
+//     range is >= one tile long, a tile is split between at most two CTAs: the
+//     head (k-blocks from 0, at the END of CTA c-1's range) and the tail (the
+//     START of CTA c's range).  Both store their fp32 partial to the
+//     boundary's two slots and bump its counter; the second to arrive adds the
+//     other's partial to its own accumulator (a + b: commutative, so the
+//     arrival order never changes a bit) and runs the epilogue — no CTA ever
+//     waits for another.  The partition is a function of (N, K) and the SM
+//     count only, never of M: batch-invariant.
+// Measured slower than the cluster path inside a launch sequence (70B gate/up
+// at M = 80, CUDA-graph replay: 215 vs 172 us; alone under ncu 218 vs 209 us,
+// both ~4.4 TB/s): the cluster path's half-full second wave is filled by the
+// NEXT kernel's PDL weight prefetch, which one CTA per SM with ~200 KB of
+// shared memory never lets in.  So it runs only when a caller passes a
+// workspace (tests, tools/probe_gemm_graph.py); the models do not.
 // ---------------------------------------------------------------------------
 template <int BN>
 struct PKCfg {
@@ -913,12 +937,13 @@ struct PKCfg {
   static constexpr int MAX_SX = 6;
   static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
-  static constexpr int XB_BYTES = 64 * 17 * 4;  // gated-epilogue exchange buffer
+  // gated epilogue: the up half [BN][65] fp32 + the bf16 output tile [BN][64]
+  static constexpr int EPI_BYTES = BN * 65 * 4 + BN * 64 * 2;
   // both rings sized by latency: weight tiles (HBM, ~2 us loaded) and token
   // tiles (L2, ~1.2 us) are consumed one of each per k-block, so the stage
   // counts go ~5:3 within the budget
   __host__ __device__ static void rings(int* sw, int* sx) {
-    const int budget = 206 * 1024 - XB_BYTES;
+    const int budget = 206 * 1024 - EPI_BYTES;
     int x = budget * 3 / (5 * W_BYTES + 3 * X_BYTES);
     x = x < 2 ? 2 : (x > MAX_SX ? MAX_SX : x);
     int w = (budget - x * X_BYTES) / W_BYTES;
@@ -926,9 +951,49 @@ struct PKCfg {
     *sx = x;
   }
   __host__ __device__ static int smem(int sw, int sx) {
-    return 1024 + sw * W_BYTES + sx * X_BYTES + XB_BYTES + (2 * MAX_SW + 2 * MAX_SX + 4) * 8 + 16;
+    return 1024 + sw * W_BYTES + sx * X_BYTES + EPI_BYTES + (2 * MAX_SW + 2 * MAX_SX + 4) * 8 + 16;
   }
 };
+
+// this CTA's (tile, k-block range) segments, in order
+struct PKSeg {
+  int64_t u, u1;   // stream-K: flat k-block range [u, u1)
+  int t, step, n;  // whole tiles: t, t + step, ... (n left)
+  int kbt;
+  bool sk;
+  __device__ bool next(int& tile, int& k0, int& k1) {
+    if (sk) {
+      if (u >= u1) return false;
+      tile = (int)(u / kbt);
+      const int64_t base = (int64_t)tile * kbt;
+      k0 = (int)(u - base);
+      const int64_t e = base + kbt < u1 ? base + kbt : u1;
+      k1 = (int)(e - base);
+      u = e;
+      return true;
+    }
+    if (n <= 0) return false;
+    tile = t;
+    k0 = 0;
+    k1 = kbt;
+    t += step;
+    --n;
+    return true;
+  }
+};
+
+__device__ __forceinline__ PKSeg pk_segments(const LinearParams& p, int c, int P) {
+  PKSeg s;
+  s.kbt = p.kb_total;
+  s.sk = p.sk_ws != nullptr;
+  const int64_t total = (int64_t)p.n_tiles * p.kb_total;
+  s.u = total * c / P;
+  s.u1 = total * (c + 1) / P;
+  s.t = c;
+  s.step = P;
+  s.n = c < p.n_tiles ? (p.n_tiles - c + P - 1) / P : 0;
+  return s;
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -940,21 +1005,20 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
   const int SW = p.sw, SX = p.sx;
   uint8_t* sW = smem;
   uint8_t* sX = smem + SW * C::W_BYTES;
-  float* xb = reinterpret_cast<float*>(sX + SX * C::X_BYTES);  // [64][17]
-  uint64_t* fullW = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xb) + C::XB_BYTES);
+  float* U = reinterpret_cast<float*>(sX + SX * C::X_BYTES);          // [BN][65]
+  __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(U + BN * 65);    // [BN][64]
+  uint64_t* fullW = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(U) + C::EPI_BYTES);
   uint64_t* emptyW = fullW + C::MAX_SW;
   uint64_t* fullX = emptyW + C::MAX_SW;
   uint64_t* emptyX = fullX + C::MAX_SX;
   uint64_t* tfull = emptyX + C::MAX_SX;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ int s_arrival;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int P = gridDim.x, c = blockIdx.x;
-  const int kbt = p.kb_total;
-  const int n_my = c < p.n_tiles ? (p.n_tiles - c + P - 1) / P : 0;  // tiles c, c+P, ...
-  const int total = n_my * kbt;                                       // flat k-block iterations
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmW);
@@ -979,21 +1043,31 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
+  int tile, k0, k1;
   if (warp == 0) {
     if (lane == 0) {
+      // weights do not depend on the previous kernel: the first SW tiles are
+      // issued before the programmatic-dependency wait (PDL prefetch)
       const uint64_t pol_w = tc::policy_evict_first();
-      const int pre = total < SW ? total : SW;
-      for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel (PDL prefetch)
-        tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
-        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (i % kbt) * kBK, (c + (i / kbt) * P) * kBM, pol_w);
+      PKSeg sg = pk_segments(p, c, P);
+      int i = 0;
+      bool waited = false;
+      while (sg.next(tile, k0, k1)) {
+        for (int kb = k0; kb < k1; ++kb, ++i) {
+          if (i == SW && !waited) {
+            pdl_wait();
+            pdl_trigger();
+            waited = true;
+          }
+          const int st = i % SW;
+          if (i >= SW) tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
+          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], kb * kBK, tile * kBM, pol_w);
+        }
       }
-      pdl_wait();
-      pdl_trigger();
-      for (int i = pre; i < total; ++i) {
-        const int st = i % SW;
-        tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
-        tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (i % kbt) * kBK, (c + (i / kbt) * P) * kBM, pol_w);
+      if (!waited) {
+        pdl_wait();
+        pdl_trigger();
       }
     } else {
       pdl_trigger();
@@ -1003,11 +1077,15 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
       const uint64_t pol_x = tc::policy_evict_last();
       pdl_wait();
       pdl_trigger();
-      for (int i = 0; i < total; ++i) {
-        const int st = i % SX;
-        if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-        tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (i % kbt) * kBK, 0, pol_x);
+      PKSeg sg = pk_segments(p, c, P);
+      int i = 0;
+      while (sg.next(tile, k0, k1)) {
+        for (int kb = k0; kb < k1; ++kb, ++i) {
+          const int st = i % SX;
+          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
+          tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], kb * kBK, 0, pol_x);
+        }
       }
     } else {
       pdl_trigger();
@@ -1016,13 +1094,14 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
     pdl_trigger();
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
-      int i = 0;
-      for (int t = 0; t < n_my; ++t) {
-        const int buf = t & 1;
-        tc::mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+      PKSeg sg = pk_segments(p, c, P);
+      int i = 0, s = 0;
+      while (sg.next(tile, k0, k1)) {
+        const int buf = s & 1;
+        tc::mbar_wait(&tempty[buf], ((s >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         tc::fence_after_sync();
         const uint32_t acc = tmem + buf * C::ACC_COLS;
-        for (int kb = 0; kb < kbt; ++kb, ++i) {
+        for (int kb = k0; kb < k1; ++kb, ++i) {
           const int ws = i % SW, xs = i % SX;
           tc::mbar_wait(&fullW[ws], (i / SW) & 1);
           tc::mbar_wait(&fullX[xs], (i / SX) & 1);
@@ -1031,11 +1110,12 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
           const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            tc::mma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            tc::mma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
           tc::mma_commit(&emptyW[ws]);
           tc::mma_commit(&emptyX[xs]);
         }
         tc::mma_commit(&tfull[buf]);
+        ++s;
       }
     }
   } else {
@@ -1043,36 +1123,92 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
     pdl_wait();
     pdl_trigger();
     const int q = warp & 3;
+    const int f = q * 32 + lane;  // this thread's feature (TMEM lane) within the tile
     const int m_hi = min(BN, p.M);
-    for (int t = 0; t < n_my; ++t) {
-      const int buf = t & 1;
-      const int tile = c + t * P;
-      tc::mbar_wait(&tfull[buf], (t >> 1) & 1);
+    PKSeg sg = pk_segments(p, c, P);
+    int s = 0;
+    while (sg.next(tile, k0, k1)) {
+      const int buf = s & 1;
+      tc::mbar_wait(&tfull[buf], (s >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t trow = tmem + buf * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
-      if (p.act == 2) {
-        const bool up = q >= 2;
-        const int of = tile * (kBM / 2) + (q & 1) * 32 + lane;
+      const float* other = nullptr;  // the other segment's partial [token][feature]
+      bool finish = true;
+      if (k0 > 0 || k1 < p.kb_total) {
+        // split tile: boundary c (this range's first segment, the tile's tail)
+        // or c + 1 (its last segment, the tile's head); slot 2*bnd + role
+        const int bnd = k0 > 0 ? c : c + 1;
+        const int role = k0 > 0 ? 1 : 0;
+        float* mine = p.sk_ws + (int64_t)(2 * bnd + role) * (BN * kBM);
         for (int c0 = 0; c0 < m_hi; c0 += 16) {
           uint32_t r[16];
           tc::tmem_ld16(trow + c0, r);
           tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < m_hi) __stcg(mine + (c0 + j) * kBM + f, __uint_as_float(r[j]));
+        }
+        __threadfence();
+        epi_bar128();
+        if (threadIdx.x == 64) {
+          const int old = atomicAdd(p.sk_cnt + bnd, 1);
+          if (old == 1) p.sk_cnt[bnd] = 0;  // both arrived: zero for the next launch
+          s_arrival = old;
+        }
+        epi_bar128();
+        finish = s_arrival == 1;  // (rewritten only after the next split's first barrier)
+        if (finish) {
+          __threadfence();
+          other = p.sk_ws + (int64_t)(2 * bnd + 1 - role) * (BN * kBM);
+        }
+      }
+      if (finish && p.act == 2) {
+        // gated SiLU: the up warps park the up half in smem, the gate warps
+        // form silu(g) * u into a bf16 tile, all four store it with 16-byte
+        // writes (output features tile*64 .. tile*64+63)
+        const bool up = q >= 2;
+        const int fu = (q & 1) * 32 + lane;
+        for (int c0 = 0; c0 < m_hi; c0 += 32) {
+          uint32_t r[32];
+          tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
+          tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+          tc::tmem_wait_ld();
           if (up) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) xb[((q - 2) * 32 + lane) * 17 + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < m_hi) {
+                const float v = __uint_as_float(r[j]);
+                U[(c0 + j) * 65 + fu] = other ? v + __ldcg(other + (c0 + j) * kBM + f) : v;
+              }
           }
-          epi_bar128();
-          if (!up) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + of;
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < m_hi)
-                o[(int64_t)(c0 + j) * p.ldc] = f2bf(silu_mul(__uint_as_float(r[j]), xb[(q * 32 + lane) * 17 + j]));
-          }
-          epi_bar128();
         }
-      } else {
-        const int feat = tile * kBM + q * 32 + lane;
+        epi_bar128();
+        if (!up) {
+          for (int c0 = 0; c0 < m_hi; c0 += 32) {
+            uint32_t r[32];
+            tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < m_hi) {
+                const float v = __uint_as_float(r[j]);
+                const float gv = other ? v + __ldcg(other + (c0 + j) * kBM + f) : v;
+                O[(c0 + j) * 64 + fu] = f2bf(silu_mul(gv, U[(c0 + j) * 65 + fu]));
+              }
+          }
+        }
+        epi_bar128();
+        const int et = threadIdx.x - 64;  // 0..127
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + tile * (kBM / 2);
+        for (int e = et; e < m_hi * 8; e += 128) {
+          const int row = e >> 3, ch = e & 7;
+          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
+              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
+        }
+        epi_bar128();  // U / O are reused by the next tile
+      } else if (finish) {
+        const int feat = tile * kBM + f;
         const bool feat_ok = feat < p.N;
         for (int c0 = 0; c0 < m_hi; c0 += 16) {
           uint32_t r[16];
@@ -1081,12 +1217,16 @@ linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
           if (feat_ok) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              if (c0 + j < m_hi) epi_store(p, c0 + j, feat, __uint_as_float(r[j]));
+              if (c0 + j < m_hi) {
+                const float v = __uint_as_float(r[j]);
+                epi_store(p, c0 + j, feat, other ? v + __ldcg(other + (c0 + j) * kBM + f) : v);
+              }
           }
         }
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty[buf]);
+      ++s;
     }
   }
   tc::fence_before_sync();
@@ -1206,6 +1346,10 @@ static int sm_count() {
   return n;
 }
 
+// stream-K persistent schedule scratch: two fp32 [BN][128] slots per range
+// boundary (SMs + 1 boundaries)
+static int64_t pk_ws_bytes(int bn) { return (int64_t)(sm_count() + 1) * 2 * bn * kBM * 4; }
+
 template <int BN>
 static int launch_linear_pk(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, cudaStream_t st) {
   using C = PKCfg<BN>;
@@ -1221,7 +1365,8 @@ static int launch_linear_pk(const CUtensorMap& tw, const CUtensorMap& tx, Linear
   p.sw = sw;
   p.sx = sx;
   p.splits = 1;
-  const int grid = p.n_tiles < sm_count() ? p.n_tiles : sm_count();
+  // stream-K: one range per SM (n_tiles >= SMs, so every range is >= one tile)
+  const int grid = p.sk_ws ? sm_count() : (p.n_tiles < sm_count() ? p.n_tiles : sm_count());
   return launch(linear_pk_kernel<BN>, dim3(grid), dim3(kThreads), C::smem(sw, sx), st, 1, tw, tx, p);
 }
 // Opt-in (MS_PK=1): measured no faster than the cluster path on the 70B
@@ -1289,8 +1434,14 @@ extern "C" int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* 
   if (M < 0 || N < 1 || K < 1) return MS_ERR_VALUE;
   const int bn = ms::pick_bn(M);
   const int g = ms::linear_sk_grid(N, K);
-  if (ws_bytes) *ws_bytes = (int64_t)g * 2 * bn * ms::kBM * 4;
-  if (n_counters) *n_counters = (N + ms::kBM - 1) / ms::kBM;
+  int64_t b = (int64_t)g * 2 * bn * ms::kBM * 4;
+  int n = (N + ms::kBM - 1) / ms::kBM;
+  if (n >= ms::sm_count()) {  // persistent stream-K schedule
+    b = b > ms::pk_ws_bytes(bn) ? b : ms::pk_ws_bytes(bn);
+    n = n > ms::sm_count() + 1 ? n : ms::sm_count() + 1;
+  }
+  if (ws_bytes) *ws_bytes = b;
+  if (n_counters) *n_counters = n;
   return MS_OK;
 }
 
@@ -1339,6 +1490,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
   p.rms_out = nullptr; p.rms_in = nullptr; p.rms_nparts = 0; p.rms_ld = 0; p.rms_eps = 0.f; p.nc = 1;
   p.tp_recv = nullptr; p.tp_rank = 0; p.tp_slice = 1; p.tp_rows = 0;
+  p.sk_ws = nullptr; p.sk_cnt = nullptr;
   p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
   if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
     p.ln_g = (const __nv_bfloat16*)g_ln_g;
@@ -1350,6 +1502,31 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
   p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
   const bool folded = rms.out || rms.in || rms.tp_recv;
+  // weight-streaming GEMMs with at least one 128-feature tile per SM and a
+  // workspace: the persistent stream-K schedule (equal weight bytes per SM)
+  const bool big = splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count();
+  if (big && ws && counters && ws_bytes >= pk_ws_bytes(bn) && n_counters >= sm_count() + 1) {
+    p.sk_ws = (float*)ws;
+    p.sk_cnt = counters;
+    switch (bn) {
+      case 16: return launch_linear_pk<16>(tw, tx, p, st);
+      case 32: return launch_linear_pk<32>(tw, tx, p, st);
+      case 48: return launch_linear_pk<48>(tw, tx, p, st);
+      case 64: return launch_linear_pk<64>(tw, tx, p, st);
+      case 80: return launch_linear_pk<80>(tw, tx, p, st);
+      case 96: return launch_linear_pk<96>(tw, tx, p, st);
+      case 112: return launch_linear_pk<112>(tw, tx, p, st);
+      case 128: return launch_linear_pk<128>(tw, tx, p, st);
+      case 144: return launch_linear_pk<144>(tw, tx, p, st);
+      case 160: return launch_linear_pk<160>(tw, tx, p, st);
+      case 176: return launch_linear_pk<176>(tw, tx, p, st);
+      case 192: return launch_linear_pk<192>(tw, tx, p, st);
+      case 208: return launch_linear_pk<208>(tw, tx, p, st);
+      case 224: return launch_linear_pk<224>(tw, tx, p, st);
+      case 240: return launch_linear_pk<240>(tw, tx, p, st);
+      default: return launch_linear_pk<256>(tw, tx, p, st);
+    }
+  }
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
   if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded &&
@@ -1381,7 +1558,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   }
   // weight-streaming GEMMs with at least one 128-feature tile per SM: the
   // persistent schedule (whole tiles; MS_PK=0 disables, for A/B runs)
-  if (splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count() && pk_enabled()) {
+  if (big && pk_enabled()) {
     switch (bn) {
       case 16: return launch_linear_pk<16>(tw, tx, p, st);
       case 32: return launch_linear_pk<32>(tw, tx, p, st);

@@ -295,3 +295,26 @@ print("ok")
     ref = _ref_linear(x.cpu(), w.cpu(), None, None if r is None else r.cpu(), 0, True) if act == 0 else None
     if ref is not None:
         torch.testing.assert_close(pk.cpu().float(), ref.float(), rtol=1.6e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("N,K,act", [(57344, 8192, 2), (32000, 8192, 0), (50272, 768, 0), (18944, 1024, 2)])
+def test_linear_stream_k_persistent(N, K, act):
+    """Persistent stream-K schedule (a Workspace with >= one tile per SM):
+    split tiles combine two fp32 partials (a + b, arrival-order free) — within
+    rounding of the cluster path, bitwise independent of M, deterministic."""
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(N + K)
+    w = (torch.randn(N, K, generator=g) * 0.02).to(torch.bfloat16).cuda()
+    x = torch.randn(256, K, generator=g).to(torch.bfloat16).cuda()
+    ws = Kn.Workspace("cuda")
+    ws.fit(256, N, K)
+    f32 = act == 0
+    full = Kn.linear(x, w, act=act, out_f32=f32, ws=ws)
+    ref = Kn.linear(x, w, act=act, out_f32=f32)  # cluster path
+    if f32:
+        torch.testing.assert_close(full, ref, rtol=1e-4, atol=2e-5 * (K ** 0.5))
+    else:
+        torch.testing.assert_close(full.float(), ref.float(), rtol=1.6e-2, atol=1e-2)
+    for M in (1, 16, 80, 176, 255):
+        assert torch.equal(Kn.linear(x[:M].contiguous(), w, act=act, out_f32=f32, ws=ws), full[:M]), M
+    assert torch.equal(Kn.linear(x, w, act=act, out_f32=f32, ws=ws), full)

@@ -38,12 +38,14 @@ for M in M_list:
                 wsp = K.Workspace("cuda")
                 wsp.fit(M, N, Kd)
                 spv = 0
+            elif sp == "auto":  # splits=0, no workspace (MS_PK=1: whole-tile persistent)
+                spv = 0
             else:
                 spv = int(sp) or K.linear_splits(N, Kd)
             if sp != "gemv":
                 def run():
                     for w in ws:
-                        K.linear(x, w, out=out, out_f32=f32, splits=spv, ws=None if act == 2 else wsp, act=act)
+                        K.linear(x, w, out=out, out_f32=f32, splits=spv, ws=wsp, act=act)
             run(); torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -56,6 +58,6 @@ for M in M_list:
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) * 1e-3 / (3 * L)
             byts = N * Kd * 2 + M * Kd * 2 + M * N * (4 if f32 else 2)
-            print(f"M={M:4d} {name:10s} N={N:6d} K={Kd:6d} splits={sp if sp in ("sk", "gemv") else spv} L={L:3d} {t*1e6:8.2f} us/launch {byts/t/1e9:7.0f} GB/s", flush=True)
+            print(f"M={M:4d} {name:10s} N={N:6d} K={Kd:6d} splits={sp if sp in ("sk", "gemv", "auto") else spv} L={L:3d} {t*1e6:8.2f} us/launch {byts/t/1e9:7.0f} GB/s", flush=True)
         del ws
         torch.cuda.empty_cache()
