@@ -472,13 +472,21 @@ constexpr int kRW = 6;                 // row warps: 96 flattened rows per CTA (
 constexpr int kRRows = 16 * kRW;
 constexpr int kRThreads = 2 * 32 * kRW;  // row warps x 2 key groups
 constexpr int kRKT = 32;               // keys per tile; a round = one tile per key group
+// round buffers: NR-1 rounds (64 keys each) in flight ahead of the one being
+// computed — a ~200-key verify context is fetched in one DRAM latency, and a
+// long context keeps ~100 KB in flight per SM (registers already hold the
+// CTA to one per SM, so the shared memory is free)
+constexpr int kRNR = 4;
+#ifndef MS_ATTN_PLO
+#define MS_ATTN_PLO 0
+#endif
 
 template <int D>
 struct RowsSmem {
   static constexpr int LD = D + 8;             // padded rows: conflict-free ldmatrix
   static constexpr int TILE = kRKT * LD;       // elements per K (or V) tile
   static constexpr int Q_ELEMS = kRRows * LD;  // the CTA's query rows
-  static constexpr int KV_ELEMS = 2 * 2 * 2 * TILE;  // [round buf][key group][K|V]
+  static constexpr int KV_ELEMS = kRNR * 2 * 2 * TILE;  // [round buf][key group][K|V]
   static constexpr int MERGE_BYTES = kRW * 16 * (D + 2) * 4;  // key group 1's (O, m, l) per row
   static constexpr int KV_BYTES = KV_ELEMS * 2 > MERGE_BYTES ? KV_ELEMS * 2 : MERGE_BYTES;
   static constexpr int BYTES = Q_ELEMS * 2 + KV_BYTES;
@@ -506,7 +514,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   pdl_wait();
   pdl_trigger();
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem);  // [kRRows][LD]
-  __nv_bfloat16* sKV = sQ + S::Q_ELEMS;                          // [2][2][K|V][kRKT][LD]
+  __nv_bfloat16* sKV = sQ + S::Q_ELEMS;                          // [kRNR][2][K|V][kRKT][LD]
 
   const int b = blockIdx.x, h = blockIdx.y;  // h: KV head
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -635,13 +643,16 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int lcol = (lane >> 4) * 8;
   const __nv_bfloat16* qw = sQ + (rw * 16 + lrow) * LD + lcol;  // this lane's ldmatrix row
 
-  if (n_rounds > 0) load_round(0, 0);
-  else cp_async_commit();
+#pragma unroll
+  for (int pp = 0; pp < kRNR - 1; ++pp) {
+    if (pp < n_rounds) load_round(pp, pp);
+    else cp_async_commit();  // empty group: keeps the wait count uniform
+  }
   for (int rd = 0; rd < n_rounds; ++rd) {
-    const int rb = rd & 1;
-    if (rd + 1 < n_rounds) load_round(rd + 1, rb ^ 1);
+    const int rb = rd % kRNR;
+    if (rd + kRNR - 1 < n_rounds) load_round(rd + kRNR - 1, (rd + kRNR - 1) % kRNR);
     else cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<kRNR - 1>();
     __syncthreads();  // (first round: also the query tile)
     const int kbase = (rd * 2 + kg) * kRKT;
     if (Q > 0 && kbase < n_keys) {  // warp-uniform
@@ -720,17 +731,25 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
         o[n][2] *= corr[1];
         o[n][3] *= corr[1];
       }
-      // O += P V over the tile's two 16-key blocks (P split bf16 hi + lo)
+      // O += P V over the tile's two 16-key blocks: P as bf16 (its fp32 row
+      // sum is the normaliser), as flash-attention kernels do; MS_ATTN_PLO=1
+      // adds the bf16 remainder P - bf16(P) as a second MMA (~fp32 P, 1.5x the
+      // tensor work of this compute-latency-bound loop)
 #pragma unroll
       for (int kb = 0; kb < 2; ++kb) {
-        uint32_t pa[4], pl[4];
+        uint32_t pa[4];
+#if MS_ATTN_PLO
+        uint32_t pl[4];
+#endif
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const float x0 = sc[2 * kb + (u >> 1)][2 * (u & 1)], x1 = sc[2 * kb + (u >> 1)][2 * (u & 1) + 1];
           const __nv_bfloat162 hi = __floats2bfloat162_rn(x0, x1);
-          const float2 hf = __bfloat1622float2(hi);
           pa[u] = *reinterpret_cast<const uint32_t*>(&hi);
+#if MS_ATTN_PLO
+          const float2 hf = __bfloat1622float2(hi);
           pl[u] = pack_bf16(x0 - hf.x, x1 - hf.y);
+#endif
         }
 #pragma unroll
         for (int n2 = 0; n2 < NT / 2; ++n2) {
@@ -739,7 +758,9 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             mma16816(o[2 * n2 + u], pa, vb[2 * u], vb[2 * u + 1]);
+#if MS_ATTN_PLO
             mma16816(o[2 * n2 + u], pl, vb[2 * u], vb[2 * u + 1]);
+#endif
           }
         }
       }

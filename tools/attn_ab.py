@@ -1,6 +1,7 @@
 """A/B of the GQA verify attention (ms_attention_gqa, Llama-2-70B heads,
 RoPE) between builds of libminions (raw ctypes, so an older build works):
-device time per call (20 back-to-back launches) and the max |difference| of
+device time per call (back-to-back launches over L distinct KV caches, like
+L layers, so K/V stream from HBM as in a forward) and the max |difference| of
 each build's output vs the first build's.
 usage: python tools/attn_ab.py lib_a.so lib_b.so ..."""
 import ctypes, sys
@@ -24,8 +25,9 @@ for ctx in (190, 1024, 4096):
         B, H, Hkv, D = 16, 64, 8, 128
         T = ctx + Q + 8
         torch.manual_seed(0)
-        kc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
-        vc = torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)
+        L = max(2, min(40, int(4e9 // (B * Hkv * T * D * 4))))
+        kcs = [torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
+        vcs = [torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16) for _ in range(L)]
         qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, device="cuda").to(torch.bfloat16)
         slot = torch.arange(B, dtype=torch.int32, device="cuda")
         start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
@@ -34,10 +36,10 @@ for ctx in (190, 1024, 4096):
         for lib in libs:
             out = torch.zeros(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
 
-            def run():
+            def run(i=0):
                 st = torch.cuda.current_stream().cuda_stream
                 assert lib.ms_attention_gqa(qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D, slot.data_ptr(),
-                                            start.data_ptr(), T, kc.data_ptr(), vc.data_ptr(), tab.data_ptr(),
+                                            start.data_ptr(), T, kcs[i].data_ptr(), vcs[i].data_ptr(), tab.data_ptr(),
                                             D ** -0.5, 1, out.data_ptr(), out.stride(0), None, 0, None, 0, st) == 0
             for _ in range(3):
                 run()
@@ -46,12 +48,14 @@ for ctx in (190, 1024, 4096):
             for _ in range(5):
                 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
                 e0.record()
-                for _ in range(20):
-                    run()
+                for i in range(L):
+                    run(i)
                 e1.record(); torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1) / 20 * 1e3)
+                ts.append(e0.elapsed_time(e1) / L * 1e3)
             res.append(round(sorted(ts)[2], 1))
             outs.append(out.float())
         diffs = [round((o - outs[0]).abs().max().item(), 5) for o in outs[1:]]
         byts = B * Hkv * (ctx + Q) * D * 4
         print(f"ctx={ctx:5d} Q={Q:2d}", res, diffs, [f"{byts / t / 1e3:.0f} GB/s" for t in res], flush=True)
+        del kcs, vcs
+        torch.cuda.empty_cache()
