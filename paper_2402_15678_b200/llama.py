@@ -174,7 +174,7 @@ class LlamaModel:
         low-latency ms_gemv (drafters' decode steps); the verifier keeps the
         tcgen05 path everywhere, so its numerics never depend on the row count.
 
-        fuse_norm (opt-in, MS_FUSE_NORM=1 or True): RMSNorm folded
+        fuse_norm (default; MS_FUSE_NORM=0 or False disables): RMSNorm folded
         across GEMMs — the gains are folded into w_qkv / w_gu / lm_head
         (LlamaWeights.fold_norms, in place), the O / down GEMMs emit per-row
         sums of squares and the QKV / gate-up / LM-head GEMMs scale by rstd:
@@ -185,11 +185,14 @@ class LlamaModel:
         self.small_gemm = small_gemm
         c = self.cfg
         if fuse_norm is None:
-            # opt-in (MS_FUSE_NORM=1): the bench A/B measured no gain — 1,929 vs
-            # 2,052 tokens/s pipelined (graph A/B of the forward alone: -0.9 ms
-            # at Q = 7, +0.35 ms at Q = 11; the token-granular producer epilogue
-            # offsets the saved norm kernels)
-            fuse_norm = os.environ.get("MS_FUSE_NORM", "0") == "1" and not small_gemm
+            # on by default (MS_FUSE_NORM=0 disables): interleaved graph A/B of
+            # the 70B verify forward (tools/ab_fuse_norm.py, same weights and
+            # process) 27.02 vs 27.84 ms at Q = 5, 29.90 vs 30.85 at Q = 7,
+            # 33.09 vs 33.62 at Q = 9, 36.89 vs 36.97 at Q = 11.  (An earlier
+            # whole-bench A/B read it as a loss, but the adaptive selector's
+            # s trajectory differs run to run, so bench lines cannot resolve
+            # a ~2% forward change.)
+            fuse_norm = os.environ.get("MS_FUSE_NORM", "1") != "0" and not small_gemm
         o_split = K.linear_splits(c.d, c.n_heads * c.head_dim)
         d_split = K.linear_splits(c.d, c.ffn)
         self.fuse_norm = bool(fuse_norm) and o_split > 1 and d_split > 1  # producers need split-K

@@ -8,9 +8,9 @@ from paper_2402_15678_b200.opt import KVCache
 c = CONFIGS["llama-2-70b"]
 w = LlamaWeights.random(c, 0)
 B = 16
-for Q in (7, 11):
+for Q in (5, 7, 9, 11):
     ms = {}
-    models = {"fused": LlamaModel(w, max_rows=B * Q), "explicit": LlamaModel(w, max_rows=B * Q, fuse_norm=False)}
+    models = {"fused": LlamaModel(w, max_rows=B * Q, fuse_norm=True), "explicit": LlamaModel(w, max_rows=B * Q, fuse_norm=False)}
     cache = KVCache(c, B, 512)
     tok = torch.randint(0, c.vocab, (B, Q), dtype=torch.int32, device="cuda")
     start = torch.full((B,), 190, dtype=torch.int32, device="cuda")
