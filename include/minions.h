@@ -187,6 +187,12 @@ int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, const void* ga
 int ms_rmsnorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, float eps,
                int R, int d, void* out, int64_t ldo, void* stream);
 
+/* Gated SiLU of a gate/up GEMM's fp32 output gu [M, ldg] (N columns, 64-row
+ * interleaved weight: tile t = 64 gate then 64 up columns) into out [M, ldo]
+ * bf16, N/2 columns: silu(g) * u in fp32, one rounding — the ms_linear act=2
+ * epilogue for prompt-prefill GEMMs run on cuBLAS. */
+int ms_gated_silu(const float* gu, int64_t ldg, int M, int N, void* out, int64_t ldo, void* stream);
+
 /* KV-cache append: rows r = b*Q + i of qkv [B*Q, ldq] (layout [q | k | v],
  * each H*D wide) are written at position start[b] + i of cache slot slot[b];
  * caches are [slots, H, T, D] bf16.  Positions outside [0, T) are skipped. */

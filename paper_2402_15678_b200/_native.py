@@ -45,6 +45,7 @@ _SIGS = {
     "ms_kv_append": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],
     "ms_kv_append_gqa": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P],
     "ms_rmsnorm": [_P, _I64, _P, _P, _F, _I, _I, _P, _I64, _P],
+    "ms_gated_silu": [_P, _I64, _I, _I, _P, _I64, _P],
     "ms_attention_gqa": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _F, _I, _P, _I64, _P, _I64,
                          _P, _I, _P],
     "ms_draft_commit": [_P, _P, _I, _I, _I, _I, _I, _P, _I64, _P, _F, ctypes.c_uint64, _P, _P, _P],

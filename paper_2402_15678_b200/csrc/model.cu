@@ -160,8 +160,33 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t 
   }
 }
 
+// Gated SiLU of a prefill gate/up GEMM's fp32 output (cuBLAS, 64-row
+// interleaved weight: output tile t = columns 128t..128t+63 gate, 128t+64..
+// 128t+127 up): out[m][64t + j] = bf16(silu(g) * u) — the same fp32 formula
+// and single rounding as ms_linear's gated epilogue.  One thread per 4 outputs
+// (16-byte gate / up loads, 8-byte store).
+__global__ void gated_silu_kernel(const float* __restrict__ gu, int64_t ldg, int M, int N2,
+                                  __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // quad index
+  const int qpr = N2 / 4;                                               // quads per row
+  if (q >= (int64_t)M * qpr) return;
+  const int m = (int)(q / qpr), o = (int)(q - (int64_t)m * qpr) * 4;  // output feature
+  const int t = o / 64, j = o - t * 64;
+  const float* row = gu + (int64_t)m * ldg + t * 128 + j;
+  const float4 g = *reinterpret_cast<const float4*>(row);
+  const float4 u = *reinterpret_cast<const float4*>(row + 64);
+  __nv_bfloat162 lo = __floats2bfloat162_rn(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
+  __nv_bfloat162 hi = __floats2bfloat162_rn(silu_mul(g.z, u.z), silu_mul(g.w, u.w));
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(out + (int64_t)m * ldo + o) = pk;
+}
+
 int preload_model() {
-  int n = preload_fn(embed_kernel) + preload_fn(kv_append_kernel);
+  int n = preload_fn(embed_kernel) + preload_fn(kv_append_kernel) + preload_fn(gated_silu_kernel);
   n += preload_fn(layernorm_kernel<1, false>) + preload_fn(layernorm_kernel<2, false>) +
        preload_fn(layernorm_kernel<3, false>) + preload_fn(layernorm_kernel<4, false>) +
        preload_fn(layernorm_kernel<5, false>) + preload_fn(layernorm_kernel<6, false>) +
@@ -227,6 +252,19 @@ extern "C" int ms_layernorm(const void* x, int64_t ldx, const int32_t* rows, con
 extern "C" int ms_rmsnorm(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, float eps,
                           int R, int d, void* out, int64_t ldo, void* stream) {
   return norm_launch<true>(x, ldx, rows, gamma, nullptr, eps, R, d, out, ldo, stream);
+}
+
+extern "C" int ms_gated_silu(const float* gu, int64_t ldg, int M, int N, void* out, int64_t ldo, void* stream) {
+  if (M < 0 || N < 0 || N % 128 || ldg < N || ldo < N / 2) return MS_ERR_VALUE;
+  if (M == 0 || N == 0) return MS_OK;
+  if (!gu || !out) return MS_ERR_VALUE;
+  if (ldg % 4 || ldo % 4 || (reinterpret_cast<uintptr_t>(gu) & 15) || (reinterpret_cast<uintptr_t>(out) & 7))
+    return MS_ERR_UNSUPPORTED;
+  const int64_t quads = (int64_t)M * (N / 8);
+  const int64_t blocks = (quads + 255) / 256;
+  if (blocks > 0x7fffffff) return MS_ERR_UNSUPPORTED;
+  return ms::launch(ms::gated_silu_kernel, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream, 1, gu, ldg, M,
+                    N / 2, (__nv_bfloat16*)out, ldo);
 }
 
 extern "C" int ms_rmsnorm_grouped(const void* x, int64_t ldx, const int32_t* rows, const void* gamma,

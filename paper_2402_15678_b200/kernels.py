@@ -74,6 +74,19 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     return out
 
 
+def gated_silu(gu: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """out [M, N/2] bf16 = silu(gate) * up of an fp32 gate/up GEMM output gu
+    [M, N] over the 64-row interleaved weight (ms_gated_silu: the act=2
+    epilogue of ms_linear, for prefill GEMMs run on cuBLAS)."""
+    M, N = gu.shape
+    if gu.dtype != torch.float32 or gu.stride(1) != 1 or out.dtype != BF16 or out.shape != (M, N // 2) \
+            or out.stride(1) != 1:
+        raise ValueError("gu [M, N] fp32 and out [M, N/2] bf16 with unit column stride")
+    _native.call("ms_gated_silu", gu.data_ptr(), gu.stride(0), M, N, out.data_ptr(), out.stride(0),
+                 _dev.stream_ptr(stream))
+    return out
+
+
 def linear_rms(x: torch.Tensor, w: torch.Tensor, *, residual: torch.Tensor | None = None, act: int = 0,
                out: torch.Tensor, out_f32: bool = False, rms_in: torch.Tensor | None = None, eps: float = 1e-5,
                rms_out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

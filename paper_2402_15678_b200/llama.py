@@ -312,14 +312,12 @@ def _prefill_linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residua
     """Prefill GEMM on cuBLAS (plain library GEMM, see LlamaModel): out =
     x @ w^T (+ residual, in place when out is residual) or, act=2, the gated
     SiLU of the 64-row interleaved gate/up weight from fp32 GEMM outputs
-    (fp32 silu * up, one bf16 rounding, as ms_linear's epilogue)."""
+    (fp32 silu * up, one bf16 rounding: ms_gated_silu, the same formula as
+    ms_linear's epilogue)."""
     with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
         if act == 2:
             gu = torch.mm(x, w.t(), out_dtype=torch.float32)
-            M, N = gu.shape
-            g4 = gu.view(M, N // 128, 2, 64)
-            out.copy_((torch.nn.functional.silu(g4[:, :, 0, :]) * g4[:, :, 1, :]).reshape(M, N // 2))
-            return out
+            return K.gated_silu(gu, out, stream=stream)
         if residual is not None:
             if out.data_ptr() == residual.data_ptr():
                 out.addmm_(x, w.t())

@@ -347,3 +347,17 @@ def test_folded_rmsnorm_matches_explicit_norm_and_reference():
     before = {k: v.clone() for k, v in wu.t.items()}
     wu.fold_norms()
     assert all(torch.equal(before[k], wu.t[k]) for k in before)
+
+
+@pytest.mark.parametrize("M,N", [(1, 128), (37, 1024), (4064, 57344 // 8)])
+def test_gated_silu_prefill_epilogue(M, N):
+    """ms_gated_silu (cuBLAS prefill gate/up GEMM epilogue) vs fp32 torch over
+    the 64-row interleaved layout: silu(g) * u, one bf16 rounding."""
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(M + N)
+    gu = (torch.randn(M, N, generator=g) * 4).cuda()
+    out = torch.empty(M, N // 2, dtype=torch.bfloat16, device="cuda")
+    Kn.gated_silu(gu, out)
+    g4 = gu.view(M, N // 128, 2, 64)
+    want = (torch.nn.functional.silu(g4[:, :, 0, :]) * g4[:, :, 1, :]).reshape(M, N // 2)
+    torch.testing.assert_close(out.float(), want, rtol=8e-3, atol=1e-5)
