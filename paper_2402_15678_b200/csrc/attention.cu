@@ -504,7 +504,8 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
                       const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                       int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
-                      int64_t ldo, KVPage pg) {
+                      int64_t ldo, int n_kv, int kct, float* __restrict__ ws, int* __restrict__ counters,
+                      KVPage pg) {
   using S = RowsSmem<D>;
   constexpr int LD = S::LD;
   constexpr int KC = D / 16;
@@ -522,7 +523,9 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int g = lane >> 2, t4 = lane & 3;
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
-  const int c0 = blockIdx.z * kRRows;         // first flattened row of the CTA
+  // blockIdx.z = (row chunk zr, cache-length chunk kvc of kct 64-key rounds)
+  const int zr = blockIdx.z / n_kv, kvc = blockIdx.z - zr * n_kv;
+  const int c0 = zr * kRRows;                 // first flattened row of the CTA
   const int crows = min(kRRows, rows_tot - c0);
   const int q0 = c0 + rw * 16;                // first row of this warp
   const int Q = max(0, min(16, rows_tot - q0));  // rows of this warp (0: idle)
@@ -541,7 +544,17 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   };
   const int QD = Hq * D, KVD = Hkv * D;
 
-  if (fuse_append && blockIdx.z == 0) {
+  // keys 0 .. the CTA's last position; split over the cache length: this CTA
+  // owns rounds [r0, r0 + kct) — fixed chunks from position 0, so a row's
+  // partition never depends on the other rows
+  const int n_keys = min(pstart + (c0 + crows - 1) / G + 1, T);
+  const int n_rounds_all = (n_keys + 2 * kRKT - 1) / (2 * kRKT);
+  const int n_chunks = (n_rounds_all + kct - 1) / kct;
+  if (kvc >= n_chunks) return;  // uniform per CTA (the unit's arrival count excludes it)
+  const int r0 = kvc * kct;
+  const int n_rounds = min(n_rounds_all, r0 + kct) - r0;
+
+  if (fuse_append && zr == 0 && kvc == 0) {
     for (int e = tid; e < 2 * Qtot * V8; e += kRThreads) {
       const int kv = e >= Qtot * V8;
       const int e2 = e - kv * Qtot * V8;
@@ -590,9 +603,6 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int fr0 = q0 + g, fr1 = q0 + g + 8;
   const bool v0 = g < Q, v1 = g + 8 < Q;
   const int pos0 = pstart + fr0 / G, pos1 = pstart + fr1 / G;
-  const int last_pos = pstart + (c0 + crows - 1) / G;
-  const int n_keys = min(last_pos + 1, T);
-  const int n_rounds = (n_keys + 2 * kRKT - 1) / (2 * kRKT);
   // keys every valid row of this warp sees (the warp's first row has the
   // smallest position): tiles below it need no causal mask
   const int warp_lim = pstart + q0 / G;
@@ -645,16 +655,16 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
 
 #pragma unroll
   for (int pp = 0; pp < kRNR - 1; ++pp) {
-    if (pp < n_rounds) load_round(pp, pp);
+    if (pp < n_rounds) load_round(r0 + pp, pp);
     else cp_async_commit();  // empty group: keeps the wait count uniform
   }
   for (int rd = 0; rd < n_rounds; ++rd) {
     const int rb = rd % kRNR;
-    if (rd + kRNR - 1 < n_rounds) load_round(rd + kRNR - 1, (rd + kRNR - 1) % kRNR);
+    if (rd + kRNR - 1 < n_rounds) load_round(r0 + rd + kRNR - 1, (rd + kRNR - 1) % kRNR);
     else cp_async_commit();
     cp_async_wait<kRNR - 1>();
     __syncthreads();  // (first round: also the query tile)
-    const int kbase = (rd * 2 + kg) * kRKT;
+    const int kbase = ((r0 + rd) * 2 + kg) * kRKT;
     if (Q > 0 && kbase < n_keys) {  // warp-uniform
       const __nv_bfloat16* kt = sKV + ((rb * 2 + kg) * 2) * S::TILE;
       const __nv_bfloat16* vt = kt + S::TILE;
@@ -787,31 +797,106 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
     }
   }
   __syncthreads();
-  if (kg == 1 || Q == 0) return;
-  float f0[2], f1[2];
+  float f0[2] = {0.f, 0.f}, f1[2] = {0.f, 0.f}, Lr[2] = {0.f, 0.f}, mr2[2] = {-INFINITY, -INFINITY};
+  if (kg == 0 && Q > 0) {
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const float* mr = mg + (g + 8 * r) * (D + 2);
-    const float m1 = mr[D], l1 = mr[D + 1];
-    const float m = fmaxf(m_r[r], m1);
-    const float a0 = m_r[r] == -INFINITY ? 0.f : exp2f(m_r[r] - m);
-    const float a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - m);
-    const float L = l_r[r] * a0 + l1 * a1;
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    f0[r] = a0 * inv;
-    f1[r] = a1 * inv;
+    for (int r = 0; r < 2; ++r) {
+      const float* mr = mg + (g + 8 * r) * (D + 2);
+      const float m1 = mr[D], l1 = mr[D + 1];
+      const float m = fmaxf(m_r[r], m1);
+      const float a0 = m_r[r] == -INFINITY ? 0.f : exp2f(m_r[r] - m);
+      const float a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - m);
+      const float L = l_r[r] * a0 + l1 * a1;
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      f0[r] = a0 * inv;
+      f1[r] = a1 * inv;
+      Lr[r] = L;
+      mr2[r] = m;
+    }
   }
-  __nv_bfloat16* o0p = out + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldo + (h * G + (v0 ? fr0 % G : 0)) * D;
-  __nv_bfloat16* o1p = out + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldo + (h * G + (v1 ? fr1 % G : 0)) * D;
+  if (ws == nullptr) {
+    if (kg == 1 || Q == 0) return;
+    __nv_bfloat16* o0p = out + (int64_t)(b * Qtot + (v0 ? fr0 / G : 0)) * ldo + (h * G + (v0 ? fr0 % G : 0)) * D;
+    __nv_bfloat16* o1p = out + (int64_t)(b * Qtot + (v1 ? fr1 / G : 0)) * ldo + (h * G + (v1 ? fr1 % G : 0)) * D;
 #pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int col = n * 8 + 2 * t4;
-    const float2 p0 = *reinterpret_cast<const float2*>(mg + g * (D + 2) + col);
-    const float2 p1 = *reinterpret_cast<const float2*>(mg + (g + 8) * (D + 2) + col);
-    if (v0) *reinterpret_cast<uint32_t*>(o0p + col) =
-        pack_bf16(o[n][0] * f0[0] + p0.x * f1[0], o[n][1] * f0[0] + p0.y * f1[0]);
-    if (v1) *reinterpret_cast<uint32_t*>(o1p + col) =
-        pack_bf16(o[n][2] * f0[1] + p1.x * f1[1], o[n][3] * f0[1] + p1.y * f1[1]);
+    for (int n = 0; n < NT; ++n) {
+      const int col = n * 8 + 2 * t4;
+      const float2 p0 = *reinterpret_cast<const float2*>(mg + g * (D + 2) + col);
+      const float2 p1 = *reinterpret_cast<const float2*>(mg + (g + 8) * (D + 2) + col);
+      if (v0) *reinterpret_cast<uint32_t*>(o0p + col) =
+          pack_bf16(o[n][0] * f0[0] + p0.x * f1[0], o[n][1] * f0[0] + p0.y * f1[0]);
+      if (v1) *reinterpret_cast<uint32_t*>(o1p + col) =
+          pack_bf16(o[n][2] * f0[1] + p1.x * f1[1], o[n][3] * f0[1] + p1.y * f1[1]);
+    }
+    return;
+  }
+  // split over the cache length: this chunk's record (m, L, A = O / L per
+  // row); with a workspace the chunk merge runs even for one chunk, so a
+  // row's output goes through the same arithmetic whatever its key count
+  constexpr int PS = kRRows * (D + 2);
+  const int nzr = gridDim.z / n_kv;
+  const int64_t unit = ((int64_t)b * Hkv + h) * nzr + zr;
+  float* rec = ws + (unit * n_kv + kvc) * PS;
+  if (kg == 0 && Q > 0) {
+    const int lr0 = rw * 16 + g, lr1 = lr0 + 8;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int col = n * 8 + 2 * t4;
+      const float2 p0 = *reinterpret_cast<const float2*>(mg + g * (D + 2) + col);
+      const float2 p1 = *reinterpret_cast<const float2*>(mg + (g + 8) * (D + 2) + col);
+      __stcg(reinterpret_cast<float2*>(rec + 2 * kRRows + lr0 * D + col),
+             make_float2(o[n][0] * f0[0] + p0.x * f1[0], o[n][1] * f0[0] + p0.y * f1[0]));
+      __stcg(reinterpret_cast<float2*>(rec + 2 * kRRows + lr1 * D + col),
+             make_float2(o[n][2] * f0[1] + p1.x * f1[1], o[n][3] * f0[1] + p1.y * f1[1]));
+    }
+    if (t4 == 0) {
+      __stcg(rec + lr0, mr2[0]);
+      __stcg(rec + lr1, mr2[1]);
+      __stcg(rec + kRRows + lr0, Lr[0]);
+      __stcg(rec + kRRows + lr1, Lr[1]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  if (tid == 0) {
+    const int old = atomicAdd(counters + unit, 1);
+    s_last = old == n_chunks - 1;
+    if (s_last) counters[unit] = 0;  // zero for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // the last chunk to finish merges all chunks in chunk order (deterministic):
+  // per-(chunk, row) weights L_c * 2^(m_c - max) and 1 / sum in shared memory
+  const float* recs = ws + unit * n_kv * PS;
+  float* wsm = reinterpret_cast<float*>(sKV);  // [8][kRRows] weights, [kRRows] 1 / sum
+  for (int r = tid; r < crows; r += kRThreads) {
+    float mx = -INFINITY;
+    for (int cc = 0; cc < n_chunks; ++cc) mx = fmaxf(mx, __ldcg(recs + cc * PS + r));
+    float L = 0.f;
+    for (int cc = 0; cc < n_chunks; ++cc) {
+      const float mc = __ldcg(recs + cc * PS + r);
+      const float wgt = mc == -INFINITY ? 0.f : __ldcg(recs + cc * PS + kRRows + r) * exp2f(mc - mx);
+      wsm[cc * kRRows + r] = wgt;
+      L += wgt;
+    }
+    wsm[8 * kRRows + r] = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
+  for (int e = tid; e < crows * (D / 2); e += kRThreads) {
+    const int r = e / (D / 2), d2 = (e - r * (D / 2)) * 2;
+    float ax = 0.f, ay = 0.f;
+    for (int cc = 0; cc < n_chunks; ++cc) {
+      const float wgt = wsm[cc * kRRows + r];
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(recs + cc * PS + 2 * kRRows + r * D + d2));
+      ax += wgt * v.x;
+      ay += wgt * v.y;
+    }
+    const float inv = wsm[8 * kRRows + r];
+    const int fr = c0 + r;
+    *reinterpret_cast<uint32_t*>(out + (int64_t)(b * Qtot + fr / G) * ldo + (h * G + fr % G) * D + d2) =
+        pack_bf16(ax * inv, ay * inv);
   }
 }
 
@@ -851,10 +936,19 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
   const bool paged = pg.table != nullptr;
   const float scale_log2 = scale * 1.4426950408889634f;
   if (Hkv < H) {  // grouped-query: row-split schedule (chosen by G, never by Q)
-    dim3 grid(B, Hkv, (Q * (H / Hkv) + kRRows - 1) / kRRows);
+    const int nzr = (Q * (H / Hkv) + kRRows - 1) / kRRows;
+    int n_kvr = 1, kctr = (T + kKT - 1) / kKT;  // default: one CTA walks all its rounds
+    if (ws) {  // split over the cache length: chunks of kv_chunk_tiles(T) 64-key rounds
+      kctr = kv_chunk_tiles(T);
+      n_kvr = ((T + kKT - 1) / kKT + kctr - 1) / kctr;
+      const int64_t need = (int64_t)B * Hkv * nzr * n_kvr * kRRows * (D + 2) * 4;
+      if (ws_bytes < need || n_counters < B * Hkv * nzr) return MS_ERR_VALUE;
+    }
+    dim3 grid(B, Hkv, nzr * n_kvr);
     return launch(paged ? attention_rows_kernel<D, true> : attention_rows_kernel<D, false>, grid,
                   dim3(kRThreads), SR::BYTES, st, 1, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
-                  (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, pg);
+                  (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, scale_log2, fuse, rope, (__nv_bfloat16*)out, ldo, n_kvr,
+                  kctr, ws, counters, pg);
   }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   int n_kv = 1, kct = (T + kKT - 1) / kKT;  // default: one CTA walks all its keys
@@ -889,10 +983,18 @@ extern "C" int ms_kv_append_paged(const void* qkv, int64_t ldq, int B, int Q, in
 
 extern "C" int ms_attention_workspace_gqa(int B, int Q, int H, int Hkv, int D, int T, int64_t* ws_bytes,
                                           int* n_counters) {
-  // split-KV scratch of the MHA kernel (the GQA row-split kernel has no
-  // split-KV path: measured 4x slower at decode contexts — the per-chunk
-  // records of 64 rows x D and the serial last-CTA merge outweigh the extra CTAs)
+  // split-KV scratch: MHA kernel (16-row query chunks) or, Hkv < H, the GQA
+  // row-split kernel (96-row records; worth it only for long caches — at
+  // decode contexts the records and the last-CTA merge outweigh the extra CTAs)
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || H % Hkv || T < 1) return MS_ERR_VALUE;
+  if (Hkv < H) {
+    const int nzr = (Q * (H / Hkv) + ms::kRRows - 1) / ms::kRRows;
+    const int kct = ms::kv_chunk_tiles(T);
+    const int n_kv = ((T + ms::kKT - 1) / ms::kKT + kct - 1) / kct;
+    if (ws_bytes) *ws_bytes = (int64_t)B * Hkv * nzr * n_kv * ms::kRRows * (D + 2) * 4;
+    if (n_counters) *n_counters = B * Hkv * nzr;
+    return MS_OK;
+  }
   const int nqc = (Q * (H / Hkv) + 15) / 16;
   const int kct = ms::kv_chunk_tiles(T);
   const int n_kv = ((T + ms::kKT - 1) / ms::kKT + kct - 1) / kct;

@@ -211,17 +211,18 @@ class LlamaModel:
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
         self.ws = None
-        # split-KV attention (MHA kernel only; chunk size from the cache length,
-        # <= 8 chunks): for decode / verify calls (Q <= 16) against caches of
-        # >= 1024 positions — where one CTA per (request, head) would walk ~66
-        # tiles serially with few CTAs in flight (cfg5 at B = 16).  Never for
-        # prefill chunks (large per-shape scratch; the prefill path is shared by
-        # the greedy teacher and the speculative run, so losslessness holds).
-        # MS_SPLITKV=auto enables that rule, =1 forces it for every decode /
-        # verify call.
-        # Opt-in: measured no gain (cfg5 on one GPU: verify 31.7 vs 29.4 ms).
+        # split over the cache length (chunks fixed by the cache length, <= 8,
+        # merged in chunk order) for decode / verify calls (Q <= 16), never for
+        # prefill chunks (large per-shape scratch; the prefill path is shared
+        # by the greedy teacher and the speculative run, so losslessness
+        # holds).  Opt-in: MS_SPLITKV=auto (caches >= 1024 positions) or 1
+        # (every decode / verify call).  Measured no gain on either kernel: MHA
+        # (cfg5 on one GPU) verify 31.7 vs 29.4 ms; GQA row kernel (70B heads,
+        # tools/attn_ab.py with AB_WS=1) 151 vs 116 us at a 4K cache, Q = 5, and
+        # slower at every shorter cache — each extra CTA repeats the query
+        # staging, the first DRAM latency and a 50 KB record.
         env = os.environ.get("MS_SPLITKV", "0")
-        self.split_kv = c.n_kv_heads == c.n_heads and env in ("1", "auto")
+        self.split_kv = env in ("1", "auto")
         self.split_kv_min_len = 0 if env == "1" else 1024
         self._aws: dict = {}
 

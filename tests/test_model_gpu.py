@@ -184,11 +184,13 @@ def test_linear_ln_matches_layernorm_then_linear(M, N, K):
         assert torch.equal(got, Kn.linear_ln(x, gam, bet, w, b, 1e-5, act=act, out_f32=True))
 
 
-@pytest.mark.parametrize("D,H,Hkv,Q", [(128, 8, 8, 5), (64, 12, 12, 1), (64, 4, 4, 13)])
+@pytest.mark.parametrize("D,H,Hkv,Q", [(128, 8, 8, 5), (64, 12, 12, 1), (64, 4, 4, 13),
+                                      (128, 64, 8, 5), (128, 16, 2, 13), (64, 8, 2, 1)])
 def test_attention_split_kv_matches_and_is_batch_invariant(D, H, Hkv, Q):
-    """Split-KV (fixed 128-key chunks, chunk-order merge; the MHA kernel)
-    agrees with the single-CTA walk and, per query, does not depend on the
-    other queries."""
+    """Split over the cache length (chunks fixed by the cache length,
+    chunk-order merge; MHA kernel and, Hkv < H, the GQA row kernel) agrees
+    with the single-CTA walk and, per query, does not depend on the other
+    queries."""
     from paper_2402_15678_b200 import kernels as Kn
     B, T = 6, 512
     g = torch.Generator().manual_seed(D + Q + H)

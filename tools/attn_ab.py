@@ -4,7 +4,7 @@ device time per call (back-to-back launches over L distinct KV caches, like
 L layers, so K/V stream from HBM as in a forward) and the max |difference| of
 each build's output vs the first build's.
 usage: python tools/attn_ab.py lib_a.so lib_b.so ..."""
-import ctypes, sys
+import ctypes, os, sys
 import torch
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 P, I, I64, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
@@ -33,6 +33,12 @@ for ctx in (190, 1024, 4096):
         start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
         tab = rope_table(T, D)
         res, outs = [], []
+        wsb, wsc = None, None
+        if os.environ.get("AB_WS") == "1":  # split over the cache length (scratch sized by the last build)
+            b_, c_ = ctypes.c_int64(), ctypes.c_int()
+            libs[-1].ms_attention_workspace_gqa(B, Q, H, Hkv, D, T, ctypes.byref(b_), ctypes.byref(c_))
+            wsb = torch.empty(b_.value // 4 + 1, dtype=torch.float32, device="cuda")
+            wsc = torch.zeros(c_.value, dtype=torch.int32, device="cuda")
         for lib in libs:
             out = torch.zeros(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
 
@@ -40,7 +46,10 @@ for ctx in (190, 1024, 4096):
                 st = torch.cuda.current_stream().cuda_stream
                 assert lib.ms_attention_gqa(qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D, slot.data_ptr(),
                                             start.data_ptr(), T, kcs[i].data_ptr(), vcs[i].data_ptr(), tab.data_ptr(),
-                                            D ** -0.5, 1, out.data_ptr(), out.stride(0), None, 0, None, 0, st) == 0
+                                            D ** -0.5, 1, out.data_ptr(), out.stride(0),
+                                            None if wsb is None else wsb.data_ptr(), 0 if wsb is None else wsb.numel() * 4,
+                                            None if wsc is None else wsc.data_ptr(), 0 if wsc is None else wsc.numel(),
+                                            st) == 0
             for _ in range(3):
                 run()
             torch.cuda.synchronize()
