@@ -283,8 +283,12 @@ class SpecEngine:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.ssm_streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
-        self.draft_stream = torch.cuda.Stream(self.dev)
-        self.verify_stream = torch.cuda.Stream(self.dev)
+        # stream priorities for the pipelined schedule (CTA scheduling order when
+        # both streams' kernels wait for SM slots): equal by default;
+        # MS_VERIFY_PRIORITY=1 / MS_DRAFT_PRIORITY=1 raise one (A/B)
+        hi = lambda k: -1 if os.environ.get(k, "0") == "1" else 0  # noqa: E731
+        self.draft_stream = torch.cuda.Stream(self.dev, priority=hi("MS_DRAFT_PRIORITY"))
+        self.verify_stream = torch.cuda.Stream(self.dev, priority=hi("MS_VERIFY_PRIORITY"))
         self.requests: list[Request] = []
         self._run_t0 = None
 
