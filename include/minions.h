@@ -121,9 +121,13 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
  * not depend on M, because the work partition depends only on N and K):
  *  - M <= 256, splits == 0 and scratch given: persistent stream-K kernel (one
  *    CTA per SM, deep TMA pipeline, (tile, k-block) iterations split evenly
- *    over the SMs, partial tiles combined in k order by the last CTA of a
- *    tile).  Scratch: ws >= ms_linear_workspace() bytes, counters >=
- *    n_counters ints, zero on first use (every launch leaves them zero).
+ *    over the SMs).  With >= one 128-feature tile per SM (act 2 allowed) a
+ *    tile is split between at most two CTAs, which both store their fp32
+ *    partial; the second to arrive adds the other's (a + b, arrival-order
+ *    free) and runs the epilogue.  Smaller N (act 0/1 only): partial tiles
+ *    combined in k order by the last CTA of a tile.  Scratch: ws >=
+ *    ms_linear_workspace() bytes, counters >= n_counters ints, zero on first
+ *    use (every launch leaves them zero).
  *  - otherwise: one CTA per (128-feature tile, split); the `splits` CTAs of a
  *    tile (0 = ms_linear_splits(N, K), max 8) form a thread-block cluster and
  *    reduce through distributed shared memory.
