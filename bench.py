@@ -220,7 +220,7 @@ def roofline_verify(engine, rounds, peaks):
         peak, src = 6650.0, "fallback"
     traffic, tnote = None, None
     try:  # ncu --metrics dram__bytes_{read,write}.sum of one verify forward (profiles/)
-        with open(os.path.join(ROOT, "profiles", "r1h_verify_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r1n_verify_traffic.json")) as fh:
             tr = json.load(fh)
         if tr["model"] == c.name.split("/")[0] and vb == tr["B"] and not getattr(engine, "tp", False):
             traffic = tr["dram_bytes"]
