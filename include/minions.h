@@ -376,6 +376,33 @@ int ms_tp_argmax_local(const float* logits, int64_t ld, int R, int Vr, int v0, u
 int ms_tp_argmax_combine(const uint64_t* const* peer, int t, int R, const int* flags,
                          const int* epoch, int32_t* out, int* err, int early, void* stream);
 
+/* ---- fp32 verification mode (csrc/fp32.cu) ---------------------------------
+ * The model forward behind ModelOracle.next_dist (aggspec/oracles.py:19-26)
+ * with fp32 activations, fp32 KV cache and fp32 accumulation (weights: the
+ * same bf16 tensors).  north_star: "accepted token sequences and vote results
+ * bit-exact in the fp32 verification mode" — SpecEngine(precision="fp32")
+ * reproduces the reference engine (aggspec/engine.py:252-330) driven by fp32
+ * CPU oracles.  Plain SIMT kernels; every output depends only on its own row.
+ *   ms_embed_f32:     out [R, d] = tok_emb[tok] (+ pos_emb[pos + pos_offset]).
+ *   ms_norm_f32:      LayerNorm (rms = 0; two-pass mean / variance) or RMSNorm
+ *                     (rms = 1, beta unused) of x rows (rows[r] or r).
+ *   ms_linear_f32:    out = act(x . w^T + bias) (+ residual), x / out / residual
+ *                     fp32, w bf16 [N, K]; act 0 none, 1 ReLU, 2 gated SiLU over
+ *                     the 64-row interleaved gate/up weight (out [M, N/2]).
+ *   ms_attention_f32: KV append (K rotated when rope != NULL; fp32 caches
+ *                     [slots, Hkv, T, D]) + causal attention of the call's rows
+ *                     (H query heads over Hkv KV heads, D <= 128); scale_q = 1
+ *                     scales q before q.k (OPT), 0 scales the score (Llama). */
+int ms_embed_f32(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb,
+                 const void* pos_emb, int pos_offset, int R, int d, float* out, void* stream);
+int ms_norm_f32(const float* x, int64_t ldx, const int32_t* rows, const void* gamma, const void* beta,
+                float eps, int rms, int R, int d, float* out, int64_t ldo, void* stream);
+int ms_linear_f32(const float* x, int64_t ldx, const void* w, const void* bias, const float* residual,
+                  int64_t ldr, float* out, int64_t ldo, int M, int N, int K, int act, void* stream);
+int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
+                     const int32_t* slot, const int32_t* start, int T, float* k_cache, float* v_cache,
+                     const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,8 +27,12 @@ def _bf(x: torch.Tensor) -> torch.Tensor:
     return x.to(BF16).to(torch.float32)
 
 
-def rmsnorm(x, g, eps):
-    return _bf(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * g)
+def _id(x: torch.Tensor) -> torch.Tensor:
+    return x
+
+
+def rmsnorm(x, g, eps, rnd=_bf):
+    return rnd(x * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps) * g)
 
 
 def rope_table(max_pos: int, D: int, theta: float) -> torch.Tensor:
@@ -37,13 +41,13 @@ def rope_table(max_pos: int, D: int, theta: float) -> torch.Tensor:
     return torch.from_numpy(np.stack([np.cos(ang), np.sin(ang)], -1).astype(np.float32))
 
 
-def rope(x: torch.Tensor, pos: torch.Tensor, table: torch.Tensor) -> torch.Tensor:
+def rope(x: torch.Tensor, pos: torch.Tensor, table: torch.Tensor, rnd=_bf) -> torch.Tensor:
     """x [T, H, D] fp32 (bf16 values), rotate-half pairing, one bf16 rounding."""
     D = x.shape[-1]
     cs = table[pos]  # [T, D/2, 2]
     c, s = cs[..., 0][:, None, :], cs[..., 1][:, None, :]
     a, b = x[..., : D // 2], x[..., D // 2:]
-    return _bf(torch.cat([a * c - b * s, b * c + a * s], dim=-1))
+    return rnd(torch.cat([a * c - b * s, b * c + a * s], dim=-1))
 
 
 def split_gate_up(w_gu: torch.Tensor, ffn: int):
@@ -68,7 +72,8 @@ def rstd(x, eps):
     return torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
 
 
-def forward(w: dict, cfg, tokens, last_only: bool = False, fused_norm: bool = False) -> torch.Tensor:
+def forward(w: dict, cfg, tokens, last_only: bool = False, fused_norm: bool = False,
+            exact: bool = False) -> torch.Tensor:
     """Full causal forward of one sequence from position 0 (no cache).
     tokens [T] -> logits [T, V] fp32 (or [1, V]).
 
@@ -76,7 +81,13 @@ def forward(w: dict, cfg, tokens, last_only: bool = False, fused_norm: bool = Fa
     into the next projection; for every layer but the first the projection
     runs on the raw residual stream and its fp32 result is scaled by
     rstd(x) = rsqrt(mean(x^2) + eps), rounded once — no bf16 normalised
-    activation in between."""
+    activation in between.
+
+    exact=True: the fp32 verification-mode contract (paper_2402_15678_b200/
+    fp32.py) — no bf16 rounding point anywhere (explicit norms only)."""
+    if exact and fused_norm:
+        raise ValueError("the fp32 mode has explicit norms (fused_norm=False)")
+    rnd = _id if exact else _bf
     if fused_norm:
         w = fold(w, cfg)
     f32 = {k: v.float() for k, v in w.items()}
@@ -92,37 +103,37 @@ def forward(w: dict, cfg, tokens, last_only: bool = False, fused_norm: bool = Fa
     for i in range(cfg.n_layers):
         p = f"l{i}."
         if fused_norm and i > 0:
-            qkv = _bf((x @ f32[p + "w_qkv"].T) * rstd(x, cfg.eps))
+            qkv = rnd((x @ f32[p + "w_qkv"].T) * rstd(x, cfg.eps))
         else:
-            h = rmsnorm(x, f32[p + "attn_norm"], cfg.eps)
-            qkv = _bf(h @ f32[p + "w_qkv"].T)
-        q = rope(qkv[:, : H * D].view(T, H, D), pos, table)
-        k = rope(qkv[:, H * D: (H + Hkv) * D].view(T, Hkv, D), pos, table)
+            h = rmsnorm(x, f32[p + "attn_norm"], cfg.eps, rnd)
+            qkv = rnd(h @ f32[p + "w_qkv"].T)
+        q = rope(qkv[:, : H * D].view(T, H, D), pos, table, rnd)
+        k = rope(qkv[:, H * D: (H + Hkv) * D].view(T, Hkv, D), pos, table, rnd)
         v = qkv[:, (H + Hkv) * D:].view(T, Hkv, D)
         k = k.repeat_interleave(G, dim=1)  # query head h reads KV head h // G
         v = v.repeat_interleave(G, dim=1)
         sc = (q.transpose(0, 1) @ k.transpose(0, 1).transpose(1, 2)) * scale
         sc = sc.masked_fill(mask, float("-inf"))
-        a = _bf((torch.softmax(sc, dim=-1) @ v.transpose(0, 1)).transpose(0, 1).reshape(T, H * D))
-        x = _bf(a @ f32[p + "w_o"].T + x)
+        a = rnd((torch.softmax(sc, dim=-1) @ v.transpose(0, 1)).transpose(0, 1).reshape(T, H * D))
+        x = rnd(a @ f32[p + "w_o"].T + x)
         wg, wu = split_gate_up(f32[p + "w_gu"], cfg.ffn)
         if fused_norm:
             r = rstd(x, cfg.eps)
             gt, up = (x @ wg.T) * r, (x @ wu.T) * r
         else:
-            h = rmsnorm(x, f32[p + "mlp_norm"], cfg.eps)
+            h = rmsnorm(x, f32[p + "mlp_norm"], cfg.eps, rnd)
             gt, up = h @ wg.T, h @ wu.T
-        ff = _bf(gt / (1.0 + torch.exp(-gt)) * up)
-        x = _bf(ff @ f32[p + "w_down"].T + x)
+        ff = rnd(gt / (1.0 + torch.exp(-gt)) * up)
+        x = rnd(ff @ f32[p + "w_down"].T + x)
     if last_only:
         x = x[-1:]
     if fused_norm:
         return (x @ f32["lm_head"].T) * rstd(x, cfg.eps)
-    return rmsnorm(x, f32["norm_f"], cfg.eps) @ f32["lm_head"].T
+    return rmsnorm(x, f32["norm_f"], cfg.eps, rnd) @ f32["lm_head"].T
 
 
-def greedy_generate(w, cfg, prompt, n_new: int, fused_norm: bool = False) -> list[int]:
+def greedy_generate(w, cfg, prompt, n_new: int, fused_norm: bool = False, exact: bool = False) -> list[int]:
     ctx = list(prompt)
     for _ in range(n_new):
-        ctx.append(int(torch.argmax(forward(w, cfg, ctx, last_only=True, fused_norm=fused_norm)[-1])))
+        ctx.append(int(torch.argmax(forward(w, cfg, ctx, last_only=True, fused_norm=fused_norm, exact=exact)[-1])))
     return ctx[len(prompt):]

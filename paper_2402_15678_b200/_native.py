@@ -51,6 +51,10 @@ _SIGS = {
     "ms_draft_commit": [_P, _P, _I, _I, _I, _I, _I, _P, _I64, _P, _F, ctypes.c_uint64, _P, _P, _P],
     "ms_pack_verify": [_P, _P, _I, _I, _P, _P],
     "ms_attention": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _F, _I, _P, _I64, _P, _I64, _P, _I, _P],
+    "ms_embed_f32": [_P, _P, _I, _P, _P, _I, _I, _I, _P, _P],
+    "ms_norm_f32": [_P, _I64, _P, _P, _P, _F, _I, _I, _I, _P, _I64, _P],
+    "ms_linear_f32": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _P],
+    "ms_attention_f32": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _F, _I, _P, _I64, _P],
     "ms_ipc_alloc": [_I64, ctypes.POINTER(ctypes.c_void_p), _P],
     "ms_ipc_handle_size": [],
     "ms_ipc_open": [_P, ctypes.POINTER(ctypes.c_void_p)],

@@ -185,6 +185,7 @@ class _Group:
         self.ctx: list[list[int]] = []
         self.ssm_cached: list[list[int]] = []
         self.pending = None  # (s, qc, active, t_start) of drafts awaiting verification
+        self.prev_states: list = []  # request states before the pending draft (discard)
 
     @staticmethod
     def _packed(sizes, dev):
@@ -212,7 +213,8 @@ class SpecEngine:
                  slots: int, max_len: int, device="cuda", use_graphs: bool = True,
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
                  record: bool = False, pipelined: bool = False, sync_time=None,
-                 kv_block_size: int = 0, kv_blocks: int | None = None):
+                 kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
+                 selector_time: str = "verify", sim_cost=None):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -221,8 +223,28 @@ class SpecEngine:
         kv_block_size > 0: the verifier's KV cache is paged (paged.PagedKVCache,
         kv_blocks pool blocks; default = slots x max_len worth): blocks are
         grown before each round and the blocks past the accepted length —
-        the KV of rejected speculative tokens — are freed after it."""
+        the KV of rejected speculative tokens — are freed after it.
+        precision "fp32": the fp32 verification mode (fp32.py) — every model
+        runs with fp32 activations and an fp32 KV cache; the parity mode
+        against the reference engine driven by fp32 oracles.
+        selector_time: what MonitorSample.t_llm gets — "verify" (default, as
+        the reference: the verify's device time, aggspec/engine.py:322),
+        "round" (verify + draft device time: the sequential schedule's round
+        period).  sim_cost: an object with t_llm(b, s) -> ms (the reference's
+        CostModel, aggspec/oracles.py:157-183); when given the selector is fed
+        t_llm(len(batch), s) exactly as the reference's simulated clock does,
+        which makes the s trajectory reproducible across runs (parity tests)."""
         validate_config(cfg)
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
+        if selector_time not in ("verify", "round"):
+            raise ValueError("selector_time must be 'verify' or 'round'")
+        if precision == "fp32" and kv_block_size > 0:
+            raise ValueError("the fp32 verification mode uses a contiguous KV cache")
+        self.precision = precision
+        self.selector_time = selector_time
+        self.sim_cost = sim_cost
+        kv_dtype = torch.float32 if precision == "fp32" else torch.bfloat16
         if len(cfg.initial_weights) != len(drafters):
             raise ValueError("initial_weights must have one entry per drafter")
         if pipelined and slots % 2:
@@ -241,7 +263,7 @@ class SpecEngine:
             self.target = target
         else:
             rows_t = max(slots * (s_cap + 1), slots * min(max_len, self.PREFILL_CHUNK))
-            self.target = make_model(target, max_rows=rows_t, device=device)
+            self.target = make_model(target, max_rows=rows_t, device=device, precision=precision)
         self.tp = hasattr(self.target, "comm")
         self.Vt = self.target.cfg.vocab                       # width of the target's logits
         V = self.Vt * (self.target.tp if self.tp else 1)      # full vocabulary
@@ -253,10 +275,10 @@ class SpecEngine:
         # (one launch per op for all drafters); MS_GROUPED_DRAFT=0 disables
         self.grouped = (len(drafters) > 1 and all(getattr(w.cfg, "family", "") == "llama" for w in drafters)
                         and all(w.cfg == drafters[0].cfg for w in drafters)
-                        and os.environ.get("MS_GROUPED_DRAFT", "1") != "0")
+                        and os.environ.get("MS_GROUPED_DRAFT", "1") != "0" and precision == "bf16")
         rows = slots * min(max_len, max(self.PREFILL_CHUNK, cfg.s_max + 2))
-        self.ssms = [] if self.grouped else [make_model(w, max_rows=rows, device=device, small_gemm=True)
-                                             for w in drafters]
+        self.ssms = [] if self.grouped else [make_model(w, max_rows=rows, device=device, small_gemm=True,
+                                                        precision=precision) for w in drafters]
         if self.grouped:
             self.ssm_g = GroupedLlamaModel(drafters, max_rows=rows, device=device)
             self.s_cache_g = KVCache(drafters[0].cfg, self.K * slots, max_len, device)
@@ -265,9 +287,10 @@ class SpecEngine:
             from .paged import PagedKVCache
             self.t_cache = PagedKVCache(self.target.cfg, slots, max_len, kv_block_size, kv_blocks, device)
         else:
-            self.t_cache = KVCache(self.target.cfg, slots, max_len, device)
+            self.t_cache = KVCache(self.target.cfg, slots, max_len, device, dtype=kv_dtype)
         self.paged = kv_block_size > 0
-        self.s_caches = [] if self.grouped else [KVCache(w.cfg, slots, max_len, device) for w in drafters]
+        self.s_caches = [] if self.grouped else [KVCache(w.cfg, slots, max_len, device, dtype=kv_dtype)
+                                                 for w in drafters]
         ng = 2 if pipelined else 1
         gb = slots // ng
         self.groups = [_Group(self, g, g * gb, gb) for g in range(ng)]
@@ -609,12 +632,26 @@ class SpecEngine:
         if not act:
             return False
         s = self.selector.current_s
+        g.prev_states = [g.requests[b].state for b in act]
         for b in act:
             g.requests[b].advance(RequestState.DRAFTING)
         qc = self._upload(g, s)
         self._launch_draft(g, s, qc)
         g.pending = (s, qc, act, time.perf_counter())
         return True
+
+    def _discard_draft(self, g: _Group) -> None:
+        """Drop a group's drafted-but-unverified round (decode stopped by
+        max_rounds while it was in flight): its requests go back to the state
+        they had before the draft, so the next decode() re-drafts them.  The
+        drafters' KV written by the discarded round lies past their cached
+        lengths (rollback arithmetic) and is simply overwritten later."""
+        if g.pending is None:
+            return
+        g.ev_d1.synchronize()
+        for b, st in zip(g.pending[2], g.prev_states):
+            g.requests[b].state = st
+        g.pending = None
 
     def _finish_verify(self, g: _Group, rnd: int) -> RoundStats:
         """Host bookkeeping of a verified group (reference semantics)."""
@@ -636,11 +673,14 @@ class SpecEngine:
         drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = g.ev_v0.elapsed_time(g.ev_v1)
         t_draft = g.ev_d0.elapsed_time(g.ev_d1)
-        # selector input (MonitorSample.t_llm): the verify's device time.  In the
-        # sequential single-GPU schedule the drafters do not overlap the
-        # verifier, so the round period the reference's pipelined assumption
-        # equates with t_llm is verify + draft; the selector gets that.
-        t_sel = t_verify if self.pipelined else t_verify + t_draft
+        # selector input (MonitorSample.t_llm): the verify's device time, as the
+        # reference (aggspec/engine.py:322); "round" adds the draft time (the
+        # sequential schedule's round period); sim_cost: the reference's
+        # simulated clock t_llm(len(batch), s) (aggspec/engine.py:359)
+        if self.sim_cost is not None:
+            t_sel = float(self.sim_cost.t_llm(len(active), s))
+        else:
+            t_sel = t_verify + (t_draft if self.selector_time == "round" else 0.0)
         if self.sync_time is not None:
             t_sel = float(self.sync_time(t_sel))
         accs, ems, vts = [], [], []
@@ -748,6 +788,8 @@ class SpecEngine:
                 res.rounds.append(self._finish_verify(cur, rnd))
                 rnd += 1
                 cur, nxt = nxt, cur
+            for g in self.groups:  # stopped by max_rounds with a draft in flight
+                self._discard_draft(g)
         torch.cuda.synchronize(self.dev)
         res.wall_s = time.perf_counter() - t0
         res.outputs = {r.id: list(r.generated) for r in self.requests}

@@ -20,113 +20,15 @@ from __future__ import annotations
 
 import math
 import os
-from dataclasses import dataclass
 
 import torch
 
 from . import kernels as K
 
+from .weights import KVCache, OPTConfig, OPTWeights  # noqa: F401
+from .weights import OPT_CONFIGS as CONFIGS  # noqa: F401
+
 BF16 = torch.bfloat16
-
-
-@dataclass(frozen=True)
-class OPTConfig:
-    name: str
-    n_layers: int
-    d: int
-    n_heads: int
-    ffn: int
-    vocab: int = 50272
-    max_pos: int = 2048
-    eps: float = 1e-5
-    pos_offset: int = 2  # OPT's learned-position offset
-
-    family = "opt"
-
-    @property
-    def head_dim(self) -> int:
-        return self.d // self.n_heads
-
-    @property
-    def n_kv_heads(self) -> int:
-        return self.n_heads
-
-    def matmul_params(self) -> int:
-        """Parameters streamed per forward (layers + tied LM head)."""
-        per_layer = 3 * self.d * self.d + self.d * self.d + 2 * self.d * self.ffn
-        return self.n_layers * per_layer + self.vocab * self.d
-
-    def kv_bytes_per_token(self) -> int:
-        return self.n_layers * 2 * self.d * 2
-
-
-CONFIGS = {
-    "opt-13b": OPTConfig("opt-13b", 40, 5120, 40, 20480),
-    "opt-125m": OPTConfig("opt-125m", 12, 768, 12, 3072),
-    # cfg1 of BASELINE.json: tiny OPT-style target and 1-layer drafters
-    "tiny-target": OPTConfig("tiny-target", 4, 256, 4, 1024),
-    "tiny-ssm": OPTConfig("tiny-ssm", 1, 256, 4, 1024),
-}
-
-
-class OPTWeights:
-    """Random-init weights (normal(0, 0.02) for Linear/Embedding, zero bias,
-    unit LayerNorm), generated with a seeded torch.Generator on `device`."""
-
-    def __init__(self, cfg: OPTConfig, tensors: dict[str, torch.Tensor]):
-        self.cfg = cfg
-        self.t = tensors
-
-    @classmethod
-    def random(cls, cfg: OPTConfig, seed: int, device="cuda", std: float = 0.02,
-               bias_std: float = 0.0) -> "OPTWeights":
-        g = torch.Generator(device=device).manual_seed(seed)
-        dev = torch.device(device)
-
-        def normal(*shape, s=std):
-            return (torch.randn(*shape, generator=g, device=dev, dtype=torch.float32) * s).to(BF16)
-
-        def bias(n):
-            return normal(n, s=bias_std) if bias_std > 0 else torch.zeros(n, dtype=BF16, device=dev)
-
-        d, f = cfg.d, cfg.ffn
-        t = {"tok_emb": normal(cfg.vocab, d), "pos_emb": normal(cfg.max_pos + cfg.pos_offset, d),
-             "lnf_g": torch.ones(d, dtype=BF16, device=dev), "lnf_b": torch.zeros(d, dtype=BF16, device=dev)}
-        for i in range(cfg.n_layers):
-            p = f"l{i}."
-            t[p + "ln1_g"] = torch.ones(d, dtype=BF16, device=dev)
-            t[p + "ln1_b"] = torch.zeros(d, dtype=BF16, device=dev)
-            t[p + "w_qkv"] = normal(3 * d, d)
-            t[p + "b_qkv"] = bias(3 * d)
-            t[p + "w_o"] = normal(d, d)
-            t[p + "b_o"] = bias(d)
-            t[p + "ln2_g"] = torch.ones(d, dtype=BF16, device=dev)
-            t[p + "ln2_b"] = torch.zeros(d, dtype=BF16, device=dev)
-            t[p + "w_fc1"] = normal(f, d)
-            t[p + "b_fc1"] = bias(f)
-            t[p + "w_fc2"] = normal(d, f)
-            t[p + "b_fc2"] = bias(d)
-        return cls(cfg, t)
-
-    def to(self, device) -> "OPTWeights":
-        return OPTWeights(self.cfg, {k: v.to(device) for k, v in self.t.items()})
-
-    def __getitem__(self, k: str) -> torch.Tensor:
-        return self.t[k]
-
-
-class KVCache:
-    """Per-layer K/V caches [slots, Hkv, T, D] bf16 (Hkv = KV heads: the query
-    heads for OPT, the grouped KV heads for Llama-2-70B)."""
-
-    def __init__(self, cfg, slots: int, max_len: int, device="cuda"):
-        shape = (slots, cfg.n_kv_heads, max_len, cfg.head_dim)
-        self.k = [torch.zeros(shape, dtype=BF16, device=device) for _ in range(cfg.n_layers)]
-        self.v = [torch.zeros(shape, dtype=BF16, device=device) for _ in range(cfg.n_layers)]
-        self.slots, self.max_len = slots, max_len
-
-    def nbytes(self) -> int:
-        return sum(t.numel() * 2 for t in self.k + self.v)
 
 
 class OPTModel:
