@@ -111,6 +111,32 @@ def test_gqa_rope_attention(H, Hkv, D, Q, rope):
         torch.testing.assert_close(kcd[b, :, p0:p0 + Q].cpu().float().transpose(0, 1), kn, rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("H,Hkv,Q", [(64, 8, 5), (40, 40, 5), (64, 8, 1)], ids=["70b-heads", "13b-heads", "70b-q1"])
+def test_attention_long_context_vs_reference(H, Hkv, Q):
+    """cfg5-length contexts: a 4,160-position cache
+    (4K prompt + generation; the reference caps contexts at 4096,
+    aggspec/core.py:171) with the 70B (64 q / 8 kv heads) and 13B (40 / 40)
+    head shapes, D = 128, RoPE, vs the fp32 restatement.  Queries are scaled
+    x4 so the softmax is peaked (a flat softmax over 4K keys averages the
+    values down to ~0.02 and would hide errors under any absolute tolerance);
+    the bound is relative to the output's max magnitude."""
+    from paper_2402_15678_b200 import kernels as Kn
+    B, T, D = 2, 4160, 128
+    g = torch.Generator().manual_seed(H + Q)
+    kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
+    vc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
+    qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g)
+    qkv[:, : H * D] *= 4.0
+    qkv = qkv.to(BF)
+    start = torch.tensor([4096, 1999], dtype=torch.int32)
+    table = llama_ref.rope_table(T + 8, D, 10000.0)
+    got = Kn.attention(qkv.cuda(), B, Q, H, D, torch.arange(B, dtype=torch.int32).cuda(), start.cuda(), kc.cuda(),
+                       vc.cuda(), D ** -0.5, n_kv_heads=Hkv, rope=table.cuda()).cpu().float()
+    want = _ref_attention(qkv, kc, vc, start, B, Q, H, Hkv, D, table)
+    rel = (got - want).abs().max().item() / want.abs().max().item()
+    assert rel < 1e-2, rel
+
+
 def _tiny_llama(seed=0, name="tiny-llama"):
     from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
     cfg = CONFIGS[name]
