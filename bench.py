@@ -22,10 +22,13 @@ the same metric through the public API (SpecEngine.run) from host prompt
 lists, H2D of prompts + per-round metadata and D2H of per-round results
 inside the timed region, prompt prefill included.
 
---impl reference: the reference's CPU path (the oracle port: the aggspec
-round logic over the fp32 CPU model under the reference's ModelOracle
-protocol — a full forward per next_dist call, no KV cache) on a bounded
-sample, scaled to tokens/s.
+--impl reference: the reference's own CPU path, timed on the host cores —
+the UNMODIFIED reference engine (aggspec run_pipelined / run_sequential from
+baseline/_ref) driving fp32 CPU ModelOracles of the same model shapes, with
+the same fidelity injection (oracle/cpu_path.py).  A step is a bounded sample
+of the workload: --ref-requests request(s) of the bench's prompt set
+generating --ref-new-tokens tokens each, timed end to end by wall clock; no
+scaling or extrapolation.  The GPU arm's `cpu_baseline` is one such step.
 
 Multi-GPU (torchrun, N>1), --parallelism tp (default): the verifier is
 tensor parallel over the N ranks (Megatron split; the sums over ranks are
@@ -58,10 +61,37 @@ def workload(args) -> str:
     if args.target == "llama-2-70b":
         return (f"cfg3: Llama-2-70B target + {k}x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, "
                 f"adaptive s")
+    if args.preset == "cfg1":
+        return (f"cfg1: tiny OPT-style target (4L d256) + {k}x tiny 1L SSMs, batch {args.batch}, s={args.fixed_s}, "
+                f"greedy, {args.new_tokens} new tokens, no fidelity injection")
     if args.preset == "cfg5":
         return (f"cfg5 on one GPU: Llama-2-13B target + {k}x {args.ssm} SSMs, {args.prompt_len}-token prompts, "
                 f"bf16, verify batch {args.batch}, {sched}, adaptive s (KV-cache-bound verify)")
     return (f"{args.target} target + {k}x {args.ssm} SSMs, bf16, verify batch {args.batch}, {sched}, adaptive s")
+
+
+def data_note(args) -> str:
+    return "synthetic prompts, random-init weights" + (", fidelity-injected drafts" if args.fidelity else "")
+
+
+def bench_config(args, ws: int, tp: bool) -> dict:
+    """The workload description both arms print (same dict: same_config)."""
+    from paper_2402_15678_b200.weights import CONFIGS  # torch-only (no libminions)
+    tcfg = CONFIGS[args.target]
+    fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else None
+    K = len(fid) if fid else 3
+    n_req = args.batch * (2 if args.schedule == "pipelined" else 1)
+    return {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * K,
+            "global_batch": n_req * (1 if tp else ws), "schedule": args.schedule,
+            "prompt_len": args.prompt_len,
+            "new_tokens": args.new_tokens, "s_init": args.fixed_s or 4,
+            "s_range": [args.fixed_s] * 2 if args.fixed_s else [1, 12], "greedy": True,
+            "fidelity": fid,
+            "parallelism": (f"tp{ws}" if tp else "replicas") if ws > 1 else "single-gpu",
+            "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
+                   "streamed per verify)"),
+            "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
+            "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous"}
 
 
 def parse():
@@ -77,12 +107,21 @@ def parse():
     ap.add_argument("--new-tokens", type=int, default=128)
     ap.add_argument("--fidelity", default="0.9,0.85,0.8",
                     help="one per drafter (the drafter count is the number of values)")
-    ap.add_argument("--preset", default="", choices=["", "cfg2", "cfg5"],
-                    help="cfg2: OPT-13B + 3x OPT-125M, sequential; cfg5: Llama-2-13B + 5 drafters, 4K prompts "
+    ap.add_argument("--preset", default="", choices=["", "cfg1", "cfg2", "cfg5"],
+                    help="cfg1: the reference's own CPU-runnable case (tiny OPT 4L d256 + 3x 1L, B=4, s=4, "
+                         "64 new tokens, no fidelity injection; the reference arm runs it in full); "
+                         "cfg2: OPT-13B + 3x OPT-125M, sequential; cfg5: Llama-2-13B + 5 drafters, 4K prompts "
                          "(verify batch 16 x 2 pipelined groups on one GPU: B=64 needs ~218 GB of KV)")
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-layers", type=int, default=1)
+    ap.add_argument("--ref-requests", type=int, default=0,
+                    help="reference arm / cpu_baseline sample: requests per step (0: 1, cfg1: all)")
+    ap.add_argument("--ref-new-tokens", type=int, default=0,
+                    help="reference arm / cpu_baseline sample: new tokens per request per step "
+                         "(0: 4, cfg1: all)")
+    ap.add_argument("--fresh-steps", type=int, default=-1,
+                    help="extra timed steps with the selector and drafter weights reset per step "
+                         "(the reference's per-run semantics); -1 = min(steps, 3), 0 = skip")
     ap.add_argument("--fixed-s", type=int, default=0, help="disable the adaptive selector, use this s")
     ap.add_argument("--kv-block-size", type=int, default=0,
                     help="> 0: the verifier's KV cache is paged with this block size (paged.PagedKVCache)")
@@ -94,11 +133,17 @@ def parse():
                          "--batch, 2x requests in flight), verify of one overlapping drafting of the "
                          "other (aggspec/engine.py:494-576); sequential: one group, draft then verify")
     a = ap.parse_args()
-    if a.preset == "cfg2":
+    if a.preset == "cfg1":
+        a.target, a.ssm, a.schedule, a.batch = "tiny-target", "tiny-ssm", "sequential", 4
+        a.prompt_len, a.new_tokens, a.fixed_s, a.fidelity = 8, 64, 4, ""
+    elif a.preset == "cfg2":
         a.target, a.ssm, a.schedule = "opt-13b", "opt-125m", "sequential"
     elif a.preset == "cfg5":
         a.target, a.ssm, a.prompt_len = "llama-2-13b", "llama-160m", 4096
         a.fidelity = "0.9,0.85,0.8,0.75,0.7"
+    full = a.preset == "cfg1"
+    a.ref_requests = a.ref_requests or (a.batch if full else 1)
+    a.ref_new_tokens = a.ref_new_tokens or (a.new_tokens if full else 4)
     return a
 
 
@@ -253,7 +298,6 @@ def run_ours(args, rank, ws):
     pipelined = args.schedule == "pipelined"
     n_req = args.batch * (2 if pipelined else 1)
     tp = ws > 1 and args.parallelism == "tp"
-    note = None
     target = None
     sync = None
     if tp:
@@ -269,17 +313,17 @@ def run_ours(args, rank, ws):
         except Exception as e:  # e.g. no CUDA IPC / peer access between the GPUs
             err = f"{type(e).__name__}: {e}"
         ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
-        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)  # all ranks take the same branch
-        if int(ok.item()) == 1:
-            target = LlamaTPModel(random_shard(tcfg, rank, ws, 0), comm, max_rows=max_rows)
+        tdist.all_reduce(ok, op=tdist.ReduceOp.MIN)  # every rank fails together
+        if int(ok.item()) != 1:
+            # never a silent fallback to replicas: --parallelism tp was asked for
+            raise RuntimeError(f"tensor-parallel setup failed ({err or 'on a peer rank'}); "
+                               "rerun with --parallelism replicas for independent replicas")
+        target = LlamaTPModel(random_shard(tcfg, rank, ws, 0), comm, max_rows=max_rows)
 
-            def sync(ms):
-                v = torch.tensor([ms], dtype=torch.float64, device="cuda")
-                tdist.all_reduce(v, op=tdist.ReduceOp.MAX)
-                return float(v.item())
-        else:
-            tp = False
-            note = f"tensor parallel unavailable ({err or 'on a peer rank'}); ran replicas"
+        def sync(ms):
+            v = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(v, op=tdist.ReduceOp.MAX)
+            return float(v.item())
     if target is None:
         target = random_weights(tcfg, 0, device="cuda")
     drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
@@ -358,6 +402,32 @@ def run_ours(args, rank, ws):
            "d2h_bytes_per_step": int((eng.d2h_bytes - d0) / args.steps),
            "includes": "prompt H2D + prefill + decode + per-round H2D/D2H"}
 
+    # ---- fresh controllers: selector + drafter weights reset every step (the
+    # reference starts both from the config per run, aggspec/engine.py:209-210)
+    n_fresh = min(args.steps, 3) if args.fresh_steps < 0 else args.fresh_steps
+    fresh_out = None
+    if n_fresh > 0:
+        barrier(ws)
+        f_tok, f_t, f_acc = 0, 0.0, []
+        for _ in range(n_fresh):
+            rs = fresh(reqs)
+            eng.prefill(rs)
+            if teacher is not None:
+                eng.set_teacher(teacher)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            res = eng.decode(reset_controllers=True)
+            e1.record()
+            torch.cuda.synchronize()
+            f_t += e0.elapsed_time(e1) * 1e-3
+            f_tok += res.tokens
+            f_acc += [a for rd in res.rounds for a in rd.accepted]
+        f_t = max_over_ranks(f_t, ws)
+        fresh_out = {"value": round(f_tok * (1 if tp else ws) / f_t, 2), "unit": "tokens/s", "steps": n_fresh,
+                     "mean_accepted_length": round(float(np.mean(f_acc)), 4) if f_acc else 0.0,
+                     "note": "selector and drafter weights reset to the config at every step"}
+
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -368,18 +438,8 @@ def run_ours(args, rank, ws):
         "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic prompts, random-init weights, fidelity-injected drafts",
-        "config": {"workload": workload(args), "target": args.target, "ssms": [args.ssm] * K,
-                   "global_batch": n_req * (1 if tp else ws), "schedule": args.schedule,
-                   "prompt_len": args.prompt_len,
-                   "new_tokens": args.new_tokens, "s_init": 4, "s_range": [1, 12], "greedy": True,
-                   "fidelity": fid,
-                   "parallelism": (f"tp{ws}" if tp else "replicas") if ws > 1 else "single-gpu",
-                   "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
-                          "streamed per verify)"),
-                   "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
-                   "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous",
-                   "graphs": not args.no_graphs},
+        "data": data_note(args),
+        "config": bench_config(args, ws, tp),
         "mean_accepted_length": round(float(np.mean(acc)), 4) if acc else 0.0,
         "mean_emitted_per_round": round(float(np.mean(emt)), 4) if emt else 0.0,
         "rounds_per_step": round(len(rounds) / args.steps, 2),
@@ -391,102 +451,30 @@ def run_ours(args, rank, ws):
         "round_ms_mean": round(float(np.mean([rd.t_round_ms for rd in rounds])), 3),
         "roofline": roofline_verify(eng, rounds, peaks),
         "e2e": e2e,
+        "fresh_controllers": fresh_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "libminions": _native.LIB_PATH,
     }
-    if note:
-        out["parallelism_note"] = note
     return out
 
 
 # ---------------------------------------------------------------- CPU baseline
-def simulated_vl(args, s: int, rounds: int = 64) -> float:
-    """Mean emitted tokens per round of the reference round logic (oracle
-    vote + greedy verify) when drafter k proposes the target's token with
-    probability f_k (fidelity injection) and a random token otherwise."""
-    import numpy as np
-
-    from oracle import aggspec_oracle as O
-    fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else [0.0] * 3
-    from paper_2402_15678_b200.models import config
-    rng = np.random.default_rng(0)
-    V = config(args.target).vocab
-    em = []
-    for _ in range(rounds * args.batch):
-        tgt = rng.integers(0, V, size=s + 1)
-        drafts = np.stack([np.where(rng.random(s) < f, tgt[:s], rng.integers(0, V, size=s)) for f in fid])
-        path, _ = O.vote_one(drafts, np.ones(len(fid)))
-        acc, emitted, _ = O.verify_greedy_one(path, tgt)
-        em.append(len(emitted))
-    return float(np.mean(em))
-
-
-def cpu_baseline(args, vl: float | None = None, threads: int | None = None):
-    """The reference's CPU path on a bounded sample.
-
-    The reference's verify loop (aggspec/engine.py:294-296) and draft loop
-    (aggspec/oracles.py:146-150) call ModelOracle.next_dist once per position
-    with the full context — no KV cache — so one round costs
-    B*K*s drafter calls + B*(s+1) target calls.  We time one target call and
-    one drafter call of the fp32 CPU model (oracle/opt_ref.py) at the mean
-    context length of the run, with the target's layer count sampled
-    (`--cpu-sample-layers` layers timed, scaled to the full depth; weights of
-    one layer reused, which leaves the FLOP/byte count unchanged), plus the
-    reference-restated vote/verify logic, and scale to tokens/s with the
-    measured emitted tokens per round (vl)."""
-    import torch
-
-    import dataclasses
-
-    from oracle import aggspec_oracle as O
-    from oracle import llama_ref, opt_ref
-    from paper_2402_15678_b200.models import config, random_weights
-
-    n_thr = threads or len(os.sched_getaffinity(0))
-    torch.set_num_threads(n_thr)
-    tcfg, scfg = config(args.target), config(args.ssm)
-    L = min(args.cpu_sample_layers, tcfg.n_layers)
-    ctx = args.prompt_len + args.new_tokens // 2
-    s = 4
-    B = args.batch
-    K = 3
-
-    def call_time(cfg, layers: int) -> float:
-        sub = dataclasses.replace(cfg, n_layers=layers)
-        w = random_weights(sub, 0, device="cpu").t
-        ref = llama_ref if cfg.family == "llama" else opt_ref
-        toks = list(range(ctx))
-        ref.forward(w, sub, toks[:8], last_only=True)  # warm
-        t0 = time.perf_counter()
-        ref.forward(w, sub, toks, last_only=True)
-        t_full = time.perf_counter() - t0
-        return t_full
-
-    t_llm_sampled = call_time(tcfg, L)
-    # subtract-free scaling: time per layer from the sampled call (the embed +
-    # LM head share is counted once)
-    t_llm = t_llm_sampled * tcfg.n_layers / L
-    t_ssm = call_time(scfg, scfg.n_layers)
-    import numpy as np
-    rng = np.random.default_rng(0)
-    t0 = time.perf_counter()
-    for _ in range(B):
-        O.vote_one(rng.integers(0, 4, size=(K, s)), np.ones(K))
-        O.verify_greedy_one(rng.integers(0, 4, size=s), rng.integers(0, 4, size=s + 1))
-    t_logic = time.perf_counter() - t0
-    t_round = B * K * s * t_ssm + B * (s + 1) * t_llm + t_logic
-    vl_src = "measured on the GPU arm"
-    if vl is None:
-        vl = simulated_vl(args, s)
-        vl_src = "simulated with the oracle vote/verify under the same fidelity injection"
-    value = B * vl / t_round
-    return {"value": value, "unit": "tokens/s", "cores": n_thr, "kind": "port",
-            "sample": (f"one {tcfg.name} next_dist call at ctx {ctx} with {L}/{tcfg.n_layers} layers "
-                       f"timed ({t_llm_sampled:.2f}s, scaled x{tcfg.n_layers / L:.0f}), one {scfg.name} "
-                       f"call ({t_ssm:.2f}s), round = B*K*s drafter + B*(s+1) target calls (s=4, B={B}) "
-                       f"+ vote/verify logic; tokens/round = B*vl, vl={vl:.3f} ({vl_src})"),
-            "t_round_s": t_round}
+def cpu_reference(args, steps: int, warmup: int) -> dict:
+    """The reference's CPU path on a bounded sample of this workload
+    (oracle/cpu_path.py): complete runs of the unmodified reference engine
+    over fp32 CPU ModelOracles, wall clock, all host threads.  Never scaled.
+    Prompts of more than 1,024 tokens (cfg5) are not sampled: their CPU
+    prefill alone is minutes per request."""
+    if args.prompt_len > 1024:
+        return {"value": None, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "reference",
+                "sample": f"n/a: {args.prompt_len}-token prompts do not prefill on the CPU in a bounded sample"}
+    from oracle.cpu_path import reference_run
+    fid = [float(x) for x in args.fidelity.split(",")] if args.fidelity else [0.0, 0.0, 0.0]
+    r = reference_run(args.target, args.ssm, fid, args.ref_requests, args.prompt_len, args.ref_new_tokens,
+                      args.schedule, steps, warmup, s_init=args.fixed_s or 4, adaptive=not args.fixed_s,
+                      log=lambda m: print(m, file=sys.stderr, flush=True))
+    return r
 
 
 def main():
@@ -495,27 +483,33 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        cb = cpu_baseline(args, vl=None)
-        line = {"metric": METRIC, "value": round(cb["value"], 6), "unit": "tokens/s", "n_gpus": args.gpus,
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        cb = cpu_reference(args, args.steps, args.warmup)
+        v = round(cb["value"], 6) if cb["value"] is not None else None
+        line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "scaling": "strong" if ws > 1 and args.parallelism == "tp" else "weak", "vs_baseline": None,
+                "dtype": "f32", "data": data_note(args),
                 "impl": "reference",
-                "config": {"workload": workload(args), "target": args.target,
-                           "ssms": [args.ssm] * (len(args.fidelity.split(",")) if args.fidelity else 3),
-                           "global_batch": args.batch * (2 if args.schedule == "pipelined" else 1),
-                           "schedule": args.schedule},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": round(cb["value"], 6), "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
+                "config": bench_config(args, ws, ws > 1 and args.parallelism == "tp"),
+                "mean_accepted_length": round(cb.get("mean_accepted_length", 0.0), 4),
+                "lossless_vs_greedy": cb.get("lossless_vs_greedy"),
+                "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cb["cores"], "kind": cb["kind"],
+                                 "sample": cb["sample"]},
+                "reference_detail": {k: cb[k] for k in ("step_s", "setup_s", "oracle_calls_per_step",
+                                                        "shared_layers", "reference_src") if k in cb},
+                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
     rank, ws, local = dist_init()
     out = run_ours(args, rank, ws)
     if rank == 0:
-        if not args.no_cpu_baseline:
-            cb = cpu_baseline(args, vl=out["mean_emitted_per_round"])
-            out["cpu_baseline"] = {k: (round(v, 6) if isinstance(v, float) else v)
-                                   for k, v in cb.items() if k != "t_round_s"}
+        if not args.no_cpu_baseline and ws == 1:
+            cb = cpu_reference(args, steps=1, warmup=0)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if cb["value"] is not None:
+                out["cpu_baseline"]["value"] = round(cb["value"], 6)
+                out["cpu_baseline"]["mean_accepted_length"] = round(cb["mean_accepted_length"], 4)
         print(json.dumps(out))
     if ws > 1:
         import torch.distributed as dist

@@ -161,8 +161,12 @@ accept_stochastic_kernel(const int32_t* __restrict__ draft, const double* __rest
     int i = 0;
     for (; i < S; ++i) {
       const int tok = d[i];
-      const double qq = qb[(int64_t)i * V + tok];
-      const double oo = ob[(int64_t)i * V + tok];
+      // a token outside [0, V) never reads out of bounds: it carries no
+      // probability on either side (the host API raises IndexError first,
+      // as the reference's probs[tok] does)
+      const bool in = tok >= 0 && tok < V;
+      const double qq = in ? qb[(int64_t)i * V + tok] : 0.0;
+      const double oo = in ? ob[(int64_t)i * V + tok] : 0.0;
       if (qq <= oo) continue;
       if (ub[i] >= 1.0 - oo / qq) continue;
       break;

@@ -164,6 +164,9 @@ def verify(draft_tokens: Sequence[int], draft_dists: Sequence[ProbDist],
     V = draft_dists[0].vocab_size
     if any(d.vocab_size != V for d in (*draft_dists, *target_dists)):
         raise DistMismatch("draft and target distributions must share a vocabulary")
+    # the reference reads probs.item(tok): negative tokens wrap, tokens outside
+    # [-V, V) raise IndexError when (and only if) verification reaches them
+    bad = next((i for i, t in enumerate(draft_tokens) if not -V <= int(t) < V), s)
     q_tok = [d.point_mass_token() for d in draft_dists]
     o_tok = [d.point_mass_token() for d in target_dists]
     dev = _dev.require_cuda()
@@ -179,12 +182,17 @@ def verify(draft_tokens: Sequence[int], draft_dists: Sequence[ProbDist],
         rng.random(acc + 2 if acc < s else s + 1)  # uniforms the reference consumes
         return VerificationResult(acc, emitted, acc / s)
     # general speculative sampling (K10), bit-exact on the same fp64 dists / uniforms
+    wrapped = [int(t) % V if -V <= int(t) < 0 else int(t) for t in draft_tokens]
+    draft = torch.tensor([wrapped], dtype=torch.int32, device=dev)  # out-of-range: no probability
     qd = torch.from_numpy(np.stack([d.probs for d in draft_dists])[None]).to(dev)
     od = torch.from_numpy(np.stack([d.probs for d in target_dists])[None]).to(dev)
     u = torch.from_numpy(peek_uniforms(rng, s + 1)[None]).to(dev)
     o, n_draws = accept_batch_stochastic(draft, qd, od, u, rem)
     acc = int(o.n_acc[0])
-    emitted = o.emitted[0, : acc + 1].tolist()
+    if acc >= bad < s:  # positions before `bad` all accepted: the reference reaches it
+        rng.random(bad)
+        raise IndexError(f"draft token {int(draft_tokens[bad])} outside the vocabulary of size {V}")
+    emitted = list(draft_tokens[:acc]) + [int(o.emitted[0, acc])]
     rng.random(int(n_draws[0]))  # advance the stream exactly as the reference did
     return VerificationResult(acc, emitted, acc / s)
 

@@ -185,3 +185,37 @@ def test_stochastic_pairwise_sum_is_numpy():
         assert out.emitted[0, : acc + 1].tolist() == em
         hits += int(acc == 0)
     assert hits > 10
+
+
+def test_verify_out_of_vocab_draft_token_like_reference():
+    """aggspec/verification.py:58-60 reads probs.item(tok): a token outside
+    [-V, V) raises IndexError when verification reaches it (after consuming
+    one uniform per earlier position), never when an earlier position
+    rejects; a negative token wraps.  The device never reads out of bounds."""
+    from paper_2402_15678_b200 import ProbDist, verify
+    V, s = 7, 4
+    o = [ProbDist(np.full(V, 1.0 / V)) for _ in range(s + 1)]
+    low = np.full(V, 0.5 / (V - 1))
+    low[3] = 0.5  # q(3) = 0.5 > o(3): rejection possible at a draft token 3
+    q_acc = [ProbDist(np.full(V, 1.0 / V)) for _ in range(s)]  # q == o: always accepted
+    rng = np.random.default_rng(5)
+    with pytest.raises(IndexError):
+        verify([1, 2, V + 3, 4], q_acc, o, rng)
+    ref = np.random.default_rng(5)
+    ref.random(2)
+    assert rng.random() == ref.random()  # two draws consumed before the error
+    # rejection before the bad token: no error
+    rng = np.random.default_rng(0)
+    while True:  # find a stream whose first uniform rejects token 3 at q=0.5, o=1/7
+        st = rng.bit_generator.state
+        u0 = rng.random()
+        rng.bit_generator.state = st
+        if u0 < 1.0 - (1.0 / V) / 0.5:
+            break
+        rng.random()
+    q_rej = [ProbDist(low)] + q_acc[1:]
+    res = verify([3, 2, -100, 4], q_rej, o, rng)
+    assert res.accepted_count == 0 and len(res.emitted) == 1
+    # a negative token wraps (probs.item(-1) == probs[V-1]) and is emitted as given
+    res = verify([-1, 2], q_acc[:2], o[:3], np.random.default_rng(1))
+    assert res.accepted_count == 2 and res.emitted[:2] == [-1, 2]

@@ -43,3 +43,35 @@ def test_roofline_fallback_peak_and_traffic_match():
     assert r["traffic"] is not None  # profiles/r1h_verify_traffic.json: 70B, verify batch 16
     r8 = bench.roofline_verify(_engine(8), [_round(4, 190, 8, 30.0)], {})
     assert r8["traffic"] is None  # captured at B = 16 only
+
+
+def test_reference_arm_is_the_reference_engine_without_libminions():
+    """--impl reference runs the unmodified reference engine (baseline/_ref or
+    the reference tree) over fp32 CPU oracles, prints the same config dict as
+    the GPU arm, and never maps libminions.so (the old arm did)."""
+    import json
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--preset', 'cfg1', "
+            "'--ref-requests', '2', '--ref-new-tokens', '6', '--steps', '1', '--warmup', '0']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "print('MAPPED', open('/proc/self/maps').read().count('libminions'))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.strip().splitlines()
+    assert lines[-1] == "MAPPED 0"
+    line = json.loads(lines[-2])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and "no scaling" in line["cpu_baseline"]["sample"]
+    assert line["lossless_vs_greedy"] is True
+    args = types.SimpleNamespace(target="tiny-target", ssm="tiny-ssm", fidelity="", batch=4, schedule="sequential",
+                                 prompt_len=8, new_tokens=64, fixed_s=4, kv_block_size=0, preset="cfg1")
+    assert line["config"] == bench.bench_config(args, 1, False)
+
+
+def test_fidelity_hash_matches_device_formula():
+    """oracle/cpu_path.inject_u restates csrc/spec.cu's draft_commit hash."""
+    from oracle.cpu_path import inject_u, request_key
+    u = [inject_u(0, request_key("req-000"), k, p) for k in range(3) for p in range(128, 160)]
+    assert all(0.0 <= x < 1.0 for x in u)
+    assert 0.35 < sum(x < 0.5 for x in u) / len(u) < 0.65
