@@ -319,11 +319,8 @@ def run_ours(args, rank, ws):
             raise RuntimeError(f"tensor-parallel setup failed ({err or 'on a peer rank'}); "
                                "rerun with --parallelism replicas for independent replicas")
         target = LlamaTPModel(random_shard(tcfg, rank, ws, 0), comm, max_rows=max_rows)
-
-        def sync(ms):
-            v = torch.tensor([ms], dtype=torch.float64, device="cuda")
-            tdist.all_reduce(v, op=tdist.ReduceOp.MAX)
-            return float(v.item())
+        from paper_2402_15678_b200.dist import sync_time_fn
+        sync = sync_time_fn("cuda")
     if target is None:
         target = random_weights(tcfg, 0, device="cuda")
     drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]

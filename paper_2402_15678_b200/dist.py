@@ -49,6 +49,19 @@ def sum_over_ranks(x: float, device="cpu") -> float:
     return _reduce(x, dist.ReduceOp.SUM if dist.is_available() else None, device)
 
 
+def sync_time_fn(device="cpu"):
+    """The tensor-parallel engine's `sync_time`: a rank's selector time ->
+    the max over ranks (fp64 all-reduce), so every rank feeds its selector
+    the same MonitorSample.t_llm and takes the same decisions (rounds.py)."""
+    import torch.distributed as dist
+
+    def sync(ms: float) -> float:
+        t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return sync
+
+
 def barrier() -> None:
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:

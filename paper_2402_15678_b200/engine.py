@@ -53,9 +53,10 @@ import os
 from .llama import GroupedLlamaModel
 from .models import make_model
 from .opt import KVCache
-from .selector import Decision, MonitorSample, SelectorState, maybe_adjust, observe
+from .rounds import NoProgress, commit_round  # noqa: F401  (NoProgress: public name)
+from .selector import SelectorState
 from .verification import AcceptOut
-from .voting import WeightTable, record_acr, update_weights
+from .voting import WeightTable
 
 I32 = torch.int32
 
@@ -65,10 +66,6 @@ class EngineFinished(AggSpecError):  # aggspec/engine.py:37
 
 
 class DeadlockError(AggSpecError):  # aggspec/engine.py:41
-    pass
-
-
-class NoProgress(AggSpecError):  # aggspec/engine.py:44
     pass
 
 
@@ -683,48 +680,19 @@ class SpecEngine:
             t_sel = t_verify + (t_draft if self.selector_time == "round" else 0.0)
         if self.sync_time is not None:
             t_sel = float(self.sync_time(t_sel))
-        accs, ems, vts = [], [], []
         t0 = self._run_t0
         ts = (t0.elapsed_time(g.ev_d0), t0.elapsed_time(g.ev_d1), t0.elapsed_time(g.ev_v0),
               t0.elapsed_time(g.ev_v1)) if t0 is not None else (None,) * 4
-        for b in active:
-            r = g.requests[b]
-            r.advance(RequestState.AWAITING_VERIFICATION)
-            acc = int(n_acc[b])
-            use = [int(t) for t in emitted[b, : n_emit[b]]]
-            record_acr(self.weights, int(voted[b]), acc / s)
-            if len(use) == 0:
-                raise NoProgress(f"request {r.id} made no progress")
-            len_before = len(g.ctx[b])
-            r.generated.extend(use)
-            g.ctx[b].extend(use)
-            stopped = self.cfg.stop_token is not None and self.cfg.stop_token in use
-            if stopped or r.remaining <= 0:
-                r.advance(RequestState.FINISHED)
-                r.finish_time = ts[3] if ts[3] is not None else time.perf_counter()  # device ms
-            else:
-                r.advance(RequestState.RUNNING)
-            if self.paged:  # free blocks holding only rejected tokens' KV (or all, when finished)
-                if r.state == RequestState.FINISHED:
+        out = commit_round(g.requests, g.ctx, g.ssm_cached, active, s, n_acc, n_emit, emitted, voted, drafts,
+                           self.weights, self.selector, self.cfg, t_sel, rnd, self.adaptive,
+                           finish_time=ts[3] if ts[3] is not None else time.perf_counter())  # device ms
+        if self.paged:  # free blocks holding only rejected tokens' KV (or all, when finished)
+            for b in active:
+                if g.requests[b].state == RequestState.FINISHED:
                     self.t_cache.mgr.release(g.slot0 + b)
                 else:
                     self.t_cache.mgr.truncate(g.slot0 + b, len(g.ctx[b]))
-            # SSM rollback: valid up to the longest prefix agreement with `use`
-            for k in range(self.K):
-                mlen = 0
-                lim = min(s - 1, len(use) - 1)  # the last context token is always re-fed
-                while mlen < lim and drafts[b, k, mlen] == use[mlen]:
-                    mlen += 1
-                g.ssm_cached[k][b] = len_before + mlen
-            accs.append(acc)
-            ems.append(len(use))
-            vts.append(int(voted[b]))
-        update_weights(self.weights, self.cfg)
-        vl = float(np.mean(ems)) if ems else 1.0
-        observe(self.selector, MonitorSample(round_index=rnd, t_llm=t_sel, vl=vl, s_used=s))
-        decision = Decision.HOLD
-        if self.adaptive:
-            _, decision = maybe_adjust(self.selector)
+        accs, ems, vts, vl, decision = out.accepted, out.emitted, out.voted, out.vl, out.decision
         trace = None
         if self.record:
             trace = dict(active=active, drafts=drafts.copy(), weights_used=g.w_dev.cpu().numpy(),
