@@ -79,6 +79,10 @@ struct LinearParams {
   const __nv_bfloat16* ln_x;
   int64_t ldx;
   float ln_eps;
+  // weight layout: 0 = nn.Linear row-major [G*N, K]; 1 = tile-blocked
+  // [G][N/128][K/64][128][64] (every 128 x 64 weight tile one contiguous 16 KB
+  // run — TMA coordinate (0, ((grp * n_tiles + tile) * kb_total + kb) * 128))
+  int w_blocked;
 };
 
 constexpr int kBM = 128;  // output features per CTA (MMA M)
@@ -256,9 +260,14 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       // kernel — issued before the programmatic-dependency wait (PDL prefetch)
       const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
       const int pre = nkb < SW ? nkb : SW;
+      // blocked layout: the tile's k-block run starts at row wblk
+      const int wblk = ((grp * p.n_tiles + tile_n) * p.kb_total + kb0) * kBM;
       for (int i = 0; i < pre; ++i) {
         tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
-        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
+        if (p.w_blocked)
+          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], 0, wblk + i * kBM, pol_w);
+        else
+          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
       }
       pdl_wait();
       pdl_trigger();
@@ -266,7 +275,10 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         const int st = i % SW;
         tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
-        tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
+        if (p.w_blocked)
+          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], 0, wblk + i * kBM, pol_w);
+        else
+          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
       }
     } else {
       pdl_trigger();
@@ -1479,7 +1491,12 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
   CUtensorMap tw, tx;
   if (G < 1 || G > 65535 || (G > 1 && g_ln_g)) return MS_ERR_VALUE;
-  if (!make_tmap(&tw, w, (int64_t)G * N, K, K, kBM)) return MS_ERR_CUDA;
+  const char* wb_env = getenv("MS_EXP_WBLOCKED");  // experiment: w is tile-blocked (see LinearParams)
+  const int w_blocked = (wb_env && wb_env[0] == '1') ? 1 : 0;
+  if (w_blocked && (N % kBM || K % kBK)) return MS_ERR_UNSUPPORTED;
+  if (w_blocked ? !make_tmap(&tw, w, (int64_t)G * N * (K / kBK), kBK, kBK, kBM)
+                : !make_tmap(&tw, w, (int64_t)G * N, K, K, kBM))
+    return MS_ERR_CUDA;
   if (!make_tmap(&tx, x, (int64_t)G * M, K, ldx, bn)) return MS_ERR_CUDA;
   LinearParams p;
   p.M = M; p.N = N; p.K = K;
@@ -1492,6 +1509,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.tp_recv = nullptr; p.tp_rank = 0; p.tp_slice = 1; p.tp_rows = 0;
   p.sk_ws = nullptr; p.sk_cnt = nullptr;
   p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
+  p.w_blocked = w_blocked;
   if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
     p.ln_g = (const __nv_bfloat16*)g_ln_g;
     p.ln_b = (const __nv_bfloat16*)g_ln_b;
@@ -1504,7 +1522,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   const bool folded = rms.out || rms.in || rms.tp_recv;
   // weight-streaming GEMMs with at least one 128-feature tile per SM and a
   // workspace: the persistent stream-K schedule (equal weight bytes per SM)
-  const bool big = splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count();
+  const bool big = splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count() && !w_blocked;
   if (big && ws && counters && ws_bytes >= pk_ws_bytes(bn) && n_counters >= sm_count() + 1) {
     p.sk_ws = (float*)ws;
     p.sk_cnt = counters;
@@ -1529,7 +1547,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   }
   // decode / verify regime: persistent stream-K kernel when scratch is given
   const int g = linear_sk_grid(N, K);
-  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded &&
+  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded && !w_blocked &&
       ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
     SKParams sk;
     sk.iters = n_tiles * kb_total;
