@@ -117,26 +117,19 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
  *   gate and up projections interleaved in 64-row blocks (rows 128t..128t+63 =
  *   gate rows 64t.., rows 128t+64..128t+127 = up rows 64t..) and
  *   out [M, N/2] = silu(gate) * up, bf16, no bias / residual, N % 128 == 0.
- * Two schedules, both deterministic and batch invariant (a row's result does
- * not depend on M, because the work partition depends only on N and K):
- *  - M <= 256, splits == 0 and scratch given: persistent stream-K kernel (one
- *    CTA per SM, deep TMA pipeline, (tile, k-block) iterations split evenly
- *    over the SMs).  With >= one 128-feature tile per SM (act 2 allowed) a
- *    tile is split between at most two CTAs, which both store their fp32
- *    partial; the second to arrive adds the other's (a + b, arrival-order
- *    free) and runs the epilogue.  Smaller N (act 0/1 only): partial tiles
- *    combined in k order by the last CTA of a tile.  Scratch: ws >=
- *    ms_linear_workspace() bytes, counters >= n_counters ints, zero on first
- *    use (every launch leaves them zero).
- *  - otherwise: one CTA per (128-feature tile, split); the `splits` CTAs of a
- *    tile (0 = ms_linear_splits(N, K), max 8) form a thread-block cluster and
- *    reduce through distributed shared memory.
+ * Schedule: one CTA per (128-feature tile, split, token tile); the `splits`
+ * CTAs of a tile (0 = ms_linear_splits(N, K), max 8) form a thread-block
+ * cluster and reduce their fp32 partials through distributed shared memory in
+ * rank order — deterministic and batch invariant (a row's result does not
+ * depend on M: the partition depends only on N and K).
+ * w_blocked = 1: w is stored tile-blocked, [N/128][K/64][128][64] (every
+ * 128 x 64 TMA tile a contiguous 16 KB run; N % 128 == 0, K % 64 == 0) —
+ * same arithmetic, bitwise the same result.
  * Limits: K % 8 == 0, ldx % 8 == 0, x and w 16-byte aligned.
  */
 int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-              int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
-              int* counters, int n_counters, void* stream);
+              int M, int N, int K, int act, int splits, int w_blocked, void* stream);
 /* ms_linear with the RMSNorm folded across GEMMs (the norm's gain is
  * pre-multiplied into the consumer's weight, so no normalised activation is
  * written): rms_out != NULL — a residual-writing split-K GEMM (bf16 out,
@@ -149,18 +142,7 @@ int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
 int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                   int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                   int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
-                  int64_t rms_ld, void* stream);
-/* ms_linear with the LayerNorm that precedes the projection fused in:
- *   out = act(LN(x) . w^T + bias) + residual,  LN(x) = (x - mean) * rstd * gamma + beta
- * (fp32 two-pass row statistics, eps).  Every CTA recomputes the statistics of
- * its token rows from x and normalises the TMA-loaded x tiles in shared memory
- * before the MMA reads them: one launch instead of LayerNorm + GEMM, meant for
- * the small decode shapes (M*K up to ~10^5) where launches, not bytes, cost.
- * Cluster split-K schedule; splits as in ms_linear. */
-int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const void* beta, float eps,
-                 const void* w, const void* bias, const void* residual, int64_t ldr,
-                 void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
-                 int splits, void* stream);
+                  int64_t rms_ld, int w_blocked, void* stream);
 /* Low-latency projection for M <= 64 token rows (the drafters' decode steps):
  * same contract as ms_linear (bias / ReLU / residual, bf16 or fp32 out), one
  * CTA per 16 output features, K split over 4 warps reduced in shared memory,
@@ -171,8 +153,6 @@ int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const v
             void* stream);
 /* Default split-K factor for an [N, K] weight (cluster path). */
 int ms_linear_splits(int N, int K);
-/* Scratch the stream-K path needs for this shape. */
-int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* n_counters);
 
 /* ---- decoder pieces around the GEMMs (OPT-style, pre-LN) ----------------
  * Token + learned-position embedding of R = B*Q rows: row r = b*Q + i is at

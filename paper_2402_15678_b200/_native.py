@@ -34,11 +34,9 @@ _SIGS = {
     "ms_argmax_rows": [_P, _I, _I, _I, _I64, _P, _P, _P],
     "ms_accept_greedy_logits": [_P, _P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "ms_accept_stochastic": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
-    "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I64, _P, _I, _P],
-    "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _P],
+    "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _I, _P],
+    "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _I, _P],
     "ms_gemv": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
-    "ms_linear_ln": [_P, _I64, _P, _P, _F, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P],
-    "ms_linear_workspace": [_I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
     "ms_linear_splits": [_I, _I],
     "ms_embed": [_P, _P, _I, _P, _P, _I, _I, _I, _P, _P],
     "ms_layernorm": [_P, _I64, _P, _P, _P, _F, _I, _I, _P, _I64, _P],

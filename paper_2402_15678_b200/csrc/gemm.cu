@@ -1,1257 +1,22 @@
-// K1/K5/K8 — the linear layers of the SSM decode and the LLM verify forward on
-// tcgen05 tensor cores.
+// Host side of K1/K5/K8 (ms_linear and its variants): tensor maps, the
+// split-K rule, the token-tile choice and the C-ABI entry points.  The kernel
+// is gemm_kernel.cuh (instantiated per token-tile width in gemm_inst*.cu).
 //
-//   out[M, N] = epi( X[M, K] · W[N, K]^T )      X: tokens (bf16), W: nn.Linear weight (bf16)
-//   epi(v)    = act(v + bias[n]) + residual[m, n]   -> bf16 or fp32
-//   act 2 (gated SiLU, Llama's SwiGLU MLP): W = the gate and up projections
-//   interleaved in 64-row blocks (rows 128t..128t+63 = gate rows 64t.., rows
-//   128t+64.. = up rows 64t..), out[m, 64t + j] = silu(g) * u in fp32, one
-//   bf16 rounding — the [M, 2F] gate/up activations never reach HBM.
-//
-// Decode/verify GEMMs have few token rows (M = B·(s+1) = 16..~300) against
-// multi-GB weights: they are HBM-bound weight streams.  Layout "swap-AB": the
-// weight tile is the MMA's M side (128 output features per CTA) and the token
-// tile its N side (BN = 16..256), so a 16-row batch still issues full-height
-// MMAs and TMEM holds a 128 x BN fp32 accumulator.
-//
-// Per CTA: warp 0 = TMA producer (W tile 128x64 + X tile BNx64 per stage,
-// 128B swizzle, mbarrier complete_tx), warp 1 = TMEM allocator + single-thread
-// tcgen05.mma issuer, warps 2-5 = epilogue (tcgen05.ld -> bias/act/residual ->
-// global).  Split-K over the reduction dimension fills the 148 SMs: the
-// `splits` CTAs of an output tile form one thread-block cluster and reduce
-// their fp32 partial tiles through distributed shared memory (no global
-// scratch, no extra launch), adding ranks in order — results are
-// deterministic and, because the split count depends only on (N, K),
-// identical for a token row whatever M is (batch invariance: a request's
-// logits do not depend on what else is in the verify batch).
+// Schedules measured slower than this cluster split-K path and removed from
+// the product library in round 2 (history: DESIGN.md §4): persistent
+// stream-K with a global workspace, whole-tile persistent, token-tile
+// multicast to N-tile pairs, LayerNorm fused into the X operand.
 #include <cstdlib>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "common.cuh"
-#include "tc.cuh"
+#include "gemm_kernel.cuh"
 
 namespace ms {
 
-struct LinearParams {
-  int M, N, K;
-  const __nv_bfloat16* bias;      // [N] or null
-  const __nv_bfloat16* residual;  // [M, ldr] or null
-  int64_t ldr;
-  void* out;                      // [M, ldc] bf16 or fp32
-  int64_t ldc;
-  int out_f32;
-  int act;                        // 0 none, 1 relu, 2 gated SiLU (interleaved gate/up)
-  int splits;
-  int kb_total;                   // K / 64 (rounded up)
-  int n_tiles;
-  int sw, sx;                     // W / X ring depths of this launch (cluster path)
-  int nc;                         // N tiles sharing one multicast X tile (cluster = splits * nc CTAs)
-  // RMSNorm folded across GEMMs (gains pre-multiplied into the consumer's
-  // weight): a residual-writing split-K GEMM emits per-(row, tile) sums of
-  // squares of the bf16 values it stores (rms_out[row * rms_ld + tile], a row's
-  // partials contiguous); the next GEMM runs on the raw residual stream and
-  // scales its fp32 accumulator by rstd[row] = rsqrt(sum_t rms_in[row * rms_ld
-  // + t] / K + eps).
-  // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
-  // output (row m, feature f) is stored straight into the receive slot of the
-  // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
-  // m) * tp_slice + f % tp_slice] (peer memory over NVLink), tile by tile as
-  // each CTA finishes, overlapping the transfer with other CTAs' mainloops
-  float* const* tp_recv;
-  int tp_rank, tp_slice, tp_rows;
-  // stream-K persistent schedule (linear_pk_kernel): two fp32 partial slots
-  // [BN][128] per CTA-range boundary, one arrival counter per boundary (zero
-  // on entry, left zero); null: whole-tile persistent schedule
-  float* sk_ws;
-  int* sk_cnt;
-  float* rms_out;
-  const float* rms_in;
-  int rms_nparts;
-  int64_t rms_ld;
-  float rms_eps;
-  // fused LayerNorm of the X operand (ln_g != null): X = LN(x) * g + b, the raw
-  // rows x [M, ldx] read for the row statistics, the TMA tile normalised in
-  // shared memory before the MMA consumes it
-  const __nv_bfloat16* ln_g;
-  const __nv_bfloat16* ln_b;
-  const __nv_bfloat16* ln_x;
-  int64_t ldx;
-  float ln_eps;
-  // weight layout: 0 = nn.Linear row-major [G*N, K]; 1 = tile-blocked
-  // [G][N/128][K/64][128][64] (every 128 x 64 weight tile one contiguous 16 KB
-  // run — TMA coordinate (0, ((grp * n_tiles + tile) * kb_total + kb) * 128))
-  int w_blocked;
-};
+MS_LINEAR_WIDTHS(MS_LINEAR_DECLARE)
 
-constexpr int kBM = 128;  // output features per CTA (MMA M)
-constexpr int kBK = 64;   // bf16 elements per 128-byte swizzled row
-constexpr int kThreads = 224;    // cluster path: W producer, MMA, 4 epilogue warps, X producer
-constexpr int kSKThreads = 192;  // stream-K path
-
-template <int BN>
-struct LinearCfg {
-  static constexpr int W_BYTES = kBM * kBK * 2;
-  static constexpr int X_BYTES = BN * kBK * 2;
-  static constexpr int MAX_SW = 14;
-  static constexpr int MAX_SX = 6;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int PART_BYTES = BN * kBM * 4;  // fp32 partial tile for the split-K reduction
-  static constexpr int NBAR = 2 * MAX_SW + 4 * MAX_SX + 1;  // mbarriers
-  // Two decoupled TMA rings: the weight ring (HBM stream — its depth is the
-  // bytes in flight that bound a weight stream by Little's law, ~6.5 TB/s x
-  // ~2 us per GPU) and a shallow token ring (the X tile is re-read by every
-  // CTA, an L2 hit).  With one shared ring, a large token tile (M ~ 200)
-  // crowded the weight stages out of the smem budget.  Budget: ~210 KB at one
-  // CTA per SM, ~104 KB at two.
-  __host__ __device__ static void rings_for(int budget, int* sw, int* sx) {
-    int x = budget >= 150 * 1024 ? 4 : (X_BYTES <= 8192 ? 3 : 2);
-    int w = (budget - x * X_BYTES) / W_BYTES;
-    if (w < 3 && x > 2) {
-      x = 2;
-      w = (budget - x * X_BYTES) / W_BYTES;
-    }
-    *sw = w < 2 ? 2 : (w > MAX_SW ? MAX_SW : w);
-    *sx = x > MAX_SX ? MAX_SX : x;
-  }
-  // the fp32 partial tile is staged in the (idle) ring smem only for the
-  // split-K cluster reduction; the single-split gated epilogue exchanges
-  // gate/up through a 4 KB buffer instead
-  static constexpr int GATED_EPI_BYTES = BN * 65 * 4 + BN * 64 * 2;  // up half + bf16 output tile
-  __host__ __device__ static int data_bytes(int sw, int sx, bool part) {
-    const int pipe = sw * W_BYTES + sx * X_BYTES;
-    int need = part ? PART_BYTES : GATED_EPI_BYTES;
-    if (need < GATED_EPI_BYTES) need = GATED_EPI_BYTES;
-    return pipe > need ? pipe : need;
-  }
-  __host__ __device__ static int smem(int sw, int sx, bool part) {
-    return 1024 + data_bytes(sw, sx, part) + NBAR * 8 + 16 + 2 * BN * 4;
-  }
-};
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// tok: global output row; feat: feature within the row group grp.  Returns
-// the value as stored (bf16-rounded for bf16 outputs).
-__device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int feat, float v, int grp = 0) {
-  if (p.bias) v += bf2f(p.bias[(int64_t)grp * p.N + feat]);
-  if (p.act == 1) v = fmaxf(v, 0.0f);
-  if (p.residual) v += bf2f(p.residual[(int64_t)tok * p.ldr + feat]);
-  if (p.tp_recv) {  // reduce-scatter: fp32 partial into the owning rank's receive slot
-    const int dst = feat / p.tp_slice;
-    p.tp_recv[dst][((int64_t)p.tp_rank * p.tp_rows + tok) * p.tp_slice + (feat - dst * p.tp_slice)] = v;
-    return v;
-  }
-  if (p.out_f32) {
-    reinterpret_cast<float*>(p.out)[(int64_t)tok * p.ldc + feat] = v;
-    return v;
-  }
-  const __nv_bfloat16 b = f2bf(v);
-  reinterpret_cast<__nv_bfloat16*>(p.out)[(int64_t)tok * p.ldc + feat] = b;
-  return bf2f(b);
-}
-
-__device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// float4 load from the shared memory of CTA `rank` of this cluster
-__device__ __forceinline__ float4 ld_dsmem_f4(const float* local, int rank) {
-  uint32_t a = tc::smem_u32(local), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
-  return v;
-}
-
-#ifdef MS_EXP_TIMING  // diagnostic build only: per-CTA globaltimer stamps
-__device__ unsigned long long g_exp_stamps[4096 * 4];
-__device__ __forceinline__ unsigned long long exp_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
-
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
-linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-              const LinearParams p) {
-  using C = LinearCfg<BN>;
-#ifdef MS_EXP_TIMING
-  const int exp_id = blockIdx.x + blockIdx.y * gridDim.x;
-  if (threadIdx.x == 0 && exp_id < 4096) g_exp_stamps[exp_id * 4] = exp_now();
-#endif
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = smem;
-  const int SW = p.sw, SX = p.sx;
-  uint8_t* sX = smem + SW * C::W_BYTES;
-  uint64_t* fullW = reinterpret_cast<uint64_t*>(smem + C::data_bytes(SW, SX, p.splits > 1));
-  uint64_t* emptyW = fullW + C::MAX_SW;
-  uint64_t* fullX = emptyW + C::MAX_SW;
-  uint64_t* emptyX = fullX + C::MAX_SX;
-  uint64_t* normed = emptyX + C::MAX_SX;  // [MAX_SX] X tile normalised (fused LayerNorm)
-  uint64_t* emptyXl = normed + C::MAX_SX;  // [MAX_SX] this CTA's MMA done with an X stage (multicast peers)
-  uint64_t* tmem_full = emptyXl + C::MAX_SX;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  float* s_mean = reinterpret_cast<float*>(tmem_slot + 4);  // [BN]
-  float* s_rstd = s_mean + BN;                              // [BN]
-  const bool fuse_ln = p.ln_g != nullptr;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  // cluster = nc N-tiles x splits K-slices; rank = j * splits + split.  The
-  // nc CTAs of one split read the same X k-blocks: the j == 0 CTA loads each
-  // X tile once from L2 and multicasts it to the others (the L2 -> SM stream
-  // of re-read token tiles, not HBM, bounds large-M weight streaming).
-  const int csize = p.splits * p.nc;
-  const int crank = (int)(blockIdx.x % csize);
-  const int jn = crank / p.splits;
-  const int split = crank - jn * p.splits;
-  const int tile_n = (int)(blockIdx.x / csize) * p.nc + jn;
-  const bool x_leader = jn == 0;
-  uint16_t x_mask = 0;
-  for (int jj = 0; jj < p.nc; ++jj) x_mask |= (uint16_t)(1u << (jj * p.splits + split));
-  const int n0 = tile_n * kBM;
-  const int m0 = blockIdx.y * BN;
-  // row group (grouped drafters): M rows of X / out and N rows of W per group
-  const int grp = blockIdx.z;
-  const int wrow = grp * p.N + n0, xrow = grp * p.M + m0, orow = grp * p.M + m0;
-  const int kb0 = (int)((int64_t)split * p.kb_total / p.splits);
-  const int kb1 = (int)((int64_t)(split + 1) * p.kb_total / p.splits);
-
-  if (warp == 0 && lane == 0) {
-    tc::prefetch_tmap(&tmW);
-    tc::prefetch_tmap(&tmX);
-    for (int s = 0; s < SW; ++s) {
-      tc::mbar_init(&fullW[s], 1);
-      tc::mbar_init(&emptyW[s], 1);
-    }
-    for (int s = 0; s < SX; ++s) {
-      tc::mbar_init(&fullX[s], 1);
-      tc::mbar_init(&emptyX[s], p.nc);  // leader: every multicast peer's MMA
-      tc::mbar_init(&normed[s], 128);
-      tc::mbar_init(&emptyXl[s], 1);
-    }
-    tc::mbar_init(tmem_full, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  if (p.nc > 1) cluster_sync_all();  // peers' barriers exist before any multicast / remote arrive
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-  // X operand ready for the MMA: the TMA barrier, or the normalisation barrier
-  uint64_t* x_ready = fuse_ln ? normed : fullX;
-
-  const int nkb = kb1 - kb0;
-  if (warp == 0) {
-    if (lane == 0) {
-      // weight producer: the first SW weight tiles do not depend on the previous
-      // kernel — issued before the programmatic-dependency wait (PDL prefetch)
-      const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
-      const int pre = nkb < SW ? nkb : SW;
-      // blocked layout: the tile's k-block run starts at row wblk
-      const int wblk = ((grp * p.n_tiles + tile_n) * p.kb_total + kb0) * kBM;
-      for (int i = 0; i < pre; ++i) {
-        tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
-        if (p.w_blocked)
-          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], 0, wblk + i * kBM, pol_w);
-        else
-          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
-      }
-      pdl_wait();
-      pdl_trigger();
-      for (int i = pre; i < nkb; ++i) {
-        const int st = i % SW;
-        tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
-        if (p.w_blocked)
-          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], 0, wblk + i * kBM, pol_w);
-        else
-          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
-      }
-    } else {
-      pdl_trigger();
-    }
-  } else if (warp == 6) {
-    if (lane == 0) {
-      // token producer (the X tile depends on the previous kernel)
-      const uint64_t pol_x = tc::policy_evict_last();  // tokens are re-read by every tile
-      pdl_wait();
-      pdl_trigger();
-      for (int i = 0; i < nkb; ++i) {
-        const int st = i % SX;
-        if (p.nc == 1) {
-          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
-#ifdef MS_EXP_NOX  // diagnostic build only: reuse the first SX token tiles (wrong results)
-          if (i >= SX) {
-            tc::mbar_arrive(&fullX[st]);
-            continue;
-          }
-#endif
-          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-          tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, pol_x);
-        } else if (x_leader) {
-          // stage free in every peer (each peer's MMA arrived on this barrier)
-          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-          tc::tma_load_2d_mc(sX + st * C::X_BYTES, &tmX, &fullX[st], (kb0 + i) * kBK, xrow, x_mask, pol_x);
-        } else {
-          // arm this CTA's barrier for the leader's multicast once our MMA
-          // released the stage (the bytes may land first: tx-count goes
-          // transiently negative, the phase still needs this arrival)
-          if (i >= SX) tc::mbar_wait(&emptyXl[st], ((i / SX) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-        }
-      }
-    } else {
-      pdl_trigger();
-    }
-  } else if (warp == 1) {
-    pdl_trigger();
-    if (lane == 0) {
-#ifdef MS_EXP_N16  // diagnostic build only: 16-column MMAs (wrong results)
-      constexpr uint32_t idesc = tc::idesc_bf16(kBM, 16);
-#else
-      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
-#endif
-      for (int i = 0; i < nkb; ++i) {
-        const int ws = i % SW, xs = i % SX;
-        tc::mbar_wait(&fullW[ws], (i / SW) & 1);
-        tc::mbar_wait(&x_ready[xs], (i / SX) & 1);
-        tc::fence_after_sync();
-        const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
-        const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)  // +32 bytes along K per UMMA_K=16 step
-          tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-        tc::mma_commit(&emptyW[ws]);
-        if (p.nc == 1) {
-          tc::mma_commit(&emptyX[xs]);
-        } else {
-          tc::mma_commit_mc(&emptyX[xs], (uint16_t)(1u << split));  // the leader of this split
-          tc::mma_commit(&emptyXl[xs]);
-        }
-      }
-      tc::mma_commit(tmem_full);
-    }
-  } else {
-    // ---------------- epilogue: warps 2..5, TMEM lane quadrant = warp % 4 ----------
-    const int q = warp & 3;
-    const int feat = n0 + q * 32 + lane;
-    const bool feat_ok = feat < p.N;
-    const int m_hi = min(BN, p.M - m0);  // valid token columns in this tile
-    pdl_wait();  // residual / outputs are ordered after the previous kernel
-    pdl_trigger();
-    if (fuse_ln) {
-      // (1) row statistics of the raw rows, fp32, two-pass, one warp per row
-      const int et = threadIdx.x - 64;  // 0..127
-      const int ew = et >> 5;
-      for (int r = ew; r < BN; r += 4) {
-        float mean = 0.f, rstd = 0.f;
-        if (r < m_hi) {
-          const __nv_bfloat16* xr = p.ln_x + (int64_t)(m0 + r) * p.ldx;
-          float sum = 0.f;
-          for (int c = lane * 8; c < p.K; c += 256) {
-            float f[8];
-            unpack8(*reinterpret_cast<const bf16x8*>(xr + c), f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sum += f[j];
-          }
-          mean = warp_sum(sum) / (float)p.K;
-          float sq = 0.f;
-          for (int c = lane * 8; c < p.K; c += 256) {
-            float f[8];
-            unpack8(*reinterpret_cast<const bf16x8*>(xr + c), f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sq += (f[j] - mean) * (f[j] - mean);
-          }
-          rstd = rsqrtf(warp_sum(sq) / (float)p.K + p.ln_eps);
-        }
-        if (lane == 0) {
-          s_mean[r] = mean;
-          s_rstd[r] = rstd;
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // (2) per stage: normalise the swizzled X tile in place, hand it to the MMA
-      for (int i = 0; i < nkb; ++i) {
-        const int stage = i % SX;
-        const int kb = kb0 + i;
-        tc::mbar_wait(&fullX[stage], (i / SX) & 1);
-        uint8_t* xs = sX + stage * C::X_BYTES;
-        for (int ch = et; ch < BN * 8; ch += 128) {  // 16-byte chunks: row r, logical chunk j
-          const int r = ch >> 3, j = ch & 7;
-          bf16x8* ptr = reinterpret_cast<bf16x8*>(xs + r * 128 + ((j ^ (r & 7)) << 4));
-          const int col = kb * kBK + j * 8;
-          float f[8], gg[8], bb[8];
-          unpack8(*ptr, f);
-          unpack8(*reinterpret_cast<const bf16x8*>(p.ln_g + col), gg);
-          unpack8(*reinterpret_cast<const bf16x8*>(p.ln_b + col), bb);
-          const float mu = s_mean[r], rs = s_rstd[r];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = (f[e] - mu) * rs * gg[e] + bb[e];
-          *ptr = pack8(f);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
-        tc::mbar_arrive(&normed[stage]);
-      }
-    }
-    if (p.rms_in) {
-      // folded RMSNorm: this tile's rows' rstd from the producer's partials
-      // (fixed summation order), while the mainloop runs
-      // one warp per row: lanes take partials l, l+32, ... (coalesced), then a
-      // fixed shuffle tree
-      for (int r = q; r < m_hi; r += 4) {
-        const float* pr = p.rms_in + (int64_t)(orow + r) * p.rms_ld;
-        float sq = 0.f;
-        for (int t = lane; t < p.rms_nparts; t += 32) sq += pr[t];
-        sq = warp_sum(sq);
-        if (lane == 0) s_rstd[r] = rsqrtf(sq / (float)p.K + p.rms_eps);
-      }
-      epi_bar128();
-    }
-    tc::mbar_wait(tmem_full, 0);
-    tc::fence_after_sync();
-#ifdef MS_EXP_TIMING
-    if (threadIdx.x == 64 && exp_id < 4096) g_exp_stamps[exp_id * 4 + 1] = exp_now();
-#endif
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-#ifdef MS_EXP_NOEPI  // diagnostic build only: no epilogue (no outputs)
-    if (p.splits == 1) goto epi_done;
-#endif
-
-    if (p.splits == 1 && p.act == 2) {
-      // gated SiLU, one split (the pipeline smem is idle once tmem_full fired):
-      // (1) the up warps (TMEM lanes 64..127) park the whole up half in smem,
-      // (2) one barrier, the gate warps form silu(g) * u into a bf16 output
-      // tile in smem, (3) one barrier, all four warps store the tile with
-      // coalesced 16-byte writes.  (The previous per-16-column exchange with
-      // two barriers per chunk and 2-byte stores cost ~13% of the 70B gate/up
-      // GEMM at M = 176.)
-      float* U = reinterpret_cast<float*>(smem);                            // [BN][65] fp32
-      __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(U + BN * 65);    // [BN][64] bf16
-      const bool up = q >= 2;
-      const int f = (q & 1) * 32 + lane;  // gate / up feature within the 64-wide half
-      for (int c0 = 0; c0 < m_hi; c0 += 32) {
-        uint32_t r[32];
-        tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
-        tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
-        tc::tmem_wait_ld();
-        if (up) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < m_hi) U[(c0 + j) * 65 + f] = __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f);
-        }
-      }
-      epi_bar128();
-      // the gate warps read their TMEM half after the barrier (re-loading is
-      // cheaper than holding up to 256 columns in registers)
-      if (!up) {
-        for (int c0 = 0; c0 < m_hi; c0 += 32) {
-          uint32_t r[32];
-          tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
-          tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < m_hi)
-              O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f),
-                                                   U[(c0 + j) * 65 + f]));
-        }
-      }
-      epi_bar128();
-      if (n0 < p.N) {  // n0 >= N: the padding tile of an odd multicast pair
-        const int et = threadIdx.x - 64;  // 0..127
-        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
-        for (int e = et; e < m_hi * 8; e += 128) {
-          const int row = e >> 3, ch = e & 7;
-          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
-              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
-        }
-      }
-    } else if (p.splits == 1) {
-      for (int c0 = 0; c0 < m_hi; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(trow + c0, r);
-        tc::tmem_wait_ld();
-        if (feat_ok) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi) epi_store(p, orow + c0 + j, feat, __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f), grp);
-        }
-      }
-    } else {
-      // stage this split's fp32 partial tile in (now idle) pipeline smem,
-      // layout P[token][feature] so a warp's 32 lanes write 32 consecutive words
-      float* P = reinterpret_cast<float*>(smem);
-      for (int c0 = 0; c0 < m_hi; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(trow + c0, r);
-        tc::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) P[(c0 + j) * kBM + q * 32 + lane] = __uint_as_float(r[j]);
-      }
-    }
-  }
-#ifdef MS_EXP_NOEPI
-epi_done:
-#endif
-  if (p.splits > 1) {
-    pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
-    // split-K reduction across the thread-block cluster through DSMEM: CTA
-    // `split` reduces a 1/splits slice of the tile, adding the partials of
-    // ranks 0..splits-1 in rank order (deterministic), then runs the epilogue.
-    // Gated SiLU: a unit covers gate features f4..f4+3 and their up partners
-    // f4+64.. of the same (staged) tile.
-    const bool cl = p.splits > 1;
-    if (cl) cluster_sync_all(); else __syncthreads();
-    const int m_hi = min(BN, p.M - m0);
-    const bool gated = p.act == 2;
-    const int upr = (gated ? kBM / 2 : kBM) / 4;  // float4 units per token row
-    const int units = m_hi * upr;
-    const int u0 = (int)((int64_t)split * units / p.splits);
-    const int u1 = (int)((int64_t)(split + 1) * units / p.splits);
-    const float* P = reinterpret_cast<const float*>(smem);
-    auto ld4 = [&](const float* a, int rk) {  // rank rk of this N-tile's split group
-      return cl ? ld_dsmem_f4(a, jn * p.splits + rk) : *reinterpret_cast<const float4*>(a);
-    };
-    if (p.rms_out && !gated) {
-      // residual producer of a folded RMSNorm: token-granular slices, one warp
-      // per token row, lane l = features 4l..4l+3; the row's sum of squares of
-      // the stored bf16 values over this tile's 128 features is a fixed-order
-      // warp reduction written to its own (tile, row) slot — deterministic
-      const int t0 = split * m_hi / p.splits, t1 = (split + 1) * m_hi / p.splits;
-      for (int j = t0 + warp; j < t1; j += kThreads / 32) {
-        const int f4 = lane * 4;
-        float4 acc = ld4(P + j * kBM + f4, 0);
-        for (int rk = 1; rk < p.splits; ++rk) {
-          const float4 v = ld4(P + j * kBM + f4, rk);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        const float rs = p.rms_in ? s_rstd[j] : 1.f;
-        const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
-        const int feat = n0 + f4;
-        float sq = 0.f;
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (feat + t < p.N) {
-            const float st = epi_store(p, orow + j, feat + t, a4[t], grp);
-            sq += st * st;
-          }
-        sq = warp_sum(sq);
-        if (lane == 0 && n0 < p.N) p.rms_out[(int64_t)(orow + j) * p.rms_ld + tile_n] = sq;
-      }
-    } else if (!gated) {
-      // batched for memory-level parallelism: each thread holds up to UB of
-      // its units, issues every partial (DSMEM) and residual load first, then
-      // computes and stores 4-wide — one latency per batch instead of one per
-      // unit (the unbatched loop cost ~12 us on a 176-row O projection, half
-      // of its mainloop)
-      constexpr int UB = 8;
-      const bool vec = (p.N % 4 == 0) && (p.ldc % 4 == 0) && (!p.residual || p.ldr % 4 == 0) && !p.tp_recv &&
-                       ((reinterpret_cast<uintptr_t>(p.out) & (p.out_f32 ? 15 : 7)) == 0) &&
-                       ((reinterpret_cast<uintptr_t>(p.residual) & 7) == 0) && !p.bias;
-      for (int ub = u0 + (int)threadIdx.x; ub < u1; ub += kThreads * UB) {
-        float4 acc[UB];
-        uint2 res[UB];
-#pragma unroll
-        for (int i = 0; i < UB; ++i) {
-          const int u = ub + i * kThreads;
-          if (u < u1) {
-            const int j = u / upr, f4 = (u - j * upr) * 4;
-            acc[i] = ld4(P + j * kBM + f4, 0);
-            if (vec && p.residual && n0 + f4 < p.N)
-              res[i] = *reinterpret_cast<const uint2*>(p.residual + (int64_t)(orow + j) * p.ldr + n0 + f4);
-          }
-        }
-        for (int rk = 1; rk < p.splits; ++rk) {
-#pragma unroll
-          for (int i = 0; i < UB; ++i) {
-            const int u = ub + i * kThreads;
-            if (u < u1) {
-              const int j = u / upr, f4 = (u - j * upr) * 4;
-              const float4 v = ld4(P + j * kBM + f4, rk);
-              acc[i].x += v.x; acc[i].y += v.y; acc[i].z += v.z; acc[i].w += v.w;
-            }
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < UB; ++i) {
-          const int u = ub + i * kThreads;
-          if (u >= u1) continue;
-          const int j = u / upr, f4 = (u - j * upr) * 4;
-          const float rs = p.rms_in ? s_rstd[j] : 1.f;
-          float a4[4] = {acc[i].x * rs, acc[i].y * rs, acc[i].z * rs, acc[i].w * rs};
-          const int feat = n0 + f4;
-          if (vec && feat < p.N) {
-            if (p.act == 1) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t) a4[t] = fmaxf(a4[t], 0.f);
-            }
-            if (p.residual) {
-              const __nv_bfloat162* rr = reinterpret_cast<const __nv_bfloat162*>(&res[i]);
-              const float2 r01 = __bfloat1622float2(rr[0]), r23 = __bfloat1622float2(rr[1]);
-              a4[0] += r01.x; a4[1] += r01.y; a4[2] += r23.x; a4[3] += r23.y;
-            }
-            if (p.out_f32) {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) =
-                  make_float4(a4[0], a4[1], a4[2], a4[3]);
-            } else {
-              uint2 pk;
-              pk.x = pack_bf16x2(a4[0], a4[1]);
-              pk.y = pack_bf16x2(a4[2], a4[3]);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) = pk;
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
-          }
-        }
-      }
-    } else {
-    for (int u = u0 + (int)threadIdx.x; u < u1; u += kThreads) {
-      const int j = u / upr;
-      const int f4 = (u - j * upr) * 4;
-      const float rs = p.rms_in ? s_rstd[j] : 1.f;
-      float4 acc = ld4(P + j * kBM + f4, 0);
-      for (int rk = 1; rk < p.splits; ++rk) {
-        const float4 v = ld4(P + j * kBM + f4, rk);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
-      float4 up = ld4(P + j * kBM + f4 + kBM / 2, 0);
-      for (int rk = 1; rk < p.splits; ++rk) {
-        const float4 v = ld4(P + j * kBM + f4 + kBM / 2, rk);
-        up.x += v.x; up.y += v.y; up.z += v.z; up.w += v.w;
-      }
-      const float u4[4] = {up.x * rs, up.y * rs, up.z * rs, up.w * rs};
-      const int of = tile_n * (kBM / 2) + f4;  // output feature
-      if (n0 >= p.N) continue;                 // padding tile of an odd multicast pair
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + of;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
-    }
-    }
-    if (cl) cluster_sync_all();  // peers may still be reading this CTA's smem
-  }
-  if (p.nc > 1 && p.splits == 1) cluster_sync_all();  // multicast peers done with each other's smem
-  tc::fence_before_sync();
-  __syncthreads();
-#ifdef MS_EXP_TIMING
-  if (threadIdx.x == 0 && exp_id < 4096) {
-    g_exp_stamps[exp_id * 4 + 2] = exp_now();
-    unsigned int smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_exp_stamps[exp_id * 4 + 3] = smid;
-  }
-#endif
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent stream-K variant for the decode / verify regime (one token tile,
-// M <= 256).  G persistent CTAs (one per SM, deep TMA pipeline: 8-11 stages of
-// weight tiles in flight) split the n_tiles x kb_total (tile, k-block)
-// iterations into G equal contiguous ranges, so every SM streams the same
-// number of weight bytes whatever N and K are.  A CTA walks its range tile
-// segment by tile segment, accumulating in one of two TMEM buffers while the
-// epilogue warps drain the other.  A segment that covers a whole tile is
-// stored directly; partial segments go to a per-CTA fp32 slot and the LAST
-// CTA to finish a tile (atomic counter) adds the slots in segment (= k) order
-// and runs the epilogue — deterministic, and M-independent (the partition is
-// a function of N, K and G only), so batch-invariant like the split-K path.
-// ---------------------------------------------------------------------------
-struct SKParams {
-  int iters;       // n_tiles * kb_total
-  int grid;        // G
-  float* ws;       // [G][2][BN][128] fp32 partial slots
-  int* counters;   // [n_tiles], zero on entry, left zero
-};
-
-template <int BN>
-struct SKCfg {
-  static constexpr int W_BYTES = kBM * kBK * 2;
-  static constexpr int X_BYTES = BN * kBK * 2;
-  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int STAGES_RAW = (216 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
-  static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered accumulator
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + (2 * STAGES + 4) * 8 + 16;
-};
-
-__device__ __forceinline__ int sk_begin(int c, int iters, int G) {
-  return (int)((int64_t)c * iters / G);
-}
-// CTA whose range contains iteration i
-__device__ __forceinline__ int sk_owner(int i, int iters, int G) {
-  int c = (int)((int64_t)i * G / iters);
-  while (c + 1 < G && sk_begin(c + 1, iters, G) <= i) ++c;
-  while (c > 0 && sk_begin(c, iters, G) > i) --c;
-  return c;
-}
-
-
-template <int BN>
-__global__ void __launch_bounds__(kSKThreads, 1)
-linear_sk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                 const LinearParams p, const SKParams sk) {
-  using C = SKCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = smem;
-  uint8_t* sX = smem + C::STAGES * C::W_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ int s_last;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const int kbt = p.kb_total;
-  const int it0 = sk_begin(c, sk.iters, sk.grid);
-  const int it1 = sk_begin(c + 1, sk.iters, sk.grid);
-
-  if (warp == 0 && lane == 0) {
-    tc::prefetch_tmap(&tmW);
-    tc::prefetch_tmap(&tmX);
-    for (int s = 0; s < C::STAGES; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 128);
-    }
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_w = tc::policy_evict_first();
-      const uint64_t pol_x = tc::policy_evict_last();
-      const int n = it1 - it0;
-      const int pre = n < C::STAGES ? n : C::STAGES;
-      for (int i = 0; i < pre; ++i) {  // weight tiles: independent of the previous kernel
-        const int it = it0 + i;
-        tc::mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &full[i], (it % kbt) * kBK, (it / kbt) * kBM, pol_w);
-      }
-      pdl_wait();
-      pdl_trigger();
-      for (int i = 0; i < n; ++i) {
-        const int it = it0 + i;
-        const int stage = i % C::STAGES;
-        if (i >= pre) {
-          tc::mbar_wait(&empty[stage], ((i / C::STAGES) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tc::tma_load_2d(sW + stage * C::W_BYTES, &tmW, &full[stage], (it % kbt) * kBK, (it / kbt) * kBM, pol_w);
-        }
-        tc::tma_load_2d(sX + stage * C::X_BYTES, &tmX, &full[stage], (it % kbt) * kBK, 0, pol_x);
-      }
-    } else {
-      pdl_trigger();
-    }
-  } else if (warp == 1) {
-    pdl_trigger();
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
-      int i = 0, seg = 0;
-      for (int it = it0; it < it1; ++seg) {
-        const int tile = it / kbt;
-        const int seg_end = min(it1, (tile + 1) * kbt);
-        const int buf = seg & 1;
-        tc::mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
-        tc::fence_after_sync();
-        const uint32_t dt = tmem + buf * C::ACC_COLS;
-        for (int j = it; j < seg_end; ++j, ++i) {
-          const int stage = i % C::STAGES;
-          tc::mbar_wait(&full[stage], (i / C::STAGES) & 1);
-          tc::fence_after_sync();
-          const uint64_t ad = tc::smem_desc_sw128(sW + stage * C::W_BYTES);
-          const uint64_t bd = tc::smem_desc_sw128(sX + stage * C::X_BYTES);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            tc::mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (j > it || k > 0) ? 1u : 0u);
-          tc::mma_commit(&empty[stage]);
-        }
-        tc::mma_commit(&tfull[buf]);
-        it = seg_end;
-      }
-    }
-  } else {
-    // ------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4 -------------
-    pdl_wait();
-    pdl_trigger();
-    const int q = warp & 3;
-    const int f = q * 32 + lane;  // feature within the tile
-    const int m_hi = min(BN, p.M);
-    int seg = 0;
-    for (int it = it0; it < it1; ++seg) {
-      const int tile = it / kbt;
-      const int seg_end = min(it1, (tile + 1) * kbt);
-      const bool whole = (it == tile * kbt) && (seg_end == (tile + 1) * kbt);
-      const int buf = seg & 1;
-      const int feat = tile * kBM + f;
-      const bool feat_ok = feat < p.N;
-      tc::mbar_wait(&tfull[buf], (seg >> 1) & 1);
-      tc::fence_after_sync();
-      const uint32_t trow = tmem + buf * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
-      const int slot = (it == it0) ? 0 : 1;
-      float* my_ws = sk.ws + ((int64_t)(c * 2 + slot) * BN) * kBM;
-      for (int c0 = 0; c0 < m_hi; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(trow + c0, r);
-        tc::tmem_wait_ld();
-        if (whole) {
-          if (feat_ok) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < m_hi) epi_store(p, c0 + j, feat, __uint_as_float(r[j]));
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi) __stcg(my_ws + (c0 + j) * kBM + f, __uint_as_float(r[j]));
-        }
-      }
-      tc::fence_before_sync();
-      tc::mbar_arrive(&tempty[buf]);  // TMEM buffer may be refilled
-      if (!whole) {
-        __threadfence();
-        epi_bar128();
-        if (warp == 2 && lane == 0) {
-          const int c_first = sk_owner(tile * kbt, sk.iters, sk.grid);
-          const int c_last = sk_owner((tile + 1) * kbt - 1, sk.iters, sk.grid);
-          const int nseg = c_last - c_first + 1;
-          const int old = atomicAdd(sk.counters + tile, 1);
-          s_last = (old == nseg - 1) ? (c_first | (c_last << 16)) : -1;
-          if (old == nseg - 1) sk.counters[tile] = 0;
-        }
-        epi_bar128();
-        const int lastv = s_last;
-        if (lastv >= 0) {
-          __threadfence();
-          const int c_first = lastv & 0xffff, c_last = lastv >> 16;
-          // fix-up: thread -> 4 consecutive features x rows rg, rg+4, ...; UNR
-          // independent 16-byte loads in flight per segment, segments added in
-          // k order (deterministic)
-          constexpr int UNR = 8;
-          const int et = threadIdx.x - 64;
-          const int fq = (et & 31) * 4, rg = et >> 5;
-          const int feat4 = tile * kBM + fq;
-          for (int j0 = rg; j0 < m_hi; j0 += 4 * UNR) {
-            float4 acc[UNR];
-            for (int cc = c_first; cc <= c_last; ++cc) {
-              const int sl = (sk_begin(cc, sk.iters, sk.grid) / kbt == tile) ? 0 : 1;
-              const float* base = sk.ws + ((int64_t)(cc * 2 + sl) * BN) * kBM + fq;
-              float4 v[UNR];
-#pragma unroll
-              for (int u = 0; u < UNR; ++u) {
-                const int j = j0 + 4 * u;
-                v[u] = j < m_hi ? __ldcg(reinterpret_cast<const float4*>(base + (int64_t)j * kBM))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-#pragma unroll
-              for (int u = 0; u < UNR; ++u) {
-                if (cc == c_first) {
-                  acc[u] = v[u];
-                } else {
-                  acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
-                }
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-              const int j = j0 + 4 * u;
-              if (j < m_hi) {
-                const float a4[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                  if (feat4 + t < p.N) epi_store(p, j, feat4 + t, a4[t]);
-              }
-            }
-          }
-        }
-        epi_bar128();  // s_last is reused by the next segment
-      }
-      it = seg_end;
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// Persistent weight-streaming schedule for GEMMs with >= one tile per SM
-// (the 70B gate/up projection: 448 tiles, the LM head: 250): one CTA per SM
-// with
-//   * decoupled TMA rings sized for ONE CTA per SM (~144 KB of weight tiles in
-//     flight — what a 6.5 TB/s stream needs per SM by Little's law — next to a
-//     shallow token ring), flowing across tile boundaries without a drain;
-//   * a double-buffered TMEM accumulator (2 x BN columns): the epilogue of tile
-//     t overlaps the mainloop of tile t + 1.
-// Two work partitions:
-//   * whole tiles (MS_PK=1, no workspace): tiles c, c + P, ... — bitwise the
-//     arithmetic of the one-split cluster path, but 448 tiles over 148 CTAs is
-//     4 vs 3 tiles per CTA (a 33% tail);
-//   * stream-K (a workspace is passed): CTA c owns the flat k-block range
-//     [c T / P, (c+1) T / P) of the tile-major iteration space (T = tiles x
-//     k-blocks), so every CTA streams the same number of weight bytes.  As a
-//     range is >= one tile long, a tile is split between at most two CTAs: the
-//     head (k-blocks from 0, at the END of CTA c-1's range) and the tail (the
-//     START of CTA c's range).  Both store their fp32 partial to the
-//     boundary's two slots and bump its counter; the second to arrive adds the
-//     other's partial to its own accumulator (a + b: commutative, so the
-//     arrival order never changes a bit) and runs the epilogue — no CTA ever
-//     waits for another.  The partition is a function of (N, K) and the SM
-//     count only, never of M: batch-invariant.
-// Measured slower than the cluster path inside a launch sequence (70B gate/up
-// at M = 80, CUDA-graph replay: 215 vs 172 us; alone under ncu 218 vs 209 us,
-// both ~4.4 TB/s): the cluster path's half-full second wave is filled by the
-// NEXT kernel's PDL weight prefetch, which one CTA per SM with ~200 KB of
-// shared memory never lets in.  So it runs only when a caller passes a
-// workspace (tests, tools/probe_gemm_graph.py); the models do not.
-// ---------------------------------------------------------------------------
-template <int BN>
-struct PKCfg {
-  static constexpr int W_BYTES = kBM * kBK * 2;
-  static constexpr int X_BYTES = BN * kBK * 2;
-  static constexpr int MAX_SW = 16;
-  static constexpr int MAX_SX = 6;
-  static constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
-  // gated epilogue: the up half [BN][65] fp32 + the bf16 output tile [BN][64]
-  static constexpr int EPI_BYTES = BN * 65 * 4 + BN * 64 * 2;
-  // both rings sized by latency: weight tiles (HBM, ~2 us loaded) and token
-  // tiles (L2, ~1.2 us) are consumed one of each per k-block, so the stage
-  // counts go ~5:3 within the budget
-  __host__ __device__ static void rings(int* sw, int* sx) {
-    const int budget = 206 * 1024 - EPI_BYTES;
-    int x = budget * 3 / (5 * W_BYTES + 3 * X_BYTES);
-    x = x < 2 ? 2 : (x > MAX_SX ? MAX_SX : x);
-    int w = (budget - x * X_BYTES) / W_BYTES;
-    *sw = w > MAX_SW ? MAX_SW : w;
-    *sx = x;
-  }
-  __host__ __device__ static int smem(int sw, int sx) {
-    return 1024 + sw * W_BYTES + sx * X_BYTES + EPI_BYTES + (2 * MAX_SW + 2 * MAX_SX + 4) * 8 + 16;
-  }
-};
-
-// this CTA's (tile, k-block range) segments, in order
-struct PKSeg {
-  int64_t u, u1;   // stream-K: flat k-block range [u, u1)
-  int t, step, n;  // whole tiles: t, t + step, ... (n left)
-  int kbt;
-  bool sk;
-  __device__ bool next(int& tile, int& k0, int& k1) {
-    if (sk) {
-      if (u >= u1) return false;
-      tile = (int)(u / kbt);
-      const int64_t base = (int64_t)tile * kbt;
-      k0 = (int)(u - base);
-      const int64_t e = base + kbt < u1 ? base + kbt : u1;
-      k1 = (int)(e - base);
-      u = e;
-      return true;
-    }
-    if (n <= 0) return false;
-    tile = t;
-    k0 = 0;
-    k1 = kbt;
-    t += step;
-    --n;
-    return true;
-  }
-};
-
-__device__ __forceinline__ PKSeg pk_segments(const LinearParams& p, int c, int P) {
-  PKSeg s;
-  s.kbt = p.kb_total;
-  s.sk = p.sk_ws != nullptr;
-  const int64_t total = (int64_t)p.n_tiles * p.kb_total;
-  s.u = total * c / P;
-  s.u1 = total * (c + 1) / P;
-  s.t = c;
-  s.step = P;
-  s.n = c < p.n_tiles ? (p.n_tiles - c + P - 1) / P : 0;
-  return s;
-}
-
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
-linear_pk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                 const LinearParams p) {
-  using C = PKCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int SW = p.sw, SX = p.sx;
-  uint8_t* sW = smem;
-  uint8_t* sX = smem + SW * C::W_BYTES;
-  float* U = reinterpret_cast<float*>(sX + SX * C::X_BYTES);          // [BN][65]
-  __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(U + BN * 65);    // [BN][64]
-  uint64_t* fullW = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(U) + C::EPI_BYTES);
-  uint64_t* emptyW = fullW + C::MAX_SW;
-  uint64_t* fullX = emptyW + C::MAX_SW;
-  uint64_t* emptyX = fullX + C::MAX_SX;
-  uint64_t* tfull = emptyX + C::MAX_SX;  // [2]
-  uint64_t* tempty = tfull + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ int s_arrival;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int P = gridDim.x, c = blockIdx.x;
-
-  if (warp == 0 && lane == 0) {
-    tc::prefetch_tmap(&tmW);
-    tc::prefetch_tmap(&tmX);
-    for (int s = 0; s < SW; ++s) {
-      tc::mbar_init(&fullW[s], 1);
-      tc::mbar_init(&emptyW[s], 1);
-    }
-    for (int s = 0; s < SX; ++s) {
-      tc::mbar_init(&fullX[s], 1);
-      tc::mbar_init(&emptyX[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 128);
-    }
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  int tile, k0, k1;
-  if (warp == 0) {
-    if (lane == 0) {
-      // weights do not depend on the previous kernel: the first SW tiles are
-      // issued before the programmatic-dependency wait (PDL prefetch)
-      const uint64_t pol_w = tc::policy_evict_first();
-      PKSeg sg = pk_segments(p, c, P);
-      int i = 0;
-      bool waited = false;
-      while (sg.next(tile, k0, k1)) {
-        for (int kb = k0; kb < k1; ++kb, ++i) {
-          if (i == SW && !waited) {
-            pdl_wait();
-            pdl_trigger();
-            waited = true;
-          }
-          const int st = i % SW;
-          if (i >= SW) tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
-          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], kb * kBK, tile * kBM, pol_w);
-        }
-      }
-      if (!waited) {
-        pdl_wait();
-        pdl_trigger();
-      }
-    } else {
-      pdl_trigger();
-    }
-  } else if (warp == 6) {
-    if (lane == 0) {
-      const uint64_t pol_x = tc::policy_evict_last();
-      pdl_wait();
-      pdl_trigger();
-      PKSeg sg = pk_segments(p, c, P);
-      int i = 0;
-      while (sg.next(tile, k0, k1)) {
-        for (int kb = k0; kb < k1; ++kb, ++i) {
-          const int st = i % SX;
-          if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
-          tc::tma_load_2d(sX + st * C::X_BYTES, &tmX, &fullX[st], kb * kBK, 0, pol_x);
-        }
-      }
-    } else {
-      pdl_trigger();
-    }
-  } else if (warp == 1) {
-    pdl_trigger();
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(kBM, BN);
-      PKSeg sg = pk_segments(p, c, P);
-      int i = 0, s = 0;
-      while (sg.next(tile, k0, k1)) {
-        const int buf = s & 1;
-        tc::mbar_wait(&tempty[buf], ((s >> 1) & 1) ^ 1);  // epilogue drained this accumulator
-        tc::fence_after_sync();
-        const uint32_t acc = tmem + buf * C::ACC_COLS;
-        for (int kb = k0; kb < k1; ++kb, ++i) {
-          const int ws = i % SW, xs = i % SX;
-          tc::mbar_wait(&fullW[ws], (i / SW) & 1);
-          tc::mbar_wait(&fullX[xs], (i / SX) & 1);
-          tc::fence_after_sync();
-          const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
-          const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            tc::mma_bf16(acc, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
-          tc::mma_commit(&emptyW[ws]);
-          tc::mma_commit(&emptyX[xs]);
-        }
-        tc::mma_commit(&tfull[buf]);
-        ++s;
-      }
-    }
-  } else {
-    // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4 ----------------
-    pdl_wait();
-    pdl_trigger();
-    const int q = warp & 3;
-    const int f = q * 32 + lane;  // this thread's feature (TMEM lane) within the tile
-    const int m_hi = min(BN, p.M);
-    PKSeg sg = pk_segments(p, c, P);
-    int s = 0;
-    while (sg.next(tile, k0, k1)) {
-      const int buf = s & 1;
-      tc::mbar_wait(&tfull[buf], (s >> 1) & 1);
-      tc::fence_after_sync();
-      const uint32_t trow = tmem + buf * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
-      const float* other = nullptr;  // the other segment's partial [token][feature]
-      bool finish = true;
-      if (k0 > 0 || k1 < p.kb_total) {
-        // split tile: boundary c (this range's first segment, the tile's tail)
-        // or c + 1 (its last segment, the tile's head); slot 2*bnd + role
-        const int bnd = k0 > 0 ? c : c + 1;
-        const int role = k0 > 0 ? 1 : 0;
-        float* mine = p.sk_ws + (int64_t)(2 * bnd + role) * (BN * kBM);
-        for (int c0 = 0; c0 < m_hi; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(trow + c0, r);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < m_hi) __stcg(mine + (c0 + j) * kBM + f, __uint_as_float(r[j]));
-        }
-        __threadfence();
-        epi_bar128();
-        if (threadIdx.x == 64) {
-          const int old = atomicAdd(p.sk_cnt + bnd, 1);
-          if (old == 1) p.sk_cnt[bnd] = 0;  // both arrived: zero for the next launch
-          s_arrival = old;
-        }
-        epi_bar128();
-        finish = s_arrival == 1;  // (rewritten only after the next split's first barrier)
-        if (finish) {
-          __threadfence();
-          other = p.sk_ws + (int64_t)(2 * bnd + 1 - role) * (BN * kBM);
-        }
-      }
-      if (finish && p.act == 2) {
-        // gated SiLU: the up warps park the up half in smem, the gate warps
-        // form silu(g) * u into a bf16 tile, all four store it with 16-byte
-        // writes (output features tile*64 .. tile*64+63)
-        const bool up = q >= 2;
-        const int fu = (q & 1) * 32 + lane;
-        for (int c0 = 0; c0 < m_hi; c0 += 32) {
-          uint32_t r[32];
-          tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
-          tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
-          tc::tmem_wait_ld();
-          if (up) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + j < m_hi) {
-                const float v = __uint_as_float(r[j]);
-                U[(c0 + j) * 65 + fu] = other ? v + __ldcg(other + (c0 + j) * kBM + f) : v;
-              }
-          }
-        }
-        epi_bar128();
-        if (!up) {
-          for (int c0 = 0; c0 < m_hi; c0 += 32) {
-            uint32_t r[32];
-            tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
-            tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + j < m_hi) {
-                const float v = __uint_as_float(r[j]);
-                const float gv = other ? v + __ldcg(other + (c0 + j) * kBM + f) : v;
-                O[(c0 + j) * 64 + fu] = f2bf(silu_mul(gv, U[(c0 + j) * 65 + fu]));
-              }
-          }
-        }
-        epi_bar128();
-        const int et = threadIdx.x - 64;  // 0..127
-        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + tile * (kBM / 2);
-        for (int e = et; e < m_hi * 8; e += 128) {
-          const int row = e >> 3, ch = e & 7;
-          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
-              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
-        }
-        epi_bar128();  // U / O are reused by the next tile
-      } else if (finish) {
-        const int feat = tile * kBM + f;
-        const bool feat_ok = feat < p.N;
-        for (int c0 = 0; c0 < m_hi; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(trow + c0, r);
-          tc::tmem_wait_ld();
-          if (feat_ok) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < m_hi) {
-                const float v = __uint_as_float(r[j]);
-                epi_store(p, c0 + j, feat, other ? v + __ldcg(other + (c0 + j) * kBM + f) : v);
-              }
-          }
-        }
-      }
-      tc::fence_before_sync();
-      tc::mbar_arrive(&tempty[buf]);
-      ++s;
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1265,17 +30,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2-D bf16 row-major [rows, cols] with row stride ld (elements); box = [64 cols, box_rows].
-static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
-                      int box_rows) {
+static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
   cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -1300,162 +64,30 @@ static int pick_bn(int M) {
   return M <= 16 ? 16 : (M + 15) / 16 * 16;
 }
 
-// Opt-in (MS_MC=1): multicasting the token tile to N-tile pairs measured
-// neutral to slightly slower (QKV at M = 176: 40.9 vs 39.9 us) — L2 -> SM
-// bandwidth (30% of peak per ncu) is not what bounds these GEMMs.
-static bool mc_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MS_MC");
-    v = (e && e[0] == '1') ? 1 : 0;
+static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int m_tiles,
+                     cudaStream_t st, int G) {
+  switch (bn) {
+#define MS_CASE(BN) \
+  case BN:          \
+    return launch_linear<BN>(tw, tx, p, m_tiles, st, G);
+    MS_LINEAR_WIDTHS(MS_CASE)
+#undef MS_CASE
+    default:
+      return MS_ERR_VALUE;
   }
-  return v == 1;
-}
-
-template <int BN>
-static int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p,
-                         int m_tiles, cudaStream_t st, int G) {
-  using C = LinearCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    int sw, sx;
-    C::rings_for(210 * 1024, &sw, &sx);
-    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::smem(sw, sx, true)) != cudaSuccess)
-      return MS_ERR_CUDA;
-    attr_set = true;
-  }
-  // multicast pairs along N once the token tile is big enough for its L2
-  // re-reads to matter (M > 48), within the portable cluster size 8
-  p.nc = (BN > 48 && p.n_tiles > 1 && p.splits * 2 <= 8 && mc_enabled()) ? 2 : 1;
-  const int n_tiles_pad = (p.n_tiles + p.nc - 1) / p.nc * p.nc;
-  const int grid = n_tiles_pad * p.splits * m_tiles * G;
-  // never deeper than the k-blocks a CTA streams: small (SSM) GEMMs then use
-  // little shared memory and several kernels / streams can share an SM
-  const int kb_per_cta = (p.kb_total + p.splits - 1) / p.splits;
-  const bool part = p.splits > 1;
-  int sw, sx;
-  C::rings_for(grid <= 148 ? 210 * 1024 : 104 * 1024, &sw, &sx);
-  // the fp32 split-K staging tile may already rule out two CTAs per SM: then
-  // take the deep single-CTA rings
-  if (part && C::smem(sw, sx, part) > 113 * 1024) C::rings_for(210 * 1024, &sw, &sx);
-  if (sw > kb_per_cta) sw = kb_per_cta < 2 ? 2 : kb_per_cta;
-  if (sx > kb_per_cta) sx = kb_per_cta < 2 ? 2 : kb_per_cta;
-  p.sw = sw;
-  p.sx = sx;
-  return launch(linear_kernel<BN>, dim3(n_tiles_pad * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part),
-                st, p.splits * p.nc /* split-K CTAs x multicast N-tiles form one cluster */, tw, tx, p);
-}
-
-
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-  }
-  return n;
-}
-
-// stream-K persistent schedule scratch: two fp32 [BN][128] slots per range
-// boundary (SMs + 1 boundaries)
-static int64_t pk_ws_bytes(int bn) { return (int64_t)(sm_count() + 1) * 2 * bn * kBM * 4; }
-
-template <int BN>
-static int launch_linear_pk(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, cudaStream_t st) {
-  using C = PKCfg<BN>;
-  int sw, sx;
-  C::rings(&sw, &sx);
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(linear_pk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(sw, sx)) !=
-        cudaSuccess)
-      return MS_ERR_CUDA;
-    attr_set = true;
-  }
-  p.sw = sw;
-  p.sx = sx;
-  p.splits = 1;
-  // stream-K: one range per SM (n_tiles >= SMs, so every range is >= one tile)
-  const int grid = p.sk_ws ? sm_count() : (p.n_tiles < sm_count() ? p.n_tiles : sm_count());
-  return launch(linear_pk_kernel<BN>, dim3(grid), dim3(kThreads), C::smem(sw, sx), st, 1, tw, tx, p);
-}
-// Opt-in (MS_PK=1): measured no faster than the cluster path on the 70B
-// shapes (gate/up at M = 112 / 176: 201 / 219 us vs 183 / 213 us) — with deep
-// rings either way the large-M tiles stay ~35% tensor-active and ~50% DRAM:
-// neither ring depth nor wave quantization is the limiter there.
-static bool pk_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("MS_PK");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-
-// Persistent grid for the stream-K path: a function of (N, K) only.
-int linear_sk_grid(int N, int K) {
-  const int iters = ((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK);
-  int g = iters / 4;  // >= 4 k-blocks per CTA
-  g = g > 148 ? 148 : g;
-  return g < 1 ? 1 : g;
-}
-
-template <int BN>
-static int launch_linear_sk(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p,
-                            const SKParams& sk, cudaStream_t st) {
-  using C = SKCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(linear_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM) != cudaSuccess)
-      return MS_ERR_CUDA;
-    attr_set = true;
-  }
-  return launch(linear_sk_kernel<BN>, dim3(sk.grid), dim3(kSKThreads), C::SMEM, st, 1, tw, tx, p, sk);
 }
 
 int preload_gemm() {
   int n = 0;
-  n += preload_fn(linear_kernel<16>) + preload_fn(linear_sk_kernel<16>) + preload_fn(linear_pk_kernel<16>);
-  n += preload_fn(linear_kernel<32>) + preload_fn(linear_sk_kernel<32>) + preload_fn(linear_pk_kernel<32>);
-  n += preload_fn(linear_kernel<48>) + preload_fn(linear_sk_kernel<48>) + preload_fn(linear_pk_kernel<48>);
-  n += preload_fn(linear_kernel<64>) + preload_fn(linear_sk_kernel<64>) + preload_fn(linear_pk_kernel<64>);
-  n += preload_fn(linear_kernel<80>) + preload_fn(linear_sk_kernel<80>) + preload_fn(linear_pk_kernel<80>);
-  n += preload_fn(linear_kernel<96>) + preload_fn(linear_sk_kernel<96>) + preload_fn(linear_pk_kernel<96>);
-  n += preload_fn(linear_kernel<112>) + preload_fn(linear_sk_kernel<112>) + preload_fn(linear_pk_kernel<112>);
-  n += preload_fn(linear_kernel<128>) + preload_fn(linear_sk_kernel<128>) + preload_fn(linear_pk_kernel<128>);
-  n += preload_fn(linear_kernel<144>) + preload_fn(linear_sk_kernel<144>) + preload_fn(linear_pk_kernel<144>);
-  n += preload_fn(linear_kernel<160>) + preload_fn(linear_sk_kernel<160>) + preload_fn(linear_pk_kernel<160>);
-  n += preload_fn(linear_kernel<176>) + preload_fn(linear_sk_kernel<176>) + preload_fn(linear_pk_kernel<176>);
-  n += preload_fn(linear_kernel<192>) + preload_fn(linear_sk_kernel<192>) + preload_fn(linear_pk_kernel<192>);
-  n += preload_fn(linear_kernel<208>) + preload_fn(linear_sk_kernel<208>) + preload_fn(linear_pk_kernel<208>);
-  n += preload_fn(linear_kernel<224>) + preload_fn(linear_sk_kernel<224>) + preload_fn(linear_pk_kernel<224>);
-  n += preload_fn(linear_kernel<240>) + preload_fn(linear_sk_kernel<240>) + preload_fn(linear_pk_kernel<240>);
-  n += preload_fn(linear_kernel<256>) + preload_fn(linear_sk_kernel<256>) + preload_fn(linear_pk_kernel<256>);
+#define MS_PRE(BN) n += preload_linear<BN>();
+  MS_LINEAR_WIDTHS(MS_PRE)
+#undef MS_PRE
   return n;
 }
 
 }  // namespace ms
 
 extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }
-
-extern "C" int ms_linear_workspace(int M, int N, int K, int64_t* ws_bytes, int* n_counters) {
-  if (M < 0 || N < 1 || K < 1) return MS_ERR_VALUE;
-  const int bn = ms::pick_bn(M);
-  const int g = ms::linear_sk_grid(N, K);
-  int64_t b = (int64_t)g * 2 * bn * ms::kBM * 4;
-  int n = (N + ms::kBM - 1) / ms::kBM;
-  if (n >= ms::sm_count()) {  // persistent stream-K schedule
-    b = b > ms::pk_ws_bytes(bn) ? b : ms::pk_ws_bytes(bn);
-    n = n > ms::sm_count() + 1 ? n : ms::sm_count() + 1;
-  }
-  if (ws_bytes) *ws_bytes = b;
-  if (n_counters) *n_counters = n;
-  return MS_OK;
-}
 
 struct RmsArgs {
   float* out = nullptr;
@@ -1468,32 +100,27 @@ struct RmsArgs {
   int tp_rank = 0, tp_slice = 1, tp_rows = 0;
 };
 
-static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias,
-                       const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-                       int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
-                       int* counters, int n_counters, const void* g_ln_g, const void* g_ln_b,
-                       float g_ln_eps, void* stream, int G = 1, RmsArgs rms = RmsArgs()) {
+static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                       int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act, int splits,
+                       int w_blocked, void* stream, int G = 1, RmsArgs rms = RmsArgs()) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
   if (!x || !w || !out) return MS_ERR_VALUE;
   if (act < 0 || act > 2) return MS_ERR_VALUE;
-  if (act == 2 && (N % kBM || bias || residual || out_f32 || ldc % 8 ||
-                   (reinterpret_cast<uintptr_t>(out) & 15)))
+  if (act == 2 && (N % kBM || bias || residual || out_f32 || ldc % 8 || (reinterpret_cast<uintptr_t>(out) & 15)))
     return MS_ERR_UNSUPPORTED;  // gated epilogue stores 16-byte vectors
   if (K % 8 != 0 || ldx % 8 != 0) return MS_ERR_UNSUPPORTED;  // TMA: 16-byte row strides
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
+  if (w_blocked && (N % kBM || K % kBK)) return MS_ERR_UNSUPPORTED;
+  if (G < 1 || G > 65535) return MS_ERR_VALUE;
   const int kb_total = (K + kBK - 1) / kBK;
   const int bn = pick_bn(M);
   const int m_tiles = (M + bn - 1) / bn;
   const int n_tiles = (N + kBM - 1) / kBM;
   if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
   CUtensorMap tw, tx;
-  if (G < 1 || G > 65535 || (G > 1 && g_ln_g)) return MS_ERR_VALUE;
-  const char* wb_env = getenv("MS_EXP_WBLOCKED");  // experiment: w is tile-blocked (see LinearParams)
-  const int w_blocked = (wb_env && wb_env[0] == '1') ? 1 : 0;
-  if (w_blocked && (N % kBM || K % kBK)) return MS_ERR_UNSUPPORTED;
   if (w_blocked ? !make_tmap(&tw, w, (int64_t)G * N * (K / kBK), kBK, kBK, kBM)
                 : !make_tmap(&tw, w, (int64_t)G * N, K, K, kBM))
     return MS_ERR_CUDA;
@@ -1504,153 +131,34 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.residual = (const __nv_bfloat16*)residual;
   p.ldr = ldr;
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
-  p.splits = splits; p.kb_total = kb_total; p.n_tiles = n_tiles;
-  p.rms_out = nullptr; p.rms_in = nullptr; p.rms_nparts = 0; p.rms_ld = 0; p.rms_eps = 0.f; p.nc = 1;
-  p.tp_recv = nullptr; p.tp_rank = 0; p.tp_slice = 1; p.tp_rows = 0;
-  p.sk_ws = nullptr; p.sk_cnt = nullptr;
-  p.ln_g = nullptr; p.ln_b = nullptr; p.ln_x = nullptr; p.ldx = ldx; p.ln_eps = 0.f;
-  p.w_blocked = w_blocked;
-  if (g_ln_g) {  // fused LayerNorm request from ms_linear_ln
-    p.ln_g = (const __nv_bfloat16*)g_ln_g;
-    p.ln_b = (const __nv_bfloat16*)g_ln_b;
-    p.ln_x = (const __nv_bfloat16*)x;
-    p.ln_eps = g_ln_eps;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
+  p.kb_total = kb_total; p.n_tiles = n_tiles; p.w_blocked = w_blocked;
+  p.sw = p.sx = 0;
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
   p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
-  const bool folded = rms.out || rms.in || rms.tp_recv;
-  // weight-streaming GEMMs with at least one 128-feature tile per SM and a
-  // workspace: the persistent stream-K schedule (equal weight bytes per SM)
-  const bool big = splits == 0 && m_tiles == 1 && G == 1 && !g_ln_g && !folded && n_tiles >= sm_count() && !w_blocked;
-  if (big && ws && counters && ws_bytes >= pk_ws_bytes(bn) && n_counters >= sm_count() + 1) {
-    p.sk_ws = (float*)ws;
-    p.sk_cnt = counters;
-    switch (bn) {
-      case 16: return launch_linear_pk<16>(tw, tx, p, st);
-      case 32: return launch_linear_pk<32>(tw, tx, p, st);
-      case 48: return launch_linear_pk<48>(tw, tx, p, st);
-      case 64: return launch_linear_pk<64>(tw, tx, p, st);
-      case 80: return launch_linear_pk<80>(tw, tx, p, st);
-      case 96: return launch_linear_pk<96>(tw, tx, p, st);
-      case 112: return launch_linear_pk<112>(tw, tx, p, st);
-      case 128: return launch_linear_pk<128>(tw, tx, p, st);
-      case 144: return launch_linear_pk<144>(tw, tx, p, st);
-      case 160: return launch_linear_pk<160>(tw, tx, p, st);
-      case 176: return launch_linear_pk<176>(tw, tx, p, st);
-      case 192: return launch_linear_pk<192>(tw, tx, p, st);
-      case 208: return launch_linear_pk<208>(tw, tx, p, st);
-      case 224: return launch_linear_pk<224>(tw, tx, p, st);
-      case 240: return launch_linear_pk<240>(tw, tx, p, st);
-      default: return launch_linear_pk<256>(tw, tx, p, st);
-    }
-  }
-  // decode / verify regime: persistent stream-K kernel when scratch is given
-  const int g = linear_sk_grid(N, K);
-  if (splits == 0 && m_tiles == 1 && ws && counters && act != 2 && G == 1 && !folded && !w_blocked &&
-      ws_bytes >= (int64_t)g * 2 * bn * kBM * 4 && n_counters >= n_tiles) {
-    SKParams sk;
-    sk.iters = n_tiles * kb_total;
-    sk.grid = g;
-    sk.ws = (float*)ws;
-    sk.counters = counters;
-    p.splits = 1;
-    switch (bn) {
-      case 16: return launch_linear_sk<16>(tw, tx, p, sk, st);
-      case 32: return launch_linear_sk<32>(tw, tx, p, sk, st);
-      case 48: return launch_linear_sk<48>(tw, tx, p, sk, st);
-      case 64: return launch_linear_sk<64>(tw, tx, p, sk, st);
-      case 80: return launch_linear_sk<80>(tw, tx, p, sk, st);
-      case 96: return launch_linear_sk<96>(tw, tx, p, sk, st);
-      case 112: return launch_linear_sk<112>(tw, tx, p, sk, st);
-      case 128: return launch_linear_sk<128>(tw, tx, p, sk, st);
-      case 144: return launch_linear_sk<144>(tw, tx, p, sk, st);
-      case 160: return launch_linear_sk<160>(tw, tx, p, sk, st);
-      case 176: return launch_linear_sk<176>(tw, tx, p, sk, st);
-      case 192: return launch_linear_sk<192>(tw, tx, p, sk, st);
-      case 208: return launch_linear_sk<208>(tw, tx, p, sk, st);
-      case 224: return launch_linear_sk<224>(tw, tx, p, sk, st);
-      case 240: return launch_linear_sk<240>(tw, tx, p, sk, st);
-      default: return launch_linear_sk<256>(tw, tx, p, sk, st);
-    }
-  }
-  // weight-streaming GEMMs with at least one 128-feature tile per SM: the
-  // persistent schedule (whole tiles; MS_PK=0 disables, for A/B runs)
-  if (big && pk_enabled()) {
-    switch (bn) {
-      case 16: return launch_linear_pk<16>(tw, tx, p, st);
-      case 32: return launch_linear_pk<32>(tw, tx, p, st);
-      case 48: return launch_linear_pk<48>(tw, tx, p, st);
-      case 64: return launch_linear_pk<64>(tw, tx, p, st);
-      case 80: return launch_linear_pk<80>(tw, tx, p, st);
-      case 96: return launch_linear_pk<96>(tw, tx, p, st);
-      case 112: return launch_linear_pk<112>(tw, tx, p, st);
-      case 128: return launch_linear_pk<128>(tw, tx, p, st);
-      case 144: return launch_linear_pk<144>(tw, tx, p, st);
-      case 160: return launch_linear_pk<160>(tw, tx, p, st);
-      case 176: return launch_linear_pk<176>(tw, tx, p, st);
-      case 192: return launch_linear_pk<192>(tw, tx, p, st);
-      case 208: return launch_linear_pk<208>(tw, tx, p, st);
-      case 224: return launch_linear_pk<224>(tw, tx, p, st);
-      case 240: return launch_linear_pk<240>(tw, tx, p, st);
-      default: return launch_linear_pk<256>(tw, tx, p, st);
-    }
-  }
   if (splits <= 0) splits = linear_auto_splits(N, K);
   if (splits > kb_total) splits = kb_total;
   if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
   if (rms.out && (splits < 2 || act == 2 || out_f32)) return MS_ERR_UNSUPPORTED;  // producer: split-K bf16 path
   p.splits = splits;
-  switch (bn) {
-    case 16: return launch_linear<16>(tw, tx, p, m_tiles, st, G);
-    case 32: return launch_linear<32>(tw, tx, p, m_tiles, st, G);
-    case 48: return launch_linear<48>(tw, tx, p, m_tiles, st, G);
-    case 64: return launch_linear<64>(tw, tx, p, m_tiles, st, G);
-    case 80: return launch_linear<80>(tw, tx, p, m_tiles, st, G);
-    case 96: return launch_linear<96>(tw, tx, p, m_tiles, st, G);
-    case 112: return launch_linear<112>(tw, tx, p, m_tiles, st, G);
-    case 128: return launch_linear<128>(tw, tx, p, m_tiles, st, G);
-    case 144: return launch_linear<144>(tw, tx, p, m_tiles, st, G);
-    case 160: return launch_linear<160>(tw, tx, p, m_tiles, st, G);
-    case 176: return launch_linear<176>(tw, tx, p, m_tiles, st, G);
-    case 192: return launch_linear<192>(tw, tx, p, m_tiles, st, G);
-    case 208: return launch_linear<208>(tw, tx, p, m_tiles, st, G);
-    case 224: return launch_linear<224>(tw, tx, p, m_tiles, st, G);
-    case 240: return launch_linear<240>(tw, tx, p, m_tiles, st, G);
-    default: return launch_linear<256>(tw, tx, p, m_tiles, st, G);
-  }
+  return launch_bn(bn, tw, tx, p, m_tiles, (cudaStream_t)stream, G);
 }
 
-extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
-                         const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-                         int M, int N, int K, int act, int splits, void* ws, int64_t ws_bytes,
-                         int* counters, int n_counters, void* stream) {
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, ws,
-                     ws_bytes, counters, n_counters, nullptr, nullptr, 0.f, stream);
+extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                         int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act, int splits,
+                         int w_blocked, void* stream) {
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, w_blocked, stream);
 }
-
-extern "C" int ms_linear_ln(const void* x, int64_t ldx, const void* gamma, const void* beta, float eps,
-                            const void* w, const void* bias, const void* residual, int64_t ldr,
-                            void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
-                            int splits, void* stream) {
-  if (!gamma || !beta) return MS_ERR_VALUE;
-  if (residual && residual == x) return MS_ERR_VALUE;  // the raw rows are re-read for statistics
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr,
-                     0, nullptr, 0, gamma, beta, eps, stream);
-}
-
 
 extern "C" int ms_linear_grouped(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                                  int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                                  int splits, int G, void* stream) {
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
-                     nullptr, nullptr, 0.f, stream, G);
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, 0, stream, G);
 }
 
 extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                              int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                              int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
-                             int64_t rms_ld, void* stream) {
+                             int64_t rms_ld, int w_blocked, void* stream) {
   if ((rms_in && rms_nparts < 1) || (!rms_in && !rms_out) || (rms_in && rms_ld < rms_nparts) ||
       (rms_out && rms_ld < (N + 127) / 128))
     return MS_ERR_VALUE;
@@ -1660,8 +168,8 @@ extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const vo
   r.nparts = rms_nparts;
   r.ld = rms_ld;
   r.eps = rms_eps;
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, nullptr, 0, nullptr, 0,
-                     nullptr, nullptr, 0.f, stream, 1, r);
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, w_blocked, stream, 1,
+                     r);
 }
 
 extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, const void* residual, int64_t ldr,
@@ -1676,12 +184,5 @@ extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, c
   r.tp_slice = N / t;
   r.tp_rows = rows;
   // `out` is unused on this path but must be a valid pointer for the checks
-  return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, nullptr, 0,
-                     nullptr, 0, nullptr, nullptr, 0.f, stream, 1, r);
+  return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, 0, stream, 1, r);
 }
-
-#ifdef MS_EXP_TIMING
-extern "C" int ms_exp_stamps(unsigned long long* host, int n) {
-  return cudaMemcpyFromSymbol(host, ms::g_exp_stamps, (size_t)n * 4 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -5;
-}
-#endif

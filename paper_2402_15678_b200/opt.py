@@ -35,12 +35,6 @@ class OPTModel:
     """Batched forward over the kernels with static activation buffers (so a
     forward of a given (B, Q) can be captured in a CUDA graph)."""
 
-    # fuse LayerNorm into the QKV / FC1 GEMMs when rows x d is at most this
-    # (every GEMM CTA re-reads the rows for their statistics).  Off by default:
-    # measured slower on the OPT-125M decode chain (2.51 vs 2.17 ms per draft
-    # round) — the statistics pass sits on the GEMM's critical path, so the
-    # saved launch is paid back; MS_FUSE_LN=1 enables it.
-    FUSE_LN_ELEMS = 131072 if os.environ.get("MS_FUSE_LN", "0") == "1" else 0
     SPLIT_KV = os.environ.get("MS_SPLITKV", "0") == "1"
 
     def __init__(self, w: OPTWeights, max_rows: int, device="cuda", small_gemm: bool = False):
@@ -59,14 +53,6 @@ class OPTModel:
         self.ff = torch.empty((max_rows, c.ffn), dtype=BF16, device=device)
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self._aws: dict = {}
-        # GEMM schedule: cluster split-K (measured faster than the persistent
-        # stream-K path, whose tile fix-up is a serial tail — tools/probe_gemm_graph.py);
-        # MS_STREAM_K=1 selects stream-K (scratch is per model = per stream)
-        self.ws = None
-        if os.environ.get("MS_STREAM_K", "0") == "1":
-            self.ws = K.Workspace(self.device)
-            for n, k in ((3 * c.d, c.d), (c.d, c.d), (c.ffn, c.d), (c.d, c.ffn), (c.vocab, c.d)):
-                self.ws.fit(min(max_rows, 256), n, k)
 
     def _attn_ws(self, B: int, Q: int, T: int):
         """Split-KV attention scratch, one per (B, Q, T) shape (allocated on the
@@ -92,12 +78,9 @@ class OPTModel:
         if R > self.max_rows:
             raise ValueError(f"{R} rows exceed max_rows={self.max_rows}")
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
-        ws = self.ws
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
         # split-KV attention is opt-in: measured slower at these context lengths
         aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
-        # small (decode-sized) activations: LayerNorm fused into the next GEMM
-        fuse_ln = R * c.d <= self.FUSE_LN_ELEMS
         small = self.small_gemm and R <= 64
 
         def lin(xx, wname, bname, **kw):
@@ -105,28 +88,20 @@ class OPTModel:
             # short K; long-K projections (FC2) keep the cluster split-K path
             if small and xx.shape[1] <= 1024:
                 return K.gemv(xx, w[wname], w[bname], stream=stream, **kw)
-            return K.linear(xx, w[wname], w[bname], ws=ws, stream=stream, **kw)
+            return K.linear(xx, w[wname], w[bname], stream=stream, **kw)
 
         for i in range(c.n_layers):
             p = f"l{i}."
-            if fuse_ln and not small:
-                K.linear_ln(x, w[p + "ln1_g"], w[p + "ln1_b"], w[p + "w_qkv"], w[p + "b_qkv"], c.eps,
-                            out=qkv, stream=stream)
-            else:
-                K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
-                lin(h, p + "w_qkv", p + "b_qkv", out=qkv)
+            K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
+            lin(h, p + "w_qkv", p + "b_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
                         self.scale, out=at, ws=aws, stream=stream, page=getattr(cache, "page", None))
             lin(at, p + "w_o", p + "b_o", residual=x, out=x)
-            if fuse_ln and not small:
-                K.linear_ln(x, w[p + "ln2_g"], w[p + "ln2_b"], w[p + "w_fc1"], w[p + "b_fc1"], c.eps,
-                            act=1, out=ff, stream=stream)
-            else:
-                K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
-                lin(h, p + "w_fc1", p + "b_fc1", act=1, out=ff)
+            K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
+            lin(h, p + "w_fc1", p + "b_fc1", act=1, out=ff)
             lin(ff, p + "w_fc2", p + "b_fc2", residual=x, out=x)
         Rh = R if head_rows is None else head_rows.numel()
         hf = self.h[:Rh]
         K.layernorm(x, w["lnf_g"], w["lnf_b"], c.eps, out=hf, rows=head_rows, stream=stream)
-        K.linear(hf, w["tok_emb"], out=logits, out_f32=True, ws=ws, stream=stream)
+        K.linear(hf, w["tok_emb"], out=logits, out_f32=True, stream=stream)
         return logits

@@ -18,7 +18,7 @@ def declared_symbols():
 def test_header_declares_entry_points():
     syms = declared_symbols()
     for s in ("ms_vote", "ms_accept_greedy", "ms_argmax_rows", "ms_linear", "ms_attention",
-              "ms_linear_workspace", "ms_draft_commit", "ms_pack_verify"):
+              "ms_linear_splits", "ms_draft_commit", "ms_pack_verify"):
         assert s in syms, s
 
 

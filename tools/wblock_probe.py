@@ -20,9 +20,7 @@ SHAPES = [("qkv", 10240, 8192, 0), ("o", 8192, 8192, 0), ("gu", 57344, 8192, 2),
           ("head", 32000, 8192, 0)]
 
 
-def blocked(w):
-    N, Kd = w.shape
-    return w.view(N // 128, 128, Kd // 64, 64).permute(0, 2, 1, 3).contiguous()
+blocked = K.block_weight
 
 
 def graph_of(fn):
@@ -56,16 +54,13 @@ for name, N, Kd, act in SHAPES:
         Nout = N // 2 if act == 2 else N
         outs = [torch.empty(M, Nout, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16) for _ in range(2)]
 
-        def run(wl, o):
+        def run(wl, o, blk):
             def f():
                 for w in wl:
-                    K.linear(x, w.view(N, Kd), out=o, out_f32=f32, act=act)
+                    K.linear(x, w, out=o, out_f32=f32, act=act, w_blocked=blk)
             return f
-        os.environ["MS_EXP_WBLOCKED"] = "0"
-        g_row = graph_of(run(ws, outs[0]))
-        os.environ["MS_EXP_WBLOCKED"] = "1"
-        g_blk = graph_of(run(wb, outs[1]))
-        os.environ["MS_EXP_WBLOCKED"] = "0"
+        g_row = graph_of(run(ws, outs[0], False))
+        g_blk = graph_of(run(wb, outs[1], True))
         same = bool(torch.equal(outs[0], outs[1]))
         tr, tb = [], []
         for _ in range(3):
