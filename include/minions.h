@@ -143,6 +143,18 @@ int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, c
                   int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                   int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
                   int64_t rms_ld, int w_blocked, void* stream);
+/* Compute-bound linear layer for prompt prefill (M >= 256 token rows; any M
+ * accepted): same contract as ms_linear (bias / ReLU / residual / gated SiLU
+ * with N % 128 == 0, bf16 or fp32 out), on CTA pairs — tcgen05.mma
+ * cta_group::2 over a 256-feature x 256-token tile (128 tokens when M < 256),
+ * persistent over tiles with a double-buffered TMEM accumulator.  Full-K
+ * accumulation in k order: deterministic; NOT split like ms_linear, so the
+ * decode / verify path (whose per-row results must not depend on M) keeps
+ * ms_linear.  Replaces the prefill GEMMs' cuBLAS calls.
+ * Limits: K % 8 == 0, ldx % 8 == 0, x and w 16-byte aligned. */
+int ms_linear_wide(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
+                   int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
+                   void* stream);
 /* Low-latency projection for M <= 64 token rows (the drafters' decode steps):
  * same contract as ms_linear (bias / ReLU / residual, bf16 or fp32 out), one
  * CTA per 16 output features, K split over 4 warps reduced in shared memory,

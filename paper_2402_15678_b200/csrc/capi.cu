@@ -26,6 +26,7 @@ int preload_model();
 int preload_attention();
 int preload_gemv();
 int preload_gemm();
+int preload_wide();
 int preload_tp();
 int preload_fp32();
 }  // namespace ms
@@ -35,7 +36,7 @@ extern "C" int ms_version(void) { return 200; }
 extern "C" int ms_preload(void) {
   const int bad = ms::preload_accept() + ms::preload_accept_stochastic() + ms::preload_vote() +
                   ms::preload_spec() + ms::preload_model() + ms::preload_attention() + ms::preload_gemv() +
-                  ms::preload_gemm() + ms::preload_tp() + ms::preload_fp32();
+                  ms::preload_gemm() + ms::preload_wide() + ms::preload_tp() + ms::preload_fp32();
   return bad ? MS_ERR_CUDA : MS_OK;
 }
 

@@ -369,11 +369,12 @@ class SpecEngine:
         for c0 in range(0, P, self.PREFILL_CHUNK):
             tc = t[:, c0: c0 + self.PREFILL_CHUNK].contiguous()
             st = torch.full((B,), c0, dtype=I32, device=self.dev)
-            self.target.forward(tc, st, self.slot, self.t_cache, tgt_dummy, head_rows=empty)
+            self.target.forward(tc, st, self.slot, self.t_cache, tgt_dummy, head_rows=empty, prefill=True)
             for m, c in zip(self.ssms, self.s_caches):
-                m.forward(tc, st, self.slot, c, dummy, head_rows=empty)
+                m.forward(tc, st, self.slot, c, dummy, head_rows=empty, prefill=True)
             if self.grouped:
-                self.ssm_g.forward(tc.repeat(G, 1), st.repeat(G), gslot, self.s_cache_g, dummy, head_rows=empty)
+                self.ssm_g.forward(tc.repeat(G, 1), st.repeat(G), gslot, self.s_cache_g, dummy, head_rows=empty,
+                                   prefill=True)
 
     def set_teacher(self, teacher: dict) -> None:
         """Target greedy continuations (request id -> tokens after the prompt)
@@ -789,7 +790,7 @@ class SpecEngine:
         for c0 in range(0, P, self.PREFILL_CHUNK):
             self.target.forward(tt[:, c0: c0 + self.PREFILL_CHUNK].contiguous(),
                                 torch.full((B,), c0, dtype=I32, device=self.dev), self.slot, cache, dummy,
-                                head_rows=empty)
+                                head_rows=empty, prefill=True)
         out = {r.id: [] for r in requests}
         lens = np.array([len(c) for c in ctx] + [1] * (B - len(ctx)))
         cur = np.array([c[-1] for c in ctx] + [0] * (B - len(ctx)), np.int32)

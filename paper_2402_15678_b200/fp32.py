@@ -98,7 +98,7 @@ class _F32Model:
 class OPTModelF32(_F32Model):
     """OPT-style decoder in fp32 (contract: oracle/opt_ref.forward(exact=True))."""
 
-    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
+    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None, prefill: bool = False):
         self._check(tokens, cache)
         c, w = self.cfg, self.w
         B, Q = tokens.shape
@@ -133,7 +133,7 @@ class LlamaModelF32(_F32Model):
         c = self.cfg
         self.rope = rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
 
-    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
+    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None, prefill: bool = False):
         self._check(tokens, cache)
         c, w = self.cfg, self.w
         if cache.max_len > c.max_pos:

@@ -56,6 +56,33 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
     return out
 
 
+def linear_wide(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
+                residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
+                out_f32: bool = False, stream=None) -> torch.Tensor:
+    """Prefill GEMM on tcgen05 CTA pairs (ms_linear_wide): same contract as
+    linear(); full-K accumulation (not M-invariant like linear's split-K)."""
+    if x.dim() != 2 or w.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
+        raise ValueError("x [M, K] and w [N, K] must be 2-D bf16")
+    M, K = x.shape
+    N = w.shape[0]
+    if w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
+        raise ValueError("shape/stride mismatch")
+    No = N // 2 if act == 2 else N
+    if out is None:
+        out = torch.empty((M, No), dtype=torch.float32 if out_f32 else BF16, device=x.device)
+    if out.stride(1) != 1 or out.shape != (M, No):
+        raise ValueError(f"out must be [M, {No}] with unit column stride")
+    if residual is not None and (residual.shape != (M, N) or residual.stride(1) != 1):
+        raise ValueError("residual must be [M, N]")
+    _native.call("ms_linear_wide", x.data_ptr(), x.stride(0), w.data_ptr(),
+                 None if bias is None else _dev.ptr(bias, BF16, "bias"),
+                 None if residual is None else residual.data_ptr(),
+                 0 if residual is None else residual.stride(0),
+                 out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act,
+                 _dev.stream_ptr(stream))
+    return out
+
+
 def block_weight(w: torch.Tensor) -> torch.Tensor:
     """[N, K] row-major -> tile-blocked [N/128, K/64, 128, 64] (contiguous):
     every 128 x 64 TMA tile of the weight one contiguous 16 KB run."""

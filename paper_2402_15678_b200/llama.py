@@ -37,16 +37,16 @@ class LlamaModel:
     """Batched forward over the kernels with static activation buffers (CUDA
     graph capturable), same interface as opt.OPTModel.
 
-    Prompt prefill (R >= PREFILL_ROWS token rows, SURVEY §8f — outside the
-    speculate-vote-verify path) is compute-bound: its layer GEMMs go to cuBLAS
-    as plain library GEMMs (measured 1.4-1.55 PFLOP/s vs 0.6-1.0 for the
-    weight-streaming ms_linear at M = 2032, tools/prefill_gemm_probe.py);
-    every decode / verify / drafter GEMM (R <= 16 * 13 rows) is ms_linear or
-    ms_gemv.  The row threshold is a constant, so a given call shape always
-    takes the same path (deterministic; prefill caches are identical for the
-    greedy teacher and the speculative run)."""
+    Prompt prefill (forward(..., prefill=True) from the engine's prompt
+    chunks) is compute-bound: with >= PREFILL_ROWS token
+    rows its layer GEMMs run on ms_linear_wide (tcgen05 CTA pairs,
+    csrc/gemm_pair.cu).  Every decode / verify / drafter GEMM is ms_linear or
+    ms_gemv whatever its row count — their per-row results never depend on
+    how many rows share a launch (the lossless property); the prefill path is
+    chosen by the caller, never by the row count, and the greedy teacher and
+    the speculative run prefill with identical calls."""
 
-    PREFILL_ROWS = 512
+    PREFILL_ROWS = 128
 
     def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False,
                  fuse_norm: bool | None = None):
@@ -118,7 +118,8 @@ class LlamaModel:
         return self._aws[key]
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
-                logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None,
+                prefill: bool = False) -> torch.Tensor:
         """Run Q positions for B requests (contract of OPTModel.forward)."""
         c, w = self.cfg, self.w
         B, Q = tokens.shape
@@ -130,7 +131,7 @@ class LlamaModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         K.embed(tokens, start, Q, w["tok_emb"], None, 0, out=x, stream=stream)
         small = self.small_gemm and R <= 64
-        prefill = R >= self.PREFILL_ROWS
+        prefill = prefill and R >= self.PREFILL_ROWS
         if self.fuse_norm and not prefill:
             return self._forward_fused(tokens, start, slot, cache, logits, head_rows, stream)
 
@@ -190,23 +191,10 @@ class LlamaModel:
 
 def _prefill_linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residual=None, act: int = 0,
                     stream=None) -> torch.Tensor:
-    """Prefill GEMM on cuBLAS (plain library GEMM, see LlamaModel): out =
-    x @ w^T (+ residual, in place when out is residual) or, act=2, the gated
-    SiLU of the 64-row interleaved gate/up weight from fp32 GEMM outputs
-    (fp32 silu * up, one bf16 rounding: ms_gated_silu, the same formula as
-    ms_linear's epilogue)."""
-    with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
-        if act == 2:
-            gu = torch.mm(x, w.t(), out_dtype=torch.float32)
-            return K.gated_silu(gu, out, stream=stream)
-        if residual is not None:
-            if out.data_ptr() == residual.data_ptr():
-                out.addmm_(x, w.t())
-            else:
-                torch.addmm(residual, x, w.t(), out=out)
-            return out
-        torch.mm(x, w.t(), out=out)
-        return out
+    """Prefill GEMM on tcgen05 CTA pairs (ms_linear_wide): out = x @ w^T
+    (+ residual, in place when out is residual) or, act=2, the gated SiLU of
+    the 64-row interleaved gate/up weight (fused epilogue)."""
+    return K.linear_wide(x, w, residual=residual, act=act, out=out, stream=stream)
 
 
 class GroupedLlamaModel:
@@ -239,7 +227,7 @@ class GroupedLlamaModel:
         self.scale = 1.0 / math.sqrt(c.head_dim)
         self.rope = K.rope_table(c.max_pos, c.head_dim, c.rope_theta, device=device)
 
-    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
+    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None, prefill: bool = False):
         c, t, G = self.cfg, self.t, self.G
         GB, Q = tokens.shape
         B = GB // G
@@ -252,7 +240,7 @@ class GroupedLlamaModel:
 
         def lin(xx, name, **kw):
             wt = t[name]  # [G, N, K]
-            if M >= LlamaModel.PREFILL_ROWS:  # prompt prefill: per-group cuBLAS (see LlamaModel)
+            if prefill and M >= LlamaModel.PREFILL_ROWS:  # prompt prefill: per-group ms_linear_wide
                 out, res = kw["out"], kw.get("residual")
                 for g in range(G):
                     sl = slice(g * M, (g + 1) * M)

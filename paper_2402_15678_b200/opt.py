@@ -64,7 +64,8 @@ class OPTModel:
         return self._aws[key]
 
     def forward(self, tokens: torch.Tensor, start: torch.Tensor, slot: torch.Tensor, cache: KVCache,
-                logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                logits: torch.Tensor, head_rows: torch.Tensor | None = None, stream=None,
+                prefill: bool = False) -> torch.Tensor:
         """Run Q positions for B requests.
 
         tokens [B, Q] int32: row b holds the tokens at positions start[b] .. start[b]+Q-1
@@ -82,8 +83,12 @@ class OPTModel:
         # split-KV attention is opt-in: measured slower at these context lengths
         aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
         small = self.small_gemm and R <= 64
+        # prompt prefill (caller-chosen, never by row count): tcgen05 CTA-pair GEMMs
+        wide = prefill and R >= 128
 
         def lin(xx, wname, bname, **kw):
+            if wide:
+                return K.linear_wide(xx, w[wname], w[bname], stream=stream, **kw)
             # ms_gemv only where it measured faster (tools/probe_gemm_graph.py):
             # short K; long-K projections (FC2) keep the cluster split-K path
             if small and xx.shape[1] <= 1024:

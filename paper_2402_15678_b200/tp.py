@@ -259,8 +259,9 @@ class LlamaTPModel(LlamaModel):
         import os
         self.fused = os.environ.get("MS_TP_FUSED", "1") != "0"
 
-    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None):
-        """Rank-local vocab slice of the logits ([R', V/t] fp32)."""
+    def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None, prefill: bool = False):
+        """Rank-local vocab slice of the logits ([R', V/t] fp32).  prefill: the
+        same tensor-parallel GEMMs (ms_linear; the row-parallel epilogues scatter)."""
         c, w, cm = self.cfg, self.w, self.comm
         B, Q = tokens.shape
         R = B * Q

@@ -160,7 +160,7 @@ def test_llama_forward_prefill_and_decode_vs_reference(small_gemm, name):
     slot = torch.arange(B, dtype=torch.int32, device="cuda")
     lg = torch.empty(B * T0, cfg.vocab, device="cuda")
     model.forward(torch.tensor(toks[:, :T0], device="cuda"), torch.zeros(B, dtype=torch.int32, device="cuda"),
-                  slot, cache, lg)
+                  slot, cache, lg, prefill=True)
     outs = [lg.view(B, T0, -1).cpu()]
     for j in range(3):
         l1 = torch.empty(B, cfg.vocab, device="cuda")
@@ -255,9 +255,9 @@ def test_llama_engine_lossless_and_rounds_match_oracle():
 
 
 def test_llama_prefill_path_large_m_vs_reference():
-    """R >= PREFILL_ROWS token rows take the prefill (cuBLAS) GEMMs; the cache
-    they build is continued by the decode kernels: both against the fp32 CPU
-    reference."""
+    """A prompt-prefill forward (prefill=True, R >= PREFILL_ROWS token rows)
+    takes the tcgen05 CTA-pair GEMMs (ms_linear_wide); the cache it builds is
+    continued by the decode kernels: both against the fp32 CPU reference."""
     from paper_2402_15678_b200.llama import LlamaModel
     cfg, w_cpu = _tiny_llama(4)
     model = LlamaModel(w_cpu.to("cuda"), max_rows=1024)
@@ -269,7 +269,7 @@ def test_llama_prefill_path_large_m_vs_reference():
     slot = torch.arange(B, dtype=torch.int32, device="cuda")
     lg = torch.empty(B * T0, cfg.vocab, device="cuda")
     model.forward(torch.tensor(toks[:, :T0], device="cuda"), torch.zeros(B, dtype=torch.int32, device="cuda"),
-                  slot, cache, lg)
+                  slot, cache, lg, prefill=True)
     l3 = torch.empty(B * 3, cfg.vocab, device="cuda")
     model.forward(torch.tensor(toks[:, T0:], device="cuda"), torch.full((B,), T0, dtype=torch.int32, device="cuda"),
                   slot, cache, l3)
