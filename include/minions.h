@@ -252,6 +252,18 @@ int ms_draft_commit(const int32_t* tok, const int32_t* ctx_len, int B, int j, in
 int ms_pack_verify(const int32_t* last, const int32_t* path, int B, int S,
                    int32_t* vin, void* stream);
 
+/* K3 stochastic — the device form of ModelOracle.next_dist + ProbDist.sample
+ * (aggspec/oracles.py:146-150, aggspec/core.py:74-78) for a softmax model:
+ * row r of logits [R, ldl] fp32 -> probs[r*ldp ..] fp64 = exp(l - max) / S,
+ * S the NumPy pairwise sum of exp(l - max) (oracle/model_oracle.softmax64),
+ * and, when uniforms != NULL, tok[r] = searchsorted(cumsum(p), u[r*ldu],
+ * 'right') clamped to V-1 (sequential fp64 cumsum).  V <= 65536. */
+int ms_softmax_sample(const float* logits, int64_t ldl, int R, int V, const double* uniforms, int64_t ldu,
+                      double* probs, int64_t ldp, int32_t* tok, void* stream);
+/* out[b] = q[voted[b]][b]: q [K][B][S][V] fp64 draft distributions -> the
+ * voted drafter's [B][S][V] (select_majority's dists, aggspec/voting.py:133-139). */
+int ms_gather_voted(const double* q, const int32_t* voted, int K, int B, int S, int V, double* out,
+                    void* stream);
 /* ---- K10: stochastic accept (speculative sampling) ------------------------
  * verify() of aggspec/verification.py:29-77 on general distributions, bit-exact
  * given the same fp64 probabilities and uniforms:

@@ -33,6 +33,8 @@ _SIGS = {
     "ms_accept_greedy": [_P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "ms_argmax_rows": [_P, _I, _I, _I, _I64, _P, _P, _P],
     "ms_accept_greedy_logits": [_P, _P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "ms_softmax_sample": [_P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P],
+    "ms_gather_voted": [_P, _P, _I, _I, _I, _I, _P, _P],
     "ms_accept_stochastic": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _I, _P],
     "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _I, _P],

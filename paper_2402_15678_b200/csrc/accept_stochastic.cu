@@ -228,7 +228,72 @@ accept_stochastic_kernel(const int32_t* __restrict__ draft, const double* __rest
   }
 }
 
-int preload_accept_stochastic() { return preload_fn(accept_stochastic_kernel); }
+// K3 stochastic — one speculative model step's distribution and sample, the
+// device form of ModelOracle.next_dist + ProbDist.sample
+// (aggspec/oracles.py:146-150, aggspec/core.py:74-78) for a transformer
+// whose distribution is softmax(logits):
+//   p = exp(l - max) / sum(exp(l - max)) in fp64 over the fp32 logits, the
+//   sum NumPy's pairwise sum (the oracle adapter's softmax64,
+//   oracle/model_oracle.py), then sample = searchsorted(cumsum(p), u,
+//   'right') clamped to V-1 with the sequential fp64 cumsum.
+// One CTA per row; the row's probabilities are kept (probs) — the draft
+// distribution the verifier's K10 needs, or the target distribution.
+__global__ void __launch_bounds__(kSThreads)
+softmax_sample_kernel(const float* __restrict__ logits, int64_t ldl, int V, const double* __restrict__ u,
+                      int64_t ldu, double* __restrict__ probs, int64_t ldp, int32_t* __restrict__ tok) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ Leaf leaves[kMaxLeaves];
+  __shared__ double leaf_sum[kMaxLeaves];
+  __shared__ double chunk[1024];
+  __shared__ float s_red[kSThreads / 32];
+  __shared__ int s_nleaves, s_idx;
+  __shared__ double s_total;
+  const int r = blockIdx.x;
+  const float* l = logits + (int64_t)r * ldl;
+  double* p = probs + (int64_t)r * ldp;
+  // max over the fp32 logits (exact in any order)
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmaxf(mx, l[j]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+  if (threadIdx.x == 0) s_nleaves = np_pairwise_leaves(V, leaves);
+  __syncthreads();
+  mx = s_red[0];
+  for (int w = 1; w < kSThreads / 32; ++w) mx = fmaxf(mx, s_red[w]);
+  const double m64 = (double)mx;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) p[j] = exp((double)l[j] - m64);
+  __syncthreads();
+  const int nl = s_nleaves;
+  for (int k = threadIdx.x; k < nl; k += blockDim.x) leaf_sum[k] = np_pairwise_leaf(p + leaves[k].lo, leaves[k].n);
+  __syncthreads();
+  if (threadIdx.x == 0) s_total = np_pairwise_combine(V, leaf_sum);
+  __syncthreads();
+  const double total = s_total;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) p[j] = p[j] / total;
+  if (!u) return;
+  __syncthreads();
+  const int t = inverse_cdf_seq(p, V, u[(int64_t)r * ldu], chunk, &s_idx);
+  if (threadIdx.x == 0) tok[r] = t;
+}
+
+// The voted drafter's distributions of each request: out[b] = q[voted[b]][b]
+// (q [K][B][S][V] fp64 -> out [B][S][V]), the draft_dists select_majority
+// attaches (aggspec/voting.py:133-139).
+__global__ void gather_voted_kernel(const double* __restrict__ q, const int32_t* __restrict__ voted, int B,
+                                    int64_t SV, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.y;
+  const double* src = q + ((int64_t)voted[b] * B + b) * SV;
+  double* dst = out + (int64_t)b * SV;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < SV; j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[j];
+}
+
+int preload_accept_stochastic() {
+  return preload_fn(accept_stochastic_kernel) + preload_fn(softmax_sample_kernel) + preload_fn(gather_voted_kernel);
+}
 
 }  // namespace ms
 
@@ -247,4 +312,26 @@ extern "C" int ms_accept_stochastic(const int32_t* draft, const double* q, const
   return ms::launch(ms::accept_stochastic_kernel, dim3(B), dim3(ms::kSThreads), 0, (cudaStream_t)stream, 1,
                     draft, q, o, uniforms, remaining, stop_token, S, V, scratch, n_acc, emitted, n_emit,
                     finished, n_draws);
+}
+
+extern "C" int ms_softmax_sample(const float* logits, int64_t ldl, int R, int V, const double* uniforms,
+                                 int64_t ldu, double* probs, int64_t ldp, int32_t* tok, void* stream) {
+  if (R < 0 || V < 1 || ldl < V || ldp < V) return MS_ERR_VALUE;
+  if (V > ms::kMaxLeaves * 64) return MS_ERR_UNSUPPORTED;
+  if (R == 0) return MS_OK;
+  if (!logits || !probs || (uniforms && !tok)) return MS_ERR_VALUE;
+  return ms::launch(ms::softmax_sample_kernel, dim3(R), dim3(ms::kSThreads), 0, (cudaStream_t)stream, 1, logits,
+                    ldl, V, uniforms, ldu, probs, ldp, tok);
+}
+
+extern "C" int ms_gather_voted(const double* q, const int32_t* voted, int K, int B, int S, int V, double* out,
+                               void* stream) {
+  if (K < 1 || B < 0 || S < 1 || V < 1) return MS_ERR_VALUE;
+  if (B == 0) return MS_OK;
+  if (!q || !voted || !out) return MS_ERR_VALUE;
+  const int64_t SV = (int64_t)S * V;
+  int gx = (int)((SV + 255) / 256);
+  gx = gx > 64 ? 64 : gx;
+  return ms::launch(ms::gather_voted_kernel, dim3(gx, B), dim3(256), 0, (cudaStream_t)stream, 1, q, voted, B, SV,
+                    out);
 }

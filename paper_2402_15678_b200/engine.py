@@ -47,7 +47,7 @@ import torch
 
 from . import _dev
 from . import _native
-from .core import AggSpecError, EngineConfig, Request, RequestState, validate_config
+from .core import AggSpecError, EngineConfig, Request, RequestState, seeded_rng, validate_config
 import os
 
 from .llama import GroupedLlamaModel
@@ -55,7 +55,7 @@ from .models import make_model
 from .opt import KVCache
 from .rounds import NoProgress, commit_round  # noqa: F401  (NoProgress: public name)
 from .selector import SelectorState
-from .verification import AcceptOut
+from .verification import AcceptOut, peek_uniforms
 from .voting import WeightTable
 
 I32 = torch.int32
@@ -133,8 +133,11 @@ class _Group:
         self.gid, self.slot0, self.B = gid, slot0, B
         dev, K, s_cap, V = eng.dev, eng.K, eng.cfg.s_max, eng.V
         z = lambda *sh: torch.zeros(sh, dtype=I32, device=dev)  # noqa: E731
-        sizes = [("w", 2 * K), ("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
-                 ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
+        sizes = [("w", 2 * K)]
+        if eng.sampling:  # fp64 uniforms (even int32 offsets: right after the fp64 weights)
+            sizes += [("u_draft", 2 * K * B * s_cap), ("u_verify", 2 * B * (s_cap + 1))]
+        sizes += [("ctx_len", B), ("c_start", B), ("c_head", B), ("v_start", B),
+                  ("last", B), ("remaining", B), ("step_start", s_cap * B), ("c_tok", B * (s_cap + 1))]
         if eng.grouped:  # the drafters' inputs replicated per row group (drafter)
             sizes += [("g_c_start", K * B), ("g_c_head", K * B), ("g_step_start", s_cap * K * B),
                       ("g_c_tok", K * B * (s_cap + 1))]
@@ -151,16 +154,29 @@ class _Group:
             self.g_ws = torch.zeros(K * B, dtype=torch.int64, device=dev)
             self.g_logits = torch.empty(K * B, V, device=dev)
         self.w_dev = mv("w").view(torch.float64)
+        if eng.sampling:
+            # stochastic drafting / verification (K3 stochastic + K10): per-round
+            # uniforms of the reference's per-request streams, the K drafters'
+            # distributions [K, B, s, V] (kept for the verifier), the voted
+            # drafter's [B, s, V], the target's [B, s+1, V], K10 scratch
+            self.u_draft = mv("u_draft").view(torch.float64)    # [K*B, s_cap]
+            self.u_verify = mv("u_verify").view(torch.float64)  # [B, s+1] compact per round
+            f64 = lambda *sh: torch.zeros(sh, dtype=torch.float64, device=dev)  # noqa: E731
+            self.q = f64(K * B * s_cap * V)
+            self.qv = f64(B * s_cap * V)
+            self.o = f64(B * (s_cap + 1) * V)
+            self.k10_scratch = f64(B * V)
         self.ctx_len, self.c_start, self.c_head = mv("ctx_len"), mv("c_start"), mv("c_head")
         self.v_start, self.last, self.remaining = mv("v_start"), mv("last"), mv("remaining")
         self.step_start = mv("step_start").view(s_cap, B)
         self.c_tok = mv("c_tok")
-        rsz = [("n_acc", B), ("n_emit", B), ("finished", B), ("voted", B),
+        rsz = [("n_acc", B), ("n_emit", B), ("finished", B), ("voted", B), ("n_draws", B),
                ("emitted", B * (s_cap + 1)), ("tgt", B * (s_cap + 1)), ("drafts", B * K * s_cap),
                ("path", B * s_cap)]
         self.res, self.res_h, self.res_off = self._packed(rsz, dev)
         rv = lambda n: self.res[self.res_off[n][0]: sum(self.res_off[n])]  # noqa: E731
         self.drafts, self.path, self.voted = rv("drafts"), rv("path"), rv("voted")
+        self.n_draws = rv("n_draws")
         self.acc = AcceptOut(rv("n_acc"), rv("emitted"), rv("n_emit"), rv("finished"), rv("tgt"))
         self.slot = torch.arange(slot0, slot0 + B, dtype=I32, device=dev)
         self.req_key = z(B)
@@ -211,7 +227,7 @@ class SpecEngine:
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
                  record: bool = False, pipelined: bool = False, sync_time=None,
                  kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
-                 selector_time: str = "verify", sim_cost=None):
+                 selector_time: str = "verify", sim_cost=None, sampling: bool = False):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -230,7 +246,15 @@ class SpecEngine:
         period).  sim_cost: an object with t_llm(b, s) -> ms (the reference's
         CostModel, aggspec/oracles.py:157-183); when given the selector is fed
         t_llm(len(batch), s) exactly as the reference's simulated clock does,
-        which makes the s trajectory reproducible across runs (parity tests)."""
+        which makes the s trajectory reproducible across runs (parity tests).
+        sampling: stochastic decoding as the reference engine does it — every
+        drafter step SAMPLES from softmax(logits) with the request's
+        draft/{rid}/{sid} stream (draft_sequence, aggspec/oracles.py:135-153)
+        and keeps its distributions; the verifier runs speculative sampling
+        (K10, verify() of aggspec/verification.py:29-77) on the voted
+        drafter's and the target's distributions with the verify/{rid}
+        stream, advanced by the draws the device made (aggspec/engine.py:
+        232-248, 285-330).  Greedy (False) is the point-mass special case."""
         validate_config(cfg)
         if precision not in ("bf16", "fp32"):
             raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
@@ -238,6 +262,9 @@ class SpecEngine:
             raise ValueError("selector_time must be 'verify' or 'round'")
         if precision == "fp32" and kv_block_size > 0:
             raise ValueError("the fp32 verification mode uses a contiguous KV cache")
+        if sampling and fidelity is not None:
+            raise ValueError("fidelity injection replaces drafted tokens: greedy decoding only")
+        self.sampling = bool(sampling)
         self.precision = precision
         self.selector_time = selector_time
         self.sim_cost = sim_cost
@@ -262,6 +289,8 @@ class SpecEngine:
             rows_t = max(slots * (s_cap + 1), slots * min(max_len, self.PREFILL_CHUNK))
             self.target = make_model(target, max_rows=rows_t, device=device, precision=precision)
         self.tp = hasattr(self.target, "comm")
+        if self.tp and sampling:
+            raise ValueError("stochastic decoding needs full-vocabulary target logits (not tensor parallel)")
         self.Vt = self.target.cfg.vocab                       # width of the target's logits
         V = self.Vt * (self.target.tp if self.tp else 1)      # full vocabulary
         if any(w.cfg.vocab != V for w in drafters):
@@ -320,6 +349,10 @@ class SpecEngine:
         if len(requests) > self.B:
             raise ValueError(f"{len(requests)} requests exceed {self.B} slots")
         self.requests = list(requests)
+        if self.sampling:  # the reference's per-request streams (aggspec/engine.py:232-248)
+            self._draft_rngs = {(r.id, k): seeded_rng(self.cfg.seed, f"draft/{r.id}/{k}")
+                                for r in requests for k in range(self.K)}
+            self._verify_rngs = {r.id: seeded_rng(self.cfg.seed, f"verify/{r.id}") for r in requests}
         ctx = [list(r.prompt) + list(r.generated) for r in requests]
         if min(len(c) for c in ctx) < 1:
             raise ValueError("context must be non-empty")
@@ -432,8 +465,13 @@ class SpecEngine:
                 m.forward(tok_in, g.g_c_start, g.g_slot, self.s_cache_g, g.g_logits, head_rows=g.g_c_head)
             else:
                 m.forward(g.g_step_tok, g.g_step_start[j - 1], g.g_slot, self.s_cache_g, g.g_logits)
-            _native.call("ms_argmax_rows", g.g_logits.data_ptr(), 0, G * B, self.V, self.V,
-                         g.g_argmax.data_ptr(), g.g_ws.data_ptr(), sp)
+            if self.sampling:  # row k*B + b: drafter k, request b; q laid out [K, B, s, V]
+                _native.call("ms_softmax_sample", g.g_logits.data_ptr(), self.V, G * B, self.V,
+                             g.u_draft.data_ptr() + j * 8, self.cfg.s_max, g.q.data_ptr() + j * self.V * 8,
+                             s * self.V, g.g_argmax.data_ptr(), sp)
+            else:
+                _native.call("ms_argmax_rows", g.g_logits.data_ptr(), 0, G * B, self.V, self.V,
+                             g.g_argmax.data_ptr(), g.g_ws.data_ptr(), sp)
             _native.call("ms_draft_commit_grouped", g.g_argmax.data_ptr(), g.ctx_len.data_ptr(), B, j, G, s,
                          teacher, self.max_len, g.req_key.data_ptr(), fid if self.fidelity else None,
                          self.inject_seed, dr.data_ptr(), g.g_step_tok.data_ptr(), sp)
@@ -463,8 +501,14 @@ class SpecEngine:
                 m.forward(tok_in, g.c_start, g.slot, cache, g.ssm_logits[k], head_rows=g.c_head, stream=st)
             else:
                 m.forward(g.step_tok[k], g.step_start[j - 1], g.slot, cache, g.ssm_logits[k], stream=st)
-            _native.call("ms_argmax_rows", g.ssm_logits[k].data_ptr(), 0, B, self.V, self.V,
-                         g.argmax[k].data_ptr(), g.ssm_ws[k].data_ptr(), sp)
+            if self.sampling:
+                _native.call("ms_softmax_sample", g.ssm_logits[k].data_ptr(), self.V, B, self.V,
+                             g.u_draft.data_ptr() + (k * B * self.cfg.s_max + j) * 8, self.cfg.s_max,
+                             g.q.data_ptr() + (k * B * s * self.V + j * self.V) * 8, s * self.V,
+                             g.argmax[k].data_ptr(), sp)
+            else:
+                _native.call("ms_argmax_rows", g.ssm_logits[k].data_ptr(), 0, B, self.V, self.V,
+                             g.argmax[k].data_ptr(), g.ssm_ws[k].data_ptr(), sp)
             _native.call("ms_draft_commit", g.argmax[k].data_ptr(), g.ctx_len.data_ptr(), B, j, k,
                          self.K, s, teacher, self.max_len, g.req_key.data_ptr(), f,
                          self.inject_seed, dr.data_ptr(), g.step_tok[k].data_ptr(), sp)
@@ -477,6 +521,17 @@ class SpecEngine:
         logits = g.v_logits[: B * (s + 1)]
         self.target.forward(vin, g.v_start, g.slot, self.t_cache, logits)
         a = g.acc
+        if self.sampling:  # target distributions, the voted drafter's, speculative sampling (K10)
+            _native.call("ms_softmax_sample", logits.data_ptr(), V, B * (s + 1), V, None, 0, g.o.data_ptr(), V,
+                         None, sp)
+            _native.call("ms_gather_voted", g.q.data_ptr(), g.voted.data_ptr(), self.K, B, s, V, g.qv.data_ptr(),
+                         sp)
+            _native.call("ms_accept_stochastic", g.path.data_ptr(), g.qv.data_ptr(), g.o.data_ptr(),
+                         g.u_verify.data_ptr(), g.remaining.data_ptr(),
+                         -1 if self.cfg.stop_token is None else self.cfg.stop_token, B, s, V,
+                         g.k10_scratch.data_ptr(), a.n_acc.data_ptr(), a.emitted.data_ptr(), a.n_emit.data_ptr(),
+                         a.finished.data_ptr(), g.n_draws.data_ptr(), sp)
+            return
         if self.tp:  # vocab-parallel logits: cross-rank argmax, then accept
             R = B * (s + 1)
             self.target.argmax(logits, a.tgt_argmax[:R])
@@ -605,6 +660,20 @@ class SpecEngine:
 
         w = np.array([self.weights.weights[k] for k in range(self.K)], np.float64)  # snapshot
         put("w", w.view(np.int32))
+        if self.sampling:
+            # draft_sequence draws s uniforms per (request, drafter) per round; the
+            # verifier's uniforms are peeked (<= s + 1) and the stream advanced by
+            # the device's n_draws after the round (verification.peek_uniforms)
+            smax = self.cfg.s_max
+            ud = np.zeros((self.K, B, smax), np.float64)
+            uv = np.zeros((B, s + 1), np.float64)
+            for b in act:
+                rid = g.requests[b].id
+                for k in range(self.K):
+                    ud[k, b, :s] = self._draft_rngs[(rid, k)].random(s)
+                uv[b] = peek_uniforms(self._verify_rngs[rid], s + 1)
+            put("u_draft", ud.view(np.int32))
+            put("u_verify", uv.view(np.int32))
         put("ctx_len", lens)
         put("c_start", start)
         put("c_head", c_head)
@@ -671,6 +740,10 @@ class SpecEngine:
         drafts = get("drafts", B * self.K * s).reshape(B, self.K, s)
         t_verify = g.ev_v0.elapsed_time(g.ev_v1)
         t_draft = g.ev_d0.elapsed_time(g.ev_d1)
+        if self.sampling:  # advance each verify stream by the uniforms the device used
+            nd = get("n_draws")
+            for b in active:
+                self._verify_rngs[g.requests[b].id].random(int(nd[b]))
         # selector input (MonitorSample.t_llm): the verify's device time, as the
         # reference (aggspec/engine.py:322); "round" adds the draft time (the
         # sequential schedule's round period); sim_cost: the reference's

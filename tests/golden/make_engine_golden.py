@@ -23,6 +23,12 @@ prompts (aggspec/bench.py:177-186).  Recorded per scenario:
   * the smallest argmax margin (top-1 minus top-2 logit) any oracle call saw
     — the fp32 parity headroom, stated in the golden.
 
+Modes: "greedy" (point-mass oracles, the fp32 verification mode's greedy
+streams) and "sample" (softmax oracles: draft_sequence SAMPLES with each
+request's draft/{rid}/{sid} stream and verify() runs speculative sampling
+with verify/{rid} — the reference engine's stochastic path, which
+SpecEngine(sampling=True) reproduces).
+
 Scenarios: "random" = the configs[0] drafters verbatim (independent random
 init: acceptance ~0, every round rolls the drafters back); "layerskip" =
 drafter k is the target's embedding + its layer k (a random-init layer-skip
@@ -137,10 +143,11 @@ def main():
            "models": "cfg1: tiny-target (OPT 4L d256) + 3 x tiny-ssm (1L), weights OPTWeights.random(cfg, seed, "
                      "device='cpu') seeds 0 / 1..3 (std 0.02)",
            "scenarios": []}
-    for kind in ("random", "layerskip"):
+    for mode in ("greedy", "sample"):
+      for kind in ("random", "layerskip"):
         for schedule in ("sequential", "pipelined"):
-            sc = run(kind, schedule)
-            print(kind, schedule, "rounds", len(sc["verify"]), "mean_acc", round(sc["mean_accepted"], 3),
+            sc = run(kind, schedule, mode=mode)
+            print(mode, kind, schedule, "rounds", len(sc["verify"]), "mean_acc", round(sc["mean_accepted"], 3),
                   "s_path", [v["s"] for v in sc["verify"]][:24], "margin", sc["margin_min"],
                   "wall", sc["wall_s"], flush=True)
             out["scenarios"].append(sc)

@@ -3,7 +3,9 @@
 tests/golden/engine_streams.json holds what the unmodified reference engine
 (aggspec run_sequential / run_pipelined, aggspec/engine.py:619-671) produced
 on cfg1 when driven by fp32 CPU transformer oracles over the same weights
-(tests/golden/make_engine_golden.py).  SpecEngine(precision="fp32") — the
+(tests/golden/make_engine_golden.py), greedy (point-mass oracles) and
+stochastic (softmax oracles: sampled drafts, speculative-sampling verify with
+the reference's per-request PCG64 streams — SpecEngine(sampling=True)).  SpecEngine(precision="fp32") — the
 fp32 verification mode (csrc/fp32.cu) — must reproduce it exactly:
 
   * every request's generated token stream,
@@ -67,7 +69,10 @@ def _scenarios():
         return json.load(f)["scenarios"]
 
 
-@pytest.mark.parametrize("idx", range(4), ids=["random-seq", "random-pipe", "layerskip-seq", "layerskip-pipe"])
+_IDS = ["random-seq", "random-pipe", "layerskip-seq", "layerskip-pipe"]
+
+
+@pytest.mark.parametrize("idx", range(8), ids=[f"{m}-{i}" for m in ("greedy", "sample") for i in _IDS])
 def test_fp32_engine_reproduces_reference_engine(idx):
     from paper_2402_15678_b200.core import EngineConfig, Request
     from paper_2402_15678_b200.engine import SpecEngine
@@ -78,7 +83,8 @@ def test_fp32_engine_reproduces_reference_engine(idx):
                        s_min=c["s_min"], s_max=c["s_max"], initial_weights=(1.0, 1.0, 1.0), seed=c["seed"])
     pipelined = sc["schedule"] == "pipelined"
     eng = SpecEngine(target, drafters, cfg, slots=4, max_len=96, precision="fp32", pipelined=pipelined,
-                     record=True, adaptive=sc["adaptive"], sim_cost=_Cost(**sc["cost"]))
+                     record=True, adaptive=sc["adaptive"], sim_cost=_Cost(**sc["cost"]),
+                     sampling=sc["mode"] == "sample")
     reqs = [Request(rid, list(p), 64) for rid, p in sc["prompts"].items()]
     res = eng.run(reqs)
     assert res.outputs == sc["outputs"]
