@@ -122,14 +122,11 @@ int ms_accept_greedy_logits(const int32_t* draft, const void* logits, int is_bf1
  * cluster and reduce their fp32 partials through distributed shared memory in
  * rank order — deterministic and batch invariant (a row's result does not
  * depend on M: the partition depends only on N and K).
- * w_blocked = 1: w is stored tile-blocked, [N/128][K/64][128][64] (every
- * 128 x 64 TMA tile a contiguous 16 KB run; N % 128 == 0, K % 64 == 0) —
- * same arithmetic, bitwise the same result.
  * Limits: K % 8 == 0, ldx % 8 == 0, x and w 16-byte aligned.
  */
 int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
               const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32,
-              int M, int N, int K, int act, int splits, int w_blocked, void* stream);
+              int M, int N, int K, int act, int splits, void* stream);
 /* ms_linear with the RMSNorm folded across GEMMs (the norm's gain is
  * pre-multiplied into the consumer's weight, so no normalised activation is
  * written): rms_out != NULL — a residual-writing split-K GEMM (bf16 out,
@@ -142,7 +139,7 @@ int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias,
 int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                   int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                   int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
-                  int64_t rms_ld, int w_blocked, void* stream);
+                  int64_t rms_ld, void* stream);
 /* Compute-bound linear layer for prompt prefill (M >= 256 token rows; any M
  * accepted): same contract as ms_linear (bias / ReLU / residual / gated SiLU
  * with N % 128 == 0, bf16 or fp32 out), on CTA pairs — tcgen05.mma

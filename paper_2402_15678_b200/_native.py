@@ -36,8 +36,8 @@ _SIGS = {
     "ms_softmax_sample": [_P, _I64, _I, _I, _P, _I64, _P, _I64, _P, _P],
     "ms_gather_voted": [_P, _P, _I, _I, _I, _I, _P, _P],
     "ms_accept_stochastic": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
-    "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _I, _P],
-    "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _I, _P],
+    "ms_linear": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P],
+    "ms_linear_rms": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P, _I, _F, _P, _I64, _P],
     "ms_linear_wide": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
     "ms_gemv": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
     "ms_linear_splits": [_I, _I],

@@ -102,7 +102,7 @@ struct RmsArgs {
 
 static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                        int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act, int splits,
-                       int w_blocked, void* stream, int G = 1, RmsArgs rms = RmsArgs()) {
+                       void* stream, int G = 1, RmsArgs rms = RmsArgs()) {
   using namespace ms;
   if (M < 0 || N < 1 || K < 1 || ldx < K || ldc < (act == 2 ? N / 2 : N)) return MS_ERR_VALUE;
   if (M == 0) return MS_OK;
@@ -113,7 +113,6 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (K % 8 != 0 || ldx % 8 != 0) return MS_ERR_UNSUPPORTED;  // TMA: 16-byte row strides
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return MS_ERR_UNSUPPORTED;
   if (residual && ldr < N) return MS_ERR_VALUE;
-  if (w_blocked && (N % kBM || K % kBK)) return MS_ERR_UNSUPPORTED;
   if (G < 1 || G > 65535) return MS_ERR_VALUE;
   const int kb_total = (K + kBK - 1) / kBK;
   const int bn = pick_bn(M);
@@ -121,9 +120,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   const int n_tiles = (N + kBM - 1) / kBM;
   if (m_tiles > 65535) return MS_ERR_UNSUPPORTED;
   CUtensorMap tw, tx;
-  if (w_blocked ? !make_tmap(&tw, w, (int64_t)G * N * (K / kBK), kBK, kBK, kBM)
-                : !make_tmap(&tw, w, (int64_t)G * N, K, K, kBM))
-    return MS_ERR_CUDA;
+  if (!make_tmap(&tw, w, (int64_t)G * N, K, K, kBM)) return MS_ERR_CUDA;
   if (!make_tmap(&tx, x, (int64_t)G * M, K, ldx, bn)) return MS_ERR_CUDA;
   LinearParams p;
   p.M = M; p.N = N; p.K = K;
@@ -131,7 +128,7 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.residual = (const __nv_bfloat16*)residual;
   p.ldr = ldr;
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
-  p.kb_total = kb_total; p.n_tiles = n_tiles; p.w_blocked = w_blocked;
+  p.kb_total = kb_total; p.n_tiles = n_tiles;
   p.sw = p.sx = 0;
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
   p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
@@ -145,20 +142,20 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
 
 extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                          int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act, int splits,
-                         int w_blocked, void* stream) {
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, w_blocked, stream);
+                         void* stream) {
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, stream);
 }
 
 extern "C" int ms_linear_grouped(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                                  int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                                  int splits, int G, void* stream) {
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, 0, stream, G);
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, stream, G);
 }
 
 extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,
                              int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act,
                              int splits, const float* rms_in, int rms_nparts, float rms_eps, float* rms_out,
-                             int64_t rms_ld, int w_blocked, void* stream) {
+                             int64_t rms_ld, void* stream) {
   if ((rms_in && rms_nparts < 1) || (!rms_in && !rms_out) || (rms_in && rms_ld < rms_nparts) ||
       (rms_out && rms_ld < (N + 127) / 128))
     return MS_ERR_VALUE;
@@ -168,8 +165,7 @@ extern "C" int ms_linear_rms(const void* x, int64_t ldx, const void* w, const vo
   r.nparts = rms_nparts;
   r.ld = rms_ld;
   r.eps = rms_eps;
-  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, w_blocked, stream, 1,
-                     r);
+  return linear_impl(x, ldx, w, bias, residual, ldr, out, ldc, out_f32, M, N, K, act, splits, stream, 1, r);
 }
 
 extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, const void* residual, int64_t ldr,
@@ -184,5 +180,5 @@ extern "C" int ms_linear_tp_scatter(const void* x, int64_t ldx, const void* w, c
   r.tp_slice = N / t;
   r.tp_rows = rows;
   // `out` is unused on this path but must be a valid pointer for the checks
-  return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, 0, stream, 1, r);
+  return linear_impl(x, ldx, w, nullptr, residual, ldr, const_cast<void*>(x), N, 1, M, N, K, 0, 0, stream, 1, r);
 }

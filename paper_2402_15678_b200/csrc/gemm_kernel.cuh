@@ -29,9 +29,9 @@
 // invariance: a request's logits do not depend on what else is in the
 // verify batch).
 //
-// Weight layouts: nn.Linear row-major [G*N, K], or tile-blocked
-// [G][N/128][K/64][128][64] — every 128 x 64 TMA tile one contiguous 16 KB
-// run of HBM (LinearParams::w_blocked).
+// (A tile-blocked weight layout — every 128 x 64 TMA tile one contiguous
+// 16 KB run — measured no faster on the 70B shapes, profiles/
+// r2_wblock_layout_ab.jsonl, and was not kept.)
 #pragma once
 #include <cuda.h>
 
@@ -53,7 +53,6 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int sw, sx;                     // weight / token ring depths of this launch
-  int w_blocked;                  // weight layout (see the header comment)
   // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
   // output (row m, feature f) is stored straight into the receive slot of the
   // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
@@ -202,6 +201,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     tc::mbar_init(tmem_full, 1);
     tc::fence_barrier_init();
   }
+  __syncwarp();  // lane 0 of warp 0 diverged above: reconverge before the aligned barrier
   if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
@@ -215,14 +215,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       // kernel — issued before the programmatic-dependency wait (PDL prefetch)
       const uint64_t pol_w = tc::policy_evict_first();  // weights stream through once
       const int pre = nkb < SW ? nkb : SW;
-      // blocked layout: this tile's k-block run starts at row wblk
-      const int wblk = ((grp * p.n_tiles + tile_n) * p.kb_total + kb0) * kBM;
       for (int i = 0; i < pre; ++i) {
         tc::mbar_arrive_expect_tx(&fullW[i], C::W_BYTES);
-        if (p.w_blocked)
-          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], 0, wblk + i * kBM, pol_w);
-        else
-          tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
+        tc::tma_load_2d(sW + i * C::W_BYTES, &tmW, &fullW[i], (kb0 + i) * kBK, wrow, pol_w);
       }
       pdl_wait();
       pdl_trigger();
@@ -230,10 +225,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         const int st = i % SW;
         tc::mbar_wait(&emptyW[st], ((i / SW) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
-        if (p.w_blocked)
-          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], 0, wblk + i * kBM, pol_w);
-        else
-          tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
+        tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
       }
     } else {
       pdl_trigger();
@@ -367,6 +359,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       }
     }
   }
+  __syncwarp();  // producer / MMA roles ran on lane 0: reconverge before the aligned cluster / CTA barriers
   if (p.splits > 1) {
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA

@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     }
     tc::fence_barrier_init();
   }
+  __syncwarp();
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
                  "n"(2 * BN)
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) arrive_leader(&tempty[a]);
+          __syncwarp();
         }
         // stage [32 tokens][128 features] fp32, feature = q*32 + lane
 #pragma unroll
@@ -302,12 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-      if (m_hi <= 0) {  // (cannot happen: tiles cover [0, M)) keep the barrier count balanced
-        tc::fence_before_sync();
-        if (lane == 0) arrive_leader(&tempty[a]);
-      }
     }
   }
+  __syncwarp();  // producer / MMA roles ran on lane 0: reconverge before the aligned cluster barrier
   tc::fence_before_sync();
   cluster_sync();  // the peer's MMAs / epilogue reads of this CTA's smem and TMEM are done
   if (warp == 1) {

@@ -22,24 +22,16 @@ def linear_splits(N: int, K: int) -> int:
 
 def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
            residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
-           out_f32: bool = False, splits: int = 0, w_blocked: bool = False, stream=None) -> torch.Tensor:
+           out_f32: bool = False, splits: int = 0, stream=None) -> torch.Tensor:
     """out = act(x @ w.T + bias) + residual on tcgen05 (ms_linear, cluster
     split-K).  act=2: gated SiLU over a 64-row interleaved gate/up weight, out
-    [M, N/2].  w_blocked: w holds the [N, K] weight tile-blocked
-    (block_weight(); any shape with N * K elements)."""
-    if x.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
-        raise ValueError("x [M, K] and w must be bf16")
+    [M, N/2]."""
+    if x.dim() != 2 or w.dim() != 2 or x.dtype != BF16 or w.dtype != BF16:
+        raise ValueError("x [M, K] and w [N, K] must be 2-D bf16")
     M, K = x.shape
-    if w_blocked:
-        if not w.is_contiguous() or w.numel() % K:
-            raise ValueError("blocked weight must be contiguous with N * K elements")
-        N = w.numel() // K
-    else:
-        if w.dim() != 2 or w.shape[1] != K or not w.is_contiguous():
-            raise ValueError("w must be [N, K] contiguous")
-        N = w.shape[0]
-    if x.stride(1) != 1:
-        raise ValueError("x must have unit column stride")
+    N = w.shape[0]
+    if w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
+        raise ValueError("shape/stride mismatch")
     No = N // 2 if act == 2 else N
     if out is None:
         out = torch.empty((M, No), dtype=torch.float32 if out_f32 else BF16, device=x.device)
@@ -52,7 +44,7 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
                  None if residual is None else residual.data_ptr(),
                  0 if residual is None else residual.stride(0),
                  out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act,
-                 splits, int(w_blocked), _dev.stream_ptr(stream))
+                 splits, _dev.stream_ptr(stream))
     return out
 
 
@@ -83,15 +75,6 @@ def linear_wide(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = No
     return out
 
 
-def block_weight(w: torch.Tensor) -> torch.Tensor:
-    """[N, K] row-major -> tile-blocked [N/128, K/64, 128, 64] (contiguous):
-    every 128 x 64 TMA tile of the weight one contiguous 16 KB run."""
-    N, K = w.shape
-    if N % 128 or K % 64:
-        raise ValueError("blocked layout needs N % 128 == 0 and K % 64 == 0")
-    return w.reshape(N // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous()
-
-
 def gated_silu(gu: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """out [M, N/2] bf16 = silu(gate) * up of an fp32 gate/up GEMM output gu
     [M, N] over the 64-row interleaved weight (ms_gated_silu: the act=2
@@ -107,21 +90,14 @@ def gated_silu(gu: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor
 
 def linear_rms(x: torch.Tensor, w: torch.Tensor, *, residual: torch.Tensor | None = None, act: int = 0,
                out: torch.Tensor, out_f32: bool = False, rms_in: torch.Tensor | None = None, eps: float = 1e-5,
-               rms_out: torch.Tensor | None = None, w_blocked: bool = False, N: int | None = None,
-               stream=None) -> torch.Tensor:
+               rms_out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """ms_linear with the RMSNorm folded across GEMMs: rms_in [rows, n_parts]
     fp32 partial sums of squares (from the producer) -> scale by rstd; rms_out
-    [rows, N / 128] fp32 -> this (residual-writing, split-K) GEMM emits them.
-    w_blocked: w is tile-blocked (block_weight()), N its row count."""
+    [rows, N / 128] fp32 -> this (residual-writing, split-K) GEMM emits them."""
     M, K = x.shape
-    if w_blocked:
-        N = w.numel() // K if N is None else N
-    else:
-        N = w.shape[0]
-        if w.shape[1] != K:
-            raise ValueError("x [M, K] and w [N, K] must agree")
-    if x.dtype != BF16 or w.dtype != BF16 or not w.is_contiguous():
-        raise ValueError("x and w must be bf16, w contiguous")
+    N = w.shape[0]
+    if x.dtype != BF16 or w.dtype != BF16 or w.shape[1] != K or not w.is_contiguous():
+        raise ValueError("x [M, K] and w [N, K] must be bf16")
     ref = rms_in if rms_in is not None else rms_out
     if ref is None or ref.dtype != torch.float32 or not ref.is_contiguous():
         raise ValueError("rms partial buffers must be contiguous fp32 [parts, ld]")
@@ -129,8 +105,7 @@ def linear_rms(x: torch.Tensor, w: torch.Tensor, *, residual: torch.Tensor | Non
                  None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
                  out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, 0,
                  None if rms_in is None else rms_in.data_ptr(), 0 if rms_in is None else rms_in.shape[1], eps,
-                 None if rms_out is None else rms_out.data_ptr(), ref.stride(0), int(w_blocked),
-                 _dev.stream_ptr(stream))
+                 None if rms_out is None else rms_out.data_ptr(), ref.stride(0), _dev.stream_ptr(stream))
     return out
 
 

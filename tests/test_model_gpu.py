@@ -231,30 +231,3 @@ def test_drafter_forward_small_gemm_vs_reference():
         ref = opt_ref.forward(w_cpu.t, cfg, toks[b])
         err = (got[b] - ref).abs().max().item() / ref.abs().max().item()
         assert err < 2e-2, err
-
-
-@pytest.mark.parametrize("M,N,K,act", [(112, 57344, 1024, 2), (176, 10240, 8192, 0), (16, 32000, 768, 0),
-                                       (80, 8192, 28672, 0), (1, 2304, 768, 0), (300, 1024, 256, 2)])
-def test_blocked_weight_layout_bitwise_equal(M, N, K, act):
-    """The tile-blocked weight layout (block_weight: every 128 x 64 TMA tile a
-    contiguous 16 KB run) is the same arithmetic: bitwise equal outputs, also
-    through the folded-RMSNorm entry point."""
-    from paper_2402_15678_b200 import kernels as Kn
-    g = torch.Generator().manual_seed(M + N + K)
-    x = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
-    w = (torch.randn(N, K, generator=g) * 0.03).to(torch.bfloat16).cuda()
-    r = None if act == 2 else torch.randn(M, N, generator=g).to(torch.bfloat16).cuda()
-    wb = Kn.block_weight(w)
-    assert wb.shape == (N // 128, K // 64, 128, 64)
-    assert torch.equal(wb[1, 2, 3, 4], w[128 + 3, 2 * 64 + 4])
-    for sp in (0, 1):
-        a = Kn.linear(x, w, residual=r, act=act, splits=sp)
-        b = Kn.linear(x, wb, residual=r, act=act, splits=sp, w_blocked=True)
-        assert torch.equal(a, b), sp
-    rin = torch.rand(M, 8, generator=g).cuda() * K
-    No = N // 2 if act == 2 else N
-    o1 = torch.empty(M, No, dtype=torch.bfloat16, device="cuda")
-    o2 = torch.empty_like(o1)
-    Kn.linear_rms(x, w, act=act, out=o1, rms_in=rin, eps=1e-5)
-    Kn.linear_rms(x, wb, act=act, out=o2, rms_in=rin, eps=1e-5, w_blocked=True, N=N)
-    assert torch.equal(o1, o2)

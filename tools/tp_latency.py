@@ -33,9 +33,17 @@ for R in (16, 80, 176):
     graphs = [torch.cuda.CUDAGraph() for _ in range(t)]
 
     def body(r, capture):
+        try:
+            _body(r, capture)
+        except Exception as e:  # surface thread errors
+            errs.append(e)
+
+    errs = []
+
+    def _body(r, capture):
         with torch.cuda.stream(streams[r]):
             if capture:
-                with torch.cuda.graph(graphs[r], stream=streams[r]):
+                with torch.cuda.graph(graphs[r], stream=streams[r], capture_error_mode="thread_local"):
                     for _ in range(N):
                         comms[r].allreduce_norm(R, gamma, 1e-5, outs[r])
             else:
@@ -52,6 +60,8 @@ for R in (16, 80, 176):
 
     both(False)  # warm (eager)
     both(True)   # capture (no kernels run)
+    if errs:
+        raise errs[0]
     ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(t)]
     torch.cuda.synchronize()
     for rep in range(2):
