@@ -91,7 +91,7 @@ int ms_accept_greedy(const int32_t* draft, const int32_t* tgt_argmax,
  * of np.argmax (aggspec/core.py:81-85).
  *   logits [R, ld] (fp32 if is_bf16 == 0, else bf16), first V columns used
  *   out    [R] int32
- *   ws     [R] uint64 scratch (contents clobbered)
+ *   ws     unused (kept for ABI stability; may be NULL) — one CTA per row
  */
 int ms_argmax_rows(const void* logits, int is_bf16, int R, int V, int64_t ld,
                    int32_t* out, void* ws, void* stream);

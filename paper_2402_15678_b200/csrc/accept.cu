@@ -13,107 +13,10 @@
 namespace ms {
 
 // ---------------------------------------------------------------------------
-// Row argmax.  Each (chunk, row) block reduces a slice of the row to a packed
-// 64-bit key (ordered value << 32 | ~index) and merges it with atomicMax, which
-// realises "max value, then smallest index" independent of arrival order.
+// Row argmax: max value, then the smallest index (np.argmax's first index).
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ uint64_t argmax_key(float v, int idx) {
-  v += 0.0f;  // -0.0 -> +0.0 (np.argmax treats them equal)
-  uint32_t u = __float_as_uint(v);
-  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-  return ((uint64_t)u << 32) | (uint32_t)(0xffffffffu - (uint32_t)idx);
-}
-
-__device__ __forceinline__ int key_index(uint64_t k) {
-  return (int)(0xffffffffu - (uint32_t)(k & 0xffffffffu));
-}
-
 constexpr int kArgmaxThreads = 256;
-
-template <bool kBf16>
-__global__ void __launch_bounds__(kArgmaxThreads)
-argmax_rows_kernel(const void* __restrict__ logits, int V, int64_t ld, int chunk,
-                   unsigned long long* __restrict__ ws) {
-  pdl_wait();
-  pdl_trigger();
-  const int row = blockIdx.y;
-  const int lo = blockIdx.x * chunk;
-  const int hi = min(V, lo + chunk);
-  float best = -INFINITY;
-  int bidx = 0x7fffffff;
-  if constexpr (kBf16) {
-    const __nv_bfloat16* p = (const __nv_bfloat16*)logits + row * ld;
-    // vector body: 8 bf16 per load when the slice start is 16B aligned
-    int i = lo + threadIdx.x * 8;
-    const bool vec = ((((uintptr_t)(p + lo)) & 15) == 0);
-    if (vec) {
-      for (; i + 8 <= hi; i += kArgmaxThreads * 8) {
-        bf16x8 v = *reinterpret_cast<const bf16x8*>(p + i);
-        float f[8];
-        unpack8(v, f);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) argmax_merge(best, bidx, f[j], i + j);
-      }
-      // tail
-      const int tail0 = lo + ((hi - lo) / 8) * 8;
-      for (int t = tail0 + threadIdx.x; t < hi; t += kArgmaxThreads)
-        argmax_merge(best, bidx, bf2f(p[t]), t);
-    } else {
-      for (int t = lo + threadIdx.x; t < hi; t += kArgmaxThreads)
-        argmax_merge(best, bidx, bf2f(p[t]), t);
-    }
-  } else {
-    const float* p = (const float*)logits + row * ld;
-    const bool vec = ((((uintptr_t)(p + lo)) & 15) == 0);
-    if (vec) {
-      int i = lo + threadIdx.x * 4;
-      for (; i + 4 <= hi; i += kArgmaxThreads * 4) {
-        float4 v = *reinterpret_cast<const float4*>(p + i);
-        argmax_merge(best, bidx, v.x, i);
-        argmax_merge(best, bidx, v.y, i + 1);
-        argmax_merge(best, bidx, v.z, i + 2);
-        argmax_merge(best, bidx, v.w, i + 3);
-      }
-      const int tail0 = lo + ((hi - lo) / 4) * 4;
-      for (int t = tail0 + threadIdx.x; t < hi; t += kArgmaxThreads)
-        argmax_merge(best, bidx, p[t], t);
-    } else {
-      for (int t = lo + threadIdx.x; t < hi; t += kArgmaxThreads)
-        argmax_merge(best, bidx, p[t], t);
-    }
-  }
-  warp_argmax(best, bidx);
-  __shared__ float sv[kArgmaxThreads / 32];
-  __shared__ int si[kArgmaxThreads / 32];
-  const int w = threadIdx.x >> 5;
-  if (lane_id() == 0) {
-    sv[w] = best;
-    si[w] = bidx;
-  }
-  __syncthreads();
-  if (w == 0) {
-    best = lane_id() < kArgmaxThreads / 32 ? sv[lane_id()] : -INFINITY;
-    bidx = lane_id() < kArgmaxThreads / 32 ? si[lane_id()] : 0x7fffffff;
-    warp_argmax(best, bidx);
-    if (lane_id() == 0 && bidx != 0x7fffffff)
-      atomicMax(ws + row, (unsigned long long)argmax_key(best, bidx));
-  }
-}
-
-__global__ void argmax_init_kernel(unsigned long long* ws, int R) {
-  pdl_wait();
-  pdl_trigger();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < R) ws[i] = 0ull;
-}
-
-__global__ void argmax_finalize_kernel(const unsigned long long* ws, int R, int32_t* out) {
-  pdl_wait();
-  pdl_trigger();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < R) out[i] = ws[i] ? key_index(ws[i]) : 0;  // all-NaN row -> 0 like np.argmax
-}
 
 // ---------------------------------------------------------------------------
 // Greedy accept: one warp per request, lanes sweep the s positions 32 at a time.
@@ -171,29 +74,74 @@ accept_greedy_kernel(const int32_t* __restrict__ draft, const int32_t* __restric
   }
 }
 
+// One CTA per row: the whole row is reduced in one block (vectorised loads,
+// fixed first-index tie-break) — one launch, no scratch, no atomics.  (The
+// earlier chunked atomicMax variant needed init + rows + finalize launches; in
+// a drafter step those three tiny launches sat on the critical path.)
+template <bool kBf16>
+__global__ void __launch_bounds__(kArgmaxThreads)
+argmax_row_kernel(const void* __restrict__ logits, int V, int64_t ld, int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x;
+  float best = -INFINITY;
+  int bidx = 0x7fffffff;
+  if constexpr (kBf16) {
+    const __nv_bfloat16* p = (const __nv_bfloat16*)logits + row * ld;
+    int v0 = 0;
+    if ((((uintptr_t)p) & 15) == 0) {
+      const int nv = V / 8;
+      for (int c = threadIdx.x; c < nv; c += kArgmaxThreads) {
+        float f[8];
+        unpack8(*reinterpret_cast<const bf16x8*>(p + c * 8), f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) argmax_merge(best, bidx, f[j], c * 8 + j);
+      }
+      v0 = nv * 8;
+    }
+    for (int t = v0 + threadIdx.x; t < V; t += kArgmaxThreads) argmax_merge(best, bidx, bf2f(p[t]), t);
+  } else {
+    const float* p = (const float*)logits + row * ld;
+    int v0 = 0;
+    if ((((uintptr_t)p) & 15) == 0) {
+      const int nv = V / 4;
+      for (int c = threadIdx.x; c < nv; c += kArgmaxThreads) {
+        const float4 v = *reinterpret_cast<const float4*>(p + c * 4);
+        argmax_merge(best, bidx, v.x, c * 4);
+        argmax_merge(best, bidx, v.y, c * 4 + 1);
+        argmax_merge(best, bidx, v.z, c * 4 + 2);
+        argmax_merge(best, bidx, v.w, c * 4 + 3);
+      }
+      v0 = nv * 4;
+    }
+    for (int t = v0 + threadIdx.x; t < V; t += kArgmaxThreads) argmax_merge(best, bidx, p[t], t);
+  }
+  warp_argmax(best, bidx);
+  __shared__ float sv[kArgmaxThreads / 32];
+  __shared__ int si[kArgmaxThreads / 32];
+  const int w = threadIdx.x >> 5;
+  if (lane_id() == 0) {
+    sv[w] = best;
+    si[w] = bidx;
+  }
+  __syncthreads();
+  if (w == 0) {
+    best = lane_id() < kArgmaxThreads / 32 ? sv[lane_id()] : -INFINITY;
+    bidx = lane_id() < kArgmaxThreads / 32 ? si[lane_id()] : 0x7fffffff;
+    warp_argmax(best, bidx);
+    if (lane_id() == 0) out[row] = bidx == 0x7fffffff ? 0 : bidx;  // all-NaN row -> 0
+  }
+}
+
 static int launch_argmax(const void* logits, int is_bf16, int R, int V, int64_t ld,
-                         unsigned long long* ws, int32_t* out, cudaStream_t st) {
-  // enough (chunk,row) blocks to cover the SMs a few times over
-  int chunks = (4 * 148 + R - 1) / R;
-  const int max_chunks = (V + 2047) / 2048;
-  chunks = max(1, min(chunks, max_chunks));
-  int chunk = (V + chunks - 1) / chunks;
-  chunk = (chunk + 7) & ~7;  // keep slices 16B aligned for bf16 / fp32 vectors
-  chunks = (V + chunk - 1) / chunk;
-  const int tb = 256;
-  int s = launch(argmax_init_kernel, dim3((R + tb - 1) / tb), dim3(tb), 0, st, 1, ws, R);
-  if (s) return s;
-  dim3 grid(chunks, R);
-  s = is_bf16 ? launch(argmax_rows_kernel<true>, grid, dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, chunk, ws)
-              : launch(argmax_rows_kernel<false>, grid, dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, chunk, ws);
-  if (s) return s;
-  return launch(argmax_finalize_kernel, dim3((R + tb - 1) / tb), dim3(tb), 0, st, 1,
-                (const unsigned long long*)ws, R, out);
+                         unsigned long long* /*ws: unused*/, int32_t* out, cudaStream_t st) {
+  return is_bf16 ? launch(argmax_row_kernel<true>, dim3(R), dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, out)
+                 : launch(argmax_row_kernel<false>, dim3(R), dim3(kArgmaxThreads), 0, st, 1, logits, V, ld, out);
 }
 
 int preload_accept() {
-  return preload_fn(argmax_rows_kernel<true>) + preload_fn(argmax_rows_kernel<false>) +
-         preload_fn(argmax_init_kernel) + preload_fn(argmax_finalize_kernel) + preload_fn(accept_greedy_kernel);
+  return preload_fn(argmax_row_kernel<true>) + preload_fn(argmax_row_kernel<false>) +
+         preload_fn(accept_greedy_kernel);
 }
 
 }  // namespace ms
