@@ -38,15 +38,15 @@ class LlamaModel:
     graph capturable), same interface as opt.OPTModel.
 
     Prompt prefill (forward(..., prefill=True) from the engine's prompt
-    chunks) is compute-bound: with >= PREFILL_ROWS token
-    rows its layer GEMMs run on ms_linear_wide (tcgen05 CTA pairs,
-    csrc/gemm_pair.cu).  Every decode / verify / drafter GEMM is ms_linear or
+    chunks) is compute-bound: its layer GEMMs run on
+    ms_linear_wide (tcgen05 CTA pairs, csrc/gemm_pair.cu) whatever the chunk's
+    row count (full-K accumulation in k order: a row's result does not depend
+    on the chunking, tests/test_paged_gpu.py).  Every decode / verify / drafter GEMM is ms_linear or
     ms_gemv whatever its row count — their per-row results never depend on
     how many rows share a launch (the lossless property); the prefill path is
     chosen by the caller, never by the row count, and the greedy teacher and
     the speculative run prefill with identical calls."""
 
-    PREFILL_ROWS = 128
 
     def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False,
                  fuse_norm: bool | None = None):
@@ -131,7 +131,6 @@ class LlamaModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         K.embed(tokens, start, Q, w["tok_emb"], None, 0, out=x, stream=stream)
         small = self.small_gemm and R <= 64
-        prefill = prefill and R >= self.PREFILL_ROWS
         if self.fuse_norm and not prefill:
             return self._forward_fused(tokens, start, slot, cache, logits, head_rows, stream)
 
@@ -240,7 +239,7 @@ class GroupedLlamaModel:
 
         def lin(xx, name, **kw):
             wt = t[name]  # [G, N, K]
-            if prefill and M >= LlamaModel.PREFILL_ROWS:  # prompt prefill: per-group ms_linear_wide
+            if prefill:  # prompt prefill: per-group ms_linear_wide
                 out, res = kw["out"], kw.get("residual")
                 for g in range(G):
                     sl = slice(g * M, (g + 1) * M)

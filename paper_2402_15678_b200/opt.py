@@ -84,7 +84,7 @@ class OPTModel:
         aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
         small = self.small_gemm and R <= 64
         # prompt prefill (caller-chosen, never by row count): tcgen05 CTA-pair GEMMs
-        wide = prefill and R >= 128
+        wide = prefill
 
         def lin(xx, wname, bname, **kw):
             if wide:

@@ -71,8 +71,9 @@ def test_engine_paged_kv_same_tokens_and_frees_rejected(pipelined):
 
 def test_chunked_prefill_same_generation():
     """Prompt prefill in 8-position chunks (SURVEY §8f chunked prefill) gives
-    exactly the generations of a one-chunk prefill (every forward here stays
-    below the cuBLAS prefill threshold, and the kernels are batch-invariant)."""
+    exactly the generations of a one-chunk prefill (the prefill GEMMs,
+    ms_linear_wide, accumulate the full K in k order whatever the chunk's row
+    count, and the other kernels are batch-invariant)."""
     from paper_2402_15678_b200.core import EngineConfig, Request
     from paper_2402_15678_b200.engine import SpecEngine
     from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
