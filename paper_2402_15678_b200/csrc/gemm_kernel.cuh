@@ -157,7 +157,11 @@ __device__ __forceinline__ float4 ld_dsmem_f4(const float* local, int rank) {
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+// minBlocks 2: two CTAs per SM must fit the register file (<= 146 registers
+// per thread at 224 threads) — the decode / verify GEMMs run at two CTAs per
+// SM, and a register-limited single CTA per SM cost 35-55% of their speed
+// (tools/ab_lib_gemm.py, round 2)
+__global__ void __launch_bounds__(kThreads, 2)
 linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const LinearParams p) {
   using C = LinearCfg<BN>;
