@@ -91,7 +91,9 @@ def bench_config(args, ws: int, tp: bool) -> dict:
             "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
                    "streamed per verify)"),
             "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
-            "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous"}
+            "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous",
+            "sm_partition": (f"drafters on a {args.draft_sms}-SM green context, verifier on the rest"
+                             if args.draft_sms and args.schedule == "pipelined" else "shared")}
 
 
 def parse():
@@ -128,6 +130,8 @@ def parse():
     ap.add_argument("--parallelism", default="tp", choices=["tp", "replicas"],
                     help="N>1: tensor-parallel verifier over the ranks (default, SURVEY §8e) or one full "
                          "replica per GPU serving its own batch")
+    ap.add_argument("--draft-sms", type=int, default=0,
+                    help="pipelined: SMs of the drafters' green context (the verifier gets the rest); 0 = shared")
     ap.add_argument("--schedule", default="pipelined", choices=["sequential", "pipelined"],
                     help="pipelined (cfg3, default): two request groups of --batch each (verify batch "
                          "--batch, 2x requests in flight), verify of one overlapping drafting of the "
@@ -326,7 +330,8 @@ def run_ours(args, rank, ws):
     drafters = [random_weights(scfg, k + 1, device="cuda") for k in range(K)]
     eng = SpecEngine(target, drafters, cfg, slots=n_req, max_len=max_len,
                      use_graphs=not args.no_graphs, fidelity=fid, pipelined=pipelined,
-                     adaptive=not args.fixed_s, sync_time=sync, kv_block_size=args.kv_block_size)
+                     adaptive=not args.fixed_s, sync_time=sync, kv_block_size=args.kv_block_size,
+                     draft_sms=args.draft_sms if pipelined else 0)
     if tp:  # every rank serves the same global batch
         reqs = make_requests(n_req, args.prompt_len, args.new_tokens, tcfg.vocab)
     else:

@@ -404,6 +404,17 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
                      const int32_t* slot, const int32_t* start, int T, float* k_cache, float* v_cache,
                      const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
 
+/* ---- SM partition for the pipelined schedule ------------------------------
+ * Replaces: the reference's separate SSM / LLM executors of run_pipelined
+ * (aggspec/engine.py:494-576 — drafting of one batch concurrent with the
+ * verification of another); the paper places SSMs on their own devices.  On
+ * one GPU: two green contexts splitting the SMs (draft_sms for the drafters,
+ * the rest for the verifier), one stream each, returned as cudaStream_t
+ * (void*).  The contexts live for the process.  MS_ERR_UNSUPPORTED when the
+ * driver has no green contexts. */
+int ms_sm_partition(int device, int draft_sms, int draft_priority, int verify_priority,
+                    void** draft_stream, void** verify_stream, int* got_draft, int* got_verify);
+
 #ifdef __cplusplus
 }
 #endif

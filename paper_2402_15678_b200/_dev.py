@@ -41,3 +41,26 @@ def as_dev(x, dtype: torch.dtype, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=dtype).contiguous()
     return torch.as_tensor(x, dtype=dtype).to(device).contiguous()
+
+
+_PARTITIONS: dict = {}
+
+
+def sm_partition_streams(draft_sms: int, device: torch.device, draft_priority: int = 0,
+                         verify_priority: int = 0):
+    """(draft stream, verify stream, draft SMs, verify SMs) on two green
+    contexts splitting the device's SMs (ms_sm_partition) — created once per
+    (device, split, priorities) per process and reused by every engine."""
+    from . import _native
+    import ctypes
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    key = (dev, draft_sms, draft_priority, verify_priority)
+    if key not in _PARTITIONS:
+        sd, sv = ctypes.c_void_p(), ctypes.c_void_p()
+        nd, nv = ctypes.c_int(), ctypes.c_int()
+        _native.call("ms_sm_partition", dev, draft_sms, draft_priority, verify_priority, ctypes.byref(sd),
+                     ctypes.byref(sv), ctypes.byref(nd), ctypes.byref(nv))
+        d = torch.device("cuda", dev)
+        _PARTITIONS[key] = (torch.cuda.ExternalStream(sd.value, device=d),
+                            torch.cuda.ExternalStream(sv.value, device=d), nd.value, nv.value)
+    return _PARTITIONS[key]

@@ -79,6 +79,8 @@ _SIGS = {
     "ms_kv_append_paged": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _P],
     "ms_attention_workspace_gqa": [_I, _I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int)],
+    "ms_sm_partition": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
     "ms_attention_workspace": [_I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
 }
 _RESTYPE = {"ms_strerror": ctypes.c_char_p, "ms_launch_count": ctypes.c_int64,

@@ -227,7 +227,8 @@ class SpecEngine:
                  fidelity: list[float] | None = None, inject_seed: int = 0, adaptive: bool = True,
                  record: bool = False, pipelined: bool = False, sync_time=None,
                  kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
-                 selector_time: str = "verify", sim_cost=None, sampling: bool = False):
+                 selector_time: str = "verify", sim_cost=None, sampling: bool = False,
+                 draft_sms: int = 0):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -254,7 +255,11 @@ class SpecEngine:
         (K10, verify() of aggspec/verification.py:29-77) on the voted
         drafter's and the target's distributions with the verify/{rid}
         stream, advanced by the draws the device made (aggspec/engine.py:
-        232-248, 285-330).  Greedy (False) is the point-mass special case."""
+        232-248, 285-330).  Greedy (False) is the point-mass special case.
+        draft_sms > 0 (pipelined): the draft and verify streams live on two
+        green contexts splitting the GPU's SMs — draft_sms for the drafters,
+        the rest for the verifier (ms_sm_partition): the drafters' small
+        kernels no longer wait for, or displace, the verify GEMMs' CTAs."""
         validate_config(cfg)
         if precision not in ("bf16", "fp32"):
             raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
@@ -336,8 +341,16 @@ class SpecEngine:
         # both streams' kernels wait for SM slots): equal by default;
         # MS_VERIFY_PRIORITY=1 / MS_DRAFT_PRIORITY=1 raise one (A/B)
         hi = lambda k: -1 if os.environ.get(k, "0") == "1" else 0  # noqa: E731
-        self.draft_stream = torch.cuda.Stream(self.dev, priority=hi("MS_DRAFT_PRIORITY"))
-        self.verify_stream = torch.cuda.Stream(self.dev, priority=hi("MS_VERIFY_PRIORITY"))
+        self.draft_sms = self.verify_sms = 0
+        if draft_sms > 0:
+            if not pipelined:
+                raise ValueError("draft_sms partitions the SMs between concurrent drafting and "
+                                 "verification: pipelined schedule only")
+            self.draft_stream, self.verify_stream, self.draft_sms, self.verify_sms = _dev.sm_partition_streams(
+                draft_sms, self.dev, hi("MS_DRAFT_PRIORITY"), hi("MS_VERIFY_PRIORITY"))
+        else:
+            self.draft_stream = torch.cuda.Stream(self.dev, priority=hi("MS_DRAFT_PRIORITY"))
+            self.verify_stream = torch.cuda.Stream(self.dev, priority=hi("MS_VERIFY_PRIORITY"))
         self.requests: list[Request] = []
         self._run_t0 = None
 

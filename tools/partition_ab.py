@@ -1,0 +1,63 @@
+"""A/B of the pipelined schedule with and without an SM partition between the
+drafters and the verifier (SpecEngine(draft_sms=N), csrc/partition.cu), in one
+process on the bench workload (cfg3: Llama-2-70B + 3 x Llama-160M, two groups
+of 16, fidelity injection), interleaved so clock drift hits every arm alike.
+usage: python tools/partition_ab.py [splits=0,16,24,32] [fixed_s=6] [reps=2] [new_tokens=128]
+prints one JSON line per (rep, split)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+from paper_2402_15678_b200.core import EngineConfig
+from paper_2402_15678_b200.engine import SpecEngine
+from paper_2402_15678_b200.models import config, make_model, random_weights
+
+splits = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,16,24,32").split(",")]
+fixed_s = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+new_tokens = int(sys.argv[4]) if len(sys.argv) > 4 else 128
+tcfg, scfg = config("llama-2-70b"), config("llama-160m")
+fid = [0.9, 0.85, 0.8]
+cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=16, b_ssm=16, s_init=fixed_s or 4, s_min=1, s_max=12,
+                   initial_weights=(1.0,) * 3, seed=0)
+max_len = 128 + new_tokens + cfg.s_max + 4
+tw = random_weights(tcfg, 0)
+target = make_model(tw, max_rows=max(32 * (cfg.s_max + 1), 32 * max_len))
+drafters = [random_weights(scfg, k + 1) for k in range(3)]
+reqs = bench.make_requests(32, 128, new_tokens, tcfg.vocab)
+teacher = None
+for rep in range(reps):
+    for n in splits:
+        eng = SpecEngine(target, drafters, cfg, slots=32, max_len=max_len, fidelity=fid, pipelined=True,
+                         adaptive=not fixed_s, draft_sms=n)
+        eng.capture_graphs()
+        if teacher is None:
+            teacher = eng.greedy_teacher(bench.fresh(reqs), new_tokens)
+        out = []
+        for it in range(3):
+            rs = bench.fresh(reqs)
+            eng.prefill(rs)
+            eng.set_teacher(teacher)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            res = eng.decode()
+            e1.record()
+            torch.cuda.synchronize()
+            if it == 0:
+                continue  # warm-up
+            out.append((res.tokens / (e0.elapsed_time(e1) * 1e-3), res))
+        tps = sum(o[0] for o in out) / len(out)
+        rounds = [rd for _, r in out for rd in r.rounds]
+        print(json.dumps({"rep": rep, "draft_sms": n, "got": [eng.draft_sms, eng.verify_sms],
+                          "fixed_s": fixed_s, "tokens_per_s": round(tps, 1),
+                          "lossless": all(r.outputs == teacher for _, r in out),
+                          "verify_ms": round(sum(r.t_verify_ms for r in rounds) / len(rounds), 3),
+                          "draft_ms": round(sum(r.t_draft_ms for r in rounds) / len(rounds), 3),
+                          "mean_s": round(sum(r.s for r in rounds) / len(rounds), 2)}), flush=True)
+        del eng
+        torch.cuda.empty_cache()
