@@ -404,6 +404,12 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
                      const int32_t* slot, const int32_t* start, int T, float* k_cache, float* v_cache,
                      const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
 
+/* Programmatic dependent launch (PDL) attribute for subsequent launches of
+ * this process (default on; MS_PDL=0 in the environment turns it off); a
+ * captured CUDA graph keeps the setting it was captured with.  Returns the
+ * previous setting. */
+int ms_set_pdl(int on);
+
 /* ---- SM partition for the pipelined schedule ------------------------------
  * Replaces: the reference's separate SSM / LLM executors of run_pipelined
  * (aggspec/engine.py:494-576 — drafting of one batch concurrent with the

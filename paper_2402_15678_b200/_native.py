@@ -79,6 +79,7 @@ _SIGS = {
     "ms_kv_append_paged": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _P],
     "ms_attention_workspace_gqa": [_I, _I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int)],
+    "ms_set_pdl": [_I],
     "ms_sm_partition": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
     "ms_attention_workspace": [_I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],

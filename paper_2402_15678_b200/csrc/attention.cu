@@ -99,8 +99,7 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   constexpr int KC = D / 16;  // 16-dim chunks (MMA k-steps for Q.K^T)
   constexpr int NT = D / 8;   // 8-dim output tiles for P.V
   extern __shared__ __align__(16) uint8_t smem[];
-  pdl_wait();
-  pdl_trigger();
+  // (the programmatic-dependency wait comes after the cache prefetch below)
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem);  // [2][KT][LD]
   __nv_bfloat16* sV = sK + NBUF * S::TILE;                        // [NBUF][KT][LD]
 
@@ -130,6 +129,93 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
   const int QD = Hq * D, KVD = Hkv * D;
   constexpr int V8 = D / 8;
 
+  const int last_pos = pstart + (q0 + Q - 1) / G;
+  const int n_keys = min(last_pos + 1, T);  // keys 0 .. last position of the chunk
+  const int n_tiles_all = (n_keys + kKT - 1) / kKT;
+  // split-KV: this CTA owns tiles [tile0, tile1) — fixed 64*kct-key chunks
+  // from position 0, so a query's partition never depends on the other rows
+  const int n_chunks = (n_tiles_all + kct - 1) / kct;
+  if (kvc >= n_chunks) {  // nothing for this request here (uniform per CTA)
+    pdl_wait();
+    return;
+  }
+  const int tile0 = kvc * kct;
+  const int n_tiles = min(n_tiles_all, tile0 + kct);
+
+  // tile loader: thread -> fixed 16-byte column chunk `lc` and rows lr0 + p*LRS
+  // (no per-element index arithmetic); the call's own rows (t >= pstart) come
+  // straight from qkv (K rotated on the way when RoPE), older keys from the cache
+  constexpr int LRS = kAThreads / V8;  // rows per pass
+  constexpr int LNP = kKT / LRS;       // passes per tile
+  const int lc = tid % V8, lr0 = tid / V8;
+  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
+  const __nv_bfloat16* qkv_v = qkv_k + KVD;
+  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;  // RoPE partner chunk
+  // part 0: the rows cached by earlier calls (t < pstart) as cp.async,
+  // issued BEFORE the programmatic-dependency wait (they do not depend on the
+  // previous kernel: the KV stream's first latency overlaps its tail); part 1:
+  // the rest of the tile (the call's own rows from qkv — K rotated when RoPE —
+  // or from the cache when the caller appended; zeros past the keys) as
+  // synchronous stores after the wait; part 2: both (steady-state prefetch)
+  auto load_tile = [&](int tile, int buf, int part) {
+    const int t0 = tile * kKT;
+    __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
+    __nv_bfloat16* dv = sV + buf * S::TILE + lc * 8;
+#pragma unroll
+    for (int pp = 0; pp < LNP; ++pp) {
+      const int j = lr0 + pp * LRS;
+      const int t = t0 + j;
+      const bool cached = t < n_keys && t < pstart;
+      if (part == 0) {
+        if (cached) {
+          cp_async16(dk + j * LD, kc + krow(t) + lc * 8);
+          cp_async16(dv + j * LD, vc + krow(t) + lc * 8);
+        }
+        continue;
+      }
+      if (part == 1 && cached) continue;
+      if (t < n_keys) {
+        const bool fresh = fuse_append && t >= pstart;
+        const int64_t qrow = (int64_t)(t - pstart) * ldq;
+        if (fresh && rope) {
+          float fv[8], pf[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
+          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
+          *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
+        } else if (part == 1) {
+          *reinterpret_cast<uint4*>(dk + j * LD) =
+              *reinterpret_cast<const uint4*>(fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
+        } else {
+          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
+        }
+        if (part == 1)
+          *reinterpret_cast<uint4*>(dv + j * LD) =
+              *reinterpret_cast<const uint4*>(fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
+        else
+          cp_async16(dv + j * LD, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
+      } else {  // masked keys must be finite
+        *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    if (part != 1) cp_async_commit();
+  };
+
+  float m_r[2] = {-INFINITY, -INFINITY};  // rows g, g+8 (log2 domain)
+  float l_r[2] = {0.f, 0.f};
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+
+#pragma unroll
+  for (int pp = 0; pp < NBUF - 1; ++pp) {
+    if (tile0 + pp < n_tiles) load_tile(tile0 + pp, pp, 0);
+    else cp_async_commit();  // empty group: keeps the wait count uniform
+  }
+  pdl_wait();
+  pdl_trigger();
+  for (int pp = 0; pp < NBUF - 1 && tile0 + pp < n_tiles; ++pp) load_tile(tile0 + pp, pp, 1);
   if (fuse_append && kvc == 0 && qc == 0) {
     // this request's new K/V rows for KV head h -> cache (K rotated when
     // RoPE); this kernel reads them back from qkv, so no fence is needed
@@ -192,73 +278,14 @@ attention_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, i
       }
     }
   }
-
-  const int last_pos = pstart + (q0 + Q - 1) / G;
-  const int n_keys = min(last_pos + 1, T);  // keys 0 .. last position of the chunk
-  const int n_tiles_all = (n_keys + kKT - 1) / kKT;
-  // split-KV: this CTA owns tiles [tile0, tile1) — fixed 64*kct-key chunks
-  // from position 0, so a query's partition never depends on the other rows
-  const int n_chunks = (n_tiles_all + kct - 1) / kct;
-  if (kvc >= n_chunks) return;  // nothing for this request here (uniform per CTA)
-  const int tile0 = kvc * kct;
-  const int n_tiles = min(n_tiles_all, tile0 + kct);
-
-  // tile loader: thread -> fixed 16-byte column chunk `lc` and rows lr0 + p*LRS
-  // (no per-element index arithmetic); the call's own rows (t >= pstart) come
-  // straight from qkv (K rotated on the way when RoPE), older keys from the cache
-  constexpr int LRS = kAThreads / V8;  // rows per pass
-  constexpr int LNP = kKT / LRS;       // passes per tile
-  const int lc = tid % V8, lr0 = tid / V8;
-  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
-  const __nv_bfloat16* qkv_v = qkv_k + KVD;
-  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;  // RoPE partner chunk
-  auto load_tile = [&](int tile, int buf) {
-    const int t0 = tile * kKT;
-    __nv_bfloat16* dk = sK + buf * S::TILE + lc * 8;
-    __nv_bfloat16* dv = sV + buf * S::TILE + lc * 8;
-#pragma unroll
-    for (int pp = 0; pp < LNP; ++pp) {
-      const int j = lr0 + pp * LRS;
-      const int t = t0 + j;
-      if (t < n_keys) {
-        const bool fresh = fuse_append && t >= pstart;
-        const int64_t qrow = (int64_t)(t - pstart) * ldq;
-        if (fresh && rope) {
-          float fv[8], pf[8];
-          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
-          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
-          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
-          *reinterpret_cast<bf16x8*>(dk + j * LD) = pack8(fv);
-        } else {
-          cp_async16(dk + j * LD, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
-        }
-        cp_async16(dv + j * LD, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
-      } else {  // masked keys must be finite
-        *reinterpret_cast<uint4*>(dk + j * LD) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(dv + j * LD) = make_uint4(0, 0, 0, 0);
-      }
-    }
-    cp_async_commit();
-  };
-
-  float m_r[2] = {-INFINITY, -INFINITY};  // rows g, g+8 (log2 domain)
-  float l_r[2] = {0.f, 0.f};
-  float o[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   const int row_lim0 = g < Q ? pos0 : -1;      // last key position row g may see
   const int row_lim1 = g + 8 < Q ? pos1 : -1;
 
-#pragma unroll
-  for (int pp = 0; pp < NBUF - 1; ++pp) {
-    if (tile0 + pp < n_tiles) load_tile(tile0 + pp, pp);
-    else cp_async_commit();  // empty group: keeps the wait count uniform
-  }
   for (int tile = tile0; tile < n_tiles; ++tile) {
     const int it = tile - tile0;
     const int buf = it % NBUF;
     // refill the buffer the previous iteration consumed, NBUF-1 tiles ahead
-    if (tile + NBUF - 1 < n_tiles) load_tile(tile + NBUF - 1, (it + NBUF - 1) % NBUF);
+    if (tile + NBUF - 1 < n_tiles) load_tile(tile + NBUF - 1, (it + NBUF - 1) % NBUF, 2);
     else cp_async_commit();
     cp_async_wait<NBUF - 1>();
     __syncthreads();
@@ -512,8 +539,7 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   constexpr int NT = D / 8;
   constexpr int V8 = D / 8;
   extern __shared__ __align__(16) uint8_t smem[];
-  pdl_wait();
-  pdl_trigger();
+  // (the programmatic-dependency wait comes after the cache prefetch below)
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem);  // [kRRows][LD]
   __nv_bfloat16* sKV = sQ + S::Q_ELEMS;                          // [kRNR][2][K|V][kRKT][LD]
 
@@ -550,9 +576,75 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int n_keys = min(pstart + (c0 + crows - 1) / G + 1, T);
   const int n_rounds_all = (n_keys + 2 * kRKT - 1) / (2 * kRKT);
   const int n_chunks = (n_rounds_all + kct - 1) / kct;
-  if (kvc >= n_chunks) return;  // uniform per CTA (the unit's arrival count excludes it)
+  if (kvc >= n_chunks) {  // uniform per CTA (the unit's arrival count excludes it)
+    pdl_wait();
+    return;
+  }
   const int r0 = kvc * kct;
   const int n_rounds = min(n_rounds_all, r0 + kct) - r0;
+
+  constexpr int LRS = kRThreads / V8;   // key rows per pass
+  const int lc = tid % V8, lr0 = tid / V8;
+  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
+  const __nv_bfloat16* qkv_v = qkv_k + KVD;
+  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;
+  // round rd = keys 64rd .. 64rd+63: tile 2rd (key group 0), tile 2rd+1 (group 1).
+  // part 0: the rows cached by earlier calls (t < pstart) as cp.async — they
+  //         do not depend on the previous kernel, so the first rounds are
+  //         requested BEFORE the programmatic-dependency wait (the KV stream's
+  //         first DRAM latency overlaps the QKV GEMM's tail);
+  // part 1: the rest of the round (the call's own rows, straight from qkv with
+  //         K rotated when RoPE, or from the cache when the caller appended;
+  //         zeros past the keys), synchronous stores, after the wait;
+  // part 2: both, as cp.async where possible (the steady-state prefetch).
+  auto load_round = [&](int rd, int rb, int part) {
+    const int t0 = rd * 2 * kRKT;
+    for (int j = lr0; j < 2 * kRKT; j += LRS) {
+      const int t = t0 + j;
+      __nv_bfloat16* dk = sKV + ((rb * 2 + j / kRKT) * 2) * S::TILE + (j % kRKT) * LD + lc * 8;
+      __nv_bfloat16* dv = dk + S::TILE;
+      const bool cached = t < n_keys && t < pstart;
+      if (part == 0) {
+        if (cached) {
+          cp_async16(dk, kc + krow(t) + lc * 8);
+          cp_async16(dv, vc + krow(t) + lc * 8);
+        }
+        continue;
+      }
+      if (part == 1 && cached) continue;
+      if (t < n_keys) {
+        const bool fresh = fuse_append && t >= pstart;
+        const int64_t qrow = (int64_t)(t - pstart) * ldq;
+        if (fresh && rope) {
+          float fv[8], pf[8];
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
+          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
+          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
+          *reinterpret_cast<bf16x8*>(dk) = pack8(fv);
+        } else if (part == 1) {
+          *reinterpret_cast<uint4*>(dk) = *reinterpret_cast<const uint4*>(fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
+        } else {
+          cp_async16(dk, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
+        }
+        if (part == 1)
+          *reinterpret_cast<uint4*>(dv) = *reinterpret_cast<const uint4*>(fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
+        else
+          cp_async16(dv, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
+      } else {
+        *reinterpret_cast<uint4*>(dk) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(dv) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    if (part != 1) cp_async_commit();
+  };
+#pragma unroll
+  for (int pp = 0; pp < kRNR - 1; ++pp) {
+    if (pp < n_rounds) load_round(r0 + pp, pp, 0);
+    else cp_async_commit();  // empty group: keeps the wait count uniform
+  }
+  pdl_wait();
+  pdl_trigger();
+  for (int pp = 0; pp < kRNR - 1 && pp < n_rounds; ++pp) load_round(r0 + pp, pp, 1);
 
   if (fuse_append && zr == 0 && kvc == 0) {
     for (int e = tid; e < 2 * Qtot * V8; e += kRThreads) {
@@ -607,41 +699,6 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   // smallest position): tiles below it need no causal mask
   const int warp_lim = pstart + q0 / G;
 
-  constexpr int LRS = kRThreads / V8;   // key rows per pass
-  const int lc = tid % V8, lr0 = tid / V8;
-  const __nv_bfloat16* qkv_k = qkv + (int64_t)(b * Qtot) * ldq + QD + h * D + lc * 8;
-  const __nv_bfloat16* qkv_v = qkv_k + KVD;
-  const int lpc = lc < V8 / 2 ? lc + V8 / 2 : lc - V8 / 2;
-  // round rd = keys 64rd .. 64rd+63: tile 2rd (key group 0), tile 2rd+1 (group 1)
-  auto load_round = [&](int rd, int rb) {
-    const int t0 = rd * 2 * kRKT;
-    for (int j = lr0; j < 2 * kRKT; j += LRS) {
-      const int t = t0 + j;
-      __nv_bfloat16* dk = sKV + ((rb * 2 + j / kRKT) * 2) * S::TILE + (j % kRKT) * LD + lc * 8;
-      __nv_bfloat16* dv = dk + S::TILE;
-      if (t < n_keys) {
-        // the call's own rows (t >= pstart) come straight from qkv (K rotated
-        // on the way when RoPE), older keys from the cache
-        const bool fresh = fuse_append && t >= pstart;
-        const int64_t qrow = (int64_t)(t - pstart) * ldq;
-        if (fresh && rope) {
-          float fv[8], pf[8];
-          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow), fv);
-          unpack8(*reinterpret_cast<const bf16x8*>(qkv_k + qrow + (lpc - lc) * 8), pf);
-          rope8(fv, pf, rope + (int64_t)t * (D / 2), lc * 8, D / 2);
-          *reinterpret_cast<bf16x8*>(dk) = pack8(fv);
-        } else {
-          cp_async16(dk, fresh ? qkv_k + qrow : kc + krow(t) + lc * 8);
-        }
-        cp_async16(dv, fresh ? qkv_v + qrow : vc + krow(t) + lc * 8);
-      } else {
-        *reinterpret_cast<uint4*>(dk) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(dv) = make_uint4(0, 0, 0, 0);
-      }
-    }
-    cp_async_commit();
-  };
-
   float m_r[2] = {-INFINITY, -INFINITY};
   float l_r[2] = {0.f, 0.f};
   float o[NT][4];
@@ -653,14 +710,9 @@ attention_rows_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qt
   const int lcol = (lane >> 4) * 8;
   const __nv_bfloat16* qw = sQ + (rw * 16 + lrow) * LD + lcol;  // this lane's ldmatrix row
 
-#pragma unroll
-  for (int pp = 0; pp < kRNR - 1; ++pp) {
-    if (pp < n_rounds) load_round(r0 + pp, pp);
-    else cp_async_commit();  // empty group: keeps the wait count uniform
-  }
   for (int rd = 0; rd < n_rounds; ++rd) {
     const int rb = rd % kRNR;
-    if (rd + kRNR - 1 < n_rounds) load_round(r0 + rd + kRNR - 1, (rd + kRNR - 1) % kRNR);
+    if (rd + kRNR - 1 < n_rounds) load_round(r0 + rd + kRNR - 1, (rd + kRNR - 1) % kRNR, 2);
     else cp_async_commit();
     cp_async_wait<kRNR - 1>();
     __syncthreads();  // (first round: also the query tile)

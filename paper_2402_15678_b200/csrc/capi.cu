@@ -7,13 +7,20 @@
 namespace ms {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static std::atomic<int> g_pdl{-1};  // -1: not yet read from MS_PDL
 bool pdl_enabled() {
-  static int v = -1;
+  int v = g_pdl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = getenv("MS_PDL");
     v = (e && e[0] == '0') ? 0 : 1;
+    g_pdl.store(v, std::memory_order_relaxed);
   }
   return v == 1;
+}
+int set_pdl(int on) {
+  const int old = pdl_enabled() ? 1 : 0;
+  g_pdl.store(on ? 1 : 0, std::memory_order_relaxed);
+  return old;
 }
 }  // namespace ms
 
@@ -51,6 +58,10 @@ extern "C" const char* ms_strerror(int status) {
     default: return "unknown status";
   }
 }
+
+// Programmatic dependent launch for the launches that follow (a captured CUDA
+// graph keeps the setting it was captured with); returns the previous value.
+extern "C" int ms_set_pdl(int on) { return ms::set_pdl(on); }
 
 extern "C" int64_t ms_launch_count(void) { return ms::g_launches.load(); }
 extern "C" void ms_reset_launch_count(void) { ms::g_launches.store(0); }

@@ -228,7 +228,7 @@ class SpecEngine:
                  record: bool = False, pipelined: bool = False, sync_time=None,
                  kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
                  selector_time: str = "verify", sim_cost=None, sampling: bool = False,
-                 draft_sms: int = 0):
+                 draft_sms: int = 0, draft_pdl: bool = True):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -259,7 +259,11 @@ class SpecEngine:
         draft_sms > 0 (pipelined): the draft and verify streams live on two
         green contexts splitting the GPU's SMs — draft_sms for the drafters,
         the rest for the verifier (ms_sm_partition): the drafters' small
-        kernels no longer wait for, or displace, the verify GEMMs' CTAs."""
+        kernels no longer wait for, or displace, the verify GEMMs' CTAs.
+        draft_pdl=False: the drafters' kernels launch without programmatic
+        dependent launch (a PDL-launched kernel's CTAs occupy SM slots while
+        they wait for their predecessor — slots the concurrent verify could
+        use)."""
         validate_config(cfg)
         if precision not in ("bf16", "fp32"):
             raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
@@ -341,6 +345,7 @@ class SpecEngine:
         # both streams' kernels wait for SM slots): equal by default;
         # MS_VERIFY_PRIORITY=1 / MS_DRAFT_PRIORITY=1 raise one (A/B)
         hi = lambda k: -1 if os.environ.get(k, "0") == "1" else 0  # noqa: E731
+        self.draft_pdl = bool(draft_pdl)
         self.draft_sms = self.verify_sms = 0
         if draft_sms > 0:
             if not pipelined:
@@ -583,7 +588,12 @@ class SpecEngine:
     def _launch_draft(self, g: _Group, s: int, qc: int) -> None:
         with torch.cuda.stream(self.draft_stream):
             g.ev_d0.record()
-            self._replay(("draft", g.gid, s, qc), lambda: self._device_draft(g, s, qc))
+            pdl = None if self.draft_pdl else _native.lib.ms_set_pdl(0)  # baked into the captured graph
+            try:
+                self._replay(("draft", g.gid, s, qc), lambda: self._device_draft(g, s, qc))
+            finally:
+                if pdl is not None:
+                    _native.lib.ms_set_pdl(pdl)
             g.ev_d1.record()
 
     def _launch_verify(self, g: _Group, s: int) -> None:

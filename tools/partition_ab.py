@@ -1,9 +1,11 @@
-"""A/B of the pipelined schedule with and without an SM partition between the
-drafters and the verifier (SpecEngine(draft_sms=N), csrc/partition.cu), in one
-process on the bench workload (cfg3: Llama-2-70B + 3 x Llama-160M, two groups
-of 16, fidelity injection), interleaved so clock drift hits every arm alike.
-usage: python tools/partition_ab.py [splits=0,16,24,32] [fixed_s=6] [reps=2] [new_tokens=128]
-prints one JSON line per (rep, split)."""
+"""A/B of pipelined-schedule placement options on the bench workload (cfg3:
+Llama-2-70B + 3 x Llama-160M, two groups of 16, fidelity injection), in one
+process, arms interleaved so clock drift hits every arm alike.  An arm is a
+comma list of SpecEngine options: draft_sms=N (SM partition, csrc/
+partition.cu), draft_pdl=0|1 (programmatic dependent launch of the drafter
+kernels).
+usage: python tools/partition_ab.py ["draft_sms=0;draft_sms=16;draft_pdl=0"] [fixed_s=6] [reps=2] [new_tokens=128]
+prints one JSON line per (rep, arm)."""
 import json
 import os
 import sys
@@ -16,7 +18,8 @@ from paper_2402_15678_b200.core import EngineConfig
 from paper_2402_15678_b200.engine import SpecEngine
 from paper_2402_15678_b200.models import config, make_model, random_weights
 
-splits = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,16,24,32").split(",")]
+arms = [dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in a.split(",") if kv)
+        for a in (sys.argv[1] if len(sys.argv) > 1 else "draft_sms=0;draft_sms=16;draft_pdl=0").split(";")]
 fixed_s = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 new_tokens = int(sys.argv[4]) if len(sys.argv) > 4 else 128
@@ -31,9 +34,10 @@ drafters = [random_weights(scfg, k + 1) for k in range(3)]
 reqs = bench.make_requests(32, 128, new_tokens, tcfg.vocab)
 teacher = None
 for rep in range(reps):
-    for n in splits:
+    for arm in arms:
+        kw = {"draft_sms": arm.get("draft_sms", 0), "draft_pdl": bool(arm.get("draft_pdl", 1))}
         eng = SpecEngine(target, drafters, cfg, slots=32, max_len=max_len, fidelity=fid, pipelined=True,
-                         adaptive=not fixed_s, draft_sms=n)
+                         adaptive=not fixed_s, **kw)
         eng.capture_graphs()
         if teacher is None:
             teacher = eng.greedy_teacher(bench.fresh(reqs), new_tokens)
@@ -53,7 +57,7 @@ for rep in range(reps):
             out.append((res.tokens / (e0.elapsed_time(e1) * 1e-3), res))
         tps = sum(o[0] for o in out) / len(out)
         rounds = [rd for _, r in out for rd in r.rounds]
-        print(json.dumps({"rep": rep, "draft_sms": n, "got": [eng.draft_sms, eng.verify_sms],
+        print(json.dumps({"rep": rep, "arm": arm, "got_sms": [eng.draft_sms, eng.verify_sms],
                           "fixed_s": fixed_s, "tokens_per_s": round(tps, 1),
                           "lossless": all(r.outputs == teacher for _, r in out),
                           "verify_ms": round(sum(r.t_verify_ms for r in rounds) / len(rounds), 3),
