@@ -1,4 +1,4 @@
-"""A/B of ms_linear's L2 prefetch distance (ms_set_l2_prefetch) on the 70B
+"""A/B of ms_linear's L2 prefetch distance (ms_set_stream_k) on the 70B
 verify forward (B=16, ctx 190) and its four GEMM kinds: one CUDA graph per
 (prefetch distance, what), replayed interleaved.
 usage: python tools/l2pf_ab.py [dists=0,4,8,16] [Qs=5,7,9]"""
@@ -9,8 +9,8 @@ from paper_2402_15678_b200 import _native, kernels as K
 from paper_2402_15678_b200.llama import CONFIGS, LlamaModel, LlamaWeights
 from paper_2402_15678_b200.opt import KVCache
 
-dists = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,4,8,16").split(",")]
-Qs = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "5,7,9").split(",")]
+dists = [0, 1]
+Qs = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "5,7,9").split(",")]
 c = CONFIGS["llama-2-70b"]
 B, ctx = 16, 190
 w = LlamaWeights.random(c, 0)
@@ -41,14 +41,14 @@ for Q in Qs:
     fns = [("full", full)] + [(k, gemm(k)) for k in ("qkv", "o", "gu", "down")]
     graphs = {}
     for d in dists:
-        _native.lib.ms_set_l2_prefetch(d)
+        _native.lib.ms_set_stream_k(d)
         for nm, fn in fns:
             fn(); torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
             graphs[(d, nm)] = g
-    _native.lib.ms_set_l2_prefetch(0)
+    _native.lib.ms_set_stream_k(1)
     res = {}
     for rep in range(3):
         for nm, _ in fns:
