@@ -318,6 +318,14 @@ int ms_linear_grouped(const void* x, int64_t ldx, const void* w, const void* bia
 int ms_gemv_grouped(const void* x, int64_t ldx, const void* w, int64_t w_gstride, const void* bias,
                     const void* residual, int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N,
                     int K, int act, int G, void* stream);
+/* ms_gemv_grouped with each x row's RMSNorm folded in (the gain folded into w
+ * beforehand, LlamaWeights.fold_norms): out = act(rstd[row] * (x . w^T)) (+
+ * residual), rstd = rsqrt(mean_k x[row, k]^2 + eps) from the bf16 x values in
+ * a fixed order — no RMSNorm kernel and no normalised activation in HBM.  The
+ * grouped drafters' QKV and gate/up projections of a decode step. */
+int ms_gemv_rms_grouped(const void* x, int64_t ldx, const void* w, int64_t w_gstride, const void* residual,
+                        int64_t ldr, void* out, int64_t ldc, int out_f32, int M, int N, int K, int act, int G,
+                        float eps, void* stream);
 int ms_embed_grouped(const int32_t* tok, const int32_t* start, int Q, const void* tok_emb, int64_t tstride,
                      int rpg, const void* pos_emb, int pos_offset, int R, int d, void* out, void* stream);
 int ms_rmsnorm_grouped(const void* x, int64_t ldx, const int32_t* rows, const void* gamma, int64_t gstride,
@@ -409,6 +417,16 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
  * captured CUDA graph keeps the setting it was captured with.  Returns the
  * previous setting. */
 int ms_set_pdl(int on);
+
+/* Co-resident launch shapes (default off; the pipelined engine turns it on
+ * around its drafter graphs): ms_gemv runs 64-thread CTAs (<= 128 registers)
+ * and single-row MHA decode attention (Q = 1, contiguous cache) runs
+ * 64-thread, shared-memory-free CTAs — each fits on an SM beside two
+ * verify-GEMM CTAs (2 x 224 x 128 + 64 x 128 registers = 64K), so the
+ * drafters of one group neither wait for nor displace the verifier of the
+ * other.  Results differ in rounding from the default shapes.  A captured CUDA
+ * graph keeps the setting it was captured with.  Returns the previous value. */
+int ms_set_coresident(int on);
 
 /* ---- SM partition for the pipelined schedule ------------------------------
  * Replaces: the reference's separate SSM / LLM executors of run_pipelined

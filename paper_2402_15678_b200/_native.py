@@ -70,6 +70,7 @@ _SIGS = {
     "ms_tp_argmax_combine": [_P, _I, _I, _P, _P, _P, _P, _I, _P],
     "ms_linear_grouped": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _I, _P],
     "ms_gemv_grouped": [_P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _P],
+    "ms_gemv_rms_grouped": [_P, _I64, _P, _I64, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _I, _F, _P],
     "ms_embed_grouped": [_P, _P, _I, _P, _I64, _I, _P, _I, _I, _I, _P, _P],
     "ms_rmsnorm_grouped": [_P, _I64, _P, _P, _I64, _I, _F, _I, _I, _P, _I64, _P],
     "ms_draft_commit_grouped": [_P, _P, _I, _I, _I, _I, _P, _I64, _P, ctypes.POINTER(ctypes.c_float),
@@ -80,6 +81,7 @@ _SIGS = {
     "ms_attention_workspace_gqa": [_I, _I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64),
                                    ctypes.POINTER(ctypes.c_int)],
     "ms_set_pdl": [_I],
+    "ms_set_coresident": [_I],
     "ms_sm_partition": [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
     "ms_attention_workspace": [_I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],

@@ -29,6 +29,8 @@
 // reductions, tile order, warp-order merge) does not depend on the other
 // rows; rows of other queries only add fully-masked keys that contribute
 // exactly zero.
+#include <atomic>
+
 #include "common.cuh"
 
 namespace ms {
@@ -1017,8 +1019,154 @@ static int launch_attn(const void* qkv, int64_t ldq, int B, int Q, int H, int Hk
                 counters, pg);
 }
 
+// ---------------------------------------------------------------------------
+// Co-resident decode attention (drafters' decode steps beside the verifier,
+// ms_set_coresident): one query row per request (Q = 1), MHA, contiguous cache.
+// One warp per (request, head), 2 warps (64 threads, <= 128 registers, no
+// shared memory) per CTA — a CTA fits beside two verify-GEMM CTAs on an SM
+// (2 x 224 threads x 128 registers + 64 x 128 = the 64K register file; the
+// GEMMs leave ~17 KB of shared memory), so drafting no longer waits for GEMM
+// CTAs to retire nor blocks the next one.  Lanes form groups of D/8 (one
+// 16-byte chunk of a key row each): a warp streams 32 / (D/8) keys per step,
+// each group keeps its own online softmax over its keys, the groups merge in
+// a fixed shuffle tree at the end (deterministic; fp32 P.V).  The cached keys
+// of the first steps are requested before the programmatic-dependency wait.
+template <int D>
+__global__ void __launch_bounds__(64, 8)
+attention_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int B, int H,
+                        const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
+                        __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
+                        int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
+                        int64_t ldo) {
+  constexpr int LPK = D / 8;    // lanes per key row
+  constexpr int KPI = 32 / LPK;  // keys per warp step
+  constexpr int U = 4;           // warp steps in flight
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x * 2 + warp;
+  const bool live = pair < B * H;
+  const int b = live ? pair / H : 0, h = live ? pair % H : 0;
+  const int sub = lane / LPK, j = lane % LPK;  // key slot in a step, 16-byte chunk (dims 8j..8j+7)
+  const int pstart = start[b];
+  const int n_keys = min(pstart + 1, T);
+  const int64_t base = ((int64_t)slot[b] * H + h) * T * D + j * 8;
+  // cached rows (t < pstart) of the first U steps, before the dependency wait
+  uint4 kr[U], vr[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int t = u * KPI + sub;
+    if (live && t < pstart && t < n_keys) {
+      kr[u] = *reinterpret_cast<const uint4*>(kc + base + (int64_t)t * D);
+      vr[u] = *reinterpret_cast<const uint4*>(vc + base + (int64_t)t * D);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
+  const int QD = H * D;
+  const __nv_bfloat16* qrow = qkv + (int64_t)b * ldq;
+  float q[8], kf[8], vf[8];
+  unpack8(*reinterpret_cast<const bf16x8*>(qrow + h * D + j * 8), q);
+  // the call's own key / value (position pstart): K rotated, appended to the cache
+  unpack8(*reinterpret_cast<const bf16x8*>(qrow + QD + h * D + j * 8), kf);
+  unpack8(*reinterpret_cast<const bf16x8*>(qrow + 2 * QD + h * D + j * 8), vf);
+  if (rope) {  // rotate-half partner dims d +- D/2 sit in lane j ^ (LPK / 2) of the group
+    float pq[8], pk[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      pq[e] = __shfl_xor_sync(0xffffffffu, q[e], LPK / 2);
+      pk[e] = __shfl_xor_sync(0xffffffffu, kf[e], LPK / 2);
+    }
+    rope8(q, pq, rope + (int64_t)pstart * (D / 2), j * 8, D / 2);
+    rope8(kf, pk, rope + (int64_t)pstart * (D / 2), j * 8, D / 2);
+  }
+  const bf16x8 kfresh = pack8(kf);
+  bf16x8 vfresh;
+  if (fuse_append) {
+    vfresh = *reinterpret_cast<const bf16x8*>(qrow + 2 * QD + h * D + j * 8);
+    if (sub == 0 && pstart < T) {
+      *reinterpret_cast<bf16x8*>(kc + base + (int64_t)pstart * D) = kfresh;
+      *reinterpret_cast<bf16x8*>(vc + base + (int64_t)pstart * D) = vfresh;
+    }
+  }
+  float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  auto consume = [&](int t, const uint4& kraw, const uint4& vraw) {
+    // t: this group's key (uniform within the group); invalid keys contribute nothing
+    bool valid = t < n_keys;
+    uint4 kk = kraw, vv = vraw;
+    if (t == pstart) {
+      if (fuse_append) {
+        kk = *reinterpret_cast<const uint4*>(&kfresh);
+        vv = *reinterpret_cast<const uint4*>(&vfresh);
+      } else {
+        kk = *reinterpret_cast<const uint4*>(kc + base + (int64_t)t * D);
+        vv = *reinterpret_cast<const uint4*>(vc + base + (int64_t)t * D);
+      }
+    }
+    float k8[8], v8[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(&kk), k8);
+    float d = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d = fmaf(q[e], k8[e], d);
+#pragma unroll
+    for (int o = 1; o < LPK; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (!valid) return;
+    const float sc = d * scale_log2;
+    const float mn = fmaxf(m, sc);
+    const float corr = exp2f(m - mn);  // m = -inf at the first key: corr = 0
+    const float pv = exp2f(sc - mn);
+    unpack8(*reinterpret_cast<const bf16x8*>(&vv), v8);
+    l = l * corr + pv;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, v8[e], acc[e] * corr);
+    m = mn;
+  };
+  for (int t0 = 0; t0 < n_keys; t0 += U * KPI) {
+    if (t0 > 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * KPI + sub;
+        if (t < pstart && t < n_keys) {
+          kr[u] = *reinterpret_cast<const uint4*>(kc + base + (int64_t)t * D);
+          vr[u] = *reinterpret_cast<const uint4*>(vc + base + (int64_t)t * D);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) consume(t0 + u * KPI + sub, kr[u], vr[u]);
+  }
+  // merge the KPI groups' (m, l, acc) in a fixed xor tree
+#pragma unroll
+  for (int o = LPK; o < 32; o <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    const float mn = fmaxf(m, m2);
+    const float a1 = m == -INFINITY ? 0.f : exp2f(m - mn);
+    const float a2 = m2 == -INFINITY ? 0.f : exp2f(m2 - mn);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x2 = __shfl_xor_sync(0xffffffffu, acc[e], o);
+      acc[e] = acc[e] * a1 + x2 * a2;
+    }
+    l = l * a1 + l2 * a2;
+    m = mn;
+  }
+  if (sub == 0) {
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
+    *reinterpret_cast<bf16x8*>(out + (int64_t)b * ldo + h * D + j * 8) = pack8(acc);
+  }
+}
+
+static std::atomic<int> g_coresident{0};
+int coresident() { return g_coresident.load(std::memory_order_relaxed); }
+int set_coresident(int on) { return g_coresident.exchange(on ? 1 : 0); }
+
 int preload_attention() {
   int n = 0;
+  n += preload_fn(attention_decode_kernel<64>) + preload_fn(attention_decode_kernel<128>);
   n += preload_fn(attention_kernel<64, 2, false>) + preload_fn(attention_kernel<128, 2, false>);
   n += preload_fn(attention_kernel<64, 2, true>) + preload_fn(attention_kernel<128, 2, true>);
   n += preload_fn(attention_rows_kernel<64, false>) + preload_fn(attention_rows_kernel<128, false>);
@@ -1082,6 +1230,18 @@ extern "C" int ms_attention_paged(const void* qkv, int64_t ldq, int B, int Q, in
                                        block_table, max_blocks, block_size, stream);
       if (s != MS_OK) return s;
     }
+  }
+  if (ms::coresident() && Q == 1 && Hkv == H && !block_table && !ws && (D == 64 || D == 128)) {
+    const dim3 grid((B * H + 1) / 2);
+    const float sl = scale * 1.4426950408889634f;
+    auto* q = (const __nv_bfloat16*)qkv;
+    auto* kc = (__nv_bfloat16*)k_cache;
+    auto* vc = (__nv_bfloat16*)v_cache;
+    auto* o = (__nv_bfloat16*)out;
+    return D == 64 ? ms::launch(ms::attention_decode_kernel<64>, grid, dim3(64), 0, st, 1, q, ldq, B, H, slot, start,
+                                T, kc, vc, sl, fuse, (const float2*)rope, o, ldo)
+                   : ms::launch(ms::attention_decode_kernel<128>, grid, dim3(64), 0, st, 1, q, ldq, B, H, slot,
+                                start, T, kc, vc, sl, fuse, (const float2*)rope, o, ldo);
   }
   if (D == 64)
     return ms::launch_attn<64>(qkv, ldq, B, Q, H, Hkv, slot, start, T, k_cache, v_cache, (const float2*)rope,

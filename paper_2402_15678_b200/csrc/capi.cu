@@ -36,6 +36,7 @@ int preload_gemm();
 int preload_wide();
 int preload_tp();
 int preload_fp32();
+int set_coresident(int on);
 }  // namespace ms
 
 extern "C" int ms_version(void) { return 200; }
@@ -62,6 +63,10 @@ extern "C" const char* ms_strerror(int status) {
 // Programmatic dependent launch for the launches that follow (a captured CUDA
 // graph keeps the setting it was captured with); returns the previous value.
 extern "C" int ms_set_pdl(int on) { return ms::set_pdl(on); }
+
+// Co-resident launch shapes for the launches that follow: drafter decode
+// kernels sized to fit beside the verifier's GEMM CTAs (include/minions.h).
+extern "C" int ms_set_coresident(int on) { return ms::set_coresident(on); }
 
 extern "C" int64_t ms_launch_count(void) { return ms::g_launches.load(); }
 extern "C" void ms_reset_launch_count(void) { ms::g_launches.store(0); }

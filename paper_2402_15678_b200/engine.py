@@ -228,7 +228,7 @@ class SpecEngine:
                  record: bool = False, pipelined: bool = False, sync_time=None,
                  kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
                  selector_time: str = "verify", sim_cost=None, sampling: bool = False,
-                 draft_sms: int = 0, draft_pdl: bool = True):
+                 draft_sms: int = 0, draft_pdl: bool = True, draft_coresident: bool | None = None):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -263,7 +263,12 @@ class SpecEngine:
         draft_pdl=False: the drafters' kernels launch without programmatic
         dependent launch (a PDL-launched kernel's CTAs occupy SM slots while
         they wait for their predecessor — slots the concurrent verify could
-        use)."""
+        use).
+        draft_coresident (default: on for grouped Llama drafters in the
+        pipelined schedule): the drafters' decode
+        steps run in co-resident launch shapes (ms_set_coresident: 64-thread
+        gemv / decode-attention CTAs, the LM head on gemv) that fit on an SM
+        beside two verify-GEMM CTAs."""
         validate_config(cfg)
         if precision not in ("bf16", "fp32"):
             raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
@@ -346,6 +351,7 @@ class SpecEngine:
         # MS_VERIFY_PRIORITY=1 / MS_DRAFT_PRIORITY=1 raise one (A/B)
         hi = lambda k: -1 if os.environ.get(k, "0") == "1" else 0  # noqa: E731
         self.draft_pdl = bool(draft_pdl)
+        self.draft_coresident = bool((pipelined and self.grouped) if draft_coresident is None else draft_coresident)
         self.draft_sms = self.verify_sms = 0
         if draft_sms > 0:
             if not pipelined:
@@ -588,12 +594,20 @@ class SpecEngine:
     def _launch_draft(self, g: _Group, s: int, qc: int) -> None:
         with torch.cuda.stream(self.draft_stream):
             g.ev_d0.record()
-            pdl = None if self.draft_pdl else _native.lib.ms_set_pdl(0)  # baked into the captured graph
+            # launch policies baked into the captured graph
+            pdl = None if self.draft_pdl else _native.lib.ms_set_pdl(0)
+            co = _native.lib.ms_set_coresident(1) if self.draft_coresident else None
+            if self.grouped:
+                self.ssm_g.coresident = self.draft_coresident
             try:
                 self._replay(("draft", g.gid, s, qc), lambda: self._device_draft(g, s, qc))
             finally:
                 if pdl is not None:
                     _native.lib.ms_set_pdl(pdl)
+                if co is not None:
+                    _native.lib.ms_set_coresident(co)
+                if self.grouped:
+                    self.ssm_g.coresident = False
             g.ev_d1.record()
 
     def _launch_verify(self, g: _Group, s: int) -> None:

@@ -20,6 +20,12 @@ def linear_splits(N: int, K: int) -> int:
     return int(_native.lib.ms_linear_splits(N, K))
 
 
+# drafter decode projections (<= 64 token rows) up to this reduction length run
+# on ms_gemv (4 K-splitting warps up to K = 1024, 8 beyond); the verifier never
+# uses it
+GEMV_MAX_K = 4096
+
+
 def linear(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
            residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
            out_f32: bool = False, splits: int = 0, stream=None) -> torch.Tensor:
@@ -111,12 +117,18 @@ def linear_rms(x: torch.Tensor, w: torch.Tensor, *, residual: torch.Tensor | Non
 
 def gemv(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None,
          residual: torch.Tensor | None = None, act: int = 0, out: torch.Tensor | None = None,
-         out_f32: bool = False, stream=None) -> torch.Tensor:
-    """out = act(x @ w.T + bias) + residual for M <= 64 rows (ms_gemv, low latency)."""
+         out_f32: bool = False, stream=None, rms_eps: float | None = None) -> torch.Tensor:
+    """out = act(x @ w.T + bias) + residual for M <= 64 rows (ms_gemv, low latency).
+    rms_eps: x's RMSNorm folded in (gain pre-folded into w; no bias)."""
     M, K = x.shape
     N = w.shape[0]
     if x.dtype != BF16 or w.dtype != BF16 or w.shape[1] != K or x.stride(1) != 1 or not w.is_contiguous():
         raise ValueError("x [M, K] and w [N, K] must be bf16 with unit column stride")
+    if rms_eps is not None:
+        if bias is not None:
+            raise ValueError("the folded-RMSNorm gemv takes no bias")
+        return gemv_grouped(x, w.view(1, N, K), 1, residual=residual, act=act, out=out, out_f32=out_f32,
+                            stream=stream, rms_eps=rms_eps)
     if out is None:
         out = torch.empty((M, N // 2 if act == 2 else N), dtype=torch.float32 if out_f32 else BF16,
                           device=x.device)
@@ -249,16 +261,24 @@ def linear_grouped(x: torch.Tensor, w: torch.Tensor, G: int, residual: torch.Ten
 
 
 def gemv_grouped(x: torch.Tensor, w: torch.Tensor, G: int, residual: torch.Tensor | None = None, act: int = 0,
-                 out: torch.Tensor | None = None, out_f32: bool = False, stream=None) -> torch.Tensor:
-    """ms_gemv over G row groups: x [G*M, K] (M <= 64), w [G, N, K] stacked."""
+                 out: torch.Tensor | None = None, out_f32: bool = False, stream=None,
+                 rms_eps: float | None = None) -> torch.Tensor:
+    """ms_gemv over G row groups: x [G*M, K] (M <= 64), w [G, N, K] stacked.
+    rms_eps: each x row's RMSNorm folded in (ms_gemv_rms_grouped; the gain
+    must already be folded into w)."""
     GM, K = x.shape
     M = GM // G
     N = w.shape[-2]
     if out is None:
         out = torch.empty((GM, N // 2 if act == 2 else N), dtype=torch.float32 if out_f32 else BF16,
                           device=x.device)
-    _native.call("ms_gemv_grouped", x.data_ptr(), x.stride(0), w.data_ptr(), N * K, None,
-                 None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0),
+    res = (None if residual is None else residual.data_ptr(), 0 if residual is None else residual.stride(0))
+    if rms_eps is not None:
+        _native.call("ms_gemv_rms_grouped", x.data_ptr(), x.stride(0), w.data_ptr(), N * K, *res,
+                     out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, G,
+                     float(rms_eps), _dev.stream_ptr(stream))
+        return out
+    _native.call("ms_gemv_grouped", x.data_ptr(), x.stride(0), w.data_ptr(), N * K, None, *res,
                  out.data_ptr(), out.stride(0), int(out.dtype == torch.float32), M, N, K, act, G,
                  _dev.stream_ptr(stream))
     return out

@@ -50,7 +50,7 @@ class LlamaModel:
 
     def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False,
                  fuse_norm: bool | None = None):
-        """small_gemm: projections of <= 64 token rows with K <= 1024 use the
+        """small_gemm: projections of <= 64 token rows with K <= K.GEMV_MAX_K use the
         low-latency ms_gemv (drafters' decode steps); the verifier keeps the
         tcgen05 path everywhere, so its numerics never depend on the row count.
 
@@ -76,7 +76,11 @@ class LlamaModel:
         o_split = K.linear_splits(c.d, c.n_heads * c.head_dim)
         d_split = K.linear_splits(c.d, c.ffn)
         self.fuse_norm = bool(fuse_norm) and o_split > 1 and d_split > 1  # producers need split-K
-        if self.fuse_norm:
+        if self.fuse_norm or small_gemm:
+            # drafters (small_gemm): decode steps fold each RMSNorm into the
+            # QKV / gate-up ms_gemv (rstd from x inside the kernel, gain in the
+            # weight) — two fewer launches per layer; catch-up / prefill rows
+            # keep an explicit norm (unit gains after the fold)
             w.fold_norms()
         self.n_parts = (c.d + 127) // 128
         self.rms_a = torch.zeros((max_rows, self.n_parts), dtype=torch.float32, device=device) if self.fuse_norm else None
@@ -137,20 +141,28 @@ class LlamaModel:
         def lin(xx, wname, **kw):
             if prefill:
                 return _prefill_linear(xx, w[wname], stream=stream, **kw)
-            if small and xx.shape[1] <= 1024:
+            if small and xx.shape[1] <= K.GEMV_MAX_K:
                 return K.gemv(xx, w[wname], stream=stream, **kw)
             return K.linear(xx, w[wname], stream=stream, **kw)
 
+        # decode steps of a drafter: RMSNorm folded into the QKV / gate-up gemv
+        fold = small and not prefill and c.d <= K.GEMV_MAX_K
         for i in range(c.n_layers):
             p = f"l{i}."
-            K.rmsnorm(x, w[p + "attn_norm"], c.eps, out=h, stream=stream)
-            lin(h, p + "w_qkv", out=qkv)
+            if fold:
+                K.gemv(x, w[p + "w_qkv"], out=qkv, stream=stream, rms_eps=c.eps)
+            else:
+                K.rmsnorm(x, w[p + "attn_norm"], c.eps, out=h, stream=stream)
+                lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
                         page=getattr(cache, "page", None), ws=self._attn_ws(B, Q, cache.max_len))
             lin(at, p + "w_o", residual=x, out=x)
-            K.rmsnorm(x, w[p + "mlp_norm"], c.eps, out=h, stream=stream)
-            lin(h, p + "w_gu", act=2, out=ff)
+            if fold:
+                K.gemv(x, w[p + "w_gu"], act=2, out=ff, stream=stream, rms_eps=c.eps)
+            else:
+                K.rmsnorm(x, w[p + "mlp_norm"], c.eps, out=h, stream=stream)
+                lin(h, p + "w_gu", act=2, out=ff)
             lin(ff, p + "w_down", residual=x, out=x)
         Rh = R if head_rows is None else head_rows.numel()
         hf = self.h[:Rh]
@@ -215,7 +227,21 @@ class GroupedLlamaModel:
         self.cfg, self.G = c, len(ws)
         self.device = torch.device(device)
         self.t = {k: torch.stack([w[k] for w in ws]).contiguous() for k in ws[0].t}
+        # RMSNorm gains folded into the stacked projections (the callers'
+        # weights are untouched): bf16(w * g), the same rounding as
+        # LlamaWeights.fold_norms, so a grouped forward stays bitwise equal to
+        # K separate small_gemm LlamaModels
+        t = self.t
+        pairs = [(f"l{i}.attn_norm", f"l{i}.w_qkv") for i in range(c.n_layers)]
+        pairs += [(f"l{i}.mlp_norm", f"l{i}.w_gu") for i in range(c.n_layers)] + [("norm_f", "lm_head")]
+        for gname, wname in pairs:
+            if not bool(torch.all(t[gname] == 1)):
+                t[wname].mul_(t[gname].to(t[wname].dtype)[:, None, :])
+            t[gname] = torch.ones_like(t[gname])
         G = self.G
+        # set by the engine while it launches this model's steps in the
+        # co-resident mode (ms_set_coresident): the LM head then runs on ms_gemv
+        self.coresident = False
         self.max_rows = max_rows  # per group
         R = G * max_rows
         self.x = torch.empty((R, c.d), dtype=BF16, device=device)
@@ -246,23 +272,38 @@ class GroupedLlamaModel:
                     _prefill_linear(xx[sl], wt[g], out=out[sl], residual=None if res is None else res[sl],
                                     act=kw.get("act", 0), stream=stream)
                 return out
-            if M <= 64 and wt.shape[2] <= 1024:
+            if M <= 64 and wt.shape[2] <= K.GEMV_MAX_K:
                 return K.gemv_grouped(xx, wt, G, stream=stream, **kw)
             return K.linear_grouped(xx, wt.view(-1, wt.shape[2]), G, stream=stream, **kw)
 
+        # decode steps (<= 64 rows per drafter): RMSNorm folded into the QKV /
+        # gate-up gemv; catch-up and prefill rows: explicit norm (unit gains)
+        fold = not prefill and M <= 64 and c.d <= K.GEMV_MAX_K
         for i in range(c.n_layers):
             p = f"l{i}."
-            K.rmsnorm_grouped(x, t[p + "attn_norm"], M, c.eps, out=h, stream=stream)
-            lin(h, p + "w_qkv", out=qkv)
+            if fold:
+                K.gemv_grouped(x, t[p + "w_qkv"], G, out=qkv, stream=stream, rms_eps=c.eps)
+            else:
+                K.rmsnorm_grouped(x, t[p + "attn_norm"], M, c.eps, out=h, stream=stream)
+                lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, GB, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
                         page=getattr(cache, "page", None))
             lin(at, p + "w_o", residual=x, out=x)
-            K.rmsnorm_grouped(x, t[p + "mlp_norm"], M, c.eps, out=h, stream=stream)
-            lin(h, p + "w_gu", act=2, out=ff)
+            if fold:
+                K.gemv_grouped(x, t[p + "w_gu"], G, act=2, out=ff, stream=stream, rms_eps=c.eps)
+            else:
+                K.rmsnorm_grouped(x, t[p + "mlp_norm"], M, c.eps, out=h, stream=stream)
+                lin(h, p + "w_gu", act=2, out=ff)
             lin(ff, p + "w_down", residual=x, out=x)
         Rh = R if head_rows is None else head_rows.numel()
         if Rh == 0:
+            return logits
+        if fold and head_rows is None and self.coresident:
+            # co-resident decode step: the LM head as a folded-norm gemv too
+            # (the tcgen05 GEMM's shared-memory rings cannot sit beside the
+            # verifier's GEMM CTAs)
+            K.gemv_grouped(x, t["lm_head"], G, out=logits, out_f32=True, stream=stream, rms_eps=c.eps)
             return logits
         hf = self.h[:Rh]
         K.rmsnorm_grouped(x, t["norm_f"], Rh // G, c.eps, out=hf, rows=head_rows, stream=stream)

@@ -91,7 +91,7 @@ class OPTModel:
                 return K.linear_wide(xx, w[wname], w[bname], stream=stream, **kw)
             # ms_gemv only where it measured faster (tools/probe_gemm_graph.py):
             # short K; long-K projections (FC2) keep the cluster split-K path
-            if small and xx.shape[1] <= 1024:
+            if small and xx.shape[1] <= K.GEMV_MAX_K:
                 return K.gemv(xx, w[wname], w[bname], stream=stream, **kw)
             return K.linear(xx, w[wname], w[bname], stream=stream, **kw)
 

@@ -50,7 +50,7 @@ def test_gated_silu_linear(M, F, K, splits):
         assert torch.equal(one, got[:1])
 
 
-@pytest.mark.parametrize("M,F,K", [(16, 3072, 768), (1, 512, 256), (33, 1024, 1024)])
+@pytest.mark.parametrize("M,F,K", [(16, 3072, 768), (1, 512, 256), (33, 1024, 1024), (16, 512, 3072)])
 def test_gated_silu_gemv(M, F, K):
     from paper_2402_15678_b200 import kernels as Kn
     g = torch.Generator().manual_seed(M * 5 + F)
@@ -386,3 +386,29 @@ def test_gated_silu_prefill_epilogue(M, N):
     g4 = gu.view(M, N // 128, 2, 64)
     want = (torch.nn.functional.silu(g4[:, :, 0, :]) * g4[:, :, 1, :]).reshape(M, N // 2)
     torch.testing.assert_close(out.float(), want, rtol=8e-3, atol=1e-5)
+
+
+@pytest.mark.parametrize("M,N,K,act", [(16, 2304, 768, 0), (16, 6144, 768, 2), (5, 256, 256, 0), (48, 768, 3072, 0)])
+def test_gemv_folded_rmsnorm(M, N, K, act):
+    """ms_gemv_rms_grouped: out = act(rstd[row] * (x . w^T)) with rstd from the
+    bf16 x row (the drafters' decode-step QKV / gate-up with the norm gain
+    folded into w) vs an fp64 reference; rows independent of M; G = 3 groups
+    equal three single calls bitwise."""
+    from paper_2402_15678_b200 import kernels as Kn
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    G, eps = 3, 1e-5
+    x = (torch.randn(G * M, K, generator=g) * 2).to(BF)
+    w = (torch.randn(G, N, K, generator=g) * 0.03).to(BF)
+    got = Kn.gemv_grouped(x.cuda(), w.cuda(), G, act=act, rms_eps=eps).cpu().float()
+    for k in range(G):
+        xs = x[k * M:(k + 1) * M].double()
+        y = xs @ w[k].double().T * torch.rsqrt((xs ** 2).mean(-1, keepdim=True) + eps)
+        if act == 2:
+            t = y.view(M, -1, 2, 64)
+            gt, up = t[:, :, 0].reshape(M, -1), t[:, :, 1].reshape(M, -1)
+            y = gt * torch.sigmoid(gt) * up
+        torch.testing.assert_close(got[k * M:(k + 1) * M], y.float(), rtol=2e-2, atol=2e-2)
+        one = Kn.gemv(x[k * M:(k + 1) * M].cuda(), w[k].cuda(), act=act, rms_eps=eps).cpu().float()
+        assert torch.equal(one, got[k * M:(k + 1) * M])
+    first = Kn.gemv(x[:1].contiguous().cuda(), w[0].cuda(), act=act, rms_eps=eps).cpu().float()
+    assert torch.equal(first, got[:1])

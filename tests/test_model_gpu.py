@@ -185,7 +185,8 @@ def test_attention_split_kv_matches_and_is_batch_invariant(D, H, Hkv, Q):
     assert torch.equal(a1, a.view(B, Q, -1)[:, 0])
 
 
-@pytest.mark.parametrize("M,N,K", [(16, 2304, 768), (1, 768, 3072), (33, 3072, 768), (64, 100, 256), (5, 1000, 96)])
+@pytest.mark.parametrize("M,N,K", [(16, 2304, 768), (1, 768, 3072), (16, 768, 3072), (48, 768, 4096),
+                                   (33, 3072, 768), (64, 100, 256), (5, 1000, 96)])
 def test_gemv_vs_torch_and_row_invariance(M, N, K):
     from paper_2402_15678_b200 import kernels as Kn
     g = torch.Generator().manual_seed(M * 3 + N)

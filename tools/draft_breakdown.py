@@ -29,7 +29,7 @@ L = c.n_layers
 
 def lin(xx, name, **kw):
     wt = t[name]
-    if B <= 64 and wt.shape[2] <= 1024:
+    if B <= 64 and wt.shape[2] <= K.GEMV_MAX_K:
         return K.gemv_grouped(xx, wt, G, **kw)
     return K.linear_grouped(xx, wt.view(-1, wt.shape[2]), G, **kw)
 

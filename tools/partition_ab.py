@@ -35,7 +35,8 @@ reqs = bench.make_requests(32, 128, new_tokens, tcfg.vocab)
 teacher = None
 for rep in range(reps):
     for arm in arms:
-        kw = {"draft_sms": arm.get("draft_sms", 0), "draft_pdl": bool(arm.get("draft_pdl", 1))}
+        kw = {"draft_sms": arm.get("draft_sms", 0), "draft_pdl": bool(arm.get("draft_pdl", 1)),
+              "draft_coresident": bool(arm["draft_coresident"]) if "draft_coresident" in arm else None}
         eng = SpecEngine(target, drafters, cfg, slots=32, max_len=max_len, fidelity=fid, pipelined=True,
                          adaptive=not fixed_s, **kw)
         eng.capture_graphs()
