@@ -1,7 +1,10 @@
-"""A/B of ms_linear's L2 prefetch distance (ms_set_stream_k) on the 70B
-verify forward (B=16, ctx 190) and its four GEMM kinds: one CUDA graph per
-(prefetch distance, what), replayed interleaved.
-usage: python tools/l2pf_ab.py [dists=0,4,8,16] [Qs=5,7,9]"""
+"""A/B of the gate/up GEMM schedule (ms_set_tail_split: 0 = one launch of
+448 one-split tiles = 1.51 waves, 1 = a full wave + a 2-way-split tail launch
+without the dependency wait) on the 70B verify forward (B=16, ctx 190) and its
+four GEMM kinds: one CUDA graph per (schedule, what), replayed interleaved.
+(The same harness ran round 2's L2-prefetch and stream-K A/Bs,
+profiles/r2_l2pf_ab.jsonl / r2_stream_k_ab.jsonl, whose knobs were removed.)
+usage: python tools/sk_ab.py [Qs=5,7,9]"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -41,14 +44,14 @@ for Q in Qs:
     fns = [("full", full)] + [(k, gemm(k)) for k in ("qkv", "o", "gu", "down")]
     graphs = {}
     for d in dists:
-        _native.lib.ms_set_stream_k(d)
+        _native.lib.ms_set_tail_split(d)
         for nm, fn in fns:
             fn(); torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
             graphs[(d, nm)] = g
-    _native.lib.ms_set_stream_k(1)
+    _native.lib.ms_set_tail_split(1)
     res = {}
     for rep in range(3):
         for nm, _ in fns:
