@@ -48,7 +48,6 @@ import torch
 from . import _dev
 from . import _native
 from .core import AggSpecError, EngineConfig, Request, RequestState, seeded_rng, validate_config
-import os
 
 from .llama import GroupedLlamaModel
 from .models import make_model
@@ -228,7 +227,8 @@ class SpecEngine:
                  record: bool = False, pipelined: bool = False, sync_time=None,
                  kv_block_size: int = 0, kv_blocks: int | None = None, precision: str = "bf16",
                  selector_time: str = "verify", sim_cost=None, sampling: bool = False,
-                 draft_sms: int = 0, draft_pdl: bool = True, draft_coresident: bool | None = None):
+                 draft_sms: int = 0, draft_pdl: bool = True, draft_coresident: bool | None = None,
+                 grouped_drafters: bool = True, stream_priority: str = "equal"):
         """target: weights (a model is built here) or a prebuilt model — e.g. a
         tp.LlamaTPModel rank, whose forward yields its vocab slice and whose
         argmax() combines across ranks.  sync_time(ms) -> ms: makes the
@@ -268,7 +268,12 @@ class SpecEngine:
         pipelined schedule): the drafters' decode
         steps run in co-resident launch shapes (ms_set_coresident: 64-thread
         gemv / decode-attention CTAs, the LM head on gemv) that fit on an SM
-        beside two verify-GEMM CTAs."""
+        beside two verify-GEMM CTAs.
+        grouped_drafters: K Llama drafters of one architecture run as row
+        groups of one model (one launch per op for all drafters; False: one
+        model per drafter on its own stream).  stream_priority ("equal",
+        "verify", "draft"): CUDA stream priorities of the pipelined schedule
+        (A/Bs in DESIGN §8)."""
         validate_config(cfg)
         if precision not in ("bf16", "fp32"):
             raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
@@ -312,10 +317,10 @@ class SpecEngine:
         self.V = V
         self.sync_time = sync_time
         # K Llama drafters of one architecture run as row groups of one model
-        # (one launch per op for all drafters); MS_GROUPED_DRAFT=0 disables
+        # (one launch per op for all drafters)
         self.grouped = (len(drafters) > 1 and all(getattr(w.cfg, "family", "") == "llama" for w in drafters)
                         and all(w.cfg == drafters[0].cfg for w in drafters)
-                        and os.environ.get("MS_GROUPED_DRAFT", "1") != "0" and precision == "bf16")
+                        and bool(grouped_drafters) and precision == "bf16")
         rows = slots * min(max_len, max(self.PREFILL_CHUNK, cfg.s_max + 2))
         self.ssms = [] if self.grouped else [make_model(w, max_rows=rows, device=device, small_gemm=True,
                                                         precision=precision) for w in drafters]
@@ -347,9 +352,10 @@ class SpecEngine:
         self.d2h_bytes = 0
         self.ssm_streams = [torch.cuda.Stream(self.dev) for _ in range(self.K)]
         # stream priorities for the pipelined schedule (CTA scheduling order when
-        # both streams' kernels wait for SM slots): equal by default;
-        # MS_VERIFY_PRIORITY=1 / MS_DRAFT_PRIORITY=1 raise one (A/B)
-        hi = lambda k: -1 if os.environ.get(k, "0") == "1" else 0  # noqa: E731
+        # both streams' kernels wait for SM slots): equal by default
+        if stream_priority not in ("equal", "verify", "draft"):
+            raise ValueError("stream_priority must be 'equal', 'verify' or 'draft'")
+        hi = lambda k: -1 if stream_priority == k else 0  # noqa: E731
         self.draft_pdl = bool(draft_pdl)
         self.draft_coresident = bool((pipelined and self.grouped) if draft_coresident is None else draft_coresident)
         self.draft_sms = self.verify_sms = 0
@@ -358,10 +364,10 @@ class SpecEngine:
                 raise ValueError("draft_sms partitions the SMs between concurrent drafting and "
                                  "verification: pipelined schedule only")
             self.draft_stream, self.verify_stream, self.draft_sms, self.verify_sms = _dev.sm_partition_streams(
-                draft_sms, self.dev, hi("MS_DRAFT_PRIORITY"), hi("MS_VERIFY_PRIORITY"))
+                draft_sms, self.dev, hi("draft"), hi("verify"))
         else:
-            self.draft_stream = torch.cuda.Stream(self.dev, priority=hi("MS_DRAFT_PRIORITY"))
-            self.verify_stream = torch.cuda.Stream(self.dev, priority=hi("MS_VERIFY_PRIORITY"))
+            self.draft_stream = torch.cuda.Stream(self.dev, priority=hi("draft"))
+            self.verify_stream = torch.cuda.Stream(self.dev, priority=hi("verify"))
         self.requests: list[Request] = []
         self._run_t0 = None
 

@@ -22,7 +22,6 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import math
-import os
 
 import torch
 
@@ -49,12 +48,12 @@ class LlamaModel:
 
 
     def __init__(self, w: LlamaWeights, max_rows: int, device="cuda", small_gemm: bool = False,
-                 fuse_norm: bool | None = None):
+                 fuse_norm: bool | None = None, split_kv: str | bool = False):
         """small_gemm: projections of <= 64 token rows with K <= K.GEMV_MAX_K use the
         low-latency ms_gemv (drafters' decode steps); the verifier keeps the
         tcgen05 path everywhere, so its numerics never depend on the row count.
 
-        fuse_norm (default; MS_FUSE_NORM=0 or False disables): RMSNorm folded
+        fuse_norm (default on for the verifier; False disables): RMSNorm folded
         across GEMMs — the gains are folded into w_qkv / w_gu / lm_head
         (LlamaWeights.fold_norms, in place), the O / down GEMMs emit per-row
         sums of squares and the QKV / gate-up / LM-head GEMMs scale by rstd:
@@ -65,14 +64,14 @@ class LlamaModel:
         self.small_gemm = small_gemm
         c = self.cfg
         if fuse_norm is None:
-            # on by default (MS_FUSE_NORM=0 disables): interleaved graph A/B of
+            # on by default: interleaved graph A/B of
             # the 70B verify forward (tools/ab_fuse_norm.py, same weights and
             # process) 27.02 vs 27.84 ms at Q = 5, 29.90 vs 30.85 at Q = 7,
             # 33.09 vs 33.62 at Q = 9, 36.89 vs 36.97 at Q = 11.  (An earlier
             # whole-bench A/B read it as a loss, but the adaptive selector's
             # s trajectory differs run to run, so bench lines cannot resolve
             # a ~2% forward change.)
-            fuse_norm = os.environ.get("MS_FUSE_NORM", "1") != "0" and not small_gemm
+            fuse_norm = not small_gemm
         o_split = K.linear_splits(c.d, c.n_heads * c.head_dim)
         d_split = K.linear_splits(c.d, c.ffn)
         self.fuse_norm = bool(fuse_norm) and o_split > 1 and d_split > 1  # producers need split-K
@@ -99,15 +98,14 @@ class LlamaModel:
         # merged in chunk order) for decode / verify calls (Q <= 16), never for
         # prefill chunks (large per-shape scratch; the prefill path is shared
         # by the greedy teacher and the speculative run, so losslessness
-        # holds).  Opt-in: MS_SPLITKV=auto (caches >= 1024 positions) or 1
+        # holds).  Opt-in: split_kv="auto" (caches >= 1024 positions) or True
         # (every decode / verify call).  Measured no gain on either kernel: MHA
         # (cfg5 on one GPU) verify 31.7 vs 29.4 ms; GQA row kernel (70B heads,
         # tools/attn_ab.py with AB_WS=1) 151 vs 116 us at a 4K cache, Q = 5, and
         # slower at every shorter cache — each extra CTA repeats the query
         # staging, the first DRAM latency and a 50 KB record.
-        env = os.environ.get("MS_SPLITKV", "0")
-        self.split_kv = env in ("1", "auto")
-        self.split_kv_min_len = 0 if env == "1" else 1024
+        self.split_kv = split_kv in (True, "auto")
+        self.split_kv_min_len = 0 if split_kv is True else 1024
         self._aws: dict = {}
 
     def _attn_ws(self, B: int, Q: int, T: int):

@@ -19,7 +19,6 @@ Memory layout (HBM):
 from __future__ import annotations
 
 import math
-import os
 
 import torch
 
@@ -35,12 +34,15 @@ class OPTModel:
     """Batched forward over the kernels with static activation buffers (so a
     forward of a given (B, Q) can be captured in a CUDA graph)."""
 
-    SPLIT_KV = os.environ.get("MS_SPLITKV", "0") == "1"
 
-    def __init__(self, w: OPTWeights, max_rows: int, device="cuda", small_gemm: bool = False):
+    def __init__(self, w: OPTWeights, max_rows: int, device="cuda", small_gemm: bool = False,
+                 split_kv: bool = False):
         """small_gemm: layer GEMMs of <= 64 token rows use the low-latency
         ms_gemv (drafters' decode steps); the verifier keeps the tcgen05 path
-        everywhere, so its numerics never depend on the row count."""
+        everywhere, so its numerics never depend on the row count.
+        split_kv: attention split over the cache length (fixed chunks, merged
+        in chunk order; measured slower on the benchmark's shapes)."""
+        self.split_kv = bool(split_kv)
         self.w, self.cfg = w, w.cfg
         self.small_gemm = small_gemm
         c = self.cfg
@@ -81,7 +83,7 @@ class OPTModel:
         x, h, qkv, at, ff = self.x[:R], self.h[:R], self.qkv[:R], self.attn[:R], self.ff[:R]
         K.embed(tokens, start, Q, w["tok_emb"], w["pos_emb"], c.pos_offset, out=x, stream=stream)
         # split-KV attention is opt-in: measured slower at these context lengths
-        aws = self._attn_ws(B, Q, cache.max_len) if self.SPLIT_KV else None
+        aws = self._attn_ws(B, Q, cache.max_len) if self.split_kv else None
         small = self.small_gemm and R <= 64
         # prompt prefill (caller-chosen, never by row count): tcgen05 CTA-pair GEMMs
         wide = prefill

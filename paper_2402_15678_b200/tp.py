@@ -246,7 +246,7 @@ class LlamaTPModel(LlamaModel):
     head / ffn / vocab counts; the residual stream x is the group's symmetric
     buffer (peers write their reduced column slices into it)."""
 
-    def __init__(self, shard: LlamaWeights, comm: TPComm, max_rows: int, device="cuda"):
+    def __init__(self, shard: LlamaWeights, comm: TPComm, max_rows: int, device="cuda", fused: bool = True):
         if max_rows > comm.max_rows:
             raise ValueError("max_rows exceeds the symmetric buffers")
         super().__init__(shard, max_rows=max_rows, device=device, fuse_norm=False)
@@ -254,10 +254,9 @@ class LlamaTPModel(LlamaModel):
         self.tp = comm.t
         self.x = comm.x  # residual stream = symmetric buffer
         self.v0 = comm.rank * shard.cfg.vocab
-        # fused GEMM -> reduce-scatter (peer stores from the O / down epilogues);
-        # MS_TP_FUSED=0: GEMM to a local partial + two-shot pull reduction
-        import os
-        self.fused = os.environ.get("MS_TP_FUSED", "1") != "0"
+        # fused (default): GEMM -> reduce-scatter by peer stores from the O /
+        # down epilogues; False: GEMM to a local partial + two-shot pull reduction
+        self.fused = bool(fused)
 
     def forward(self, tokens, start, slot, cache, logits, head_rows=None, stream=None, prefill: bool = False):
         """Rank-local vocab slice of the logits ([R', V/t] fp32).  prefill: the

@@ -315,7 +315,7 @@ def test_grouped_drafters_equal_separate_models(Q, B):
     assert torch.equal(glg, torch.cat(ref))
 
 
-def test_llama_engine_grouped_equals_per_drafter(monkeypatch):
+def test_llama_engine_grouped_equals_per_drafter():
     """The engine's grouped drafting and the per-drafter streams produce the
     same rounds (drafts, votes, accepted counts)."""
     from paper_2402_15678_b200.core import EngineConfig, Request
@@ -325,12 +325,11 @@ def test_llama_engine_grouped_equals_per_drafter(monkeypatch):
     target = LlamaWeights.random(tcfg, 0, device="cuda", std=0.05)
     drafters = [LlamaWeights.random(scfg, k + 1, device="cuda", std=0.05) for k in range(3)]
     outs = []
-    for grouped in ("1", "0"):
-        monkeypatch.setenv("MS_GROUPED_DRAFT", grouped)
+    for grouped in (True, False):
         cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=4, b_ssm=4, s_init=4, initial_weights=(1.0,) * 3)
         eng = SpecEngine(target, drafters, cfg, slots=4, max_len=128, fidelity=[0.9, 0.7, 0.5], record=True,
-                         adaptive=False)
-        assert eng.grouped == (grouped == "1")
+                         adaptive=False, grouped_drafters=grouped)
+        assert eng.grouped == grouped
         rng = np.random.default_rng(0)
         reqs = [Request(f"req-{i:03d}", [int(t) for t in rng.integers(0, tcfg.vocab, size=6)], 40) for i in range(4)]
         teacher = eng.greedy_teacher([Request(r.id, list(r.prompt), 40) for r in reqs], 40)

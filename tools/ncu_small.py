@@ -3,7 +3,8 @@ vote (K4), greedy accept from logits (K8 + K9) and one grouped drafter decode
 step (3 x Llama-160M, 16 requests, 200-position caches: rmsnorm, gemv QKV /
 O / gate-up, cluster GEMM down-proj, GQA/MHA attention, LM head, argmax).
 
-usage: python tools/ncu_small.py [vote|accept|draft|all]
+usage: python tools/ncu_small.py [vote|accept|va|draft|draftco|all]
+(draftco: the co-resident launch shapes the pipelined engine uses)
 """
 import os
 import sys
@@ -43,7 +44,7 @@ if what in ("accept", "va", "all"):
                          B, s, tgt.data_ptr(), ws.data_ptr(), n_acc.data_ptr(), emitted.data_ptr(),
                          n_emit.data_ptr(), fin.data_ptr(), None, st())
 
-if what in ("draft", "all"):
+if what in ("draft", "draftco", "all"):
     from paper_2402_15678_b200.llama import GroupedLlamaModel
     from paper_2402_15678_b200.weights import CONFIGS, KVCache, LlamaWeights
     c = CONFIGS["llama-160m"]
@@ -56,6 +57,9 @@ if what in ("draft", "all"):
     logits = torch.empty(G * B, c.vocab, device="cuda")
     am = torch.zeros(G * B, dtype=torch.int32, device="cuda")
     aws = torch.zeros(G * B, dtype=torch.int64, device="cuda")
+    if what == "draftco":  # the pipelined engine's co-resident decode shapes
+        _native.lib.ms_set_coresident(1)
+        m.coresident = True
     for _ in range(3):
         m.forward(tokens, start, slot, cache, logits)
         _native.call("ms_argmax_rows", logits.data_ptr(), 0, G * B, c.vocab, c.vocab, am.data_ptr(),
