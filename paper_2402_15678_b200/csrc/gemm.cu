@@ -7,15 +7,19 @@
 // stream-K with a global workspace, whole-tile persistent, token-tile
 // multicast to N-tile pairs, LayerNorm fused into the X operand.
 #include <cstdlib>
+#include <cstring>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "gemm_kernel.cuh"
+#include "gemm_gated.cuh"
 
 namespace ms {
 
 MS_LINEAR_WIDTHS(MS_LINEAR_DECLARE)
+MS_GATED_WIDTHS(MS_GATED_DECLARE)
+int g_gemm_probe = 0;  // ms_set_gemm_probe (timing probes only; results are garbage when != 0)
+unsigned long long* g_gemm_trace = nullptr;  // ms_set_gemm_trace (per-CTA phase timestamps)
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -43,6 +47,21 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
+// 2-D bf16 row-major [rows, cols] output, box = [64 cols, box_rows], no
+// swizzle (the source tile in shared memory is plain row-major)
+static bool make_tmap_store(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Split count for the weight-streaming regime, a function of (N, K) only.
 // From the measured sweep (tools/probe_gemm_graph.py, OPT-13B / OPT-125M
 // shapes at M = 16 and 80): about 260 CTAs (~1.75 per SM) is best — fewer
@@ -64,13 +83,40 @@ static int pick_bn(int M) {
   return M <= 16 ? 16 : (M + 15) / 16 * 16;
 }
 
-static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int m_tiles,
-                     cudaStream_t st, int G) {
+static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to,
+                     const LinearParams& p, int m_tiles, cudaStream_t st, int G) {
   switch (bn) {
 #define MS_CASE(BN) \
   case BN:          \
-    return launch_linear<BN>(tw, tx, p, m_tiles, st, G);
+    return launch_linear<BN>(tw, tx, to, p, m_tiles, st, G);
     MS_LINEAR_WIDTHS(MS_CASE)
+#undef MS_CASE
+    default:
+      return MS_ERR_VALUE;
+  }
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// persistent two-per-SM schedule of the wide gated GEMM (gemm_gated.cuh;
+// ms_set_gated_persistent, read at launch)
+static int g_gated_persistent = 1;
+
+static int launch_gated_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int m_tiles,
+                           int P, cudaStream_t st) {
+  switch (bn) {
+#define MS_CASE(BN) \
+  case BN:          \
+    return launch_linear_gated<BN>(tw, tx, p, m_tiles, P, st);
+    MS_GATED_WIDTHS(MS_CASE)
 #undef MS_CASE
     default:
       return MS_ERR_VALUE;
@@ -79,6 +125,9 @@ static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const
 
 int preload_gemm() {
   int n = 0;
+#define MS_PREG(BN) n += preload_linear_gated<BN>();
+  MS_GATED_WIDTHS(MS_PREG)
+#undef MS_PREG
 #define MS_PRE(BN) n += preload_linear<BN>();
   MS_LINEAR_WIDTHS(MS_PRE)
 #undef MS_PRE
@@ -88,6 +137,38 @@ int preload_gemm() {
 }  // namespace ms
 
 extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }
+
+// ring-depth override for probes (0, 0 = the per-launch rule)
+static int g_ring_sw = 0, g_ring_sx = 0;
+extern "C" int ms_set_gated_persistent(int on) {
+  const int old = ms::g_gated_persistent;
+  ms::g_gated_persistent = on ? 1 : 0;
+  return old;
+}
+
+extern "C" int ms_set_gemm_trace(void* buf) {
+  ms::g_gemm_trace = (unsigned long long*)buf;
+  return MS_OK;
+}
+
+extern "C" int ms_set_gemm_probe(int mode) {
+  if (mode < 0 || mode > 5) return MS_ERR_VALUE;
+  ms::g_gemm_probe = mode;
+  return MS_OK;
+}
+namespace ms {
+int ring_override(int* sw, int* sx) {
+  if (g_ring_sw > 0) *sw = g_ring_sw;
+  if (g_ring_sx > 0) *sx = g_ring_sx;
+  return 0;
+}
+}  // namespace ms
+extern "C" int ms_set_ring(int sw, int sx) {
+  if (sw < 0 || sw > 14 || sx < 0 || sx > 6 || (sw > 0 && sw < 2) || (sx > 0 && sx < 2)) return MS_ERR_VALUE;
+  g_ring_sw = sw;
+  g_ring_sx = sx;
+  return MS_OK;
+}
 
 struct RmsArgs {
   float* out = nullptr;
@@ -130,6 +211,8 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.kb_total = kb_total; p.n_tiles = n_tiles;
   p.sw = p.sx = 0;
+  p.dbg = ms::g_gemm_probe;
+  p.trace = ms::g_gemm_trace;
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
   p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
   if (splits <= 0) splits = linear_auto_splits(N, K);
@@ -137,7 +220,23 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   if (splits > 8) return MS_ERR_UNSUPPORTED;  // portable cluster size
   if (rms.out && (splits < 2 || act == 2 || out_f32)) return MS_ERR_UNSUPPORTED;  // producer: split-K bf16 path
   p.splits = splits;
-  return launch_bn(bn, tw, tx, p, m_tiles, (cudaStream_t)stream, G);
+  const int slots = 2 * sm_count();
+  if (g_gated_persistent && act == 2 && splits == 1 && G == 1 && bn <= 128 && n_tiles > slots && !rms.tp_recv &&
+      !out_f32 && !rms.out) {
+    // more one-split gated tiles than two-per-SM slots (the 70B gate/up):
+    // persistent CTAs with double-buffered TMEM, bitwise the same outputs
+    p.tma_store = 0;
+    return launch_gated_bn(bn, tw, tx, p, m_tiles, slots, (cudaStream_t)stream);
+  }
+  // gated one-split GEMMs store their output tiles with TMA (gemm_kernel.cuh)
+  CUtensorMap to;
+  memset(&to, 0, sizeof(to));
+  p.tma_store = 0;
+  if (splits == 1 && act == 2 && G == 1 && !rms.tp_recv && !out_f32 && ldc % 8 == 0) {
+    if (!make_tmap_store(&to, out, M, N / 2, ldc, bn)) return MS_ERR_CUDA;
+    p.tma_store = 1;
+  }
+  return launch_bn(bn, tw, tx, to, p, m_tiles, (cudaStream_t)stream, G);
 }
 
 extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,

@@ -53,6 +53,10 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int sw, sx;                     // weight / token ring depths of this launch
+  int dbg;                        // probe only (ms_set_gemm_probe): 1 no MMA / no X, 2 no MMA, 3 no X loads,
+                                  // 4 no epilogue, 5 = 1 + 4
+  int tma_store;                  // gated one-split epilogue: the output tile leaves smem by one TMA store (tmO)
+  unsigned long long* trace;      // probe only (ms_set_gemm_trace): per-CTA %globaltimer stamps [grid][12]
   // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
   // output (row m, feature f) is stored straight into the receive slot of the
   // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
@@ -103,7 +107,10 @@ struct LinearCfg {
   // the fp32 partial tile is staged in the (idle) ring smem only for the
   // split-K cluster reduction; the single-split gated epilogue exchanges
   // gate/up through smem as well
-  static constexpr int GATED_EPI_BYTES = BN * 65 * 4 + BN * 64 * 2;  // up half + bf16 output tile
+  // up half [BN][65] fp32, then the bf16 output tile [BN][64] at a 1024-byte
+  // aligned offset (the source of a TMA store)
+  static constexpr int O_OFF = (BN * 65 * 4 + 1023) / 1024 * 1024;
+  static constexpr int GATED_EPI_BYTES = O_OFF + BN * 64 * 2;
   __host__ __device__ static int data_bytes(int sw, int sx, bool part) {
     const int pipe = sw * W_BYTES + sx * X_BYTES;
     int need = part ? PART_BYTES : GATED_EPI_BYTES;
@@ -142,6 +149,14 @@ __device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int f
 
 __device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+__device__ __forceinline__ void trace_stamp(const LinearParams& p, int slot) {
+  if (!p.trace) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  p.trace[(int64_t)cta * 12 + slot] = t;
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -163,7 +178,7 @@ template <int BN>
 // (tools/ab_lib_gemm.py, round 2)
 __global__ void __launch_bounds__(kThreads, 2)
 linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-              const LinearParams p) {
+              const __grid_constant__ CUtensorMap tmO, const LinearParams p) {
   using C = LinearCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -213,6 +228,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   const uint32_t tmem = *tmem_slot;
 
   const int nkb = kb1 - kb0;
+  if (threadIdx.x == 64) trace_stamp(p, 0);
   if (warp == 0) {
     if (lane == 0) {
       // weight producer: the first SW weight tiles do not depend on the previous
@@ -231,6 +247,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
         tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
       }
+      trace_stamp(p, 1);
     } else {
       pdl_trigger();
     }
@@ -240,7 +257,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       const uint64_t pol_x = tc::policy_evict_last();  // tokens are re-read by every tile
       pdl_wait();
       pdl_trigger();
-      for (int i = 0; i < nkb; ++i) {
+      for (int i = 0; i < nkb && (p.dbg != 1 && p.dbg != 3 && p.dbg != 5); ++i) {
         const int st = i % SX;
         if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
@@ -256,7 +273,15 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       for (int i = 0; i < nkb; ++i) {
         const int ws = i % SW, xs = i % SX;
         tc::mbar_wait(&fullW[ws], (i / SW) & 1);
-        tc::mbar_wait(&fullX[xs], (i / SX) & 1);
+        if (p.dbg == 1 || p.dbg == 2 || p.dbg == 5) {  // probe: release the stages without an MMA
+          if (p.dbg == 2) {
+            tc::mbar_wait(&fullX[xs], (i / SX) & 1);
+            tc::mbar_arrive(&emptyX[xs]);
+          }
+          tc::mbar_arrive(&emptyW[ws]);
+          continue;
+        }
+        if (p.dbg != 3) tc::mbar_wait(&fullX[xs], (i / SX) & 1);
         tc::fence_after_sync();
         const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
         const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
@@ -267,6 +292,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         tc::mma_commit(&emptyX[xs]);
       }
       tc::mma_commit(tmem_full);
+      trace_stamp(p, 2);
     }
   } else {
     // ---------------- epilogue: warps 2..5, TMEM lane quadrant = warp % 4 ----------
@@ -291,16 +317,19 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
+    if (threadIdx.x == 64) trace_stamp(p, 3);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 
-    if (p.splits == 1 && p.act == 2) {
+    if (p.dbg >= 4) {
+      // probe: no epilogue work (4: with MMA + token loads, 5: weight stream only)
+    } else if (p.splits == 1 && p.act == 2) {
       // gated SiLU, one split (the pipeline smem is idle once tmem_full fired):
       // (1) the up warps (TMEM lanes 64..127) park the whole up half in smem,
       // (2) one barrier, the gate warps form silu(g) * u into a bf16 output
       // tile in smem, (3) one barrier, all four warps store the tile with
       // coalesced 16-byte writes.
-      float* U = reinterpret_cast<float*>(smem);                            // [BN][65] fp32
-      __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(U + BN * 65);    // [BN][64] bf16
+      float* U = reinterpret_cast<float*>(smem);                                // [BN][65] fp32
+      __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(smem + C::O_OFF);    // [BN][64] bf16
       const bool up = q >= 2;
       const int f = (q & 1) * 32 + lane;  // gate / up feature within the 64-wide half
       for (int c0 = 0; c0 < m_hi; c0 += 32) {
@@ -315,6 +344,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
       }
       epi_bar128();
+      if (threadIdx.x == 64) trace_stamp(p, 4);
       // the gate warps read their TMEM half after the barrier (re-loading is
       // cheaper than holding up to 256 columns in registers)
       if (!up) {
@@ -329,14 +359,27 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
               O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f),
                                                    U[(c0 + j) * 65 + f]));
         }
+        if (p.tma_store) tc::fence_proxy_async_smem();  // O visible to the TMA (async proxy)
       }
       epi_bar128();
-      const int et = threadIdx.x - 64;  // 0..127
-      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
-      for (int e = et; e < m_hi * 8; e += 128) {
-        const int row = e >> 3, ch = e & 7;
-        *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
-            *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
+      if (threadIdx.x == 64) trace_stamp(p, 5);
+      if (p.tma_store) {
+        // one bulk tensor store of the [m_hi x 64] tile (rows past M are
+        // clipped by the tensor map): the 16-byte store loop cost ~13 us per
+        // CTA at M = 112 beside the co-resident CTA's weight stream
+        if (threadIdx.x == 64) {
+          tc::tma_store_2d(&tmO, O, tile_n * (kBM / 2), orow);
+          tc::bulk_commit_group();
+          tc::bulk_wait_group_read0();  // smem may be released once the TMA has read it
+        }
+      } else {
+        const int et = threadIdx.x - 64;  // 0..127
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
+        for (int e = et; e < m_hi * 8; e += 128) {
+          const int row = e >> 3, ch = e & 7;
+          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
+              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
+        }
       }
     } else if (p.splits == 1) {
       for (int c0 = 0; c0 < m_hi; c0 += 16) {
@@ -365,6 +408,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   }
   __syncwarp();  // producer / MMA roles ran on lane 0: reconverge before the aligned cluster / CTA barriers
   if (p.splits > 1) {
+    if (threadIdx.x == 64) trace_stamp(p, 4);
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
     // `split` reduces a 1/splits slice of the tile, adding the partials of
@@ -372,6 +416,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     // Gated SiLU: a unit covers gate features f4..f4+3 and their up partners
     // f4+64.. of the same (staged) tile.
     cluster_sync_all();
+    if (threadIdx.x == 64) trace_stamp(p, 5);
     const int m_hi = min(BN, p.M - m0);
     const bool gated = p.act == 2;
     const int upr = (gated ? kBM / 2 : kBM) / 4;  // float4 units per token row
@@ -439,6 +484,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
             }
           }
         }
+        if (threadIdx.x == 64 && ub == u0 + 64) trace_stamp(p, 8);
 #pragma unroll
         for (int i = 0; i < UB; ++i) {
           const int u = ub + i * kThreads;
@@ -496,30 +542,33 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
       }
     }
+    if (threadIdx.x == 64) trace_stamp(p, 9);
     cluster_sync_all();  // peers may still be reading this CTA's smem
   }
+  if (threadIdx.x == 64) trace_stamp(p, 6);
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc<C::TMEM_COLS>(tmem);
   }
+  if (threadIdx.x == 64) trace_stamp(p, 7);
 }
 
 // Launch one linear_kernel<BN> (host).  Ring depths per launch: ~210 KB of
 // stages when the grid fits one CTA per SM, ~104 KB at two per SM, never more
 // stages than k-blocks per CTA (so small drafter GEMMs leave shared memory
 // for concurrent kernels).
+int ring_override(int* sw, int* sx);  // gemm.cu (ms_set_ring, A/B probes)
+
 template <int BN>
-int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, int m_tiles, cudaStream_t st,
-                  int G) {
+int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to, LinearParams p, int m_tiles,
+                  cudaStream_t st, int G) {
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    int sw, sx;
-    C::rings_for(210 * 1024, &sw, &sx);
-    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::smem(sw, sx, true)) != cudaSuccess)
+    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        cudaSuccess)
       return MS_ERR_CUDA;
     attr_set = true;
   }
@@ -531,12 +580,14 @@ int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, 
   // the fp32 split-K staging tile may already rule out two CTAs per SM: then
   // take the deep single-CTA rings
   if (part && C::smem(sw, sx, part) > 113 * 1024) C::rings_for(210 * 1024, &sw, &sx);
+  ring_override(&sw, &sx);
   if (sw > kb_per_cta) sw = kb_per_cta < 2 ? 2 : kb_per_cta;
   if (sx > kb_per_cta) sx = kb_per_cta < 2 ? 2 : kb_per_cta;
+  if (C::smem(sw, sx, part) > 227 * 1024) return MS_ERR_UNSUPPORTED;
   p.sw = sw;
   p.sx = sx;
   return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part),
-                st, p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
+                st, p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, to, p);
 }
 
 template <int BN>
@@ -548,12 +599,12 @@ int preload_linear() {
 #define MS_LINEAR_WIDTHS(X) X(16) X(32) X(48) X(64) X(80) X(96) X(112) X(128) X(144) X(160) X(176) X(192) \
   X(208) X(224) X(240) X(256)
 #define MS_LINEAR_DECLARE(BN)                                                                         \
-  extern template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, LinearParams, int,      \
-                                        cudaStream_t, int);                                             \
+  extern template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,    \
+                                        LinearParams, int, cudaStream_t, int);                          \
   extern template int preload_linear<BN>();
 #define MS_LINEAR_INSTANTIATE(BN)                                                                     \
-  template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, LinearParams, int, cudaStream_t, \
-                                 int);                                                                  \
+  template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, LinearParams, int, \
+                                 cudaStream_t, int);                                                    \
   template int preload_linear<BN>();
 
 }  // namespace ms

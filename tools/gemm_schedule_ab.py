@@ -1,10 +1,10 @@
-"""A/B of the gate/up GEMM schedule (ms_set_tail_split: 0 = one launch of
-448 one-split tiles = 1.51 waves, 1 = a full wave + a 2-way-split tail launch
-without the dependency wait) on the 70B verify forward (B=16, ctx 190) and its
-four GEMM kinds: one CUDA graph per (schedule, what), replayed interleaved.
-(The same harness ran round 2's L2-prefetch and stream-K A/Bs,
-profiles/r2_l2pf_ab.jsonl / r2_stream_k_ab.jsonl, whose knobs were removed.)
-usage: python tools/sk_ab.py [Qs=5,7,9]"""
+"""A/B of the gate/up GEMM schedule (ms_set_gated_persistent: 0 = one tile
+per CTA, 448 tiles = 1.51 waves; 1 = persistent two-per-SM CTAs with
+double-buffered TMEM, gemm_gated.cuh) on the 70B verify forward (B=16, ctx 190)
+and its four GEMM kinds: one CUDA graph per (schedule, what), replayed
+interleaved.  (The same harness ran round 2's L2-prefetch, stream-K and
+tail-split A/Bs, profiles/r2_*_ab.jsonl, whose knobs were removed.)
+usage: python tools/gemm_schedule_ab.py [Qs=5,7,9]"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -44,14 +44,14 @@ for Q in Qs:
     fns = [("full", full)] + [(k, gemm(k)) for k in ("qkv", "o", "gu", "down")]
     graphs = {}
     for d in dists:
-        _native.lib.ms_set_tail_split(d)
+        _native.lib.ms_set_gated_persistent(d)
         for nm, fn in fns:
             fn(); torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
             graphs[(d, nm)] = g
-    _native.lib.ms_set_tail_split(1)
+    _native.lib.ms_set_gated_persistent(1)
     res = {}
     for rep in range(3):
         for nm, _ in fns:

@@ -1,0 +1,58 @@
+"""A/B of ms_linear's TMA ring depths (ms_set_ring) on 80-layer graph chains
+of the 70B verify GEMMs at M rows: weight stages sw x token stages sx; two
+CTAs per SM need smem <= ~113 KB (sw*16 KB + sx*BN*128 B), one CTA per SM
+<= 227 KB.  usage: python tools/ring_ab.py [M=112] ["sw:sx,..."]"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2402_15678_b200 import _native, kernels as K
+from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 112
+cfgs = [tuple(int(v) for v in c.split(":")) for c in (sys.argv[2] if len(sys.argv) > 2 else
+        "0:0,4:2,3:3,2:4,5:2,6:2,8:2,10:2,8:4,12:2").split(",")]
+c = CONFIGS["llama-2-70b"]
+w = LlamaWeights.random(c, 0)
+L = c.n_layers
+h = torch.randn(M, c.d, device="cuda").to(torch.bfloat16)
+x = torch.randn(M, c.d, device="cuda").to(torch.bfloat16)
+ff = torch.randn(M, c.ffn, device="cuda").to(torch.bfloat16)
+ffo = torch.empty(M, c.ffn, device="cuda", dtype=torch.bfloat16)
+def chain(kind):
+    def f():
+        for i in range(L):
+            p = f"l{i}."
+            if kind == "gu":
+                K.linear(h, w[p + "w_gu"], act=2, out=ffo)
+            else:
+                K.linear(ff, w[p + "w_down"], residual=x, out=x)
+    return f
+size = {"gu": 2 * c.d * c.ffn, "down": c.d * c.ffn}
+for kind in ("gu", "down"):
+    graphs = {}
+    for sw, sx in cfgs:
+        if _native.lib.ms_set_ring(sw, sx) != 0:
+            continue
+        f = chain(kind)
+        try:
+            f(); torch.cuda.synchronize()
+        except Exception as e:
+            print(json.dumps({"gemm": kind, "sw": sw, "sx": sx, "error": str(e)[:80]}), flush=True)
+            continue
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            f()
+        graphs[(sw, sx)] = g
+    _native.lib.ms_set_ring(0, 0)
+    res = {k: [] for k in graphs}
+    for rep in range(3):
+        for k, g in graphs.items():
+            g.replay(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record(); g.replay(); g.replay(); e1.record(); torch.cuda.synchronize()
+            res[k].append(e0.elapsed_time(e1) / 2)
+    for k, v in res.items():
+        us = min(v) * 1e3 / L
+        print(json.dumps({"gemm": kind, "M": M, "sw": k[0], "sx": k[1], "us_per_layer": round(us, 2),
+                          "TBs": round(2 * size[kind] / (us * 1e-6) / 1e12, 3)}), flush=True)
+    del graphs
