@@ -430,8 +430,74 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       // the stored bf16 values over this tile's 128 features is a fixed-order
       // warp reduction written to its own (tile, row) slot — deterministic
       const int t0 = split * m_hi / p.splits, t1 = (split + 1) * m_hi / p.splits;
+      const int f4 = lane * 4;
+      const int feat = n0 + f4;
+      const bool vec = (p.N % 4 == 0) && (p.ldc % 4 == 0) && (!p.residual || p.ldr % 4 == 0) && !p.tp_recv &&
+                       !p.out_f32 && ((reinterpret_cast<uintptr_t>(p.out) & 7) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(p.residual) & 7) == 0) && !p.bias;
+      if (vec && p.splits <= 4) {
+        // RB rows per warp at once: every partial (DSMEM) and residual load of
+        // the batch is issued before the first add — one latency per batch
+        // instead of (splits + 1) per row; the same additions in the same
+        // (rank) order and the same stores / sums of squares as epi_store
+        constexpr int RB = 4;
+        constexpr int W = kThreads / 32;
+        for (int jb = t0 + warp; jb < t1; jb += W * RB) {
+          float4 part[RB][4];
+          uint2 res[RB];
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            const int j = jb + i * W;
+            if (j < t1) {
+#pragma unroll
+              for (int rk = 0; rk < 4; ++rk)
+                if (rk < p.splits) part[i][rk] = ld_dsmem_f4(P + j * kBM + f4, rk);
+              if (p.residual && feat < p.N)
+                res[i] = *reinterpret_cast<const uint2*>(p.residual + (int64_t)(orow + j) * p.ldr + feat);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            const int j = jb + i * W;
+            if (j >= t1) break;  // warp-uniform
+            float4 acc = part[i][0];
+#pragma unroll
+            for (int rk = 1; rk < 4; ++rk)
+              if (rk < p.splits) {
+                acc.x += part[i][rk].x; acc.y += part[i][rk].y; acc.z += part[i][rk].z; acc.w += part[i][rk].w;
+              }
+            const float rs = p.rms_in ? s_rstd[j] : 1.f;
+            float v4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
+            float sq = 0.f;
+            if (feat < p.N) {
+              if (p.act == 1) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) v4[t] = fmaxf(v4[t], 0.0f);
+              }
+              if (p.residual) {
+                const __nv_bfloat162* rr = reinterpret_cast<const __nv_bfloat162*>(&res[i]);
+                const float2 r01 = __bfloat1622float2(rr[0]), r23 = __bfloat1622float2(rr[1]);
+                v4[0] += r01.x; v4[1] += r01.y; v4[2] += r23.x; v4[3] += r23.y;
+              }
+              __nv_bfloat16 b[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t) b[t] = f2bf(v4[t]);
+              uint2 pk;
+              pk.x = (uint32_t)__bfloat16_as_ushort(b[0]) | ((uint32_t)__bfloat16_as_ushort(b[1]) << 16);
+              pk.y = (uint32_t)__bfloat16_as_ushort(b[2]) | ((uint32_t)__bfloat16_as_ushort(b[3]) << 16);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) = pk;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float st = bf2f(b[t]);
+                sq += st * st;
+              }
+            }
+            sq = warp_sum(sq);
+            if (lane == 0) p.rms_out[(int64_t)(orow + j) * p.rms_ld + tile_n] = sq;
+          }
+        }
+      } else
       for (int j = t0 + warp; j < t1; j += kThreads / 32) {
-        const int f4 = lane * 4;
         float4 acc = ld_dsmem_f4(P + j * kBM + f4, 0);
         for (int rk = 1; rk < p.splits; ++rk) {
           const float4 v = ld_dsmem_f4(P + j * kBM + f4, rk);
@@ -439,7 +505,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
         const float rs = p.rms_in ? s_rstd[j] : 1.f;
         const float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
-        const int feat = n0 + f4;
         float sq = 0.f;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
