@@ -525,6 +525,71 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       const bool vec = (p.N % 4 == 0) && (p.ldc % 4 == 0) && (!p.residual || p.ldr % 4 == 0) && !p.tp_recv &&
                        ((reinterpret_cast<uintptr_t>(p.out) & (p.out_f32 ? 15 : 7)) == 0) &&
                        ((reinterpret_cast<uintptr_t>(p.residual) & 7) == 0) && !p.bias;
+      // one unit's epilogue: rstd, act, residual, 4-wide store
+      auto finish = [&](int u, const float4& acc, const uint2& res) {
+        const int j = u / upr, f4 = (u - j * upr) * 4;
+        const float rs = p.rms_in ? s_rstd[j] : 1.f;
+        float a4[4] = {acc.x * rs, acc.y * rs, acc.z * rs, acc.w * rs};
+        const int feat = n0 + f4;
+        if (vec && feat < p.N) {
+          if (p.act == 1) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) a4[t] = fmaxf(a4[t], 0.f);
+          }
+          if (p.residual) {
+            const __nv_bfloat162* rr = reinterpret_cast<const __nv_bfloat162*>(&res);
+            const float2 r01 = __bfloat1622float2(rr[0]), r23 = __bfloat1622float2(rr[1]);
+            a4[0] += r01.x; a4[1] += r01.y; a4[2] += r23.x; a4[3] += r23.y;
+          }
+          if (p.out_f32) {
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) =
+                make_float4(a4[0], a4[1], a4[2], a4[3]);
+          } else {
+            uint2 pk;
+            pk.x = pack_bf16x2(a4[0], a4[1]);
+            pk.y = pack_bf16x2(a4[2], a4[3]);
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) = pk;
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
+        }
+      };
+      if (p.splits <= 4) {
+        // 4 units per thread with every rank's partial (DSMEM) and the residual
+        // loaded before the first add: one latency per batch; the additions in
+        // rank order as below
+        constexpr int UW = 4;
+        for (int ub = u0 + (int)threadIdx.x; ub < u1; ub += kThreads * UW) {
+          float4 part[UW][4];
+          uint2 res[UW];
+#pragma unroll
+          for (int i = 0; i < UW; ++i) {
+            const int u = ub + i * kThreads;
+            if (u < u1) {
+              const int j = u / upr, f4 = (u - j * upr) * 4;
+#pragma unroll
+              for (int rk = 0; rk < 4; ++rk)
+                if (rk < p.splits) part[i][rk] = ld_dsmem_f4(P + j * kBM + f4, rk);
+              if (vec && p.residual && n0 + f4 < p.N)
+                res[i] = *reinterpret_cast<const uint2*>(p.residual + (int64_t)(orow + j) * p.ldr + n0 + f4);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < UW; ++i) {
+            const int u = ub + i * kThreads;
+            if (u >= u1) continue;
+            float4 acc = part[i][0];
+#pragma unroll
+            for (int rk = 1; rk < 4; ++rk)
+              if (rk < p.splits) {
+                acc.x += part[i][rk].x; acc.y += part[i][rk].y; acc.z += part[i][rk].z; acc.w += part[i][rk].w;
+              }
+            finish(u, acc, res[i]);
+          }
+        }
+      } else
       for (int ub = u0 + (int)threadIdx.x; ub < u1; ub += kThreads * UB) {
         float4 acc[UB];
         uint2 res[UB];
@@ -549,39 +614,10 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
             }
           }
         }
-        if (threadIdx.x == 64 && ub == u0 + 64) trace_stamp(p, 8);
 #pragma unroll
         for (int i = 0; i < UB; ++i) {
           const int u = ub + i * kThreads;
-          if (u >= u1) continue;
-          const int j = u / upr, f4 = (u - j * upr) * 4;
-          const float rs = p.rms_in ? s_rstd[j] : 1.f;
-          float a4[4] = {acc[i].x * rs, acc[i].y * rs, acc[i].z * rs, acc[i].w * rs};
-          const int feat = n0 + f4;
-          if (vec && feat < p.N) {
-            if (p.act == 1) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t) a4[t] = fmaxf(a4[t], 0.f);
-            }
-            if (p.residual) {
-              const __nv_bfloat162* rr = reinterpret_cast<const __nv_bfloat162*>(&res[i]);
-              const float2 r01 = __bfloat1622float2(rr[0]), r23 = __bfloat1622float2(rr[1]);
-              a4[0] += r01.x; a4[1] += r01.y; a4[2] += r23.x; a4[3] += r23.y;
-            }
-            if (p.out_f32) {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) =
-                  make_float4(a4[0], a4[1], a4[2], a4[3]);
-            } else {
-              uint2 pk;
-              pk.x = pack_bf16x2(a4[0], a4[1]);
-              pk.y = pack_bf16x2(a4[2], a4[3]);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)(orow + j) * p.ldc + feat) = pk;
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (feat + t < p.N) epi_store(p, orow + j, feat + t, a4[t], grp);
-          }
+          if (u < u1) finish(u, acc[i], res[i]);
         }
       }
     } else {
