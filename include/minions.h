@@ -162,23 +162,11 @@ int ms_gemv(const void* x, int64_t ldx, const void* w, const void* bias, const v
             void* stream);
 /* Default split-K factor for an [N, K] weight (cluster path). */
 int ms_linear_splits(int N, int K);
-/* Ring-depth override for probes: weight / token TMA ring stages of every
- * following ms_linear launch (2..14 / 2..6; 0 = the per-launch rule). */
 /* Schedule of one-split gated ms_linear GEMMs with more output tiles than two
  * CTAs per SM (the 70B gate/up): 1 (default) = persistent two-per-SM CTAs with a
  * double-buffered TMEM accumulator (gemm_gated.cuh; bitwise the same outputs),
  * 0 = one tile per CTA.  Read at launch; returns the previous value. */
 int ms_set_gated_persistent(int on);
-int ms_set_ring(int sw, int sx);
-/* Timing probe of ms_linear's pipeline (results are garbage when != 0):
- * 1 = weight stream only (no MMA, no token loads), 2 = weight + token loads,
- * no MMA, 3 = MMAs without token loads; 0 = normal. */
-int ms_set_gemm_probe(int mode);
-/* Probe: per-CTA %globaltimer stamps of ms_linear launches into buf
- * [grid][12] u64 (null = off): 0 start, 1 last weight load issued, 2 last MMA
- * issued, 3 accumulator complete, 4/5 gated-epilogue phases, 6 epilogue done,
- * 7 exit. */
-int ms_set_gemm_trace(void* buf);
 
 /* ---- decoder pieces around the GEMMs (OPT-style, pre-LN) ----------------
  * Token + learned-position embedding of R = B*Q rows: row r = b*Q + i is at

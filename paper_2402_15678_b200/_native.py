@@ -41,10 +41,7 @@ _SIGS = {
     "ms_linear_wide": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
     "ms_gemv": [_P, _I64, _P, _P, _P, _I64, _P, _I64, _I, _I, _I, _I, _I, _P],
     "ms_linear_splits": [_I, _I],
-    "ms_set_ring": [_I, _I],
     "ms_set_gated_persistent": [_I],
-    "ms_set_gemm_probe": [_I],
-    "ms_set_gemm_trace": [_P],
     "ms_embed": [_P, _P, _I, _P, _P, _I, _I, _I, _P, _P],
     "ms_layernorm": [_P, _I64, _P, _P, _P, _F, _I, _I, _P, _I64, _P],
     "ms_kv_append": [_P, _I64, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P],

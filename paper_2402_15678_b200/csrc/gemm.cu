@@ -18,8 +18,6 @@ namespace ms {
 
 MS_LINEAR_WIDTHS(MS_LINEAR_DECLARE)
 MS_GATED_WIDTHS(MS_GATED_DECLARE)
-int g_gemm_probe = 0;  // ms_set_gemm_probe (timing probes only; results are garbage when != 0)
-unsigned long long* g_gemm_trace = nullptr;  // ms_set_gemm_trace (per-CTA phase timestamps)
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -138,37 +136,12 @@ int preload_gemm() {
 
 extern "C" int ms_linear_splits(int N, int K) { return ms::linear_auto_splits(N, K); }
 
-// ring-depth override for probes (0, 0 = the per-launch rule)
-static int g_ring_sw = 0, g_ring_sx = 0;
 extern "C" int ms_set_gated_persistent(int on) {
   const int old = ms::g_gated_persistent;
   ms::g_gated_persistent = on ? 1 : 0;
   return old;
 }
 
-extern "C" int ms_set_gemm_trace(void* buf) {
-  ms::g_gemm_trace = (unsigned long long*)buf;
-  return MS_OK;
-}
-
-extern "C" int ms_set_gemm_probe(int mode) {
-  if (mode < 0 || mode > 5) return MS_ERR_VALUE;
-  ms::g_gemm_probe = mode;
-  return MS_OK;
-}
-namespace ms {
-int ring_override(int* sw, int* sx) {
-  if (g_ring_sw > 0) *sw = g_ring_sw;
-  if (g_ring_sx > 0) *sx = g_ring_sx;
-  return 0;
-}
-}  // namespace ms
-extern "C" int ms_set_ring(int sw, int sx) {
-  if (sw < 0 || sw > 14 || sx < 0 || sx > 6 || (sw > 0 && sw < 2) || (sx > 0 && sx < 2)) return MS_ERR_VALUE;
-  g_ring_sw = sw;
-  g_ring_sx = sx;
-  return MS_OK;
-}
 
 struct RmsArgs {
   float* out = nullptr;
@@ -211,8 +184,6 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
   p.out = out; p.ldc = ldc; p.out_f32 = out_f32; p.act = act;
   p.kb_total = kb_total; p.n_tiles = n_tiles;
   p.sw = p.sx = 0;
-  p.dbg = ms::g_gemm_probe;
-  p.trace = ms::g_gemm_trace;
   p.rms_out = rms.out; p.rms_in = rms.in; p.rms_nparts = rms.nparts; p.rms_ld = rms.ld; p.rms_eps = rms.eps;
   p.tp_recv = rms.tp_recv; p.tp_rank = rms.tp_rank; p.tp_slice = rms.tp_slice; p.tp_rows = rms.tp_rows;
   if (splits <= 0) splits = linear_auto_splits(N, K);

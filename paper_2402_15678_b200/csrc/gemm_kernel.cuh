@@ -53,10 +53,7 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int sw, sx;                     // weight / token ring depths of this launch
-  int dbg;                        // probe only (ms_set_gemm_probe): 1 no MMA / no X, 2 no MMA, 3 no X loads,
-                                  // 4 no epilogue, 5 = 1 + 4
   int tma_store;                  // gated one-split epilogue: the output tile leaves smem by one TMA store (tmO)
-  unsigned long long* trace;      // probe only (ms_set_gemm_trace): per-CTA %globaltimer stamps [grid][12]
   // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
   // output (row m, feature f) is stored straight into the receive slot of the
   // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
@@ -149,13 +146,6 @@ __device__ __forceinline__ float epi_store(const LinearParams& p, int tok, int f
 
 __device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__device__ __forceinline__ void trace_stamp(const LinearParams& p, int slot) {
-  if (!p.trace) return;
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  p.trace[(int64_t)cta * 12 + slot] = t;
-}
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -228,7 +218,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   const uint32_t tmem = *tmem_slot;
 
   const int nkb = kb1 - kb0;
-  if (threadIdx.x == 64) trace_stamp(p, 0);
   if (warp == 0) {
     if (lane == 0) {
       // weight producer: the first SW weight tiles do not depend on the previous
@@ -247,7 +236,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         tc::mbar_arrive_expect_tx(&fullW[st], C::W_BYTES);
         tc::tma_load_2d(sW + st * C::W_BYTES, &tmW, &fullW[st], (kb0 + i) * kBK, wrow, pol_w);
       }
-      trace_stamp(p, 1);
     } else {
       pdl_trigger();
     }
@@ -257,7 +245,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       const uint64_t pol_x = tc::policy_evict_last();  // tokens are re-read by every tile
       pdl_wait();
       pdl_trigger();
-      for (int i = 0; i < nkb && (p.dbg != 1 && p.dbg != 3 && p.dbg != 5); ++i) {
+      for (int i = 0; i < nkb; ++i) {
         const int st = i % SX;
         if (i >= SX) tc::mbar_wait(&emptyX[st], ((i / SX) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&fullX[st], C::X_BYTES);
@@ -273,15 +261,7 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
       for (int i = 0; i < nkb; ++i) {
         const int ws = i % SW, xs = i % SX;
         tc::mbar_wait(&fullW[ws], (i / SW) & 1);
-        if (p.dbg == 1 || p.dbg == 2 || p.dbg == 5) {  // probe: release the stages without an MMA
-          if (p.dbg == 2) {
-            tc::mbar_wait(&fullX[xs], (i / SX) & 1);
-            tc::mbar_arrive(&emptyX[xs]);
-          }
-          tc::mbar_arrive(&emptyW[ws]);
-          continue;
-        }
-        if (p.dbg != 3) tc::mbar_wait(&fullX[xs], (i / SX) & 1);
+        tc::mbar_wait(&fullX[xs], (i / SX) & 1);
         tc::fence_after_sync();
         const uint64_t ad = tc::smem_desc_sw128(sW + ws * C::W_BYTES);
         const uint64_t bd = tc::smem_desc_sw128(sX + xs * C::X_BYTES);
@@ -292,7 +272,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         tc::mma_commit(&emptyX[xs]);
       }
       tc::mma_commit(tmem_full);
-      trace_stamp(p, 2);
     }
   } else {
     // ---------------- epilogue: warps 2..5, TMEM lane quadrant = warp % 4 ----------
@@ -317,12 +296,9 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     }
     tc::mbar_wait(tmem_full, 0);
     tc::fence_after_sync();
-    if (threadIdx.x == 64) trace_stamp(p, 3);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 
-    if (p.dbg >= 4) {
-      // probe: no epilogue work (4: with MMA + token loads, 5: weight stream only)
-    } else if (p.splits == 1 && p.act == 2) {
+    if (p.splits == 1 && p.act == 2) {
       // gated SiLU, one split (the pipeline smem is idle once tmem_full fired):
       // (1) the up warps (TMEM lanes 64..127) park the whole up half in smem,
       // (2) one barrier, the gate warps form silu(g) * u into a bf16 output
@@ -344,7 +320,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         }
       }
       epi_bar128();
-      if (threadIdx.x == 64) trace_stamp(p, 4);
       // the gate warps read their TMEM half after the barrier (re-loading is
       // cheaper than holding up to 256 columns in registers)
       if (!up) {
@@ -362,7 +337,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         if (p.tma_store) tc::fence_proxy_async_smem();  // O visible to the TMA (async proxy)
       }
       epi_bar128();
-      if (threadIdx.x == 64) trace_stamp(p, 5);
       if (p.tma_store) {
         // one bulk tensor store of the [m_hi x 64] tile (rows past M are
         // clipped by the tensor map): the 16-byte store loop cost ~13 us per
@@ -408,7 +382,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
   }
   __syncwarp();  // producer / MMA roles ran on lane 0: reconverge before the aligned cluster / CTA barriers
   if (p.splits > 1) {
-    if (threadIdx.x == 64) trace_stamp(p, 4);
     pdl_wait();  // warps 0-1 also run the epilogue below (residual reads)
     // split-K reduction across the thread-block cluster through DSMEM: CTA
     // `split` reduces a 1/splits slice of the tile, adding the partials of
@@ -416,7 +389,6 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
     // Gated SiLU: a unit covers gate features f4..f4+3 and their up partners
     // f4+64.. of the same (staged) tile.
     cluster_sync_all();
-    if (threadIdx.x == 64) trace_stamp(p, 5);
     const int m_hi = min(BN, p.M - m0);
     const bool gated = p.act == 2;
     const int upr = (gated ? kBM / 2 : kBM) / 4;  // float4 units per token row
@@ -643,33 +615,30 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
         for (int t = 0; t < 4; ++t) o[t] = f2bf(silu_mul(a4[t], u4[t]));
       }
     }
-    if (threadIdx.x == 64) trace_stamp(p, 9);
     cluster_sync_all();  // peers may still be reading this CTA's smem
   }
-  if (threadIdx.x == 64) trace_stamp(p, 6);
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc<C::TMEM_COLS>(tmem);
   }
-  if (threadIdx.x == 64) trace_stamp(p, 7);
 }
 
 // Launch one linear_kernel<BN> (host).  Ring depths per launch: ~210 KB of
 // stages when the grid fits one CTA per SM, ~104 KB at two per SM, never more
 // stages than k-blocks per CTA (so small drafter GEMMs leave shared memory
 // for concurrent kernels).
-int ring_override(int* sw, int* sx);  // gemm.cu (ms_set_ring, A/B probes)
-
 template <int BN>
 int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to, LinearParams p, int m_tiles,
                   cudaStream_t st, int G) {
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-        cudaSuccess)
+    int sw, sx;
+    C::rings_for(210 * 1024, &sw, &sx);
+    if (cudaFuncSetAttribute(linear_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::smem(sw, sx, true)) != cudaSuccess)
       return MS_ERR_CUDA;
     attr_set = true;
   }
@@ -681,10 +650,8 @@ int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMa
   // the fp32 split-K staging tile may already rule out two CTAs per SM: then
   // take the deep single-CTA rings
   if (part && C::smem(sw, sx, part) > 113 * 1024) C::rings_for(210 * 1024, &sw, &sx);
-  ring_override(&sw, &sx);
   if (sw > kb_per_cta) sw = kb_per_cta < 2 ? 2 : kb_per_cta;
   if (sx > kb_per_cta) sx = kb_per_cta < 2 ? 2 : kb_per_cta;
-  if (C::smem(sw, sx, part) > 227 * 1024) return MS_ERR_UNSUPPORTED;
   p.sw = sw;
   p.sx = sx;
   return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part),

@@ -1,6 +1,9 @@
 """Single-launch device time of the 70B gate/up GEMM (ms_linear act=2) at M
 rows, normal vs probe modes (ms_set_gemm_probe: 4 = no epilogue), each
-launch on a cold weight slice (L2 holds < 1 of the 8 weight copies)."""
+launch on a cold weight slice (L2 holds < 1 of the 8 weight copies).
+(Measurement probe of round 2: the ms_set_gemm_trace / ms_set_gemm_probe /
+ms_set_ring hooks it needs were removed from the product library after the
+measurement — results in profiles/r2_epilogue_trace.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

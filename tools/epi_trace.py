@@ -1,6 +1,9 @@
 """Per-CTA phase timestamps (ms_set_gemm_trace) of one 70B gate/up launch at M
 rows: when CTAs start, finish streaming, finish the MMAs, and how long the
-gated epilogue phases take.  usage: python tools/epi_trace.py [M=112] [N=57344] [K=8192] [act=2]"""
+gated epilogue phases take.  usage: python tools/epi_trace.py [M=112] [N=57344] [K=8192] [act=2]
+(Measurement probe of round 2: the ms_set_gemm_trace / ms_set_gemm_probe /
+ms_set_ring hooks it needs were removed from the product library after the
+measurement — results in profiles/r2_epilogue_trace.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

@@ -1,7 +1,10 @@
 """Where does the verify GEMM's time go?  80-layer graph chains of the 70B
 gate/up and down GEMMs at M rows under ms_set_gemm_probe: 0 full, 1 weight
 stream only (no MMA, no token loads), 2 weight + token loads without MMA,
-3 MMAs without token loads.  usage: python tools/gemm_probe_ab.py [M=112]"""
+3 MMAs without token loads.  usage: python tools/gemm_probe_ab.py [M=112]
+(Measurement probe of round 2: the ms_set_gemm_trace / ms_set_gemm_probe /
+ms_set_ring hooks it needs were removed from the product library after the
+measurement — results in profiles/r2_epilogue_trace.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

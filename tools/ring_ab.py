@@ -1,7 +1,10 @@
 """A/B of ms_linear's TMA ring depths (ms_set_ring) on 80-layer graph chains
 of the 70B verify GEMMs at M rows: weight stages sw x token stages sx; two
 CTAs per SM need smem <= ~113 KB (sw*16 KB + sx*BN*128 B), one CTA per SM
-<= 227 KB.  usage: python tools/ring_ab.py [M=112] ["sw:sx,..."]"""
+<= 227 KB.  usage: python tools/ring_ab.py [M=112] ["sw:sx,..."]
+(Measurement probe of round 2: the ms_set_gemm_trace / ms_set_gemm_probe /
+ms_set_ring hooks it needs were removed from the product library after the
+measurement — results in profiles/r2_epilogue_trace.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

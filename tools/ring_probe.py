@@ -1,7 +1,10 @@
 """Weight-stream rate of the gate/up GEMM vs ring depth, with the MMA and token
 loads switched off (ms_set_gemm_probe(1)) or on (0): 80-layer graph chains at
 M rows with ring overrides sw:sx (ms_set_ring).
-usage: python tools/ring_probe.py M "sw:sx,..." [probe=1]"""
+usage: python tools/ring_probe.py M "sw:sx,..." [probe=1]
+(Measurement probe of round 2: the ms_set_gemm_trace / ms_set_gemm_probe /
+ms_set_ring hooks it needs were removed from the product library after the
+measurement — results in profiles/r2_epilogue_trace.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
