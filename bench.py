@@ -14,8 +14,11 @@ never agree with the target, drafts use fidelity injection
 replaced by the target's greedy continuation — every kernel still runs in
 full and the output stays exactly the target's greedy decode.
 
-One step = one generation batch: decode of 16 requests x 128 new tokens, from
-prefilled KV caches (prompt prefill is outside the hot path) to
+One step = one generation batch: decode of 16 requests x 128 new tokens (x2
+groups pipelined), from prefilled KV caches, the speculation-length selector and
+the drafter weights starting from the config (--controllers fresh, default: the
+reference engine's per-run semantics; warm = they persist across steps, both
+reported) (prompt prefill is outside the hot path) to
 the last request finishing.  `value` = generated tokens / device time of the
 decode (CUDA events, weights 137 GB >> L2 so no flush is needed).  `e2e` =
 the same metric through the public API (SpecEngine.run) from host prompt
@@ -90,7 +93,9 @@ def bench_config(args, ws: int, tp: bool) -> dict:
             "parallelism": (f"tp{ws}" if tp else "replicas") if ws > 1 else "single-gpu",
             "l2": (f"inputs larger than L2 ({2 * tcfg.matmul_params() / 1e9:.1f} GB of weights "
                    "streamed per verify)"),
-            "controllers": "selector + drafter weights persist across batches (adapted in warm-up)",
+            "controllers": ("selector + drafter weights reset to the config at every step (as the reference "
+                            "engine starts each run, aggspec/engine.py:209-210)" if args.controllers == "fresh" else
+                            "selector + drafter weights persist across batches (adapted in warm-up)"),
             "kv_cache": f"paged, {args.kv_block_size}-token blocks" if args.kv_block_size else "contiguous",
             "sm_partition": (f"drafters on a {args.draft_sms}-SM green context, verifier on the rest"
                              if args.draft_sms and args.schedule == "pipelined" else "shared")}
@@ -121,6 +126,9 @@ def parse():
     ap.add_argument("--ref-new-tokens", type=int, default=0,
                     help="reference arm / cpu_baseline sample: new tokens per request per step "
                          "(0: 4, cfg1: all)")
+    ap.add_argument("--controllers", default="fresh", choices=["fresh", "warm"],
+                    help="fresh: the selector and drafter weights restart from the config every step (the reference "
+                         "engine's per-run semantics); warm: they persist across steps")
     ap.add_argument("--fresh-steps", type=int, default=-1,
                     help="extra timed steps with the selector and drafter weights reset per step "
                          "(the reference's per-run semantics); -1 = min(steps, 3), 0 = skip")
@@ -351,7 +359,7 @@ def run_ours(args, rank, ws):
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         n0 = eng.kernel_launches
         e0.record()
-        res = eng.decode()
+        res = eng.decode(reset_controllers=args.controllers == "fresh")
         e1.record()
         torch.cuda.synchronize()
         return res, e0.elapsed_time(e1) * 1e-3, eng.kernel_launches - n0
@@ -395,7 +403,7 @@ def run_ours(args, rank, ws):
         if teacher is not None:
             eng.set_teacher(teacher)
             eng.h2d_bytes += eng.teacher.numel() * 4
-        res = eng.decode()
+        res = eng.decode(reset_controllers=args.controllers == "fresh")
         e2e_tokens += res.tokens
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(time.perf_counter() - t0, ws)
@@ -404,8 +412,10 @@ def run_ours(args, rank, ws):
            "d2h_bytes_per_step": int((eng.d2h_bytes - d0) / args.steps),
            "includes": "prompt H2D + prefill + decode + per-round H2D/D2H"}
 
-    # ---- fresh controllers: selector + drafter weights reset every step (the
-    # reference starts both from the config per run, aggspec/engine.py:209-210)
+    # ---- the other controller mode beside the headline one (fresh: selector
+    # + drafter weights reset every step, as the reference starts both from the
+    # config per run, aggspec/engine.py:209-210; warm: they persist)
+    other = "warm" if args.controllers == "fresh" else "fresh"
     n_fresh = min(args.steps, 3) if args.fresh_steps < 0 else args.fresh_steps
     fresh_out = None
     if n_fresh > 0:
@@ -419,7 +429,7 @@ def run_ours(args, rank, ws):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record()
-            res = eng.decode(reset_controllers=True)
+            res = eng.decode(reset_controllers=other == "fresh")
             e1.record()
             torch.cuda.synchronize()
             f_t += e0.elapsed_time(e1) * 1e-3
@@ -428,7 +438,8 @@ def run_ours(args, rank, ws):
         f_t = max_over_ranks(f_t, ws)
         fresh_out = {"value": round(f_tok * (1 if tp else ws) / f_t, 2), "unit": "tokens/s", "steps": n_fresh,
                      "mean_accepted_length": round(float(np.mean(f_acc)), 4) if f_acc else 0.0,
-                     "note": "selector and drafter weights reset to the config at every step"}
+                     "note": ("selector and drafter weights reset to the config at every step" if other == "fresh"
+                              else "selector and drafter weights persist across steps")}
 
     peaks = {}
     try:
@@ -453,7 +464,7 @@ def run_ours(args, rank, ws):
         "round_ms_mean": round(float(np.mean([rd.t_round_ms for rd in rounds])), 3),
         "roofline": roofline_verify(eng, rounds, peaks),
         "e2e": e2e,
-        "fresh_controllers": fresh_out,
+        f"{other}_controllers": fresh_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "libminions": _native.LIB_PATH,

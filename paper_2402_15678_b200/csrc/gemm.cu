@@ -45,21 +45,6 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t co
   return r == CUDA_SUCCESS;
 }
 
-// 2-D bf16 row-major [rows, cols] output, box = [64 cols, box_rows], no
-// swizzle (the source tile in shared memory is plain row-major)
-static bool make_tmap_store(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // Split count for the weight-streaming regime, a function of (N, K) only.
 // From the measured sweep (tools/probe_gemm_graph.py, OPT-13B / OPT-125M
 // shapes at M = 16 and 80): about 260 CTAs (~1.75 per SM) is best — fewer
@@ -81,12 +66,12 @@ static int pick_bn(int M) {
   return M <= 16 ? 16 : (M + 15) / 16 * 16;
 }
 
-static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to,
-                     const LinearParams& p, int m_tiles, cudaStream_t st, int G) {
+static int launch_bn(int bn, const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int m_tiles,
+                     cudaStream_t st, int G) {
   switch (bn) {
 #define MS_CASE(BN) \
   case BN:          \
-    return launch_linear<BN>(tw, tx, to, p, m_tiles, st, G);
+    return launch_linear<BN>(tw, tx, p, m_tiles, st, G);
     MS_LINEAR_WIDTHS(MS_CASE)
 #undef MS_CASE
     default:
@@ -196,18 +181,9 @@ static int linear_impl(const void* x, int64_t ldx, const void* w, const void* bi
       !out_f32 && !rms.out) {
     // more one-split gated tiles than two-per-SM slots (the 70B gate/up):
     // persistent CTAs with double-buffered TMEM, bitwise the same outputs
-    p.tma_store = 0;
     return launch_gated_bn(bn, tw, tx, p, m_tiles, slots, (cudaStream_t)stream);
   }
-  // gated one-split GEMMs store their output tiles with TMA (gemm_kernel.cuh)
-  CUtensorMap to;
-  memset(&to, 0, sizeof(to));
-  p.tma_store = 0;
-  if (splits == 1 && act == 2 && G == 1 && !rms.tp_recv && !out_f32 && ldc % 8 == 0) {
-    if (!make_tmap_store(&to, out, M, N / 2, ldc, bn)) return MS_ERR_CUDA;
-    p.tma_store = 1;
-  }
-  return launch_bn(bn, tw, tx, to, p, m_tiles, (cudaStream_t)stream, G);
+  return launch_bn(bn, tw, tx, p, m_tiles, (cudaStream_t)stream, G);
 }
 
 extern "C" int ms_linear(const void* x, int64_t ldx, const void* w, const void* bias, const void* residual,

@@ -53,7 +53,6 @@ struct LinearParams {
   int kb_total;                   // K / 64 (rounded up)
   int n_tiles;
   int sw, sx;                     // weight / token ring depths of this launch
-  int tma_store;                  // gated one-split epilogue: the output tile leaves smem by one TMA store (tmO)
   // tensor-parallel reduce-scatter fused into the epilogue: the fp32 value of
   // output (row m, feature f) is stored straight into the receive slot of the
   // rank owning f's column slice: tp_recv[f / tp_slice][(tp_rank * tp_rows +
@@ -104,9 +103,8 @@ struct LinearCfg {
   // the fp32 partial tile is staged in the (idle) ring smem only for the
   // split-K cluster reduction; the single-split gated epilogue exchanges
   // gate/up through smem as well
-  // up half [BN][65] fp32, then the bf16 output tile [BN][64] at a 1024-byte
-  // aligned offset (the source of a TMA store)
-  static constexpr int O_OFF = (BN * 65 * 4 + 1023) / 1024 * 1024;
+  // up half [BN][65] fp32, then the bf16 output tile [BN][64]
+  static constexpr int O_OFF = BN * 65 * 4;
   static constexpr int GATED_EPI_BYTES = O_OFF + BN * 64 * 2;
   __host__ __device__ static int data_bytes(int sw, int sx, bool part) {
     const int pipe = sw * W_BYTES + sx * X_BYTES;
@@ -168,7 +166,7 @@ template <int BN>
 // (tools/ab_lib_gemm.py, round 2)
 __global__ void __launch_bounds__(kThreads, 2)
 linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-              const __grid_constant__ CUtensorMap tmO, const LinearParams p) {
+              const LinearParams p) {
   using C = LinearCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -334,26 +332,14 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
               O[(c0 + j) * 64 + f] = f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f),
                                                    U[(c0 + j) * 65 + f]));
         }
-        if (p.tma_store) tc::fence_proxy_async_smem();  // O visible to the TMA (async proxy)
       }
       epi_bar128();
-      if (p.tma_store) {
-        // one bulk tensor store of the [m_hi x 64] tile (rows past M are
-        // clipped by the tensor map): the 16-byte store loop cost ~13 us per
-        // CTA at M = 112 beside the co-resident CTA's weight stream
-        if (threadIdx.x == 64) {
-          tc::tma_store_2d(&tmO, O, tile_n * (kBM / 2), orow);
-          tc::bulk_commit_group();
-          tc::bulk_wait_group_read0();  // smem may be released once the TMA has read it
-        }
-      } else {
-        const int et = threadIdx.x - 64;  // 0..127
-        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
-        for (int e = et; e < m_hi * 8; e += 128) {
-          const int row = e >> 3, ch = e & 7;
-          *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
-              *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
-        }
+      const int et = threadIdx.x - 64;  // 0..127
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)orow * p.ldc + tile_n * (kBM / 2);
+      for (int e = et; e < m_hi * 8; e += 128) {
+        const int row = e >> 3, ch = e & 7;
+        *reinterpret_cast<uint4*>(ob + (int64_t)row * p.ldc + ch * 8) =
+            *reinterpret_cast<const uint4*>(O + row * 64 + ch * 8);
       }
     } else if (p.splits == 1) {
       for (int c0 = 0; c0 < m_hi; c0 += 16) {
@@ -630,8 +616,8 @@ linear_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ C
 // stages than k-blocks per CTA (so small drafter GEMMs leave shared memory
 // for concurrent kernels).
 template <int BN>
-int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& to, LinearParams p, int m_tiles,
-                  cudaStream_t st, int G) {
+int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, LinearParams p, int m_tiles, cudaStream_t st,
+                  int G) {
   using C = LinearCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -655,7 +641,7 @@ int launch_linear(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMa
   p.sw = sw;
   p.sx = sx;
   return launch(linear_kernel<BN>, dim3(p.n_tiles * p.splits, m_tiles, G), dim3(kThreads), C::smem(sw, sx, part),
-                st, p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, to, p);
+                st, p.splits /* the split-K CTAs of a tile form one cluster */, tw, tx, p);
 }
 
 template <int BN>
@@ -667,12 +653,12 @@ int preload_linear() {
 #define MS_LINEAR_WIDTHS(X) X(16) X(32) X(48) X(64) X(80) X(96) X(112) X(128) X(144) X(160) X(176) X(192) \
   X(208) X(224) X(240) X(256)
 #define MS_LINEAR_DECLARE(BN)                                                                         \
-  extern template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,    \
-                                        LinearParams, int, cudaStream_t, int);                          \
+  extern template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, LinearParams, int,      \
+                                        cudaStream_t, int);                                             \
   extern template int preload_linear<BN>();
 #define MS_LINEAR_INSTANTIATE(BN)                                                                     \
-  template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, LinearParams, int, \
-                                 cudaStream_t, int);                                                    \
+  template int launch_linear<BN>(const CUtensorMap&, const CUtensorMap&, LinearParams, int, cudaStream_t, \
+                                 int);                                                                  \
   template int preload_linear<BN>();
 
 }  // namespace ms

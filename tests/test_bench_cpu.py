@@ -66,7 +66,7 @@ def test_reference_arm_is_the_reference_engine_without_libminions():
     assert line["lossless_vs_greedy"] is True
     args = types.SimpleNamespace(target="tiny-target", ssm="tiny-ssm", fidelity="", batch=4, schedule="sequential",
                                  prompt_len=8, new_tokens=64, fixed_s=4, kv_block_size=0, preset="cfg1",
-                                 draft_sms=0)
+                                 draft_sms=0, controllers="fresh")
     assert line["config"] == bench.bench_config(args, 1, False)
 
 
