@@ -265,7 +265,7 @@ class SpecEngine:
         they wait for their predecessor — slots the concurrent verify could
         use).
         draft_coresident (default: on for grouped Llama drafters in the
-        pipelined schedule): the drafters' decode
+        pipelined schedule with caches <= 1,024 positions): the drafters' decode
         steps run in co-resident launch shapes (ms_set_coresident: 64-thread
         gemv / decode-attention CTAs, the LM head on gemv) that fit on an SM
         beside two verify-GEMM CTAs.
@@ -357,7 +357,12 @@ class SpecEngine:
             raise ValueError("stream_priority must be 'equal', 'verify' or 'draft'")
         hi = lambda k: -1 if stream_priority == k else 0  # noqa: E731
         self.draft_pdl = bool(draft_pdl)
-        self.draft_coresident = bool((pipelined and self.grouped) if draft_coresident is None else draft_coresident)
+        # co-resident drafter shapes by default only for short caches: their
+        # one-warp-per-(request, head) decode attention streams ~1.9 TB/s, fine
+        # beside the verifier at a few hundred keys but the critical path of a
+        # draft-bound 4K-context round (cfg5: attention 307 vs 111 us per layer)
+        self.draft_coresident = bool((pipelined and self.grouped and max_len <= 1024)
+                                     if draft_coresident is None else draft_coresident)
         self.draft_sms = self.verify_sms = 0
         if draft_sms > 0:
             if not pipelined:

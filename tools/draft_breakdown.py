@@ -1,7 +1,7 @@
 """Warm per-op timing of the grouped drafter decode step (3 x Llama-160M, 16
 requests each, one position, ctx keys): each op kind as a 12-layer chain
 captured in a CUDA graph (PDL on), µs per layer, and the op's algorithmic
-bytes / time.  usage: python tools/draft_breakdown.py [ctx=200] [B=16] [G=3]"""
+bytes / time.  usage: python tools/draft_breakdown.py [ctx=200] [B=16] [G=3] [co]"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,6 +10,7 @@ from paper_2402_15678_b200.llama import GroupedLlamaModel
 from paper_2402_15678_b200.weights import CONFIGS, KVCache, LlamaWeights
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+CO = len(sys.argv) > 4 and sys.argv[4] == "co"  # the co-resident launch shapes (ms_set_coresident)
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 G = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 c = CONFIGS["llama-160m"]
@@ -45,6 +46,8 @@ ops = {
     "down": (lambda i: lin(ff, f"l{i}.w_down", residual=x, out=x), 2 * G * c.d * c.ffn),
 }
 out = {}
+if CO:
+    _native.lib.ms_set_coresident(1)
 for nm, (fn, byt) in ops.items():
     def chain():
         for i in range(L):

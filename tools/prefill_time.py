@@ -17,13 +17,13 @@ slot = torch.arange(B, dtype=torch.int32, device="cuda")
 empty = torch.zeros(0, dtype=torch.int32, device="cuda")
 dummy = torch.empty(0, c.vocab, device="cuda")
 for _ in range(2):
-    m.forward(tok, st, slot, cache, dummy, head_rows=empty)
+    m.forward(tok, st, slot, cache, dummy, head_rows=empty, prefill=True)
 torch.cuda.synchronize()
 ts = []
 for _ in range(3):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    m.forward(tok, st, slot, cache, dummy, head_rows=empty)
+    m.forward(tok, st, slot, cache, dummy, head_rows=empty, prefill=True)
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
