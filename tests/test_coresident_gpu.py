@@ -111,3 +111,21 @@ def test_pipelined_grouped_drafters_coresident_lossless():
     res = eng.decode()
     assert res.outputs == teacher
     assert res.mean_accepted > 1.0
+
+
+def test_coresident_default_policy():
+    """On by default for grouped drafters in the pipelined schedule with short
+    caches only (the one-warp decode attention is slow at 4K contexts)."""
+    from paper_2402_15678_b200.core import EngineConfig
+    from paper_2402_15678_b200.engine import SpecEngine
+    from paper_2402_15678_b200.llama import CONFIGS, LlamaWeights
+    tcfg, scfg = CONFIGS["tiny-llama"], CONFIGS["tiny-llama-ssm"]
+    target = LlamaWeights.random(tcfg, 0, device="cuda", std=0.05)
+    drafters = [LlamaWeights.random(scfg, k + 1, device="cuda", std=0.05) for k in range(3)]
+    cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=2, b_ssm=2, s_init=4, initial_weights=(1.0,) * 3)
+    short = SpecEngine(target, drafters, cfg, slots=4, max_len=200, pipelined=True)
+    long_ = SpecEngine(target, drafters, cfg, slots=4, max_len=1000 + 24, pipelined=True)
+    seq = SpecEngine(target, drafters, cfg, slots=4, max_len=200)
+    forced = SpecEngine(target, drafters, cfg, slots=4, max_len=1000 + 24, pipelined=True, draft_coresident=True)
+    assert short.draft_coresident and not long_.draft_coresident and not seq.draft_coresident
+    assert forced.draft_coresident
