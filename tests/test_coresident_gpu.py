@@ -124,8 +124,8 @@ def test_coresident_default_policy():
     drafters = [LlamaWeights.random(scfg, k + 1, device="cuda", std=0.05) for k in range(3)]
     cfg = EngineConfig(vocab_size=tcfg.vocab, b_llm=2, b_ssm=2, s_init=4, initial_weights=(1.0,) * 3)
     short = SpecEngine(target, drafters, cfg, slots=4, max_len=200, pipelined=True)
-    long_ = SpecEngine(target, drafters, cfg, slots=4, max_len=1000 + 24, pipelined=True)
+    long_ = SpecEngine(target, drafters, cfg, slots=4, max_len=1100, pipelined=True)
     seq = SpecEngine(target, drafters, cfg, slots=4, max_len=200)
-    forced = SpecEngine(target, drafters, cfg, slots=4, max_len=1000 + 24, pipelined=True, draft_coresident=True)
+    forced = SpecEngine(target, drafters, cfg, slots=4, max_len=1100, pipelined=True, draft_coresident=True)
     assert short.draft_coresident and not long_.draft_coresident and not seq.draft_coresident
     assert forced.draft_coresident
