@@ -417,6 +417,16 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
                      const int32_t* slot, const int32_t* start, int T, float* k_cache, float* v_cache,
                      const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
 
+/* Grouped-query attention of Q <= 16 query positions per request on tcgen05
+ * (head dim 128, Q * H / Hkv <= 128 flattened rows; contiguous cache of n_slots
+ * slots [n_slots, Hkv, T, 128]): K / V read by TMA in 128-key chunks, S = Q K^T
+ * and O += P V on tcgen05 with TMEM accumulators, online softmax per row,
+ * K/V append fused (append != 0).  Same contract as ms_attention_gqa for
+ * those shapes (csrc/attention_tc.cu). */
+int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D, const int32_t* slot,
+                    const int32_t* start, int T, int n_slots, void* k_cache, void* v_cache, const void* rope,
+                    float scale, int append, void* out, int64_t ldo, void* stream);
+
 /* Programmatic dependent launch (PDL) attribute for subsequent launches of
  * this process (default on; MS_PDL=0 in the environment turns it off); a
  * captured CUDA graph keeps the setting it was captured with.  Returns the

@@ -36,6 +36,7 @@ int preload_gemm();
 int preload_wide();
 int preload_tp();
 int preload_fp32();
+int preload_attention_tc();
 int set_coresident(int on);
 }  // namespace ms
 
@@ -44,7 +45,8 @@ extern "C" int ms_version(void) { return 200; }
 extern "C" int ms_preload(void) {
   const int bad = ms::preload_accept() + ms::preload_accept_stochastic() + ms::preload_vote() +
                   ms::preload_spec() + ms::preload_model() + ms::preload_attention() + ms::preload_gemv() +
-                  ms::preload_gemm() + ms::preload_wide() + ms::preload_tp() + ms::preload_fp32();
+                  ms::preload_gemm() + ms::preload_wide() + ms::preload_tp() + ms::preload_fp32() +
+                  ms::preload_attention_tc();
   return bad ? MS_ERR_CUDA : MS_OK;
 }
 

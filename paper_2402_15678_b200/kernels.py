@@ -210,6 +210,11 @@ class AttnWorkspace:
         self.counters = torch.zeros(c.value, dtype=torch.int32, device=device)
 
 
+# grouped-query decode / verify attention (head dim 128, <= 16 positions) on
+# the tcgen05 kernel (csrc/attention_tc.cu) instead of the warp-MMA row kernel
+TC_ATTENTION = False
+
+
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
               out: torch.Tensor | None = None, append: bool = True, ws: AttnWorkspace | None = None,
@@ -228,6 +233,13 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
     if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < T or rope.shape[1] * 2 != D):
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
+    if (TC_ATTENTION and Hkv < H and D == 128 and page is None and ws is None and Q <= 16
+            and Q * (H // Hkv) <= 128 and k_cache.is_contiguous() and v_cache.is_contiguous()):
+        _native.call("ms_attention_tc", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
+                     _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, k_cache.shape[0],
+                     _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), None if rope is None else rope.data_ptr(),
+                     scale, int(append), out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
+        return out
     _native.call("ms_attention_paged", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,
                  _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16),
