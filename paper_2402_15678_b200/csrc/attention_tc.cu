@@ -9,13 +9,16 @@
 //   * S = Q K^T on tcgen05 (M = 128 flattened rows — position i, group head j
 //     -> row i * G + j, Q staged RoPE-rotated into a swizzled K-major tile —,
 //     N = 128 keys, K = 128 dims), fp32 accumulator in TMEM;
-//   * four warps own one TMEM lane = one row each: causal mask, online softmax
+//   * two key groups (warpgroups) take alternate chunks concurrently, each
+//     with its own S / O accumulators in TMEM, P tile and softmax state; in a
+//     group four warps own one TMEM lane = one row each: causal mask, online softmax
 //     in the exp2 domain (running max / sum per row, the O accumulator in TMEM
 //     rescaled in place when the max moves), P written back as bf16 into a
 //     swizzled K-major tile;
 //   * O += P V on tcgen05 with V as the MN-major operand (keys along K, dims
 //     along N, straight from the TMA tile);
-//   * the epilogue reads O from TMEM, divides by the row sum and stores bf16.
+//   * the epilogue merges the two groups' (m, l, O) in group order through
+//     shared memory, divides by the row sum and stores bf16.
 //
 // Every row's arithmetic depends only on its own query and the keys it sees
 // (chunking fixed by key position, fixed per-row reduction orders): the
@@ -37,17 +40,18 @@ namespace atc {
 constexpr int kD = 128;       // head dim
 constexpr int kRows = 128;    // MMA M: flattened (position, group head) rows
 constexpr int kKeys = 128;    // keys per chunk (MMA N of S, K of P.V)
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;  // two key groups (warpgroups) of 4 warps
 constexpr int BLK = kRows * 64 * 2;  // one [128 x 64] bf16 swizzled block = 16 KB
 
 struct Smem {
-  // all tiles 1024-byte aligned (128-byte swizzle atoms)
+  // all tiles 1024-byte aligned (128-byte swizzle atoms); buffer / tile g
+  // belongs to key group g (chunks ch with ch % 2 == g)
   static constexpr int Q_OFF = 0;                     // Q [128 rows x 128 dims] = 2 blocks
-  static constexpr int K_OFF = Q_OFF + 2 * BLK;       // K [2 bufs][128 keys x 128 dims]
-  static constexpr int V_OFF = K_OFF + 4 * BLK;       // V [2 bufs][128 keys x 128 dims]
-  static constexpr int P_OFF = V_OFF + 4 * BLK;       // P [128 rows x 128 keys]
-  static constexpr int BAR_OFF = P_OFF + 2 * BLK;
-  static constexpr int BYTES = BAR_OFF + 64 + 1024;   // + alignment slack
+  static constexpr int K_OFF = Q_OFF + 2 * BLK;       // K [2 groups][128 keys x 128 dims]
+  static constexpr int V_OFF = K_OFF + 4 * BLK;       // V [2 groups][128 keys x 128 dims]
+  static constexpr int P_OFF = V_OFF + 4 * BLK;       // P [2 groups][128 rows x 128 keys]
+  static constexpr int BAR_OFF = P_OFF + 4 * BLK;
+  static constexpr int BYTES = BAR_OFF + 64 + 1024 + 1024;  // barriers, group 1 (m, l) per row, alignment slack
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -109,13 +113,17 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   uint8_t* sK = sm + Smem::K_OFF;
   uint8_t* sV = sm + Smem::V_OFF;
   uint8_t* sP = sm + Smem::P_OFF;
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2]
-  uint64_t* s_full = kv_full + 2;
-  uint64_t* pv_done = s_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2 groups]
+  uint64_t* s_full = kv_full + 2;                                       // [2]
+  uint64_t* pv_done = s_full + 2;                                       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  float* stat = reinterpret_cast<float*>(tmem_slot + 4);                // [128 rows][2]: group 1's (m, l)
 
   const int b = blockIdx.x, h = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int g = warp >> 2;          // key group
+  const int gt = tid & 127;         // thread within the group = row (TMEM lane)
+  const bool issuer = gt == 0;      // the group's TMA / MMA thread
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
   const int QD = Hq * kD, KVD = Hkv * kD;
@@ -124,19 +132,23 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   if (tid == 0) {
     tc::prefetch_tmap(&tmK);
     tc::prefetch_tmap(&tmV);
-    tc::mbar_init(&kv_full[0], 1);
-    tc::mbar_init(&kv_full[1], 1);
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&pv_done[i], 1);
+    }
     tc::fence_barrier_init();
   }
   __syncwarp();
-  if (warp == 0) tc::tmem_alloc<256>(tmem_slot);  // S: columns 0..127, O: 128..255
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);  // S0 | S1 | O0 | O1, 128 columns each
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t tS = tmem + g * 128, tO = tmem + 256 + g * 128;
+  uint8_t* gK = sK + 2 * g * BLK;
+  uint8_t* gV = sV + 2 * g * BLK;
+  uint8_t* gP = sP + 2 * g * BLK;
 
   // the cache rows of earlier calls (keys < pstart) do not depend on the
   // previous kernel: chunks made only of them are requested before the
@@ -147,7 +159,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // cache row of key 0
   const int n_keys = min(pstart + Qtot, T);
   const int n_chunks = (n_keys + kKeys - 1) / kKeys;
-  auto load_chunk = [&](int ch) {  // thread 0
+  auto load_chunk = [&](int ch) {  // the issuer of group ch % 2
     const int buf = ch & 1;
     tc::mbar_arrive_expect_tx(&kv_full[buf], 4 * BLK);
     const int y = (int)(row0 + ch * kKeys);
@@ -157,9 +169,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       tc::tma_load_2d(sV + (2 * buf + half) * BLK, &tmV, &kv_full[buf], half * 64, y, pol);
     }
   };
-  const int early = min(min(n_chunks, 2), pstart / kKeys);  // leading chunks entirely below pstart
-  if (tid == 0)
-    for (int ch = 0; ch < early; ++ch) load_chunk(ch);
+  const bool early = g < n_chunks && (g + 1) * kKeys <= pstart;  // this group's first chunk is all cache
+  if (issuer && early) load_chunk(g);
   pdl_wait();
   pdl_trigger();
 
@@ -209,37 +220,36 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   tc::fence_proxy_async_smem();
   __syncthreads();
 
-
   constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
   constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
-  auto issue_S = [&](int ch) {  // thread 0: S = Q K_ch^T
-    const int buf = ch & 1;
-    MBW(&kv_full[buf], (ch >> 1) & 1, 1);
+  auto issue_S = [&](int ch) {  // the group's issuer: S = Q K_ch^T
+    MBW(&kv_full[g], (ch >> 1) & 1, 1);
     tc::fence_after_sync();
 #pragma unroll
     for (int k = 0; k < kD / 16; ++k) {
       const uint64_t ad = tc::smem_desc_sw128(sQ + (k >> 2) * BLK) + 2 * (k & 3);
-      const uint64_t bd = tc::smem_desc_sw128(sK + (2 * buf + (k >> 2)) * BLK) + 2 * (k & 3);
+      const uint64_t bd = tc::smem_desc_sw128(gK + (k >> 2) * BLK) + 2 * (k & 3);
       tc::mma_bf16(tS, ad, bd, idS, k > 0 ? 1u : 0u);
     }
-    tc::mma_commit(s_full);
+    tc::mma_commit(&s_full[g]);
   };
-  if (tid == 0) {
-    for (int ch = early; ch < min(n_chunks, 2); ++ch) load_chunk(ch);
-    issue_S(0);
+  if (issuer && g < n_chunks) {
+    if (!early) load_chunk(g);
+    issue_S(g);
   }
-  __syncwarp();  // lane 0 of warp 0 diverged: reconverge before the aligned tcgen05.ld
+  __syncwarp();  // the issuer lane diverged: reconverge before the aligned tcgen05.ld
 
-  // softmax state of this thread's row (= TMEM lane tid)
-  const int r = tid;
+  // softmax state of this thread's row (= TMEM lane gt) over its group's chunks
+  const int r = gt;
   const int row_pos = r < rows_tot ? pstart + r / G : -1;  // last key this row may see
   float m_run = -INFINITY, l_run = 0.f;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    MBW(s_full, ch & 1, 2);
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+  int it = 0;  // this group's chunk count so far
+  for (int ch = g; ch < n_chunks; ch += 2, ++it) {
+    MBW(&s_full[g], it & 1, 2);
     tc::fence_after_sync();
     const int kbase = ch * kKeys;
-    // pass 1: masked max of this chunk (16 columns per TMEM load)
+    // pass 1: masked max of this chunk
     float mx = -INFINITY;
 #pragma unroll 1
     for (int c0 = 0; c0 < kKeys; c0 += 32) {
@@ -255,9 +265,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     }
     const float m_new = fmaxf(m_run, mx);
     const float corr = m_run == -INFINITY ? 0.f : (m_new == m_run ? 1.f : exp2f(m_run - m_new));
-    // the previous chunk's P.V must be done before O is rescaled and P rewritten
-    if (ch > 0) {
-      MBW(pv_done, (ch - 1) & 1, 3);
+    // the group's previous P.V must be done before O is rescaled and P rewritten
+    if (it > 0) {
+      MBW(&pv_done[g], (it - 1) & 1, 3);
       tc::fence_after_sync();
       if (__any_sync(0xffffffffu, corr != 1.f)) {  // warp-uniform: the TMEM ops are warp-collective
 #pragma unroll 1
@@ -274,7 +284,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         tmem_wait_st();
       }
     }
-    // pass 2: P = exp2(s - m_new) (masked -> 0), row sum, P -> swizzled tile
+    // pass 2: P = exp2(s - m_new) (masked -> 0), row sum, P -> the group's swizzled tile
     float psum = 0.f;
 #pragma unroll 1
     for (int c0 = 0; c0 < kKeys; c0 += 32) {
@@ -293,54 +303,76 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
           psum += pv[j];
         }
         const int c = (c0 >> 3) + q4;  // 16-byte chunk (8 keys) within the 128 keys
-        *reinterpret_cast<bf16x8*>(sP + (c >> 3) * BLK + swz(r, c & 7)) = pack8(pv);
+        *reinterpret_cast<bf16x8*>(gP + (c >> 3) * BLK + swz(r, c & 7)) = pack8(pv);
       }
     }
     l_run = l_run * corr + psum;
     m_run = m_new;
     tc::fence_proxy_async_smem();  // P visible to the MMA (async proxy)
     tc::fence_before_sync();       // S reads and O stores ordered before the next MMAs
-    __syncthreads();
-    if (tid == 0) {
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the group's 4 warps
+    if (issuer) {
       tc::fence_after_sync();
-      const int buf = ch & 1;
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
-        const uint64_t ad = tc::smem_desc_sw128(sP + (k >> 2) * BLK) + 2 * (k & 3);
+        const uint64_t ad = tc::smem_desc_sw128(gP + (k >> 2) * BLK) + 2 * (k & 3);
         // V rows 16k..16k+15 (2048 bytes per 16 keys), the two 64-dim boxes BLK apart
-        const uint64_t bd = desc_mn_sw128(sV + (2 * buf) * BLK + k * 2048, BLK);
-        tc::mma_bf16(tO, ad, bd, idPV, (ch > 0 || k > 0) ? 1u : 0u);
+        const uint64_t bd = desc_mn_sw128(gV + k * 2048, BLK);
+        tc::mma_bf16(tO, ad, bd, idPV, (it > 0 || k > 0) ? 1u : 0u);
       }
-      tc::mma_commit(pv_done);
-      if (ch + 1 < n_chunks) {
-        issue_S(ch + 1);  // S is free: every row read it before the barrier
-        // K/V buffer `buf` is free once this P.V completes: refill it with chunk ch + 2
-        if (ch + 2 < n_chunks) {
-          MBW(pv_done, ch & 1, 4);
-          load_chunk(ch + 2);
-        }
+      tc::mma_commit(&pv_done[g]);
+      if (ch + 2 < n_chunks) {
+        // the group's K/V buffer is free once this P.V completes
+        MBW(&pv_done[g], it & 1, 4);
+        load_chunk(ch + 2);
+        issue_S(ch + 2);
       }
     }
     __syncwarp();
   }
-  // epilogue: O / l -> bf16
-  MBW(pv_done, (n_chunks - 1) & 1, 5);
-  tc::fence_after_sync();
-  const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-  __nv_bfloat16* op = out + (int64_t)(b * Qtot + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * kD;
+  // epilogue: group 1 hands its row statistics (m, l) to group 0 through shared
+  // memory; group 0 reads both groups' O rows from TMEM (its warps own the same
+  // TMEM lanes), merges them in group order, divides and stores
+  const int nit = it;
+  if (nit > 0) {
+    MBW(&pv_done[g], (nit - 1) & 1, 5);
+    tc::fence_after_sync();
+  }
+  if (g == 1) {
+    stat[2 * r] = nit > 0 ? m_run : -INFINITY;
+    stat[2 * r + 1] = nit > 0 ? l_run : 0.f;
+  }
+  tc::fence_before_sync();
+  __syncthreads();  // every P.V of both groups is complete
+  if (g == 0) {
+    tc::fence_after_sync();
+    const float m1 = stat[2 * r], l1 = stat[2 * r + 1];
+    const bool has1 = n_chunks > 1;  // group 1 wrote O1
+    const float m = fmaxf(m_run, m1);
+    const float a0 = m_run == -INFINITY ? 0.f : exp2f(m_run - m);
+    const float a1 = (!has1 || m1 == -INFINITY) ? 0.f : exp2f(m1 - m);
+    const float L = l_run * a0 + l1 * a1;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const uint32_t tO1 = tmem + 384;
+    __nv_bfloat16* op = out + (int64_t)(b * Qtot + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * kD;
 #pragma unroll 1
-  for (int c0 = 0; c0 < kD; c0 += 32) {
-    uint32_t ov[32];
-    tc::tmem_ld16(tO + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(ov));
-    tc::tmem_ld16(tO + lane_base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(ov + 16));
-    tc::tmem_wait_ld();
-    if (r < rows_tot) {
+    for (int c0 = 0; c0 < kD; c0 += 16) {
+      uint32_t o0[16], o1[16];
+      tc::tmem_ld16(tO + lane_base + c0, o0);
+      tc::tmem_ld16(tO1 + lane_base + c0, o1);
+      tc::tmem_wait_ld();
+      if (r < rows_tot) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float f[8];
+        for (int c = 0; c < 2; ++c) {
+          float f[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(ov[c * 8 + j]) * inv;
-        *reinterpret_cast<bf16x8*>(op + c0 + c * 8) = pack8(f);
+          for (int j = 0; j < 8; ++j) {
+            const float x0 = nit > 0 ? __uint_as_float(o0[c * 8 + j]) : 0.f;
+            const float x1 = has1 ? __uint_as_float(o1[c * 8 + j]) : 0.f;
+            f[j] = (x0 * a0 + x1 * a1) * inv;
+          }
+          *reinterpret_cast<bf16x8*>(op + c0 + c * 8) = pack8(f);
+        }
       }
     }
   }
@@ -348,7 +380,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   __syncthreads();
   if (warp == 0) {
     tc::fence_after_sync();
-    tc::tmem_dealloc<256>(tmem);
+    tc::tmem_dealloc<512>(tmem);
   }
 }
 
