@@ -84,6 +84,22 @@ __device__ __forceinline__ void wait_dbg(uint64_t* bar, uint32_t parity, int tag
 #define MBW(bar, par, tag) tc::mbar_wait(bar, par)
 #endif
 
+#ifdef ATC_PROF
+// diagnostic build only (tools/atc_prof.py): thread 0's %globaltimer at each
+// phase of the last launch, per CTA
+__device__ unsigned long long g_atc_prof[4096][12];
+#define PROF(i)                                                                       \
+  do {                                                                                \
+    if (threadIdx.x == 0) {                                                           \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_atc_prof[blockIdx.x * gridDim.y + blockIdx.y][i] = t_;                        \
+    }                                                                                 \
+  } while (0)
+#else
+#define PROF(i)
+#endif
+
 // byte offset of the 16-byte chunk `c` (0..7) of row r in a [rows x 64] bf16
 // block with the 128-byte swizzle (chunk index XOR row % 8)
 __device__ __forceinline__ int swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
@@ -127,8 +143,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
   const int QD = Hq * kD, KVD = Hkv * kD;
-  constexpr int V8 = kD / 8;
 
+  // start / slot come from kernels complete before the previous one (the
+  // round's upload): read first, their latency hidden by the setup below
+  const int pstart = start[b];
+  const int kv_slot = slot[b];
   if (tid == 0) {
     tc::prefetch_tmap(&tmK);
     tc::prefetch_tmap(&tmV);
@@ -154,8 +173,6 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   // previous kernel: chunks made only of them are requested before the
   // programmatic-dependency wait and the append (start / slot come from
   // earlier kernels, complete by then)
-  const int pstart = start[b];
-  const int kv_slot = slot[b];
   const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // cache row of key 0
   const int n_keys = min(pstart + Qtot, T);
   const int n_chunks = (n_keys + kKeys - 1) / kKeys;
@@ -174,49 +191,98 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   pdl_wait();
   pdl_trigger();
 
-  // (1) the call's own K / V rows -> cache (K rotated); visible to the TMA
-  // (async proxy) after the proxy fence + barrier
-  if (fuse_append) {
-    for (int e = tid; e < 2 * Qtot * V8; e += kThreads) {
-      const int kv = e >= Qtot * V8;
-      const int e2 = e - kv * Qtot * V8;
-      const int i = e2 / V8, c = e2 - i * V8;
-      const int p = pstart + i;
-      if (p < 0 || p >= T) continue;
-      const __nv_bfloat16* rowp = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * kD;
-      bf16x8 val = *reinterpret_cast<const bf16x8*>(rowp + c * 8);
-      if (!kv && rope) {
-        const int pc = c < V8 / 2 ? c + V8 / 2 : c - V8 / 2;
-        float fv[8], pf[8];
-        unpack8(val, fv);
-        unpack8(*reinterpret_cast<const bf16x8*>(rowp + pc * 8), pf);
-        rope8(fv, pf, rope + (int64_t)p * (kD / 2), c * 8, kD / 2);
-        val = pack8(fv);
+  // (1) the call's own K / V rows -> cache (K rotated) and (2) Q -> the
+  // swizzled K-major tile (RoPE applied, rows past the call zero).  A unit is
+  // one row's dims {8j..8j+7} and {64+8j..64+8j+7} — a RoPE pair, one (cos,
+  // sin) run; each thread issues every load of its units (kQU of Q, at most
+  // one of the append: 2 * Qtot * 8 <= 256) before using any, so the staging
+  // costs one global latency.  The appended rows are visible to the TMA
+  // (async proxy) after the proxy fence + barrier.
+  constexpr int kQU = kRows * 8 / kThreads;
+  const int n_app = fuse_append ? 2 * Qtot * 8 : 0;
+  bf16x8 ux0[kQU + 1], ux1[kQU + 1];
+  float2 ucs[kQU + 1][8];
+  auto unit = [&](int u, const __nv_bfloat16*& src, __nv_bfloat16*& dst, int& r, int& j, int& p, bool& rot) {
+    src = nullptr;
+    dst = nullptr;
+    rot = false;
+    if (u < kQU) {  // Q unit: row r = e / 8
+      const int e = tid + u * kThreads;
+      r = e >> 3;
+      j = e & 7;
+      p = pstart + r / G;
+      if (r < rows_tot) {
+        src = qkv + (int64_t)(b * Qtot + r / G) * ldq + (h * G + r % G) * kD + 8 * j;
+        rot = rope != nullptr;
       }
-      *reinterpret_cast<bf16x8*>((kv ? vc : kc) + (row0 + p) * kD + c * 8) = val;
+    } else if (tid < n_app) {  // append unit: K rows, then V rows
+      const int kv = tid >= Qtot * 8;
+      const int e2 = tid - kv * Qtot * 8;
+      const int i = e2 >> 3;
+      j = e2 & 7;
+      p = pstart + i;
+      r = -1;
+      if (p >= 0 && p < T) {
+        src = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * kD + 8 * j;
+        dst = (kv ? vc : kc) + (row0 + p) * kD + 8 * j;
+        rot = !kv && rope != nullptr;
+      }
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+  };
+#pragma unroll
+  for (int u = 0; u <= kQU; ++u) {
+    const __nv_bfloat16* src;
+    __nv_bfloat16* dst;
+    int r, j, p;
+    bool rot;
+    unit(u, src, dst, r, j, p, rot);
+    if (src) {
+      ux0[u] = *reinterpret_cast<const bf16x8*>(src);
+      ux1[u] = *reinterpret_cast<const bf16x8*>(src + 64);
+      if (rot) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (kD / 2) + 8 * j + k];
+      }
+    }
   }
-  // (2) Q -> swizzled K-major tile (rows past the call are zero), RoPE applied
-  for (int e = tid; e < kRows * V8; e += kThreads) {
-    const int r = e / V8, c = e - r * V8;  // row, 16-byte chunk (dims 8c..8c+7)
-    bf16x8 val;
-    if (r < rows_tot) {
-      const __nv_bfloat16* qp = qkv + (int64_t)(b * Qtot + r / G) * ldq + (h * G + r % G) * kD;
-      val = *reinterpret_cast<const bf16x8*>(qp + c * 8);
-      if (rope) {
-        const int pc = c < V8 / 2 ? c + V8 / 2 : c - V8 / 2;
-        float fv[8], pf[8];
-        unpack8(val, fv);
-        unpack8(*reinterpret_cast<const bf16x8*>(qp + pc * 8), pf);
-        rope8(fv, pf, rope + (int64_t)(pstart + r / G) * (kD / 2), c * 8, kD / 2);
-        val = pack8(fv);
+#pragma unroll
+  for (int u = 0; u <= kQU; ++u) {
+    const __nv_bfloat16* src;
+    __nv_bfloat16* dst;
+    int r, j, p;
+    bool rot;
+    unit(u, src, dst, r, j, p, rot);
+    bf16x8 v0, v1;
+    if (src) {
+      v0 = ux0[u];
+      v1 = ux1[u];
+      if (rot) {
+        float f0[8], f1[8];
+        unpack8(v0, f0);
+        unpack8(v1, f1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 t = ucs[u][k];
+          const float a = f0[k], c = f1[k];
+          f0[k] = a * t.x - c * t.y;
+          f1[k] = c * t.x + a * t.y;
+        }
+        v0 = pack8(f0);
+        v1 = pack8(f1);
       }
     } else {
-      *reinterpret_cast<uint4*>(&val) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(&v0) = make_uint4(0, 0, 0, 0);
+      v1 = v0;
     }
-    *reinterpret_cast<bf16x8*>(sQ + (c >> 3) * BLK + swz(r, c & 7)) = val;
+    if (u < kQU) {
+      *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
+      *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
+    } else if (dst) {
+      *reinterpret_cast<bf16x8*>(dst) = v0;
+      *reinterpret_cast<bf16x8*>(dst + 64) = v1;
+    }
   }
+  if (fuse_append) asm volatile("fence.proxy.async.global;" ::: "memory");
   tc::fence_proxy_async_smem();
   __syncthreads();
 
@@ -384,6 +450,323 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   }
 }
 
+// Short caches (T <= kShortKeys = 384, the benchmark's verify contexts): the
+// whole context in one pass, no online rescaling, 16 warps.
+//
+//   * every K / V chunk is requested by TMA at kernel entry, before the
+//     programmatic-dependency wait (the rows of earlier calls do not depend on
+//     the previous kernel); the call's own K / V rows are written into the
+//     landed tiles from registers (and to the cache), the (cos, sin) rows of
+//     RoPE are read before the wait too;
+//   * S = Q K^T for every needed 128-key chunk in TMEM columns 0..383;
+//   * four warps per TMEM lane quadrant take the 32-key groups g = part (mod
+//     4) of every row: masked max (exchanged through shared memory), then
+//     P = exp2(s - m) as bf16 over the consumed K tiles and the partial row
+//     sums (each warp's keys in order, then parts 0 + 1 + 2 + 3);
+//   * one P.V MMA chain over the keys up to the last visible one into O
+//     (TMEM columns 384..511); the epilogue scales by 1 / sum, stages the bf16
+//     rows in shared memory and stores them coalesced.
+//
+// The key -> warp assignment and the reduction orders depend only on key
+// positions, so a row's arithmetic does not depend on Q (batch invariance);
+// P.V steps past a row's last visible key add exact zeros.
+constexpr int kShortKeys = 384;
+constexpr int kShortThreads = 512;
+
+struct SmemShort {
+  static constexpr int Q_OFF = 0;                 // Q [128 rows x 128 dims]: 2 blocks; later the exchange arrays
+  static constexpr int K_OFF = Q_OFF + 2 * BLK;   // K [384 keys x 128 dims]: 6 blocks; then P; then the O rows
+  static constexpr int V_OFF = K_OFF + 6 * BLK;   // V [384 keys x 128 dims]: 6 blocks
+  static constexpr int BAR_OFF = V_OFF + 6 * BLK;
+  static constexpr int BYTES = BAR_OFF + 64 + 1024;  // barriers, alignment slack
+};
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(kShortThreads, 1)
+attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                          const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
+                          const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
+                          __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
+                          int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
+                          int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm + SmemShort::Q_OFF;
+  uint8_t* sK = sm + SmemShort::K_OFF;
+  uint8_t* sV = sm + SmemShort::V_OFF;
+  uint8_t* sP = sK;                                                          // after S is complete
+  uint8_t* sO = sK;                                                          // after P.V is complete
+  float* red = reinterpret_cast<float*>(sQ);                                 // [4 parts][128 rows]: max, then sum
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + SmemShort::BAR_OFF);  // [3 chunks]
+  uint64_t* s_full = kv_full + 3;
+  uint64_t* pv_done = s_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int pstart = start[b];
+  const int kv_slot = slot[b];
+  const int G = Hq / Hkv;
+  const int rows_tot = Qtot * G;
+  const int QD = Hq * kD, KVD = Hkv * kD;
+  const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;
+  const int n_keys = min(pstart + Qtot, T);
+  const int n_chunks = n_keys > 0 ? (n_keys + kKeys - 1) / kKeys : 0;
+  PROF(0);
+
+  if (tid == 0) {
+    tc::prefetch_tmap(&tmK);
+    tc::prefetch_tmap(&tmV);
+    for (int i = 0; i < 3; ++i) tc::mbar_init(&kv_full[i], 1);
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(pv_done, 1);
+    tc::fence_barrier_init();
+    const uint64_t pol = tc::policy_evict_first();
+    for (int c = 0; c < n_chunks; ++c) {
+      tc::mbar_arrive_expect_tx(&kv_full[c], 4 * BLK);
+      const int y = (int)(row0 + c * kKeys);
+      for (int half = 0; half < 2; ++half) {
+        tc::tma_load_2d(sK + (2 * c + half) * BLK, &tmK, &kv_full[c], half * 64, y, pol);
+        tc::tma_load_2d(sV + (2 * c + half) * BLK, &tmV, &kv_full[c], half * 64, y, pol);
+      }
+    }
+  }
+  __syncwarp();
+  if (warp == 0) tc::tmem_alloc<512>(tmem_slot);  // S: columns 0..383, O: 384..511
+
+  // staging units: one row's dims {8j..8j+7} and {64+8j..64+8j+7} (a RoPE
+  // pair); kQU of Q per thread, at most one of the append (2 * Qtot * 8 <= 256)
+  constexpr int kQU = kRows * 8 / kShortThreads;
+  const int n_app = fuse_append ? 2 * Qtot * 8 : 0;
+  auto unit = [&](int u, bool& live, int& r, int& j, int& p, int& i, int& kv, bool& rot) {
+    live = false;
+    rot = false;
+    kv = 0;
+    if (u < kQU) {
+      const int e = tid + u * kShortThreads;
+      r = e >> 3;
+      j = e & 7;
+      i = r / G;
+      p = pstart + i;
+      live = r < rows_tot;
+      rot = live && rope != nullptr;
+    } else if (tid < n_app) {
+      kv = tid >= Qtot * 8;
+      const int e2 = tid - kv * Qtot * 8;
+      i = e2 >> 3;
+      j = e2 & 7;
+      p = pstart + i;
+      r = -1;
+      live = p >= 0 && p < T;
+      rot = live && !kv && rope != nullptr;
+    }
+  };
+  float2 ucs[kQU + 1][8];  // the (cos, sin) rows: constant, read before the dependency wait
+#pragma unroll
+  for (int u = 0; u <= kQU; ++u) {
+    bool live, rot;
+    int r, j, p, i, kv;
+    unit(u, live, r, j, p, i, kv, rot);
+    if (rot) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (kD / 2) + 8 * j + k];
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + kShortKeys;
+  PROF(1);
+  pdl_wait();
+  pdl_trigger();
+  PROF(2);
+
+  bf16x8 ux0[kQU + 1], ux1[kQU + 1];
+#pragma unroll
+  for (int u = 0; u <= kQU; ++u) {
+    bool live, rot;
+    int r, j, p, i, kv;
+    unit(u, live, r, j, p, i, kv, rot);
+    if (live) {
+      const __nv_bfloat16* src = u < kQU ? qkv + (int64_t)(b * Qtot + i) * ldq + (h * G + r % G) * kD + 8 * j
+                                         : qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * kD + 8 * j;
+      ux0[u] = *reinterpret_cast<const bf16x8*>(src);
+      ux1[u] = *reinterpret_cast<const bf16x8*>(src + 64);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u <= kQU; ++u) {
+    bool live, rot;
+    int r, j, p, i, kv;
+    unit(u, live, r, j, p, i, kv, rot);
+    bf16x8 v0, v1;
+    if (live) {
+      v0 = ux0[u];
+      v1 = ux1[u];
+      if (rot) {
+        float f0[8], f1[8];
+        unpack8(v0, f0);
+        unpack8(v1, f1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float2 t = ucs[u][k];
+          const float a = f0[k], c = f1[k];
+          f0[k] = a * t.x - c * t.y;
+          f1[k] = c * t.x + a * t.y;
+        }
+        v0 = pack8(f0);
+        v1 = pack8(f1);
+      }
+    } else {
+      *reinterpret_cast<uint4*>(&v0) = make_uint4(0, 0, 0, 0);
+      v1 = v0;
+    }
+    if (u < kQU) {
+      *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
+      *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
+    } else if (live) {
+      __nv_bfloat16* dst = (kv ? vc : kc) + (row0 + p) * kD + 8 * j;
+      *reinterpret_cast<bf16x8*>(dst) = v0;
+      *reinterpret_cast<bf16x8*>(dst + 64) = v1;
+      const int c = p / kKeys, rr = p - c * kKeys;  // and into its chunk's landed tile
+      tc::mbar_wait(&kv_full[c], 0);
+      uint8_t* t = (kv ? sV : sK) + 2 * c * BLK;
+      *reinterpret_cast<bf16x8*>(t + swz(rr, j)) = v0;
+      *reinterpret_cast<bf16x8*>(t + BLK + swz(rr, j)) = v1;
+    }
+  }
+  if (fuse_append) asm volatile("fence.proxy.async.global;" ::: "memory");
+  tc::fence_proxy_async_smem();
+  __syncthreads();
+  PROF(3);
+
+  constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
+  constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
+  if (tid == 0 && n_chunks > 0) {
+    for (int c = 0; c < n_chunks; ++c) {
+      tc::mbar_wait(&kv_full[c], 0);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint64_t ad = tc::smem_desc_sw128(sQ + (k >> 2) * BLK) + 2 * (k & 3);
+        const uint64_t bd = tc::smem_desc_sw128(sK + (2 * c + (k >> 2)) * BLK) + 2 * (k & 3);
+        tc::mma_bf16(tmem + c * kKeys, ad, bd, idS, k > 0 ? 1u : 0u);
+      }
+    }
+    tc::mma_commit(s_full);
+  }
+  __syncwarp();
+
+  const int q = warp & 3, part = warp >> 2;  // TMEM lane quadrant, key part (32-key groups part mod 4)
+  const int r = q * 32 + (tid & 31);         // this thread's row = TMEM lane
+  const int row_pos = r < rows_tot ? pstart + r / G : -1;
+  const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+  const int n_grp = (n_keys + 31) / 32;      // groups holding a key < n_keys
+  float m = -INFINITY, psum = 0.f;
+  if (n_chunks > 0) {
+    tc::mbar_wait(s_full, 0);
+    tc::fence_after_sync();
+    PROF(4);
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int gi = part; gi < n_grp; gi += 4) {
+      uint32_t sv[32];
+      tc::tmem_ld16(tmem + lane_base + gi * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
+      tc::tmem_ld16(tmem + lane_base + gi * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int key = gi * 32 + jj;
+        if (key <= row_pos && key < n_keys) mx = fmaxf(mx, __uint_as_float(sv[jj]) * scale_log2);
+      }
+    }
+    red[part * kRows + r] = mx;
+  }
+  __syncthreads();  // (S complete: the Q region is free for the exchange)
+  PROF(5);
+  if (n_chunks > 0) {
+    m = fmaxf(fmaxf(red[r], red[kRows + r]), fmaxf(red[2 * kRows + r], red[3 * kRows + r]));
+#pragma unroll 1
+    for (int gi = part; gi < n_grp; gi += 4) {
+      uint32_t sv[32];
+      tc::tmem_ld16(tmem + lane_base + gi * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
+      tc::tmem_ld16(tmem + lane_base + gi * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        float pv[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int key = gi * 32 + q4 * 8 + jj;
+          const bool vis = key <= row_pos && key < n_keys && m != -INFINITY;
+          const float e = ex2_ftz(__uint_as_float(sv[q4 * 8 + jj]) * scale_log2 - m);
+          pv[jj] = vis ? e : 0.f;
+          psum += pv[jj];
+        }
+        const int c8 = gi * 4 + q4;  // 8-key chunk; P block = 64 keys
+        *reinterpret_cast<bf16x8*>(sP + (c8 >> 3) * BLK + swz(r, c8 & 7)) = pack8(pv);
+      }
+    }
+  }
+  tc::fence_proxy_async_smem();  // P visible to the MMA
+  tc::fence_before_sync();
+  __syncthreads();               // every max read before the sums overwrite them
+  PROF(6);
+  red[part * kRows + r] = psum;
+  if (tid == 0 && n_chunks > 0) {
+    tc::fence_after_sync();
+    const int n_steps = (n_keys + 15) / 16;  // 16-key steps up to the last key (P written for whole groups)
+    for (int k = 0; k < n_steps; ++k) {
+      const uint64_t ad = tc::smem_desc_sw128(sP + (k >> 2) * BLK) + 2 * (k & 3);
+      // V rows 16k..16k+15 of chunk k / 8, the two 64-dim boxes BLK apart
+      const uint64_t bd = desc_mn_sw128(sV + (k >> 3) * 2 * BLK + (k & 7) * 2048, BLK);
+      tc::mma_bf16(tO, ad, bd, idPV, k > 0 ? 1u : 0u);
+    }
+    tc::mma_commit(pv_done);
+  }
+  __syncwarp();
+  if (n_chunks > 0) tc::mbar_wait(pv_done, 0);
+  tc::fence_after_sync();
+  __syncthreads();  // the sums; P.V complete (the K / P region is free for the O rows)
+  PROF(7);
+  const float L = ((red[r] + red[kRows + r]) + red[2 * kRows + r]) + red[3 * kRows + r];
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  {  // this warp's 32 dims of its rows -> bf16 rows in shared memory (16-byte chunks XOR-swizzled by row)
+    uint32_t o[32];
+    tc::tmem_ld16(tO + lane_base + part * 32, *reinterpret_cast<uint32_t(*)[16]>(o));
+    tc::tmem_ld16(tO + lane_base + part * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(o + 16));
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float f[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) f[jj] = n_chunks > 0 ? __uint_as_float(o[c * 8 + jj]) * inv : 0.f;
+      const int ch = part * 4 + c;  // 16-byte chunk of the 256-byte row
+      *reinterpret_cast<bf16x8*>(sO + r * 256 + ((ch ^ (r & 15)) << 4)) = pack8(f);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  PROF(8);
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+  // coalesced stores: half a warp per row (16 lanes x 16 bytes)
+  for (int e = tid; e < rows_tot * 16; e += kShortThreads) {
+    const int rr = e >> 4, ch = e & 15;
+    const bf16x8 v = *reinterpret_cast<const bf16x8*>(sO + rr * 256 + ((ch ^ (rr & 15)) << 4));
+    *reinterpret_cast<bf16x8*>(out + (int64_t)(b * Qtot + rr / G) * ldo + (h * G + rr % G) * kD + ch * 8) = v;
+  }
+  PROF(9);
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -411,9 +794,18 @@ static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows) {
 
 }  // namespace atc
 
-int preload_attention_tc() { return preload_fn(atc::attention_tc_kernel); }
+int preload_attention_tc() {
+  const int e = preload_fn(atc::attention_tc_kernel);
+  return e ? e : preload_fn(atc::attention_tc_short_kernel);
+}
 
 }  // namespace ms
+
+#ifdef ATC_PROF
+extern "C" int ms_atc_prof_read(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, ms::atc::g_atc_prof, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
                                const int32_t* slot, const int32_t* start, int T, int n_slots, void* k_cache,
@@ -430,10 +822,18 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(atc::attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             atc::Smem::BYTES) != cudaSuccess)
+                             atc::Smem::BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(atc::attention_tc_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             atc::SmemShort::BYTES) != cudaSuccess)
       return MS_ERR_CUDA;
     attr = true;
   }
+  // the kernel is chosen by the cache length T, never by Q (batch invariance)
+  if (T <= atc::kShortKeys)
+    return launch(atc::attention_tc_short_kernel, dim3(B, Hkv), dim3(atc::kShortThreads), atc::SmemShort::BYTES,
+                  (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
+                  (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
+                  (const float2*)rope, (__nv_bfloat16*)out, ldo);
   return launch(atc::attention_tc_kernel, dim3(B, Hkv), dim3(atc::kThreads), atc::Smem::BYTES,
                 (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,

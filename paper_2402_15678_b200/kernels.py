@@ -211,8 +211,14 @@ class AttnWorkspace:
 
 
 # grouped-query decode / verify attention (head dim 128, <= 16 positions) on
-# the tcgen05 kernel (csrc/attention_tc.cu) instead of the warp-MMA row kernel
-TC_ATTENTION = False
+# the tcgen05 kernels (csrc/attention_tc.cu) instead of the warp-MMA row
+# kernel.  "auto": for caches of <= TC_SHORT_KEYS positions (the one-pass
+# kernel, 1.3-2.4x faster than the row kernel at the benchmark's ~200-key
+# contexts); longer caches keep the row kernel (the online-softmax tcgen05
+# kernel measured 3-12 % slower there).  True: tcgen05 for every length;
+# False: the row kernel.  Chosen by the cache length, never by Q.
+TC_ATTENTION: bool | str = "auto"
+TC_SHORT_KEYS = 384
 
 
 def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Tensor,
@@ -233,7 +239,8 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
     if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < T or rope.shape[1] * 2 != D):
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
-    if (TC_ATTENTION and Hkv < H and D == 128 and page is None and ws is None and Q <= 16
+    use_tc = TC_ATTENTION is True or (TC_ATTENTION == "auto" and T <= TC_SHORT_KEYS)
+    if (use_tc and Hkv < H and D == 128 and page is None and ws is None and Q <= 16
             and Q * (H // Hkv) <= 128 and k_cache.is_contiguous() and v_cache.is_contiguous()):
         _native.call("ms_attention_tc", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                      _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, k_cache.shape[0],

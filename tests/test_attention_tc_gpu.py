@@ -28,6 +28,7 @@ def _run(qkv, B, Q, H, Hkv, D, start, kc, vc, table):
 
 
 @pytest.mark.parametrize("H,Hkv,Q,T,rope", [(64, 8, 5, 320, True), (64, 8, 16, 320, True), (64, 8, 1, 320, True),
+                                            (64, 8, 7, 272, True), (64, 8, 3, 384, True), (64, 8, 5, 100, True),
                                             (16, 2, 7, 640, False), (64, 8, 7, 4300, True)])
 def test_tc_attention_vs_reference(H, Hkv, Q, T, rope):
     D = 128
@@ -36,7 +37,7 @@ def test_tc_attention_vs_reference(H, Hkv, Q, T, rope):
     kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     vc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g).to(BF)
-    starts = [0, 127, T - Q - 1] if T < 1000 else [0, 1500, T - Q - 1]
+    starts = [0, min(127, T // 2), T - Q - 1] if T < 1000 else [0, 1500, T - Q - 1]
     start = torch.tensor(starts, dtype=torch.int32)
     table = llama_ref.rope_table(T + 4, D, 10000.0) if rope else None
     kcd, vcd = kc.cuda(), vc.cuda()
@@ -53,16 +54,18 @@ def test_tc_attention_vs_reference(H, Hkv, Q, T, rope):
         torch.testing.assert_close(vcd[b, :, p0:p0 + Q].cpu().float().transpose(0, 1), vn, rtol=0, atol=0)
 
 
-def test_tc_attention_batch_invariant():
+@pytest.mark.parametrize("T", [272, 400])
+def test_tc_attention_batch_invariant(T):
     """Row (request b, position i) equals the same row computed with Q = i + 1
-    (a shorter verify of the same prefix) and with the request alone."""
-    H, Hkv, D, T, Q = 64, 8, 128, 400, 9
+    (a shorter verify of the same prefix) and with the request alone — for the
+    one-pass short-cache kernel (T <= 384) and the online-softmax one."""
+    H, Hkv, D, Q = 64, 8, 128, 9
     B = 2
     g = torch.Generator().manual_seed(5)
     kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     vc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g).to(BF)
-    start = torch.tensor([190, 250], dtype=torch.int32)
+    start = torch.tensor([122, 250], dtype=torch.int32)  # request 0's rows cross a 128-key chunk
     table = llama_ref.rope_table(T + 4, D, 10000.0)
     full = _run(qkv, B, Q, H, Hkv, D, start, kc.cuda(), vc.cuda(), table).cpu()
     q3 = qkv.view(B, Q, -1)[:, :4].reshape(B * 4, -1).contiguous()

@@ -11,7 +11,7 @@ BF = torch.bfloat16
 
 
 @pytest.mark.parametrize("H,Hkv,D,Q", [(8, 2, 128, 5), (12, 12, 64, 1), (8, 8, 128, 20), (64, 8, 128, 11)])
-def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q):
+def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q, monkeypatch):
     from paper_2402_15678_b200 import kernels as Kn
     B, T, bs = 3, 96, 16
     nb = T // bs
@@ -31,6 +31,7 @@ def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q):
     start = torch.tensor([0, 33, T - Q - 1], dtype=torch.int32, device="cuda")
     slot = torch.arange(B, dtype=torch.int32, device="cuda")
     tab = Kn.rope_table(T, D, device="cuda")
+    monkeypatch.setattr(Kn, "TC_ATTENTION", False)  # paged caches run on the row kernel: compare like with like
     a = Kn.attention(qkv, B, Q, H, D, slot, start, kc, vc, D ** -0.5, n_kv_heads=Hkv, rope=tab)
     p = Kn.attention(qkv, B, Q, H, D, slot, start, kp, vp, D ** -0.5, n_kv_heads=Hkv, rope=tab, page=(table, bs))
     assert torch.equal(a, p)

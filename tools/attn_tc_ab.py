@@ -31,7 +31,7 @@ for Q, ctx in cases:
         with torch.cuda.graph(g):
             f()
         graphs[tc_on] = g
-    K.TC_ATTENTION = False
+    K.TC_ATTENTION = "auto"
     res = {k: [] for k in graphs}
     for rep in range(3):
         for k, g in graphs.items():

@@ -4,7 +4,7 @@ process, arms interleaved so clock drift hits every arm alike.  An arm is a
 comma list of SpecEngine options: draft_sms=N (SM partition, csrc/
 partition.cu), draft_pdl=0|1 (programmatic dependent launch of the drafter
 kernels), draft_coresident=0|1, gated_persistent=0|1 (gate/up schedule,
-ms_set_gated_persistent), tc_attention=0|1 (kernels.TC_ATTENTION).
+ms_set_gated_persistent), tc_attention=0|1|2 (kernels.TC_ATTENTION False / True / "auto").
 usage: python tools/partition_ab.py ["draft_sms=0;draft_sms=16;draft_pdl=0"] [fixed_s=6] [reps=2] [new_tokens=128]
 prints one JSON line per (rep, arm)."""
 import json
@@ -41,12 +41,14 @@ for rep in range(reps):
         from paper_2402_15678_b200 import _native
         _native.lib.ms_set_gated_persistent(arm.get("gated_persistent", 1))  # baked into the captured graphs
         from paper_2402_15678_b200 import kernels as _K
-        _K.TC_ATTENTION = bool(arm.get("tc_attention", int(_K.TC_ATTENTION)))
+        if "tc_attention" in arm:  # 0: row kernel, 1: tcgen05 everywhere, 2: auto (by cache length)
+            _K.TC_ATTENTION = {0: False, 1: True, 2: "auto"}[arm["tc_attention"]]
         eng = SpecEngine(target, drafters, cfg, slots=32, max_len=max_len, fidelity=fid, pipelined=True,
                          adaptive=not fixed_s, **kw)
         eng.capture_graphs()
-        if teacher is None:
-            teacher = eng.greedy_teacher(bench.fresh(reqs), new_tokens)
+        # the greedy teacher of this arm's kernels (arms that change the target's
+        # arithmetic, e.g. tc_attention, have their own greedy continuation)
+        teacher = eng.greedy_teacher(bench.fresh(reqs), new_tokens)
         out = []
         for it in range(3):
             rs = bench.fresh(reqs)
