@@ -16,7 +16,7 @@ out = torch.empty(B * Q, H * D, device="cuda", dtype=torch.bfloat16)
 slot = torch.arange(B, dtype=torch.int32, device="cuda")
 start = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
 rope = K.rope_table(T + 8, D, 10000.0)
-for tc in (True, False):
+for tc in ("auto", False):
     K.TC_ATTENTION = tc
     for _ in range(3):
         K.attention(qkv, B, Q, H, D, slot, start, kc, vc, D ** -0.5, out=out, n_kv_heads=Hkv, rope=rope)
