@@ -418,14 +418,20 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
                      const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
 
 /* Grouped-query attention of Q <= 16 query positions per request on tcgen05
- * (head dim 128, Q * H / Hkv <= 128 flattened rows; contiguous cache of n_slots
- * slots [n_slots, Hkv, T, 128]): K / V read by TMA in 128-key chunks, S = Q K^T
- * and O += P V on tcgen05 with TMEM accumulators, online softmax per row,
- * K/V append fused (append != 0).  Same contract as ms_attention_gqa for
- * those shapes (csrc/attention_tc.cu). */
+ * (head dim 128, Q * H / Hkv <= 128 flattened rows): K / V read by TMA in
+ * 128-key chunks, S = Q K^T and P V on tcgen05 with TMEM accumulators, K/V
+ * append fused (append != 0).  T <= 384: one pass over the whole context;
+ * longer caches: online softmax over chunks.  Cache: contiguous
+ * [n_slots, Hkv, T, 128] (block_table NULL) or a paged pool of n_slots blocks
+ * [n_slots, Hkv, block_size, 128] with block_table [slots, max_blocks]
+ * (T = max_blocks * block_size <= 384, block_size a multiple of 16 dividing
+ * 128).  Replaces the attention inside ModelOracle.next_dist for the verify
+ * positions (aggspec/oracles.py:19-26, aggspec/engine.py:294-296); same
+ * contract as ms_attention_paged for those shapes (csrc/attention_tc.cu). */
 int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D, const int32_t* slot,
                     const int32_t* start, int T, int n_slots, void* k_cache, void* v_cache, const void* rope,
-                    float scale, int append, void* out, int64_t ldo, void* stream);
+                    float scale, int append, void* out, int64_t ldo, const int32_t* block_table,
+                    int max_blocks, int block_size, void* stream);
 
 /* Programmatic dependent launch (PDL) attribute for subsequent launches of
  * this process (default on; MS_PDL=0 in the environment turns it off); a

@@ -76,7 +76,7 @@ _SIGS = {
     "ms_rmsnorm_grouped": [_P, _I64, _P, _P, _I64, _I, _F, _I, _I, _P, _I64, _P],
     "ms_draft_commit_grouped": [_P, _P, _I, _I, _I, _I, _P, _I64, _P, ctypes.POINTER(ctypes.c_float),
                                 ctypes.c_uint64, _P, _P, _P],
-    "ms_attention_tc": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _F, _I, _P, _I64, _P],
+    "ms_attention_tc": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _F, _I, _P, _I64, _P, _I, _I, _P],
     "ms_attention_paged": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _F, _I, _P, _I64, _P, _I64,
                            _P, _I, _P, _I, _I, _P],
     "ms_kv_append_paged": [_P, _I64, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _P],

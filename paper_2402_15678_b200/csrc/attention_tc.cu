@@ -493,7 +493,7 @@ attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_
                           const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                           __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
                           int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out,
-                          int64_t ldo) {
+                          int64_t ldo, const int32_t* __restrict__ block_table, int max_blocks, int bs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm + SmemShort::Q_OFF;
@@ -514,25 +514,43 @@ attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
   const int QD = Hq * kD, KVD = Hkv * kD;
-  const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;
+  const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // contiguous: cache row of key 0
+  // cache row of key t (paged: pool block table[slot][t / bs], row t % bs)
+  auto cache_row = [&](int t) -> int64_t {
+    if (!block_table) return row0 + t;
+    return ((int64_t)block_table[(int64_t)kv_slot * max_blocks + t / bs] * Hkv + h) * bs + t % bs;
+  };
   const int n_keys = min(pstart + Qtot, T);
   const int n_chunks = n_keys > 0 ? (n_keys + kKeys - 1) / kKeys : 0;
+  const int n_steps = (n_keys + 15) / 16;  // 16-key P.V steps up to the last key
   PROF(0);
 
-  if (tid == 0) {
-    tc::prefetch_tmap(&tmK);
-    tc::prefetch_tmap(&tmV);
-    for (int i = 0; i < 3; ++i) tc::mbar_init(&kv_full[i], 1);
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(pv_done, 1);
-    tc::fence_barrier_init();
+  // every needed K / V chunk now: the rows of earlier calls do not depend on
+  // the previous kernel, the rows this call appends are overwritten in shared
+  // memory below.  Paged: one box of bs rows per block, blocks holding a key
+  // below 16 * n_steps (the P.V range; the rest of the chunk is masked)
+  if (warp == 0) {
+    const int nb_c = block_table ? kKeys / bs : 1;  // boxes per chunk and operand half
+    const int need = block_table ? (16 * n_steps + bs - 1) / bs : n_chunks;
+    if (tid == 0) {
+      tc::prefetch_tmap(&tmK);
+      tc::prefetch_tmap(&tmV);
+      for (int i = 0; i < 3; ++i) tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(s_full, 1);
+      tc::mbar_init(pv_done, 1);
+      tc::fence_barrier_init();
+      for (int c = 0; c < n_chunks; ++c)
+        tc::mbar_arrive_expect_tx(&kv_full[c], 4 * BLK / nb_c * (min(need, (c + 1) * nb_c) - c * nb_c));
+    }
+    __syncwarp();
     const uint64_t pol = tc::policy_evict_first();
-    for (int c = 0; c < n_chunks; ++c) {
-      tc::mbar_arrive_expect_tx(&kv_full[c], 4 * BLK);
-      const int y = (int)(row0 + c * kKeys);
+    for (int i = tid; i < need; i += 32) {  // box i: chunk i / nb_c
+      const int c = i / nb_c;
+      const int y = (int)(block_table ? cache_row(i * bs) : row0 + c * kKeys);
+      const int off = (i - c * nb_c) * (BLK / nb_c);
       for (int half = 0; half < 2; ++half) {
-        tc::tma_load_2d(sK + (2 * c + half) * BLK, &tmK, &kv_full[c], half * 64, y, pol);
-        tc::tma_load_2d(sV + (2 * c + half) * BLK, &tmV, &kv_full[c], half * 64, y, pol);
+        tc::tma_load_2d(sK + (2 * c + half) * BLK + off, &tmK, &kv_full[c], half * 64, y, pol);
+        tc::tma_load_2d(sV + (2 * c + half) * BLK + off, &tmV, &kv_full[c], half * 64, y, pol);
       }
     }
   }
@@ -631,7 +649,7 @@ attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_
       *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
       *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
     } else if (live) {
-      __nv_bfloat16* dst = (kv ? vc : kc) + (row0 + p) * kD + 8 * j;
+      __nv_bfloat16* dst = (kv ? vc : kc) + cache_row(p) * kD + 8 * j;
       *reinterpret_cast<bf16x8*>(dst) = v0;
       *reinterpret_cast<bf16x8*>(dst + 64) = v1;
       const int c = p / kKeys, rr = p - c * kKeys;  // and into its chunk's landed tile
@@ -721,8 +739,7 @@ attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_
   red[part * kRows + r] = psum;
   if (tid == 0 && n_chunks > 0) {
     tc::fence_after_sync();
-    const int n_steps = (n_keys + 15) / 16;  // 16-key steps up to the last key (P written for whole groups)
-    for (int k = 0; k < n_steps; ++k) {
+    for (int k = 0; k < n_steps; ++k) {  // (P written for whole 32-key groups)
       const uint64_t ad = tc::smem_desc_sw128(sP + (k >> 2) * BLK) + 2 * (k & 3);
       // V rows 16k..16k+15 of chunk k / 8, the two 64-dim boxes BLK apart
       const uint64_t bd = desc_mn_sw128(sV + (k >> 3) * 2 * BLK + (k & 7) * 2048, BLK);
@@ -779,13 +796,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// the cache [rows, 128] bf16 as 2-D, box = [64 dims, 128 keys], 128-byte swizzle
-static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows) {
+// the cache [rows, 128] bf16 as 2-D, box = [64 dims, box_rows keys], 128-byte swizzle
+static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int box_rows = kKeys) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(kD * 2)};
-  cuuint32_t box[2] = {64, (cuuint32_t)kKeys};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -810,15 +827,20 @@ extern "C" int ms_atc_prof_read(void* host, size_t bytes) {
 extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D,
                                const int32_t* slot, const int32_t* start, int T, int n_slots, void* k_cache,
                                void* v_cache, const void* rope, float scale, int append, void* out, int64_t ldo,
-                               void* stream) {
+                               const int32_t* block_table, int max_blocks, int block_size, void* stream) {
   using namespace ms;
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || T < 1 || n_slots < 1 || H % Hkv) return MS_ERR_VALUE;
   if (D != atc::kD || Q * (H / Hkv) > atc::kRows || Q > 16) return MS_ERR_UNSUPPORTED;
+  if (block_table && (block_size < 16 || atc::kKeys % block_size || max_blocks < 1 || T != max_blocks * block_size))
+    return MS_ERR_VALUE;
+  if (block_table && T > atc::kShortKeys) return MS_ERR_UNSUPPORTED;  // paged: the one-pass kernel only
   if (B == 0) return MS_OK;
   if (!qkv || !slot || !start || !k_cache || !v_cache || !out || ldq % 8 || ldo % 8) return MS_ERR_VALUE;
-  const int64_t rows = (int64_t)n_slots * Hkv * T;
+  // contiguous: n_slots slots of T rows per KV head; paged: n_slots pool blocks of block_size rows
+  const int64_t rows = (int64_t)n_slots * Hkv * (block_table ? block_size : T);
+  const int box = block_table ? block_size : atc::kKeys;
   CUtensorMap tk, tv;
-  if (!atc::cache_tmap(&tk, k_cache, rows) || !atc::cache_tmap(&tv, v_cache, rows)) return MS_ERR_CUDA;
+  if (!atc::cache_tmap(&tk, k_cache, rows, box) || !atc::cache_tmap(&tv, v_cache, rows, box)) return MS_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(atc::attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -833,7 +855,7 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
     return launch(atc::attention_tc_short_kernel, dim3(B, Hkv), dim3(atc::kShortThreads), atc::SmemShort::BYTES,
                   (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                   (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
-                  (const float2*)rope, (__nv_bfloat16*)out, ldo);
+                  (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);
   return launch(atc::attention_tc_kernel, dim3(B, Hkv), dim3(atc::kThreads), atc::Smem::BYTES,
                 (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,

@@ -214,8 +214,9 @@ class AttnWorkspace:
 # the tcgen05 kernels (csrc/attention_tc.cu) instead of the warp-MMA row
 # kernel.  "auto": for caches of <= TC_SHORT_KEYS positions (the one-pass
 # kernel, 1.3-2.4x faster than the row kernel at the benchmark's ~200-key
-# contexts); longer caches keep the row kernel (the online-softmax tcgen05
-# kernel measured 3-12 % slower there).  True: tcgen05 for every length;
+# contexts; contiguous or paged with 16..128-row blocks); longer caches keep
+# the row kernel (the online-softmax tcgen05 kernel measured 3-12 % slower
+# there).  True: tcgen05 for every length;
 # False: the row kernel.  Chosen by the cache length, never by Q.
 TC_ATTENTION: bool | str = "auto"
 TC_SHORT_KEYS = 384
@@ -240,12 +241,17 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
     use_tc = TC_ATTENTION is True or (TC_ATTENTION == "auto" and T <= TC_SHORT_KEYS)
-    if (use_tc and Hkv < H and D == 128 and page is None and ws is None and Q <= 16
+    if page is not None:  # paged pools: the one-pass kernel, 16..128-row blocks
+        use_tc = use_tc and T <= TC_SHORT_KEYS and page[1] % 16 == 0 and 128 % page[1] == 0
+    if (use_tc and Hkv < H and D == 128 and ws is None and Q <= 16
             and Q * (H // Hkv) <= 128 and k_cache.is_contiguous() and v_cache.is_contiguous()):
         _native.call("ms_attention_tc", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                      _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, k_cache.shape[0],
                      _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), None if rope is None else rope.data_ptr(),
-                     scale, int(append), out.data_ptr(), out.stride(0), _dev.stream_ptr(stream))
+                     scale, int(append), out.data_ptr(), out.stride(0),
+                     None if page is None else _dev.ptr(page[0], torch.int32, "block_table"),
+                     0 if page is None else page[0].shape[1], 0 if page is None else page[1],
+                     _dev.stream_ptr(stream))
         return out
     _native.call("ms_attention_paged", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                  _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T,

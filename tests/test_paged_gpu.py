@@ -10,10 +10,14 @@ pytestmark = pytest.mark.gpu
 BF = torch.bfloat16
 
 
-@pytest.mark.parametrize("H,Hkv,D,Q", [(8, 2, 128, 5), (12, 12, 64, 1), (8, 8, 128, 20), (64, 8, 128, 11)])
-def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q, monkeypatch):
+@pytest.mark.parametrize("H,Hkv,D,Q,T,bs", [(8, 2, 128, 5, 96, 16), (12, 12, 64, 1, 96, 16), (8, 8, 128, 20, 96, 16),
+                                           (64, 8, 128, 11, 96, 16), (64, 8, 128, 7, 320, 32)])
+@pytest.mark.parametrize("tc", [False, "auto"])
+def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q, T, bs, tc, monkeypatch):
+    """Either GQA kernel (the row kernel, or the tcgen05 one where "auto"
+    selects it: 70B-style heads, caches <= 384 positions)."""
     from paper_2402_15678_b200 import kernels as Kn
-    B, T, bs = 3, 96, 16
+    B = 3
     nb = T // bs
     g = torch.Generator().manual_seed(H + Q)
     kc = torch.randn(B, Hkv, T, D, generator=g).to(BF).cuda()
@@ -31,7 +35,7 @@ def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q, monkeypatch):
     start = torch.tensor([0, 33, T - Q - 1], dtype=torch.int32, device="cuda")
     slot = torch.arange(B, dtype=torch.int32, device="cuda")
     tab = Kn.rope_table(T, D, device="cuda")
-    monkeypatch.setattr(Kn, "TC_ATTENTION", False)  # paged caches run on the row kernel: compare like with like
+    monkeypatch.setattr(Kn, "TC_ATTENTION", tc)
     a = Kn.attention(qkv, B, Q, H, D, slot, start, kc, vc, D ** -0.5, n_kv_heads=Hkv, rope=tab)
     p = Kn.attention(qkv, B, Q, H, D, slot, start, kp, vp, D ** -0.5, n_kv_heads=Hkv, rope=tab, page=(table, bs))
     assert torch.equal(a, p)
