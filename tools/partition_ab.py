@@ -4,7 +4,8 @@ process, arms interleaved so clock drift hits every arm alike.  An arm is a
 comma list of SpecEngine options: draft_sms=N (SM partition, csrc/
 partition.cu), draft_pdl=0|1 (programmatic dependent launch of the drafter
 kernels), draft_coresident=0|1, gated_persistent=0|1 (gate/up schedule,
-ms_set_gated_persistent), tc_attention=0|1|2 (kernels.TC_ATTENTION False / True / "auto").
+ms_set_gated_persistent), stream_priority=0|1|2 (equal / verify / draft
+high), tc_attention=0|1|2 (kernels.TC_ATTENTION False / True / "auto").
 usage: python tools/partition_ab.py ["draft_sms=0;draft_sms=16;draft_pdl=0"] [fixed_s=6] [reps=2] [new_tokens=128]
 prints one JSON line per (rep, arm)."""
 import json
@@ -37,6 +38,7 @@ teacher = None
 for rep in range(reps):
     for arm in arms:
         kw = {"draft_sms": arm.get("draft_sms", 0), "draft_pdl": bool(arm.get("draft_pdl", 1)),
+              "stream_priority": ("equal", "verify", "draft")[arm.get("stream_priority", 0)],
               "draft_coresident": bool(arm["draft_coresident"]) if "draft_coresident" in arm else None}
         from paper_2402_15678_b200 import _native
         _native.lib.ms_set_gated_persistent(arm.get("gated_persistent", 1))  # baked into the captured graphs
