@@ -51,7 +51,7 @@ struct Smem {
   static constexpr int V_OFF = K_OFF + 4 * BLK;       // V [2 groups][128 keys x 128 dims]
   static constexpr int P_OFF = V_OFF + 4 * BLK;       // P [2 groups][128 rows x 128 keys]
   static constexpr int BAR_OFF = P_OFF + 4 * BLK;
-  static constexpr int BYTES = BAR_OFF + 64 + 1024 + 1024;  // barriers, group 1 (m, l) per row, alignment slack
+  static constexpr int BYTES = BAR_OFF + 128 + 1024 + 1024;  // barriers, group 1 (m, l) per row, alignment slack
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -100,6 +100,12 @@ __device__ unsigned long long g_atc_prof[4096][12];
 #define PROF(i)
 #endif
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // byte offset of the 16-byte chunk `c` (0..7) of row r in a [rows x 64] bf16
 // block with the 128-byte swizzle (chunk index XOR row % 8)
 __device__ __forceinline__ int swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
@@ -129,8 +135,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   uint8_t* sK = sm + Smem::K_OFF;
   uint8_t* sV = sm + Smem::V_OFF;
   uint8_t* sP = sm + Smem::P_OFF;
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2 groups]
-  uint64_t* s_full = kv_full + 2;                                       // [2]
+  uint64_t* k_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2 groups]
+  uint64_t* v_full = k_full + 2;                                       // [2]
+  uint64_t* s_full = v_full + 2;                                       // [2]
   uint64_t* pv_done = s_full + 2;                                       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
   float* stat = reinterpret_cast<float*>(tmem_slot + 4);                // [128 rows][2]: group 1's (m, l)
@@ -152,7 +159,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     tc::prefetch_tmap(&tmK);
     tc::prefetch_tmap(&tmV);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&k_full[i], 1);
+      tc::mbar_init(&v_full[i], 1);
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&pv_done[i], 1);
     }
@@ -176,18 +184,23 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // cache row of key 0
   const int n_keys = min(pstart + Qtot, T);
   const int n_chunks = (n_keys + kKeys - 1) / kKeys;
-  auto load_chunk = [&](int ch) {  // the issuer of group ch % 2
+  // K and V of a chunk on separate barriers: the group's K buffer is free once
+  // its S MMA is complete (refilled while the softmax runs), its V buffer once
+  // its P.V is complete (refilled while the next chunk's softmax runs)
+  auto load_kv = [&](int ch, bool v) {  // the issuer of group ch % 2
     const int buf = ch & 1;
-    tc::mbar_arrive_expect_tx(&kv_full[buf], 4 * BLK);
+    uint64_t* bar = v ? &v_full[buf] : &k_full[buf];
+    tc::mbar_arrive_expect_tx(bar, 2 * BLK);
     const int y = (int)(row0 + ch * kKeys);
     const uint64_t pol = tc::policy_evict_first();
-    for (int half = 0; half < 2; ++half) {
-      tc::tma_load_2d(sK + (2 * buf + half) * BLK, &tmK, &kv_full[buf], half * 64, y, pol);
-      tc::tma_load_2d(sV + (2 * buf + half) * BLK, &tmV, &kv_full[buf], half * 64, y, pol);
-    }
+    for (int half = 0; half < 2; ++half)
+      tc::tma_load_2d((v ? sV : sK) + (2 * buf + half) * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
   };
   const bool early = g < n_chunks && (g + 1) * kKeys <= pstart;  // this group's first chunk is all cache
-  if (issuer && early) load_chunk(g);
+  if (issuer && early) {
+    load_kv(g, false);
+    load_kv(g, true);
+  }
   pdl_wait();
   pdl_trigger();
 
@@ -289,7 +302,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
   constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
   auto issue_S = [&](int ch) {  // the group's issuer: S = Q K_ch^T
-    MBW(&kv_full[g], (ch >> 1) & 1, 1);
+    MBW(&k_full[g], (ch >> 1) & 1, 1);
     tc::fence_after_sync();
 #pragma unroll
     for (int k = 0; k < kD / 16; ++k) {
@@ -300,7 +313,10 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     tc::mma_commit(&s_full[g]);
   };
   if (issuer && g < n_chunks) {
-    if (!early) load_chunk(g);
+    if (!early) {
+      load_kv(g, false);
+      load_kv(g, true);
+    }
     issue_S(g);
   }
   __syncwarp();  // the issuer lane diverged: reconverge before the aligned tcgen05.ld
@@ -314,6 +330,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   for (int ch = g; ch < n_chunks; ch += 2, ++it) {
     MBW(&s_full[g], it & 1, 2);
     tc::fence_after_sync();
+    if (issuer && ch + 2 < n_chunks) load_kv(ch + 2, false);  // S(ch) done: the K buffer is free
+    __syncwarp();
     const int kbase = ch * kKeys;
     // pass 1: masked max of this chunk
     float mx = -INFINITY;
@@ -365,7 +383,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         for (int j = 0; j < 8; ++j) {
           const int key = kbase + c0 + q4 * 8 + j;
           const bool vis = key <= row_pos && key < n_keys && m_new != -INFINITY;
-          pv[j] = vis ? exp2f(__uint_as_float(sv[q4 * 8 + j]) * scale_log2 - m_new) : 0.f;
+          const float e = ex2_ftz(__uint_as_float(sv[q4 * 8 + j]) * scale_log2 - m_new);
+          pv[j] = vis ? e : 0.f;
           psum += pv[j];
         }
         const int c = (c0 >> 3) + q4;  // 16-byte chunk (8 keys) within the 128 keys
@@ -379,6 +398,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the group's 4 warps
     if (issuer) {
       tc::fence_after_sync();
+      MBW(&v_full[g], (ch >> 1) & 1, 6);
+      tc::fence_after_sync();
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
         const uint64_t ad = tc::smem_desc_sw128(gP + (k >> 2) * BLK) + 2 * (k & 3);
@@ -388,10 +409,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
       tc::mma_commit(&pv_done[g]);
       if (ch + 2 < n_chunks) {
-        // the group's K/V buffer is free once this P.V completes
-        MBW(&pv_done[g], it & 1, 4);
-        load_chunk(ch + 2);
-        issue_S(ch + 2);
+        issue_S(ch + 2);            // K(ch + 2) was requested when S(ch) completed
+        MBW(&pv_done[g], it & 1, 4);  // this P.V done: the V buffer is free
+        load_kv(ch + 2, true);
       }
     }
     __syncwarp();
@@ -480,12 +500,6 @@ struct SmemShort {
   static constexpr int BAR_OFF = V_OFF + 6 * BLK;
   static constexpr int BYTES = BAR_OFF + 64 + 1024;  // barriers, alignment slack
 };
-
-__device__ __forceinline__ float ex2_ftz(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __global__ void __launch_bounds__(kShortThreads, 1)
 attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,

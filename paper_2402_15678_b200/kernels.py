@@ -212,12 +212,12 @@ class AttnWorkspace:
 
 # grouped-query decode / verify attention (head dim 128, <= 16 positions) on
 # the tcgen05 kernels (csrc/attention_tc.cu) instead of the warp-MMA row
-# kernel.  "auto": for caches of <= TC_SHORT_KEYS positions (the one-pass
-# kernel, 1.3-2.4x faster than the row kernel at the benchmark's ~200-key
-# contexts; contiguous or paged with 16..128-row blocks); longer caches keep
-# the row kernel (the online-softmax tcgen05 kernel measured 3-12 % slower
-# there).  True: tcgen05 for every length;
-# False: the row kernel.  Chosen by the cache length, never by Q.
+# kernel: one pass for caches of <= TC_SHORT_KEYS positions (contiguous or
+# paged with 16..128-row blocks), online softmax over 128-key chunks for
+# longer contiguous caches — faster than the row kernel at every measured
+# length (ctx 190 Q = 7: 9.1 vs 12.7 us per 70B layer; 4K Q = 5: 90 vs 117).
+# "auto" (default) and True: tcgen05 wherever the shape allows; False: the
+# row kernel.  Chosen by shape and cache length, never by Q alone.
 TC_ATTENTION: bool | str = "auto"
 TC_SHORT_KEYS = 384
 
@@ -240,7 +240,7 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
     if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < T or rope.shape[1] * 2 != D):
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
-    use_tc = TC_ATTENTION is True or (TC_ATTENTION == "auto" and T <= TC_SHORT_KEYS)
+    use_tc = TC_ATTENTION in (True, "auto")
     if page is not None:  # paged pools: the one-pass kernel, 16..128-row blocks
         use_tc = use_tc and T <= TC_SHORT_KEYS and page[1] % 16 == 0 and 128 % page[1] == 0
     if (use_tc and Hkv < H and D == 128 and ws is None and Q <= 16
