@@ -216,8 +216,13 @@ class AttnWorkspace:
 # paged with 16..128-row blocks), online softmax over 128-key chunks for
 # longer contiguous caches — faster than the row kernel at every measured
 # length (ctx 190 Q = 7: 9.1 vs 12.7 us per 70B layer; 4K Q = 5: 90 vs 117).
-# "auto" (default) and True: tcgen05 wherever the shape allows; False: the
-# row kernel.  Chosen by shape and cache length, never by Q alone.
+# "auto" (default): tcgen05 for grouped-query heads wherever the shape allows;
+# True: also multi-head (G = 1) shapes — correct (tests), but slower there
+# than the row kernel at every measured length (Llama-2-13B heads, B = 16:
+# 44.6 vs 26.9 us at ctx 190, 437 vs 271 at 4K; profiles/
+# r2_attn_tc_mha_ab.jsonl: one query row per head leaves the 128-row MMA
+# tile nearly empty while the row kernel's 640 CTAs stream 4.9 TB/s);
+# False: the row kernel.  Chosen by shape and cache length, never by Q alone.
 TC_ATTENTION: bool | str = "auto"
 TC_SHORT_KEYS = 384
 
@@ -243,7 +248,7 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
     use_tc = TC_ATTENTION in (True, "auto")
     if page is not None:  # paged pools: the one-pass kernel, 16..128-row blocks
         use_tc = use_tc and T <= TC_SHORT_KEYS and page[1] % 16 == 0 and 128 % page[1] == 0
-    if (use_tc and Hkv < H and D == 128 and ws is None and Q <= 16
+    if (use_tc and (Hkv < H or TC_ATTENTION is True) and D == 128 and ws is None and Q <= 16
             and Q * (H // Hkv) <= 128 and k_cache.is_contiguous() and v_cache.is_contiguous()):
         _native.call("ms_attention_tc", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
                      _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, k_cache.shape[0],

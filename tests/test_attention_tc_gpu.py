@@ -29,7 +29,8 @@ def _run(qkv, B, Q, H, Hkv, D, start, kc, vc, table):
 
 @pytest.mark.parametrize("H,Hkv,Q,T,rope", [(64, 8, 5, 320, True), (64, 8, 16, 320, True), (64, 8, 1, 320, True),
                                             (64, 8, 7, 272, True), (64, 8, 3, 384, True), (64, 8, 5, 100, True),
-                                            (16, 2, 7, 640, False), (64, 8, 7, 4300, True)])
+                                            (16, 2, 7, 640, False), (64, 8, 7, 4300, True),
+                                            (40, 40, 5, 320, True), (40, 40, 7, 4300, True), (40, 40, 1, 600, True)])
 def test_tc_attention_vs_reference(H, Hkv, Q, T, rope):
     D = 128
     B = 3

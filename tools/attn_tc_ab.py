@@ -1,14 +1,16 @@
 """A/B of the 70B verify attention: the tcgen05 kernel (csrc/attention_tc.cu)
 vs the warp-MMA row kernel, 80-layer chains (one KV cache per layer, B=16)
 captured as CUDA graphs, replays interleaved; µs per layer and KV GB/s.
-usage: python tools/attn_tc_ab.py ["Q:ctx,..."]"""
+usage: python tools/attn_tc_ab.py ["Q:ctx,..."] ["H:Hkv:B:L"]   (default 64:8:16:80, the
+70B heads; 40:40:16:40 = Llama-2-13B's multi-head attention, cfg5)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2402_15678_b200 import kernels as K
 cases = [tuple(int(v) for v in c.split(":")) for c in (sys.argv[1] if len(sys.argv) > 1 else
          "5:190,7:190,9:190,13:190,7:1000,5:4096").split(",")]
-H, Hkv, D, B, L = 64, 8, 128, 16, 80
+H, Hkv, B, L = (int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "64:8:16:80").split(":"))
+D = 128
 for Q, ctx in cases:
     T = ctx + 32
     caches = [(torch.zeros(B, Hkv, T, D, device="cuda", dtype=torch.bfloat16),
@@ -40,7 +42,7 @@ for Q, ctx in cases:
             e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
             res[k].append(e0.elapsed_time(e1) * 1e3 / L)
     kvb = B * Hkv * (ctx + Q) * D * 2 * 2
-    row = {"Q": Q, "ctx": ctx}
+    row = {"H": H, "Hkv": Hkv, "B": B, "Q": Q, "ctx": ctx}
     for k, v in res.items():
         us = min(v)
         row["tc" if k else "rows"] = {"us_per_layer": round(us, 2), "GBs": round(kvb / (us * 1e-6) / 1e9)}
