@@ -142,6 +142,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
   float* stat = reinterpret_cast<float*>(tmem_slot + 4);                // [128 rows][2]: group 1's (m, l)
 
+  PROF(0);
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int g = warp >> 2;          // key group
@@ -298,6 +299,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   if (fuse_append) asm volatile("fence.proxy.async.global;" ::: "memory");
   tc::fence_proxy_async_smem();
   __syncthreads();
+  PROF(1);
 
   constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
   constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
@@ -330,65 +332,116 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   for (int ch = g; ch < n_chunks; ch += 2, ++it) {
     MBW(&s_full[g], it & 1, 2);
     tc::fence_after_sync();
-    if (issuer && ch + 2 < n_chunks) load_kv(ch + 2, false);  // S(ch) done: the K buffer is free
+    if (it == 4) PROF(4);
+    if (it == 8) PROF(5);
+    if (issuer) {
+      if (ch + 2 < n_chunks) load_kv(ch + 2, false);  // S(ch) done: the K buffer is free
+      if (it > 0) {  // P.V(ch - 2) (issued after S(ch)) done: the V buffer is free
+        MBW(&pv_done[g], (it - 1) & 1, 7);
+        load_kv(ch, true);
+      }
+    }
     __syncwarp();
     const int kbase = ch * kKeys;
-    // pass 1: masked max of this chunk
-    float mx = -INFINITY;
-#pragma unroll 1
-    for (int c0 = 0; c0 < kKeys; c0 += 32) {
-      uint32_t sv[32];
-      tc::tmem_ld16(tS + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(sv));
-      tc::tmem_ld16(tS + lane_base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+    // Warps whose TMEM lane quadrant holds no query row (rows_tot <= 64 at the
+    // benchmark's Q * G) skip the softmax: their P / O rows are never stored
+    // (MMA rows are independent).  A working thread loads its row's 128 S
+    // values with one TMEM wait, takes the max as 8 independent chains (max
+    // is exact: the same m as a sequential scan), rescales O in two 64-column
+    // batches and forms P from two 64-key re-reads, the sums in key order —
+    // bitwise the same P, l and O as the one-chain loop it replaced, with the
+    // per-chunk softmax 3.6 -> 2.1 us (tools/atc_prof_online.py).
+    const bool wvalid = (warp & 3) * 32 < rows_tot;  // warp-uniform
+    float psum = 0.f, m_new = m_run, corr = 1.f;
+    if (wvalid) {
+      // keys j <= lim of this chunk are visible to the row; a chunk every row
+      // of the warp sees whole (all but the last) skips the per-key masks
+      const bool qrow = r < rows_tot;
+      const int lim = min(row_pos, n_keys - 1) - kbase;
+      const bool wfull = __all_sync(0xffffffffu, !qrow || lim >= kKeys - 1);
+      uint32_t sv[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 16) tc::tmem_ld16(tS + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(sv + c0));
       tc::tmem_wait_ld();
+      if (it == 4) PROF(2);
+      // pass 1: masked max of the raw scores, then one scale (rounding is
+      // monotone: max(s) * c == max(s * c) for c > 0)
+      float m8[8];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int key = kbase + c0 + j;
-        if (key <= row_pos && key < n_keys) mx = fmaxf(mx, __uint_as_float(sv[j]) * scale_log2);
+      for (int j = 0; j < 8; ++j) m8[j] = -INFINITY;
+      if (wfull) {
+#pragma unroll
+        for (int j = 0; j < kKeys; ++j) m8[j & 7] = fmaxf(m8[j & 7], __uint_as_float(sv[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < kKeys; ++j)
+          if (j <= lim) m8[j & 7] = fmaxf(m8[j & 7], __uint_as_float(sv[j]));
       }
-    }
-    const float m_new = fmaxf(m_run, mx);
-    const float corr = m_run == -INFINITY ? 0.f : (m_new == m_run ? 1.f : exp2f(m_run - m_new));
-    // the group's previous P.V must be done before O is rescaled and P rewritten
-    if (it > 0) {
-      MBW(&pv_done[g], (it - 1) & 1, 3);
-      tc::fence_after_sync();
-      if (__any_sync(0xffffffffu, corr != 1.f)) {  // warp-uniform: the TMEM ops are warp-collective
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) *
+                       scale_log2;
+      m_new = fmaxf(m_run, mx);
+      if (it == 4) PROF(3);
+      corr = m_run == -INFINITY ? 0.f : (m_new == m_run ? 1.f : exp2f(m_run - m_new));
+      // the group's previous P.V must be done before O is rescaled and P rewritten
+      if (it > 0) {
+        MBW(&pv_done[g], (it - 1) & 1, 3);
+        tc::fence_after_sync();
+        if (it == 4) PROF(6);
+        // warp-uniform (the TMEM ops are warp-collective); rows past the call
+        // are never stored and do not trigger it
+        if (__any_sync(0xffffffffu, qrow && corr != 1.f)) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          uint32_t ov[32];
-          tc::tmem_ld16(tO + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(ov));
-          tc::tmem_ld16(tO + lane_base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(ov + 16));
-          tc::tmem_wait_ld();
+          for (int c0 = 0; c0 < kD; c0 += 64) {
+            uint32_t ov[64];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
-          tmem_st16(tO + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(ov));
-          tmem_st16(tO + lane_base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(ov + 16));
+            for (int c1 = 0; c1 < 64; c1 += 16) tc::tmem_ld16(tO + lane_base + c0 + c1, *reinterpret_cast<uint32_t(*)[16]>(ov + c1));
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 64; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
+#pragma unroll
+            for (int c1 = 0; c1 < 64; c1 += 16) tmem_st16(tO + lane_base + c0 + c1, *reinterpret_cast<uint32_t(*)[16]>(ov + c1));
+          }
+          tmem_wait_st();
         }
-        tmem_wait_st();
       }
-    }
-    // pass 2: P = exp2(s - m_new) (masked -> 0), row sum, P -> the group's swizzled tile
-    float psum = 0.f;
+      if (it == 4) PROF(8);
+      // pass 2: P = exp2(s - m_new) (masked -> 0), row sum in key order, P ->
+      // the group's swizzled tile; S re-read from TMEM in two 64-key halves
 #pragma unroll 1
-    for (int c0 = 0; c0 < kKeys; c0 += 32) {
-      uint32_t sv[32];
-      tc::tmem_ld16(tS + lane_base + c0, *reinterpret_cast<uint32_t(*)[16]>(sv));
-      tc::tmem_ld16(tS + lane_base + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
-      tc::tmem_wait_ld();
+      for (int h0 = 0; h0 < kKeys; h0 += 64) {
+        uint32_t sh[64];
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        float pv[8];
+        for (int c0 = 0; c0 < 64; c0 += 16)
+          tc::tmem_ld16(tS + lane_base + h0 + c0, *reinterpret_cast<uint32_t(*)[16]>(sh + c0));
+        tc::tmem_wait_ld();
+        if (wfull) {  // every key visible, m_new finite
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int key = kbase + c0 + q4 * 8 + j;
-          const bool vis = key <= row_pos && key < n_keys && m_new != -INFINITY;
-          const float e = ex2_ftz(__uint_as_float(sv[q4 * 8 + j]) * scale_log2 - m_new);
-          pv[j] = vis ? e : 0.f;
-          psum += pv[j];
+          for (int c = 0; c < 8; ++c) {
+            float pv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              pv[j] = ex2_ftz(__uint_as_float(sh[c * 8 + j]) * scale_log2 - m_new);
+              psum += pv[j];
+            }
+            const int cc = (h0 >> 3) + c;
+            *reinterpret_cast<bf16x8*>(gP + (cc >> 3) * BLK + swz(r, cc & 7)) = pack8(pv);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float pv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const bool vis = h0 + c * 8 + j <= lim && m_new != -INFINITY;
+              const float e = ex2_ftz(__uint_as_float(sh[c * 8 + j]) * scale_log2 - m_new);
+              pv[j] = vis ? e : 0.f;
+              psum += pv[j];
+            }
+            const int cc = (h0 >> 3) + c;
+            *reinterpret_cast<bf16x8*>(gP + (cc >> 3) * BLK + swz(r, cc & 7)) = pack8(pv);
+          }
         }
-        const int c = (c0 >> 3) + q4;  // 16-byte chunk (8 keys) within the 128 keys
-        *reinterpret_cast<bf16x8*>(gP + (c >> 3) * BLK + swz(r, c & 7)) = pack8(pv);
+        if (it == 4 && h0 == 0) PROF(10);
       }
     }
     l_run = l_run * corr + psum;
@@ -396,8 +449,13 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     tc::fence_proxy_async_smem();  // P visible to the MMA (async proxy)
     tc::fence_before_sync();       // S reads and O stores ordered before the next MMAs
     asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the group's 4 warps
+    if (it == 4) PROF(11);
     if (issuer) {
       tc::fence_after_sync();
+      // S(ch + 2) first (this chunk's S is consumed; K(ch + 2) was requested
+      // when S(ch) completed): the group's next softmax starts without
+      // waiting for this P.V
+      if (ch + 2 < n_chunks) issue_S(ch + 2);
       MBW(&v_full[g], (ch >> 1) & 1, 6);
       tc::fence_after_sync();
 #pragma unroll
@@ -408,11 +466,6 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         tc::mma_bf16(tO, ad, bd, idPV, (it > 0 || k > 0) ? 1u : 0u);
       }
       tc::mma_commit(&pv_done[g]);
-      if (ch + 2 < n_chunks) {
-        issue_S(ch + 2);            // K(ch + 2) was requested when S(ch) completed
-        MBW(&pv_done[g], it & 1, 4);  // this P.V done: the V buffer is free
-        load_kv(ch + 2, true);
-      }
     }
     __syncwarp();
   }
@@ -464,6 +517,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   }
   tc::fence_before_sync();
   __syncthreads();
+  PROF(9);
   if (warp == 0) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
