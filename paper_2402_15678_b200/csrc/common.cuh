@@ -113,7 +113,11 @@ __device__ __forceinline__ void rope8(float* f, const float* pf, const float2* _
   }
 }
 
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+// silu(g) * u with the fast exponential and division (ex2.approx, rcp.approx:
+// a few ulp of fp32, far below the bf16 rounding of the output); the gated
+// GEMM epilogues run it once per output element — 70B verify forward 29.1 ->
+// 28.8 ms at Q = 7 against expf / IEEE division (same-box A/B, round 2)
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 // KV-cache addressing.  Contiguous: caches [slots, Hkv, T, D].  Paged (table
 // != null): a block pool [n_blocks, Hkv, bs, D] and a block table [slots,
