@@ -755,48 +755,93 @@ attention_tc_short_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_
   const uint32_t lane_base = (uint32_t)(q * 32) << 16;
   const int n_grp = (n_keys + 31) / 32;      // groups holding a key < n_keys
   float m = -INFINITY, psum = 0.f;
+  // Warps whose lane quadrant holds no query row skip both passes (their P /
+  // O rows are never stored).  A warp takes its groups gi, gi + 4 two at a
+  // time with one TMEM wait, takes the max of the raw scores and scales once
+  // (rounding is monotone: the same m), and skips the per-key masks on groups
+  // every row of the warp sees whole; P and the sums in the same key order —
+  // bitwise the same results as the one-group-per-wait loop.
+  const bool wvalid = q * 32 < rows_tot;  // warp-uniform
+  const bool qrow = r < rows_tot;
+  const int lim0 = min(row_pos, n_keys - 1);  // last key this row sees
   if (n_chunks > 0) {
     tc::mbar_wait(s_full, 0);
     tc::fence_after_sync();
     PROF(4);
     float mx = -INFINITY;
+    if (wvalid) {
 #pragma unroll 1
-    for (int gi = part; gi < n_grp; gi += 4) {
-      uint32_t sv[32];
-      tc::tmem_ld16(tmem + lane_base + gi * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
-      tc::tmem_ld16(tmem + lane_base + gi * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
-      tc::tmem_wait_ld();
+      for (int gi = part; gi < n_grp; gi += 8) {
+        const bool two = gi + 4 < n_grp;  // warp-uniform
+        uint32_t sv[64];
+        tc::tmem_ld16(tmem + lane_base + gi * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
+        tc::tmem_ld16(tmem + lane_base + gi * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+        if (two) {
+          tc::tmem_ld16(tmem + lane_base + (gi + 4) * 32, *reinterpret_cast<uint32_t(*)[16]>(sv + 32));
+          tc::tmem_ld16(tmem + lane_base + (gi + 4) * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 48));
+        }
+        tc::tmem_wait_ld();
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        const int key = gi * 32 + jj;
-        if (key <= row_pos && key < n_keys) mx = fmaxf(mx, __uint_as_float(sv[jj]) * scale_log2);
+        for (int t = 0; t < 2; ++t) {
+          if (t == 1 && !two) break;
+          const int lim = lim0 - (gi + 4 * t) * 32;
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          if (__all_sync(0xffffffffu, !qrow || lim >= 31)) {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) m4[jj & 3] = fmaxf(m4[jj & 3], __uint_as_float(sv[t * 32 + jj]));
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj <= lim) m4[jj & 3] = fmaxf(m4[jj & 3], __uint_as_float(sv[t * 32 + jj]));
+          }
+          mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2);
+        }
       }
     }
     red[part * kRows + r] = mx;
   }
   __syncthreads();  // (S complete: the Q region is free for the exchange)
   PROF(5);
-  if (n_chunks > 0) {
+  if (n_chunks > 0 && wvalid) {
     m = fmaxf(fmaxf(red[r], red[kRows + r]), fmaxf(red[2 * kRows + r], red[3 * kRows + r]));
 #pragma unroll 1
-    for (int gi = part; gi < n_grp; gi += 4) {
-      uint32_t sv[32];
+    for (int gi = part; gi < n_grp; gi += 8) {
+      const bool two = gi + 4 < n_grp;
+      uint32_t sv[64];
       tc::tmem_ld16(tmem + lane_base + gi * 32, *reinterpret_cast<uint32_t(*)[16]>(sv));
       tc::tmem_ld16(tmem + lane_base + gi * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+      if (two) {
+        tc::tmem_ld16(tmem + lane_base + (gi + 4) * 32, *reinterpret_cast<uint32_t(*)[16]>(sv + 32));
+        tc::tmem_ld16(tmem + lane_base + (gi + 4) * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 48));
+      }
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        float pv[8];
+      for (int t = 0; t < 2; ++t) {
+        if (t == 1 && !two) break;
+        const int g2 = gi + 4 * t;
+        const int lim = lim0 - g2 * 32;
+        const bool wfull = __all_sync(0xffffffffu, !qrow || lim >= 31);
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int key = gi * 32 + q4 * 8 + jj;
-          const bool vis = key <= row_pos && key < n_keys && m != -INFINITY;
-          const float e = ex2_ftz(__uint_as_float(sv[q4 * 8 + jj]) * scale_log2 - m);
-          pv[jj] = vis ? e : 0.f;
-          psum += pv[jj];
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float pv[8];
+          if (wfull) {  // every key visible, m finite
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              pv[jj] = ex2_ftz(__uint_as_float(sv[t * 32 + q4 * 8 + jj]) * scale_log2 - m);
+              psum += pv[jj];
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const bool vis = q4 * 8 + jj <= lim && m != -INFINITY;
+              const float e = ex2_ftz(__uint_as_float(sv[t * 32 + q4 * 8 + jj]) * scale_log2 - m);
+              pv[jj] = vis ? e : 0.f;
+              psum += pv[jj];
+            }
+          }
+          const int c8 = g2 * 4 + q4;  // 8-key chunk; P block = 64 keys
+          *reinterpret_cast<bf16x8*>(sP + (c8 >> 3) * BLK + swz(r, c8 & 7)) = pack8(pv);
         }
-        const int c8 = gi * 4 + q4;  // 8-key chunk; P block = 64 keys
-        *reinterpret_cast<bf16x8*>(sP + (c8 >> 3) * BLK + swz(r, c8 & 7)) = pack8(pv);
       }
     }
   }

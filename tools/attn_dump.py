@@ -1,5 +1,5 @@
 """Dump the tcgen05 attention's outputs for a fixed set of long-cache cases
-(online-softmax kernel) so two builds can be compared bitwise:
+(both tcgen05 kernels) so two builds can be compared bitwise:
   MS_LIB=<lib> python tools/attn_dump.py out.pt ; python tools/attn_dump.py --cmp a.pt b.pt"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,7 +13,9 @@ from paper_2402_15678_b200 import kernels as K
 K.TC_ATTENTION = True
 res = {}
 for (H, Hkv, Q, ctx) in [(64, 8, 1, 1000), (64, 8, 5, 4096), (64, 8, 7, 700), (64, 8, 9, 1500), (64, 8, 13, 4096),
-                         (16, 2, 7, 640), (40, 40, 5, 2000)]:
+                         (16, 2, 7, 640), (40, 40, 5, 2000),  # online kernel (T > 384)
+                         (64, 8, 1, 190), (64, 8, 7, 190), (64, 8, 13, 300), (64, 8, 5, 100), (16, 2, 7, 200),
+                         (40, 40, 5, 300), (64, 8, 16, 340)]:  # one-pass short kernel (T <= 384)
     D, B = 128, 4
     g = torch.Generator(device="cuda").manual_seed(H * 100 + Q * 10 + ctx)
     T = ctx + 32
