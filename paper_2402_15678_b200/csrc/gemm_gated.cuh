@@ -31,10 +31,15 @@ struct GatedCfg {
   static constexpr int MAX_SX = 4;
   static constexpr int ACC = BN <= 32 ? 32 : BN <= 64 ? 64 : 128;
   static constexpr int TMEM_COLS = 2 * ACC;
-  static constexpr int U_BYTES = 32 * 64 * 4;  // one 32-column chunk of the up half, fp32
+  static constexpr int U_CHUNK = 32 * 64 * 4;  // one 32-column chunk of the up half, fp32
+  // two chunk buffers (the up warps park chunk i + 1 while the gate warps
+  // still read chunk i: one barrier per chunk) where two CTAs per SM still fit
+  // beside the ring; BN = 128 keeps one (two barriers per chunk)
+  static constexpr int U_BUFS = BN <= 112 ? 2 : 1;
+  static constexpr int U_BYTES = U_BUFS * U_CHUNK;
   static constexpr int NBAR = 2 * MAX_SW + 2 * MAX_SX + 4;
   __host__ __device__ static void rings(int* sw, int* sx) {
-    const int budget = 104 * 1024 - U_BYTES;  // two CTAs per SM
+    const int budget = 104 * 1024 - U_CHUNK;  // two CTAs per SM
     int x = X_BYTES <= 8192 ? 3 : 2;
     int w = (budget - x * X_BYTES) / W_BYTES;
     *sw = w < 2 ? 2 : (w > MAX_SW ? MAX_SW : w);
@@ -183,14 +188,15 @@ linear_gated_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       }
     }
     epi_bar128();
-    int s = 0;
+    int s = 0, chunk = 0;  // chunk: running count over tiles (U buffer = chunk % U_BUFS)
     for (int t = c; t < p.n_tiles; t += P, ++s) {
       const int buf = s & 1;
       tc::mbar_wait(&tfull[buf], (s >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t trow = tmem + buf * C::ACC + ((uint32_t)(q * 32) << 16);
       __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)m0 * p.ldc + t * (kBM / 2) + fu;
-      for (int c0 = 0; c0 < m_hi; c0 += 32) {
+      for (int c0 = 0; c0 < m_hi; c0 += 32, ++chunk) {
+        float* Ub = U + (C::U_BUFS == 2 ? (chunk & 1) : 0) * (32 * 64);
         uint32_t r[32];
         tc::tmem_ld16(trow + c0, *reinterpret_cast<uint32_t(*)[16]>(r));
         tc::tmem_ld16(trow + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
@@ -198,17 +204,20 @@ linear_gated_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         if (up) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (c0 + j < m_hi) U[j * 64 + fu] = __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f);
+            if (c0 + j < m_hi) Ub[j * 64 + fu] = __uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f);
         }
+        // with two buffers this one barrier also orders the gate warps' reads
+        // of chunk - 2 (done before they arrived here) before its buffer is
+        // rewritten (after it)
         epi_bar128();
         if (!up) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (c0 + j < m_hi)
               ob[(int64_t)(c0 + j) * p.ldc] =
-                  f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f), U[j * 64 + fu]));
+                  f2bf(silu_mul(__uint_as_float(r[j]) * (p.rms_in ? s_rstd[c0 + j] : 1.f), Ub[j * 64 + fu]));
         }
-        epi_bar128();  // U is rewritten by the next chunk
+        if (C::U_BUFS == 1) epi_bar128();  // U is rewritten by the next chunk
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty[buf]);
