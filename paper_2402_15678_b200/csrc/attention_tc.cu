@@ -5,7 +5,8 @@
 //
 //   * the call's own K / V rows are appended to the cache (K rotated), then the
 //     cache is read in 128-key chunks by TMA (two 64-dim boxes per operand,
-//     128-byte swizzle), double-buffered;
+//     128-byte swizzle); long caches: one producer warp per key group issues
+//     its K (two buffers) and V (one buffer) loads as the buffers retire;
 //   * S = Q K^T on tcgen05 (M = 128 flattened rows — position i, group head j
 //     -> row i * G + j, Q staged RoPE-rotated into a swizzled K-major tile —,
 //     N = 128 keys, K = 128 dims), fp32 accumulator in TMEM;
@@ -16,7 +17,8 @@
 //     rescaled in place when the max moves), P written back as bf16 into a
 //     swizzled K-major tile;
 //   * O += P V on tcgen05 with V as the MN-major operand (keys along K, dims
-//     along N, straight from the TMA tile);
+//     along N, straight from the TMA tile); in the online kernel P stays in
+//     TMEM (bf16, over the consumed S columns) as the MMA's A operand;
 //   * the epilogue merges the two groups' (m, l, O) in group order through
 //     shared memory, divides by the row sum and stores bf16.
 //
@@ -41,16 +43,17 @@ constexpr int kD = 128;       // head dim
 constexpr int kRows = 128;    // MMA M: flattened (position, group head) rows
 constexpr int kKeys = 128;    // keys per chunk (MMA N of S, K of P.V)
 constexpr int kThreads = 256;  // two key groups (warpgroups) of 4 warps
+constexpr int kThreadsOnline = kThreads + 64;  // online kernel: + one K / V producer warp per group
 constexpr int BLK = kRows * 64 * 2;  // one [128 x 64] bf16 swizzled block = 16 KB
 
 struct Smem {
-  // all tiles 1024-byte aligned (128-byte swizzle atoms); buffer / tile g
-  // belongs to key group g (chunks ch with ch % 2 == g)
+  // all tiles 1024-byte aligned (128-byte swizzle atoms); buffers g* belong to
+  // key group g (chunks ch with ch % 2 == g).  P lives in TMEM (aliased onto
+  // the consumed S columns), which leaves room for two K buffers per group.
   static constexpr int Q_OFF = 0;                     // Q [128 rows x 128 dims] = 2 blocks
-  static constexpr int K_OFF = Q_OFF + 2 * BLK;       // K [2 groups][128 keys x 128 dims]
-  static constexpr int V_OFF = K_OFF + 4 * BLK;       // V [2 groups][128 keys x 128 dims]
-  static constexpr int P_OFF = V_OFF + 4 * BLK;       // P [2 groups][128 rows x 128 keys]
-  static constexpr int BAR_OFF = P_OFF + 4 * BLK;
+  static constexpr int K_OFF = Q_OFF + 2 * BLK;       // K [2 groups][2 buffers][128 keys x 128 dims]
+  static constexpr int V_OFF = K_OFF + 8 * BLK;       // V [2 groups][128 keys x 128 dims]
+  static constexpr int BAR_OFF = V_OFF + 4 * BLK;
   static constexpr int BYTES = BAR_OFF + 128 + 1024 + 1024;  // barriers, group 1 (m, l) per row, alignment slack
 };
 
@@ -63,6 +66,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D (TMEM) (+)= A (TMEM, M = 128 rows in lanes, K = 16 bf16 in 8 columns) x
+// B (shared memory descriptor): the P.V step with P kept in TMEM
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 #ifdef ATC_DEBUG
 // bounded wait: report the barrier that never completed and trap
@@ -123,7 +138,7 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(const void* base, uint32_t lbo
   return d;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsOnline, 1)
 attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                     const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
@@ -134,9 +149,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   uint8_t* sQ = sm + Smem::Q_OFF;
   uint8_t* sK = sm + Smem::K_OFF;
   uint8_t* sV = sm + Smem::V_OFF;
-  uint8_t* sP = sm + Smem::P_OFF;
-  uint64_t* k_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2 groups]
-  uint64_t* v_full = k_full + 2;                                       // [2]
+  uint64_t* k_full = reinterpret_cast<uint64_t*>(sm + Smem::BAR_OFF);  // [2 groups][2 buffers]
+  uint64_t* v_full = k_full + 4;                                       // [2]
   uint64_t* s_full = v_full + 2;                                       // [2]
   uint64_t* pv_done = s_full + 2;                                       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
@@ -145,9 +159,15 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   PROF(0);
   const int b = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int g = warp >> 2;          // key group
+  // warps 0-7: two key groups of 4 softmax warps; warps 8, 9: the K / V
+  // producers of group 0 / 1 (lane 0 issues the group's TMA loads in chunk
+  // order, each as soon as its buffer retires, so no softmax warp waits for
+  // a buffer to free)
+  const bool producer = warp >= 8;
+  const int g = producer ? warp - 8 : warp >> 2;  // key group
   const int gt = tid & 127;         // thread within the group = row (TMEM lane)
-  const bool issuer = gt == 0;      // the group's TMA / MMA thread
+  const bool issuer = !producer && gt == 0;        // the group's MMA thread
+  const bool loader = producer && (tid & 31) == 0;  // the group's TMA thread
   const int G = Hq / Hkv;
   const int rows_tot = Qtot * G;
   const int QD = Hq * kD, KVD = Hkv * kD;
@@ -159,8 +179,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   if (tid == 0) {
     tc::prefetch_tmap(&tmK);
     tc::prefetch_tmap(&tmV);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&k_full[i], 1);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&k_full[i], 1);
       tc::mbar_init(&v_full[i], 1);
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&pv_done[i], 1);
@@ -174,9 +194,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem + g * 128, tO = tmem + 256 + g * 128;
-  uint8_t* gK = sK + 2 * g * BLK;
   uint8_t* gV = sV + 2 * g * BLK;
-  uint8_t* gP = sP + 2 * g * BLK;
 
   // the cache rows of earlier calls (keys < pstart) do not depend on the
   // previous kernel: chunks made only of them are requested before the
@@ -185,23 +203,30 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // cache row of key 0
   const int n_keys = min(pstart + Qtot, T);
   const int n_chunks = (n_keys + kKeys - 1) / kKeys;
-  // K and V of a chunk on separate barriers: the group's K buffer is free once
-  // its S MMA is complete (refilled while the softmax runs), its V buffer once
-  // its P.V is complete (refilled while the next chunk's softmax runs)
-  auto load_kv = [&](int ch, bool v) {  // the issuer of group ch % 2
-    const int buf = ch & 1;
-    uint64_t* bar = v ? &v_full[buf] : &k_full[buf];
+  // K and V of a chunk on separate barriers.  A group's chunks are ch = g +
+  // 2i; K(ch) goes to the group's K buffer i % 2 (two per group: K(ch + 4) is
+  // requested when S(ch) completes, two chunks ahead of its use), V(ch) to
+  // the group's one V buffer (requested when P.V(ch - 2) retires)
+  auto kbuf = [&](int ch) { return sK + (2 * (ch & 1) + ((ch >> 1) & 1)) * 2 * BLK; };
+  auto kbar = [&](int ch) { return &k_full[2 * (ch & 1) + ((ch >> 1) & 1)]; };
+  auto load_kv = [&](int ch, bool v) {  // the loader of group ch % 2
+    uint64_t* bar = v ? &v_full[ch & 1] : kbar(ch);
+    uint8_t* dst = v ? sV + 2 * (ch & 1) * BLK : kbuf(ch);
     tc::mbar_arrive_expect_tx(bar, 2 * BLK);
     const int y = (int)(row0 + ch * kKeys);
     const uint64_t pol = tc::policy_evict_first();
     for (int half = 0; half < 2; ++half)
-      tc::tma_load_2d((v ? sV : sK) + (2 * buf + half) * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
+      tc::tma_load_2d(dst + half * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
   };
+  // chunks made only of cache rows of earlier calls are requested before the
+  // dependency wait; the others after the append below
   const bool early = g < n_chunks && (g + 1) * kKeys <= pstart;  // this group's first chunk is all cache
-  if (issuer && early) {
+  const bool early2 = g + 2 < n_chunks && (g + 3) * kKeys <= pstart;
+  if (loader && early) {
     load_kv(g, false);
     load_kv(g, true);
   }
+  if (loader && early2) load_kv(g + 2, false);
   pdl_wait();
   pdl_trigger();
 
@@ -243,57 +268,59 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       }
     }
   };
-#pragma unroll
-  for (int u = 0; u <= kQU; ++u) {
-    const __nv_bfloat16* src;
-    __nv_bfloat16* dst;
-    int r, j, p;
-    bool rot;
-    unit(u, src, dst, r, j, p, rot);
-    if (src) {
-      ux0[u] = *reinterpret_cast<const bf16x8*>(src);
-      ux1[u] = *reinterpret_cast<const bf16x8*>(src + 64);
-      if (rot) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (kD / 2) + 8 * j + k];
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u <= kQU; ++u) {
-    const __nv_bfloat16* src;
-    __nv_bfloat16* dst;
-    int r, j, p;
-    bool rot;
-    unit(u, src, dst, r, j, p, rot);
-    bf16x8 v0, v1;
-    if (src) {
-      v0 = ux0[u];
-      v1 = ux1[u];
-      if (rot) {
-        float f0[8], f1[8];
-        unpack8(v0, f0);
-        unpack8(v1, f1);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float2 t = ucs[u][k];
-          const float a = f0[k], c = f1[k];
-          f0[k] = a * t.x - c * t.y;
-          f1[k] = c * t.x + a * t.y;
+  if (!producer) {  // the producers take no staging units
+  #pragma unroll
+    for (int u = 0; u <= kQU; ++u) {
+      const __nv_bfloat16* src;
+      __nv_bfloat16* dst;
+      int r, j, p;
+      bool rot;
+      unit(u, src, dst, r, j, p, rot);
+      if (src) {
+        ux0[u] = *reinterpret_cast<const bf16x8*>(src);
+        ux1[u] = *reinterpret_cast<const bf16x8*>(src + 64);
+        if (rot) {
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (kD / 2) + 8 * j + k];
         }
-        v0 = pack8(f0);
-        v1 = pack8(f1);
       }
-    } else {
-      *reinterpret_cast<uint4*>(&v0) = make_uint4(0, 0, 0, 0);
-      v1 = v0;
     }
-    if (u < kQU) {
-      *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
-      *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
-    } else if (dst) {
-      *reinterpret_cast<bf16x8*>(dst) = v0;
-      *reinterpret_cast<bf16x8*>(dst + 64) = v1;
+  #pragma unroll
+    for (int u = 0; u <= kQU; ++u) {
+      const __nv_bfloat16* src;
+      __nv_bfloat16* dst;
+      int r, j, p;
+      bool rot;
+      unit(u, src, dst, r, j, p, rot);
+      bf16x8 v0, v1;
+      if (src) {
+        v0 = ux0[u];
+        v1 = ux1[u];
+        if (rot) {
+          float f0[8], f1[8];
+          unpack8(v0, f0);
+          unpack8(v1, f1);
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float2 t = ucs[u][k];
+            const float a = f0[k], c = f1[k];
+            f0[k] = a * t.x - c * t.y;
+            f1[k] = c * t.x + a * t.y;
+          }
+          v0 = pack8(f0);
+          v1 = pack8(f1);
+        }
+      } else {
+        *reinterpret_cast<uint4*>(&v0) = make_uint4(0, 0, 0, 0);
+        v1 = v0;
+      }
+      if (u < kQU) {
+        *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
+        *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
+      } else if (dst) {
+        *reinterpret_cast<bf16x8*>(dst) = v0;
+        *reinterpret_cast<bf16x8*>(dst + 64) = v1;
+      }
     }
   }
   if (fuse_append) asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -304,8 +331,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
   constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
   auto issue_S = [&](int ch) {  // the group's issuer: S = Q K_ch^T
-    MBW(&k_full[g], (ch >> 1) & 1, 1);
+    MBW(kbar(ch), (ch >> 2) & 1, 1);
     tc::fence_after_sync();
+    uint8_t* gK = kbuf(ch);
 #pragma unroll
     for (int k = 0; k < kD / 16; ++k) {
       const uint64_t ad = tc::smem_desc_sw128(sQ + (k >> 2) * BLK) + 2 * (k & 3);
@@ -314,14 +342,23 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     }
     tc::mma_commit(&s_full[g]);
   };
-  if (issuer && g < n_chunks) {
+  if (loader && g < n_chunks) {
     if (!early) {
       load_kv(g, false);
       load_kv(g, true);
     }
-    issue_S(g);
+    if (g + 2 < n_chunks && !early2) load_kv(g + 2, false);
+    // then every later chunk of the group in order: K(ch + 4) into the K
+    // buffer S(ch) retires, V(ch + 2) into the V buffer P.V(ch) retires
+    for (int ch = g, i = 0; ch + 2 < n_chunks; ch += 2, ++i) {
+      MBW(&s_full[g], i & 1, 8);
+      if (ch + 4 < n_chunks) load_kv(ch + 4, false);
+      MBW(&pv_done[g], i & 1, 9);
+      load_kv(ch + 2, true);
+    }
   }
-  __syncwarp();  // the issuer lane diverged: reconverge before the aligned tcgen05.ld
+  if (issuer && g < n_chunks) issue_S(g);
+  __syncwarp();  // the issuer / loader lanes diverged: reconverge before the aligned tcgen05.ld
 
   // softmax state of this thread's row (= TMEM lane gt) over its group's chunks
   const int r = gt;
@@ -329,19 +366,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   float m_run = -INFINITY, l_run = 0.f;
   const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   int it = 0;  // this group's chunk count so far
-  for (int ch = g; ch < n_chunks; ch += 2, ++it) {
+  for (int ch = g; !producer && ch < n_chunks; ch += 2, ++it) {
     MBW(&s_full[g], it & 1, 2);
     tc::fence_after_sync();
     if (it == 4) PROF(4);
     if (it == 8) PROF(5);
-    if (issuer) {
-      if (ch + 2 < n_chunks) load_kv(ch + 2, false);  // S(ch) done: the K buffer is free
-      if (it > 0) {  // P.V(ch - 2) (issued after S(ch)) done: the V buffer is free
-        MBW(&pv_done[g], (it - 1) & 1, 7);
-        load_kv(ch, true);
-      }
-    }
-    __syncwarp();
     const int kbase = ch * kKeys;
     // Warps whose TMEM lane quadrant holds no query row (rows_tot <= 64 at the
     // benchmark's Q * G) skip the softmax: their P / O rows are never stored
@@ -405,8 +434,10 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         }
       }
       if (it == 4) PROF(8);
-      // pass 2: P = exp2(s - m_new) (masked -> 0), row sum in key order, P ->
-      // the group's swizzled tile; S re-read from TMEM in two 64-key halves
+      // pass 2: P = exp2(s - m_new) (masked -> 0), row sum in key order; S
+      // re-read from TMEM in two 64-key halves and P (bf16, keys 2c / 2c + 1
+      // in column c) stored over the consumed S columns 0..63 — the P.V MMA
+      // reads it from TMEM
 #pragma unroll 1
       for (int h0 = 0; h0 < kKeys; h0 += 64) {
         uint32_t sh[64];
@@ -414,6 +445,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         for (int c0 = 0; c0 < 64; c0 += 16)
           tc::tmem_ld16(tS + lane_base + h0 + c0, *reinterpret_cast<uint32_t(*)[16]>(sh + c0));
         tc::tmem_wait_ld();
+        uint32_t pw[32];
         if (wfull) {  // every key visible, m_new finite
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -423,8 +455,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
               pv[j] = ex2_ftz(__uint_as_float(sh[c * 8 + j]) * scale_log2 - m_new);
               psum += pv[j];
             }
-            const int cc = (h0 >> 3) + c;
-            *reinterpret_cast<bf16x8*>(gP + (cc >> 3) * BLK + swz(r, cc & 7)) = pack8(pv);
+            const bf16x8 b8 = pack8(pv);
+            const uint4 u = *reinterpret_cast<const uint4*>(&b8);
+            pw[4 * c] = u.x; pw[4 * c + 1] = u.y; pw[4 * c + 2] = u.z; pw[4 * c + 3] = u.w;
           }
         } else {
 #pragma unroll
@@ -437,35 +470,37 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
               pv[j] = vis ? e : 0.f;
               psum += pv[j];
             }
-            const int cc = (h0 >> 3) + c;
-            *reinterpret_cast<bf16x8*>(gP + (cc >> 3) * BLK + swz(r, cc & 7)) = pack8(pv);
+            const bf16x8 b8 = pack8(pv);
+            const uint4 u = *reinterpret_cast<const uint4*>(&b8);
+            pw[4 * c] = u.x; pw[4 * c + 1] = u.y; pw[4 * c + 2] = u.z; pw[4 * c + 3] = u.w;
           }
         }
+        tmem_st16(tS + lane_base + (h0 >> 1), *reinterpret_cast<uint32_t(*)[16]>(pw));
+        tmem_st16(tS + lane_base + (h0 >> 1) + 16, *reinterpret_cast<uint32_t(*)[16]>(pw + 16));
         if (it == 4 && h0 == 0) PROF(10);
       }
+      tmem_wait_st();
     }
     l_run = l_run * corr + psum;
     m_run = m_new;
-    tc::fence_proxy_async_smem();  // P visible to the MMA (async proxy)
-    tc::fence_before_sync();       // S reads and O stores ordered before the next MMAs
+    tc::fence_before_sync();  // P stores (TMEM) and O stores ordered before the next MMAs
     asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the group's 4 warps
     if (it == 4) PROF(11);
     if (issuer) {
       tc::fence_after_sync();
-      // S(ch + 2) first (this chunk's S is consumed; K(ch + 2) was requested
-      // when S(ch) completed): the group's next softmax starts without
-      // waiting for this P.V
-      if (ch + 2 < n_chunks) issue_S(ch + 2);
       MBW(&v_full[g], (ch >> 1) & 1, 6);
       tc::fence_after_sync();
 #pragma unroll
       for (int k = 0; k < kKeys / 16; ++k) {
-        const uint64_t ad = tc::smem_desc_sw128(gP + (k >> 2) * BLK) + 2 * (k & 3);
-        // V rows 16k..16k+15 (2048 bytes per 16 keys), the two 64-dim boxes BLK apart
+        // A = P from TMEM (8 columns per 16 keys); V rows 16k..16k+15 (2048
+        // bytes per 16 keys), the two 64-dim boxes BLK apart
         const uint64_t bd = desc_mn_sw128(gV + k * 2048, BLK);
-        tc::mma_bf16(tO, ad, bd, idPV, (it > 0 || k > 0) ? 1u : 0u);
+        mma_bf16_ts(tO, tS + 8 * k, bd, idPV, (it > 0 || k > 0) ? 1u : 0u);
       }
       tc::mma_commit(&pv_done[g]);
+      // S(ch + 2) after the P.V that reads P from the same columns (the MMAs
+      // of one thread run in issue order); K(ch + 2) landed an iteration ago
+      if (ch + 2 < n_chunks) issue_S(ch + 2);
     }
     __syncwarp();
   }
@@ -477,13 +512,13 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     MBW(&pv_done[g], (nit - 1) & 1, 5);
     tc::fence_after_sync();
   }
-  if (g == 1) {
+  if (!producer && g == 1) {
     stat[2 * r] = nit > 0 ? m_run : -INFINITY;
     stat[2 * r + 1] = nit > 0 ? l_run : 0.f;
   }
   tc::fence_before_sync();
   __syncthreads();  // every P.V of both groups is complete
-  if (g == 0) {
+  if (!producer && g == 0) {
     tc::fence_after_sync();
     const float m1 = stat[2 * r], l1 = stat[2 * r + 1];
     const bool has1 = n_chunks > 1;  // group 1 wrote O1
@@ -969,7 +1004,7 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
                   (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                   (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
                   (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);
-  return launch(atc::attention_tc_kernel, dim3(B, Hkv), dim3(atc::kThreads), atc::Smem::BYTES,
+  return launch(atc::attention_tc_kernel, dim3(B, Hkv), dim3(atc::kThreadsOnline), atc::Smem::BYTES,
                 (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
                 (const float2*)rope, (__nv_bfloat16*)out, ldo);

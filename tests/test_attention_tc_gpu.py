@@ -55,7 +55,7 @@ def test_tc_attention_vs_reference(H, Hkv, Q, T, rope):
         torch.testing.assert_close(vcd[b, :, p0:p0 + Q].cpu().float().transpose(0, 1), vn, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("T", [272, 400])
+@pytest.mark.parametrize("T", [272, 400, 1500])
 def test_tc_attention_batch_invariant(T):
     """Row (request b, position i) equals the same row computed with Q = i + 1
     (a shorter verify of the same prefix) and with the request alone — for the
@@ -66,7 +66,9 @@ def test_tc_attention_batch_invariant(T):
     kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     vc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
     qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g).to(BF)
-    start = torch.tensor([122, 250], dtype=torch.int32)  # request 0's rows cross a 128-key chunk
+    # request 0's rows cross a 128-key chunk; at T = 1500 request 1 sees full
+    # chunks (the online kernel's mask-free path) and a partial last one
+    start = torch.tensor([122, 250 if T < 1000 else 1400], dtype=torch.int32)
     table = llama_ref.rope_table(T + 4, D, 10000.0)
     full = _run(qkv, B, Q, H, Hkv, D, start, kc.cuda(), vc.cuda(), table).cpu()
     q3 = qkv.view(B, Q, -1)[:, :4].reshape(B * 4, -1).contiguous()
