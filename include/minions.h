@@ -418,7 +418,8 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
                      const float* rope, float scale, int scale_q, float* out, int64_t ldo, void* stream);
 
 /* Grouped-query attention of Q <= 16 query positions per request on tcgen05
- * (head dim 128, Q * H / Hkv <= 128 flattened rows): K / V read by TMA in
+ * (head dim 128, H % Hkv == 0 — multi-head G = 1 accepted —, Q * H / Hkv <=
+ * 128 flattened rows): K / V read by TMA in
  * 128-key chunks, S = Q K^T and P V on tcgen05 with TMEM accumulators, K/V
  * append fused (append != 0).  T <= 384: one pass over the whole context;
  * longer caches: online softmax over chunks.  Cache: contiguous
