@@ -143,7 +143,8 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
                     const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
                     const int32_t* __restrict__ slot, const int32_t* __restrict__ start, int T,
                     __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, float scale_log2,
-                    int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+                    int fuse_append, const float2* __restrict__ rope, __nv_bfloat16* __restrict__ out, int64_t ldo,
+                    const int32_t* __restrict__ block_table, int max_blocks, int bs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = sm + Smem::Q_OFF;
@@ -169,12 +170,20 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const bool issuer = !producer && gt == 0;        // the group's MMA thread
   const bool loader = producer && (tid & 31) == 0;  // the group's TMA thread
   const int G = Hq / Hkv;
-  const int rows_tot = Qtot * G;
+  // query tile (prompt prefill: Qtot > 16 or Qtot * G > 128 — one CTA per
+  // (request, KV head, Qt positions), the call's K / V appended beforehand):
+  // positions q0 .. q0 + Qc - 1 of the call; decode / verify: one tile
+  const int Qt = kRows / G;
+  const int q0 = blockIdx.z * Qt;
+  const int Qc = min(Qt, Qtot - q0);
+  const int64_t qrow0 = (int64_t)blockIdx.x * Qtot + q0;  // qkv / out row of the tile's first position
+  const int rows_tot = Qc * G;
   const int QD = Hq * kD, KVD = Hkv * kD;
 
   // start / slot come from kernels complete before the previous one (the
   // round's upload): read first, their latency hidden by the setup below
-  const int pstart = start[b];
+  const int pcall = start[b];       // position of the call's first query
+  const int pstart = pcall + q0;    // ... and of this tile's
   const int kv_slot = slot[b];
   if (tid == 0) {
     tc::prefetch_tmap(&tmK);
@@ -201,7 +210,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   // programmatic-dependency wait and the append (start / slot come from
   // earlier kernels, complete by then)
   const int64_t row0 = ((int64_t)kv_slot * Hkv + h) * T;  // cache row of key 0
-  const int n_keys = min(pstart + Qtot, T);
+  const int n_keys = min(pstart + Qc, T);
   const int n_chunks = (n_keys + kKeys - 1) / kKeys;
   // K and V of a chunk on separate barriers.  A group's chunks are ch = g +
   // 2i; K(ch) goes to the group's K buffer i % 2 (two per group: K(ch + 4) is
@@ -213,15 +222,28 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     uint64_t* bar = v ? &v_full[ch & 1] : kbar(ch);
     uint8_t* dst = v ? sV + 2 * (ch & 1) * BLK : kbuf(ch);
     tc::mbar_arrive_expect_tx(bar, 2 * BLK);
-    const int y = (int)(row0 + ch * kKeys);
     const uint64_t pol = tc::policy_evict_first();
-    for (int half = 0; half < 2; ++half)
-      tc::tma_load_2d(dst + half * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
+    if (!block_table) {
+      const int y = (int)(row0 + ch * kKeys);
+      for (int half = 0; half < 2; ++half)
+        tc::tma_load_2d(dst + half * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
+    } else {  // paged (prefill tiles): one box of bs rows per block; blocks past
+              // the table repeat its last block (finite rows, masked keys)
+      const int nb = kKeys / bs;
+      for (int j = 0; j < nb; ++j) {
+        const int t = min(ch * kKeys + j * bs, T - bs);
+        const int y = (int)(((int64_t)block_table[(int64_t)kv_slot * max_blocks + t / bs] * Hkv + h) * bs);
+        for (int half = 0; half < 2; ++half)
+          tc::tma_load_2d(dst + half * BLK + j * (BLK / nb), v ? &tmV : &tmK, bar, half * 64, y, pol);
+      }
+    }
   };
   // chunks made only of cache rows of earlier calls are requested before the
   // dependency wait; the others after the append below
-  const bool early = g < n_chunks && (g + 1) * kKeys <= pstart;  // this group's first chunk is all cache
-  const bool early2 = g + 2 < n_chunks && (g + 3) * kKeys <= pstart;
+  // (keys below pcall: earlier calls' rows; the call's own rows come from
+  // the append, in this kernel or the one before it)
+  const bool early = g < n_chunks && (g + 1) * kKeys <= pcall;  // this group's first chunk is all cache
+  const bool early2 = g + 2 < n_chunks && (g + 3) * kKeys <= pcall;
   if (loader && early) {
     load_kv(g, false);
     load_kv(g, true);
@@ -251,7 +273,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       j = e & 7;
       p = pstart + r / G;
       if (r < rows_tot) {
-        src = qkv + (int64_t)(b * Qtot + r / G) * ldq + (h * G + r % G) * kD + 8 * j;
+        src = qkv + (qrow0 + r / G) * ldq + (h * G + r % G) * kD + 8 * j;
         rot = rope != nullptr;
       }
     } else if (tid < n_app) {  // append unit: K rows, then V rows
@@ -528,7 +550,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     const float L = l_run * a0 + l1 * a1;
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const uint32_t tO1 = tmem + 384;
-    __nv_bfloat16* op = out + (int64_t)(b * Qtot + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * kD;
+    __nv_bfloat16* op = out + (qrow0 + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * kD;
 #pragma unroll 1
     for (int c0 = 0; c0 < kD; c0 += 16) {
       uint32_t o0[16], o1[16];
@@ -978,10 +1000,16 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
                                const int32_t* block_table, int max_blocks, int block_size, void* stream) {
   using namespace ms;
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || T < 1 || n_slots < 1 || H % Hkv) return MS_ERR_VALUE;
-  if (D != atc::kD || Q * (H / Hkv) > atc::kRows || Q > 16) return MS_ERR_UNSUPPORTED;
+  if (D != atc::kD) return MS_ERR_UNSUPPORTED;
+  // prompt prefill (more positions than one 128-row tile or 16): query tiles
+  // of the online kernel; the K / V rows must already be in the cache
+  const bool tiles = Q * (H / Hkv) > atc::kRows || Q > 16;
+  if (tiles && append) return MS_ERR_UNSUPPORTED;
   if (block_table && (block_size < 16 || atc::kKeys % block_size || max_blocks < 1 || T != max_blocks * block_size))
     return MS_ERR_VALUE;
-  if (block_table && T > atc::kShortKeys) return MS_ERR_UNSUPPORTED;  // paged: the one-pass kernel only
+  // paged with a fused append: the one-pass kernel only (prefill tiles read
+  // a paged cache the append kernel has written)
+  if (block_table && !tiles && T > atc::kShortKeys) return MS_ERR_UNSUPPORTED;
   if (B == 0) return MS_OK;
   if (!qkv || !slot || !start || !k_cache || !v_cache || !out || ldq % 8 || ldo % 8) return MS_ERR_VALUE;
   // contiguous: n_slots slots of T rows per KV head; paged: n_slots pool blocks of block_size rows
@@ -998,14 +1026,16 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
       return MS_ERR_CUDA;
     attr = true;
   }
-  // the kernel is chosen by the cache length T, never by Q (batch invariance)
-  if (T <= atc::kShortKeys)
+  // the kernel is chosen by the cache length T, never by Q (batch invariance);
+  // prefill tiles always take the online kernel
+  if (T <= atc::kShortKeys && !tiles)
     return launch(atc::attention_tc_short_kernel, dim3(B, Hkv), dim3(atc::kShortThreads), atc::SmemShort::BYTES,
                   (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                   (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
                   (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);
-  return launch(atc::attention_tc_kernel, dim3(B, Hkv), dim3(atc::kThreadsOnline), atc::Smem::BYTES,
+  const int qt = atc::kRows / (H / Hkv);
+  return launch(atc::attention_tc_kernel, dim3(B, Hkv, (Q + qt - 1) / qt), dim3(atc::kThreadsOnline), atc::Smem::BYTES,
                 (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
-                (const float2*)rope, (__nv_bfloat16*)out, ldo);
+                (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);
 }

@@ -224,6 +224,10 @@ class AttnWorkspace:
 # tile nearly empty while the row kernel's 640 CTAs stream 4.9 TB/s);
 # False: the row kernel.  Chosen by shape and cache length, never by Q alone.
 TC_ATTENTION: bool | str = "auto"
+# prompt-prefill calls (more than 16 positions or 128 flattened rows, head
+# dim 128, contiguous caches, GQA and multi-head alike): append, then the
+# online kernel in 128-row query tiles
+TC_PREFILL = True
 TC_SHORT_KEYS = 384
 
 
@@ -246,6 +250,25 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
     use_tc = TC_ATTENTION in (True, "auto")
+    if (use_tc and TC_PREFILL and (Q > 16 or Q * (H // Hkv) > 128) and D == 128 and ws is None
+            and (page is None or (page[1] % 16 == 0 and 128 % page[1] == 0))
+            and k_cache.is_contiguous() and v_cache.is_contiguous()):
+        # prompt prefill: the call's K / V rows appended first, then query
+        # tiles of the online tcgen05 kernel (128 rows each) read them back
+        # (contiguous or paged alike, so the two stay bitwise equal)
+        tab = None if page is None else _dev.ptr(page[0], torch.int32, "block_table")
+        if append:
+            _native.call("ms_kv_append_paged", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
+                         _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, _dev.ptr(k_cache, BF16),
+                         _dev.ptr(v_cache, BF16), None if rope is None else rope.data_ptr(), tab,
+                         0 if page is None else page[0].shape[1], 0 if page is None else page[1],
+                         _dev.stream_ptr(stream))
+        _native.call("ms_attention_tc", qkv.data_ptr(), qkv.stride(0), B, Q, H, Hkv, D,
+                     _dev.ptr(slot, torch.int32), _dev.ptr(start, torch.int32), T, k_cache.shape[0],
+                     _dev.ptr(k_cache, BF16), _dev.ptr(v_cache, BF16), None if rope is None else rope.data_ptr(),
+                     scale, 0, out.data_ptr(), out.stride(0), tab, 0 if page is None else page[0].shape[1],
+                     0 if page is None else page[1], _dev.stream_ptr(stream))
+        return out
     if page is not None:  # paged pools: the one-pass kernel, 16..128-row blocks
         use_tc = use_tc and T <= TC_SHORT_KEYS and page[1] % 16 == 0 and 128 % page[1] == 0
     if (use_tc and (Hkv < H or TC_ATTENTION is True) and D == 128 and ws is None and Q <= 16

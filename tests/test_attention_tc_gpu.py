@@ -77,3 +77,44 @@ def test_tc_attention_batch_invariant(T):
     one = _run(qkv.view(B, Q, -1)[1].contiguous(), 1, Q, H, Hkv, D, start[1:], kc[1:].contiguous().cuda(),
                vc[1:].contiguous().cuda(), table).cpu()
     assert torch.equal(one, full.view(B, Q, -1)[1])
+
+
+@pytest.mark.parametrize("H,Hkv,Q,T,starts", [(64, 8, 100, 300, [0, 60]), (40, 40, 300, 700, [0, 350]),
+                                              (16, 2, 200, 1100, [0, 800]), (40, 40, 130, 4300, [4000, 0])])
+def test_tc_attention_prefill_tiles_vs_reference(H, Hkv, Q, T, starts):
+    """Prompt-prefill calls (Q > 16 or Q * G > 128): the K / V rows appended,
+    then 128-row query tiles of the online kernel — against the fp32
+    restatement, GQA and multi-head, tiles crossing 128-key chunks."""
+    D = 128
+    B = len(starts)
+    g = torch.Generator().manual_seed(H + Q + T)
+    kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
+    vc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
+    qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, generator=g).to(BF)
+    start = torch.tensor(starts, dtype=torch.int32)
+    table = llama_ref.rope_table(T + 4, D, 10000.0)
+    kcd, vcd = kc.cuda(), vc.cuda()
+    got = _run(qkv, B, Q, H, Hkv, D, start, kcd, vcd, table).cpu().float()
+    want = _ref_attention(qkv, kc, vc, start, B, Q, H, Hkv, D, table)
+    torch.testing.assert_close(got, want, rtol=2e-2, atol=2e-2)
+    for b in range(B):
+        p0 = int(start[b])
+        vn = qkv.float().view(B, Q, -1)[b, :, (H + Hkv) * D:].view(Q, Hkv, D)
+        torch.testing.assert_close(vcd[b, :, p0:p0 + Q].cpu().float().transpose(0, 1), vn, rtol=0, atol=0)
+
+
+def test_tc_attention_prefill_chunked_equals_whole():
+    """A prompt prefilled in two calls gives bitwise the rows of one call
+    (a row's arithmetic depends only on its position and keys)."""
+    H, Hkv, D, T, P = 40, 40, 128, 640, 500
+    g = torch.Generator().manual_seed(7)
+    qkv = torch.randn(P, (H + 2 * Hkv) * D, generator=g).to(BF)
+    table = llama_ref.rope_table(T + 4, D, 10000.0)
+    z = torch.zeros(1, Hkv, T, D, dtype=BF)
+    kc1, vc1 = z.clone().cuda(), z.clone().cuda()
+    whole = _run(qkv, 1, P, H, Hkv, D, torch.tensor([0], dtype=torch.int32), kc1, vc1, table).cpu()
+    kc2, vc2 = z.clone().cuda(), z.clone().cuda()
+    a = _run(qkv[:300].contiguous(), 1, 300, H, Hkv, D, torch.tensor([0], dtype=torch.int32), kc2, vc2, table).cpu()
+    b = _run(qkv[300:].contiguous(), 1, 200, H, Hkv, D, torch.tensor([300], dtype=torch.int32), kc2, vc2, table).cpu()
+    assert torch.equal(torch.cat([a, b]), whole)
+    assert torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
