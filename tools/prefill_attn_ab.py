@@ -6,13 +6,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2402_15678_b200 import kernels as K
 
-cases = [  # (name, H, Hkv, B, Q, start, T, L)
-    ("13b 4K chunk 4", 40, 40, 32, 1024, 3072, 4160, 4),
-    ("13b 4K chunk 1", 40, 40, 32, 1024, 0, 4160, 4),
-    ("70b 128-token prompts", 64, 8, 32, 127, 0, 272, 8),
+cases = [  # (name, H, Hkv, B, Q, start, T, L, D)
+    ("13b 4K chunk 4", 40, 40, 32, 1024, 3072, 4160, 4, 128),
+    ("13b 4K chunk 1", 40, 40, 32, 1024, 0, 4160, 4, 128),
+    ("70b 128-token prompts", 64, 8, 32, 127, 0, 272, 8, 128),
+    ("5 x 160m 4K chunk 4 (D = 64: row kernel only)", 12, 12, 160, 1024, 3072, 4160, 2, 64),
 ]
-for name, H, Hkv, B, Q, st, T, L in cases:
-    D = 128
+if len(sys.argv) > 1:
+    cases = [c for c in cases if sys.argv[1] in c[0]]
+for name, H, Hkv, B, Q, st, T, L, D in cases:
     caches = [(torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16),
                torch.randn(B, Hkv, T, D, device="cuda").to(torch.bfloat16)) for _ in range(L)]
     qkv = torch.randn(B * Q, (H + 2 * Hkv) * D, device="cuda").to(torch.bfloat16)
