@@ -11,7 +11,9 @@ BF = torch.bfloat16
 
 
 @pytest.mark.parametrize("H,Hkv,D,Q,T,bs", [(8, 2, 128, 5, 96, 16), (12, 12, 64, 1, 96, 16), (8, 8, 128, 20, 96, 16),
-                                           (64, 8, 128, 11, 96, 16), (64, 8, 128, 7, 320, 32)])
+                                           (64, 8, 128, 11, 96, 16), (64, 8, 128, 7, 320, 32),
+                                           # prompt-prefill tiles through the block table (Q * G > 128)
+                                           (64, 8, 128, 40, 320, 32), (40, 40, 128, 130, 640, 64)])
 @pytest.mark.parametrize("tc", [False, "auto"])
 def test_paged_attention_bitwise_equals_contiguous(H, Hkv, D, Q, T, bs, tc, monkeypatch):
     """Either GQA kernel (the row kernel, or the tcgen05 one where "auto"
