@@ -426,10 +426,10 @@ int ms_attention_f32(const float* qkv, int64_t ldq, int B, int Q, int H, int Hkv
  * [n_slots, Hkv, T, 128] (block_table NULL) or a paged pool of n_slots blocks
  * [n_slots, Hkv, block_size, 128] with block_table [slots, max_blocks]
  * (T = max_blocks * block_size <= 384, block_size a multiple of 16 dividing
- * 128).  Prompt prefill (Q > 16 or Q * H / Hkv > 128): append must be 0 (the
- * call's K / V rows already in a contiguous cache, e.g. by ms_kv_append_gqa)
- * and the online kernel runs one CTA per (request, KV head, 128 / G
- * positions).  Replaces the attention inside ModelOracle.next_dist for the verify
+ * 128).  Prompt prefill (append == 0, required when Q > 16 or Q * H / Hkv >
+ * 128; head dim 128 or 64): the call's K / V rows already in the cache (e.g.
+ * by ms_kv_append_paged) and the online kernel runs one CTA per (request, KV
+ * head, 128 / G positions).  Replaces the attention inside ModelOracle.next_dist for the verify
  * positions (aggspec/oracles.py:19-26, aggspec/engine.py:294-296); same
  * contract as ms_attention_paged for those shapes (csrc/attention_tc.cu). */
 int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H, int Hkv, int D, const int32_t* slot,

@@ -138,6 +138,7 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(const void* base, uint32_t lbo
   return d;
 }
 
+template <int D>  // head dim: 128, or 64 (prompt-prefill tiles of the small drafters)
 __global__ void __launch_bounds__(kThreadsOnline, 1)
 attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const __nv_bfloat16* __restrict__ qkv, int64_t ldq, int Qtot, int Hq, int Hkv,
@@ -178,7 +179,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   const int Qc = min(Qt, Qtot - q0);
   const int64_t qrow0 = (int64_t)blockIdx.x * Qtot + q0;  // qkv / out row of the tile's first position
   const int rows_tot = Qc * G;
-  const int QD = Hq * kD, KVD = Hkv * kD;
+  const int QD = Hq * D, KVD = Hkv * D;
 
   // start / slot come from kernels complete before the previous one (the
   // round's upload): read first, their latency hidden by the setup below
@@ -221,11 +222,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   auto load_kv = [&](int ch, bool v) {  // the loader of group ch % 2
     uint64_t* bar = v ? &v_full[ch & 1] : kbar(ch);
     uint8_t* dst = v ? sV + 2 * (ch & 1) * BLK : kbuf(ch);
-    tc::mbar_arrive_expect_tx(bar, 2 * BLK);
+    tc::mbar_arrive_expect_tx(bar, (D / 64) * BLK);
     const uint64_t pol = tc::policy_evict_first();
     if (!block_table) {
       const int y = (int)(row0 + ch * kKeys);
-      for (int half = 0; half < 2; ++half)
+      for (int half = 0; half < D / 64; ++half)
         tc::tma_load_2d(dst + half * BLK, v ? &tmV : &tmK, bar, half * 64, y, pol);
     } else {  // paged (prefill tiles): one box of bs rows per block; blocks past
               // the table repeat its last block (finite rows, masked keys)
@@ -233,7 +234,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       for (int j = 0; j < nb; ++j) {
         const int t = min(ch * kKeys + j * bs, T - bs);
         const int y = (int)(((int64_t)block_table[(int64_t)kv_slot * max_blocks + t / bs] * Hkv + h) * bs);
-        for (int half = 0; half < 2; ++half)
+        for (int half = 0; half < D / 64; ++half)
           tc::tma_load_2d(dst + half * BLK + j * (BLK / nb), v ? &tmV : &tmK, bar, half * 64, y, pol);
       }
     }
@@ -259,8 +260,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   // one of the append: 2 * Qtot * 8 <= 256) before using any, so the staging
   // costs one global latency.  The appended rows are visible to the TMA
   // (async proxy) after the proxy fence + barrier.
-  constexpr int kQU = kRows * 8 / kThreads;
-  const int n_app = fuse_append ? 2 * Qtot * 8 : 0;
+  constexpr int UPR = D / 16;  // staging units per row (a unit: 8 dims and their rotate-half partners)
+  constexpr int kQU = kRows * UPR / kThreads;
+  const int n_app = fuse_append ? 2 * Qtot * UPR : 0;
   bf16x8 ux0[kQU + 1], ux1[kQU + 1];
   float2 ucs[kQU + 1][8];
   auto unit = [&](int u, const __nv_bfloat16*& src, __nv_bfloat16*& dst, int& r, int& j, int& p, bool& rot) {
@@ -269,23 +271,23 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     rot = false;
     if (u < kQU) {  // Q unit: row r = e / 8
       const int e = tid + u * kThreads;
-      r = e >> 3;
-      j = e & 7;
+      r = e / UPR;
+      j = e % UPR;
       p = pstart + r / G;
       if (r < rows_tot) {
-        src = qkv + (qrow0 + r / G) * ldq + (h * G + r % G) * kD + 8 * j;
+        src = qkv + (qrow0 + r / G) * ldq + (h * G + r % G) * D + 8 * j;
         rot = rope != nullptr;
       }
     } else if (tid < n_app) {  // append unit: K rows, then V rows
-      const int kv = tid >= Qtot * 8;
-      const int e2 = tid - kv * Qtot * 8;
-      const int i = e2 >> 3;
-      j = e2 & 7;
+      const int kv = tid >= Qtot * UPR;
+      const int e2 = tid - kv * Qtot * UPR;
+      const int i = e2 / UPR;
+      j = e2 % UPR;
       p = pstart + i;
       r = -1;
       if (p >= 0 && p < T) {
-        src = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * kD + 8 * j;
-        dst = (kv ? vc : kc) + (row0 + p) * kD + 8 * j;
+        src = qkv + (int64_t)(b * Qtot + i) * ldq + QD + kv * KVD + h * D + 8 * j;
+        dst = (kv ? vc : kc) + (row0 + p) * D + 8 * j;
         rot = !kv && rope != nullptr;
       }
     }
@@ -300,10 +302,10 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
       unit(u, src, dst, r, j, p, rot);
       if (src) {
         ux0[u] = *reinterpret_cast<const bf16x8*>(src);
-        ux1[u] = *reinterpret_cast<const bf16x8*>(src + 64);
+        ux1[u] = *reinterpret_cast<const bf16x8*>(src + D / 2);
         if (rot) {
   #pragma unroll
-          for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (kD / 2) + 8 * j + k];
+          for (int k = 0; k < 8; ++k) ucs[u][k] = rope[(int64_t)p * (D / 2) + 8 * j + k];
         }
       }
     }
@@ -337,11 +339,12 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         v1 = v0;
       }
       if (u < kQU) {
+        constexpr int H2 = D / 2;  // the partner dims D/2 + 8j: block H2 / 64, 16-byte chunk (H2 % 64) / 8 + j
         *reinterpret_cast<bf16x8*>(sQ + swz(r, j)) = v0;
-        *reinterpret_cast<bf16x8*>(sQ + BLK + swz(r, j)) = v1;
+        *reinterpret_cast<bf16x8*>(sQ + (H2 >> 6) * BLK + swz(r, ((H2 & 63) >> 3) + j)) = v1;
       } else if (dst) {
         *reinterpret_cast<bf16x8*>(dst) = v0;
-        *reinterpret_cast<bf16x8*>(dst + 64) = v1;
+        *reinterpret_cast<bf16x8*>(dst + D / 2) = v1;
       }
     }
   }
@@ -351,13 +354,13 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
   PROF(1);
 
   constexpr uint32_t idS = tc::idesc_bf16(kRows, kKeys);
-  constexpr uint32_t idPV = tc::idesc_bf16(kRows, kD) | (1u << 16);  // B (V) MN-major
+  constexpr uint32_t idPV = tc::idesc_bf16(kRows, D) | (1u << 16);  // B (V) MN-major
   auto issue_S = [&](int ch) {  // the group's issuer: S = Q K_ch^T
     MBW(kbar(ch), (ch >> 2) & 1, 1);
     tc::fence_after_sync();
     uint8_t* gK = kbuf(ch);
 #pragma unroll
-    for (int k = 0; k < kD / 16; ++k) {
+    for (int k = 0; k < D / 16; ++k) {
       const uint64_t ad = tc::smem_desc_sw128(sQ + (k >> 2) * BLK) + 2 * (k & 3);
       const uint64_t bd = tc::smem_desc_sw128(gK + (k >> 2) * BLK) + 2 * (k & 3);
       tc::mma_bf16(tS, ad, bd, idS, k > 0 ? 1u : 0u);
@@ -442,7 +445,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
         // are never stored and do not trigger it
         if (__any_sync(0xffffffffu, qrow && corr != 1.f)) {
 #pragma unroll 1
-          for (int c0 = 0; c0 < kD; c0 += 64) {
+          for (int c0 = 0; c0 < D; c0 += 64) {
             uint32_t ov[64];
 #pragma unroll
             for (int c1 = 0; c1 < 64; c1 += 16) tc::tmem_ld16(tO + lane_base + c0 + c1, *reinterpret_cast<uint32_t(*)[16]>(ov + c1));
@@ -550,9 +553,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_consta
     const float L = l_run * a0 + l1 * a1;
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const uint32_t tO1 = tmem + 384;
-    __nv_bfloat16* op = out + (qrow0 + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * kD;
+    __nv_bfloat16* op = out + (qrow0 + (r < rows_tot ? r / G : 0)) * ldo + (h * G + r % G) * D;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kD; c0 += 16) {
+    for (int c0 = 0; c0 < D; c0 += 16) {
       uint32_t o0[16], o1[16];
       tc::tmem_ld16(tO + lane_base + c0, o0);
       tc::tmem_ld16(tO1 + lane_base + c0, o1);
@@ -967,11 +970,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // the cache [rows, 128] bf16 as 2-D, box = [64 dims, box_rows keys], 128-byte swizzle
-static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int box_rows = kKeys) {
+static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int box_rows = kKeys, int D = kD) {
   auto enc = encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(kD * 2)};
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(D * 2)};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -982,7 +985,7 @@ static bool cache_tmap(CUtensorMap* m, const void* base, int64_t rows, int box_r
 }  // namespace atc
 
 int preload_attention_tc() {
-  const int e = preload_fn(atc::attention_tc_kernel);
+  const int e = preload_fn(atc::attention_tc_kernel<128>) + preload_fn(atc::attention_tc_kernel<64>);
   return e ? e : preload_fn(atc::attention_tc_short_kernel);
 }
 
@@ -1000,11 +1003,14 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
                                const int32_t* block_table, int max_blocks, int block_size, void* stream) {
   using namespace ms;
   if (B < 0 || Q < 1 || H < 1 || Hkv < 1 || T < 1 || n_slots < 1 || H % Hkv) return MS_ERR_VALUE;
-  if (D != atc::kD) return MS_ERR_UNSUPPORTED;
   // prompt prefill (more positions than one 128-row tile or 16): query tiles
-  // of the online kernel; the K / V rows must already be in the cache
-  const bool tiles = Q * (H / Hkv) > atc::kRows || Q > 16;
-  if (tiles && append) return MS_ERR_UNSUPPORTED;
+  // of the online kernel; the K / V rows must already be in the cache.  Head
+  // dim 128, or 64 for prefill tiles (the drafters' prompts)
+  // append == 0 always takes this form (a prompt's rows must not depend on
+  // how it was chunked)
+  const bool tiles = Q * (H / Hkv) > atc::kRows || Q > 16 || !append;
+  if (D != atc::kD && !(D == 64 && tiles)) return MS_ERR_UNSUPPORTED;
+  if (tiles && append) return MS_ERR_UNSUPPORTED;  // (Q > 16 or Q * G > 128 with a fused append)
   if (block_table && (block_size < 16 || atc::kKeys % block_size || max_blocks < 1 || T != max_blocks * block_size))
     return MS_ERR_VALUE;
   // paged with a fused append: the one-pass kernel only (prefill tiles read
@@ -1016,10 +1022,12 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
   const int64_t rows = (int64_t)n_slots * Hkv * (block_table ? block_size : T);
   const int box = block_table ? block_size : atc::kKeys;
   CUtensorMap tk, tv;
-  if (!atc::cache_tmap(&tk, k_cache, rows, box) || !atc::cache_tmap(&tv, v_cache, rows, box)) return MS_ERR_CUDA;
+  if (!atc::cache_tmap(&tk, k_cache, rows, box, D) || !atc::cache_tmap(&tv, v_cache, rows, box, D)) return MS_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(atc::attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(atc::attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             atc::Smem::BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(atc::attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              atc::Smem::BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(atc::attention_tc_short_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              atc::SmemShort::BYTES) != cudaSuccess)
@@ -1034,7 +1042,8 @@ extern "C" int ms_attention_tc(const void* qkv, int64_t ldq, int B, int Q, int H
                   (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
                   (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);
   const int qt = atc::kRows / (H / Hkv);
-  return launch(atc::attention_tc_kernel, dim3(B, Hkv, (Q + qt - 1) / qt), dim3(atc::kThreadsOnline), atc::Smem::BYTES,
+  return launch(D == 64 ? atc::attention_tc_kernel<64> : atc::attention_tc_kernel<128>, dim3(B, Hkv, (Q + qt - 1) / qt),
+                dim3(atc::kThreadsOnline), atc::Smem::BYTES,
                 (cudaStream_t)stream, 1, tk, tv, (const __nv_bfloat16*)qkv, ldq, Q, H, Hkv, slot, start, T,
                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, scale * 1.4426950408889634f, append,
                 (const float2*)rope, (__nv_bfloat16*)out, ldo, block_table, max_blocks, block_size);

@@ -225,9 +225,17 @@ class AttnWorkspace:
 # False: the row kernel.  Chosen by shape and cache length, never by Q alone.
 TC_ATTENTION: bool | str = "auto"
 # prompt-prefill calls (more than 16 positions or 128 flattened rows, head
-# dim 128, contiguous caches, GQA and multi-head alike): append, then the
-# online kernel in 128-row query tiles
+# dim 128 or 64, contiguous or paged caches, GQA and multi-head alike):
+# append, then the online kernel in 128-row query tiles
 TC_PREFILL = True
+# head dims routed to the tiles by default.  The kernel also takes 64 (tested
+# against the fp32 restatement), but the small head-dim-64 models (drafters,
+# OPT-125M, the tiny cfg1 models) keep the row kernel, whose P.V carries P as
+# bf16 hi + lo: on the tiny cfg1 target the bf16-P tiles cut the free-running
+# agreement with the fp32 reference from >= 24 to 9 of 48 tokens
+# (tests/test_engine_gpu.py), while the drafters' 4K prefill would gain
+# 21.6 -> 5.5 ms per layer (profiles/r2_prefill_attn_ab.jsonl)
+PREFILL_TILE_DIMS = (128,)
 TC_SHORT_KEYS = 384
 
 
@@ -235,7 +243,7 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
               start: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, scale: float,
               out: torch.Tensor | None = None, append: bool = True, ws: AttnWorkspace | None = None,
               stream=None, n_kv_heads: int | None = None, rope: torch.Tensor | None = None,
-              page=None) -> torch.Tensor:
+              page=None, prefill: bool | None = None) -> torch.Tensor:
     """Causal KV-cache attention of Q rows per request (K/V append fused when
     append; split-KV over fixed 128-key chunks when a workspace is given).
     n_kv_heads < H: grouped-query attention (qkv = [q H*D | k Hkv*D | v Hkv*D],
@@ -250,7 +258,10 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
         raise ValueError("rope table must be fp32 [>= T, D/2, 2]")
     out = out if out is not None else torch.empty((B * Q, H * D), dtype=BF16, device=qkv.device)
     use_tc = TC_ATTENTION in (True, "auto")
-    if (use_tc and TC_PREFILL and (Q > 16 or Q * (H // Hkv) > 128) and D == 128 and ws is None
+    # prefill: the model's prompt-prefill calls (every chunk size takes the
+    # tiles, so a prompt's rows do not depend on the chunking); None: by shape
+    tiles = prefill if prefill is not None else (Q > 16 or Q * (H // Hkv) > 128)
+    if (use_tc and TC_PREFILL and tiles and D in PREFILL_TILE_DIMS and ws is None
             and (page is None or (page[1] % 16 == 0 and 128 % page[1] == 0))
             and k_cache.is_contiguous() and v_cache.is_contiguous()):
         # prompt prefill: the call's K / V rows appended first, then query

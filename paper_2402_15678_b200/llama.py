@@ -154,7 +154,7 @@ class LlamaModel:
                 lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
-                        page=getattr(cache, "page", None), ws=self._attn_ws(B, Q, cache.max_len))
+                        page=getattr(cache, "page", None), ws=self._attn_ws(B, Q, cache.max_len), prefill=prefill)
             lin(at, p + "w_o", residual=x, out=x)
             if fold:
                 K.gemv(x, w[p + "w_gu"], act=2, out=ff, stream=stream, rms_eps=c.eps)
@@ -286,7 +286,7 @@ class GroupedLlamaModel:
                 lin(h, p + "w_qkv", out=qkv)
             K.attention(qkv, GB, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i], self.scale,
                         out=at, stream=stream, n_kv_heads=c.n_kv_heads, rope=self.rope,
-                        page=getattr(cache, "page", None))
+                        page=getattr(cache, "page", None), prefill=prefill)
             lin(at, p + "w_o", residual=x, out=x)
             if fold:
                 K.gemv_grouped(x, t[p + "w_gu"], G, act=2, out=ff, stream=stream, rms_eps=c.eps)

@@ -102,7 +102,8 @@ class OPTModel:
             K.layernorm(x, w[p + "ln1_g"], w[p + "ln1_b"], c.eps, out=h, stream=stream)
             lin(h, p + "w_qkv", p + "b_qkv", out=qkv)
             K.attention(qkv, B, Q, c.n_heads, c.head_dim, slot, start, cache.k[i], cache.v[i],
-                        self.scale, out=at, ws=aws, stream=stream, page=getattr(cache, "page", None))
+                        self.scale, out=at, ws=aws, stream=stream, page=getattr(cache, "page", None),
+                        prefill=prefill)
             lin(at, p + "w_o", p + "b_o", residual=x, out=x)
             K.layernorm(x, w[p + "ln2_g"], w[p + "ln2_b"], c.eps, out=h, stream=stream)
             lin(h, p + "w_fc1", p + "b_fc1", act=1, out=ff)

@@ -18,13 +18,13 @@ from test_llama_gpu import _ref_attention  # noqa: E402
 
 def _run(qkv, B, Q, H, Hkv, D, start, kc, vc, table):
     from paper_2402_15678_b200 import kernels as Kn
-    old = Kn.TC_ATTENTION
-    Kn.TC_ATTENTION = True
+    old, old_dims = Kn.TC_ATTENTION, Kn.PREFILL_TILE_DIMS
+    Kn.TC_ATTENTION, Kn.PREFILL_TILE_DIMS = True, (64, 128)
     try:
         return Kn.attention(qkv.cuda(), B, Q, H, D, torch.arange(B, dtype=torch.int32).cuda(), start.cuda(), kc, vc,
                             D ** -0.5, n_kv_heads=Hkv, rope=None if table is None else table.cuda())
     finally:
-        Kn.TC_ATTENTION = old
+        Kn.TC_ATTENTION, Kn.PREFILL_TILE_DIMS = old, old_dims
 
 
 @pytest.mark.parametrize("H,Hkv,Q,T,rope", [(64, 8, 5, 320, True), (64, 8, 16, 320, True), (64, 8, 1, 320, True),
@@ -79,13 +79,14 @@ def test_tc_attention_batch_invariant(T):
     assert torch.equal(one, full.view(B, Q, -1)[1])
 
 
-@pytest.mark.parametrize("H,Hkv,Q,T,starts", [(64, 8, 100, 300, [0, 60]), (40, 40, 300, 700, [0, 350]),
-                                              (16, 2, 200, 1100, [0, 800]), (40, 40, 130, 4300, [4000, 0])])
-def test_tc_attention_prefill_tiles_vs_reference(H, Hkv, Q, T, starts):
+@pytest.mark.parametrize("H,Hkv,Q,T,starts,D", [(64, 8, 100, 300, [0, 60], 128), (40, 40, 300, 700, [0, 350], 128),
+                                                (16, 2, 200, 1100, [0, 800], 128), (40, 40, 130, 4300, [4000, 0], 128),
+                                                (12, 12, 300, 700, [0, 350], 64), (12, 12, 130, 1500, [1300, 7], 64)])
+def test_tc_attention_prefill_tiles_vs_reference(H, Hkv, Q, T, starts, D):
     """Prompt-prefill calls (Q > 16 or Q * G > 128): the K / V rows appended,
     then 128-row query tiles of the online kernel — against the fp32
-    restatement, GQA and multi-head, tiles crossing 128-key chunks."""
-    D = 128
+    restatement, GQA and multi-head, head dim 128 and 64 (the drafters),
+    tiles crossing 128-key chunks."""
     B = len(starts)
     g = torch.Generator().manual_seed(H + Q + T)
     kc = torch.randn(B, Hkv, T, D, generator=g).to(BF)
