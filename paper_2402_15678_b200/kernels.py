@@ -236,6 +236,9 @@ TC_PREFILL = True
 # (tests/test_engine_gpu.py), while the drafters' 4K prefill would gain
 # 21.6 -> 5.5 ms per layer (profiles/r2_prefill_attn_ab.jsonl)
 PREFILL_TILE_DIMS = (128,)
+# ... except long caches (chosen by the cache length, never by Q or the
+# chunking): the drafters' 4K-prompt prefill (cfg5) takes the D = 64 tiles
+PREFILL_TILE_D64_MIN_T = 1024
 TC_SHORT_KEYS = 384
 
 
@@ -261,7 +264,8 @@ def attention(qkv: torch.Tensor, B: int, Q: int, H: int, D: int, slot: torch.Ten
     # prefill: the model's prompt-prefill calls (every chunk size takes the
     # tiles, so a prompt's rows do not depend on the chunking); None: by shape
     tiles = prefill if prefill is not None else (Q > 16 or Q * (H // Hkv) > 128)
-    if (use_tc and TC_PREFILL and tiles and D in PREFILL_TILE_DIMS and ws is None
+    tile_d = D in PREFILL_TILE_DIMS or (D == 64 and T >= PREFILL_TILE_D64_MIN_T)
+    if (use_tc and TC_PREFILL and tiles and tile_d and ws is None
             and (page is None or (page[1] % 16 == 0 and 128 % page[1] == 0))
             and k_cache.is_contiguous() and v_cache.is_contiguous()):
         # prompt prefill: the call's K / V rows appended first, then query
